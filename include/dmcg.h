@@ -1,0 +1,210 @@
+/*
+ * dmcg.h — C ABI of the B200 dynamic-mesh codec (libdmcg.so).
+ *
+ * Drop-in boundary for the reference's encode/decode hot path (pca_qp,
+ * n_b = 1): plain pointers and sizes, no exceptions, no Eigen or torch types.
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).  The C++ drop-in
+ * (include/dmc/codec.hpp: dmc::encode / dmc::decode with the reference's
+ * signatures) is a thin layer over these functions; see INTEGRATION.md for
+ * the bindings a maintainer adds on the reference side.
+ *
+ * Return convention: 0 on success, otherwise the reference dmc::Error code
+ * (include/dmc/errors.hpp:43-61: 3 parse, 4 index/validation, 5 config,
+ * 6 corrupt, 7 version, 8 io, 9 numerical) or DMCG_E_CUDA /
+ * DMCG_E_UNSUPPORTED.  dmcg_last_error() returns "<Kind>: <message>" like
+ * dmc::Error::what().  A context is single-threaded; distinct contexts are
+ * independent (the reference is reentrant).
+ *
+ * Memory layout of a trajectory axis: the reference MeshSequence stores each
+ * axis as a k x n column-major Eigen::MatrixXd (include/dmc/mesh.hpp:33-35,
+ * 56), i.e. n vertex rows of F contiguous frames: x[i*F + f].  dmcg uses that
+ * layout unchanged on the host and in HBM.
+ */
+#ifndef DMCG_H
+#define DMCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMCG_ABI_VERSION 1
+
+enum dmcg_status {
+  DMCG_OK = 0,
+  DMCG_E_PARSE = 3,       /* ParseError / VertexCountMismatch / ConnectivityMismatch */
+  DMCG_E_INDEX = 4,       /* IndexOutOfRange / DegenerateFace / ValidationError */
+  DMCG_E_CONFIG = 5,      /* DimensionMismatch / ConfigError / InvalidBits / InvalidCount */
+  DMCG_E_CORRUPT = 6,     /* CorruptPayload / CorruptStream */
+  DMCG_E_VERSION = 7,     /* VersionMismatch */
+  DMCG_E_IO = 8,          /* IoError */
+  DMCG_E_NUMERICAL = 9,   /* ConvergenceFailure / SingularSystem */
+  DMCG_E_CUDA = 10,       /* CUDA runtime / launch failure (new) */
+  DMCG_E_UNSUPPORTED = 11 /* variant outside the B200 path (new) */
+};
+
+enum dmcg_dtype { DMCG_F64 = 0, DMCG_F32 = 1 };
+
+/* Variant values = reference Variant (include/dmc/stream.hpp:38-46). */
+enum dmcg_variant {
+  DMCG_PCA = 0, DMCG_PCA_Q = 1, DMCG_V2V = 2, DMCG_PCA_QS = 3, DMCG_PCA_QP = 4,
+  DMCG_BLOCKS = 5, DMCG_PER_MESH_GFT = 6
+};
+
+typedef struct dmcg_ctx dmcg_ctx;
+typedef struct dmcg_plan dmcg_plan;
+
+/* ---- context ---------------------------------------------------------- */
+int dmcg_create(dmcg_ctx** ctx, int device);
+void dmcg_destroy(dmcg_ctx* ctx);
+const char* dmcg_last_error(const dmcg_ctx* ctx);
+int dmcg_abi_version(void);
+
+/* ---- configuration ----------------------------------------------------- */
+/* Field-for-field mirror of dmc::EncoderConfig (include/dmc/codec.hpp:30-49)
+ * plus the B200 basis controls.  dmcg_config_default() fills the reference
+ * defaults (codec.hpp:31-48) and oi_rounds = 0. */
+typedef struct {
+  int variant;              /* DMCG_PCA_QP is the only variant on this path */
+  uint32_t k_l;             /* retained rows (default 20) */
+  const int* row_bits;      /* k_l entries or NULL = all 16 (codec.cpp:106-113) */
+  uint32_t n_row_bits;
+  uint16_t n_b;             /* blocks; must be 1 */
+  int t_max;                /* block OI rounds (unused at n_b = 1, validated) */
+  double anchor_fraction;   /* default 0.01 */
+  int anchor_bits;          /* default 16 */
+  int dict_bits;            /* default 16 */
+  int diff_bits;            /* default 8 (header echo only at n_b = 1) */
+  int anchor_strategy;      /* 0 Stride, 1 SeededRandom */
+  uint64_t seed;            /* anchor seed */
+  int laplacian;            /* 0 Combinatorial (1 Normalized: unsupported) */
+  int raw_payload;          /* must be 0 */
+  /* B200 basis: 0 = full F x F eigenbasis, the reference's n_b = 1 path
+   * (codec.cpp:158-159); N > 0 = rank-k_l orthogonal iterations (N rounds)
+   * + Rayleigh-Ritz + Householder completion (K3). */
+  int oi_rounds;
+  uint64_t oi_seed;         /* start matrix seed (axis a uses oi_seed + a) */
+} dmcg_config;
+
+void dmcg_config_default(dmcg_config* cfg);
+
+/* Decoder-side solver controls (the reference factors L^T L + S^T S by
+ * SimplicialLDLT, solver.cpp:62-90; the B200 path solves it by CG). */
+typedef struct {
+  double cg_rtol;           /* per-column ||r||/||b|| stop, default 1e-10 */
+  int cg_max_iter;          /* default 20000 */
+} dmcg_decode_options;
+
+void dmcg_decode_options_default(dmcg_decode_options* opt);
+
+/* ---- data views -------------------------------------------------------- */
+/* Input sequence: replaces const dmc::MeshSequence& (mesh.hpp:36-57). */
+typedef struct {
+  uint32_t n, F;            /* vertices, frames (MeshSequence::n(), k()) */
+  int dtype;                /* DMCG_F64 (reference) or DMCG_F32 */
+  const void* axes[3];      /* host (or device, for plan calls) pointers, x[i*F+f] */
+  const uint32_t* faces;    /* 3 * n_faces vertex indices */
+  uint32_t n_faces;
+} dmcg_seq;
+
+/* Compressed animation, pca_qp / n_b = 1 subset of dmc::CompressedAnimation
+ * (include/dmc/stream.hpp:130-155).  All arrays are caller-allocated with
+ * the sizes from dmcg_encoded_sizes(); levels are 16-bit because every bit
+ * depth is limited to 1..16 (codec.cpp:82-86,114-118).
+ *   dict_q[a]   F*F levels, column-major (pack_matrix order, codec.cpp:122)
+ *   row_*[a]    k_l quantiser headers (QuantRow, stream.hpp:86-93)
+ *   coeff_q[a]  k_l*n levels, row r at [r*n]; degenerate rows hold zeros
+ *   anchor_q[a] n_c*F levels, anchor-major (codec.cpp:466-468) */
+typedef struct {
+  uint32_t n, F, k_l, n_c, n_faces;
+  uint8_t variant, flags, anchor_bits, dict_bits, diff_bits;
+  const uint32_t* faces;
+  uint16_t* dict_q[3];
+  float* row_min[3];
+  float* row_max[3];
+  uint8_t* row_bits[3];
+  uint16_t* coeff_q[3];
+  uint32_t* anchor_idx;
+  float anchor_min[3], anchor_max[3];
+  uint16_t* anchor_q[3];
+} dmcg_encoded;
+
+/* Element counts of each dmcg_encoded array for (n, F, cfg). */
+typedef struct {
+  size_t dict_q, rows, coeff_q, anchor_idx, anchor_q;
+} dmcg_sizes;
+int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_sizes* out);
+
+/* ---- drop-in entry points (host in, host out) --------------------------- */
+/* dmc::encode(const MeshSequence&, const EncoderConfig&)
+ * (include/dmc/codec.hpp:90; src/codec.cpp:351-473). */
+int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg_encoded* out);
+/* dmc::decode(const CompressedAnimation&) (include/dmc/codec.hpp:91;
+ * src/codec.cpp:475-552).  out_axes: 3 host arrays of n*F elements of
+ * out_dtype; opt may be NULL. */
+int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options* opt,
+                void* const out_axes[3], int out_dtype);
+
+/* ---- stream (src/stream.cpp:172-469) ----------------------------------- */
+typedef struct {
+  size_t header, connectivity, dict_payload, dict_ranges, coeff_headers, coeff_payload,
+      means, anchor_indices, anchor_ranges, anchor_payload;
+} dmcg_sections;   /* SectionSizes (stream.hpp:159-175) */
+/* serialize(): writes the DMC1 stream into out (cap bytes; out may be NULL
+ * to query the size).  Returns the stream size, 0 on error. */
+size_t dmcg_serialize(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sections* s);
+/* parse(): two phases.  dmcg_parse_header fills the scalar fields of hdr so
+ * the caller can size the arrays; dmcg_parse then fills them (strict: the
+ * reference's checks, stream.cpp:294-469). */
+int dmcg_parse_header(const uint8_t* data, size_t size, dmcg_encoded* hdr);
+int dmcg_parse(const uint8_t* data, size_t size, dmcg_encoded* out, dmcg_sections* s);
+/* Message of the last failed parse on this thread ("CorruptStream: ..."). */
+const char* dmcg_parse_error(void);
+/* rate_exact (src/metrics.cpp:46-59): q, q_a, q_d, aux, q_s. */
+void dmcg_rate_exact(const dmcg_sections* s, uint32_t n, uint32_t F, double out[5]);
+
+/* ---- host helpers mirroring reference free functions -------------------- */
+uint32_t dmcg_anchor_count(uint32_t n, double fraction);               /* codec.cpp:199 */
+int dmcg_select_anchors(uint32_t n, uint32_t n_c, int strategy, uint64_t seed,
+                        uint32_t* out);                                 /* codec.cpp:204 */
+
+/* ---- device-resident plan (bench `value`, serving) ----------------------
+ * A plan binds one connectivity + config to device buffers: it validates
+ * the faces, builds the Laplacian CSR and anchor set once, and keeps every
+ * intermediate in HBM.  Encode and decode then run with no host round trip. */
+int dmcg_plan_create(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uint32_t* faces,
+                     uint32_t n_faces, const dmcg_config* cfg, dmcg_plan** plan);
+void dmcg_plan_destroy(dmcg_plan* plan);
+/* d_axes: 3 device arrays (n*F of the plan dtype).  Leaves the encoded
+ * symbols in device memory. */
+int dmcg_plan_encode_device(dmcg_plan* plan, const void* const d_axes[3]);
+/* Decodes the device-resident symbols into 3 device arrays (plan dtype). */
+int dmcg_plan_decode_device(dmcg_plan* plan, const dmcg_decode_options* opt,
+                            void* const d_out[3]);
+/* D2H / H2D of the encoded representation. */
+int dmcg_plan_download(dmcg_plan* plan, dmcg_encoded* out);
+int dmcg_plan_upload(dmcg_plan* plan, const dmcg_encoded* in);
+/* Device copy of the F x F basis of axis a (column-major) and its Ritz /
+ * eigen values, for parity checks. */
+int dmcg_plan_basis(dmcg_plan* plan, int axis, double* U_host, double* evals_host);
+
+typedef struct {
+  int cg_iterations_max;     /* max over columns in the last decode */
+  double cg_rel_residual_max;
+  float ms_encode, ms_decode; /* device time of the last calls (CUDA events) */
+  float ms_delta, ms_gram, ms_basis, ms_project, ms_reconstruct, ms_cg;
+  int kernel_launches_encode, kernel_launches_decode;
+} dmcg_stats;
+int dmcg_plan_stats(const dmcg_plan* plan, dmcg_stats* out);
+/* Stats of the last drop-in dmcg_encode / dmcg_decode on this context. */
+int dmcg_ctx_stats(const dmcg_ctx* ctx, dmcg_stats* out);
+/* Stream the plan runs on (cudaStream_t), for event timing by callers. */
+void* dmcg_plan_stream(dmcg_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,286 @@
+// Decode-side kernels: dequantiser parameters, the anchored right-hand side
+// and K7, the column-block conjugate-gradient solve of the anchored normal
+// equations (reference: SimplicialLDLT + one refinement, src/solver.cpp:
+// 62-90).
+//
+// CG layout.  The 3F right-hand sides (all axes, all frames) are solved
+// together.  Vectors are stored column-block-major: block c/kCB holds rows
+// 0..n-1, each a 32-byte group of kCB = 4 columns, so one CTA owns complete
+// columns.  Every CTA therefore runs an independent CG on its 4 columns:
+// dot products are CTA-local (deterministic, no grid-wide sync), converged
+// columns freeze, and each neighbour gather is exactly one 32 B sector.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dmcg {
+
+namespace {
+
+__global__ void k_row_params(int rows, const float* rmin, const float* rmax, const uint8_t* rbits,
+                             double* rowp) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows) return;
+  const QParams q = make_qparams(rmin[t], rmax[t], rbits[t]);
+  rowp[2 * t] = q.min_;
+  rowp[2 * t + 1] = q.degenerate ? 0.0 : q.width;
+}
+
+// rhs = L^T delta~ + S^T a  (solver.cpp:77-80).  One thread per (row,
+// column block); Laplacian values implicit; anchors dequantised on the fly
+// (anchor_matrix, codec.cpp:174-195).
+__global__ void k_rhs(int n, int F, int W, int nblk, const uint32_t* __restrict__ rp,
+                      const uint32_t* __restrict__ ci, const int32_t* __restrict__ apos, int n_c,
+                      const uint16_t* __restrict__ aq, const float* __restrict__ arng, int abits,
+                      const double* __restrict__ D, double* __restrict__ B, int* flags) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)n * nblk) return;
+  const int blk = (int)(t / n), i = (int)(t % n);
+  const uint32_t pb = rp[i], pe = rp[i + 1];
+  const double deg = (double)(pe - pb - 1);
+  const double* Db = D + (size_t)blk * n * kCB;
+  double acc[kCB] = {0.0, 0.0, 0.0, 0.0};
+  for (uint32_t p = pb; p < pe; ++p) {
+    const uint32_t j = ci[p];
+    const double v = (j == (uint32_t)i) ? deg : -1.0;
+    const double2* dj = reinterpret_cast<const double2*>(Db + (size_t)j * kCB);
+    const double2 d0 = dj[0], d1 = dj[1];
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(v, d0.x));
+    acc[1] = __dadd_rn(acc[1], __dmul_rn(v, d0.y));
+    acc[2] = __dadd_rn(acc[2], __dmul_rn(v, d1.x));
+    acc[3] = __dadd_rn(acc[3], __dmul_rn(v, d1.y));
+  }
+  const int slot = apos[i];
+  if (slot >= 0) {
+    const uint32_t levels = 1u << abits;
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) {
+      const int col = blk * kCB + c;
+      if (col >= W) continue;
+      const int a = col / F, f = col % F;
+      const QParams q = make_qparams(arng[2 * a], arng[2 * a + 1], abits);
+      const uint32_t lv = aq[((size_t)a * n_c + slot) * F + f];
+      if (lv >= levels) atomicOr(flags, 1);
+      acc[c] = __dadd_rn(acc[c], dequantize_level(q.min_, q.width, q.degenerate, lv));
+    }
+  }
+  double2* o = reinterpret_cast<double2*>(B + ((size_t)blk * n + i) * kCB);
+  o[0] = make_double2(acc[0], acc[1]);
+  o[1] = make_double2(acc[2], acc[3]);
+}
+
+constexpr int kCgThreads = 512;
+
+__device__ __forceinline__ void load4(const double* p, double (&v)[kCB]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = b.x;
+  v[3] = b.y;
+}
+__device__ __forceinline__ void store4(double* p, const double (&v)[kCB]) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+
+// Sums 4 per-thread partials over the CTA; result in out[0..3] (smem).
+__device__ __forceinline__ void block_sum4(double (&v)[kCB], double* red, double* out) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < kCB; ++c) v[c] = warp_sum(v[c]);
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) red[w * kCB + c] = v[c];
+  __syncthreads();
+  if (threadIdx.x < kCB) {
+    double s = 0.0;
+    for (int i = 0; i < kCgThreads / 32; ++i) s += red[i * kCB + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// K7: CG on M = L^T L + S^T S for the 4 columns of block blockIdx.x.
+// x0 = 0, r0 = b (stored in R on entry).  Per iteration: q = M p (gather),
+// alpha = rho / p.q; x += alpha p; r -= alpha q; beta = rho'/rho;
+// p = r + beta p.  A column stops when ||r|| <= rtol ||b||.
+__global__ void __launch_bounds__(kCgThreads)
+    k_cg(int n, int W, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+         const float* __restrict__ val, double* X, double* R, double* P, double* Q, double rtol,
+         int maxit, int* iters_out, double* res_out) {
+  __shared__ double red[(kCgThreads / 32) * kCB];
+  __shared__ double s_dot[kCB];
+  __shared__ double s_rho[kCB], s_bn[kCB], s_alpha[kCB], s_beta[kCB];
+  __shared__ int s_done[kCB], s_it[kCB];
+  const int blk = blockIdx.x;
+  const size_t off = (size_t)blk * n * kCB;
+  double* x = X + off;
+  double* r = R + off;
+  double* p = P + off;
+  double* q = Q + off;
+  const int tid = threadIdx.x;
+
+  double acc[kCB] = {0.0, 0.0, 0.0, 0.0};
+  for (int i = tid; i < n; i += kCgThreads) {
+    double v[kCB];
+    load4(r + (size_t)i * kCB, v);
+    store4(p + (size_t)i * kCB, v);
+    const double z[kCB] = {0.0, 0.0, 0.0, 0.0};
+    store4(x + (size_t)i * kCB, z);
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) acc[c] += v[c] * v[c];
+  }
+  block_sum4(acc, red, s_dot);
+  if (tid < kCB) {
+    const int col = blk * kCB + tid;
+    s_rho[tid] = s_dot[tid];
+    s_bn[tid] = s_dot[tid];
+    s_done[tid] = (col >= W) || !(s_dot[tid] > 0.0);
+    s_it[tid] = 0;
+  }
+  __syncthreads();
+
+  for (int it = 0; it < maxit; ++it) {
+    if (s_done[0] && s_done[1] && s_done[2] && s_done[3]) break;
+    // q = M p ; p.q
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) acc[c] = 0.0;
+    for (int i = tid; i < n; i += kCgThreads) {
+      double qi[kCB] = {0.0, 0.0, 0.0, 0.0};
+      const uint32_t pb = rp[i], pe = rp[i + 1];
+      for (uint32_t e = pb; e < pe; ++e) {
+        const double mv = (double)val[e];
+        double pj[kCB];
+        load4(p + (size_t)ci[e] * kCB, pj);
+#pragma unroll
+        for (int c = 0; c < kCB; ++c) qi[c] += mv * pj[c];
+      }
+      store4(q + (size_t)i * kCB, qi);
+      double pi[kCB];
+      load4(p + (size_t)i * kCB, pi);
+#pragma unroll
+      for (int c = 0; c < kCB; ++c) acc[c] += pi[c] * qi[c];
+    }
+    block_sum4(acc, red, s_dot);
+    if (tid < kCB) {
+      const double pq = s_dot[tid];
+      if (s_done[tid] || !(pq > 0.0)) {
+        s_alpha[tid] = 0.0;
+        if (!s_done[tid]) s_done[tid] = 1;
+      } else {
+        s_alpha[tid] = s_rho[tid] / pq;
+      }
+    }
+    __syncthreads();
+    double al[kCB];
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) {
+      al[c] = s_alpha[c];
+      acc[c] = 0.0;
+    }
+    for (int i = tid; i < n; i += kCgThreads) {
+      double xi[kCB], ri[kCB], pi[kCB], qi[kCB];
+      load4(x + (size_t)i * kCB, xi);
+      load4(r + (size_t)i * kCB, ri);
+      load4(p + (size_t)i * kCB, pi);
+      load4(q + (size_t)i * kCB, qi);
+#pragma unroll
+      for (int c = 0; c < kCB; ++c) {
+        xi[c] += al[c] * pi[c];
+        ri[c] -= al[c] * qi[c];
+        acc[c] += ri[c] * ri[c];
+      }
+      store4(x + (size_t)i * kCB, xi);
+      store4(r + (size_t)i * kCB, ri);
+    }
+    block_sum4(acc, red, s_dot);
+    if (tid < kCB) {
+      if (!s_done[tid]) {
+        const double rr = s_dot[tid];
+        s_beta[tid] = rr / s_rho[tid];
+        s_rho[tid] = rr;
+        s_it[tid] = it + 1;
+        if (rr <= rtol * rtol * s_bn[tid]) s_done[tid] = 1;
+      } else {
+        s_beta[tid] = 0.0;
+      }
+    }
+    __syncthreads();
+    double be[kCB];
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) be[c] = s_beta[c];
+    for (int i = tid; i < n; i += kCgThreads) {
+      double ri[kCB], pi[kCB];
+      load4(r + (size_t)i * kCB, ri);
+      load4(p + (size_t)i * kCB, pi);
+#pragma unroll
+      for (int c = 0; c < kCB; ++c) pi[c] = ri[c] + be[c] * pi[c];
+      store4(p + (size_t)i * kCB, pi);
+    }
+    __syncthreads();
+  }
+  if (tid < kCB) {
+    const int col = blk * kCB + tid;
+    if (col < W) {
+      iters_out[col] = s_it[tid];
+      res_out[col] = s_bn[tid] > 0.0 ? sqrt(s_rho[tid] / s_bn[tid]) : 0.0;
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_output(int n, int F, const double* __restrict__ X, T* o0, T* o1, T* o2) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long total = 3L * n * F;
+  if (t >= total) return;
+  const int a = (int)(t / ((long)n * F));
+  const long rem = t % ((long)n * F);
+  const int i = (int)(rem / F), f = (int)(rem % F);
+  const int col = a * F + f;
+  const double v = X[((size_t)(col / kCB) * n + i) * kCB + col % kCB];
+  T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
+  o[rem] = (T)v;
+}
+
+}  // namespace
+
+cudaError_t launch_row_params(cudaStream_t s, int rows, const float* rmin, const float* rmax,
+                              const uint8_t* rbits, double* rowp) {
+  if (rows <= 0) return cudaSuccess;
+  k_row_params<<<(rows + 255) / 256, 256, 0, s>>>(rows, rmin, rmax, rbits, rowp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rhs(cudaStream_t s, int n, int F, int W, int nblk, const uint32_t* lap_rp,
+                       const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
+                       const uint16_t* anchor_q, const float* anchor_rng, int anchor_bits,
+                       const double* D, double* B, int* flags) {
+  const long total = (long)n * nblk;
+  k_rhs<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, F, W, nblk, lap_rp, lap_ci, anchor_pos,
+                                                        n_c, anchor_q, anchor_rng, anchor_bits, D,
+                                                        B, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg(cudaStream_t s, int n, int W, int nblk, const uint32_t* m_rp,
+                      const uint32_t* m_ci, const float* m_val, double* X, double* R, double* P,
+                      double* Q, double rtol, int maxit, int* iters, double* res) {
+  k_cg<<<nblk, kCgThreads, 0, s>>>(n, W, m_rp, m_ci, m_val, X, R, P, Q, rtol, maxit, iters, res);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_output(cudaStream_t s, int n, int F, const double* X, void* const out[3],
+                          bool f32) {
+  const long total = 3L * n * F;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  if (f32)
+    k_output<float><<<grid, 256, 0, s>>>(n, F, X, (float*)out[0], (float*)out[1], (float*)out[2]);
+  else
+    k_output<double><<<grid, 256, 0, s>>>(n, F, X, (double*)out[0], (double*)out[1],
+                                          (double*)out[2]);
+  return cudaGetLastError();
+}
+
+}  // namespace dmcg

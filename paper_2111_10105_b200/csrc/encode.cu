@@ -1,0 +1,226 @@
+// Encode-side kernels that must reproduce the reference arithmetic exactly.
+// Compiled with --fmad=false (and explicit _rn intrinsics) because the
+// reference Release build has no FMA contraction (CMakeLists.txt:7-9).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace dmcg {
+
+namespace {
+
+// K1 — delta coordinates (src/laplacian.cpp:39-46, called at codec.cpp:419).
+// One warp per vertex row; lanes stride the F frames (coalesced 256 B /
+// 128 B per warp access).  The row's CSR column list is sorted with the
+// diagonal in place, so accumulating in list order reproduces Eigen's
+// column-major sparse x dense product order; L's values are implicit
+// (degree on the diagonal, -1 off it: laplacian.cpp:27-30).
+constexpr int kDeltaWarps = 8;
+constexpr int kDeltaChunk = 8;  // 8 x 32 = 256 frames per pass
+
+template <typename T>
+__global__ void __launch_bounds__(kDeltaWarps * 32)
+    k_delta(int n, int F, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+            const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2,
+            double* __restrict__ delta, int* flags) {
+  const int a = blockIdx.y;
+  const T* __restrict__ X = a == 0 ? x0 : (a == 1 ? x1 : x2);
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kDeltaWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const uint32_t pb = rp[i], pe = rp[i + 1];
+  const double deg = (double)(pe - pb - 1);
+  double* out = delta + ((size_t)a * n + i) * F;
+  bool bad = false;
+  for (int f0 = 0; f0 < F; f0 += 32 * kDeltaChunk) {
+    double acc[kDeltaChunk];
+#pragma unroll
+    for (int c = 0; c < kDeltaChunk; ++c) acc[c] = 0.0;
+    for (uint32_t p = pb; p < pe; ++p) {
+      const uint32_t j = ci[p];
+      const double v = (j == (uint32_t)i) ? deg : -1.0;
+      const T* xr = X + (size_t)j * F;
+#pragma unroll
+      for (int c = 0; c < kDeltaChunk; ++c) {
+        const int f = f0 + c * 32 + lane;
+        if (f < F) {
+          const double xv = (double)xr[f];
+          if (j == (uint32_t)i && !isfinite(xv)) bad = true;
+          acc[c] = __dadd_rn(acc[c], __dmul_rn(v, xv));
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kDeltaChunk; ++c) {
+      const int f = f0 + c * 32 + lane;
+      if (f < F) out[f] = acc[c];
+    }
+  }
+  if (bad) atomicOr(flags, 1 << a);
+}
+
+// Gram reduction: S = sum of split-K partials in split order, then
+// R = 0.5 * (S + S^T) exactly as spectral.cpp:38 symmetrises.
+__global__ void k_reduce_sym(int F, int splits, int nbatch, const double* __restrict__ part,
+                             double* __restrict__ R) {
+  const long FF = (long)F * F;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (t >= FF) return;
+  const int f = (int)(t / F), g = (int)(t % F);
+  double s1 = 0.0, s2 = 0.0;
+  for (int sp = 0; sp < splits; ++sp) {
+    const double* P = part + ((long)sp * nbatch + b) * FF;
+    s1 = __dadd_rn(s1, P[(long)f * F + g]);
+    s2 = __dadd_rn(s2, P[(long)g * F + f]);
+  }
+  R[b * FF + (long)g * F + f] = __dmul_rn(0.5, __dadd_rn(s1, s2));
+}
+
+// pack_matrix with UniformQuantizer(-1.0f, 1.0f, dict_bits) (codec.cpp:122-129).
+__global__ void k_quant_dict(long count, int bits, const double* __restrict__ U,
+                             uint16_t* __restrict__ q) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const QParams qp = make_qparams(-1.0f, 1.0f, bits);
+  q[t] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, false, U[t]);
+}
+
+__global__ void k_init_keys(long rows, unsigned long long* keys) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= rows) return;
+  keys[2 * t] = ~0ull;  // running min
+  keys[2 * t + 1] = 0ull;  // running max
+}
+
+// quantize_rows (codec.cpp:244-265): row r of axis a over its own widened
+// float range; one CTA per (row, axis).
+__global__ void k_quant_rows(int k, int n, const unsigned long long* __restrict__ keys,
+                             const uint8_t* __restrict__ bits_in, const double* __restrict__ C,
+                             float* rmin, float* rmax, uint8_t* rbits, uint16_t* __restrict__ q) {
+  const int r = blockIdx.x, a = blockIdx.y;
+  const long row = (long)a * k + r;
+  const double lo = key_to_double(keys[2 * row]);
+  const double hi = key_to_double(keys[2 * row + 1]);
+  float flo, fhi;
+  widened_range(lo, hi, &flo, &fhi);
+  const int bits = bits_in[r];
+  const QParams qp = make_qparams(flo, fhi, bits);
+  if (threadIdx.x == 0) {
+    rmin[row] = flo;
+    rmax[row] = fhi;
+    rbits[row] = (uint8_t)bits;
+  }
+  const double* c = C + row * n;
+  uint16_t* o = q + row * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    o[i] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, c[i]);
+}
+
+// Anchor payload (codec.cpp:444-471): global min/max over the anchor
+// trajectories of one axis, widened, then quantised anchor-major.
+template <typename T>
+__global__ void __launch_bounds__(1024)
+    k_anchors(int n_c, int F, const uint32_t* __restrict__ idx, const T* __restrict__ x0,
+              const T* __restrict__ x1, const T* __restrict__ x2, int bits, float* rng,
+              uint16_t* __restrict__ q) {
+  const int a = blockIdx.x;
+  const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
+  const long total = (long)n_c * F;
+  double lo = INFINITY, hi = -INFINITY;
+  for (long t = threadIdx.x; t < total; t += blockDim.x) {
+    const double v = (double)X[(size_t)idx[t / F] * F + t % F];
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  __shared__ double slo[32], shi[32];
+  __shared__ float sf[2];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    slo[w] = lo;
+    shi[w] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+      lo = fmin(lo, slo[i]);
+      hi = fmax(hi, shi[i]);
+    }
+    float flo, fhi;
+    widened_range(lo, hi, &flo, &fhi);
+    sf[0] = flo;
+    sf[1] = fhi;
+    rng[2 * a] = flo;
+    rng[2 * a + 1] = fhi;
+  }
+  __syncthreads();
+  const QParams qp = make_qparams(sf[0], sf[1], bits);
+  uint16_t* o = q + (size_t)a * total;
+  for (long t = threadIdx.x; t < total; t += blockDim.x) {
+    const double v = (double)X[(size_t)idx[t / F] * F + t % F];
+    o[t] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
+                         const uint32_t* lap_ci, const void* const x[3], bool f32, double* delta,
+                         int* flags) {
+  dim3 grid((n + kDeltaWarps - 1) / kDeltaWarps, 3);
+  if (f32)
+    k_delta<float><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const float*)x[0],
+                                                     (const float*)x[1], (const float*)x[2],
+                                                     delta, flags);
+  else
+    k_delta<double><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const double*)x[0],
+                                                      (const double*)x[1], (const double*)x[2],
+                                                      delta, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, const double* part,
+                              double* R) {
+  const long FF = (long)F * F;
+  dim3 grid((unsigned)((FF + 255) / 256), nbatch);
+  k_reduce_sym<<<grid, 256, 0, s>>>(F, splits, nbatch, part, R);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_dict(cudaStream_t s, long count, int bits, const double* U, uint16_t* q) {
+  k_quant_dict<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(count, bits, U, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_keys(cudaStream_t s, long rows, unsigned long long* keys) {
+  if (rows <= 0) return cudaSuccess;
+  k_init_keys<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(rows, keys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long long* keys,
+                              const uint8_t* bits_in, const double* C, float* rmin, float* rmax,
+                              uint8_t* rbits, uint16_t* q) {
+  if (k <= 0) return cudaSuccess;
+  k_quant_rows<<<dim3(k, 3), 256, 0, s>>>(k, n, keys, bits_in, C, rmin, rmax, rbits, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
+                           const void* const x[3], bool f32, int bits, float* rng, uint16_t* q) {
+  if (f32)
+    k_anchors<float><<<3, 1024, 0, s>>>(n_c, F, idx, (const float*)x[0], (const float*)x[1],
+                                        (const float*)x[2], bits, rng, q);
+  else
+    k_anchors<double><<<3, 1024, 0, s>>>(n_c, F, idx, (const double*)x[0], (const double*)x[1],
+                                         (const double*)x[2], bits, rng, q);
+  return cudaGetLastError();
+}
+
+}  // namespace dmcg

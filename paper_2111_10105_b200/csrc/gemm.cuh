@@ -1,0 +1,222 @@
+// FP64 tensor-core GEMM for the small-k / tall-skinny contractions of the
+// codec (Gram A A^T, R Q, Q^T Z, Q W, U^T delta^T, U~ c~).
+//
+// sm_100a has no tcgen05 kind::f64 (ptxas rejects it),
+// so FP64 tensor math is DMMA: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4),
+// measured at 37 TFLOP/s on this pool's B200 (tools/peak_fp64.cu,
+// profiles/r01_peaks.md).  Tile 64x64x16 per 128-thread CTA, each warp a
+// 32x32 sub-tile (4x4 DMMA tiles), register-staged double-buffered smem.
+//
+// C[b](m, n) = sum_k A[b](k, m) * B[b](k, n).  Operands are read through
+// loader functors (so dequantisation / f32 upcast fuse into the tile load)
+// and written through epilogue functors (strided store, split-K partial,
+// row min/max, CG column-block layout).
+#pragma once
+#include "common.cuh"
+
+namespace dmcg {
+
+constexpr int kBM = 64, kBN = 64, kBK = 16, kGemmThreads = 128;
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Accumulator fragment of one warp: acc[i][j][e] is element
+//   (row = i*8 + lane/4, col = j*8 + (lane%4)*2 + e) of the warp's 32x32 tile.
+struct WarpTile {
+  double acc[4][4][2];
+};
+
+template <class LA, class LB, class EP>
+__global__ void __launch_bounds__(kGemmThreads)
+    gemm_dmma_kernel(int M, int N, int K, int k_chunk, LA la, LB lb, EP ep) {
+  __shared__ double As[2][kBK][kBM + 8];
+  __shared__ double Bs[2][kBK][kBN + 8];
+  const int b = blockIdx.z;
+  const int tiles_n = (N + kBN - 1) / kBN;
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int split = blockIdx.y;
+  const int kbeg = split * k_chunk;
+  const int kend = min(K, kbeg + k_chunk);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wm = w >> 1, wn = w & 1;
+  const int m0 = tm * kBM, n0 = tn * kBN;
+
+  WarpTile wt;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) wt.acc[i][j][0] = wt.acc[i][j][1] = 0.0;
+
+  double ra[8], rb[8];
+  auto load_tile = [&](int kt) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = t + q * kGemmThreads;
+      int k, m;
+      if (LA::kKContig) {
+        k = e % kBK;
+        m = e / kBK;
+      } else {
+        m = e % kBM;
+        k = e / kBM;
+      }
+      const int gk = kt + k, gm = m0 + m;
+      ra[q] = (gk < kend && gm < M) ? la(b, gk, gm) : 0.0;
+      int kb, nb;
+      if (LB::kKContig) {
+        kb = e % kBK;
+        nb = e / kBK;
+      } else {
+        nb = e % kBN;
+        kb = e / kBN;
+      }
+      const int gkb = kt + kb, gn = n0 + nb;
+      rb[q] = (gkb < kend && gn < N) ? lb(b, gkb, gn) : 0.0;
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = t + q * kGemmThreads;
+      if (LA::kKContig)
+        As[buf][e % kBK][e / kBK] = ra[q];
+      else
+        As[buf][e / kBM][e % kBM] = ra[q];
+      if (LB::kKContig)
+        Bs[buf][e % kBK][e / kBK] = rb[q];
+      else
+        Bs[buf][e / kBN][e % kBN] = rb[q];
+    }
+  };
+
+  int buf = 0;
+  if (kbeg < kend) {
+    load_tile(kbeg);
+    store_tile(0);
+  }
+  __syncthreads();
+  for (int kt = kbeg; kt < kend; kt += kBK) {
+    const bool more = kt + kBK < kend;
+    if (more) load_tile(kt + kBK);
+#pragma unroll
+    for (int kk = 0; kk < kBK / 4; ++kk) {
+      const int kr = kk * 4 + (lane & 3);
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][kr][wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(wt.acc[i][j], a[i], bb[j]);
+    }
+    if (more) store_tile(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  ep(b, split, m0 + wm * 32, n0 + wn * 32, lane, M, N, wt);
+}
+
+// ---- loaders -------------------------------------------------------------
+// Dense operand X(k, idx) = p[b*sb + k*sk + idx*si]; KC = k is contiguous.
+template <typename T, bool KC>
+struct LoadDense {
+  static constexpr bool kKContig = KC;
+  const T* p;
+  long sb, sk, si;
+  __device__ __forceinline__ double operator()(int b, int k, int i) const {
+    return (double)p[b * sb + (long)k * sk + (long)i * si];
+  }
+};
+
+// Per-batch pointer table variant (independent axis buffers).
+template <typename T, bool KC>
+struct LoadDense3 {
+  static constexpr bool kKContig = KC;
+  const T* p0;
+  const T* p1;
+  const T* p2;
+  long sk, si;
+  __device__ __forceinline__ double operator()(int b, int k, int i) const {
+    const T* p = b == 0 ? p0 : (b == 1 ? p1 : p2);
+    return (double)p[(long)k * sk + (long)i * si];
+  }
+};
+
+// ---- epilogues -----------------------------------------------------------
+__device__ __forceinline__ void frag_rc(int i, int j, int e, int lane, int* r, int* c) {
+  *r = i * 8 + (lane >> 2);
+  *c = j * 8 + (lane & 3) * 2 + e;
+}
+
+// C[b*sb + m*sm + n*sn] = v
+struct StoreStrided {
+  double* C;
+  long sb, sm, sn;
+  __device__ __forceinline__ void operator()(int b, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int m = mb + r, n = nb + c;
+          if (m < M && n < N) C[b * sb + (long)m * sm + (long)n * sn] = wt.acc[i][j][e];
+        }
+  }
+};
+
+// Split-K partial: P[((split * nbatch + b) * M + m) * N + n]
+struct StorePartial {
+  double* P;
+  int nbatch;
+  __device__ __forceinline__ void operator()(int b, int split, int mb, int nb, int lane, int M,
+                                             int N, const WarpTile& wt) const {
+    double* base = P + ((long)split * nbatch + b) * (long)M * N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int m = mb + r, n = nb + c;
+          if (m < M && n < N) base[(long)m * N + n] = wt.acc[i][j][e];
+        }
+  }
+};
+
+// Effective split count (every split gets >= 1 K-tile) and its chunk size.
+inline int gemm_splits(int K, int splits, int* k_chunk_out) {
+  if (splits < 1) splits = 1;
+  int k_chunk = (K + splits - 1) / splits;
+  k_chunk = ((k_chunk + kBK - 1) / kBK) * kBK;
+  if (k_chunk <= 0) k_chunk = kBK;
+  int eff = (K + k_chunk - 1) / k_chunk;
+  if (eff < 1) eff = 1;
+  if (k_chunk_out) *k_chunk_out = k_chunk;
+  return eff;
+}
+
+template <class LA, class LB, class EP>
+cudaError_t launch_gemm(cudaStream_t s, int nbatch, int M, int N, int K, int splits, LA la, LB lb,
+                        EP ep) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  int k_chunk;
+  splits = gemm_splits(K, splits, &k_chunk);
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+  dim3 grid(tiles, splits, nbatch);
+  gemm_dmma_kernel<LA, LB, EP><<<grid, kGemmThreads, 0, s>>>(M, N, K, k_chunk, la, lb, ep);
+  return cudaGetLastError();
+}
+
+}  // namespace dmcg

@@ -1,0 +1,762 @@
+// Host side of libdmcg: the C ABI (include/dmcg.h), mesh preprocessing,
+// configuration checks, plan lifetime and the DMC1 stream.  Reference
+// behaviour is cited per function (paths relative to /root/reference/proj).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace dmcg {
+
+constexpr uint32_t kColBlock = 4;  // CG column-block width, = kCB in common.cuh
+
+Status plan_encode(dmcg_plan* p, const void* const x[3]);
+Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]);
+
+#define CUDA_OK(expr)                                                                      \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return Status{DMCG_E_CUDA, std::string("CudaError: ") + cudaGetErrorString(_e)};     \
+  } while (0)
+
+// ---- device pool -----------------------------------------------------------
+void* DevicePool::get(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  auto it = free_.find(bytes);
+  if (it != free_.end()) {
+    void* p = it->second;
+    free_.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    // trim the cache and retry once
+    release_all();
+    cudaGetLastError();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+  }
+  return p;
+}
+void DevicePool::put(void* p, size_t bytes) {
+  if (!p) return;
+  bytes = (bytes + 255) & ~size_t(255);
+  free_.emplace(bytes, p);
+}
+void DevicePool::release_all() {
+  for (auto& kv : free_) cudaFree(kv.second);
+  free_.clear();
+}
+
+// ---- mesh --------------------------------------------------------------------
+// build_connectivity (src/mesh.cpp:60-86) with the errors of mesh.cpp:66-75.
+Status build_mesh(const uint32_t* faces, uint32_t n_faces, uint32_t n, MeshHost* out) {
+  if (n_faces == 0) return {DMCG_E_INDEX, "ValidationError: face list is empty"};
+  for (uint32_t t = 0; t < n_faces; ++t) {
+    const uint32_t* f = faces + 3 * (size_t)t;
+    for (int j = 0; j < 3; ++j)
+      if (f[j] >= n)
+        return {DMCG_E_INDEX, "IndexOutOfRange: face " + std::to_string(t) + " refers to vertex " +
+                                  std::to_string(f[j]) + " >= " + std::to_string(n)};
+    if (f[0] == f[1] || f[1] == f[2] || f[0] == f[2])
+      return {DMCG_E_INDEX, "DegenerateFace: face " + std::to_string(t) + " repeats a vertex index"};
+  }
+  out->n = n;
+  std::vector<uint32_t> cnt((size_t)n + 1, 0);
+  for (size_t t = 0; t < 3 * (size_t)n_faces; ++t) cnt[faces[t] + 1] += 2;
+  for (uint32_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  std::vector<uint32_t> col(cnt[n]);
+  std::vector<uint32_t> fill(cnt.begin(), cnt.end() - 1);
+  for (uint32_t t = 0; t < n_faces; ++t) {
+    const uint32_t* f = faces + 3 * (size_t)t;
+    for (int j = 0; j < 3; ++j) {
+      col[fill[f[j]]++] = f[(j + 1) % 3];
+      col[fill[f[j]]++] = f[(j + 2) % 3];
+    }
+  }
+  out->adj_rp.assign((size_t)n + 1, 0);
+  out->adj_ci.clear();
+  out->adj_ci.reserve(col.size() / 2 + 1);
+  for (uint32_t i = 0; i < n; ++i) {
+    auto b = col.begin() + cnt[i], e = col.begin() + cnt[i + 1];
+    std::sort(b, e);
+    auto u = std::unique(b, e);
+    out->adj_ci.insert(out->adj_ci.end(), b, u);
+    out->adj_rp[i + 1] = (uint32_t)out->adj_ci.size();
+  }
+  // Laplacian structure (laplacian.cpp:21-37): diagonal in sorted position.
+  out->lap_rp.assign((size_t)n + 1, 0);
+  out->lap_ci.clear();
+  out->lap_ci.reserve(out->adj_ci.size() + n);
+  for (uint32_t i = 0; i < n; ++i) {
+    bool placed = false;
+    for (uint32_t p = out->adj_rp[i]; p < out->adj_rp[i + 1]; ++p) {
+      if (!placed && out->adj_ci[p] > i) {
+        out->lap_ci.push_back(i);
+        placed = true;
+      }
+      out->lap_ci.push_back(out->adj_ci[p]);
+    }
+    if (!placed) out->lap_ci.push_back(i);
+    out->lap_rp[i + 1] = (uint32_t)out->lap_ci.size();
+  }
+  return Status::ok();
+}
+
+// validate_sequence's graph checks (src/mesh.cpp:108-136): isolated vertex,
+// connectivity by BFS (mesh.cpp:88-106).
+Status validate_mesh(const MeshHost& m) {
+  std::string issues;
+  for (uint32_t i = 0; i < m.n; ++i)
+    if (m.adj_rp[i] == m.adj_rp[i + 1]) {
+      issues = "vertex " + std::to_string(i) + " is isolated";
+      break;
+    }
+  std::vector<char> seen(m.n, 0);
+  std::deque<uint32_t> queue{0};
+  seen[0] = 1;
+  uint32_t visited = 1;
+  while (!queue.empty()) {
+    const uint32_t v = queue.front();
+    queue.pop_front();
+    for (uint32_t p = m.adj_rp[v]; p < m.adj_rp[v + 1]; ++p) {
+      const uint32_t w = m.adj_ci[p];
+      if (!seen[w]) {
+        seen[w] = 1;
+        ++visited;
+        queue.push_back(w);
+      }
+    }
+  }
+  if (visited != m.n) issues += std::string(issues.empty() ? "" : "; ") + "graph not connected";
+  if (!issues.empty()) return {DMCG_E_INDEX, "ValidationError: " + issues};
+  return Status::ok();
+}
+
+// anchored_normal_matrix (src/solver.cpp:25-39): M = L^T L + S^T S.  L is
+// symmetric and integer valued, so M's entries are small integers held
+// exactly in float.
+void build_normal_matrix(MeshHost* m) {
+  const uint32_t n = m->n;
+  std::vector<double> acc(n, 0.0);
+  std::vector<int64_t> mark(n, -1);
+  std::vector<uint32_t> list;
+  m->m_rp.assign((size_t)n + 1, 0);
+  m->m_ci.clear();
+  m->m_val.clear();
+  m->m_ci.reserve((size_t)n * 20);
+  m->m_val.reserve((size_t)n * 20);
+  auto lval = [&](uint32_t row, uint32_t p) -> double {
+    return m->lap_ci[p] == row ? (double)(m->lap_rp[row + 1] - m->lap_rp[row] - 1) : -1.0;
+  };
+  for (uint32_t i = 0; i < n; ++i) {
+    list.clear();
+    for (uint32_t p = m->lap_rp[i]; p < m->lap_rp[i + 1]; ++p) {
+      const uint32_t k = m->lap_ci[p];
+      const double a = lval(i, p);  // L^T(i,k) = L(k,i) = L(i,k)
+      for (uint32_t q = m->lap_rp[k]; q < m->lap_rp[k + 1]; ++q) {
+        const uint32_t j = m->lap_ci[q];
+        if (mark[j] != (int64_t)i) {
+          mark[j] = i;
+          acc[j] = 0.0;
+          list.push_back(j);
+        }
+        acc[j] += a * lval(k, q);
+      }
+    }
+    if (m->anchor_pos[i] >= 0) acc[i] += 1.0;
+    std::sort(list.begin(), list.end());
+    for (uint32_t j : list) {
+      m->m_ci.push_back(j);
+      m->m_val.push_back((float)acc[j]);
+    }
+    m->m_rp[i + 1] = (uint32_t)m->m_ci.size();
+  }
+}
+
+// ---- anchors (src/codec.cpp:199-242) ----------------------------------------
+namespace {
+struct Mt64 {  // MT19937-64, the engine std::mt19937_64 specifies
+  uint64_t mt[312];
+  int mti = 313;
+  explicit Mt64(uint64_t seed) {
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+    mti = 312;
+  }
+  uint64_t next() {
+    static const uint64_t mag01[2] = {0ull, 0xB5026F5AA96619E9ull};
+    const uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
+    if (mti >= 312) {
+      int i;
+      uint64_t x;
+      for (i = 0; i < 156; ++i) {
+        x = (mt[i] & UM) | (mt[i + 1] & LM);
+        mt[i] = mt[i + 156] ^ (x >> 1) ^ mag01[x & 1ull];
+      }
+      for (; i < 311; ++i) {
+        x = (mt[i] & UM) | (mt[i + 1] & LM);
+        mt[i] = mt[i - 156] ^ (x >> 1) ^ mag01[x & 1ull];
+      }
+      x = (mt[311] & UM) | (mt[0] & LM);
+      mt[311] = mt[155] ^ (x >> 1) ^ mag01[x & 1ull];
+      mti = 0;
+    }
+    uint64_t x = mt[mti++];
+    x ^= (x >> 29) & 0x5555555555555555ull;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+    x ^= (x << 37) & 0xFFF7EEE000000000ull;
+    x ^= (x >> 43);
+    return x;
+  }
+};
+
+uint64_t splitmix64(uint64_t* s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+Status check_config(const dmcg_config& cfg, uint32_t n, uint32_t k, std::vector<int>* row_bits) {
+  // src/codec.cpp:69-120, in the reference's order.
+  if (cfg.n_b < 1) return {DMCG_E_CONFIG, "ConfigError: block count must be >= 1"};
+  if (cfg.variant != DMCG_BLOCKS && cfg.n_b != 1)
+    return {DMCG_E_CONFIG, "ConfigError: block count > 1 requires the blocks variant"};
+  if (cfg.n_b > k)
+    return {DMCG_E_CONFIG, "BlockSizeError: cannot split " + std::to_string(k) + " frames into " +
+                               std::to_string(cfg.n_b) + " blocks"};
+  if (cfg.t_max < 1) return {DMCG_E_CONFIG, "ConfigError: t_max must be >= 1"};
+  if (!(cfg.anchor_fraction >= 0.0 && cfg.anchor_fraction <= 1.0))
+    return {DMCG_E_CONFIG, "ConfigError: anchor fraction outside [0, 1]"};
+  for (int bits : {cfg.anchor_bits, cfg.dict_bits, cfg.diff_bits})
+    if (bits < 1 || bits > 16)
+      return {DMCG_E_CONFIG, "InvalidBits: bit depth " + std::to_string(bits) + " outside 1..16"};
+  const uint32_t pad = (cfg.n_b - k % cfg.n_b) % cfg.n_b;
+  const uint32_t k_f = (k + pad) / cfg.n_b;
+  if (cfg.variant == DMCG_PER_MESH_GFT) {
+    if (n > 5000) return {DMCG_E_CONFIG, "ConfigError: per_mesh_gft limited to n <= 5000"};
+  } else if (cfg.k_l > k_f) {
+    return {DMCG_E_CONFIG, "ConfigError: k_l = " + std::to_string(cfg.k_l) +
+                               " exceeds dictionary dimension " + std::to_string(k_f)};
+  }
+  row_bits->clear();
+  if (!cfg.row_bits || cfg.n_row_bits == 0) {
+    if (cfg.row_bits && cfg.n_row_bits == 0 && cfg.k_l != 0)
+      return {DMCG_E_CONFIG, "ConfigError: row_bits must have one entry per retained row"};
+    row_bits->assign(cfg.k_l, 16);
+  } else {
+    if (cfg.n_row_bits != cfg.k_l)
+      return {DMCG_E_CONFIG, "ConfigError: row_bits must have one entry per retained row"};
+    row_bits->assign(cfg.row_bits, cfg.row_bits + cfg.k_l);
+  }
+  for (int bits : *row_bits)
+    if (bits < 1 || bits > 16)
+      return {DMCG_E_CONFIG,
+              "InvalidBits: row bit depth " + std::to_string(bits) + " outside 1..16"};
+  // Scope of the B200 path.
+  if (cfg.variant != DMCG_PCA_QP)
+    return {DMCG_E_UNSUPPORTED, "Unsupported: only variant pca_qp is on the B200 path"};
+  if (cfg.raw_payload) return {DMCG_E_UNSUPPORTED, "Unsupported: raw_payload debug mode"};
+  if (cfg.laplacian != 0)
+    return {DMCG_E_UNSUPPORTED, "Unsupported: only the combinatorial Laplacian"};
+  if (cfg.oi_rounds < 0) return {DMCG_E_CONFIG, "ConfigError: oi_rounds must be >= 0"};
+  if (k > 512) return {DMCG_E_UNSUPPORTED, "Unsupported: more than 512 frames"};
+  return Status::ok();
+}
+}  // namespace
+
+}  // namespace dmcg
+
+using namespace dmcg;
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int dmcg_abi_version(void) { return DMCG_ABI_VERSION; }
+
+int dmcg_create(dmcg_ctx** out, int device) {
+  if (!out) return DMCG_E_CONFIG;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return DMCG_E_CUDA;
+  }
+  if (device < 0 || device >= count) return DMCG_E_CONFIG;
+  if (cudaSetDevice(device) != cudaSuccess) return DMCG_E_CUDA;
+  auto* c = new dmcg_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return DMCG_E_CUDA;
+  }
+  *out = c;
+  return DMCG_OK;
+}
+
+void dmcg_destroy(dmcg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->pool.release_all();
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* dmcg_last_error(const dmcg_ctx* c) { return c ? c->err.c_str() : "no context"; }
+
+void dmcg_config_default(dmcg_config* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->variant = DMCG_PCA_QP;  // include/dmc/codec.hpp:31-48
+  cfg->k_l = 20;
+  cfg->n_b = 1;
+  cfg->t_max = 4;
+  cfg->anchor_fraction = 0.01;
+  cfg->anchor_bits = 16;
+  cfg->dict_bits = 16;
+  cfg->diff_bits = 8;
+  cfg->anchor_strategy = 0;
+  cfg->seed = 0;
+  cfg->laplacian = 0;
+  cfg->raw_payload = 0;
+  cfg->oi_rounds = 0;
+  cfg->oi_seed = 0;
+}
+
+void dmcg_decode_options_default(dmcg_decode_options* o) {
+  o->cg_rtol = 1e-10;
+  o->cg_max_iter = 20000;
+}
+
+uint32_t dmcg_anchor_count(uint32_t n, double fraction) {
+  const auto rounded = (int64_t)std::llround(fraction * n);
+  return (uint32_t)std::clamp<int64_t>(rounded, 1, n);
+}
+
+int dmcg_select_anchors(uint32_t n, uint32_t n_c, int strategy, uint64_t seed, uint32_t* out) {
+  if (n_c < 1 || n_c > n) return DMCG_E_CONFIG;  // InvalidCount
+  std::vector<uint32_t> idx;
+  idx.reserve(n_c);
+  if (strategy == 0) {
+    for (uint64_t j = 0; j < n_c; ++j) idx.push_back((uint32_t)(j * n / n_c));
+    std::sort(idx.begin(), idx.end());
+    idx.erase(std::unique(idx.begin(), idx.end()), idx.end());
+    std::vector<char> used(n, 0);
+    for (uint32_t v : idx) used[v] = 1;
+    for (uint32_t i = 0; idx.size() < n_c && i < n; ++i)
+      if (!used[i]) {
+        idx.push_back(i);
+        used[i] = 1;
+      }
+    std::sort(idx.begin(), idx.end());
+  } else {
+    std::vector<uint32_t> pool(n);
+    for (uint32_t i = 0; i < n; ++i) pool[i] = i;
+    Mt64 rng(seed);
+    for (uint32_t i = n - 1; i > 0; --i) {
+      const uint64_t j = rng.next() % ((uint64_t)i + 1);
+      std::swap(pool[i], pool[j]);
+    }
+    idx.assign(pool.begin(), pool.begin() + n_c);
+    std::sort(idx.begin(), idx.end());
+  }
+  std::memcpy(out, idx.data(), idx.size() * sizeof(uint32_t));
+  return DMCG_OK;
+}
+
+int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_sizes* out) {
+  if (!cfg || !out) return DMCG_E_CONFIG;
+  out->dict_q = (size_t)F * F;
+  out->rows = cfg->k_l;
+  out->coeff_q = (size_t)cfg->k_l * n;
+  out->anchor_idx = dmcg_anchor_count(n, cfg->anchor_fraction);
+  out->anchor_q = out->anchor_idx * (size_t)F;
+  return DMCG_OK;
+}
+
+// ---- plan ---------------------------------------------------------------------
+static void* plan_get(dmcg_plan* p, size_t bytes) {
+  if (bytes == 0) bytes = 256;
+  void* d = p->ctx->pool.get(bytes);
+  if (d) p->owned.emplace_back(d, bytes);
+  return d;
+}
+
+void dmcg_plan_destroy(dmcg_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  for (auto& kv : p->owned) p->ctx->pool.put(kv.first, kv.second);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  delete p;
+}
+
+static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
+                               const uint32_t* faces, uint32_t n_faces, const dmcg_config* cfg,
+                               const uint32_t* anchors_given, uint32_t n_c_given,
+                               dmcg_plan** out) {
+  *out = nullptr;
+  if (n == 0 || F == 0) return {DMCG_E_INDEX, "ValidationError: sequence is empty"};
+  if (dtype != DMCG_F64 && dtype != DMCG_F32) return {DMCG_E_CONFIG, "ConfigError: bad dtype"};
+  auto* p = new dmcg_plan();
+  p->ctx = ctx;
+  p->n = n;
+  p->F = F;
+  p->dtype = dtype;
+  p->n_faces = n_faces;
+  p->faces.assign(faces, faces + 3 * (size_t)n_faces);
+  Status st = build_mesh(faces, n_faces, n, &p->mesh);
+  if (st.good() && !anchors_given) st = validate_mesh(p->mesh);
+  if (st.good()) st = check_config(*cfg, n, F, &p->row_bits);
+  if (!st.good()) {
+    delete p;
+    return st;
+  }
+  p->k = cfg->k_l;
+  p->rounds = cfg->oi_rounds;
+  p->oi_seed = cfg->oi_seed;
+  p->anchor_bits = cfg->anchor_bits;
+  p->dict_bits = cfg->dict_bits;
+  p->diff_bits = cfg->diff_bits;
+  // anchors (codec.cpp:374, 445)
+  if (anchors_given) {
+    p->n_c = n_c_given;
+    p->mesh.anchors.assign(anchors_given, anchors_given + n_c_given);
+  } else {
+    p->n_c = dmcg_anchor_count(n, cfg->anchor_fraction);
+    p->mesh.anchors.resize(p->n_c);
+    if (dmcg_select_anchors(n, p->n_c, cfg->anchor_strategy, cfg->seed, p->mesh.anchors.data())) {
+      delete p;
+      return {DMCG_E_CONFIG, "InvalidCount: anchor count outside 1..n"};
+    }
+  }
+  p->mesh.anchor_pos.assign(n, -1);
+  for (uint32_t t = 0; t < p->n_c; ++t) p->mesh.anchor_pos[p->mesh.anchors[t]] = (int32_t)t;
+  build_normal_matrix(&p->mesh);
+
+  const uint32_t k = p->k;
+  p->W = 3 * F;
+  p->W_pad = (p->W + kColBlock - 1) / kColBlock * kColBlock;
+  p->nblk = p->W_pad / kColBlock;
+  const size_t es = dtype == DMCG_F32 ? 4 : 8;
+  const size_t nF = (size_t)n * F, FF = (size_t)F * F;
+  const uint32_t F2 = F + (F & 1);
+  const size_t kk = (size_t)std::max<uint32_t>(k, 1);
+  bool ok = true;
+  auto get = [&](size_t bytes) {
+    void* d = plan_get(p, bytes);
+    ok = ok && d;
+    return d;
+  };
+  const MeshHost& m = p->mesh;
+  p->d_lap_rp = (uint32_t*)get(m.lap_rp.size() * 4);
+  p->d_lap_ci = (uint32_t*)get(m.lap_ci.size() * 4);
+  p->d_m_rp = (uint32_t*)get(m.m_rp.size() * 4);
+  p->d_m_ci = (uint32_t*)get(m.m_ci.size() * 4);
+  p->d_m_val = (float*)get(m.m_val.size() * 4);
+  p->d_anchor_idx = (uint32_t*)get((size_t)p->n_c * 4);
+  p->d_anchor_pos = (int32_t*)get((size_t)n * 4);
+  for (int a = 0; a < 3; ++a) {
+    p->d_x_in[a] = get(nF * es);
+    p->d_x_out[a] = get(nF * es);
+  }
+  p->d_delta = (double*)get(3 * nF * 8);
+  p->d_R = (double*)get(3 * FF * 8);
+  const int tiles = ((F + 63) / 64) * ((F + 63) / 64);
+  size_t splits = std::max<size_t>(1, (2 * 148 + tiles * 3 - 1) / (tiles * 3));
+  p->part_elems = splits * 3 * FF;
+  p->d_part = (double*)get(p->part_elems * 8);
+  p->d_U = (double*)get(3 * FF * 8);
+  p->d_evals = (double*)get(3 * (size_t)F * 8);
+  p->d_Q = (double*)get(3 * (size_t)F * kk * 8);
+  p->d_Z = (double*)get(3 * (size_t)F * kk * 8);
+  p->d_tau = (double*)get(3 * (size_t)F * 8);
+  p->d_H = (double*)get(3 * 2 * (size_t)F2 * F2 * 8);
+  p->d_V = (double*)get(3 * FF * 8);
+  p->d_w = (double*)get(3 * (size_t)F * 8);
+  p->d_start = (double*)get(3 * (size_t)F * kk * 8);
+  p->d_C = (double*)get(3 * kk * std::max<size_t>(n, kk) * 8);
+  p->d_keys = (unsigned long long*)get(3 * kk * 2 * 8);
+  p->d_flags = (int*)get(8 * sizeof(int));
+  p->d_dict_q = (uint16_t*)get(3 * FF * 2);
+  p->d_row_min = (float*)get(3 * kk * 4);
+  p->d_row_max = (float*)get(3 * kk * 4);
+  p->d_row_bits = (uint8_t*)get(4 * kk);
+  p->d_coeff_q = (uint16_t*)get(3 * kk * n * 2);
+  p->d_anchor_rng = (float*)get(6 * 4);
+  p->d_anchor_q = (uint16_t*)get(3 * (size_t)p->n_c * F * 2);
+  p->d_rowp = (double*)get(3 * kk * 2 * 8);
+  const size_t vec = (size_t)p->nblk * n * kColBlock * 8;
+  p->d_cg_x = (double*)get(vec);
+  p->d_cg_r = (double*)get(vec);
+  p->d_cg_p = (double*)get(vec);
+  p->d_cg_q = (double*)get(vec);
+  p->d_cg_iters = (int*)get(p->W_pad * 4);
+  p->d_cg_res = (double*)get(p->W_pad * 8);
+  if (!ok) {
+    dmcg_plan_destroy(p);
+    return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  }
+  for (auto& e : p->ev) cudaEventCreate(&e);
+  cudaStream_t s = ctx->stream;
+  auto h2d = [&](void* d, const void* h, size_t bytes) {
+    if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  };
+  h2d(p->d_lap_rp, m.lap_rp.data(), m.lap_rp.size() * 4);
+  h2d(p->d_lap_ci, m.lap_ci.data(), m.lap_ci.size() * 4);
+  h2d(p->d_m_rp, m.m_rp.data(), m.m_rp.size() * 4);
+  h2d(p->d_m_ci, m.m_ci.data(), m.m_ci.size() * 4);
+  h2d(p->d_m_val, m.m_val.data(), m.m_val.size() * 4);
+  h2d(p->d_anchor_idx, m.anchors.data(), (size_t)p->n_c * 4);
+  h2d(p->d_anchor_pos, m.anchor_pos.data(), (size_t)n * 4);
+  std::vector<uint8_t> rb(4 * kk, 0);
+  for (uint32_t r = 0; r < k; ++r) rb[3 * kk + r] = (uint8_t)p->row_bits[r];
+  h2d(p->d_row_bits, rb.data(), rb.size());
+  // OI start matrices: SplitMix64 uniform in [-1, 1), column-major F x k,
+  // axis a seeded with oi_seed + a (same stream as oracle orc_start_matrix).
+  std::vector<double> start(3 * (size_t)F * kk, 0.0);
+  if (k > 0)
+    for (int a = 0; a < 3; ++a) {
+      uint64_t st64 = p->oi_seed + (uint64_t)a;
+      for (size_t t = 0; t < (size_t)F * k; ++t)
+        start[a * (size_t)F * k + t] = (double)(splitmix64(&st64) >> 11) * 0x1.0p-52 - 1.0;
+    }
+  h2d(p->d_start, start.data(), start.size() * 8);
+  if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
+  if (!ok) {
+    dmcg_plan_destroy(p);
+    return {DMCG_E_CUDA, "CudaError: plan upload failed"};
+  }
+  *out = p;
+  return Status::ok();
+}
+
+int dmcg_plan_create(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uint32_t* faces,
+                     uint32_t n_faces, const dmcg_config* cfg, dmcg_plan** plan) {
+  if (!ctx || !plan || !cfg) return DMCG_E_CONFIG;
+  cudaSetDevice(ctx->device);
+  Status st = plan_create_impl(ctx, n, F, dtype, faces, n_faces, cfg, nullptr, 0, plan);
+  return ctx->set_error(st);
+}
+
+int dmcg_plan_encode_device(dmcg_plan* p, const void* const d_axes[3]) {
+  if (!p) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  return p->ctx->set_error(plan_encode(p, d_axes));
+}
+
+int dmcg_plan_decode_device(dmcg_plan* p, const dmcg_decode_options* opt, void* const d_out[3]) {
+  if (!p) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  dmcg_decode_options o;
+  dmcg_decode_options_default(&o);
+  if (opt) o = *opt;
+  return p->ctx->set_error(plan_decode(p, &o, d_out));
+}
+
+static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
+  cudaStream_t s = p->ctx->stream;
+  const size_t n = p->n, F = p->F, k = p->k, FF = F * F;
+  e->n = p->n;
+  e->F = p->F;
+  e->k_l = p->k;
+  e->n_c = p->n_c;
+  e->n_faces = p->n_faces;
+  e->variant = DMCG_PCA_QP;
+  e->flags = 0;
+  e->anchor_bits = (uint8_t)p->anchor_bits;
+  e->dict_bits = (uint8_t)p->dict_bits;
+  e->diff_bits = (uint8_t)p->diff_bits;
+  if (!e->faces) e->faces = p->faces.data();
+  float rng[6];
+  for (int a = 0; a < 3; ++a) {
+    CUDA_OK(cudaMemcpyAsync(e->dict_q[a], p->d_dict_q + a * FF, FF * 2, cudaMemcpyDeviceToHost, s));
+    if (k) {
+      CUDA_OK(cudaMemcpyAsync(e->row_min[a], p->d_row_min + a * k, k * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaMemcpyAsync(e->row_max[a], p->d_row_max + a * k, k * 4, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaMemcpyAsync(e->row_bits[a], p->d_row_bits + a * k, k, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaMemcpyAsync(e->coeff_q[a], p->d_coeff_q + a * k * n, k * n * 2,
+                              cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_OK(cudaMemcpyAsync(e->anchor_q[a], p->d_anchor_q + a * (size_t)p->n_c * F,
+                            (size_t)p->n_c * F * 2, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  std::memcpy(e->anchor_idx, p->mesh.anchors.data(), (size_t)p->n_c * 4);
+  for (int a = 0; a < 3; ++a) {
+    e->anchor_min[a] = rng[2 * a];
+    e->anchor_max[a] = rng[2 * a + 1];
+  }
+  // Degenerate rows carry no payload (codec.cpp:259-262): zero their levels
+  // so the representation is canonical.
+  for (int a = 0; a < 3; ++a)
+    for (size_t r = 0; r < k; ++r)
+      if (e->row_min[a][r] == e->row_max[a][r])
+        std::memset(e->coeff_q[a] + r * n, 0, n * 2);
+  return Status::ok();
+}
+
+int dmcg_plan_download(dmcg_plan* p, dmcg_encoded* out) {
+  if (!p || !out) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  return p->ctx->set_error(download_impl(p, out));
+}
+
+static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
+  cudaStream_t s = p->ctx->stream;
+  const size_t n = p->n, F = p->F, k = p->k, FF = F * F;
+  float rng[6];
+  for (int a = 0; a < 3; ++a) {
+    CUDA_OK(cudaMemcpyAsync(p->d_dict_q + a * FF, e->dict_q[a], FF * 2, cudaMemcpyHostToDevice, s));
+    if (k) {
+      CUDA_OK(cudaMemcpyAsync(p->d_row_min + a * k, e->row_min[a], k * 4, cudaMemcpyHostToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(p->d_row_max + a * k, e->row_max[a], k * 4, cudaMemcpyHostToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(p->d_row_bits + a * k, e->row_bits[a], k, cudaMemcpyHostToDevice, s));
+      CUDA_OK(cudaMemcpyAsync(p->d_coeff_q + a * k * n, e->coeff_q[a], k * n * 2,
+                              cudaMemcpyHostToDevice, s));
+    }
+    CUDA_OK(cudaMemcpyAsync(p->d_anchor_q + a * (size_t)p->n_c * F, e->anchor_q[a],
+                            (size_t)p->n_c * F * 2, cudaMemcpyHostToDevice, s));
+    rng[2 * a] = e->anchor_min[a];
+    rng[2 * a + 1] = e->anchor_max[a];
+  }
+  CUDA_OK(cudaMemcpyAsync(p->d_anchor_rng, rng, sizeof(rng), cudaMemcpyHostToDevice, s));
+  CUDA_OK(cudaStreamSynchronize(s));  // rng is a stack buffer
+  return Status::ok();
+}
+
+int dmcg_plan_upload(dmcg_plan* p, const dmcg_encoded* in) {
+  if (!p || !in) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  return p->ctx->set_error(upload_impl(p, in));
+}
+
+int dmcg_plan_basis(dmcg_plan* p, int axis, double* U_host, double* evals_host) {
+  if (!p || axis < 0 || axis > 2) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  const size_t FF = (size_t)p->F * p->F;
+  cudaStream_t s = p->ctx->stream;
+  if (U_host) cudaMemcpyAsync(U_host, p->d_U + axis * FF, FF * 8, cudaMemcpyDeviceToHost, s);
+  if (evals_host)
+    cudaMemcpyAsync(evals_host, p->d_evals + (size_t)axis * p->F, p->F * 8, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return DMCG_E_CUDA;
+  return DMCG_OK;
+}
+
+int dmcg_plan_stats(const dmcg_plan* p, dmcg_stats* out) {
+  if (!p || !out) return DMCG_E_CONFIG;
+  *out = p->stats;
+  return DMCG_OK;
+}
+
+int dmcg_ctx_stats(const dmcg_ctx* c, dmcg_stats* out) {
+  if (!c || !out) return DMCG_E_CONFIG;
+  *out = c->last_stats;
+  return DMCG_OK;
+}
+
+void* dmcg_plan_stream(dmcg_plan* p) { return p ? (void*)p->ctx->stream : nullptr; }
+
+// ---- drop-in encode / decode -------------------------------------------------
+int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg_encoded* out) {
+  if (!ctx || !seq || !cfg || !out) return DMCG_E_CONFIG;
+  cudaSetDevice(ctx->device);
+  dmcg_plan* p = nullptr;
+  Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
+                               nullptr, 0, &p);
+  if (!st.good()) return ctx->set_error(st);
+  const size_t bytes = (size_t)seq->n * seq->F * (seq->dtype == DMCG_F32 ? 4 : 8);
+  for (int a = 0; a < 3 && st.good(); ++a)
+    if (cudaMemcpyAsync(p->d_x_in[a], seq->axes[a], bytes, cudaMemcpyHostToDevice, ctx->stream) !=
+        cudaSuccess)
+      st = {DMCG_E_CUDA, "CudaError: H2D copy failed"};
+  if (st.good()) st = plan_encode(p, p->d_x_in);
+  if (st.good()) {
+    if (!out->faces) out->faces = seq->faces;
+    st = download_impl(p, out);
+    out->faces = seq->faces;
+  }
+  if (st.good()) {
+    const dmcg_stats& e = p->stats;
+    ctx->last_stats.ms_encode = e.ms_encode;
+    ctx->last_stats.ms_delta = e.ms_delta;
+    ctx->last_stats.ms_gram = e.ms_gram;
+    ctx->last_stats.ms_basis = e.ms_basis;
+    ctx->last_stats.ms_project = e.ms_project;
+    ctx->last_stats.kernel_launches_encode = e.kernel_launches_encode;
+  }
+  dmcg_plan_destroy(p);
+  return ctx->set_error(st);
+}
+
+int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options* opt,
+                void* const out_axes[3], int out_dtype) {
+  if (!ctx || !in || !out_axes) return DMCG_E_CONFIG;
+  cudaSetDevice(ctx->device);
+  // Header sanity (the same bounds parse() enforces, stream.cpp:322-336).
+  if (in->n < 1 || in->F < 1) return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: empty animation"});
+  if (in->variant != DMCG_PCA_QP)
+    return ctx->set_error({DMCG_E_UNSUPPORTED, "Unsupported: only variant pca_qp is on the B200 path"});
+  if (in->k_l > in->F)
+    return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: retained row count exceeds dictionary dimension"});
+  if (in->n_c < 1 || in->n_c > in->n)
+    return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: anchor count out of range"});
+  for (uint32_t t = 0; t < in->n_c; ++t)
+    if (in->anchor_idx[t] >= in->n || (t && in->anchor_idx[t] <= in->anchor_idx[t - 1]))
+      return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: anchor indices invalid"});
+  dmcg_config cfg;
+  dmcg_config_default(&cfg);
+  cfg.k_l = in->k_l;
+  std::vector<int> rb(in->k_l, 16);
+  for (uint32_t r = 0; r < in->k_l; ++r) {
+    rb[r] = in->row_bits[0][r];
+    for (int a = 0; a < 3; ++a)
+      if (in->row_bits[a][r] < 1 || in->row_bits[a][r] > 16)
+        return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: row bit depth outside 1..16"});
+  }
+  cfg.row_bits = rb.data();
+  cfg.n_row_bits = in->k_l;
+  cfg.anchor_bits = in->anchor_bits;
+  cfg.dict_bits = in->dict_bits;
+  cfg.diff_bits = in->diff_bits ? in->diff_bits : 8;
+  dmcg_plan* p = nullptr;
+  Status st = plan_create_impl(ctx, in->n, in->F, out_dtype, in->faces, in->n_faces, &cfg,
+                               in->anchor_idx, in->n_c, &p);
+  if (!st.good()) return ctx->set_error(st);
+  st = upload_impl(p, in);
+  if (st.good()) {
+    dmcg_decode_options o;
+    dmcg_decode_options_default(&o);
+    if (opt) o = *opt;
+    st = plan_decode(p, &o, p->d_x_out);
+  }
+  const size_t bytes = (size_t)in->n * in->F * (out_dtype == DMCG_F32 ? 4 : 8);
+  for (int a = 0; a < 3 && st.good(); ++a)
+    if (cudaMemcpyAsync(out_axes[a], p->d_x_out[a], bytes, cudaMemcpyDeviceToHost, ctx->stream) !=
+        cudaSuccess)
+      st = {DMCG_E_CUDA, "CudaError: D2H copy failed"};
+  if (st.good() && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
+  if (st.good()) {
+    ctx->last_stats.cg_iterations_max = p->stats.cg_iterations_max;
+    ctx->last_stats.cg_rel_residual_max = p->stats.cg_rel_residual_max;
+    ctx->last_stats.ms_decode = p->stats.ms_decode;
+    ctx->last_stats.ms_reconstruct = p->stats.ms_reconstruct;
+    ctx->last_stats.ms_cg = p->stats.ms_cg;
+    ctx->last_stats.kernel_launches_decode = p->stats.kernel_launches_decode;
+  }
+  dmcg_plan_destroy(p);
+  return ctx->set_error(st);
+}
+
+}  // extern "C"

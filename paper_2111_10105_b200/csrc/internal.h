@@ -1,0 +1,115 @@
+// Internal host-side structures shared by host.cpp (C ABI, mesh / stream
+// logic) and pipeline.cu (device orchestration).  Not installed.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/dmcg.h"
+
+namespace dmcg {
+
+struct Status {
+  int code = 0;
+  std::string msg;
+  static Status ok() { return {}; }
+  bool good() const { return code == 0; }
+};
+
+// Caching device allocator owned by a context: blocks are recycled by size
+// so repeated drop-in calls do not pay cudaMalloc (like a stream-ordered
+// pool; all work of a context runs on its single stream).
+class DevicePool {
+ public:
+  void* get(size_t bytes);
+  void put(void* p, size_t bytes);
+  void release_all();
+  ~DevicePool() { release_all(); }
+
+ private:
+  std::multimap<size_t, void*> free_;
+};
+
+// Host-side mesh artefacts derived from the faces (reference src/mesh.cpp,
+// src/laplacian.cpp, src/solver.cpp:25-39).
+struct MeshHost {
+  uint32_t n = 0;
+  std::vector<uint32_t> adj_rp, adj_ci;   // one-ring CSR (sorted, dedup)
+  std::vector<uint32_t> lap_rp, lap_ci;   // Laplacian structure incl. diagonal
+  std::vector<uint32_t> m_rp, m_ci;       // M = L^T L + S^T S
+  std::vector<float> m_val;
+  std::vector<uint32_t> anchors;
+  std::vector<int32_t> anchor_pos;        // vertex -> anchor slot or -1
+};
+
+Status build_mesh(const uint32_t* faces, uint32_t n_faces, uint32_t n, MeshHost* out);
+Status validate_mesh(const MeshHost& m);   // isolated / connected (mesh.cpp:108-136)
+void build_normal_matrix(MeshHost* m);     // needs anchors set
+
+}  // namespace dmcg
+
+struct dmcg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  dmcg::DevicePool pool;
+  dmcg_stats last_stats = {};  // stats of the last drop-in encode / decode
+  int set_error(const dmcg::Status& s) {
+    err = s.msg;
+    return s.code;
+  }
+};
+
+struct dmcg_plan {
+  dmcg_ctx* ctx = nullptr;
+  // geometry / config
+  uint32_t n = 0, F = 0, k = 0, n_c = 0, n_faces = 0;
+  int dtype = DMCG_F64;
+  int rounds = 0;
+  int anchor_bits = 16, dict_bits = 16, diff_bits = 8;
+  uint64_t oi_seed = 0;
+  std::vector<int> row_bits;
+  std::vector<uint32_t> faces;
+  dmcg::MeshHost mesh;
+  uint32_t W = 0, W_pad = 0, nblk = 0;   // CG columns (3F), padded to kCB
+
+  // device buffers (owned; returned to ctx->pool on destroy)
+  std::vector<std::pair<void*, size_t>> owned;
+  uint32_t *d_lap_rp = nullptr, *d_lap_ci = nullptr;
+  uint32_t *d_m_rp = nullptr, *d_m_ci = nullptr;
+  float* d_m_val = nullptr;
+  uint32_t* d_anchor_idx = nullptr;
+  int32_t* d_anchor_pos = nullptr;
+  void* d_x_in[3] = {nullptr, nullptr, nullptr};   // plan-owned input staging
+  void* d_x_out[3] = {nullptr, nullptr, nullptr};  // plan-owned output staging
+  double* d_delta = nullptr;       // 3 x n x F
+  double* d_R = nullptr;           // 3 x F x F
+  double* d_part = nullptr;        // split-K partials
+  size_t part_elems = 0;
+  double* d_U = nullptr;           // 3 x F x F (col-major)
+  double* d_evals = nullptr;       // 3 x F
+  double *d_Q = nullptr, *d_Z = nullptr, *d_tau = nullptr;  // 3 x F x k, 3 x F
+  double *d_H = nullptr, *d_V = nullptr, *d_w = nullptr;    // jacobi work (3 x m2 x m2)
+  double* d_start = nullptr;       // 3 x F x k OI start matrices
+  double* d_C = nullptr;           // 3 x k x n coefficients
+  unsigned long long* d_keys = nullptr;  // 3 x k x 2 (min,max) ordered keys
+  int* d_flags = nullptr;          // [0] non-finite axes mask, [1] corrupt payload, [2] cg fail
+  // encoded (device-resident)
+  uint16_t* d_dict_q = nullptr;    // 3 x F x F
+  float *d_row_min = nullptr, *d_row_max = nullptr;  // 3 x k
+  uint8_t* d_row_bits = nullptr;   // 3 x k
+  uint16_t* d_coeff_q = nullptr;   // 3 x k x n
+  float* d_anchor_rng = nullptr;   // 3 x 2
+  uint16_t* d_anchor_q = nullptr;  // 3 x n_c x F
+  // decode
+  double* d_rowp = nullptr;        // 3 x k x 2 (min_, width) dequantiser params
+  double *d_cg_x = nullptr, *d_cg_r = nullptr, *d_cg_p = nullptr, *d_cg_q = nullptr;
+  int* d_cg_iters = nullptr;       // per column
+  double* d_cg_res = nullptr;      // per column relative residual
+
+  cudaEvent_t ev[8] = {};
+  dmcg_stats stats = {};
+};

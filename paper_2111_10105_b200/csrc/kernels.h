@@ -1,0 +1,68 @@
+// Host launchers of the dmcg sm_100a kernels (one per .cu translation unit
+// group).  All launches go to the caller's stream; none synchronise.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace dmcg {
+
+// ---- encode.cu (compiled with --fmad=false) -----------------------------
+// K1: delta = L * A^T per axis (src/laplacian.cpp:39-46), bit-exact order.
+// f32 selects float input.  flags[0] |= 1<<axis on non-finite input.
+cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
+                         const uint32_t* lap_ci, const void* const x[3], bool f32, double* delta,
+                         int* flags);
+// Sum split-K Gram partials in split order and symmetrise (spectral.cpp:37-38).
+cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, const double* part,
+                              double* R);
+// Dictionary levels over [-1, 1] (codec.cpp:122-129, 300-301).
+cudaError_t launch_quant_dict(cudaStream_t s, long count, int bits, const double* U, uint16_t* q);
+cudaError_t launch_init_keys(cudaStream_t s, long rows, unsigned long long* keys);
+// quantize_rows (codec.cpp:244-265) from the row min/max keys.
+cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long long* keys,
+                              const uint8_t* bits_in, const double* C, float* rmin, float* rmax,
+                              uint8_t* rbits, uint16_t* q);
+// Anchor quantisation (codec.cpp:444-471), one CTA per axis.
+cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
+                           const void* const x[3], bool f32, int bits, float* rng, uint16_t* q);
+
+// ---- basis.cu (compiled with --fmad=false) ------------------------------
+// Householder factor of p columns of Z (m x p, per batch, in place) and
+// Qout (m x ncols) = H_0 ... H_{p-1} [e_c0 ... e_{c0+ncols-1}].
+cudaError_t launch_householder(cudaStream_t s, int nbatch, int m, int p, int c0, int ncols,
+                               double* Z, double* tau, double* Qout);
+// Round-robin Jacobi eigensolver of symmetric m x m A (col-major, per
+// batch).  work: nbatch * 2 * m2 * m2 doubles (m2 = m + m%2).  Writes V
+// (m x m) and w (m).  flags[3] set on non-convergence.
+cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
+                          double* V, double* w, int* flags);
+// Stable descending order of w: Vs[:, j] = V[:, idx[j]], ws[j] = w[idx[j]];
+// ld = leading dimension (rows) of V.
+cudaError_t launch_sort_basis(cudaStream_t s, int nbatch, int m, int ncols_store, const double* V,
+                              const double* w, double* Vs, long vs_batch_stride, double* ws,
+                              long ws_batch_stride);
+// canonicalize_signs (spectral.cpp:41-47) on columns [c0, c0+ncols) of
+// m-row column-major U (batch stride bs).
+cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int ncols, double* U,
+                               long bs);
+cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H);
+cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count);
+
+// ---- decode.cu ------------------------------------------------------------
+// Dequantiser parameters per retained row (QParams of quantize.cpp:15-20).
+cudaError_t launch_row_params(cudaStream_t s, int k, const float* rmin, const float* rmax,
+                              const uint8_t* rbits, double* rowp);
+// rhs = L^T delta~ + S^T a (solver.cpp:77-80) in the CG column-block layout.
+cudaError_t launch_rhs(cudaStream_t s, int n, int F, int W, int nblk, const uint32_t* lap_rp,
+                       const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
+                       const uint16_t* anchor_q, const float* anchor_rng, int anchor_bits,
+                       const double* D, double* B, int* flags);
+// Column-block CG on M = L^T L + S^T S (K7).
+cudaError_t launch_cg(cudaStream_t s, int n, int W, int nblk, const uint32_t* m_rp,
+                      const uint32_t* m_ci, const float* m_val, double* X, double* R, double* P,
+                      double* Q, double rtol, int maxit, int* iters, double* res);
+cudaError_t launch_output(cudaStream_t s, int n, int F, const double* X, void* const out[3],
+                          bool f32);
+
+}  // namespace dmcg

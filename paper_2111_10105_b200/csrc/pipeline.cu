@@ -1,0 +1,316 @@
+// Device orchestration of one plan: encode (K1 delta, K2 Gram, K3 basis,
+// K4 projection + quantisation, K5 dictionary / anchors) and decode (K6
+// dequantise + reconstruct + rhs, K7 CG), all on the context stream.
+// Reference call stacks: src/codec.cpp:351-473 (encode), 475-552 (decode).
+#include <cstring>
+#include <string>
+
+#include "gemm.cuh"
+#include "internal.h"
+#include "kernels.h"
+
+namespace dmcg {
+
+#define DMCG_TRY(expr)                                                            \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess)                                                        \
+      return Status{DMCG_E_CUDA, std::string("CudaError: ") + cudaGetErrorString(_e) + \
+                                     " at " #expr};                               \
+  } while (0)
+
+namespace {
+
+// ---- GEMM operand loaders / epilogues specific to the codec --------------
+
+// Projection epilogue (codec.cpp:420 + the row min/max of codec.cpp:253):
+// C[b][m][n] row-major (k x n), per-row running min/max as ordered keys.
+struct StoreCoeffMinMax {
+  double* C;
+  unsigned long long* keys;
+  __device__ __forceinline__ void operator()(int b, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = mb + i * 8 + (lane >> 2);
+      double lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = nb + j * 8 + (lane & 3) * 2 + e;
+          if (m < M && n < N) {
+            const double v = wt.acc[i][j][e];
+            C[((long)b * M + m) * N + n] = v;
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+          }
+        }
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, 2));
+      if ((lane & 3) == 0 && m < M && lo <= hi) {
+        atomicMin(&keys[2 * ((long)b * M + m)], ordered_key(lo));
+        atomicMax(&keys[2 * ((long)b * M + m) + 1], ordered_key(hi));
+      }
+    }
+  }
+};
+
+// Decode operand A(k = r, m = i) = dequantised coefficient c~(r, i) of axis
+// b (dequantize_rows, codec.cpp:267-288).  Out-of-range levels set flag.
+struct LoadCoeffDeq {
+  static constexpr bool kKContig = false;
+  const uint16_t* q;
+  const double* rowp;
+  const uint8_t* rbits;
+  int* flags;
+  int n, k;
+  __device__ __forceinline__ double operator()(int b, int r, int i) const {
+    const long row = (long)b * k + r;
+    const uint32_t lv = q[row * n + i];
+    const double min_ = rowp[2 * row], width = rowp[2 * row + 1];
+    if (width == 0.0) return min_;
+    if (lv >= (1u << rbits[row])) atomicOr(flags, 1);
+    return dequantize_level(min_, width, false, lv);
+  }
+};
+
+// Decode operand B(k = r, n = f) = U~(f, r), the dequantised dictionary
+// (decode_dictionaries / unpack_matrix, codec.cpp:330-349, 131-142).
+struct LoadDictDeq {
+  static constexpr bool kKContig = false;
+  const uint16_t* q;
+  double width;
+  uint32_t levels;
+  int F;
+  int* flags;
+  __device__ __forceinline__ double operator()(int b, int r, int f) const {
+    const uint32_t lv = q[((long)b * F + r) * F + f];
+    if (lv >= levels) atomicOr(flags, 1);
+    return dequantize_level(-1.0, width, false, lv);
+  }
+};
+
+// delta~ into the CG column-block layout: column c = b*F + f.
+struct StoreCG {
+  double* D;
+  int n, F;
+  __device__ __forceinline__ void operator()(int b, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int m = mb + r, f = nb + c;
+          if (m < M && f < N) {
+            const int col = b * F + f;
+            D[((size_t)(col / kCB) * n + m) * kCB + col % kCB] = wt.acc[i][j][e];
+          }
+        }
+  }
+};
+
+int pick_splits(int tiles, int nbatch, int K) {
+  const int want = 2 * 148;
+  int s = (want + tiles * nbatch - 1) / (tiles * nbatch);
+  const int maxs = (K + kBK - 1) / kBK;
+  if (s > maxs) s = maxs;
+  if (s < 1) s = 1;
+  return s;
+}
+
+template <typename T>
+Status gram(dmcg_plan* p, const void* const x[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int F = (int)p->F, n = (int)p->n;
+  const int tiles = ((F + kBM - 1) / kBM) * ((F + kBN - 1) / kBN);
+  int splits = pick_splits(tiles, 3, n);
+  const long maxs = (long)(p->part_elems / (3L * F * F));
+  if (splits > maxs) splits = (int)maxs;
+  splits = gemm_splits(n, splits, nullptr);
+  // R(f, g) = sum_i X(i, f) X(i, g): both operands X(k = i, m = f) = x[i*F + f].
+  LoadDense3<T, false> la{(const T*)x[0], (const T*)x[1], (const T*)x[2], (long)F, 1L};
+  DMCG_TRY(launch_gemm(s, 3, F, F, n, splits, la, la, StorePartial{p->d_part, 3}));
+  DMCG_TRY(launch_reduce_sym(s, F, splits, 3, p->d_part, p->d_R));
+  return Status::ok();
+}
+
+Status basis(dmcg_plan* p) {
+  cudaStream_t s = p->ctx->stream;
+  const int F = (int)p->F, k = (int)p->k;
+  const long FF = (long)F * F;
+  if (p->rounds <= 0 || k >= F || k == 0) {
+    // Reference n_b = 1 path: full_eigenbasis (spectral.cpp:49-67).
+    DMCG_TRY(launch_jacobi(s, 3, F, p->d_R, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
+    DMCG_TRY(launch_sort_basis(s, 3, F, F, p->d_V, p->d_w, p->d_U, FF, p->d_evals, F));
+    DMCG_TRY(launch_canon_signs(s, 3, F, 0, F, p->d_U, FF));
+    return Status::ok();
+  }
+  const long Fk = (long)F * k;
+  // Q0 = Householder Q of the seeded start matrix.
+  DMCG_TRY(cudaMemcpyAsync(p->d_Z, p->d_start, 3 * Fk * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  DMCG_TRY(launch_householder(s, 3, F, k, 0, k, p->d_Z, p->d_tau, p->d_Q));
+  // Z = R Q: A(k = f, m = g) = R[f*F + g], B(k = f, n = j) = Q[j*F + f].
+  LoadDense<double, false> lR{p->d_R, FF, (long)F, 1L};
+  LoadDense<double, true> lQ{p->d_Q, Fk, 1L, (long)F};
+  StoreStrided sZ{p->d_Z, Fk, 1L, (long)F};
+  for (int t = 0; t < p->rounds; ++t) {
+    DMCG_TRY(launch_gemm(s, 3, F, k, F, 1, lR, lQ, sZ));
+    DMCG_TRY(launch_householder(s, 3, F, k, 0, k, p->d_Z, p->d_tau, p->d_Q));
+  }
+  // Rayleigh-Ritz: H = Q^T (R Q).
+  DMCG_TRY(launch_gemm(s, 3, F, k, F, 1, lR, lQ, sZ));
+  LoadDense<double, true> lQt{p->d_Q, Fk, 1L, (long)F};
+  LoadDense<double, true> lZ{p->d_Z, Fk, 1L, (long)F};
+  double* H = p->d_C;  // k x k scratch (coefficient buffer is free here)
+  DMCG_TRY(launch_gemm(s, 3, k, k, F, 1, lQt, lZ, StoreStrided{H, (long)k * k, 1L, (long)k}));
+  DMCG_TRY(launch_symmetrize(s, 3, k, H));
+  DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
+  double* Ws = p->d_Z;  // k x k sorted Ritz vectors (Z is free)
+  DMCG_TRY(launch_sort_basis(s, 3, k, k, p->d_V, p->d_w, Ws, (long)k * k, p->d_evals, F));
+  // U[:, :k] = Q Ws: A(k = t, m = g) = Q[t*F + g], B(k = t, n = j) = Ws[j*k + t].
+  LoadDense<double, false> lQm{p->d_Q, Fk, (long)F, 1L};
+  LoadDense<double, true> lW{Ws, (long)k * k, 1L, (long)k};
+  DMCG_TRY(launch_gemm(s, 3, F, k, k, 1, lQm, lW, StoreStrided{p->d_U, FF, 1L, (long)F}));
+  DMCG_TRY(launch_canon_signs(s, 3, F, 0, k, p->d_U, FF));
+  // Completion to F x F: columns k..F-1 of the full Householder Q of U_k.
+  for (int a = 0; a < 3; ++a)
+    DMCG_TRY(cudaMemcpyAsync(p->d_Q + a * Fk, p->d_U + a * FF, Fk * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+  double* comp = p->d_H;  // F x (F-k) per axis scratch (jacobi work is free)
+  DMCG_TRY(launch_householder(s, 3, F, k, k, F - k, p->d_Q, p->d_tau, comp));
+  for (int a = 0; a < 3; ++a)
+    DMCG_TRY(cudaMemcpyAsync(p->d_U + a * FF + Fk, comp + (long)a * F * (F - k),
+                             (size_t)F * (F - k) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  DMCG_TRY(launch_canon_signs(s, 3, F, k, F - k, p->d_U, FF));
+  for (int a = 0; a < 3; ++a)
+    DMCG_TRY(launch_fill_zero(s, p->d_evals + (long)a * F + k, F - k));
+  return Status::ok();
+}
+
+}  // namespace
+
+// Host-side wrapper used by host.cpp.
+Status plan_encode(dmcg_plan* p, const void* const x[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
+  const bool f32 = p->dtype == DMCG_F32;
+  const long FF = (long)F * F;
+  DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
+  DMCG_TRY(cudaEventRecord(p->ev[0], s));
+  // K1 delta coordinates (codec.cpp:419).
+  DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
+  DMCG_TRY(cudaEventRecord(p->ev[1], s));
+  // K2 autocorrelation (spectral.cpp:35-39).
+  Status st = f32 ? gram<float>(p, x) : gram<double>(p, x);
+  if (!st.good()) return st;
+  DMCG_TRY(cudaEventRecord(p->ev[2], s));
+  // K3 basis.
+  st = basis(p);
+  if (!st.good()) return st;
+  DMCG_TRY(cudaEventRecord(p->ev[3], s));
+  // K5a dictionary levels (encode_dictionaries first block).
+  DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
+  // K4 projection coeffs = U_k^T delta^T (codec.cpp:420) + row min/max, then
+  // quantize_rows (codec.cpp:426).
+  if (k > 0) {
+    DMCG_TRY(launch_init_keys(s, 3L * k, p->d_keys));
+    LoadDense<double, true> lU{p->d_U, FF, 1L, (long)F};
+    LoadDense<double, true> lD{p->d_delta, (long)n * F, 1L, (long)F};
+    DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lD, StoreCoeffMinMax{p->d_C, p->d_keys}));
+    DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
+                               p->d_row_max, p->d_row_bits, p->d_coeff_q));
+  }
+  DMCG_TRY(cudaEventRecord(p->ev[4], s));
+  // K5b anchors (codec.cpp:444-471).
+  DMCG_TRY(launch_anchors(s, (int)p->n_c, F, p->d_anchor_idx, x, f32, p->anchor_bits,
+                          p->d_anchor_rng, p->d_anchor_q));
+  DMCG_TRY(cudaEventRecord(p->ev[5], s));
+  int flags[8];
+  DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  DMCG_TRY(cudaStreamSynchronize(s));
+  float ms;
+  cudaEventElapsedTime(&ms, p->ev[0], p->ev[5]);
+  p->stats.ms_encode = ms;
+  cudaEventElapsedTime(&p->stats.ms_delta, p->ev[0], p->ev[1]);
+  cudaEventElapsedTime(&p->stats.ms_gram, p->ev[1], p->ev[2]);
+  cudaEventElapsedTime(&p->stats.ms_basis, p->ev[2], p->ev[3]);
+  cudaEventElapsedTime(&p->stats.ms_project, p->ev[3], p->ev[4]);
+  p->stats.kernel_launches_encode =
+      1 + 2 + (p->rounds > 0 && k < F ? 2 * p->rounds + 12 : 3) + 1 + (k > 0 ? 3 : 0) + 1;
+  if (flags[0]) {
+    std::string axes;
+    for (int a = 0; a < 3; ++a)
+      if (flags[0] & (1 << a)) axes += (axes.empty() ? "" : ", ") + std::string(1, "xyz"[a]);
+    return Status{DMCG_E_INDEX, "ValidationError: non-finite coordinate in axis " + axes};
+  }
+  if (flags[3])
+    return Status{DMCG_E_NUMERICAL,
+                  "ConvergenceFailure: symmetric eigendecomposition did not converge"};
+  return Status::ok();
+}
+
+Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
+  const bool f32 = p->dtype == DMCG_F32;
+  DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
+  DMCG_TRY(cudaEventRecord(p->ev[0], s));
+  // K6: dequantise + reconstruct delta~ = (U~ c~)^T (codec.cpp:528-533)
+  // straight into the CG layout; rows >= k_l are exactly zero in the
+  // reference, so the contraction runs over r < k_l only.
+  const size_t vec = (size_t)p->nblk * n * kCB;
+  DMCG_TRY(cudaMemsetAsync(p->d_cg_q, 0, vec * sizeof(double), s));
+  if (k > 0) {
+    DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
+    LoadCoeffDeq la{p->d_coeff_q, p->d_rowp, p->d_row_bits, p->d_flags + 1, n, k};
+    const uint32_t levels = 1u << p->dict_bits;
+    LoadDictDeq lb{p->d_dict_q, 2.0 / (double)levels, levels, F, p->d_flags + 1};
+    DMCG_TRY(launch_gemm(s, 3, n, F, k, 1, la, lb, StoreCG{p->d_cg_q, n, F}));
+  }
+  // rhs = L^T delta~ + S^T a (solver.cpp:77-80) -> r
+  DMCG_TRY(launch_rhs(s, n, F, (int)p->W, (int)p->nblk, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos,
+                      (int)p->n_c, p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_cg_q,
+                      p->d_cg_r, p->d_flags + 1));
+  DMCG_TRY(cudaEventRecord(p->ev[1], s));
+  // K7 CG.
+  const double rtol = opt ? opt->cg_rtol : 1e-10;
+  const int maxit = opt ? opt->cg_max_iter : 20000;
+  DMCG_TRY(launch_cg(s, n, (int)p->W, (int)p->nblk, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_cg_x,
+                     p->d_cg_r, p->d_cg_p, p->d_cg_q, rtol, maxit, p->d_cg_iters, p->d_cg_res));
+  DMCG_TRY(cudaEventRecord(p->ev[2], s));
+  DMCG_TRY(launch_output(s, n, F, p->d_cg_x, out, f32));
+  DMCG_TRY(cudaEventRecord(p->ev[3], s));
+  int flags[8];
+  DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  std::vector<int> iters(p->W);
+  std::vector<double> res(p->W);
+  DMCG_TRY(cudaMemcpyAsync(iters.data(), p->d_cg_iters, p->W * sizeof(int), cudaMemcpyDeviceToHost, s));
+  DMCG_TRY(cudaMemcpyAsync(res.data(), p->d_cg_res, p->W * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DMCG_TRY(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&p->stats.ms_decode, p->ev[0], p->ev[3]);
+  cudaEventElapsedTime(&p->stats.ms_reconstruct, p->ev[0], p->ev[1]);
+  cudaEventElapsedTime(&p->stats.ms_cg, p->ev[1], p->ev[2]);
+  p->stats.kernel_launches_decode = (k > 0 ? 2 : 0) + 3;
+  int itmax = 0;
+  double resmax = 0.0;
+  for (uint32_t c = 0; c < p->W; ++c) {
+    itmax = iters[c] > itmax ? iters[c] : itmax;
+    resmax = res[c] > resmax ? res[c] : resmax;
+  }
+  p->stats.cg_iterations_max = itmax;
+  p->stats.cg_rel_residual_max = resmax;
+  if (flags[1]) return Status{DMCG_E_CORRUPT, "CorruptPayload: packed value out of range"};
+  if (!(resmax <= rtol))
+    return Status{DMCG_E_NUMERICAL, "SingularSystem: anchored solve did not converge (residual " +
+                                        std::to_string(resmax) + ")"};
+  return Status::ok();
+}
+
+}  // namespace dmcg
