@@ -197,6 +197,8 @@ typedef struct {
   float ms_encode, ms_decode; /* device time of the last calls (CUDA events) */
   float ms_delta, ms_gram, ms_basis, ms_project, ms_reconstruct, ms_cg;
   int kernel_launches_encode, kernel_launches_decode;
+  long long nnz_normal;       /* nnz of M = L^T L + S^T S */
+  long long nnz_laplacian;    /* nnz of L (incl. diagonal) */
 } dmcg_stats;
 int dmcg_plan_stats(const dmcg_plan* plan, dmcg_stats* out);
 /* Stats of the last drop-in dmcg_encode / dmcg_decode on this context. */

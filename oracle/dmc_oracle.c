@@ -530,7 +530,7 @@ void orc_start_matrix(uint64_t seed, size_t count, double* out) {
 
 int orc_basis(uint32_t F, uint32_t k, const double* R, int rounds, uint64_t seed, double* U,
               double* evals) {
-  if (rounds <= 0 || k >= F) {
+  if (rounds <= 0 || k >= F || k == 0) {
     /* rounds == 0: the reference's n_b = 1 path, codec.cpp:158-159. */
     return orc_full_eigenbasis(F, R, U, evals);
   }
@@ -1158,6 +1158,14 @@ static void spmm(uint32_t n, const uint32_t* lrow, const uint32_t* lcol, const d
   (void)nthreads;
 }
 
+static size_t g_last_lnz = 0;
+static double g_last_flops = 0.0;
+/* Factor statistics of the last orc_solve_anchored call (test / docs aid). */
+void orc_last_factor_stats(size_t* lnz, double* flops) {
+  *lnz = g_last_lnz;
+  *flops = g_last_flops;
+}
+
 int orc_solve_anchored(uint32_t n, const uint32_t* lrow, const uint32_t* lcol, const double* lval,
                        uint32_t W, const double* delta, uint32_t n_c, const uint32_t* idx,
                        const double* anchors, double* X, int nthreads) {
@@ -1189,6 +1197,13 @@ int orc_solve_anchored(uint32_t n, const uint32_t* lrow, const uint32_t* lcol, c
   }
   int rc = ldl_factorize(&M, &f);
   if (rc == 0) {
+    g_last_lnz = f.Lp[n];
+    double fl = 0.0;
+    for (uint32_t j = 0; j < n; ++j) {
+      const double c = (double)(f.Lp[j + 1] - f.Lp[j]);
+      fl += c * c;
+    }
+    g_last_flops = fl;
     /* rhs = L^T delta + S^T a (solver.cpp:77-80) */
     double* rhs = malloc((size_t)n * W * sizeof(double));
     spmm(n, lrow, lcol, lval, delta, rhs, W, nthreads);

@@ -81,7 +81,8 @@ class DmcgStats(ctypes.Structure):
                 ("ms_delta", ctypes.c_float), ("ms_gram", ctypes.c_float),
                 ("ms_basis", ctypes.c_float), ("ms_project", ctypes.c_float),
                 ("ms_reconstruct", ctypes.c_float), ("ms_cg", ctypes.c_float),
-                ("kernel_launches_encode", ctypes.c_int), ("kernel_launches_decode", ctypes.c_int)]
+                ("kernel_launches_encode", ctypes.c_int), ("kernel_launches_decode", ctypes.c_int),
+                ("nnz_normal", ctypes.c_longlong), ("nnz_laplacian", ctypes.c_longlong)]
 
 
 _lib = None

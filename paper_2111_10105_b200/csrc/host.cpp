@@ -442,6 +442,8 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->mesh.anchor_pos.assign(n, -1);
   for (uint32_t t = 0; t < p->n_c; ++t) p->mesh.anchor_pos[p->mesh.anchors[t]] = (int32_t)t;
   build_normal_matrix(&p->mesh);
+  p->stats.nnz_normal = (long long)p->mesh.m_ci.size();
+  p->stats.nnz_laplacian = (long long)p->mesh.lap_ci.size();
 
   const uint32_t k = p->k;
   p->W = 3 * F;

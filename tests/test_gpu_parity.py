@@ -1,0 +1,263 @@
+"""GPU parity: libdmcg (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances:
+
+  P1/P2  anchor indices, anchor levels + ranges, header, section sizes: bit-exact
+  P3     basis columns j with lambda_j >= 1e-6 lambda_1 and relative gaps
+         >= 1e-3 to both neighbours: max|u_gpu - u_cpu| <= 1e-9, and their
+         16-bit dictionary levels bit-exact
+  P4     coefficient symbols on those rows: bit-exact except <= 1e-4 of a
+         row with |delta| = 1 (fp64 boundary ties); row (min, max) equal
+  P5     same stream decoded: max|x_gpu - x_cpu| <= 1e-8 bbox (f64, CG rtol
+         1e-10) / 1e-4 bbox (f32 output); end to end |RMSE_gpu/RMSE_cpu - 1| <= 1e-3
+  P6     bvpv identical
+"""
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_2111_10105_b200 import codec as C
+from paper_2111_10105_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(cfgspec, rounds=None):
+    return C.EncoderConfig(k_l=cfgspec.k, row_bits=[cfgspec.bits] * cfgspec.k,
+                           oi_rounds=cfgspec.rounds if rounds is None else rounds)
+
+
+def _agreeing_columns(ev, k):
+    ev = np.asarray(ev[:k], dtype=float)
+    cols = []
+    for j in range(k):
+        if ev[j] < 1e-6 * ev[0]:
+            break
+        lo = ev[j + 1] if j + 1 < len(ev) else 0.0
+        gap_lo = (ev[j] - lo) / ev[j]
+        gap_hi = (ev[j - 1] - ev[j]) / ev[j - 1] if j > 0 else 1.0
+        if gap_lo >= 1e-3 and gap_hi >= 1e-3:
+            cols.append(j)
+    return cols
+
+
+def _oracle_stream_of(g, s):
+    og = O.Encoded(g.n, g.F, g.k_l, g.n_c, s.faces, g.anchor_bits, g.dict_bits)
+    for a in range(3):
+        og.dict_q[a][:] = g.dict_q[a]
+        if g.k_l:
+            og.row_min[a][:] = g.row_min[a][:g.k_l]
+            og.row_max[a][:] = g.row_max[a][:g.k_l]
+            og.row_bits[a][:] = g.row_bits[a][:g.k_l]
+            og.coeff_q[a][:] = g.coeff_q[a][:g.k_l]
+        og.anchor_q[a][:] = g.anchor_q[a]
+        og.s.anchor_min[a] = g.anchor_min[a]
+        og.s.anchor_max[a] = g.anchor_max[a]
+    og.anchor_idx[:] = g.anchor_idx
+    return og
+
+
+def check_parity(codec, s, spec, rounds=None, f32_out=False):
+    rounds = spec.rounds if rounds is None else rounds
+    ec = _cfg(spec, rounds)
+    g = codec.encode(s, ec)
+    o = O.encode(s, spec.k, spec.bits, rounds=rounds, seed=0, nthreads=8)
+    n, F, k = s.n, s.F, spec.k
+    # P1 / P2
+    assert np.array_equal(g.anchor_idx, o.anchor_idx)
+    for a in range(3):
+        assert np.array_equal(g.anchor_q[a], o.anchor_q[a])
+        assert g.anchor_min[a] == o.s.anchor_min[a] and g.anchor_max[a] == o.s.anchor_max[a]
+    gb, gs = C.serialize(g)
+    ob, os_ = O.serialize(o)
+    assert gs == os_ and len(gb) == len(ob)
+    # P6
+    assert C.rate_exact(g) == pytest.approx(O.rate_exact(o), rel=0, abs=0)
+    # P3 / P4
+    for a in range(3):
+        cols = _agreeing_columns(o.evals[a], k)
+        assert cols and cols[0] == 0
+        Ug = g.dict_q[a]  # levels; compare the float basis through the plan below
+        for j in cols:
+            assert np.array_equal(Ug[j], o.dict_q[a][j]), (a, j)
+            assert g.row_min[a][j] == o.row_min[a][j] and g.row_max[a][j] == o.row_max[a][j], (a, j)
+            d = g.coeff_q[a][j].astype(np.int64) - o.coeff_q[a][j].astype(np.int64)
+            assert np.abs(d).max() <= 1 and np.count_nonzero(d) <= max(1, 1e-4 * n), (a, j)
+    # P5 same stream
+    xg = codec.decode(g, rtol=1e-10, dtype=np.float32 if f32_out else np.float64)
+    xo = O.decode(_oracle_stream_of(g, s), nthreads=8)
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
+    tol = (1e-4 if f32_out else 1e-8) * bbox
+    for a in range(3):
+        assert np.abs(xg[a].astype(np.float64) - xo[a]).max() <= tol
+    # P5 end to end
+    xoo = O.decode(o, nthreads=8)
+    r_g = O.frame_rms([np.asarray(x, np.float64) for x in s.axes], [x.astype(np.float64) for x in xg])
+    r_o = O.frame_rms([np.asarray(x, np.float64) for x in s.axes], xoo)
+    assert abs(r_g.mean() / r_o.mean() - 1) <= 1e-3
+    return g, o
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_config_parity(codec, name):
+    spec = synth.CONFIGS[name]
+    check_parity(codec, spec.make(), spec)
+
+
+def test_config4_sequence_parity(codec):
+    spec = synth.CONFIGS["c4"]
+    check_parity(codec, spec.make(3), spec)
+
+
+def test_config2_parity_f64(codec):
+    spec = synth.CONFIGS["c2"]
+    check_parity(codec, spec.make(), spec)
+
+
+def test_config2_parity_f32(codec):
+    spec = synth.CONFIGS["c2f32"]
+    s = spec.make()
+    check_parity(codec, s, spec, f32_out=True)
+
+
+def test_full_eigenbasis_mode_matches_reference_path(codec):
+    """oi_rounds = 0 is the reference's own n_b = 1 path (codec.cpp:158-159)."""
+    spec = synth.CONFIGS["c0"]
+    check_parity(codec, spec.make(), spec, rounds=0)
+
+
+def test_basis_float_parity_and_orthonormality(codec):
+    spec = synth.CONFIGS["c0"]
+    s = spec.make()
+    plan = C.Plan(codec, s.n, s.F, s.faces, _cfg(spec))
+    import torch
+    d = [torch.from_numpy(x).cuda() for x in s.axes]
+    plan.encode_device([t.data_ptr() for t in d])
+    for a in range(3):
+        Ug, evg = plan.basis(a)
+        Uo, evo = O.basis(O.autocorrelation(s.axes[a]), spec.k, spec.rounds, a)
+        assert np.abs(Ug.T @ Ug - np.eye(s.F)).max() < 1e-8
+        for j in _agreeing_columns(evo, spec.k):
+            assert np.abs(Ug[:, j] - Uo[:, j]).max() <= 1e-9
+            assert abs(evg[j] - evo[j]) <= 1e-12 * evo[0]
+
+
+def test_device_plan_matches_dropin(codec):
+    import torch
+    spec = synth.CONFIGS["c0"]
+    s = spec.make()
+    ec = _cfg(spec)
+    g = codec.encode(s, ec)
+    plan = C.Plan(codec, s.n, s.F, s.faces, ec)
+    d = [torch.from_numpy(x).cuda() for x in s.axes]
+    out = [torch.empty_like(t) for t in d]
+    plan.encode_device([t.data_ptr() for t in d])
+    p = plan.download()
+    assert C.serialize(p)[0] == C.serialize(g)[0]
+    plan.decode_device([t.data_ptr() for t in out])
+    xg = codec.decode(g)
+    for a in range(3):
+        assert np.array_equal(out[a].cpu().numpy(), xg[a])
+    st = plan.stats()
+    assert st["cg_iterations_max"] > 0 and st["cg_rel_residual_max"] <= 1e-10
+
+
+def test_stream_roundtrip_through_gpu(codec):
+    spec = synth.CONFIGS["c0"]
+    s = spec.make()
+    g = codec.encode(s, _cfg(spec))
+    data, _ = C.serialize(g)
+    p = C.parse(data)
+    x1 = codec.decode(g)
+    x2 = codec.decode(p)
+    for a in range(3):
+        assert np.array_equal(x1[a], x2[a])
+
+
+# ---- edge cases -------------------------------------------------------------
+
+def _small(F=16, level=1, seed=5):
+    return synth.sphere(level, F, 3, 0, seed=seed)
+
+
+def test_kl_zero(codec):
+    s = _small()
+    g = codec.encode(s, C.EncoderConfig(k_l=0, oi_rounds=3, anchor_fraction=0.1))
+    o = O.encode(s, 0, 12, rounds=3, anchor_fraction=0.1)
+    assert C.serialize(g)[0] == O.serialize(o)[0]
+    x = codec.decode(g)
+    xo = O.decode(o)
+    for a in range(3):
+        assert np.abs(x[a] - xo[a]).max() < 1e-8
+
+
+def test_static_animation_degenerate_rows(codec):
+    s = _small()
+    s.axes = [np.repeat(ax[:, :1], s.F, axis=1).copy() for ax in s.axes]
+    spec = synth.Config("static", 4, 5, 12, "f64", None)
+    g, o = check_parity(codec, s, spec, rounds=5)
+    assert C.rate_exact(g)["q_s"] == O.rate_exact(o)["q_s"]
+
+
+def test_tiny_mesh_full_rank(codec):
+    s = synth.sphere(0, 5, 2, 0, seed=9)   # icosahedron: 12 vertices, F = 5
+    spec = synth.Config("tiny", 5, 0, 16, "f64", None)
+    g, _ = check_parity(codec, s, spec, rounds=0)
+    x = codec.decode(g)
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
+    for a in range(3):  # lossless limit
+        assert np.abs(x[a] - s.axes[a]).max() < 1e-3 * bbox
+
+
+def test_varying_row_bits(codec):
+    s = _small(F=20)
+    bits = [16, 14, 12, 10, 8, 6, 4, 2]
+    g = codec.encode(s, C.EncoderConfig(k_l=8, row_bits=bits, oi_rounds=0, anchor_fraction=0.1))
+    o = O.encode(s, 8, bits, rounds=0, anchor_fraction=0.1)
+    for a in range(3):
+        assert list(g.row_bits[a][:8]) == bits
+    assert len(C.serialize(g)[0]) == len(O.serialize(o)[0])
+
+
+def test_errors(codec):
+    s = _small()
+    bad = [ax.copy() for ax in s.axes]
+    bad[1][3, 2] = np.nan
+    s_bad = synth.Sequence(s.faces, bad)
+    with pytest.raises(C.DmcError) as e:
+        codec.encode(s_bad, C.EncoderConfig(k_l=4))
+    assert e.value.code == 4 and "axis y" in str(e.value)
+    with pytest.raises(C.DmcError) as e:
+        codec.encode(s, C.EncoderConfig(k_l=s.F + 1))
+    assert e.value.code == 5
+    with pytest.raises(C.DmcError) as e:
+        codec.encode(s, C.EncoderConfig(k_l=4, anchor_bits=17))
+    assert e.value.code == 5
+    with pytest.raises(C.DmcError) as e:
+        codec.encode(s, C.EncoderConfig(k_l=4, variant=3))
+    assert e.value.code == 11
+    two = synth.Sequence(np.array([[0, 1, 2], [3, 4, 5]], np.uint32),
+                         [np.random.default_rng(0).normal(size=(6, 3)) for _ in range(3)])
+    with pytest.raises(C.DmcError) as e:
+        codec.encode(two, C.EncoderConfig(k_l=2))
+    assert e.value.code == 4 and "not connected" in str(e.value)
+    # corrupt payload: a dictionary level beyond 2^dict_bits
+    g = codec.encode(s, C.EncoderConfig(k_l=4, dict_bits=8, oi_rounds=2))
+    g.dict_q[0][0, 0] = 300
+    with pytest.raises(C.DmcError) as e:
+        codec.decode(g)
+    assert e.value.code == 6
+
+
+@pytest.mark.slow
+def test_config3_full_size_properties(codec):
+    """C3 is too large for the oracle; check size-independent properties."""
+    spec = synth.CONFIGS["c3"]
+    s = spec.make()
+    g = codec.encode(s, _cfg(spec))
+    data, _ = C.serialize(g)
+    assert abs(C.rate_exact(g)["q_s"] - 18.948) < 2e-3   # BASELINE.md §2 analytic
+    assert C.serialize(C.parse(data))[0] == data
+    x = codec.decode(g, dtype=np.float32)
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
+    err = max(np.abs(x[a] - s.axes[a]).max() for a in range(3))
+    assert err < 1e-2 * bbox
