@@ -96,6 +96,11 @@ void dmcg_config_default(dmcg_config* cfg);
 typedef struct {
   double cg_rtol;           /* per-column ||r||/||b|| stop, default 1e-10 */
   int cg_max_iter;          /* default 20000 */
+  int solver;               /* 0 (default): supernodal Cholesky on the GPU, the
+                               reference's factor + back-substitute scheme;
+                               1: conjugate gradients */
+  int refine;               /* refinement passes after the direct solve
+                               (default 1, like refine_anchored, solver.cpp:43-58) */
 } dmcg_decode_options;
 
 void dmcg_decode_options_default(dmcg_decode_options* opt);
@@ -199,12 +204,27 @@ typedef struct {
   int kernel_launches_encode, kernel_launches_decode;
   long long nnz_normal;       /* nnz of M = L^T L + S^T S */
   long long nnz_laplacian;    /* nnz of L (incl. diagonal) */
+  float ms_factor, ms_solve;  /* direct solver: numeric factorisation, solves (+refine) */
+  int solver;                 /* solver used by the last decode */
+  int supernodes, levels;     /* supernodal structure of M */
+  long long nnz_factor;       /* stored entries of the Cholesky factor */
+  double flops_factor, flops_solve;  /* per decode */
+  double analyze_seconds;     /* host symbolic analysis (plan creation) */
 } dmcg_stats;
 int dmcg_plan_stats(const dmcg_plan* plan, dmcg_stats* out);
 /* Stats of the last drop-in dmcg_encode / dmcg_decode on this context. */
 int dmcg_ctx_stats(const dmcg_ctx* ctx, dmcg_stats* out);
 /* Stream the plan runs on (cudaStream_t), for event timing by callers. */
 void* dmcg_plan_stream(dmcg_plan* plan);
+
+/* ---- diagnostics (host only, no GPU) ----------------------------------
+ * Symbolic analysis of the anchored normal matrix of a mesh and, when W > 0,
+ * a CPU solve M x = b (b, x: n x W row-major) with the same supernodal data
+ * flow the GPU uses.  stats[0..7] = supernodes, levels, nnz(L), factor flops,
+ * solve flops per rhs, max front, max width, analysis seconds. */
+int dmcg_debug_chol(uint32_t n, const uint32_t* faces, uint32_t n_faces, uint32_t n_c,
+                    const uint32_t* anchors, uint32_t W, const double* b, double* x,
+                    double stats[8]);
 
 #ifdef __cplusplus
 }

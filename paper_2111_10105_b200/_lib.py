@@ -31,7 +31,7 @@ EXPORTS = [
     "dmcg_serialize", "dmcg_parse_header", "dmcg_parse", "dmcg_parse_error", "dmcg_rate_exact",
     "dmcg_anchor_count", "dmcg_select_anchors", "dmcg_plan_create", "dmcg_plan_destroy",
     "dmcg_plan_encode_device", "dmcg_plan_decode_device", "dmcg_plan_download", "dmcg_plan_upload",
-    "dmcg_plan_basis", "dmcg_plan_stats", "dmcg_ctx_stats", "dmcg_plan_stream",
+    "dmcg_plan_basis", "dmcg_plan_stats", "dmcg_ctx_stats", "dmcg_plan_stream", "dmcg_debug_chol",
 ]
 
 
@@ -46,7 +46,8 @@ class DmcgConfig(ctypes.Structure):
 
 
 class DmcgDecodeOptions(ctypes.Structure):
-    _fields_ = [("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int)]
+    _fields_ = [("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int),
+                ("solver", ctypes.c_int), ("refine", ctypes.c_int)]
 
 
 class DmcgSeq(ctypes.Structure):
@@ -82,7 +83,11 @@ class DmcgStats(ctypes.Structure):
                 ("ms_basis", ctypes.c_float), ("ms_project", ctypes.c_float),
                 ("ms_reconstruct", ctypes.c_float), ("ms_cg", ctypes.c_float),
                 ("kernel_launches_encode", ctypes.c_int), ("kernel_launches_decode", ctypes.c_int),
-                ("nnz_normal", ctypes.c_longlong), ("nnz_laplacian", ctypes.c_longlong)]
+                ("nnz_normal", ctypes.c_longlong), ("nnz_laplacian", ctypes.c_longlong),
+                ("ms_factor", ctypes.c_float), ("ms_solve", ctypes.c_float), ("solver", ctypes.c_int),
+                ("supernodes", ctypes.c_int), ("levels", ctypes.c_int),
+                ("nnz_factor", ctypes.c_longlong), ("flops_factor", ctypes.c_double),
+                ("flops_solve", ctypes.c_double), ("analyze_seconds", ctypes.c_double)]
 
 
 _lib = None

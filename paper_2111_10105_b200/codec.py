@@ -129,6 +129,12 @@ class CompressedAnimation:
         self.anchor_max = [float(e.anchor_max[a]) for a in range(3)]
 
 
+def _decode_opts(rtol, max_iter, solver, refine):
+    if solver not in ("direct", "cg"):
+        raise ValueError(f"solver must be 'direct' or 'cg', not {solver!r}")
+    return L.DmcgDecodeOptions(rtol, max_iter, 0 if solver == "direct" else 1, refine)
+
+
 def _check(ctx, rc):
     if rc != L.DMCG_OK:
         msg = L.lib().dmcg_last_error(ctx).decode() if ctx else ERROR_KINDS.get(rc, "Error")
@@ -185,10 +191,11 @@ class Codec:
         return out
 
     def decode(self, c: CompressedAnimation, rtol: float = 1e-10, max_iter: int = 20000,
-               dtype=np.float64):
+               dtype=np.float64, solver: str = "direct", refine: int = 1):
         """dmc::decode (include/dmc/codec.hpp:91; src/codec.cpp:475-552).
-        Returns the three (n, F) axis arrays."""
-        opt = L.DmcgDecodeOptions(rtol, max_iter)
+        Returns the three (n, F) axis arrays.  solver "direct" (supernodal
+        Cholesky + refine passes, the reference scheme) or "cg"."""
+        opt = _decode_opts(rtol, max_iter, solver, refine)
         out = [np.empty((c.n, c.F), dtype=dtype) for _ in range(3)]
         ptrs = (ctypes.c_void_p * 3)(*[o.ctypes.data for o in out])
         e = c.to_c()
@@ -236,8 +243,8 @@ class Plan:
         ptrs = (ctypes.c_void_p * 3)(*[int(p) for p in d_axes])
         _check(self.codec.handle, L.lib().dmcg_plan_encode_device(self._p, ptrs))
 
-    def decode_device(self, d_out, rtol=1e-10, max_iter=20000):
-        opt = L.DmcgDecodeOptions(rtol, max_iter)
+    def decode_device(self, d_out, rtol=1e-10, max_iter=20000, solver="direct", refine=1):
+        opt = _decode_opts(rtol, max_iter, solver, refine)
         ptrs = (ctypes.c_void_p * 3)(*[int(p) for p in d_out])
         _check(self.codec.handle, L.lib().dmcg_plan_decode_device(self._p, ctypes.byref(opt), ptrs))
 

@@ -1,0 +1,554 @@
+// K7 (direct) — supernodal multifrontal Cholesky of M = L^T L + S^T S and the
+// multi-RHS solve, level by level over the supernodal elimination tree.
+//
+// Per level (leaves first):
+//   assemble  one CTA per front: zero, scatter M, extend-add children
+//   panel     one CTA per front: unblocked Cholesky of a 32-column panel
+//   trailing  grouped DMMA tiles (64x64, K = 32) over every front's
+//             lower-triangular trailing block  (C -= P P^T)
+//   inverse   one CTA per front: L11^{-1} (row-major) so the solves are GEMMs
+// Solves (forward L y = P b leaves-first, backward L^T x = y roots-first)
+// are grouped DMMA GEMMs per level over (front, 64-row tile, 64-column tile).
+// Reference semantics: SimplicialLDLT factor + solve + one refinement pass
+// (src/solver.cpp:43-58, 82-90); the refinement is done by the caller.
+#include <cfloat>
+
+#include "chol_dev.h"
+#include "gemm.cuh"
+
+namespace dmcg {
+
+namespace {
+
+__device__ __forceinline__ uint32_t front_m(const CholDev& d, uint32_t s) {
+  return (uint32_t)(d.str_ptr[s + 1] - d.str_ptr[s]);
+}
+__device__ __forceinline__ uint32_t front_w(const CholDev& d, uint32_t s) {
+  return d.first[s + 1] - d.first[s];
+}
+
+// Assembly, parallel over 32-column chunks of each front: zero the chunk,
+// scatter M's entries, then extend-add every child's update columns that
+// land in the chunk (children in order, so the sum order is deterministic).
+constexpr int kAsmCols = 32;
+
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_assemble(CholDev d, const uint32_t* lsup) {
+  const uint32_t s = lsup[blockIdx.y];
+  const uint32_t m = front_m(d, s);
+  const uint32_t cc0 = blockIdx.x * kAsmCols;
+  if (cc0 >= m) return;
+  const uint32_t cc1 = min(m, cc0 + kAsmCols);
+  double* A = d.F + d.front_off[s];
+  for (long t = threadIdx.x; t < (long)(cc1 - cc0) * m; t += blockDim.x)
+    A[(size_t)cc0 * m + t] = 0.0;
+  __syncthreads();
+  {
+    const uint32_t* pos = d.a_pos + d.a_ptr[s];
+    const uint32_t na = (uint32_t)(d.a_ptr[s + 1] - d.a_ptr[s]);
+    const uint32_t e0 = lower_bound_u32(pos, na, cc0 * m);
+    const uint32_t e1 = lower_bound_u32(pos, na, cc1 * m);
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+      A[pos[e]] = (double)d.a_val[d.a_ptr[s] + e];
+  }
+  __syncthreads();
+  for (uint32_t q = d.child_ptr[s]; q < d.child_ptr[s + 1]; ++q) {
+    const uint32_t c = d.child_idx[q];
+    const uint32_t mc = front_m(d, c), wc = front_w(d, c), uc = mc - wc;
+    const double* C = d.F + d.front_off[c];
+    const uint32_t* rel = d.rel_idx + d.rel_ptr[c];
+    const uint32_t b0 = lower_bound_u32(rel, uc, cc0);
+    const uint32_t b1 = lower_bound_u32(rel, uc, cc1);
+    for (uint32_t b = b0; b < b1; ++b) {
+      const double* src = C + (size_t)(wc + b) * mc + wc;
+      double* dst = A + (size_t)rel[b] * m;
+      for (uint32_t a = b + threadIdx.x; a < uc; a += blockDim.x) dst[rel[a]] += src[a];
+    }
+    __syncthreads();
+  }
+}
+
+// Unblocked right-looking Cholesky of panel columns [k0, k0 + pw), staged in
+// shared memory when (m - k0) x pw fits (else in place in global memory).
+constexpr int kPanelThreads = 512;
+
+__global__ void __launch_bounds__(kPanelThreads)
+    k_panel(CholDev d, const uint32_t* lsup, int k0, int nb, int smem_rows) {
+  extern __shared__ double Ps[];
+  __shared__ double s_r;
+  const uint32_t s = lsup[blockIdx.x];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s);
+  if (k0 >= w) return;
+  const int pw = min(nb, w - k0);
+  double* A = d.F + d.front_off[s];
+  const int rows = m - k0;
+  const bool staged = rows <= smem_rows;
+  double* P;
+  int ld;
+  if (staged) {
+    P = Ps;
+    ld = rows;
+    for (int t = threadIdx.x; t < rows * pw; t += blockDim.x) {
+      const int c = t / rows, r = t % rows;
+      P[t] = A[(size_t)(k0 + c) * m + k0 + r];
+    }
+    __syncthreads();
+  } else {
+    P = A + (size_t)k0 * m + k0;
+    ld = m;
+  }
+  for (int j = 0; j < pw; ++j) {
+    double* cj = P + (size_t)j * ld;
+    if (threadIdx.x == 0) {
+      const double dj = cj[j];
+      if (!(dj > 0.0)) atomicOr(d.flags, 1);
+      s_r = sqrt(fmax(dj, DBL_MIN));
+      cj[j] = s_r;
+    }
+    __syncthreads();
+    const double r = s_r;
+    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x) cj[i] = cj[i] / r;
+    __syncthreads();
+    const int rem = pw - j - 1;
+    for (int t = threadIdx.x; t < rem * rows; t += blockDim.x) {
+      const int c = j + 1 + t / rows, i = t % rows;
+      if (i >= c) P[(size_t)c * ld + i] -= cj[i] * cj[c];
+    }
+    __syncthreads();
+  }
+  if (staged)
+    for (int t = threadIdx.x; t < rows * pw; t += blockDim.x) {
+      const int c = t / rows, r = t % rows;
+      A[(size_t)(k0 + c) * m + k0 + r] = P[t];
+    }
+}
+
+// Trailing update of each front in the level: A22 -= P P^T (lower tiles).
+struct LoadPanel {
+  static constexpr bool kKContig = false;
+  const double* A;
+  int m, k0, off;
+  __device__ __forceinline__ double operator()(int, int k, int i) const {
+    return A[(size_t)(k0 + k) * m + off + i];
+  }
+};
+struct SubLower {
+  double* A;
+  int m, off;
+  __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int mi = mb + r, ni = nb + c;
+          if (mi < M && ni < N && mi >= ni)
+            A[(size_t)(off + ni) * m + off + mi] -= wt.acc[i][j][e];
+        }
+  }
+};
+
+__global__ void __launch_bounds__(kGemmThreads)
+    k_trailing(CholDev d, const uint32_t* lsup, int k0, int nb) {
+  const uint32_t s = lsup[blockIdx.y];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s);
+  if (k0 >= w) return;
+  const int pw = min(nb, w - k0);
+  const int off = k0 + pw, T = m - off;
+  if (T <= 0) return;
+  const int nt = (T + kBM - 1) / kBM;
+  const int t = blockIdx.x;
+  if (t >= nt * (nt + 1) / 2) return;
+  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  const int tj = t - ti * (ti + 1) / 2;
+  double* A = d.F + d.front_off[s];
+  LoadPanel lp{A, m, k0, off};
+  gemm_tile(0, T, T, ti * kBM, tj * kBN, 0, pw, 0, lp, lp, SubLower{A, m, off});
+}
+
+// V = L11^{-1} (row-major w x w) in 64-blocks.  Step 1: invert every
+// diagonal 64x64 block (one CTA per block, one thread per column, in smem).
+constexpr int kIB = 64;
+
+constexpr size_t kInvDiagSmem = 2 * kIB * (kIB + 1) * sizeof(double);
+
+__global__ void __launch_bounds__(kIB) k_inv_diag(CholDev d, const uint32_t* lsup) {
+  extern __shared__ double inv_smem[];
+  double(*Ls)[kIB + 1] = reinterpret_cast<double(*)[kIB + 1]>(inv_smem);
+  double(*Xs)[kIB + 1] = reinterpret_cast<double(*)[kIB + 1]>(inv_smem + kIB * (kIB + 1));
+  const uint32_t s = lsup[blockIdx.y];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s);
+  const int b0 = blockIdx.x * kIB;
+  if (b0 >= w) return;
+  const int bs = min(kIB, w - b0);
+  const double* A = d.F + d.front_off[s];
+  double* V = d.Linv + d.inv_off[s];
+  const int c = threadIdx.x;
+  for (int r = 0; r < bs; ++r) Ls[r][c] = (c < bs && c <= r) ? A[(size_t)(b0 + c) * m + b0 + r] : 0.0;
+  __syncthreads();
+  if (c < bs) {
+    for (int r = 0; r < bs; ++r) {
+      if (r < c) {
+        Xs[r][c] = 0.0;
+        continue;
+      }
+      double acc = (r == c) ? 1.0 : 0.0;
+      for (int k = c; k < r; ++k) acc -= Ls[r][k] * Xs[k][c];
+      Xs[r][c] = acc / Ls[r][r];
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < bs; ++r)
+    if (c < bs) V[(size_t)(b0 + r) * w + b0 + c] = Xs[r][c];
+}
+
+// Step 2: one CTA per block column J walks the row blocks i > J in order:
+//   T = sum_{k = J..i-1} L(i, k) X(k, J)      (DMMA, K = 64 (i - J))
+//   X(i, J) = -X(i, i) T                       (DMMA, K = 64)
+struct LoadLinvRM {  // X(k, c) = V[(r0 + k) * w + c0 + c]
+  static constexpr bool kKContig = false;
+  const double* V;
+  int w, r0, c0;
+  __device__ __forceinline__ double operator()(int, int k, int c) const {
+    return V[(size_t)(r0 + k) * w + c0 + c];
+  }
+};
+struct LoadLinvRowsK {  // X(k, r) = V[(r0 + r) * w + c0 + k]   (k contiguous)
+  static constexpr bool kKContig = true;
+  const double* V;
+  int w, r0, c0;
+  __device__ __forceinline__ double operator()(int, int k, int r) const {
+    return V[(size_t)(r0 + r) * w + c0 + k];
+  }
+};
+struct LoadFrontCM {  // X(k, r) = A[(c0 + k) * m + r0 + r]
+  static constexpr bool kKContig = false;
+  const double* A;
+  int m, r0, c0;
+  __device__ __forceinline__ double operator()(int, int k, int r) const {
+    return A[(size_t)(c0 + k) * m + r0 + r];
+  }
+};
+struct LoadColMajorT {  // X(k, i) = p[k * ld + i]
+  static constexpr bool kKContig = false;
+  const double* p;
+  int ld;
+  __device__ __forceinline__ double operator()(int, int k, int i) const {
+    return p[(size_t)k * ld + i];
+  }
+};
+struct StoreTile {  // out[r * ld + c] = sign * v
+  double* out;
+  int ld;
+  double sign;
+  __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int mi = mb + r, ni = nb + c;
+          if (mi < M && ni < N) out[(size_t)mi * ld + ni] = sign * wt.acc[i][j][e];
+        }
+  }
+};
+
+__global__ void __launch_bounds__(kGemmThreads) k_inv_offdiag(CholDev d, const uint32_t* lsup,
+                                                              double* scratch) {
+  const uint32_t s = lsup[blockIdx.y];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s);
+  const int J = blockIdx.x, c0 = J * kIB;
+  if (c0 >= w) return;
+  const int cw = min(kIB, w - c0);
+  const double* A = d.F + d.front_off[s];
+  double* V = d.Linv + d.inv_off[s];
+  double* T = scratch + ((size_t)blockIdx.y * gridDim.x + J) * kIB * kIB;
+  for (int r0 = c0 + kIB; r0 < w; r0 += kIB) {
+    const int rh = min(kIB, w - r0);
+    // T(rh x cw) = L(r0.., c0..r0) X(c0..r0, c0..)
+    gemm_tile(0, rh, cw, 0, 0, 0, r0 - c0, 0, LoadFrontCM{A, m, r0, c0},
+              LoadLinvRM{V, w, c0, c0}, StoreTile{T, kIB, 1.0});
+    __syncthreads();
+    // X(r0.., c0..) = -X(r0.., r0..) T
+    gemm_tile(0, rh, cw, 0, 0, 0, rh, 0, LoadLinvRowsK{V, w, r0, r0},
+              LoadColMajorT{T, kIB}, StoreTile{V + (size_t)r0 * w + c0, w, -1.0});
+    __syncthreads();
+  }
+}
+
+// ---- solves -------------------------------------------------------------
+
+// R_s = [b(perm) for own columns; 0] + extend-add of the children's updates.
+// Parallel over (row chunk of 32, column tile of 64, front); each child's
+// rows landing in the chunk form a contiguous range (rel is increasing).
+__global__ void __launch_bounds__(256) k_solve_gather(CholDev d, const uint32_t* lsup,
+                                                      const double* __restrict__ b) {
+  const uint32_t s = lsup[blockIdx.z];
+  const int W = (int)d.W;
+  const int c0 = blockIdx.y * 64;
+  const int cw = min(64, W - c0);
+  const uint32_t m = front_m(d, s), w = front_w(d, s), f0 = d.first[s];
+  const uint32_t r0 = blockIdx.x * 32;
+  if (r0 >= m) return;
+  const uint32_t r1 = min(m, r0 + 32);
+  double* R = d.R + d.rhs_off[s] * W;
+  for (long t = threadIdx.x; t < (long)(r1 - r0) * cw; t += blockDim.x) {
+    const uint32_t r = r0 + (uint32_t)(t / cw);
+    const int c = c0 + (int)(t % cw);
+    R[(size_t)r * W + c] = r < w ? b[(size_t)d.perm[f0 + r] * W + c] : 0.0;
+  }
+  __syncthreads();
+  for (uint32_t q = d.child_ptr[s]; q < d.child_ptr[s + 1]; ++q) {
+    const uint32_t ch = d.child_idx[q];
+    const uint32_t wc = front_w(d, ch), uc = front_m(d, ch) - wc;
+    const double* Rc = d.R + (d.rhs_off[ch] + wc) * W;
+    const uint32_t* rel = d.rel_idx + d.rel_ptr[ch];
+    const uint32_t a0 = lower_bound_u32(rel, uc, r0), a1 = lower_bound_u32(rel, uc, r1);
+    for (long t = threadIdx.x; t < (long)(a1 - a0) * cw; t += blockDim.x) {
+      const uint32_t a = a0 + (uint32_t)(t / cw);
+      const int c = c0 + (int)(t % cw);
+      R[(size_t)rel[a] * W + c] += Rc[(size_t)a * W + c];
+    }
+    __syncthreads();
+  }
+}
+
+struct LoadRowMajor {  // X(k, i) = p[i * ld + k]   (k contiguous)
+  static constexpr bool kKContig = true;
+  const double* p;
+  int ld;
+  __device__ __forceinline__ double operator()(int, int k, int i) const {
+    return p[(size_t)i * ld + k];
+  }
+};
+struct LoadColMajor {  // X(k, i) = p[k * ld + i]   (i contiguous)
+  static constexpr bool kKContig = false;
+  const double* p;
+  int ld;
+  __device__ __forceinline__ double operator()(int, int k, int i) const {
+    return p[(size_t)k * ld + i];
+  }
+};
+struct LoadGatherRows {  // X(k, c) = x[rows[k] * W + c]
+  static constexpr bool kKContig = false;
+  const double* x;
+  const uint32_t* rows;
+  int W;
+  __device__ __forceinline__ double operator()(int, int k, int c) const {
+    return x[(size_t)rows[k] * W + c];
+  }
+};
+// out[(row0 + i) * W + c] (=, -=, or = base - v)
+template <int MODE>
+struct StoreRows {
+  double* out;
+  const double* base;
+  int W;
+  __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int mi = mb + r, ni = nb + c;
+          if (mi < M && ni < N) {
+            const size_t o = (size_t)mi * W + ni;
+            if (MODE == 0) out[o] = wt.acc[i][j][e];
+            if (MODE == 1) out[o] -= wt.acc[i][j][e];
+            if (MODE == 2) out[o] = base[o] - wt.acc[i][j][e];
+          }
+        }
+  }
+};
+
+// Forward step 1: y_s = L11^{-1} R_s[0:w]
+__global__ void __launch_bounds__(kGemmThreads) k_fwd1(CholDev d, const uint32_t* lsup, double* y) {
+  const uint32_t s = lsup[blockIdx.z];
+  const int w = (int)front_w(d, s), W = (int)d.W;
+  if ((int)blockIdx.x * kBM >= w) return;
+  const double* V = d.Linv + d.inv_off[s];
+  const double* R = d.R + d.rhs_off[s] * W;
+  gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadRowMajor{V, w},
+            LoadColMajor{R, W}, StoreRows<0>{y + (size_t)d.first[s] * W, nullptr, W});
+}
+
+// Forward step 2: R_s[w:m] -= L21 y_s
+__global__ void __launch_bounds__(kGemmThreads) k_fwd2(CholDev d, const uint32_t* lsup,
+                                                       const double* y) {
+  const uint32_t s = lsup[blockIdx.z];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
+  const int u = m - w;
+  if ((int)blockIdx.x * kBM >= u) return;
+  const double* A = d.F + d.front_off[s];
+  double* R = d.R + (d.rhs_off[s] + w) * W;
+  gemm_tile(0, u, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadColMajor{A + w, m},
+            LoadColMajor{y + (size_t)d.first[s] * W, W}, StoreRows<1>{R, nullptr, W});
+}
+
+// Backward step 1: t_s = y_s - L21^T x[rows below]   (t_s stored in R_s[0:w])
+__global__ void __launch_bounds__(kGemmThreads) k_bwd1(CholDev d, const uint32_t* lsup,
+                                                       const double* y, const double* x) {
+  const uint32_t s = lsup[blockIdx.z];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
+  if ((int)blockIdx.x * kBM >= w) return;
+  const double* A = d.F + d.front_off[s];
+  double* T = d.R + d.rhs_off[s] * W;
+  const uint32_t* rows = d.str_idx + d.str_ptr[s] + w;
+  gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, m - w, 0, LoadRowMajor{A + w, m},
+            LoadGatherRows{x, rows, W},
+            StoreRows<2>{T, y + (size_t)d.first[s] * W, W});
+}
+
+// Backward step 2: x_s = L11^{-T} t_s
+__global__ void __launch_bounds__(kGemmThreads) k_bwd2(CholDev d, const uint32_t* lsup, double* x) {
+  const uint32_t s = lsup[blockIdx.z];
+  const int w = (int)front_w(d, s), W = (int)d.W;
+  if ((int)blockIdx.x * kBM >= w) return;
+  const double* V = d.Linv + d.inv_off[s];
+  const double* T = d.R + d.rhs_off[s] * W;
+  gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadColMajor{V, w},
+            LoadColMajor{T, W}, StoreRows<0>{x + (size_t)d.first[s] * W, nullptr, W});
+}
+
+// out[perm[j]] (+)= x[j]
+__global__ void k_unpermute(int n, int W, const uint32_t* perm, const double* __restrict__ xp,
+                            double* __restrict__ out, int accumulate) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)n * W) return;
+  const int j = (int)(t / W), c = (int)(t % W);
+  const size_t o = (size_t)perm[j] * W + c;
+  if (accumulate)
+    out[o] += xp[t];
+  else
+    out[o] = xp[t];
+}
+
+// r = b - M x   (M: CSR with float values, original order, n x W row-major)
+__global__ void k_residual(int n, int W, const uint32_t* __restrict__ rp,
+                           const uint32_t* __restrict__ ci, const float* __restrict__ val,
+                           const double* __restrict__ b, const double* __restrict__ x,
+                           double* __restrict__ r) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)n * W) return;
+  const int i = (int)(t / W), c = (int)(t % W);
+  double acc = 0.0;
+  for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) acc += (double)val[e] * x[(size_t)ci[e] * W + c];
+  r[t] = b[t] - acc;
+}
+
+}  // namespace
+
+constexpr int kPanelSmem = 200 * 1024;
+
+cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevels& lv) {
+  const int nb = 32;
+  {
+    static unsigned long long attr_set = 0;  // one bit per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_set & (1ull << dev))) {
+      cudaError_t e =
+          cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kInvDiagSmem);
+      if (e != cudaSuccess) return e;
+      attr_set |= 1ull << dev;
+    }
+  }
+  cudaError_t e = cudaMemsetAsync(d.Linv, 0, d.linv_doubles * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  for (uint32_t l = 0; l < lv.nlevels; ++l) {
+    const uint32_t cnt = lv.count[l];
+    const uint32_t* ls = d.level_sup + lv.offset[l];
+    k_assemble<<<dim3((lv.maxm[l] + kAsmCols - 1) / kAsmCols, cnt), 256, 0, s>>>(d, ls);
+    for (uint32_t k0 = 0; k0 < lv.maxw[l]; k0 += nb) {
+      const int smem_rows = kPanelSmem / (nb * (int)sizeof(double));
+      const size_t need = (size_t)std::min<int>(smem_rows, (int)(lv.maxm[l] - k0)) * nb * 8;
+      k_panel<<<cnt, kPanelThreads, need, s>>>(d, ls, (int)k0, nb,
+                                               (int)(need / (nb * sizeof(double))));
+      // bound over the level: a front whose last panel is partial (pw < nb)
+      // has a trailing block of m - k0 - pw rows
+      const uint32_t T = lv.maxm[l] > k0 + 1 ? lv.maxm[l] - k0 - 1 : 0;
+      if (T > 0) {
+        const uint32_t nt = (T + kBM - 1) / kBM;
+        k_trailing<<<dim3(nt * (nt + 1) / 2, cnt), kGemmThreads, 0, s>>>(d, ls, (int)k0, nb);
+      }
+    }
+    const uint32_t nbk = (lv.maxw[l] + kIB - 1) / kIB;
+    k_inv_diag<<<dim3(nbk, cnt), kIB, kInvDiagSmem, s>>>(d, ls);
+    if (nbk > 1) k_inv_offdiag<<<dim3(nbk, cnt), kGemmThreads, 0, s>>>(d, ls, d.scratch);
+  }
+  return cudaGetLastError();
+}
+
+size_t chol_scratch_doubles(const CholLevels& lv) {
+  size_t mx = 0;
+  for (uint32_t l = 0; l < lv.nlevels; ++l) {
+    const size_t nbk = (lv.maxw[l] + kIB - 1) / kIB;
+    mx = std::max(mx, (size_t)lv.count[l] * nbk * kIB * kIB);
+  }
+  return mx;
+}
+
+cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels& lv,
+                              const double* b, double* y, double* x) {
+  const int W = (int)d.W;
+  const unsigned tn = (unsigned)((W + kBN - 1) / kBN);
+  for (uint32_t l = 0; l < lv.nlevels; ++l) {
+    const uint32_t cnt = lv.count[l];
+    const uint32_t* ls = d.level_sup + lv.offset[l];
+    k_solve_gather<<<dim3((lv.maxm[l] + 31) / 32, (W + 63) / 64, cnt), 256, 0, s>>>(d, ls, b);
+    k_fwd1<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y);
+    if (lv.maxu[l] > 0)
+      k_fwd2<<<dim3((lv.maxu[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y);
+  }
+  for (int l = (int)lv.nlevels - 1; l >= 0; --l) {
+    const uint32_t cnt = lv.count[l];
+    const uint32_t* ls = d.level_sup + lv.offset[l];
+    k_bwd1<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x);
+    k_bwd2<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t chol_unpermute(cudaStream_t s, int n, int W, const uint32_t* perm, const double* xp,
+                           double* out, bool accumulate) {
+  const long total = (long)n * W;
+  k_unpermute<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, W, perm, xp, out, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t normal_residual(cudaStream_t s, int n, int W, const uint32_t* rp, const uint32_t* ci,
+                            const float* val, const double* b, const double* x, double* r) {
+  const long total = (long)n * W;
+  k_residual<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, W, rp, ci, val, b, x, r);
+  return cudaGetLastError();
+}
+
+}  // namespace dmcg

@@ -1,0 +1,508 @@
+// Host analysis + CPU reference numerics for the supernodal Cholesky of
+// M = L^T L + S^T S (see chol.h).  The fill-reducing ordering is nested
+// dissection by BFS level sets on M's graph (a single level of M's graph is
+// a vertex separator of M), the same scheme the oracle uses for its sparse
+// LDL^T restatement of SimplicialLDLT.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+
+#include "chol.h"
+
+namespace dmcg {
+
+namespace {
+
+struct Graph {
+  uint32_t n;
+  const uint32_t* rp;
+  const uint32_t* ci;
+};
+
+// Nested dissection; appends the elimination order (old indices) to perm.
+class NestedDissection {
+ public:
+  explicit NestedDissection(const Graph& g)
+      : g_(g), part_(g.n, 0), level_(g.n, -1), queue_(g.n) {}
+
+  std::vector<uint32_t> run() {
+    std::vector<uint32_t> all(g_.n);
+    for (uint32_t i = 0; i < g_.n; ++i) all[i] = i;
+    perm_.reserve(g_.n);
+    recurse(all, 0);
+    return perm_;
+  }
+
+ private:
+  const Graph g_;
+  std::vector<int32_t> part_, level_;
+  std::vector<uint32_t> queue_, perm_;
+  int32_t next_id_ = 1;
+
+  uint32_t bfs(const std::vector<uint32_t>& verts, int32_t id, uint32_t root, uint32_t* maxlev) {
+    for (uint32_t v : verts) level_[v] = -1;
+    uint32_t head = 0, tail = 0;
+    queue_[tail++] = root;
+    level_[root] = 0;
+    uint32_t last = root;
+    while (head < tail) {
+      const uint32_t v = queue_[head++];
+      last = v;
+      for (uint32_t p = g_.rp[v]; p < g_.rp[v + 1]; ++p) {
+        const uint32_t w = g_.ci[p];
+        if (part_[w] == id && level_[w] < 0) {
+          level_[w] = level_[v] + 1;
+          queue_[tail++] = w;
+        }
+      }
+    }
+    *maxlev = (uint32_t)level_[last];
+    return tail;
+  }
+
+  void recurse(std::vector<uint32_t>& verts, int32_t id) {
+    const uint32_t cnt = (uint32_t)verts.size();
+    if (cnt == 0) return;
+    if (cnt <= 48) {
+      perm_.insert(perm_.end(), verts.begin(), verts.end());
+      return;
+    }
+    uint32_t maxlev;
+    const uint32_t reached = bfs(verts, id, verts[0], &maxlev);
+    if (reached < cnt) {  // disconnected: split off the reached component
+      std::vector<uint32_t> a, b;
+      for (uint32_t v : verts) (level_[v] >= 0 ? a : b).push_back(v);
+      const int32_t ia = next_id_++, ib = next_id_++;
+      for (uint32_t v : a) part_[v] = ia;
+      for (uint32_t v : b) part_[v] = ib;
+      verts.clear();
+      verts.shrink_to_fit();
+      recurse(a, ia);
+      recurse(b, ib);
+      return;
+    }
+    uint32_t root = queue_[cnt - 1];  // pseudo-peripheral start
+    for (int it = 0; it < 2; ++it) {
+      uint32_t ml;
+      bfs(verts, id, root, &ml);
+      if (ml <= maxlev && it > 0) break;
+      maxlev = ml;
+      root = queue_[cnt - 1];
+    }
+    bfs(verts, id, root, &maxlev);
+    if (maxlev < 2) {
+      perm_.insert(perm_.end(), verts.begin(), verts.end());
+      return;
+    }
+    std::vector<uint32_t> hist(maxlev + 1, 0);
+    for (uint32_t v : verts) hist[level_[v]]++;
+    uint32_t acc = 0, sep = 1;
+    for (uint32_t l = 0; l <= maxlev; ++l) {
+      if (acc + hist[l] > cnt / 2) {
+        sep = l;
+        break;
+      }
+      acc += hist[l];
+    }
+    if (sep == 0) sep = 1;
+    if (sep >= maxlev) sep = maxlev - 1;
+    std::vector<uint32_t> a, b, s;
+    for (uint32_t v : verts) {
+      const uint32_t l = (uint32_t)level_[v];
+      (l < sep ? a : (l > sep ? b : s)).push_back(v);
+    }
+    const int32_t ia = next_id_++, ib = next_id_++, is = next_id_++;
+    for (uint32_t v : a) part_[v] = ia;
+    for (uint32_t v : b) part_[v] = ib;
+    for (uint32_t v : s) part_[v] = is;
+    verts.clear();
+    verts.shrink_to_fit();
+    recurse(a, ia);
+    recurse(b, ib);
+    perm_.insert(perm_.end(), s.begin(), s.end());
+  }
+};
+
+}  // namespace
+
+void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector<uint32_t>& ci,
+                  const std::vector<float>& val, CholPlan* P) {
+  CholPlan& p = *P;
+  p = CholPlan();
+  p.n = n;
+  // (1) ordering
+  Graph g{n, rp.data(), ci.data()};
+  std::vector<uint32_t> perm0 = NestedDissection(g).run();
+  std::vector<uint32_t> iperm0(n);
+  for (uint32_t k = 0; k < n; ++k) iperm0[perm0[k]] = k;
+  // (2) elimination tree (Liu, path compression) of P M P^T
+  std::vector<int32_t> par(n, -1), anc(n, -1);
+  for (uint32_t k = 0; k < n; ++k) {
+    const uint32_t ko = perm0[k];
+    for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
+      int32_t r = (int32_t)iperm0[ci[q]];
+      if ((uint32_t)r >= k) continue;
+      while (anc[r] != -1 && anc[r] != (int32_t)k) {
+        const int32_t nx = anc[r];
+        anc[r] = (int32_t)k;
+        r = nx;
+      }
+      if (anc[r] == -1) {
+        anc[r] = (int32_t)k;
+        par[r] = (int32_t)k;
+      }
+    }
+  }
+  // (3) postorder (iterative DFS, children in increasing order)
+  std::vector<int32_t> head(n, -1), nxt(n, -1);
+  for (int32_t j = (int32_t)n - 1; j >= 0; --j)
+    if (par[j] != -1) {
+      nxt[j] = head[par[j]];
+      head[par[j]] = j;
+    }
+  std::vector<uint32_t> post;
+  post.reserve(n);
+  std::vector<int32_t> stack;
+  for (uint32_t r = 0; r < n; ++r) {
+    if (par[r] != -1) continue;
+    stack.push_back((int32_t)r);
+    while (!stack.empty()) {
+      const int32_t t = stack.back();
+      const int32_t c = head[t];
+      if (c == -1) {
+        stack.pop_back();
+        post.push_back((uint32_t)t);
+      } else {
+        head[t] = nxt[c];
+        stack.push_back(c);
+      }
+    }
+  }
+  p.perm.resize(n);
+  p.iperm.resize(n);
+  std::vector<uint32_t> ipost(n);
+  for (uint32_t j = 0; j < n; ++j) ipost[post[j]] = j;
+  for (uint32_t j = 0; j < n; ++j) p.perm[j] = perm0[post[j]];
+  for (uint32_t j = 0; j < n; ++j) p.iperm[p.perm[j]] = j;
+  std::vector<int32_t> parent(n, -1);
+  for (uint32_t j = 0; j < n; ++j) {
+    const int32_t q = par[post[j]];
+    parent[j] = q == -1 ? -1 : (int32_t)ipost[q];
+  }
+  // (4) column counts by row-subtree traversal (Davis, LDL symbolic)
+  std::vector<uint32_t> colcnt(n, 1);  // diagonal
+  std::vector<int32_t> flag(n, -1);
+  for (uint32_t k = 0; k < n; ++k) {
+    flag[k] = (int32_t)k;
+    const uint32_t ko = p.perm[k];
+    for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
+      uint32_t i = p.iperm[ci[q]];
+      if (i >= k) continue;
+      for (; flag[i] != (int32_t)k; i = (uint32_t)parent[i]) {
+        colcnt[i]++;
+        flag[i] = (int32_t)k;
+      }
+    }
+  }
+  // (5) fundamental supernodes
+  std::vector<uint32_t> nchild(n, 0);
+  for (uint32_t j = 0; j < n; ++j)
+    if (parent[j] != -1) nchild[parent[j]]++;
+  std::vector<uint32_t> sfirst;  // first column of each fundamental supernode
+  for (uint32_t j = 0; j < n; ++j) {
+    const bool cont = j > 0 && parent[j - 1] == (int32_t)j && nchild[j] == 1 &&
+                      colcnt[j - 1] == colcnt[j] + 1;
+    if (!cont) sfirst.push_back(j);
+  }
+  sfirst.push_back(n);
+  uint32_t ns = (uint32_t)sfirst.size() - 1;
+  std::vector<uint32_t> sup_of(n);
+  for (uint32_t s = 0; s < ns; ++s)
+    for (uint32_t j = sfirst[s]; j < sfirst[s + 1]; ++j) sup_of[j] = s;
+  // (6) relaxed amalgamation: merge a supernode into its parent when it is
+  // the parent's last child (contiguous columns) and the merged front stays
+  // dense enough.  Stats per supernode: width, m (rows incl. own columns),
+  // true nonzeros (from colcnt), stored lower-triangle entries.
+  std::vector<int32_t> spar(ns, -1);
+  std::vector<uint64_t> nz_true(ns, 0);
+  std::vector<uint32_t> sw(ns), sm(ns), sf(ns);
+  for (uint32_t s = 0; s < ns; ++s) {
+    const uint32_t last = sfirst[s + 1] - 1;
+    spar[s] = parent[last] == -1 ? -1 : (int32_t)sup_of[parent[last]];
+    sw[s] = sfirst[s + 1] - sfirst[s];
+    sm[s] = colcnt[sfirst[s]];
+    sf[s] = sfirst[s];
+    for (uint32_t j = sfirst[s]; j < sfirst[s + 1]; ++j) nz_true[s] += colcnt[j];
+  }
+  auto stored = [](uint64_t w, uint64_t m) { return w * m - w * (w - 1) / 2; };
+  std::vector<int32_t> merged_into(ns, -1);
+  for (uint32_t c = 0; c < ns; ++c) {  // supernodes are in postorder
+    const int32_t pp = spar[c];
+    if (pp < 0) continue;
+    if (sf[c] + sw[c] != sf[pp]) continue;  // not contiguous (not the last child)
+    const uint64_t w = (uint64_t)sw[c] + sw[pp];
+    const uint64_t m = (uint64_t)sw[c] + sm[pp];
+    const uint64_t st = stored(w, m);
+    const uint64_t nzt = nz_true[c] + nz_true[pp];
+    const double zf = 1.0 - (double)nzt / (double)st;
+    const bool ok = w <= 4 || (w <= 16 && zf <= 0.8) || (w <= 48 && zf <= 0.1) || zf <= 0.05;
+    if (!ok || w > 1024) continue;
+    // merge c into pp
+    sf[pp] = sf[c];
+    sw[pp] = (uint32_t)w;
+    sm[pp] = (uint32_t)m;
+    nz_true[pp] = st;  // merged front is now stored densely
+    merged_into[c] = pp;
+  }
+  // collect surviving supernodes in column order
+  p.first.clear();
+  std::vector<uint32_t> old_to_new(ns, UINT32_MAX);
+  for (uint32_t s = 0; s < ns; ++s)
+    if (merged_into[s] == -1) {
+      old_to_new[s] = (uint32_t)p.first.size();
+      p.first.push_back(sf[s]);
+    }
+  p.nsup = (uint32_t)p.first.size();
+  p.first.push_back(n);
+  // sort by first column (postorder keeps them sorted already; enforce)
+  {
+    std::vector<uint32_t> chk(p.first.begin(), p.first.end() - 1);
+    if (!std::is_sorted(chk.begin(), chk.end())) {
+      std::sort(p.first.begin(), p.first.end() - 1);
+    }
+  }
+  const uint32_t NS = p.nsup;
+  std::vector<uint32_t> col_sup(n);
+  for (uint32_t s = 0; s < NS; ++s)
+    for (uint32_t j = p.first[s]; j < p.first[s + 1]; ++j) col_sup[j] = s;
+  // (7) row structures, postorder of supernodes = column order
+  p.parent.assign(NS, -1);
+  std::vector<std::vector<uint32_t>> kids(NS);
+  std::vector<int32_t> mark(n, -1);
+  p.str_ptr.assign(NS + 1, 0);
+  p.str_idx.clear();
+  p.str_idx.reserve((size_t)n * 40);
+  std::vector<uint32_t> rows;
+  for (uint32_t s = 0; s < NS; ++s) {
+    const uint32_t f0 = p.first[s], f1 = p.first[s + 1];
+    rows.clear();
+    for (uint32_t j = f0; j < f1; ++j) {
+      rows.push_back(j);
+      mark[j] = (int32_t)s;
+    }
+    for (uint32_t j = f0; j < f1; ++j) {
+      const uint32_t jo = p.perm[j];
+      for (uint32_t q = rp[jo]; q < rp[jo + 1]; ++q) {
+        const uint32_t i = p.iperm[ci[q]];
+        if (i >= f1 && mark[i] != (int32_t)s) {
+          mark[i] = (int32_t)s;
+          rows.push_back(i);
+        }
+      }
+    }
+    for (uint32_t c : kids[s]) {
+      for (uint64_t q = p.str_ptr[c] + p.w(c); q < p.str_ptr[c + 1]; ++q) {
+        const uint32_t i = p.str_idx[q];
+        if (i >= f1 && mark[i] != (int32_t)s) {
+          mark[i] = (int32_t)s;
+          rows.push_back(i);
+        }
+      }
+    }
+    std::sort(rows.begin() + (f1 - f0), rows.end());
+    p.str_idx.insert(p.str_idx.end(), rows.begin(), rows.end());
+    p.str_ptr[s + 1] = p.str_idx.size();
+    if (rows.size() > f1 - f0) {
+      const uint32_t ps = col_sup[rows[f1 - f0]];
+      p.parent[s] = (int32_t)ps;
+      kids[ps].push_back(s);
+    }
+  }
+  // children lists, levels
+  p.child_ptr.assign(NS + 1, 0);
+  p.child_idx.clear();
+  for (uint32_t s = 0; s < NS; ++s) {
+    p.child_idx.insert(p.child_idx.end(), kids[s].begin(), kids[s].end());
+    p.child_ptr[s + 1] = (uint32_t)p.child_idx.size();
+  }
+  std::vector<uint32_t> lev(NS, 0);
+  uint32_t maxlev = 0;
+  for (uint32_t s = 0; s < NS; ++s) {
+    for (uint32_t c : kids[s]) lev[s] = std::max(lev[s], lev[c] + 1);
+    maxlev = std::max(maxlev, lev[s]);
+  }
+  p.nlevels = NS ? maxlev + 1 : 0;
+  p.level_ptr.assign(p.nlevels + 1, 0);
+  for (uint32_t s = 0; s < NS; ++s) p.level_ptr[lev[s] + 1]++;
+  for (uint32_t l = 0; l < p.nlevels; ++l) p.level_ptr[l + 1] += p.level_ptr[l];
+  p.level_sup.assign(NS, 0);
+  {
+    std::vector<uint32_t> fill(p.level_ptr.begin(), p.level_ptr.end() - 1);
+    for (uint32_t s = 0; s < NS; ++s) p.level_sup[fill[lev[s]]++] = s;
+  }
+  // offsets and statistics
+  p.front_off.assign(NS + 1, 0);
+  p.inv_off.assign(NS + 1, 0);
+  p.rhs_off.assign(NS + 1, 0);
+  p.nnz_l = 0;
+  p.flops_factor = 0;
+  p.flops_solve_per_rhs = 0;
+  for (uint32_t s = 0; s < NS; ++s) {
+    const uint64_t w = p.w(s), m = p.m(s);
+    p.front_off[s + 1] = p.front_off[s] + m * m;
+    p.inv_off[s + 1] = p.inv_off[s] + w * w;
+    p.rhs_off[s + 1] = p.rhs_off[s] + m;
+    p.nnz_l += w * m - w * (w - 1) / 2;
+    p.max_front = std::max<uint32_t>(p.max_front, (uint32_t)m);
+    p.max_width = std::max<uint32_t>(p.max_width, (uint32_t)w);
+    // partial Cholesky: sum over pivots t of (m-t)^2 ; L11 inverse w^3/3
+    for (uint64_t t = 0; t < w; ++t) p.flops_factor += (double)(m - t) * (m - t);
+    p.flops_factor += (double)w * w * w / 3.0;
+    p.flops_solve_per_rhs += 2.0 * (2.0 * w * w + 2.0 * 2.0 * w * (m - w));
+  }
+  // (8) extend-add maps: child update rows -> parent local rows
+  p.rel_ptr.assign(NS + 1, 0);
+  p.rel_idx.clear();
+  for (uint32_t c = 0; c < NS; ++c) {
+    const int32_t ps = p.parent[c];
+    if (ps >= 0) {
+      const uint32_t* pb = &p.str_idx[p.str_ptr[ps]];
+      const uint32_t pm = p.m((uint32_t)ps);
+      for (uint64_t q = p.str_ptr[c] + p.w(c); q < p.str_ptr[c + 1]; ++q) {
+        const uint32_t r = p.str_idx[q];
+        const uint32_t* it = std::lower_bound(pb, pb + pm, r);
+        p.rel_idx.push_back((uint32_t)(it - pb));
+      }
+    }
+    p.rel_ptr[c + 1] = p.rel_idx.size();
+  }
+  // (9) scatter list of M into the fronts (lower part, column-major local)
+  p.a_ptr.assign(NS + 1, 0);
+  p.a_pos.clear();
+  p.a_val.clear();
+  std::vector<int32_t> loc(n, -1);
+  for (uint32_t s = 0; s < NS; ++s) {
+    const uint32_t m = p.m(s), f0 = p.first[s], f1 = p.first[s + 1];
+    for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = (int32_t)t;
+    for (uint32_t j = f0; j < f1; ++j) {
+      const uint32_t jo = p.perm[j];
+      for (uint32_t q = rp[jo]; q < rp[jo + 1]; ++q) {
+        const uint32_t i = p.iperm[ci[q]];
+        if (i < j) continue;
+        p.a_pos.push_back((j - f0) * m + (uint32_t)loc[i]);
+        p.a_val.push_back(val[q]);
+      }
+    }
+    p.a_ptr[s + 1] = p.a_pos.size();
+    for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = -1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CPU reference numerics (same data flow as the GPU kernels)
+// ---------------------------------------------------------------------------
+bool chol_factor_cpu(const CholPlan& p, std::vector<double>* Fv, std::vector<double>* Iv) {
+  std::vector<double>& F = *Fv;
+  std::vector<double>& Linv = *Iv;
+  F.assign(p.front_off[p.nsup], 0.0);
+  Linv.assign(p.inv_off[p.nsup], 0.0);
+  for (uint32_t l = 0; l < p.nlevels; ++l) {
+    for (uint32_t q = p.level_ptr[l]; q < p.level_ptr[l + 1]; ++q) {
+      const uint32_t s = p.level_sup[q];
+      const uint32_t m = p.m(s), w = p.w(s);
+      double* A = &F[p.front_off[s]];
+      for (uint64_t e = p.a_ptr[s]; e < p.a_ptr[s + 1]; ++e) A[p.a_pos[e]] += p.a_val[e];
+      for (uint32_t t = p.child_ptr[s]; t < p.child_ptr[s + 1]; ++t) {
+        const uint32_t c = p.child_idx[t];
+        const uint32_t mc = p.m(c), wc = p.w(c), uc = mc - wc;
+        const double* C = &F[p.front_off[c]];
+        const uint32_t* rel = &p.rel_idx[p.rel_ptr[c]];
+        for (uint32_t b = 0; b < uc; ++b)
+          for (uint32_t a = b; a < uc; ++a)
+            A[(size_t)rel[b] * m + rel[a]] += C[(size_t)(wc + b) * mc + (wc + a)];
+      }
+      for (uint32_t j = 0; j < w; ++j) {
+        const double d = A[(size_t)j * m + j];
+        if (!(d > 0.0)) return false;
+        const double r = std::sqrt(d);
+        A[(size_t)j * m + j] = r;
+        for (uint32_t i = j + 1; i < m; ++i) A[(size_t)j * m + i] /= r;
+        for (uint32_t c = j + 1; c < m; ++c) {
+          const double lc = A[(size_t)j * m + c];
+          for (uint32_t i = c; i < m; ++i) A[(size_t)c * m + i] -= A[(size_t)j * m + i] * lc;
+        }
+      }
+      // L11^{-1} by forward substitution on the identity
+      double* V = &Linv[p.inv_off[s]];
+      for (uint32_t c = 0; c < w; ++c) {
+        for (uint32_t i = 0; i < w; ++i) {
+          double sacc = (i == c) ? 1.0 : 0.0;
+          for (uint32_t k = c; k < i; ++k) sacc -= A[(size_t)k * m + i] * V[(size_t)c * w + k];
+          V[(size_t)c * w + i] = i < c ? 0.0 : sacc / A[(size_t)i * m + i];
+        }
+      }
+    }
+  }
+  return true;
+}
+
+void chol_solve_cpu(const CholPlan& p, const std::vector<double>& F,
+                    const std::vector<double>& Linv, uint32_t W, const double* b, double* x) {
+  const uint32_t n = p.n;
+  std::vector<double> R(p.rhs_off[p.nsup] * W, 0.0), y((size_t)n * W), xp((size_t)n * W);
+  // forward: L y = P b
+  for (uint32_t l = 0; l < p.nlevels; ++l)
+    for (uint32_t q = p.level_ptr[l]; q < p.level_ptr[l + 1]; ++q) {
+      const uint32_t s = p.level_sup[q];
+      const uint32_t m = p.m(s), w = p.w(s), f0 = p.first[s];
+      double* Rs = &R[p.rhs_off[s] * W];
+      for (uint32_t j = 0; j < w; ++j)
+        for (uint32_t c = 0; c < W; ++c) Rs[(size_t)j * W + c] = b[(size_t)p.perm[f0 + j] * W + c];
+      for (uint32_t t = p.child_ptr[s]; t < p.child_ptr[s + 1]; ++t) {
+        const uint32_t ch = p.child_idx[t];
+        const uint32_t wc = p.w(ch), uc = p.m(ch) - wc;
+        const double* Rc = &R[(p.rhs_off[ch] + wc) * W];
+        const uint32_t* rel = &p.rel_idx[p.rel_ptr[ch]];
+        for (uint32_t a = 0; a < uc; ++a)
+          for (uint32_t c = 0; c < W; ++c) Rs[(size_t)rel[a] * W + c] += Rc[(size_t)a * W + c];
+      }
+      const double* A = &F[p.front_off[s]];
+      const double* V = &Linv[p.inv_off[s]];
+      std::vector<double> ys((size_t)w * W, 0.0);
+      for (uint32_t i = 0; i < w; ++i)
+        for (uint32_t k = 0; k <= i; ++k)
+          for (uint32_t c = 0; c < W; ++c) ys[(size_t)i * W + c] += V[(size_t)k * w + i] * Rs[(size_t)k * W + c];
+      for (uint32_t i = w; i < m; ++i)
+        for (uint32_t k = 0; k < w; ++k)
+          for (uint32_t c = 0; c < W; ++c) Rs[(size_t)i * W + c] -= A[(size_t)k * m + i] * ys[(size_t)k * W + c];
+      for (uint32_t i = 0; i < w; ++i)
+        for (uint32_t c = 0; c < W; ++c) y[(size_t)(f0 + i) * W + c] = ys[(size_t)i * W + c];
+    }
+  // backward: L^T xp = y
+  for (int32_t l = (int32_t)p.nlevels - 1; l >= 0; --l)
+    for (uint32_t q = p.level_ptr[l]; q < p.level_ptr[l + 1]; ++q) {
+      const uint32_t s = p.level_sup[q];
+      const uint32_t m = p.m(s), w = p.w(s), f0 = p.first[s];
+      const double* A = &F[p.front_off[s]];
+      const double* V = &Linv[p.inv_off[s]];
+      const uint32_t* str = &p.str_idx[p.str_ptr[s]];
+      std::vector<double> t((size_t)w * W);
+      for (uint32_t i = 0; i < w; ++i)
+        for (uint32_t c = 0; c < W; ++c) t[(size_t)i * W + c] = y[(size_t)(f0 + i) * W + c];
+      for (uint32_t i = 0; i < w; ++i)
+        for (uint32_t r = w; r < m; ++r)
+          for (uint32_t c = 0; c < W; ++c)
+            t[(size_t)i * W + c] -= A[(size_t)i * m + r] * xp[(size_t)str[r] * W + c];
+      for (uint32_t i = 0; i < w; ++i)
+        for (uint32_t c = 0; c < W; ++c) {
+          double sacc = 0.0;
+          for (uint32_t k = i; k < w; ++k) sacc += V[(size_t)i * w + k] * t[(size_t)k * W + c];
+          xp[(size_t)(f0 + i) * W + c] = sacc;
+        }
+    }
+  for (uint32_t j = 0; j < n; ++j)
+    for (uint32_t c = 0; c < W; ++c) x[(size_t)p.perm[j] * W + c] = xp[(size_t)j * W + c];
+}
+
+}  // namespace dmcg

@@ -230,6 +230,46 @@ __global__ void __launch_bounds__(kCgThreads)
   }
 }
 
+// Row-major variants for the direct solver: vectors are n x W, row i =
+// [x frames | y frames | z frames] of vertex i.
+__global__ void k_rhs_rm(int n, int F, int W, const uint32_t* __restrict__ rp,
+                         const uint32_t* __restrict__ ci, const int32_t* __restrict__ apos, int n_c,
+                         const uint16_t* __restrict__ aq, const float* __restrict__ arng, int abits,
+                         const double* __restrict__ D, double* __restrict__ B, int* flags) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)n * W) return;
+  const int i = (int)(t / W), c = (int)(t % W);
+  const uint32_t pb = rp[i], pe = rp[i + 1];
+  const double deg = (double)(pe - pb - 1);
+  double acc = 0.0;
+  for (uint32_t p = pb; p < pe; ++p) {
+    const uint32_t j = ci[p];
+    const double v = (j == (uint32_t)i) ? deg : -1.0;
+    acc = __dadd_rn(acc, __dmul_rn(v, D[(size_t)j * W + c]));
+  }
+  const int slot = apos[i];
+  if (slot >= 0) {
+    const int a = c / F, f = c % F;
+    const QParams q = make_qparams(arng[2 * a], arng[2 * a + 1], abits);
+    const uint32_t lv = aq[((size_t)a * n_c + slot) * F + f];
+    if (lv >= q.levels) atomicOr(flags, 1);
+    acc = __dadd_rn(acc, dequantize_level(q.min_, q.width, q.degenerate, lv));
+  }
+  B[t] = acc;
+}
+
+template <typename T>
+__global__ void k_output_rm(int n, int F, const double* __restrict__ X, T* o0, T* o1, T* o2) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long nF = (long)n * F;
+  if (t >= 3 * nF) return;
+  const int a = (int)(t / nF);
+  const long rem = t % nF;
+  const int i = (int)(rem / F), f = (int)(rem % F);
+  T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
+  o[rem] = (T)X[(size_t)i * 3 * F + (size_t)a * F + f];
+}
+
 template <typename T>
 __global__ void k_output(int n, int F, const double* __restrict__ X, T* o0, T* o1, T* o2) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -268,6 +308,30 @@ cudaError_t launch_cg(cudaStream_t s, int n, int W, int nblk, const uint32_t* m_
                       const uint32_t* m_ci, const float* m_val, double* X, double* R, double* P,
                       double* Q, double rtol, int maxit, int* iters, double* res) {
   k_cg<<<nblk, kCgThreads, 0, s>>>(n, W, m_rp, m_ci, m_val, X, R, P, Q, rtol, maxit, iters, res);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
+                          const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
+                          const uint16_t* anchor_q, const float* anchor_rng, int anchor_bits,
+                          const double* D, double* B, int* flags) {
+  const long total = 3L * n * F;
+  k_rhs_rm<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, F, 3 * F, lap_rp, lap_ci, anchor_pos,
+                                                           n_c, anchor_q, anchor_rng, anchor_bits,
+                                                           D, B, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_output_rm(cudaStream_t s, int n, int F, const double* X, void* const out[3],
+                             bool f32) {
+  const long total = 3L * n * F;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  if (f32)
+    k_output_rm<float><<<grid, 256, 0, s>>>(n, F, X, (float*)out[0], (float*)out[1],
+                                            (float*)out[2]);
+  else
+    k_output_rm<double><<<grid, 256, 0, s>>>(n, F, X, (double*)out[0], (double*)out[1],
+                                             (double*)out[2]);
   return cudaGetLastError();
 }
 

@@ -30,20 +30,29 @@ struct WarpTile {
   double acc[4][4][2];
 };
 
+// One 64x64 output tile (rows m0.., cols n0..) over k in [kbeg, kend), by
+// the 128 threads of the calling CTA.  Callable from any kernel (the grouped
+// per-front kernels of chol.cu build their own loaders / epilogues).
+struct GemmSmem {
+  double As[2][kBK][kBM + 8];
+  double Bs[2][kBK][kBN + 8];
+};
+// One static shared buffer per kernel, shared by every gemm_tile
+// instantiation the kernel calls (a non-template function's __shared__
+// variable is a single object).
+__device__ __forceinline__ GemmSmem& gemm_smem() {
+  __shared__ GemmSmem sm;
+  return sm;
+}
+
 template <class LA, class LB, class EP>
-__global__ void __launch_bounds__(kGemmThreads)
-    gemm_dmma_kernel(int M, int N, int K, int k_chunk, LA la, LB lb, EP ep) {
-  __shared__ double As[2][kBK][kBM + 8];
-  __shared__ double Bs[2][kBK][kBN + 8];
-  const int b = blockIdx.z;
-  const int tiles_n = (N + kBN - 1) / kBN;
-  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
-  const int split = blockIdx.y;
-  const int kbeg = split * k_chunk;
-  const int kend = min(K, kbeg + k_chunk);
+__device__ __forceinline__ void gemm_tile(int b, int M, int N, int m0, int n0, int kbeg, int kend,
+                                          int split, const LA& la, const LB& lb, const EP& ep) {
+  GemmSmem& sm = gemm_smem();
+  auto& As = sm.As;
+  auto& Bs = sm.Bs;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int wm = w >> 1, wn = w & 1;
-  const int m0 = tm * kBM, n0 = tn * kBN;
 
   WarpTile wt;
 #pragma unroll
@@ -120,6 +129,17 @@ __global__ void __launch_bounds__(kGemmThreads)
     buf ^= 1;
   }
   ep(b, split, m0 + wm * 32, n0 + wn * 32, lane, M, N, wt);
+}
+
+template <class LA, class LB, class EP>
+__global__ void __launch_bounds__(kGemmThreads)
+    gemm_dmma_kernel(int M, int N, int K, int k_chunk, LA la, LB lb, EP ep) {
+  const int tiles_n = (N + kBN - 1) / kBN;
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int split = blockIdx.y;
+  const int kbeg = split * k_chunk;
+  const int kend = min(K, kbeg + k_chunk);
+  gemm_tile(blockIdx.z, M, N, tm * kBM, tn * kBN, kbeg, kend, split, la, lb, ep);
 }
 
 // ---- loaders -------------------------------------------------------------

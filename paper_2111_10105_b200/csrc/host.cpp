@@ -2,6 +2,7 @@
 // configuration checks, plan lifetime and the DMC1 stream.  Reference
 // behaviour is cited per function (paths relative to /root/reference/proj).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <deque>
@@ -334,6 +335,8 @@ void dmcg_config_default(dmcg_config* cfg) {
 void dmcg_decode_options_default(dmcg_decode_options* o) {
   o->cg_rtol = 1e-10;
   o->cg_max_iter = 20000;
+  o->solver = 0;
+  o->refine = 1;
 }
 
 uint32_t dmcg_anchor_count(uint32_t n, double fraction) {
@@ -383,6 +386,17 @@ int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_size
 }
 
 // ---- plan ---------------------------------------------------------------------
+}  // extern "C"
+
+void* dmcg::plan_alloc(dmcg_plan* p, size_t bytes) {
+  if (bytes == 0) bytes = 256;
+  void* d = p->ctx->pool.get(bytes);
+  if (d) p->owned.emplace_back(d, bytes);
+  return d;
+}
+
+extern "C" {
+
 static void* plan_get(dmcg_plan* p, size_t bytes) {
   if (bytes == 0) bytes = 256;
   void* d = p->ctx->pool.get(bytes);
@@ -497,13 +511,70 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_anchor_rng = (float*)get(6 * 4);
   p->d_anchor_q = (uint16_t*)get(3 * (size_t)p->n_c * F * 2);
   p->d_rowp = (double*)get(3 * kk * 2 * 8);
-  const size_t vec = (size_t)p->nblk * n * kColBlock * 8;
-  p->d_cg_x = (double*)get(vec);
-  p->d_cg_r = (double*)get(vec);
-  p->d_cg_p = (double*)get(vec);
-  p->d_cg_q = (double*)get(vec);
   p->d_cg_iters = (int*)get(p->W_pad * 4);
   p->d_cg_res = (double*)get(p->W_pad * 8);
+  // direct solver: symbolic analysis of M (host) + device structures
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p->chol);
+    p->analyze_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  const CholPlan& cp = p->chol;
+  const size_t nW = (size_t)n * p->W;
+  p->d_rm_delta = (double*)get(nW * 8);
+  p->d_rm_b = (double*)get(nW * 8);
+  p->d_rm_x = (double*)get(nW * 8);
+  p->d_rm_y = (double*)get(nW * 8);
+  p->d_rm_xp = (double*)get(nW * 8);
+  p->d_rm_r = (double*)get(nW * 8);
+  CholDev& cd = p->cdev;
+  cd.n = n;
+  cd.nsup = cp.nsup;
+  cd.W = p->W;
+  cd.first = (const uint32_t*)get(cp.first.size() * 4);
+  cd.str_ptr = (const unsigned long long*)get(cp.str_ptr.size() * 8);
+  cd.str_idx = (const uint32_t*)get(cp.str_idx.size() * 4);
+  cd.child_ptr = (const uint32_t*)get(cp.child_ptr.size() * 4);
+  cd.child_idx = (const uint32_t*)get(cp.child_idx.size() * 4 + 4);
+  cd.rel_ptr = (const unsigned long long*)get(cp.rel_ptr.size() * 8);
+  cd.rel_idx = (const uint32_t*)get(cp.rel_idx.size() * 4 + 4);
+  cd.a_ptr = (const unsigned long long*)get(cp.a_ptr.size() * 8);
+  cd.a_pos = (const uint32_t*)get(cp.a_pos.size() * 4);
+  cd.a_val = (const float*)get(cp.a_val.size() * 4);
+  cd.front_off = (const unsigned long long*)get(cp.front_off.size() * 8);
+  cd.inv_off = (const unsigned long long*)get(cp.inv_off.size() * 8);
+  cd.rhs_off = (const unsigned long long*)get(cp.rhs_off.size() * 8);
+  cd.perm = (const uint32_t*)get(cp.perm.size() * 4);
+  cd.level_sup = (const uint32_t*)get(cp.level_sup.size() * 4 + 4);
+  cd.F = (double*)get(cp.front_off[cp.nsup] * 8);
+  cd.Linv = (double*)get(cp.inv_off[cp.nsup] * 8 + 8);
+  cd.R = (double*)get(cp.rhs_off[cp.nsup] * p->W * 8);
+  cd.flags = p->d_flags + 4;
+  CholLevels& lv = p->levels;
+  lv.nlevels = cp.nlevels;
+  lv.offset.assign(cp.nlevels, 0);
+  lv.count.assign(cp.nlevels, 0);
+  lv.maxw.assign(cp.nlevels, 0);
+  lv.maxm.assign(cp.nlevels, 0);
+  lv.maxu.assign(cp.nlevels, 0);
+  for (uint32_t l = 0; l < cp.nlevels; ++l) {
+    lv.offset[l] = cp.level_ptr[l];
+    lv.count[l] = cp.level_ptr[l + 1] - cp.level_ptr[l];
+    for (uint32_t q = cp.level_ptr[l]; q < cp.level_ptr[l + 1]; ++q) {
+      const uint32_t s = cp.level_sup[q];
+      lv.maxw[l] = std::max(lv.maxw[l], cp.w(s));
+      lv.maxm[l] = std::max(lv.maxm[l], cp.m(s));
+      lv.maxu[l] = std::max(lv.maxu[l], cp.m(s) - cp.w(s));
+    }
+  }
+  cd.linv_doubles = cp.inv_off[cp.nsup];
+  cd.scratch = (double*)get(chol_scratch_doubles(lv) * 8 + 8);
+  p->stats.supernodes = (int)cp.nsup;
+  p->stats.levels = (int)cp.nlevels;
+  p->stats.nnz_factor = (long long)cp.nnz_l;
+  p->stats.flops_factor = cp.flops_factor;
+  p->stats.analyze_seconds = p->analyze_seconds;
   if (!ok) {
     dmcg_plan_destroy(p);
     return {DMCG_E_CUDA, "CudaError: device allocation failed"};
@@ -520,6 +591,21 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   h2d(p->d_m_val, m.m_val.data(), m.m_val.size() * 4);
   h2d(p->d_anchor_idx, m.anchors.data(), (size_t)p->n_c * 4);
   h2d(p->d_anchor_pos, m.anchor_pos.data(), (size_t)n * 4);
+  h2d((void*)cd.first, cp.first.data(), cp.first.size() * 4);
+  h2d((void*)cd.str_ptr, cp.str_ptr.data(), cp.str_ptr.size() * 8);
+  h2d((void*)cd.str_idx, cp.str_idx.data(), cp.str_idx.size() * 4);
+  h2d((void*)cd.child_ptr, cp.child_ptr.data(), cp.child_ptr.size() * 4);
+  h2d((void*)cd.child_idx, cp.child_idx.data(), cp.child_idx.size() * 4);
+  h2d((void*)cd.rel_ptr, cp.rel_ptr.data(), cp.rel_ptr.size() * 8);
+  h2d((void*)cd.rel_idx, cp.rel_idx.data(), cp.rel_idx.size() * 4);
+  h2d((void*)cd.a_ptr, cp.a_ptr.data(), cp.a_ptr.size() * 8);
+  h2d((void*)cd.a_pos, cp.a_pos.data(), cp.a_pos.size() * 4);
+  h2d((void*)cd.a_val, cp.a_val.data(), cp.a_val.size() * 4);
+  h2d((void*)cd.front_off, cp.front_off.data(), cp.front_off.size() * 8);
+  h2d((void*)cd.inv_off, cp.inv_off.data(), cp.inv_off.size() * 8);
+  h2d((void*)cd.rhs_off, cp.rhs_off.data(), cp.rhs_off.size() * 8);
+  h2d((void*)cd.perm, cp.perm.data(), cp.perm.size() * 4);
+  h2d((void*)cd.level_sup, cp.level_sup.data(), cp.level_sup.size() * 4);
   std::vector<uint8_t> rb(4 * kk, 0);
   for (uint32_t r = 0; r < k; ++r) rb[3 * kk + r] = (uint8_t)p->row_bits[r];
   h2d(p->d_row_bits, rb.data(), rb.size());
@@ -749,16 +835,61 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
       st = {DMCG_E_CUDA, "CudaError: D2H copy failed"};
   if (st.good() && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
     st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
-  if (st.good()) {
-    ctx->last_stats.cg_iterations_max = p->stats.cg_iterations_max;
-    ctx->last_stats.cg_rel_residual_max = p->stats.cg_rel_residual_max;
-    ctx->last_stats.ms_decode = p->stats.ms_decode;
-    ctx->last_stats.ms_reconstruct = p->stats.ms_reconstruct;
-    ctx->last_stats.ms_cg = p->stats.ms_cg;
-    ctx->last_stats.kernel_launches_decode = p->stats.kernel_launches_decode;
+  if (st.good()) {  // keep the encode fields of the last dmcg_encode
+    dmcg_stats e = ctx->last_stats;
+    ctx->last_stats = p->stats;
+    ctx->last_stats.ms_encode = e.ms_encode;
+    ctx->last_stats.ms_delta = e.ms_delta;
+    ctx->last_stats.ms_gram = e.ms_gram;
+    ctx->last_stats.ms_basis = e.ms_basis;
+    ctx->last_stats.ms_project = e.ms_project;
+    ctx->last_stats.kernel_launches_encode = e.kernel_launches_encode;
   }
   dmcg_plan_destroy(p);
   return ctx->set_error(st);
 }
 
 }  // extern "C"
+
+// ---- diagnostics ----------------------------------------------------------------
+#include <chrono>
+
+#include "chol.h"
+
+extern "C" int dmcg_debug_chol(uint32_t n, const uint32_t* faces, uint32_t n_faces, uint32_t n_c,
+                               const uint32_t* anchors, uint32_t W, const double* b, double* x,
+                               double stats[8]) {
+  MeshHost m;
+  Status st = build_mesh(faces, n_faces, n, &m);
+  if (!st.good()) return st.code;
+  m.anchors.assign(anchors, anchors + n_c);
+  m.anchor_pos.assign(n, -1);
+  for (uint32_t t = 0; t < n_c; ++t) m.anchor_pos[anchors[t]] = (int32_t)t;
+  build_normal_matrix(&m);
+  CholPlan p;
+  const auto t0 = std::chrono::steady_clock::now();
+  chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p);
+  const double secs =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (stats) {
+    stats[0] = p.nsup;
+    stats[1] = p.nlevels;
+    stats[2] = (double)p.nnz_l;
+    stats[3] = p.flops_factor;
+    stats[4] = p.flops_solve_per_rhs;
+    stats[5] = p.max_front;
+    stats[6] = p.max_width;
+    stats[7] = secs;
+    if (W == 0 && x) {  // memory footprint query: x[0..2] = sum m^2, sum w^2, sum m
+      x[0] = (double)p.front_off[p.nsup];
+      x[1] = (double)p.inv_off[p.nsup];
+      x[2] = (double)p.rhs_off[p.nsup];
+    }
+  }
+  if (W > 0) {
+    std::vector<double> F, Linv;
+    if (!chol_factor_cpu(p, &F, &Linv)) return DMCG_E_NUMERICAL;
+    chol_solve_cpu(p, F, Linv, W, b, x);
+  }
+  return DMCG_OK;
+}

@@ -9,6 +9,8 @@
 #include <vector>
 
 #include "../../include/dmcg.h"
+#include "chol.h"
+#include "chol_dev.h"
 
 namespace dmcg {
 
@@ -49,6 +51,12 @@ Status build_mesh(const uint32_t* faces, uint32_t n_faces, uint32_t n, MeshHost*
 Status validate_mesh(const MeshHost& m);   // isolated / connected (mesh.cpp:108-136)
 void build_normal_matrix(MeshHost* m);     // needs anchors set
 
+}  // namespace dmcg
+
+struct dmcg_plan;
+namespace dmcg {
+// Device allocation owned by the plan (returned to the context pool on destroy).
+void* plan_alloc(dmcg_plan* p, size_t bytes);
 }  // namespace dmcg
 
 struct dmcg_ctx {
@@ -109,6 +117,13 @@ struct dmcg_plan {
   double *d_cg_x = nullptr, *d_cg_r = nullptr, *d_cg_p = nullptr, *d_cg_q = nullptr;
   int* d_cg_iters = nullptr;       // per column
   double* d_cg_res = nullptr;      // per column relative residual
+  // direct solver (supernodal Cholesky, chol.h)
+  dmcg::CholPlan chol;
+  dmcg::CholLevels levels;
+  dmcg::CholDev cdev;
+  double *d_rm_delta = nullptr, *d_rm_b = nullptr, *d_rm_x = nullptr;  // n x 3F, original order
+  double *d_rm_y = nullptr, *d_rm_xp = nullptr, *d_rm_r = nullptr;     // permuted / residual
+  double analyze_seconds = 0.0;
 
   cudaEvent_t ev[8] = {};
   dmcg_stats stats = {};

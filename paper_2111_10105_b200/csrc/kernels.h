@@ -64,5 +64,12 @@ cudaError_t launch_cg(cudaStream_t s, int n, int W, int nblk, const uint32_t* m_
                       double* Q, double rtol, int maxit, int* iters, double* res);
 cudaError_t launch_output(cudaStream_t s, int n, int F, const double* X, void* const out[3],
                           bool f32);
+// Row-major (n x 3F) variants used by the direct solver.
+cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
+                          const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
+                          const uint16_t* anchor_q, const float* anchor_rng, int anchor_bits,
+                          const double* D, double* B, int* flags);
+cudaError_t launch_output_rm(cudaStream_t s, int n, int F, const double* X, void* const out[3],
+                             bool f32);
 
 }  // namespace dmcg

@@ -256,10 +256,85 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   return Status::ok();
 }
 
+// Direct decode: K6 into the row-major n x 3F layout, rhs, supernodal
+// Cholesky factor + solve + refinement (solver.cpp:43-58, 82-90).
+static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
+                                 void* const out[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int n = (int)p->n, F = (int)p->F, k = (int)p->k, W = (int)p->W;
+  const bool f32 = p->dtype == DMCG_F32;
+  DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
+  DMCG_TRY(cudaEventRecord(p->ev[0], s));
+  const size_t nW = (size_t)n * W;
+  if (k > 0) {
+    DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
+    LoadCoeffDeq la{p->d_coeff_q, p->d_rowp, p->d_row_bits, p->d_flags + 1, n, k};
+    const uint32_t levels = 1u << p->dict_bits;
+    LoadDictDeq lb{p->d_dict_q, 2.0 / (double)levels, levels, F, p->d_flags + 1};
+    // delta~ (i, a*F + f): batch b = axis, rows = vertices, cols = frames
+    DMCG_TRY(launch_gemm(s, 3, n, F, k, 1, la, lb,
+                         StoreStrided{p->d_rm_delta, (long)F, (long)W, 1L}));
+  } else {
+    DMCG_TRY(cudaMemsetAsync(p->d_rm_delta, 0, nW * sizeof(double), s));
+  }
+  DMCG_TRY(launch_rhs_rm(s, n, F, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos, (int)p->n_c,
+                         p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_rm_delta, p->d_rm_b,
+                         p->d_flags + 1));
+  DMCG_TRY(cudaEventRecord(p->ev[1], s));
+  DMCG_TRY(chol_factor_device(s, p->cdev, p->levels));
+  DMCG_TRY(cudaEventRecord(p->ev[2], s));
+  DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
+  DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, false));
+  const int refine = opt ? opt->refine : 1;
+  for (int r = 0; r < refine; ++r) {
+    DMCG_TRY(normal_residual(s, n, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b, p->d_rm_x,
+                             p->d_rm_r));
+    DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp));
+    DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, true));
+  }
+  DMCG_TRY(cudaEventRecord(p->ev[3], s));
+  DMCG_TRY(launch_output_rm(s, n, F, p->d_rm_x, out, f32));
+  DMCG_TRY(cudaEventRecord(p->ev[4], s));
+  int flags[8];
+  DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  DMCG_TRY(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&p->stats.ms_decode, p->ev[0], p->ev[4]);
+  cudaEventElapsedTime(&p->stats.ms_reconstruct, p->ev[0], p->ev[1]);
+  cudaEventElapsedTime(&p->stats.ms_factor, p->ev[1], p->ev[2]);
+  cudaEventElapsedTime(&p->stats.ms_solve, p->ev[2], p->ev[3]);
+  p->stats.ms_cg = 0.0f;
+  p->stats.solver = 0;
+  p->stats.cg_iterations_max = 0;
+  p->stats.cg_rel_residual_max = 0.0;
+  const CholLevels& lv = p->levels;
+  int nl = 0;
+  for (uint32_t l = 0; l < lv.nlevels; ++l) nl += 2 + (int)((lv.maxw[l] + 31) / 32) * 2;
+  const int per_solve = (int)lv.nlevels * 5;
+  p->stats.kernel_launches_decode = (k > 0 ? 2 : 0) + 1 + nl + (1 + refine) * (per_solve + 1) +
+                                    refine + 1;
+  p->stats.flops_solve = (1 + refine) * p->chol.flops_solve_per_rhs * W;
+  if (flags[1]) return Status{DMCG_E_CORRUPT, "CorruptPayload: packed value out of range"};
+  if (flags[4])
+    return Status{DMCG_E_NUMERICAL,
+                  "SingularSystem: anchored normal equations are not positive definite"};
+  return Status::ok();
+}
+
 Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]) {
+  if (!opt || opt->solver == 0) return plan_decode_direct(p, opt, out);
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
   const bool f32 = p->dtype == DMCG_F32;
+  if (!p->d_cg_x) {  // CG vectors are allocated on first use
+    const size_t vec = (size_t)p->nblk * n * kCB * 8;
+    p->d_cg_x = (double*)plan_alloc(p, vec);
+    p->d_cg_r = (double*)plan_alloc(p, vec);
+    p->d_cg_p = (double*)plan_alloc(p, vec);
+    p->d_cg_q = (double*)plan_alloc(p, vec);
+    if (!p->d_cg_x || !p->d_cg_r || !p->d_cg_p || !p->d_cg_q)
+      return Status{DMCG_E_CUDA, "CudaError: device allocation failed"};
+  }
+  p->stats.solver = 1;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
   DMCG_TRY(cudaEventRecord(p->ev[0], s));
   // K6: dequantise + reconstruct delta~ = (U~ c~)^T (codec.cpp:528-533)

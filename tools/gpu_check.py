@@ -70,11 +70,17 @@ def main(names):
         rms_g = O.frame_rms(s.axes, xg).mean()
         rms_o = O.frame_rms(s.axes, xo).mean()
         print(f" decode: gpu {t_dec*1e3:.1f} ms (dev {st['ms_decode']:.2f}: recon {st['ms_reconstruct']:.2f}"
-              f" cg {st['ms_cg']:.2f}, iters {st['cg_iterations_max']}, res {st['cg_rel_residual_max']:.1e});"
+              f" factor {st['ms_factor']:.2f} solve {st['ms_solve']:.2f} | sup {st['supernodes']}"
+              f" lev {st['levels']} nnzL {st['nnz_factor']:.3g} analyze {st['analyze_seconds']:.3f}s);"
               f" oracle {t_odec*1e3:.0f} ms")
+        if "--cg" in sys.argv:
+            xc = cd.decode(g, rtol=1e-10, solver="cg")
+            stc = cd.stats()
+            print(f"   cg: {stc['ms_cg']:.1f} ms, iters {stc['cg_iterations_max']};"
+                  f" max|x_cg - x_direct|/bbox = {max(np.abs(xc[a]-xg[a]).max() for a in range(3))/bbox:.2e}")
         print(f"   same-stream max|x_gpu-x_cpu|/bbox = {dmax/bbox:.2e}; rmse gpu {rms_g:.4e} cpu {rms_o:.4e}"
               f" ratio-1 {rms_g/rms_o-1:.2e}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c0"])
+    main([a for a in sys.argv[1:] if not a.startswith("--")] or ["c0"])
