@@ -1,8 +1,10 @@
 // K3 — small dense kernels of the temporal basis: Householder QR (rank
 // safe), round-robin Jacobi eigensolver, descending sort, canonical signs.
 // One CTA per axis; matrices are F x k / k x k (F <= 512) and live in L2 /
-// shared memory.  Compiled with --fmad=false so the arithmetic mirrors the
-// oracle restatement (oracle/dmc_oracle.c) operation for operation.
+// shared memory.  Same algorithms and formulas as the oracle restatement
+// (oracle/dmc_oracle.c: householder_factor, orc_jacobi_eig, orc_basis);
+// reductions run in parallel order and use FMA, so results agree with the
+// oracle to rounding, not bit for bit (P3).
 #include <cfloat>
 
 #include "common.cuh"
@@ -13,6 +15,7 @@ namespace dmcg {
 namespace {
 
 constexpr int kBasisThreads = 1024;
+constexpr int kOiThreads = 512;  // fused OI kernels: 128 registers per thread
 
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -310,6 +313,295 @@ __global__ void k_symmetrize(int m, double* Hall) {
   H[(size_t)i * m + j] = s;
 }
 
+// ---------------------------------------------------------------------------
+// Fused orthogonal iterations: one CTA per axis runs every round
+//   Z = R Q  (SIMT, R from L2, Q in smem);  Q = thin Householder Q of Z
+// and the Rayleigh-Ritz matrix H = Q^T R Q, with Z and Q in shared memory
+// when 2 F k doubles fit (else in a global work area, L1/L2 resident).
+// The Householder QR needs one CTA barrier per column: the warp that
+// updates column j+1 in step j also computes column j+1's reflector, and
+// the scaling of reflector j is deferred to step j+1 (column j is read
+// unscaled, divided on the fly, during step j).
+// ---------------------------------------------------------------------------
+struct QrShared {
+  double tau[512], rinv[512];
+};
+
+// Register-blocked warp primitives: a lane owns rows j+1+lane+32t,
+// t < MAXR (MAXR = ceil(F/32) <= 16), so all its loads issue back to back.
+
+// Reflector of column c (rows >= c) by one warp: tau and 1/(c0 - beta), the
+// diagonal set to beta (the oracle's householder_factor formulas; the GPU
+// scales by the reciprocal instead of dividing element by element, a
+// 1-ulp difference inside the P3 tolerance).
+template <int MAXR, typename P>
+__device__ __forceinline__ void qr_reflector(P Z, int m, int c, QrShared& q, int lane) {
+  P x = Z + c * m;
+  double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t) {
+    const int i = c + 1 + lane + 32 * t;
+    const double xi = i < m ? x[i] : 0.0;
+    if (t & 1)
+      p1 += xi * xi;
+    else
+      p0 += xi * xi;
+  }
+  const double tail = warp_sum(p0 + p1);
+  const double c0 = x[c];
+  double rinv = 0.0, tau = 0.0;
+  if (tail > DBL_MIN) {
+    const double s2 = c0 * c0 + tail;
+    const double r = rsqrt(s2);
+    const double nrm = s2 * r;
+    const double bb = c0 >= 0.0 ? -nrm : nrm;
+    const double ibb = c0 >= 0.0 ? -r : r;
+    rinv = __drcp_rn(c0 - bb);
+    tau = (bb - c0) * ibb;
+    __syncwarp();
+    if (lane == 0) x[c] = bb;
+  }
+  if (lane == 0) {
+    q.tau[c] = tau;
+    q.rinv[c] = rinv;
+  }
+  __syncwarp();
+}
+
+// y_c -= tau v (v^T y_c) for columns c = c0, c0 + stride, ... < cend (rows > j
+// of v are vs * v[i]; v[j] = 1 implicit), two columns per pass so their
+// warp reductions overlap.
+template <int MAXR, typename PY, typename PV>
+__device__ __forceinline__ void apply_reflector_cols(PY Y, int ld, int j, PV v, double vs,
+                                                     double tau, int c0, int cend, int stride,
+                                                     int lane, int m) {
+  if (c0 >= cend) return;
+  double vr[MAXR];
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t) {
+    const int i = j + 1 + lane + 32 * t;
+    vr[t] = i < m ? v[i] * vs : 0.0;
+  }
+  for (int c = c0; c < cend; c += 2 * stride) {
+    const bool two = c + stride < cend;
+    PY ya = Y + c * ld;
+    PY yb = Y + (two ? c + stride : c) * ld;
+    double ra[MAXR], rb[MAXR];
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int i = j + 1 + lane + 32 * t;
+      ra[t] = i < m ? ya[i] : 0.0;
+      rb[t] = (two && i < m) ? yb[i] : 0.0;
+    }
+    double da0 = 0.0, da1 = 0.0, db0 = 0.0, db1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      if (t & 1) {
+        da1 += vr[t] * ra[t];
+        db1 += vr[t] * rb[t];
+      } else {
+        da0 += vr[t] * ra[t];
+        db0 += vr[t] * rb[t];
+      }
+    }
+    double da = da0 + da1, db = db0 + db1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      da += __shfl_xor_sync(0xffffffffu, da, o);
+      db += __shfl_xor_sync(0xffffffffu, db, o);
+    }
+    const double yja = ya[j], yjb = two ? yb[j] : 0.0;
+    da = tau * (yja + da);
+    db = tau * (yjb + db);
+    __syncwarp();
+    if (lane == 0) {
+      ya[j] = yja - da;
+      if (two) yb[j] = yjb - db;
+    }
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int i = j + 1 + lane + 32 * t;
+      if (i < m) {
+        ya[i] = ra[t] - da * vr[t];
+        if (two) yb[i] = rb[t] - db * vr[t];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void qr_scale(P Z, int m, int j, const QrShared& q) {
+  P x = Z + j * m;
+  const double r = q.rinv[j];
+  const bool zero = q.tau[j] == 0.0;
+  for (int i = j + 1 + (int)threadIdx.x; i < m; i += blockDim.x) x[i] = zero ? 0.0 : x[i] * r;
+}
+
+// In-place Householder factorisation of the m x p column-major Z; on exit
+// column j below the diagonal holds the scaled reflector (Eigen layout).
+// One CTA barrier per column: reflector j+1 is computed by warp 0 right
+// after it updates column j+1, and the scaling of column j is deferred to
+// step j+1 (during step j the raw column is read and scaled on the fly).
+template <int MAXR, typename P>
+__device__ void qr_factor(P Z, int m, int p, QrShared& q) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int pe = p < m ? p : m;
+  if (pe <= 0) return;
+  if (warp == 0) qr_reflector<MAXR>(Z, m, 0, q, lane);
+  __syncthreads();
+  for (int j = 0; j < pe; ++j) {
+    const double tj = q.tau[j], rj = q.rinv[j];
+    if (j > 0) qr_scale(Z, m, j - 1, q);
+    // warp 0: column j+1 alone, then reflector j+1, then its share of the
+    // rest; columns j+2.. are spread over all warps.
+    if (warp == 0 && j + 1 < p) {
+      if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 1, j + 2, 1, lane, m);
+      if (j + 1 < pe) qr_reflector<MAXR>(Z, m, j + 1, q, lane);
+    }
+    if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 2 + warp, p, nw, lane, m);
+    __syncthreads();
+  }
+  qr_scale(Z, m, pe - 1, q);
+  __syncthreads();
+}
+
+// Qout (m x ncols, leading dimension ldq) = H_0 ... H_{pe-1} [e_c0 ...].
+template <int MAXR, typename PZ, typename PQ>
+__device__ void qr_form(PZ Z, int m, int p, int c0, int ncols, PQ Qo, int ldq, const QrShared& q) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int pe = p < m ? p : m;
+  for (int t = threadIdx.x; t < m * ncols; t += blockDim.x) {
+    const int c = t / m, r = t % m;
+    Qo[c * ldq + r] = (r == c0 + c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = pe - 1; j >= 0; --j) {
+    const double tj = q.tau[j];
+    if (tj == 0.0) continue;
+    PZ v = Z + j * m;
+    const int cstart = (c0 == 0) ? (j < ncols ? j : ncols) : 0;
+    apply_reflector_cols<MAXR>(Qo, ldq, j, v, 1.0, tj, cstart + warp, ncols, nw, lane, m);
+    __syncthreads();
+  }
+}
+
+// Z (F x k) = R (F x F, symmetric, global) * Q (F x k) on the FP64 tensor
+// pipe: each warp owns an 8-row block and up to 64 columns (8 DMMA tiles of
+// 8x8, K = F in steps of 4).  A fragments stream from L2, B from Q.
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <typename PA, typename PB, typename PC>
+__device__ void warp_gemm_tn(int M, int N, int K, PA A, int lda, PB B, int ldb, PC C, int ldc) {
+  // C (M x N, col-major ldc) = A^T B with A (K x M, col-major lda: A(k,i) =
+  // A[i*lda + k]) ... general form: C(i, j) = sum_k A[i*lda + k] * B[j*ldb + k]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mb = (M + 7) / 8, nbk = (N + 63) / 64;
+  for (int t = warp; t < mb * nbk; t += nw) {
+    const int i0 = (t % mb) * 8, j00 = (t / mb) * 64;
+    double acc[8][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const int ia = i0 + (lane >> 2);
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int ka = k0 + (lane & 3);
+      const double a = (ia < M && ka < K) ? A[ia * lda + ka] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int jb = j00 + u * 8 + (lane >> 2);
+        const double b = (jb < N && ka < K) ? B[jb * ldb + ka] : 0.0;
+        dmma884(acc[u], a, b);
+      }
+    }
+    const int ir = i0 + (lane >> 2);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int jc = j00 + u * 8 + (lane & 3) * 2 + e;
+        if (ir < M && jc < N) C[jc * ldc + ir] = acc[u][e];
+      }
+  }
+}
+
+// Z = R Q: Z(g, j) = sum_f R(g, f) Q(f, j) = sum_f R[g*F + f] Q[j*F + f]
+// (R symmetric, so its column g is its row g).
+template <typename P>
+__device__ void oi_apply(const double* __restrict__ R, int F, int k, P Q, P Z) {
+  warp_gemm_tn(F, k, F, R, F, Q, F, Z, F);
+  __syncthreads();
+}
+
+template <int MAXR, typename P>
+__device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
+                        const double* __restrict__ start, P Z, P Q, double* Qo, double* H,
+                        QrShared& q) {
+  const int Fk = F * k;
+  for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = start[t];
+  __syncthreads();
+  qr_factor<MAXR>(Z, F, k, q);
+  qr_form<MAXR>(Z, F, k, 0, k, Q, F, q);
+  for (int r = 0; r < rounds; ++r) {
+    oi_apply(R, F, k, Q, Z);
+    qr_factor<MAXR>(Z, F, k, q);
+    qr_form<MAXR>(Z, F, k, 0, k, Q, F, q);
+  }
+  // Rayleigh-Ritz: H = Q^T (R Q), symmetrised; Q out.
+  oi_apply(R, F, k, Q, Z);
+  // H(i, j) = sum_g Q(g, i) Z(g, j), then symmetrised like the oracle
+  warp_gemm_tn(k, k, F, Q, F, Z, F, H, k);
+  __syncthreads();
+  for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
+    const int i = t % k, j = t / k;
+    if (i >= j) continue;
+    const double sv = 0.5 * (H[j * k + i] + H[i * k + j]);
+    H[j * k + i] = sv;
+    H[i * k + j] = sv;
+  }
+  for (int t = threadIdx.x; t < Fk; t += blockDim.x) Qo[t] = Q[t];
+}
+
+template <bool SMEM, int MAXR>
+__global__ void __launch_bounds__(kOiThreads)
+    k_oi_fused(int F, int k, int rounds, const double* __restrict__ Rall,
+               const double* __restrict__ start, double* Qall, double* Hall, double* work) {
+  extern __shared__ double dyn[];
+  __shared__ QrShared q;
+  const int b = blockIdx.x;
+  const size_t Fk = (size_t)F * k;
+  const double* R = Rall + (size_t)b * F * F;
+  if (SMEM)
+    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Fk, Qall + b * Fk, Hall + (size_t)b * k * k, q);
+  else
+    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Fk, work + b * 2 * Fk + Fk, Qall + b * Fk,
+            Hall + (size_t)b * k * k, q);
+}
+
+// Completion: columns k..F-1 of the full Householder Q of U_k (F x k, the
+// first k columns of U), written straight into U.
+template <bool SMEM, int MAXR>
+__global__ void __launch_bounds__(kOiThreads) k_complete(int F, int k, double* Uall, double* work) {
+  extern __shared__ double dyn[];
+  __shared__ QrShared q;
+  const int b = blockIdx.x;
+  const int Fk = F * k;
+  double* Z = SMEM ? dyn : work + (size_t)b * Fk;
+  double* U = Uall + (size_t)b * F * F;
+  for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = U[t];
+  __syncthreads();
+  if (SMEM) {
+    qr_factor<MAXR>(dyn, F, k, q);
+    qr_form<MAXR>(dyn, F, k, k, F - k, U + Fk, F, q);
+  } else {
+    qr_factor<MAXR>(Z, F, k, q);
+    qr_form<MAXR>(Z, F, k, k, F - k, U + Fk, F, q);
+  }
+}
+
 __global__ void k_fill_zero(double* p, long count) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (t < count) p[t] = 0.0;
@@ -358,6 +650,57 @@ cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H) {
   dim3 grid((unsigned)(((long)m * m + 255) / 256), nbatch);
   k_symmetrize<<<grid, 256, 0, s>>>(m, H);
   return cudaGetLastError();
+}
+
+static cudaError_t set_smem_attr(const void* fn, size_t bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+constexpr size_t kBasisSmemMax = 200 * 1024;  // + ~17 KB static QrShared <= 227 KB
+
+template <int MAXR>
+static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int rounds,
+                                 const double* R, const double* start, double* Q, double* H,
+                                 double* work) {
+  const size_t smem = (size_t)2 * F * k * sizeof(double);
+  if (smem <= kBasisSmemMax) {
+    cudaError_t e = set_smem_attr((const void*)k_oi_fused<true, MAXR>, smem);
+    if (e != cudaSuccess) return e;
+    k_oi_fused<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work);
+  } else {
+    k_oi_fused<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, rounds, R, start, Q, H, work);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
+                            const double* start, double* Q, double* H, double* work) {
+  if (F > 512) return cudaErrorInvalidValue;
+  if (F <= 64) return oi_fused_impl<2>(s, nbatch, F, k, rounds, R, start, Q, H, work);
+  if (F <= 128) return oi_fused_impl<4>(s, nbatch, F, k, rounds, R, start, Q, H, work);
+  if (F <= 256) return oi_fused_impl<8>(s, nbatch, F, k, rounds, R, start, Q, H, work);
+  return oi_fused_impl<16>(s, nbatch, F, k, rounds, R, start, Q, H, work);
+}
+
+template <int MAXR>
+static cudaError_t complete_impl(cudaStream_t s, int nbatch, int F, int k, double* U, double* work) {
+  const size_t smem = (size_t)F * k * sizeof(double);
+  if (smem <= kBasisSmemMax) {
+    cudaError_t e = set_smem_attr((const void*)k_complete<true, MAXR>, smem);
+    if (e != cudaSuccess) return e;
+    k_complete<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, U, work);
+  } else {
+    k_complete<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, U, work);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work) {
+  if (F > 512) return cudaErrorInvalidValue;
+  if (F <= 64) return complete_impl<2>(s, nbatch, F, k, U, work);
+  if (F <= 128) return complete_impl<4>(s, nbatch, F, k, U, work);
+  if (F <= 256) return complete_impl<8>(s, nbatch, F, k, U, work);
+  return complete_impl<16>(s, nbatch, F, k, U, work);
 }
 
 cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count) {

@@ -79,59 +79,76 @@ __global__ void __launch_bounds__(256) k_assemble(CholDev d, const uint32_t* lsu
   }
 }
 
-// Unblocked right-looking Cholesky of panel columns [k0, k0 + pw), staged in
-// shared memory when (m - k0) x pw fits (else in place in global memory).
-constexpr int kPanelThreads = 512;
+// Panel [k0, k0 + pw) of a front: warp 0 factors the pw x pw diagonal
+// block in shared memory (right-looking, lanes own rows), then every thread
+// solves its own rows of the panel below against it (row-wise TRSM, no
+// barriers inside).  The diagonal is inverted once and applied by
+// multiplication (the CPU reference divides; results agree to rounding).
+constexpr int kPanelThreads = 256;  // 32 panel values per thread stay in registers
+constexpr int kNB = 32;
 
 __global__ void __launch_bounds__(kPanelThreads)
-    k_panel(CholDev d, const uint32_t* lsup, int k0, int nb, int smem_rows) {
-  extern __shared__ double Ps[];
-  __shared__ double s_r;
+    k_panel(CholDev d, const uint32_t* lsup, int k0, int nb) {
+  __shared__ double D[kNB][kNB + 1];
+  __shared__ double dinv[kNB];
   const uint32_t s = lsup[blockIdx.x];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s);
   if (k0 >= w) return;
   const int pw = min(nb, w - k0);
   double* A = d.F + d.front_off[s];
-  const int rows = m - k0;
-  const bool staged = rows <= smem_rows;
-  double* P;
-  int ld;
-  if (staged) {
-    P = Ps;
-    ld = rows;
-    for (int t = threadIdx.x; t < rows * pw; t += blockDim.x) {
-      const int c = t / rows, r = t % rows;
-      P[t] = A[(size_t)(k0 + c) * m + k0 + r];
-    }
-    __syncthreads();
-  } else {
-    P = A + (size_t)k0 * m + k0;
-    ld = m;
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
+    const int c = t / pw, r = t % pw;
+    D[r][c] = r >= c ? A[(size_t)(k0 + c) * m + k0 + r] : 0.0;
   }
-  for (int j = 0; j < pw; ++j) {
-    double* cj = P + (size_t)j * ld;
-    if (threadIdx.x == 0) {
-      const double dj = cj[j];
-      if (!(dj > 0.0)) atomicOr(d.flags, 1);
-      s_r = sqrt(fmax(dj, DBL_MIN));
-      cj[j] = s_r;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int r = lane;
+    for (int j = 0; j < pw; ++j) {
+      const double djj = D[j][j];
+      if (djj <= 0.0 || !(djj == djj)) {
+        if (lane == 0) atomicOr(d.flags, 1);
+      }
+      const double piv = sqrt(fmax(djj, DBL_MIN));
+      const double ip = 1.0 / piv;
+      __syncwarp();
+      if (r == j) {
+        D[j][j] = piv;
+        dinv[j] = ip;
+      }
+      if (r > j && r < pw) D[r][j] *= ip;
+      __syncwarp();
+      if (r > j && r < pw) {
+        const double lrj = D[r][j];
+        for (int c = j + 1; c <= r; ++c) D[r][c] -= lrj * D[c][j];
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    const double r = s_r;
-    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x) cj[i] = cj[i] / r;
-    __syncthreads();
-    const int rem = pw - j - 1;
-    for (int t = threadIdx.x; t < rem * rows; t += blockDim.x) {
-      const int c = j + 1 + t / rows, i = t % rows;
-      if (i >= c) P[(size_t)c * ld + i] -= cj[i] * cj[c];
-    }
-    __syncthreads();
   }
-  if (staged)
-    for (int t = threadIdx.x; t < rows * pw; t += blockDim.x) {
-      const int c = t / rows, r = t % rows;
-      A[(size_t)(k0 + c) * m + k0 + r] = P[t];
+  __syncthreads();
+  // write the factored diagonal block back
+  for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
+    const int c = t / pw, r = t % pw;
+    if (r >= c) A[(size_t)(k0 + c) * m + k0 + r] = D[r][c];
+  }
+  // rows below: x = a L^{-T}, forward substitution per row
+  for (int i = k0 + pw + threadIdx.x; i < m; i += blockDim.x) {
+    double x[kNB];
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) x[c] = c < pw ? A[(size_t)(k0 + c) * m + i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+      if (j < pw) {
+        double acc = x[j];
+#pragma unroll
+        for (int c = 0; c < j; ++c) acc -= x[c] * D[j][c];
+        x[j] = acc * dinv[j];
+      }
     }
+#pragma unroll
+    for (int c = 0; c < kNB; ++c)
+      if (c < pw) A[(size_t)(k0 + c) * m + i] = x[c];
+  }
 }
 
 // Trailing update of each front in the level: A22 -= P P^T (lower tiles).
@@ -463,8 +480,6 @@ __global__ void k_residual(int n, int W, const uint32_t* __restrict__ rp,
 
 }  // namespace
 
-constexpr int kPanelSmem = 200 * 1024;
-
 cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevels& lv) {
   const int nb = 32;
   {
@@ -472,10 +487,7 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_set & (1ull << dev))) {
-      cudaError_t e =
-          cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaError_t e = cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kInvDiagSmem);
       if (e != cudaSuccess) return e;
       attr_set |= 1ull << dev;
@@ -488,10 +500,7 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
     const uint32_t* ls = d.level_sup + lv.offset[l];
     k_assemble<<<dim3((lv.maxm[l] + kAsmCols - 1) / kAsmCols, cnt), 256, 0, s>>>(d, ls);
     for (uint32_t k0 = 0; k0 < lv.maxw[l]; k0 += nb) {
-      const int smem_rows = kPanelSmem / (nb * (int)sizeof(double));
-      const size_t need = (size_t)std::min<int>(smem_rows, (int)(lv.maxm[l] - k0)) * nb * 8;
-      k_panel<<<cnt, kPanelThreads, need, s>>>(d, ls, (int)k0, nb,
-                                               (int)(need / (nb * sizeof(double))));
+      k_panel<<<cnt, kPanelThreads, 0, s>>>(d, ls, (int)k0, nb);
       // bound over the level: a front whose last panel is partial (pw < nb)
       // has a trailing block of m - k0 - pw rows
       const uint32_t T = lv.maxm[l] > k0 + 1 ? lv.maxm[l] - k0 - 1 : 0;

@@ -513,6 +513,60 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_rowp = (double*)get(3 * kk * 2 * 8);
   p->d_cg_iters = (int*)get(p->W_pad * 4);
   p->d_cg_res = (double*)get(p->W_pad * 8);
+  if (!ok) {
+    dmcg_plan_destroy(p);
+    return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  }
+  for (auto& e : p->ev) cudaEventCreate(&e);
+  cudaStream_t s = ctx->stream;
+  auto h2d = [&](void* d, const void* h, size_t bytes) {
+    if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  };
+  h2d(p->d_lap_rp, m.lap_rp.data(), m.lap_rp.size() * 4);
+  h2d(p->d_lap_ci, m.lap_ci.data(), m.lap_ci.size() * 4);
+  h2d(p->d_m_rp, m.m_rp.data(), m.m_rp.size() * 4);
+  h2d(p->d_m_ci, m.m_ci.data(), m.m_ci.size() * 4);
+  h2d(p->d_m_val, m.m_val.data(), m.m_val.size() * 4);
+  h2d(p->d_anchor_idx, m.anchors.data(), (size_t)p->n_c * 4);
+  h2d(p->d_anchor_pos, m.anchor_pos.data(), (size_t)n * 4);
+  std::vector<uint8_t> rb(4 * kk, 0);
+  for (uint32_t r = 0; r < k; ++r) rb[3 * kk + r] = (uint8_t)p->row_bits[r];
+  h2d(p->d_row_bits, rb.data(), rb.size());
+  // OI start matrices: SplitMix64 uniform in [-1, 1), column-major F x k,
+  // axis a seeded with oi_seed + a (same stream as oracle orc_start_matrix).
+  std::vector<double> start(3 * (size_t)F * kk, 0.0);
+  if (k > 0)
+    for (int a = 0; a < 3; ++a) {
+      uint64_t st64 = p->oi_seed + (uint64_t)a;
+      for (size_t t = 0; t < (size_t)F * k; ++t)
+        start[a * (size_t)F * k + t] = (double)(splitmix64(&st64) >> 11) * 0x1.0p-52 - 1.0;
+    }
+  h2d(p->d_start, start.data(), start.size() * 8);
+  if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
+  if (!ok) {
+    dmcg_plan_destroy(p);
+    return {DMCG_E_CUDA, "CudaError: plan upload failed"};
+  }
+  *out = p;
+  return Status::ok();
+}
+
+}  // extern "C"
+
+// Decode-side state (symbolic Cholesky analysis of M, factor / RHS buffers)
+// is built on the first decode of a plan only: encode-only plans never pay
+// for it.  Reference: the normal matrix and its factorisation are per
+// decode call (solver.cpp:62-90).
+dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
+  if (p->decode_ready) return Status::ok();
+  const uint32_t n = p->n;
+  const MeshHost& m = p->mesh;
+  bool ok = true;
+  auto get = [&](size_t bytes) {
+    void* d = plan_alloc(p, bytes);
+    ok = ok && d;
+    return d;
+  };
   // direct solver: symbolic analysis of M (host) + device structures
   {
     const auto t0 = std::chrono::steady_clock::now();
@@ -575,22 +629,11 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->stats.nnz_factor = (long long)cp.nnz_l;
   p->stats.flops_factor = cp.flops_factor;
   p->stats.analyze_seconds = p->analyze_seconds;
-  if (!ok) {
-    dmcg_plan_destroy(p);
-    return {DMCG_E_CUDA, "CudaError: device allocation failed"};
-  }
-  for (auto& e : p->ev) cudaEventCreate(&e);
-  cudaStream_t s = ctx->stream;
+  if (!ok) return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  cudaStream_t s = p->ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
   };
-  h2d(p->d_lap_rp, m.lap_rp.data(), m.lap_rp.size() * 4);
-  h2d(p->d_lap_ci, m.lap_ci.data(), m.lap_ci.size() * 4);
-  h2d(p->d_m_rp, m.m_rp.data(), m.m_rp.size() * 4);
-  h2d(p->d_m_ci, m.m_ci.data(), m.m_ci.size() * 4);
-  h2d(p->d_m_val, m.m_val.data(), m.m_val.size() * 4);
-  h2d(p->d_anchor_idx, m.anchors.data(), (size_t)p->n_c * 4);
-  h2d(p->d_anchor_pos, m.anchor_pos.data(), (size_t)n * 4);
   h2d((void*)cd.first, cp.first.data(), cp.first.size() * 4);
   h2d((void*)cd.str_ptr, cp.str_ptr.data(), cp.str_ptr.size() * 8);
   h2d((void*)cd.str_idx, cp.str_idx.data(), cp.str_idx.size() * 4);
@@ -606,27 +649,13 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   h2d((void*)cd.rhs_off, cp.rhs_off.data(), cp.rhs_off.size() * 8);
   h2d((void*)cd.perm, cp.perm.data(), cp.perm.size() * 4);
   h2d((void*)cd.level_sup, cp.level_sup.data(), cp.level_sup.size() * 4);
-  std::vector<uint8_t> rb(4 * kk, 0);
-  for (uint32_t r = 0; r < k; ++r) rb[3 * kk + r] = (uint8_t)p->row_bits[r];
-  h2d(p->d_row_bits, rb.data(), rb.size());
-  // OI start matrices: SplitMix64 uniform in [-1, 1), column-major F x k,
-  // axis a seeded with oi_seed + a (same stream as oracle orc_start_matrix).
-  std::vector<double> start(3 * (size_t)F * kk, 0.0);
-  if (k > 0)
-    for (int a = 0; a < 3; ++a) {
-      uint64_t st64 = p->oi_seed + (uint64_t)a;
-      for (size_t t = 0; t < (size_t)F * k; ++t)
-        start[a * (size_t)F * k + t] = (double)(splitmix64(&st64) >> 11) * 0x1.0p-52 - 1.0;
-    }
-  h2d(p->d_start, start.data(), start.size() * 8);
   if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
-  if (!ok) {
-    dmcg_plan_destroy(p);
-    return {DMCG_E_CUDA, "CudaError: plan upload failed"};
-  }
-  *out = p;
+  if (!ok) return {DMCG_E_CUDA, "CudaError: decode plan upload failed"};
+  p->decode_ready = true;
   return Status::ok();
 }
+
+extern "C" {
 
 int dmcg_plan_create(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uint32_t* faces,
                      uint32_t n_faces, const dmcg_config* cfg, dmcg_plan** plan) {

@@ -57,6 +57,8 @@ struct dmcg_plan;
 namespace dmcg {
 // Device allocation owned by the plan (returned to the context pool on destroy).
 void* plan_alloc(dmcg_plan* p, size_t bytes);
+// Builds the decode-side state on first use (host.cpp).
+Status plan_prepare_decode(dmcg_plan* p);
 }  // namespace dmcg
 
 struct dmcg_ctx {
@@ -124,6 +126,7 @@ struct dmcg_plan {
   double *d_rm_delta = nullptr, *d_rm_b = nullptr, *d_rm_x = nullptr;  // n x 3F, original order
   double *d_rm_y = nullptr, *d_rm_xp = nullptr, *d_rm_r = nullptr;     // permuted / residual
   double analyze_seconds = 0.0;
+  bool decode_ready = false;
 
   cudaEvent_t ev[8] = {};
   dmcg_stats stats = {};

@@ -47,6 +47,13 @@ cudaError_t launch_sort_basis(cudaStream_t s, int nbatch, int m, int ncols_store
 cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int ncols, double* U,
                                long bs);
 cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H);
+// Fused orthogonal iterations (one CTA per axis): Q0 = qr(start), `rounds`
+// x {Z = R Q; Q = qr(Z)}, then H = Q^T R Q (symmetrised).  work: nbatch *
+// 2 F k doubles (used when the pair does not fit in shared memory).
+cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
+                            const double* start, double* Q, double* H, double* work);
+// U[:, k:F] = columns k..F-1 of the full Householder Q of U[:, :k].
+cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work);
 cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count);
 
 // ---- decode.cu ------------------------------------------------------------

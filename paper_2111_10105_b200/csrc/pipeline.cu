@@ -153,24 +153,10 @@ Status basis(dmcg_plan* p) {
     return Status::ok();
   }
   const long Fk = (long)F * k;
-  // Q0 = Householder Q of the seeded start matrix.
-  DMCG_TRY(cudaMemcpyAsync(p->d_Z, p->d_start, 3 * Fk * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  DMCG_TRY(launch_householder(s, 3, F, k, 0, k, p->d_Z, p->d_tau, p->d_Q));
-  // Z = R Q: A(k = f, m = g) = R[f*F + g], B(k = f, n = j) = Q[j*F + f].
-  LoadDense<double, false> lR{p->d_R, FF, (long)F, 1L};
-  LoadDense<double, true> lQ{p->d_Q, Fk, 1L, (long)F};
-  StoreStrided sZ{p->d_Z, Fk, 1L, (long)F};
-  for (int t = 0; t < p->rounds; ++t) {
-    DMCG_TRY(launch_gemm(s, 3, F, k, F, 1, lR, lQ, sZ));
-    DMCG_TRY(launch_householder(s, 3, F, k, 0, k, p->d_Z, p->d_tau, p->d_Q));
-  }
-  // Rayleigh-Ritz: H = Q^T (R Q).
-  DMCG_TRY(launch_gemm(s, 3, F, k, F, 1, lR, lQ, sZ));
-  LoadDense<double, true> lQt{p->d_Q, Fk, 1L, (long)F};
-  LoadDense<double, true> lZ{p->d_Z, Fk, 1L, (long)F};
+  // Q0 = qr(start); rounds x {Z = R Q; Q = qr(Z)}; H = Q^T R Q — one fused
+  // kernel, one CTA per axis (basis.cu k_oi_fused).
   double* H = p->d_C;  // k x k scratch (coefficient buffer is free here)
-  DMCG_TRY(launch_gemm(s, 3, k, k, F, 1, lQt, lZ, StoreStrided{H, (long)k * k, 1L, (long)k}));
-  DMCG_TRY(launch_symmetrize(s, 3, k, H));
+  DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H));
   DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
   double* Ws = p->d_Z;  // k x k sorted Ritz vectors (Z is free)
   DMCG_TRY(launch_sort_basis(s, 3, k, k, p->d_V, p->d_w, Ws, (long)k * k, p->d_evals, F));
@@ -180,14 +166,7 @@ Status basis(dmcg_plan* p) {
   DMCG_TRY(launch_gemm(s, 3, F, k, k, 1, lQm, lW, StoreStrided{p->d_U, FF, 1L, (long)F}));
   DMCG_TRY(launch_canon_signs(s, 3, F, 0, k, p->d_U, FF));
   // Completion to F x F: columns k..F-1 of the full Householder Q of U_k.
-  for (int a = 0; a < 3; ++a)
-    DMCG_TRY(cudaMemcpyAsync(p->d_Q + a * Fk, p->d_U + a * FF, Fk * sizeof(double),
-                             cudaMemcpyDeviceToDevice, s));
-  double* comp = p->d_H;  // F x (F-k) per axis scratch (jacobi work is free)
-  DMCG_TRY(launch_householder(s, 3, F, k, k, F - k, p->d_Q, p->d_tau, comp));
-  for (int a = 0; a < 3; ++a)
-    DMCG_TRY(cudaMemcpyAsync(p->d_U + a * FF + Fk, comp + (long)a * F * (F - k),
-                             (size_t)F * (F - k) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  DMCG_TRY(launch_complete(s, 3, F, k, p->d_U, p->d_H));
   DMCG_TRY(launch_canon_signs(s, 3, F, k, F - k, p->d_U, FF));
   for (int a = 0; a < 3; ++a)
     DMCG_TRY(launch_fill_zero(s, p->d_evals + (long)a * F + k, F - k));
@@ -321,7 +300,11 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
 }
 
 Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]) {
-  if (!opt || opt->solver == 0) return plan_decode_direct(p, opt, out);
+  if (!opt || opt->solver == 0) {
+    Status st = plan_prepare_decode(p);
+    if (!st.good()) return st;
+    return plan_decode_direct(p, opt, out);
+  }
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
   const bool f32 = p->dtype == DMCG_F32;
