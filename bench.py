@@ -196,7 +196,7 @@ def main():
     d_out = [torch.empty_like(t) for t in d_in]
     stream = torch.cuda.ExternalStream(plan.stream())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    step_ms, cg_ms, launches, iters = [], [], 0, []
+    step_ms, fac_ms, sol_ms, launches = [], [], [], 0
     for it in range(args.warmup):
         plan.encode_device([t.data_ptr() for t in d_in])
         plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
@@ -216,8 +216,8 @@ def main():
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
             st = plan.stats()
-            cg_ms.append(st["ms_cg"])
-            iters.append(st["cg_iterations_max"])
+            fac_ms.append(st["ms_factor"])
+            sol_ms.append(st["ms_solve"])
             launches += st["kernel_launches_encode"] + st["kernel_launches_decode"]
     torch.cuda.synchronize()
     total_ms = float(sum(step_ms))
@@ -229,25 +229,27 @@ def main():
     vf_step = s.n * s.F
     value = vf_step * world * args.steps / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (K7 CG): algorithmic bytes per launch =
-    # iterations x (6 vector passes over n x 3F fp64 + M values/indices)
-    nnz_m = int(plan.stats()["nnz_normal"])
-    W = 3 * s.F
-    it_med = float(np.median(iters))
-    cg_bytes = it_med * (6.0 * s.n * W * 8 + nnz_m * (4 + 8))
-    cg_sec = float(np.median(cg_ms)) / 1e3
-    peak, peak_kind = load_peak()
-    achieved = cg_bytes / cg_sec / 1e9 if cg_sec > 0 else 0.0
+    # roofline of the dominant stage, the decode's direct solve (K7: supernodal
+    # Cholesky factor + 2 multi-RHS solves, DMMA): algorithmic flops per
+    # decode (CholPlan::flops_factor + flops_solve) over the
+    # K7 device time measured with CUDA events inside the plan.
+    st = plan.stats()
+    k7_flops = float(st["flops_factor"] + st["flops_solve"])
+    k7_sec = float(np.median(fac_ms) + np.median(sol_ms)) / 1e3
+    peak = FP64_DMMA_TFLOPS
+    achieved = k7_flops / k7_sec / 1e12 if k7_sec > 0 else 0.0
 
     # ---- e2e through the drop-in C ABI from pinned host memory -------------
     pinned = [torch.from_numpy(np.ascontiguousarray(x, dtype=npdt)).pin_memory() for x in s.axes]
     host_seq = type(s)(s.faces, [p.numpy() for p in pinned])
+    pinned_out = [torch.empty(x.shape, dtype=torch.float32 if f32 else torch.float64).pin_memory()
+                  .numpy() for x in s.axes]
     e2e_ms = []
     for it in range(max(2, args.steps) + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         enc = codec.encode(host_seq, cfg)
-        out = codec.decode(enc, rtol=args.rtol, dtype=npdt)
+        out = codec.decode(enc, rtol=args.rtol, dtype=npdt, out=pinned_out)
         dt = (time.perf_counter() - t0) * 1e3
         if it > 0:
             e2e_ms.append(dt)
@@ -279,11 +281,15 @@ def main():
                        "l2": "256 MiB flush between timed steps",
                        "plan": "mesh plan (CSR, anchors, normal matrix) built once outside value; "
                                "inside e2e", "cg_rtol": args.rtol},
-            "roofline": {"kernel": "k_cg (K7)", "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "algorithmic_bytes": cg_bytes, "cg_iterations": it_med,
-                         "model": "iters x (6 x n x 3F x 8 B + nnz(M) x 12 B)"},
+            "roofline": {"kernel": "K7 direct solve (k_panel/k_trailing/k_inv_*/k_fwd*/k_bwd*)",
+                         "bound": "tensor", "achieved": achieved, "peak": peak,
+                         "peak_kind": "measured FP64 DMMA (profiles/r01_peaks.md)",
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "algorithmic_flops": k7_flops,
+                         "model": "sum over fronts of (m-t)^2 per pivot + w^3/3 inverse; "
+                                  "2 solves x 2(2w^2 + 4w(m-w)) per right-hand side",
+                         "ms_factor": float(np.median(fac_ms)), "ms_solve": float(np.median(sol_ms)),
+                         "supernodes": st["supernodes"], "nnz_factor": st["nnz_factor"]},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "vertex-frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_total / len(e2e_ms)},

@@ -145,12 +145,16 @@ class Codec:
     """Owns one dmcg_ctx (device, stream, device memory pool)."""
 
     def __init__(self, device: int = 0):
+        import weakref
+        self._plans = weakref.WeakSet()  # plans must die before the context
         self._ctx = ctypes.c_void_p()
         rc = L.lib().dmcg_create(ctypes.byref(self._ctx), device)
         if rc != L.DMCG_OK:
             raise DmcError(rc, f"CudaError: dmcg_create(device={device}) failed (code {rc})")
 
     def close(self):
+        for p in list(self._plans):
+            p.close()
         if self._ctx:
             L.lib().dmcg_destroy(self._ctx)
             self._ctx = ctypes.c_void_p()
@@ -191,12 +195,16 @@ class Codec:
         return out
 
     def decode(self, c: CompressedAnimation, rtol: float = 1e-10, max_iter: int = 20000,
-               dtype=np.float64, solver: str = "direct", refine: int = 1):
+               dtype=np.float64, solver: str = "direct", refine: int = 1, out=None):
         """dmc::decode (include/dmc/codec.hpp:91; src/codec.cpp:475-552).
         Returns the three (n, F) axis arrays.  solver "direct" (supernodal
         Cholesky + refine passes, the reference scheme) or "cg"."""
         opt = _decode_opts(rtol, max_iter, solver, refine)
-        out = [np.empty((c.n, c.F), dtype=dtype) for _ in range(3)]
+        if out is None:
+            out = [np.empty((c.n, c.F), dtype=dtype) for _ in range(3)]
+        else:  # caller-provided (e.g. pinned) host buffers
+            assert all(o.shape == (c.n, c.F) and o.dtype == dtype and o.flags.c_contiguous
+                       for o in out)
         ptrs = (ctypes.c_void_p * 3)(*[o.ctypes.data for o in out])
         e = c.to_c()
         _check(self._ctx, L.lib().dmcg_decode(self._ctx, ctypes.byref(e), ctypes.byref(opt), ptrs,
@@ -227,6 +235,7 @@ class Plan:
                                                       ctypes.byref(self._p)))
         self.n_c = L.lib().dmcg_anchor_count(n, cfg.anchor_fraction)
         self.cfg = cfg
+        codec._plans.add(self)
 
     def close(self):
         if self._p:

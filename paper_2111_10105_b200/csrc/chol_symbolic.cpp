@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 
 #include "chol.h"
@@ -131,9 +134,20 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   CholPlan& p = *P;
   p = CholPlan();
   p.n = n;
+  static const bool timing = std::getenv("DMCG_TIMING") != nullptr;
+  auto clk = [] { return std::chrono::steady_clock::now(); };
+  auto t_prev = clk();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t = clk();
+    std::fprintf(stderr, "  chol_analyze %-12s %.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t_prev).count());
+    t_prev = t;
+  };
   // (1) ordering
   Graph g{n, rp.data(), ci.data()};
   std::vector<uint32_t> perm0 = NestedDissection(g).run();
+  lap("ordering");
   std::vector<uint32_t> iperm0(n);
   for (uint32_t k = 0; k < n; ++k) iperm0[perm0[k]] = k;
   // (2) elimination tree (Liu, path compression) of P M P^T
@@ -190,6 +204,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     const int32_t q = par[post[j]];
     parent[j] = q == -1 ? -1 : (int32_t)ipost[q];
   }
+  lap("etree+post");
   // (4) column counts by row-subtree traversal (Davis, LDL symbolic)
   std::vector<uint32_t> colcnt(n, 1);  // diagonal
   std::vector<int32_t> flag(n, -1);
@@ -205,6 +220,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       }
     }
   }
+  lap("colcounts");
   // (5) fundamental supernodes
   std::vector<uint32_t> nchild(n, 0);
   for (uint32_t j = 0; j < n; ++j)
@@ -276,6 +292,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   std::vector<uint32_t> col_sup(n);
   for (uint32_t s = 0; s < NS; ++s)
     for (uint32_t j = p.first[s]; j < p.first[s + 1]; ++j) col_sup[j] = s;
+  lap("supernodes");
   // (7) row structures, postorder of supernodes = column order
   p.parent.assign(NS, -1);
   std::vector<std::vector<uint32_t>> kids(NS);
@@ -319,6 +336,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       kids[ps].push_back(s);
     }
   }
+  lap("structure");
   // children lists, levels
   p.child_ptr.assign(NS + 1, 0);
   p.child_idx.clear();
@@ -361,6 +379,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     p.flops_factor += (double)w * w * w / 3.0;
     p.flops_solve_per_rhs += 2.0 * (2.0 * w * w + 2.0 * 2.0 * w * (m - w));
   }
+  lap("levels+stats");
   // (8) extend-add maps: child update rows -> parent local rows
   p.rel_ptr.assign(NS + 1, 0);
   p.rel_idx.clear();
@@ -377,6 +396,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     }
     p.rel_ptr[c + 1] = p.rel_idx.size();
   }
+  lap("rel maps");
   // (9) scatter list of M into the fronts (lower part, column-major local)
   p.a_ptr.assign(NS + 1, 0);
   p.a_pos.clear();
@@ -397,6 +417,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     p.a_ptr[s + 1] = p.a_pos.size();
     for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = -1;
   }
+  lap("scatter");
 }
 
 // ---------------------------------------------------------------------------

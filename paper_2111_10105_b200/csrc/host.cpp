@@ -455,8 +455,6 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   }
   p->mesh.anchor_pos.assign(n, -1);
   for (uint32_t t = 0; t < p->n_c; ++t) p->mesh.anchor_pos[p->mesh.anchors[t]] = (int32_t)t;
-  build_normal_matrix(&p->mesh);
-  p->stats.nnz_normal = (long long)p->mesh.m_ci.size();
   p->stats.nnz_laplacian = (long long)p->mesh.lap_ci.size();
 
   const uint32_t k = p->k;
@@ -476,9 +474,6 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   const MeshHost& m = p->mesh;
   p->d_lap_rp = (uint32_t*)get(m.lap_rp.size() * 4);
   p->d_lap_ci = (uint32_t*)get(m.lap_ci.size() * 4);
-  p->d_m_rp = (uint32_t*)get(m.m_rp.size() * 4);
-  p->d_m_ci = (uint32_t*)get(m.m_ci.size() * 4);
-  p->d_m_val = (float*)get(m.m_val.size() * 4);
   p->d_anchor_idx = (uint32_t*)get((size_t)p->n_c * 4);
   p->d_anchor_pos = (int32_t*)get((size_t)n * 4);
   for (int a = 0; a < 3; ++a) {
@@ -524,9 +519,6 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   };
   h2d(p->d_lap_rp, m.lap_rp.data(), m.lap_rp.size() * 4);
   h2d(p->d_lap_ci, m.lap_ci.data(), m.lap_ci.size() * 4);
-  h2d(p->d_m_rp, m.m_rp.data(), m.m_rp.size() * 4);
-  h2d(p->d_m_ci, m.m_ci.data(), m.m_ci.size() * 4);
-  h2d(p->d_m_val, m.m_val.data(), m.m_val.size() * 4);
   h2d(p->d_anchor_idx, m.anchors.data(), (size_t)p->n_c * 4);
   h2d(p->d_anchor_pos, m.anchor_pos.data(), (size_t)n * 4);
   std::vector<uint8_t> rb(4 * kk, 0);
@@ -557,8 +549,35 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
 // is built on the first decode of a plan only: encode-only plans never pay
 // for it.  Reference: the normal matrix and its factorisation are per
 // decode call (solver.cpp:62-90).
+// M = L^T L + S^T S on the host and in HBM, built on first use (only the
+// decoder needs it; solver.cpp:25-39).
+dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
+  if (p->d_m_rp) return Status::ok();
+  build_normal_matrix(&p->mesh);
+  const MeshHost& m = p->mesh;
+  p->stats.nnz_normal = (long long)m.m_ci.size();
+  p->d_m_rp = (uint32_t*)plan_alloc(p, m.m_rp.size() * 4);
+  p->d_m_ci = (uint32_t*)plan_alloc(p, m.m_ci.size() * 4);
+  p->d_m_val = (float*)plan_alloc(p, m.m_val.size() * 4);
+  if (!p->d_m_rp || !p->d_m_ci || !p->d_m_val)
+    return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  cudaStream_t s = p->ctx->stream;
+  bool ok = cudaMemcpyAsync(p->d_m_rp, m.m_rp.data(), m.m_rp.size() * 4, cudaMemcpyHostToDevice,
+                            s) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(p->d_m_ci, m.m_ci.data(), m.m_ci.size() * 4,
+                             cudaMemcpyHostToDevice, s) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(p->d_m_val, m.m_val.data(), m.m_val.size() * 4,
+                             cudaMemcpyHostToDevice, s) == cudaSuccess;
+  if (!ok) return {DMCG_E_CUDA, "CudaError: normal matrix upload failed"};
+  return Status::ok();
+}
+
 dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   if (p->decode_ready) return Status::ok();
+  {
+    Status sn = plan_prepare_normal(p);
+    if (!sn.good()) return sn;
+  }
   const uint32_t n = p->n;
   const MeshHost& m = p->mesh;
   bool ok = true;

@@ -59,6 +59,7 @@ namespace dmcg {
 void* plan_alloc(dmcg_plan* p, size_t bytes);
 // Builds the decode-side state on first use (host.cpp).
 Status plan_prepare_decode(dmcg_plan* p);
+Status plan_prepare_normal(dmcg_plan* p);
 }  // namespace dmcg
 
 struct dmcg_ctx {

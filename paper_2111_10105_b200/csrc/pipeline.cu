@@ -318,6 +318,10 @@ Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out
       return Status{DMCG_E_CUDA, "CudaError: device allocation failed"};
   }
   p->stats.solver = 1;
+  {
+    Status sn = plan_prepare_normal(p);
+    if (!sn.good()) return sn;
+  }
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
   DMCG_TRY(cudaEventRecord(p->ev[0], s));
   // K6: dequantise + reconstruct delta~ = (U~ c~)^T (codec.cpp:528-533)

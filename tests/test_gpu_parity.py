@@ -56,7 +56,7 @@ def _oracle_stream_of(g, s):
     return og
 
 
-def check_parity(codec, s, spec, rounds=None, f32_out=False):
+def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3):
     rounds = spec.rounds if rounds is None else rounds
     ec = _cfg(spec, rounds)
     g = codec.encode(s, ec)
@@ -98,7 +98,7 @@ def check_parity(codec, s, spec, rounds=None, f32_out=False):
     xoo = O.decode(o, nthreads=8)
     r_g = O.frame_rms([np.asarray(x, np.float64) for x in s.axes], [x.astype(np.float64) for x in xg])
     r_o = O.frame_rms([np.asarray(x, np.float64) for x in s.axes], xoo)
-    assert abs(r_g.mean() / r_o.mean() - 1) <= 1e-3
+    assert abs(r_g.mean() / r_o.mean() - 1) <= e2e_tol
     return g, o
 
 
@@ -163,7 +163,15 @@ def test_device_plan_matches_dropin(codec):
     for a in range(3):
         assert np.array_equal(out[a].cpu().numpy(), xg[a])
     st = plan.stats()
-    assert st["cg_iterations_max"] > 0 and st["cg_rel_residual_max"] <= 1e-10
+    assert st["solver"] == 0 and st["supernodes"] > 0 and st["ms_factor"] > 0
+    # the CG option reaches the same solution to its tolerance
+    out_cg = [torch.empty_like(t) for t in d]
+    plan.decode_device([t.data_ptr() for t in out_cg], solver="cg", rtol=1e-12)
+    st = plan.stats()
+    assert st["solver"] == 1 and st["cg_rel_residual_max"] <= 1e-12
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
+    for a in range(3):
+        assert np.abs(out_cg[a].cpu().numpy() - xg[a]).max() <= 1e-9 * bbox
 
 
 def test_stream_roundtrip_through_gpu(codec):
@@ -202,7 +210,10 @@ def test_static_animation_degenerate_rows(codec):
     s = _small()
     s.axes = [np.repeat(ax[:, :1], s.F, axis=1).copy() for ax in s.axes]
     spec = synth.Config("static", 4, 5, 12, "f64", None)
-    g, o = check_parity(codec, s, spec, rounds=5)
+    # rank 1: rows 1.. are round-off whose (valid, different) bases on the two
+    # sides dominate the tiny reconstruction error, so only P1-P4 and the
+    # same-stream decode are tight here
+    g, o = check_parity(codec, s, spec, rounds=5, e2e_tol=0.05)
     assert C.rate_exact(g)["q_s"] == O.rate_exact(o)["q_s"]
 
 
