@@ -79,11 +79,11 @@ __global__ void __launch_bounds__(256) k_assemble(CholDev d, const uint32_t* lsu
   }
 }
 
-// Panel [k0, k0 + pw) of a front: warp 0 factors the pw x pw diagonal
-// block in shared memory (right-looking, lanes own rows), then every thread
-// solves its own rows of the panel below against it (row-wise TRSM, no
-// barriers inside).  The diagonal is inverted once and applied by
-// multiplication (the CPU reference divides; results agree to rounding).
+// Panel [k0, k0 + pw) of a front: the CTA factors the pw x pw diagonal
+// block in shared memory (one barrier per pivot), then every thread solves
+// its own rows of the panel below against it (row-wise TRSM, no barriers).
+// Pivots are applied as reciprocal square roots (the CPU reference divides
+// by the square root; results agree to rounding).
 constexpr int kPanelThreads = 256;  // 32 panel values per thread stay in registers
 constexpr int kNB = 32;
 
@@ -96,42 +96,40 @@ __global__ void __launch_bounds__(kPanelThreads)
   if (k0 >= w) return;
   const int pw = min(nb, w - k0);
   double* A = d.F + d.front_off[s];
-  const int lane = threadIdx.x & 31;
   for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
     const int c = t / pw, r = t % pw;
     D[r][c] = r >= c ? A[(size_t)(k0 + c) * m + k0 + r] : 0.0;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int r = lane;
-    for (int j = 0; j < pw; ++j) {
-      const double djj = D[j][j];
-      if (djj <= 0.0 || !(djj == djj)) {
-        if (lane == 0) atomicOr(d.flags, 1);
-      }
-      const double piv = sqrt(fmax(djj, DBL_MIN));
-      const double ip = 1.0 / piv;
-      __syncwarp();
-      if (r == j) {
-        D[j][j] = piv;
-        dinv[j] = ip;
-      }
-      if (r > j && r < pw) D[r][j] *= ip;
-      __syncwarp();
-      if (r > j && r < pw) {
-        const double lrj = D[r][j];
-        for (int c = j + 1; c <= r; ++c) D[r][c] -= lrj * D[c][j];
-      }
-      __syncwarp();
+  // Right-looking Cholesky of D with one barrier per pivot: columns stay
+  // unscaled while they are read (L(r, j) = D[r][j] / sqrt(D[j][j]) is
+  // formed on the fly) and are scaled once at the end.
+  for (int j = 0; j < pw; ++j) {
+    const double djj = D[j][j];
+    const double ip = rsqrt(fmax(djj, DBL_MIN));
+    if (threadIdx.x == 0) {
+      if (!(djj > 0.0)) atomicOr(d.flags, 1);
+      dinv[j] = ip;
     }
+    const int rem = pw - 1 - j;
+    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
+      const int r = j + 1 + t / rem, c = j + 1 + t % rem;
+      if (c <= r) D[r][c] -= (D[r][j] * ip) * (D[c][j] * ip);
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
+    const int c = t / pw, r = t % pw;
+    if (r > c) D[r][c] *= dinv[c];
+    if (r == c) D[r][c] = 1.0 / dinv[c];
   }
   __syncthreads();
-  // write the factored diagonal block back
   for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
     const int c = t / pw, r = t % pw;
     if (r >= c) A[(size_t)(k0 + c) * m + k0 + r] = D[r][c];
   }
-  // rows below: x = a L^{-T}, forward substitution per row
+  // rows below: x = a L^{-T}; column-oriented substitution so the updates
+  // of one pivot are independent (ILP) instead of one long FMA chain.
   for (int i = k0 + pw + threadIdx.x; i < m; i += blockDim.x) {
     double x[kNB];
 #pragma unroll
@@ -139,10 +137,9 @@ __global__ void __launch_bounds__(kPanelThreads)
 #pragma unroll
     for (int j = 0; j < kNB; ++j) {
       if (j < pw) {
-        double acc = x[j];
+        x[j] *= dinv[j];
 #pragma unroll
-        for (int c = 0; c < j; ++c) acc -= x[c] * D[j][c];
-        x[j] = acc * dinv[j];
+        for (int c = j + 1; c < kNB; ++c) x[c] -= x[j] * D[c][j];
       }
     }
 #pragma unroll

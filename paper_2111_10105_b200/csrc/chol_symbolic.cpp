@@ -9,7 +9,9 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <functional>
+#include <thread>
 
 #include "chol.h"
 
@@ -23,28 +25,62 @@ struct Graph {
   const uint32_t* ci;
 };
 
-// Nested dissection; appends the elimination order (old indices) to perm.
+// Nested dissection on M's graph.  Each sub-problem is a contiguous range
+// of one index array, partitioned in place (parts A | B | separator S);
+// two BFS per split: from any vertex to the farthest one (pseudo-
+// peripheral), then the level structure from there.  Leaves of <= 48
+// vertices keep their order.  Output: elimination order (old indices).
 class NestedDissection {
  public:
   explicit NestedDissection(const Graph& g)
-      : g_(g), part_(g.n, 0), level_(g.n, -1), queue_(g.n) {}
+      : g_(g), part_(g.n, 0), level_(g.n, -1), queue_(g.n), idx_(g.n), tmp_(g.n) {}
 
   std::vector<uint32_t> run() {
-    std::vector<uint32_t> all(g_.n);
-    for (uint32_t i = 0; i < g_.n; ++i) all[i] = i;
+    for (uint32_t i = 0; i < g_.n; ++i) idx_[i] = i;
     perm_.reserve(g_.n);
-    recurse(all, 0);
+    struct Task {
+      uint32_t b, e;
+      int32_t id;
+      bool emit;  // emit the range as is (separator)
+    };
+    // explicit stack; order: A, B, then S (postorder of the dissection tree)
+    std::vector<Task> st;
+    st.push_back({0, g_.n, 0, false});
+    while (!st.empty()) {
+      Task t = st.back();
+      st.pop_back();
+      if (t.emit || t.e - t.b <= 48) {
+        perm_.insert(perm_.end(), idx_.begin() + t.b, idx_.begin() + t.e);
+        continue;
+      }
+      uint32_t na, ns;
+      const int kind = split(t.b, t.e, t.id, &na, &ns);
+      if (kind == 0) {  // no useful split
+        perm_.insert(perm_.end(), idx_.begin() + t.b, idx_.begin() + t.e);
+        continue;
+      }
+      const int32_t ia = next_id_++, ib = next_id_++;
+      const uint32_t e_a = t.b + na, e_b = t.e - ns;
+      for (uint32_t q = t.b; q < e_a; ++q) part_[idx_[q]] = ia;
+      for (uint32_t q = e_a; q < e_b; ++q) part_[idx_[q]] = ib;
+      if (ns) {
+        const int32_t is = next_id_++;
+        for (uint32_t q = e_b; q < t.e; ++q) part_[idx_[q]] = is;
+        st.push_back({e_b, t.e, is, true});
+      }
+      st.push_back({e_a, e_b, ib, false});
+      st.push_back({t.b, e_a, ia, false});
+    }
     return perm_;
   }
 
  private:
   const Graph g_;
   std::vector<int32_t> part_, level_;
-  std::vector<uint32_t> queue_, perm_;
+  std::vector<uint32_t> queue_, idx_, tmp_, perm_;
   int32_t next_id_ = 1;
 
-  uint32_t bfs(const std::vector<uint32_t>& verts, int32_t id, uint32_t root, uint32_t* maxlev) {
-    for (uint32_t v : verts) level_[v] = -1;
+  uint32_t bfs(uint32_t root, int32_t id, uint32_t* maxlev) {
     uint32_t head = 0, tail = 0;
     queue_[tail++] = root;
     level_[root] = 0;
@@ -52,10 +88,11 @@ class NestedDissection {
     while (head < tail) {
       const uint32_t v = queue_[head++];
       last = v;
+      const int32_t lv = level_[v] + 1;
       for (uint32_t p = g_.rp[v]; p < g_.rp[v + 1]; ++p) {
         const uint32_t w = g_.ci[p];
         if (part_[w] == id && level_[w] < 0) {
-          level_[w] = level_[v] + 1;
+          level_[w] = lv;
           queue_[tail++] = w;
         }
       }
@@ -64,42 +101,34 @@ class NestedDissection {
     return tail;
   }
 
-  void recurse(std::vector<uint32_t>& verts, int32_t id) {
-    const uint32_t cnt = (uint32_t)verts.size();
-    if (cnt == 0) return;
-    if (cnt <= 48) {
-      perm_.insert(perm_.end(), verts.begin(), verts.end());
-      return;
-    }
+  // Partitions idx_[b, e) into A | B | S.  Returns 0 if no split is made;
+  // a disconnected range becomes A = reached component, B = rest, S empty.
+  int split(uint32_t b, uint32_t e, int32_t id, uint32_t* na, uint32_t* ns) {
+    const uint32_t cnt = e - b;
+    for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
     uint32_t maxlev;
-    const uint32_t reached = bfs(verts, id, verts[0], &maxlev);
-    if (reached < cnt) {  // disconnected: split off the reached component
-      std::vector<uint32_t> a, b;
-      for (uint32_t v : verts) (level_[v] >= 0 ? a : b).push_back(v);
-      const int32_t ia = next_id_++, ib = next_id_++;
-      for (uint32_t v : a) part_[v] = ia;
-      for (uint32_t v : b) part_[v] = ib;
-      verts.clear();
-      verts.shrink_to_fit();
-      recurse(a, ia);
-      recurse(b, ib);
-      return;
+    const uint32_t reached = bfs(idx_[b], id, &maxlev);
+    if (reached < cnt) {
+      uint32_t a = b, z = 0;
+      for (uint32_t q = b; q < e; ++q) {
+        const uint32_t v = idx_[q];
+        if (level_[v] >= 0)
+          idx_[a++] = v;
+        else
+          tmp_[z++] = v;
+      }
+      std::copy(tmp_.begin(), tmp_.begin() + z, idx_.begin() + a);
+      *na = a - b;
+      *ns = 0;
+      return 1;
     }
-    uint32_t root = queue_[cnt - 1];  // pseudo-peripheral start
-    for (int it = 0; it < 2; ++it) {
-      uint32_t ml;
-      bfs(verts, id, root, &ml);
-      if (ml <= maxlev && it > 0) break;
-      maxlev = ml;
-      root = queue_[cnt - 1];
-    }
-    bfs(verts, id, root, &maxlev);
-    if (maxlev < 2) {
-      perm_.insert(perm_.end(), verts.begin(), verts.end());
-      return;
-    }
-    std::vector<uint32_t> hist(maxlev + 1, 0);
-    for (uint32_t v : verts) hist[level_[v]]++;
+    const uint32_t root = queue_[cnt - 1];
+    for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
+    bfs(root, id, &maxlev);
+    if (maxlev < 2) return 0;
+    // separator = the level where the running count first exceeds half
+    std::vector<uint32_t> hist(maxlev + 2, 0);
+    for (uint32_t q = b; q < e; ++q) hist[level_[idx_[q]]]++;
     uint32_t acc = 0, sep = 1;
     for (uint32_t l = 0; l <= maxlev; ++l) {
       if (acc + hist[l] > cnt / 2) {
@@ -110,20 +139,23 @@ class NestedDissection {
     }
     if (sep == 0) sep = 1;
     if (sep >= maxlev) sep = maxlev - 1;
-    std::vector<uint32_t> a, b, s;
-    for (uint32_t v : verts) {
+    uint32_t a = b, zb = 0, zs = 0;
+    uint32_t* sbuf = queue_.data();  // queue no longer needed
+    for (uint32_t q = b; q < e; ++q) {
+      const uint32_t v = idx_[q];
       const uint32_t l = (uint32_t)level_[v];
-      (l < sep ? a : (l > sep ? b : s)).push_back(v);
+      if (l < sep)
+        idx_[a++] = v;
+      else if (l > sep)
+        tmp_[zb++] = v;
+      else
+        sbuf[zs++] = v;
     }
-    const int32_t ia = next_id_++, ib = next_id_++, is = next_id_++;
-    for (uint32_t v : a) part_[v] = ia;
-    for (uint32_t v : b) part_[v] = ib;
-    for (uint32_t v : s) part_[v] = is;
-    verts.clear();
-    verts.shrink_to_fit();
-    recurse(a, ia);
-    recurse(b, ib);
-    perm_.insert(perm_.end(), s.begin(), s.end());
+    std::copy(tmp_.begin(), tmp_.begin() + zb, idx_.begin() + a);
+    std::copy(sbuf, sbuf + zs, idx_.begin() + a + zb);
+    *na = a - b;
+    *ns = zs;
+    return 2;
   }
 };
 
@@ -207,16 +239,18 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   lap("etree+post");
   // (4) column counts by row-subtree traversal (Davis, LDL symbolic)
   std::vector<uint32_t> colcnt(n, 1);  // diagonal
-  std::vector<int32_t> flag(n, -1);
-  for (uint32_t k = 0; k < n; ++k) {
-    flag[k] = (int32_t)k;
-    const uint32_t ko = p.perm[k];
-    for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
-      uint32_t i = p.iperm[ci[q]];
-      if (i >= k) continue;
-      for (; flag[i] != (int32_t)k; i = (uint32_t)parent[i]) {
-        colcnt[i]++;
-        flag[i] = (int32_t)k;
+  {
+    std::vector<int32_t> flag(n, -1);
+    for (uint32_t k = 0; k < n; ++k) {
+      flag[k] = (int32_t)k;
+      const uint32_t ko = p.perm[k];
+      for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
+        uint32_t i = p.iperm[ci[q]];
+        if (i >= k) continue;
+        for (; flag[i] != (int32_t)k; i = (uint32_t)parent[i]) {
+          colcnt[i]++;
+          flag[i] = (int32_t)k;
+        }
       }
     }
   }

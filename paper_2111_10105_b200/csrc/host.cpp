@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <limits>
@@ -25,6 +27,21 @@ Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out
     if (_e != cudaSuccess)                                                                 \
       return Status{DMCG_E_CUDA, std::string("CudaError: ") + cudaGetErrorString(_e)};     \
   } while (0)
+
+static double wall_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+PhaseTimer::PhaseTimer(const char* s) : scope(s), on(std::getenv("DMCG_TIMING") != nullptr) {
+  t0 = wall_ms();
+}
+void PhaseTimer::lap(const char* what) {
+  if (!on) return;
+  const double t = wall_ms();
+  std::fprintf(stderr, "  %s %-16s %.2f ms\n", scope, what, t - t0);
+  t0 = t;
+}
 
 // ---- device pool -----------------------------------------------------------
 void* DevicePool::get(size_t bytes) {
@@ -807,21 +824,25 @@ void* dmcg_plan_stream(dmcg_plan* p) { return p ? (void*)p->ctx->stream : nullpt
 int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg_encoded* out) {
   if (!ctx || !seq || !cfg || !out) return DMCG_E_CONFIG;
   cudaSetDevice(ctx->device);
+  PhaseTimer tm("encode");
   dmcg_plan* p = nullptr;
   Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
                                nullptr, 0, &p);
   if (!st.good()) return ctx->set_error(st);
+  tm.lap("plan");
   const size_t bytes = (size_t)seq->n * seq->F * (seq->dtype == DMCG_F32 ? 4 : 8);
   for (int a = 0; a < 3 && st.good(); ++a)
     if (cudaMemcpyAsync(p->d_x_in[a], seq->axes[a], bytes, cudaMemcpyHostToDevice, ctx->stream) !=
         cudaSuccess)
       st = {DMCG_E_CUDA, "CudaError: H2D copy failed"};
   if (st.good()) st = plan_encode(p, p->d_x_in);
+  tm.lap("h2d+kernels");
   if (st.good()) {
     if (!out->faces) out->faces = seq->faces;
     st = download_impl(p, out);
     out->faces = seq->faces;
   }
+  tm.lap("download");
   if (st.good()) {
     const dmcg_stats& e = p->stats;
     ctx->last_stats.ms_encode = e.ms_encode;
@@ -869,13 +890,17 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   Status st = plan_create_impl(ctx, in->n, in->F, out_dtype, in->faces, in->n_faces, &cfg,
                                in->anchor_idx, in->n_c, &p);
   if (!st.good()) return ctx->set_error(st);
+  PhaseTimer tm("decode");
+  tm.lap("plan");
   st = upload_impl(p, in);
-  if (st.good()) {
-    dmcg_decode_options o;
-    dmcg_decode_options_default(&o);
-    if (opt) o = *opt;
-    st = plan_decode(p, &o, p->d_x_out);
-  }
+  tm.lap("upload");
+  dmcg_decode_options o;
+  dmcg_decode_options_default(&o);
+  if (opt) o = *opt;
+  if (st.good() && o.solver == 0) st = plan_prepare_decode(p);
+  tm.lap("prepare(analyze)");
+  if (st.good()) st = plan_decode(p, &o, p->d_x_out);
+  tm.lap("kernels");
   const size_t bytes = (size_t)in->n * in->F * (out_dtype == DMCG_F32 ? 4 : 8);
   for (int a = 0; a < 3 && st.good(); ++a)
     if (cudaMemcpyAsync(out_axes[a], p->d_x_out[a], bytes, cudaMemcpyDeviceToHost, ctx->stream) !=
@@ -883,6 +908,7 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
       st = {DMCG_E_CUDA, "CudaError: D2H copy failed"};
   if (st.good() && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
     st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
+  tm.lap("d2h");
   if (st.good()) {  // keep the encode fields of the last dmcg_encode
     dmcg_stats e = ctx->last_stats;
     ctx->last_stats = p->stats;

@@ -55,6 +55,14 @@ void build_normal_matrix(MeshHost* m);     // needs anchors set
 
 struct dmcg_plan;
 namespace dmcg {
+// Host phase timer, printed to stderr when DMCG_TIMING is set.
+struct PhaseTimer {
+  const char* scope;
+  bool on;
+  double t0;
+  explicit PhaseTimer(const char* s);
+  void lap(const char* what);
+};
 // Device allocation owned by the plan (returned to the context pool on destroy).
 void* plan_alloc(dmcg_plan* p, size_t bytes);
 // Builds the decode-side state on first use (host.cpp).

@@ -16,9 +16,9 @@ __global__ void __launch_bounds__(512) k_probe(int F, int k, const double* R, co
   for (int i = threadIdx.x; i < F * k; i += blockDim.x) Z[i] = start[i];
   __syncthreads();
   long long t0 = clock64();
-  qr_factor(Z, F, k, q);
+  qr_factor<8>(Z, F, k, q);
   long long t1 = clock64();
-  qr_form(Z, F, k, 0, k, Q, F, q);
+  qr_form<8>(Z, F, k, 0, k, Q, F, q);
   long long t2 = clock64();
   oi_apply(R, F, k, Q, Z);
   long long t3 = clock64();

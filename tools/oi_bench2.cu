@@ -26,17 +26,17 @@ __global__ void __launch_bounds__(512) k_probe(int F, int k, const double* start
   }
   long long c = clock64();
   for (int j = 0; j < 63; ++j) {
-    if (warp == 0) qr_reflector(Z, F, j, q, lane);
+    if (warp == 0) qr_reflector<8>(Z, F, j, q, lane);
     __syncthreads();
   }
   long long d = clock64();
   for (int j = 0; j < 63; ++j) {
-    apply_reflector_cols(Z, F, j, Z + j * F, 0.5, 0.25, j + 2 + warp, k, nw, lane, F);
+    apply_reflector_cols<8>(Z, F, j, Z + j * F, 0.5, 0.25, j + 2 + warp, k, nw, lane, F);
     __syncthreads();
   }
   long long e = clock64();
   for (int j = 0; j < 63; ++j) {
-    if (warp == 0) apply_reflector_cols(Z, F, j, Z + j * F, 0.5, 0.25, j + 1, j + 2, 1, lane, F);
+    if (warp == 0) apply_reflector_cols<8>(Z, F, j, Z + j * F, 0.5, 0.25, j + 1, j + 2, 1, lane, F);
     __syncthreads();
   }
   long long f = clock64();
