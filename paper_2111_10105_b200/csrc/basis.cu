@@ -536,19 +536,185 @@ __device__ void oi_apply(const double* __restrict__ R, int F, int k, P Q, P Z) {
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Blocked (compact-WY) Householder QR.  Columns are factored in panels of
+// QNB: only the panel sees per-column steps (one barrier each); the rest of
+// the matrix and the formation of Q are updated with small DMMA GEMMs,
+//   Y <- (I - V T V^T)^T Y,   Q <- (I - V T V^T) Q,
+// T being the LAPACK dlarft forward/columnwise triangular factor.  Scratch
+// (global, L1-resident): T of every panel, W (QNB x ncols), G (QNB x QNB).
+// ---------------------------------------------------------------------------
+constexpr int QNB = 16;
+
+// CTA GEMM on the FP64 tensor pipe with functor operands:
+//   for m < M, n < N:  st(m, n, sum_k la(m, k) * lb(k, n))
+template <class LA, class LB, class ST>
+__device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const ST& st) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mt = (M + 7) / 8, nt = (N + 31) / 32;
+  for (int t = warp; t < mt * nt; t += nw) {
+    const int m0 = (t % mt) * 8, n0 = (t / mt) * 32;
+    double acc[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = 0.0;
+    const int ma = m0 + (lane >> 2);
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int ka = k0 + (lane & 3);
+      const double a = (ma < M && ka < K) ? la(ma, ka) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int nb = n0 + u * 8 + (lane >> 2);
+        const double b = (nb < N && ka < K) ? lb(ka, nb) : 0.0;
+        dmma884(acc[u], a, b);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int nc = n0 + u * 8 + (lane & 3) * 2 + e;
+        if (ma < M && nc < N) st(ma, nc, acc[u][e]);
+      }
+  }
+  __syncthreads();
+}
+
+// V(g, i) of the panel starting at column c0, g counted from row c0: unit
+// diagonal, zero above it, the stored (scaled) reflector below.
+template <typename P>
+struct PanelV {
+  P Z;
+  int m, c0;
+  __device__ __forceinline__ double operator()(int g, int i) const {
+    return g < i ? 0.0 : (g == i ? 1.0 : Z[(c0 + i) * m + c0 + g]);
+  }
+};
+
+// Unblocked factorisation of the panel columns [c0, ce), one barrier per column.
+template <int MAXR, typename P>
+__device__ void panel_factor(P Z, int m, int c0, int ce, QrShared& q) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (warp == 0) qr_reflector<MAXR>(Z, m, c0, q, lane);
+  __syncthreads();
+  for (int j = c0; j < ce; ++j) {
+    const double tj = q.tau[j], rj = q.rinv[j];
+    if (j > c0) qr_scale(Z, m, j - 1, q);
+    if (warp == 0 && j + 1 < ce) {
+      if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 1, j + 2, 1, lane, m);
+      qr_reflector<MAXR>(Z, m, j + 1, q, lane);
+    }
+    if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 2 + warp, ce, nw, lane, m);
+    __syncthreads();
+  }
+  qr_scale(Z, m, ce - 1, q);
+  __syncthreads();
+}
+
+// T (row-major QNB x QNB, upper) of the panel [c0, c0+pb): T(i,i) = tau_i,
+// T(0:i, i) = -tau_i T(0:i, 0:i) (V(:, 0:i)^T v_i).
+template <typename P>
+__device__ void panel_T(P Z, int m, int c0, int pb, const QrShared& q, double* T, double* G) {
+  PanelV<P> V{Z, m, c0};
+  cta_gemm(pb, pb, m - c0, [&](int a, int g) { return V(g, a); }, V,
+           [&](int a, int b, double v) { G[a * QNB + b] = v; });
+  if (threadIdx.x < 32) {
+    const int j = threadIdx.x;
+    for (int i = 0; i < pb; ++i) {
+      const double ti = q.tau[c0 + i];
+      if (j < i) {
+        double acc = 0.0;
+        for (int l = j; l < i; ++l) acc += T[j * QNB + l] * G[l * QNB + i];
+        T[j * QNB + i] = -ti * acc;
+      }
+      if (j == i) T[i * QNB + i] = ti;
+      if (j > i) T[j * QNB + i] = 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+template <int MAXR, typename P>
+__device__ void bqr_factor(P Z, int m, int p, QrShared& q, double* scr) {
+  const int pe = p < m ? p : m;
+  double* G = scr;                 // QNB x QNB
+  double* W = G + QNB * QNB;       // QNB x p
+  double* Ts = W + QNB * p;        // T of every panel
+  for (int c0 = 0; c0 < pe; c0 += QNB) {
+    const int pb = min(QNB, pe - c0);
+    panel_factor<MAXR>(Z, m, c0, c0 + pb, q);
+    double* T = Ts + (c0 / QNB) * QNB * QNB;
+    panel_T(Z, m, c0, pb, q, T, G);
+    const int rem = p - (c0 + pb);
+    if (rem <= 0) continue;
+    PanelV<P> V{Z, m, c0};
+    P Y = Z + (c0 + pb) * m + c0;  // rows c0.., columns c0+pb..
+    // W = V^T Y
+    cta_gemm(pb, rem, m - c0, [&](int i, int g) { return V(g, i); },
+             [&](int g, int c) { return Y[c * m + g]; }, [&](int i, int c, double v) { W[i * rem + c] = v; });
+    // W <- T^T W  (row i needs rows l <= i: descending in place)
+    for (int c = threadIdx.x; c < rem; c += blockDim.x)
+      for (int i = pb - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int l = 0; l <= i; ++l) acc += T[l * QNB + i] * W[l * rem + c];
+        W[i * rem + c] = acc;
+      }
+    __syncthreads();
+    // Y -= V W
+    cta_gemm(m - c0, rem, pb, V, [&](int i, int c) { return W[i * rem + c]; },
+             [&](int g, int c, double v) { Y[c * m + g] -= v; });
+  }
+}
+
+// Qout (m x ncols, leading dimension ldq) = H_0 ... H_{pe-1} [e_cid ...].
+template <typename PZ, typename PQ>
+__device__ void bqr_form(PZ Z, int m, int p, int cid, int ncols, PQ Qo, int ldq, double* scr) {
+  const int pe = p < m ? p : m;
+  double* W = scr + QNB * QNB;
+  const double* Ts = W + QNB * (p > ncols ? p : ncols);
+  for (int t = threadIdx.x; t < m * ncols; t += blockDim.x) {
+    const int c = t / m, r = t % m;
+    Qo[c * ldq + r] = (r == cid + c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int npan = (pe + QNB - 1) / QNB;
+  for (int pi = npan - 1; pi >= 0; --pi) {
+    const int c0 = pi * QNB, pb = min(QNB, pe - c0);
+    const double* T = Ts + pi * QNB * QNB;
+    PanelV<PZ> V{Z, m, c0};
+    // columns whose rows >= c0 are still zero are untouched (thin Q: c < c0)
+    const int cs = (cid == 0) ? (c0 < ncols ? c0 : ncols) : 0;
+    const int nc = ncols - cs;
+    if (nc <= 0) continue;
+    PQ Y = Qo + cs * ldq + c0;
+    cta_gemm(pb, nc, m - c0, [&](int i, int g) { return V(g, i); },
+             [&](int g, int c) { return Y[c * ldq + g]; }, [&](int i, int c, double v) { W[i * nc + c] = v; });
+    // W <- T W  (row i needs rows l >= i: ascending in place)
+    for (int c = threadIdx.x; c < nc; c += blockDim.x)
+      for (int i = 0; i < pb; ++i) {
+        double acc = 0.0;
+        for (int l = i; l < pb; ++l) acc += T[i * QNB + l] * W[l * nc + c];
+        W[i * nc + c] = acc;
+      }
+    __syncthreads();
+    cta_gemm(m - c0, nc, pb, V, [&](int i, int c) { return W[i * nc + c]; },
+             [&](int g, int c, double v) { Y[c * ldq + g] -= v; });
+  }
+}
+
 template <int MAXR, typename P>
 __device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
                         const double* __restrict__ start, P Z, P Q, double* Qo, double* H,
-                        QrShared& q) {
+                        QrShared& q, double* scr) {
   const int Fk = F * k;
   for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = start[t];
   __syncthreads();
-  qr_factor<MAXR>(Z, F, k, q);
-  qr_form<MAXR>(Z, F, k, 0, k, Q, F, q);
+  bqr_factor<MAXR>(Z, F, k, q, scr);
+  bqr_form(Z, F, k, 0, k, Q, F, scr);
   for (int r = 0; r < rounds; ++r) {
     oi_apply(R, F, k, Q, Z);
-    qr_factor<MAXR>(Z, F, k, q);
-    qr_form<MAXR>(Z, F, k, 0, k, Q, F, q);
+    bqr_factor<MAXR>(Z, F, k, q, scr);
+    bqr_form(Z, F, k, 0, k, Q, F, scr);
   }
   // Rayleigh-Ritz: H = Q^T (R Q), symmetrised; Q out.
   oi_apply(R, F, k, Q, Z);
@@ -568,37 +734,42 @@ __device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
 template <bool SMEM, int MAXR>
 __global__ void __launch_bounds__(kOiThreads)
     k_oi_fused(int F, int k, int rounds, const double* __restrict__ Rall,
-               const double* __restrict__ start, double* Qall, double* Hall, double* work) {
+               const double* __restrict__ start, double* Qall, double* Hall, double* work,
+               double* scr_all, size_t scr_stride) {
   extern __shared__ double dyn[];
   __shared__ QrShared q;
   const int b = blockIdx.x;
   const size_t Fk = (size_t)F * k;
   const double* R = Rall + (size_t)b * F * F;
+  double* scr = scr_all + b * scr_stride;
   if (SMEM)
-    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Fk, Qall + b * Fk, Hall + (size_t)b * k * k, q);
+    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Fk, Qall + b * Fk,
+                  Hall + (size_t)b * k * k, q, scr);
   else
-    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Fk, work + b * 2 * Fk + Fk, Qall + b * Fk,
-            Hall + (size_t)b * k * k, q);
+    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Fk, work + b * 2 * Fk + Fk,
+                  Qall + b * Fk, Hall + (size_t)b * k * k, q, scr);
 }
 
 // Completion: columns k..F-1 of the full Householder Q of U_k (F x k, the
 // first k columns of U), written straight into U.
 template <bool SMEM, int MAXR>
-__global__ void __launch_bounds__(kOiThreads) k_complete(int F, int k, double* Uall, double* work) {
+__global__ void __launch_bounds__(kOiThreads)
+    k_complete(int F, int k, double* Uall, double* work, double* scr_all, size_t scr_stride) {
   extern __shared__ double dyn[];
   __shared__ QrShared q;
   const int b = blockIdx.x;
   const int Fk = F * k;
   double* Z = SMEM ? dyn : work + (size_t)b * Fk;
   double* U = Uall + (size_t)b * F * F;
+  double* scr = scr_all + b * scr_stride;
   for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = U[t];
   __syncthreads();
   if (SMEM) {
-    qr_factor<MAXR>(dyn, F, k, q);
-    qr_form<MAXR>(dyn, F, k, k, F - k, U + Fk, F, q);
+    bqr_factor<MAXR>(dyn, F, k, q, scr);
+    bqr_form(dyn, F, k, k, F - k, U + Fk, F, scr);
   } else {
-    qr_factor<MAXR>(Z, F, k, q);
-    qr_form<MAXR>(Z, F, k, k, F - k, U + Fk, F, q);
+    bqr_factor<MAXR>(Z, F, k, q, scr);
+    bqr_form(Z, F, k, k, F - k, U + Fk, F, scr);
   }
 }
 
@@ -658,49 +829,60 @@ static cudaError_t set_smem_attr(const void* fn, size_t bytes) {
 
 constexpr size_t kBasisSmemMax = 200 * 1024;  // + ~17 KB static QrShared <= 227 KB
 
+size_t qr_scratch_doubles(int F, int k) {
+  const int npan = (k + QNB - 1) / QNB;
+  return (size_t)QNB * QNB + (size_t)QNB * (F > k ? F : k) + (size_t)npan * QNB * QNB + 64;
+}
+
 template <int MAXR>
 static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                  const double* R, const double* start, double* Q, double* H,
-                                 double* work) {
+                                 double* work, double* scr) {
   const size_t smem = (size_t)2 * F * k * sizeof(double);
+  const size_t ss = qr_scratch_doubles(F, k);
   if (smem <= kBasisSmemMax) {
     cudaError_t e = set_smem_attr((const void*)k_oi_fused<true, MAXR>, smem);
     if (e != cudaSuccess) return e;
-    k_oi_fused<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work);
+    k_oi_fused<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work,
+                                                            scr, ss);
   } else {
-    k_oi_fused<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, rounds, R, start, Q, H, work);
+    k_oi_fused<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, rounds, R, start, Q, H, work, scr,
+                                                          ss);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
-                            const double* start, double* Q, double* H, double* work) {
+                            const double* start, double* Q, double* H, double* work, double* scr) {
   if (F > 512) return cudaErrorInvalidValue;
-  if (F <= 64) return oi_fused_impl<2>(s, nbatch, F, k, rounds, R, start, Q, H, work);
-  if (F <= 128) return oi_fused_impl<4>(s, nbatch, F, k, rounds, R, start, Q, H, work);
-  if (F <= 256) return oi_fused_impl<8>(s, nbatch, F, k, rounds, R, start, Q, H, work);
-  return oi_fused_impl<16>(s, nbatch, F, k, rounds, R, start, Q, H, work);
+  if (F <= 64) return oi_fused_impl<2>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);
+  if (F <= 128) return oi_fused_impl<4>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);
+  if (F <= 256) return oi_fused_impl<8>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);
+  return oi_fused_impl<16>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);
 }
 
 template <int MAXR>
-static cudaError_t complete_impl(cudaStream_t s, int nbatch, int F, int k, double* U, double* work) {
+static cudaError_t complete_impl(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
+                                 double* scr) {
   const size_t smem = (size_t)F * k * sizeof(double);
+  const size_t ss = qr_scratch_doubles(F, k);
   if (smem <= kBasisSmemMax) {
     cudaError_t e = set_smem_attr((const void*)k_complete<true, MAXR>, smem);
     if (e != cudaSuccess) return e;
-    k_complete<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, U, work);
+    k_complete<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, U, work, scr, ss);
   } else {
-    k_complete<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, U, work);
+    k_complete<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, U, work, scr, ss);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work) {
+cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
+                            double* scr) {
   if (F > 512) return cudaErrorInvalidValue;
-  if (F <= 64) return complete_impl<2>(s, nbatch, F, k, U, work);
-  if (F <= 128) return complete_impl<4>(s, nbatch, F, k, U, work);
-  if (F <= 256) return complete_impl<8>(s, nbatch, F, k, U, work);
-  return complete_impl<16>(s, nbatch, F, k, U, work);
+  if (F <= 64) return complete_impl<2>(s, nbatch, F, k, U, work, scr);
+  if (F <= 128) return complete_impl<4>(s, nbatch, F, k, U, work, scr);
+  if (F <= 256) return complete_impl<8>(s, nbatch, F, k, U, work, scr);
+  return complete_impl<16>(s, nbatch, F, k, U, work, scr);
 }
 
 cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count) {

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "kernels.h"
 
 namespace dmcg {
 
@@ -510,6 +511,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_tau = (double*)get(3 * (size_t)F * 8);
   p->d_H = (double*)get(3 * 2 * (size_t)F2 * F2 * 8);
   p->d_V = (double*)get(3 * FF * 8);
+  p->d_qr_scr = (double*)get(3 * dmcg::qr_scratch_doubles((int)F, (int)kk) * 8);
   p->d_w = (double*)get(3 * (size_t)F * 8);
   p->d_start = (double*)get(3 * (size_t)F * kk * 8);
   p->d_C = (double*)get(3 * kk * std::max<size_t>(n, kk) * 8);

@@ -51,9 +51,12 @@ cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H);
 // x {Z = R Q; Q = qr(Z)}, then H = Q^T R Q (symmetrised).  work: nbatch *
 // 2 F k doubles (used when the pair does not fit in shared memory).
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
-                            const double* start, double* Q, double* H, double* work);
+                            const double* start, double* Q, double* H, double* work, double* scr);
 // U[:, k:F] = columns k..F-1 of the full Householder Q of U[:, :k].
-cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work);
+cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
+                            double* scr);
+// Per-axis scratch (doubles) of the blocked QR used by the two kernels above.
+size_t qr_scratch_doubles(int F, int k);
 cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count);
 
 // ---- decode.cu ------------------------------------------------------------

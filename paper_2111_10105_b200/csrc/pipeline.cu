@@ -156,7 +156,8 @@ Status basis(dmcg_plan* p) {
   // Q0 = qr(start); rounds x {Z = R Q; Q = qr(Z)}; H = Q^T R Q — one fused
   // kernel, one CTA per axis (basis.cu k_oi_fused).
   double* H = p->d_C;  // k x k scratch (coefficient buffer is free here)
-  DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H));
+  DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H,
+                                  p->d_qr_scr));
   DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
   double* Ws = p->d_Z;  // k x k sorted Ritz vectors (Z is free)
   DMCG_TRY(launch_sort_basis(s, 3, k, k, p->d_V, p->d_w, Ws, (long)k * k, p->d_evals, F));
@@ -166,7 +167,7 @@ Status basis(dmcg_plan* p) {
   DMCG_TRY(launch_gemm(s, 3, F, k, k, 1, lQm, lW, StoreStrided{p->d_U, FF, 1L, (long)F}));
   DMCG_TRY(launch_canon_signs(s, 3, F, 0, k, p->d_U, FF));
   // Completion to F x F: columns k..F-1 of the full Householder Q of U_k.
-  DMCG_TRY(launch_complete(s, 3, F, k, p->d_U, p->d_H));
+  DMCG_TRY(launch_complete(s, 3, F, k, p->d_U, p->d_H, p->d_qr_scr));
   DMCG_TRY(launch_canon_signs(s, 3, F, k, F - k, p->d_U, FF));
   for (int a = 0; a < 3; ++a)
     DMCG_TRY(launch_fill_zero(s, p->d_evals + (long)a * F + k, F - k));
