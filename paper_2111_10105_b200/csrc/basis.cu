@@ -115,64 +115,81 @@ __global__ void __launch_bounds__(kBasisThreads)
   }
 }
 
-// Round-robin pairing (identical to oracle rr_pair).
-__device__ __forceinline__ void rr_pair(int m2, int s, int i, int* p, int* q) {
-  const int r = m2 - 1;
-  int a, bb;
-  if (i == 0) {
-    a = 0;
-    bb = (s + r - 1) % r + 1;
-  } else {
-    a = (i + s - 1) % r + 1;
-    bb = (r - i + s - 1) % r + 1;
-  }
-  *p = a < bb ? a : bb;
-  *q = a < bb ? bb : a;
-}
-
 // Parallel (round-robin) cyclic Jacobi.  Every step applies m2/2 disjoint
-// rotations at once; each 2x2 block of A is transformed independently, so
-// the arithmetic per element equals the sequential oracle's.
-__global__ void __launch_bounds__(kBasisThreads)
+// rotations at once; each 2x2 block of A is transformed independently.  A
+// lives in shared memory with an odd leading dimension (m2 + 1: the 2x2
+// block gathers of a warp hit distinct banks).  The eigenvector rows are
+// split over gridDim.y CTAs per matrix: each CTA repeats the (cheap,
+// deterministic) A updates and rotates only its slice of V rows, so no
+// inter-CTA traffic is needed.  a_smem = 0 keeps A and V in `work`
+// (gridDim.y must then be 1).
+constexpr int kJacThreads = 512;
+
+__global__ void __launch_bounds__(kJacThreads)
     k_jacobi(int m, const double* __restrict__ Aall, double* work, double* Vall, double* wall,
-             int* flags, int use_smem) {
+             int* flags, int a_smem, int vrows) {
   extern __shared__ double dyn[];
   __shared__ double cs[256], sn[256], tn[256];
   __shared__ int P[256], Qi[256];
-  __shared__ unsigned char act[256];
-  __shared__ int s_rot;
   __shared__ double red[33];
-  const int b = blockIdx.x;
-  const int m2 = m + (m & 1), h = m2 / 2;
-  double* A = use_smem ? dyn : work + (size_t)b * 2 * m2 * m2;
-  double* V = A + (size_t)m2 * m2;
-  const double* Ain = Aall + (size_t)b * m * m;
-  const int tid = threadIdx.x;
-  double part = 0.0;
-  for (long t = tid; t < (long)m2 * m2; t += blockDim.x) {
-    const int c = (int)(t / m2), r = (int)(t % m2);
-    const double v = (r < m && c < m) ? Ain[(size_t)c * m + r] : 0.0;
-    A[t] = v;
-    V[t] = (r == c) ? 1.0 : 0.0;
-    part += v * v;
+  const int b = blockIdx.x, sp = blockIdx.y;
+  const int m2 = m + (m & 1), h = m2 / 2, ld = m2 + 1, rr = m2 - 1;
+  const int r0 = sp * vrows, r1 = min(m2, r0 + vrows), nr = r1 - r0;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  double* A;
+  double* V;  // V(c, r) = V[c * ldv + r - r0]
+  int ldv;
+  if (a_smem) {
+    A = dyn;
+    V = dyn + (size_t)m2 * ld;
+    ldv = nr;
+  } else {
+    A = work + (size_t)b * 2 * m2 * ld;
+    V = A + (size_t)m2 * ld;
+    ldv = m2;
   }
+  const double* Ain = Aall + (size_t)b * m * m;
+  double part = 0.0;
+  for (int c = 0; c < m2; ++c)
+    for (int r = tid; r < m2; r += NT) {
+      const double v = (r < m && c < m) ? Ain[(size_t)c * m + r] : 0.0;
+      A[c * ld + r] = v;
+      part += v * v;
+    }
+  for (int c = 0; c < m2; ++c)
+    for (int r = r0 + tid; r < r1; r += NT) V[c * ldv + r - r0] = (r == c) ? 1.0 : 0.0;
   const double fro = sqrt(block_sum(part, red));
   const double abs_thresh = fro * 1e-22 + DBL_MIN;
+  // per-thread task cursors (square h x h for A blocks, h x nr for V rows)
+  const int da = NT / h, db = NT % h;
+  const int dva = nr > 0 ? NT / nr : 0, dvr = nr > 0 ? NT % nr : 0;
   bool converged = (m2 <= 1);
   for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
-    if (tid == 0) s_rot = 0;
-    __syncthreads();
+    int any = 0;
     for (int s = 0; s + 1 < m2; ++s) {
-      for (int i = tid; i < h; i += blockDim.x) {
-        int p, q;
-        rr_pair(m2, s, i, &p, &q);
+      int on = 0;
+      for (int i = tid; i < h; i += NT) {
+        int x, y;
+        if (i == 0) {
+          x = 0;
+          y = s + rr - 1;
+          if (y >= rr) y -= rr;
+          ++y;
+        } else {
+          x = i + s - 1;
+          if (x >= rr) x -= rr;
+          ++x;
+          y = rr - i + s - 1;
+          if (y >= rr) y -= rr;
+          ++y;
+        }
+        const int p = x < y ? x : y, q = x < y ? y : x;
         P[i] = p;
         Qi[i] = q;
-        const double app = A[(size_t)p * m2 + p], aqq = A[(size_t)q * m2 + q];
-        const double apq = A[(size_t)q * m2 + p];
+        const double app = A[p * ld + p], aqq = A[q * ld + q];
+        const double apq = A[q * ld + p];
         const double rel = 1e-17 * sqrt(fabs(app) * fabs(aqq));
         const double thresh = rel > abs_thresh ? rel : abs_thresh;
-        unsigned char on = 0;
         double c = 1.0, sv = 0.0, tt = 0.0;
         if (fabs(apq) > thresh) {
           const double theta = (aqq - app) / (2.0 * apq);
@@ -180,70 +197,87 @@ __global__ void __launch_bounds__(kBasisThreads)
             tt = 0.5 / theta;
           else
             tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = 1.0 / sqrt(tt * tt + 1.0);
+          c = rsqrt(tt * tt + 1.0);
           sv = tt * c;
           on = 1;
-          atomicAdd(&s_rot, 1);
         }
         cs[i] = c;
         sn[i] = sv;
         tn[i] = tt;
-        act[i] = on;
       }
-      __syncthreads();
-      for (int t = tid; t < h * h; t += blockDim.x) {
-        const int a = t / h, bb = t % h;
-        if (bb < a) continue;
-        const int p1 = P[a], q1 = Qi[a], p2 = P[bb], q2 = Qi[bb];
-        if (a == bb) {
-          if (act[a]) {
-            const double apq = A[(size_t)q1 * m2 + p1];
-            A[(size_t)p1 * m2 + p1] = A[(size_t)p1 * m2 + p1] - tn[a] * apq;
-            A[(size_t)q1 * m2 + q1] = A[(size_t)q1 * m2 + q1] + tn[a] * apq;
-            A[(size_t)q1 * m2 + p1] = 0.0;
-            A[(size_t)p1 * m2 + q1] = 0.0;
+      if (!__syncthreads_or(on)) continue;  // nothing to rotate at this step
+      any = 1;
+      {
+        int a = tid / h, bb = tid % h;
+        for (; a < h; a += da, bb += db) {
+          if (bb >= h) {
+            bb -= h;
+            ++a;
+            if (a >= h) break;
           }
-          continue;
+          if (bb < a) continue;
+          const int p1 = P[a], q1 = Qi[a];
+          if (a == bb) {
+            const double t = tn[a];
+            if (t != 0.0) {
+              const double apq = A[q1 * ld + p1];
+              A[p1 * ld + p1] = A[p1 * ld + p1] - t * apq;
+              A[q1 * ld + q1] = A[q1 * ld + q1] + t * apq;
+              A[q1 * ld + p1] = 0.0;
+              A[p1 * ld + q1] = 0.0;
+            }
+            continue;
+          }
+          const double sa = sn[a], sb = sn[bb];
+          if (sa == 0.0 && sb == 0.0) continue;
+          const int p2 = P[bb], q2 = Qi[bb];
+          const double ca = cs[a], cb = cs[bb];
+          const double b00 = A[p2 * ld + p1], b01 = A[q2 * ld + p1];
+          const double b10 = A[p2 * ld + q1], b11 = A[q2 * ld + q1];
+          const double r00 = ca * b00 - sa * b10, r01 = ca * b01 - sa * b11;
+          const double r10 = sa * b00 + ca * b10, r11 = sa * b01 + ca * b11;
+          const double n00 = cb * r00 - sb * r01, n01 = sb * r00 + cb * r01;
+          const double n10 = cb * r10 - sb * r11, n11 = sb * r10 + cb * r11;
+          A[p2 * ld + p1] = n00;
+          A[p1 * ld + p2] = n00;
+          A[q2 * ld + p1] = n01;
+          A[p1 * ld + q2] = n01;
+          A[p2 * ld + q1] = n10;
+          A[q1 * ld + p2] = n10;
+          A[q2 * ld + q1] = n11;
+          A[q1 * ld + q2] = n11;
         }
-        if (!act[a] && !act[bb]) continue;
-        const double ca = cs[a], sa = sn[a], cb = cs[bb], sb = sn[bb];
-        const double b00 = A[(size_t)p2 * m2 + p1], b01 = A[(size_t)q2 * m2 + p1];
-        const double b10 = A[(size_t)p2 * m2 + q1], b11 = A[(size_t)q2 * m2 + q1];
-        const double r00 = ca * b00 - sa * b10, r01 = ca * b01 - sa * b11;
-        const double r10 = sa * b00 + ca * b10, r11 = sa * b01 + ca * b11;
-        const double n00 = cb * r00 - sb * r01, n01 = sb * r00 + cb * r01;
-        const double n10 = cb * r10 - sb * r11, n11 = sb * r10 + cb * r11;
-        A[(size_t)p2 * m2 + p1] = n00;
-        A[(size_t)p1 * m2 + p2] = n00;
-        A[(size_t)q2 * m2 + p1] = n01;
-        A[(size_t)p1 * m2 + q2] = n01;
-        A[(size_t)p2 * m2 + q1] = n10;
-        A[(size_t)q1 * m2 + p2] = n10;
-        A[(size_t)q2 * m2 + q1] = n11;
-        A[(size_t)q1 * m2 + q2] = n11;
       }
-      for (int t = tid; t < h * m2; t += blockDim.x) {
-        const int a = t / m2, r = t % m2;
-        if (!act[a]) continue;
-        double* vp = V + (size_t)P[a] * m2;
-        double* vq = V + (size_t)Qi[a] * m2;
-        const double x = vp[r], y = vq[r];
-        vp[r] = cs[a] * x - sn[a] * y;
-        vq[r] = sn[a] * x + cs[a] * y;
+      if (nr > 0) {
+        int a = tid / nr, r = tid % nr;
+        for (; a < h; a += dva, r += dvr) {
+          if (r >= nr) {
+            r -= nr;
+            ++a;
+            if (a >= h) break;
+          }
+          const double sa = sn[a];
+          if (sa == 0.0) continue;
+          const double ca = cs[a];
+          double* vp = V + P[a] * ldv;
+          double* vq = V + Qi[a] * ldv;
+          const double x = vp[r], y = vq[r];
+          vp[r] = ca * x - sa * y;
+          vq[r] = sa * x + ca * y;
+        }
       }
       __syncthreads();
     }
-    converged = (s_rot == 0);
-    __syncthreads();
+    converged = !any;
   }
   double* Vo = Vall + (size_t)b * m * m;
-  double* wo = wall + (size_t)b * m;
-  for (long t = tid; t < (long)m * m; t += blockDim.x) {
-    const int c = (int)(t / m), r = (int)(t % m);
-    Vo[t] = V[(size_t)c * m2 + r];
+  for (int c = 0; c < m; ++c)
+    for (int r = r0 + tid; r < min(r1, m); r += NT) Vo[(size_t)c * m + r] = V[c * ldv + r - r0];
+  if (sp == 0) {
+    double* wo = wall + (size_t)b * m;
+    for (int j = tid; j < m; j += NT) wo[j] = A[j * ld + j];
+    if (!converged && tid == 0) atomicOr(flags, 1);
   }
-  for (int j = tid; j < m; j += blockDim.x) wo[j] = A[(size_t)j * m2 + j];
-  if (!converged && tid == 0) atomicOr(flags, 1);
 }
 
 // Stable descending order by rank counting; Vs[:, j] = V[:, idx[j]].
@@ -627,7 +661,7 @@ __device__ void panel_T(P Z, int m, int c0, int pb, const QrShared& q, double* T
         T[j * QNB + i] = -ti * acc;
       }
       if (j == i) T[i * QNB + i] = ti;
-      if (j > i) T[j * QNB + i] = 0.0;
+      if (j > i && j < QNB) T[j * QNB + i] = 0.0;
       __syncwarp();
     }
   }
@@ -635,11 +669,11 @@ __device__ void panel_T(P Z, int m, int c0, int pb, const QrShared& q, double* T
 }
 
 template <int MAXR, typename P>
-__device__ void bqr_factor(P Z, int m, int p, QrShared& q, double* scr) {
+__device__ void bqr_factor(P Z, int m, int p, QrShared& q, double* scr, int wcols) {
   const int pe = p < m ? p : m;
   double* G = scr;                 // QNB x QNB
-  double* W = G + QNB * QNB;       // QNB x p
-  double* Ts = W + QNB * p;        // T of every panel
+  double* W = G + QNB * QNB;       // QNB x wcols (wcols >= p)
+  double* Ts = W + QNB * wcols;    // T of every panel
   for (int c0 = 0; c0 < pe; c0 += QNB) {
     const int pb = min(QNB, pe - c0);
     panel_factor<MAXR>(Z, m, c0, c0 + pb, q);
@@ -668,10 +702,11 @@ __device__ void bqr_factor(P Z, int m, int p, QrShared& q, double* scr) {
 
 // Qout (m x ncols, leading dimension ldq) = H_0 ... H_{pe-1} [e_cid ...].
 template <typename PZ, typename PQ>
-__device__ void bqr_form(PZ Z, int m, int p, int cid, int ncols, PQ Qo, int ldq, double* scr) {
+__device__ void bqr_form(PZ Z, int m, int p, int cid, int ncols, PQ Qo, int ldq, double* scr,
+                         int wcols) {
   const int pe = p < m ? p : m;
-  double* W = scr + QNB * QNB;
-  const double* Ts = W + QNB * (p > ncols ? p : ncols);
+  double* W = scr + QNB * QNB;     // QNB x wcols (wcols >= ncols)
+  const double* Ts = W + QNB * wcols;
   for (int t = threadIdx.x; t < m * ncols; t += blockDim.x) {
     const int c = t / m, r = t % m;
     Qo[c * ldq + r] = (r == cid + c) ? 1.0 : 0.0;
@@ -709,12 +744,12 @@ __device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
   const int Fk = F * k;
   for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = start[t];
   __syncthreads();
-  bqr_factor<MAXR>(Z, F, k, q, scr);
-  bqr_form(Z, F, k, 0, k, Q, F, scr);
+  bqr_factor<MAXR>(Z, F, k, q, scr, k);
+  bqr_form(Z, F, k, 0, k, Q, F, scr, k);
   for (int r = 0; r < rounds; ++r) {
     oi_apply(R, F, k, Q, Z);
-    bqr_factor<MAXR>(Z, F, k, q, scr);
-    bqr_form(Z, F, k, 0, k, Q, F, scr);
+    bqr_factor<MAXR>(Z, F, k, q, scr, k);
+    bqr_form(Z, F, k, 0, k, Q, F, scr, k);
   }
   // Rayleigh-Ritz: H = Q^T (R Q), symmetrised; Q out.
   oi_apply(R, F, k, Q, Z);
@@ -735,13 +770,13 @@ template <bool SMEM, int MAXR>
 __global__ void __launch_bounds__(kOiThreads)
     k_oi_fused(int F, int k, int rounds, const double* __restrict__ Rall,
                const double* __restrict__ start, double* Qall, double* Hall, double* work,
-               double* scr_all, size_t scr_stride) {
+               double* scr_all, size_t scr_stride, int scr_smem) {
   extern __shared__ double dyn[];
   __shared__ QrShared q;
   const int b = blockIdx.x;
   const size_t Fk = (size_t)F * k;
   const double* R = Rall + (size_t)b * F * F;
-  double* scr = scr_all + b * scr_stride;
+  double* scr = scr_smem ? dyn + (SMEM ? 2 * Fk : 0) : scr_all + b * scr_stride;
   if (SMEM)
     oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Fk, Qall + b * Fk,
                   Hall + (size_t)b * k * k, q, scr);
@@ -754,22 +789,24 @@ __global__ void __launch_bounds__(kOiThreads)
 // first k columns of U), written straight into U.
 template <bool SMEM, int MAXR>
 __global__ void __launch_bounds__(kOiThreads)
-    k_complete(int F, int k, double* Uall, double* work, double* scr_all, size_t scr_stride) {
+    k_complete(int F, int k, double* Uall, double* work, double* scr_all, size_t scr_stride,
+               int scr_smem) {
   extern __shared__ double dyn[];
   __shared__ QrShared q;
   const int b = blockIdx.x;
   const int Fk = F * k;
   double* Z = SMEM ? dyn : work + (size_t)b * Fk;
   double* U = Uall + (size_t)b * F * F;
-  double* scr = scr_all + b * scr_stride;
+  double* scr = scr_smem ? dyn + (SMEM ? Fk : 0) : scr_all + b * scr_stride;
+  const int wc = k > F - k ? k : F - k;
   for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = U[t];
   __syncthreads();
   if (SMEM) {
-    bqr_factor<MAXR>(dyn, F, k, q, scr);
-    bqr_form(dyn, F, k, k, F - k, U + Fk, F, scr);
+    bqr_factor<MAXR>(dyn, F, k, q, scr, wc);
+    bqr_form(dyn, F, k, k, F - k, U + Fk, F, scr, wc);
   } else {
-    bqr_factor<MAXR>(Z, F, k, q, scr);
-    bqr_form(Z, F, k, k, F - k, U + Fk, F, scr);
+    bqr_factor<MAXR>(Z, F, k, q, scr, wc);
+    bqr_form(Z, F, k, k, F - k, U + Fk, F, scr, wc);
   }
 }
 
@@ -783,21 +820,6 @@ __global__ void k_fill_zero(double* p, long count) {
 cudaError_t launch_householder(cudaStream_t s, int nbatch, int m, int p, int c0, int ncols,
                                double* Z, double* tau, double* Qout) {
   k_householder<<<nbatch, kBasisThreads, 0, s>>>(m, p, c0, ncols, Z, tau, Qout);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
-                          double* V, double* w, int* flags) {
-  if (m > 512) return cudaErrorInvalidValue;
-  const int m2 = m + (m & 1);
-  const size_t smem = (size_t)2 * m2 * m2 * sizeof(double);
-  int use_smem = smem <= 200 * 1024;
-  if (use_smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_jacobi<<<nbatch, kBasisThreads, use_smem ? smem : 0, s>>>(m, A, work, V, w, flags, use_smem);
   return cudaGetLastError();
 }
 
@@ -829,25 +851,77 @@ static cudaError_t set_smem_attr(const void* fn, size_t bytes) {
 
 constexpr size_t kBasisSmemMax = 200 * 1024;  // + ~17 KB static QrShared <= 227 KB
 
-size_t qr_scratch_doubles(int F, int k) {
+// Blocked-QR scratch: G (QNB^2) | W (QNB x wcols) | T of every panel.
+static size_t qr_scratch(int wcols, int k) {
   const int npan = (k + QNB - 1) / QNB;
-  return (size_t)QNB * QNB + (size_t)QNB * (F > k ? F : k) + (size_t)npan * QNB * QNB + 64;
+  return (size_t)QNB * QNB + (size_t)QNB * wcols + (size_t)npan * QNB * QNB;
+}
+
+size_t qr_scratch_doubles(int F, int k) { return qr_scratch(F > k ? F : k, k); }
+
+// Dynamic shared memory left for `fn` next to its static shared memory.
+static size_t smem_room(const void* fn) {
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      optin = 227 * 1024;
+  }
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return 0;
+  return (size_t)optin > fa.sharedSizeBytes + 256 ? optin - fa.sharedSizeBytes - 256 : 0;
+}
+
+cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
+                          double* V, double* w, int* flags) {
+  if (m > 512) return cudaErrorInvalidValue;
+  const int m2 = m + (m & 1);
+  const size_t abytes = (size_t)m2 * (m2 + 1) * sizeof(double);
+  const size_t room = smem_room((const void*)k_jacobi);
+  int nsplit = 0;
+  for (int sp = 1; sp <= 8 && abytes < room; sp *= 2) {
+    const int vr = (m2 + sp - 1) / sp;
+    if (abytes + (size_t)m2 * vr * sizeof(double) <= room) {
+      nsplit = sp;
+      break;
+    }
+  }
+  if (nsplit > 0) {
+    const int vr = (m2 + nsplit - 1) / nsplit;
+    const size_t smem = abytes + (size_t)m2 * vr * sizeof(double);
+    cudaError_t e = set_smem_attr((const void*)k_jacobi, smem);
+    if (e != cudaSuccess) return e;
+    k_jacobi<<<dim3(nbatch, nsplit), kJacThreads, smem, s>>>(m, A, work, V, w, flags, 1, vr);
+  } else {
+    k_jacobi<<<dim3(nbatch, 1), kJacThreads, 0, s>>>(m, A, work, V, w, flags, 0, m2);
+  }
+  return cudaGetLastError();
 }
 
 template <int MAXR>
 static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                  const double* R, const double* start, double* Q, double* H,
                                  double* work, double* scr) {
-  const size_t smem = (size_t)2 * F * k * sizeof(double);
+  const size_t pair = (size_t)2 * F * k * sizeof(double);
+  const size_t sbytes = qr_scratch(k, k) * sizeof(double);
   const size_t ss = qr_scratch_doubles(F, k);
-  if (smem <= kBasisSmemMax) {
-    cudaError_t e = set_smem_attr((const void*)k_oi_fused<true, MAXR>, smem);
+  if (pair <= kBasisSmemMax) {
+    const void* fn = (const void*)k_oi_fused<true, MAXR>;
+    const int in_smem = pair + sbytes <= smem_room(fn);
+    const size_t smem = pair + (in_smem ? sbytes : 0);
+    cudaError_t e = set_smem_attr(fn, smem);
     if (e != cudaSuccess) return e;
     k_oi_fused<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work,
-                                                            scr, ss);
+                                                            scr, ss, in_smem);
   } else {
-    k_oi_fused<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, rounds, R, start, Q, H, work, scr,
-                                                          ss);
+    const void* fn = (const void*)k_oi_fused<false, MAXR>;
+    const int in_smem = sbytes <= smem_room(fn);
+    const size_t smem = in_smem ? sbytes : 0;
+    cudaError_t e = set_smem_attr(fn, smem);
+    if (e != cudaSuccess) return e;
+    k_oi_fused<false, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work,
+                                                             scr, ss, in_smem);
   }
   return cudaGetLastError();
 }
@@ -864,14 +938,23 @@ cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds
 template <int MAXR>
 static cudaError_t complete_impl(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
                                  double* scr) {
-  const size_t smem = (size_t)F * k * sizeof(double);
+  const size_t zb = (size_t)F * k * sizeof(double);
+  const size_t sbytes = qr_scratch(k > F - k ? k : F - k, k) * sizeof(double);
   const size_t ss = qr_scratch_doubles(F, k);
-  if (smem <= kBasisSmemMax) {
-    cudaError_t e = set_smem_attr((const void*)k_complete<true, MAXR>, smem);
+  if (zb <= kBasisSmemMax) {
+    const void* fn = (const void*)k_complete<true, MAXR>;
+    const int in_smem = zb + sbytes <= smem_room(fn);
+    const size_t smem = zb + (in_smem ? sbytes : 0);
+    cudaError_t e = set_smem_attr(fn, smem);
     if (e != cudaSuccess) return e;
-    k_complete<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, U, work, scr, ss);
+    k_complete<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, U, work, scr, ss, in_smem);
   } else {
-    k_complete<false, MAXR><<<nbatch, kOiThreads, 0, s>>>(F, k, U, work, scr, ss);
+    const void* fn = (const void*)k_complete<false, MAXR>;
+    const int in_smem = sbytes <= smem_room(fn);
+    const size_t smem = in_smem ? sbytes : 0;
+    cudaError_t e = set_smem_attr(fn, smem);
+    if (e != cudaSuccess) return e;
+    k_complete<false, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, U, work, scr, ss, in_smem);
   }
   return cudaGetLastError();
 }

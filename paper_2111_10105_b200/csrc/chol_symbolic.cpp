@@ -14,6 +14,7 @@
 #include <thread>
 
 #include "chol.h"
+#include "par.h"
 
 namespace dmcg {
 
@@ -29,7 +30,12 @@ struct Graph {
 // of one index array, partitioned in place (parts A | B | separator S);
 // two BFS per split: from any vertex to the farthest one (pseudo-
 // peripheral), then the level structure from there.  Leaves of <= 48
-// vertices keep their order.  Output: elimination order (old indices).
+// vertices keep their order.  Because every range is partitioned in place
+// as A | B | S, the final index array IS the elimination order (old
+// indices; A's order, then B's, then S).  The two halves of the upper
+// dissection levels run on separate threads: they touch disjoint ranges,
+// and the only cross-range read (part_ of a neighbour) compares against an
+// id the other range never holds.
 class NestedDissection {
  public:
   explicit NestedDissection(const Graph& g)
@@ -37,63 +43,66 @@ class NestedDissection {
 
   std::vector<uint32_t> run() {
     for (uint32_t i = 0; i < g_.n; ++i) idx_[i] = i;
-    perm_.reserve(g_.n);
-    struct Task {
-      uint32_t b, e;
-      int32_t id;
-      bool emit;  // emit the range as is (separator)
-    };
-    // explicit stack; order: A, B, then S (postorder of the dissection tree)
-    std::vector<Task> st;
-    st.push_back({0, g_.n, 0, false});
-    while (!st.empty()) {
-      Task t = st.back();
-      st.pop_back();
-      if (t.emit || t.e - t.b <= 48) {
-        perm_.insert(perm_.end(), idx_.begin() + t.b, idx_.begin() + t.e);
-        continue;
-      }
-      uint32_t na, ns;
-      const int kind = split(t.b, t.e, t.id, &na, &ns);
-      if (kind == 0) {  // no useful split
-        perm_.insert(perm_.end(), idx_.begin() + t.b, idx_.begin() + t.e);
-        continue;
-      }
-      const int32_t ia = next_id_++, ib = next_id_++;
-      const uint32_t e_a = t.b + na, e_b = t.e - ns;
-      for (uint32_t q = t.b; q < e_a; ++q) part_[idx_[q]] = ia;
-      for (uint32_t q = e_a; q < e_b; ++q) part_[idx_[q]] = ib;
-      if (ns) {
-        const int32_t is = next_id_++;
-        for (uint32_t q = e_b; q < t.e; ++q) part_[idx_[q]] = is;
-        st.push_back({e_b, t.e, is, true});
-      }
-      st.push_back({e_a, e_b, ib, false});
-      st.push_back({t.b, e_a, ia, false});
-    }
-    return perm_;
+    process(0, g_.n, 0, 0);
+    return std::move(idx_);
   }
 
  private:
+  static constexpr int kParDepth = 3;      // up to 2^3 concurrent ranges
+  static constexpr uint32_t kParMin = 4096;  // smallest half worth a thread
   const Graph g_;
   std::vector<int32_t> part_, level_;
-  std::vector<uint32_t> queue_, idx_, tmp_, perm_;
-  int32_t next_id_ = 1;
+  std::vector<uint32_t> queue_, idx_, tmp_;
+  std::atomic<int32_t> next_id_{1};
 
-  uint32_t bfs(uint32_t root, int32_t id, uint32_t* maxlev) {
+  int32_t part(uint32_t v) const { return __atomic_load_n(&part_[v], __ATOMIC_RELAXED); }
+  void set_part(uint32_t v, int32_t id) { __atomic_store_n(&part_[v], id, __ATOMIC_RELAXED); }
+
+  void process(uint32_t b0, uint32_t e0, int32_t id0, int depth0) {
+    struct Task {
+      uint32_t b, e;
+      int32_t id;
+      int depth;
+    };
+    std::vector<Task> st;
+    st.push_back({b0, e0, id0, depth0});
+    while (!st.empty()) {
+      const Task t = st.back();
+      st.pop_back();
+      if (t.e - t.b <= 48) continue;
+      uint32_t na, ns;
+      if (split(t.b, t.e, t.id, &na, &ns) == 0) continue;  // no useful split
+      const int32_t ia = next_id_.fetch_add(3), ib = ia + 1, is = ia + 2;
+      const uint32_t e_a = t.b + na, e_b = t.e - ns;
+      for (uint32_t q = t.b; q < e_a; ++q) set_part(idx_[q], ia);
+      for (uint32_t q = e_a; q < e_b; ++q) set_part(idx_[q], ib);
+      for (uint32_t q = e_b; q < t.e; ++q) set_part(idx_[q], is);
+      if (t.depth < kParDepth && na >= kParMin && e_b - e_a >= kParMin) {
+        std::thread th([this, t, e_a, ia] { process(t.b, e_a, ia, t.depth + 1); });
+        process(e_a, e_b, ib, t.depth + 1);
+        th.join();
+        continue;
+      }
+      st.push_back({e_a, e_b, ib, t.depth + 1});
+      st.push_back({t.b, e_a, ia, t.depth + 1});
+    }
+  }
+
+  // BFS over the vertices of part `id`; queue = range-local buffer.
+  uint32_t bfs(uint32_t root, int32_t id, uint32_t* queue, uint32_t* maxlev) {
     uint32_t head = 0, tail = 0;
-    queue_[tail++] = root;
+    queue[tail++] = root;
     level_[root] = 0;
     uint32_t last = root;
     while (head < tail) {
-      const uint32_t v = queue_[head++];
+      const uint32_t v = queue[head++];
       last = v;
       const int32_t lv = level_[v] + 1;
       for (uint32_t p = g_.rp[v]; p < g_.rp[v + 1]; ++p) {
         const uint32_t w = g_.ci[p];
-        if (part_[w] == id && level_[w] < 0) {
+        if (part(w) == id && level_[w] < 0) {
           level_[w] = lv;
-          queue_[tail++] = w;
+          queue[tail++] = w;
         }
       }
     }
@@ -105,9 +114,11 @@ class NestedDissection {
   // a disconnected range becomes A = reached component, B = rest, S empty.
   int split(uint32_t b, uint32_t e, int32_t id, uint32_t* na, uint32_t* ns) {
     const uint32_t cnt = e - b;
+    uint32_t* queue = queue_.data() + b;
+    uint32_t* tmp = tmp_.data() + b;
     for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
     uint32_t maxlev;
-    const uint32_t reached = bfs(idx_[b], id, &maxlev);
+    const uint32_t reached = bfs(idx_[b], id, queue, &maxlev);
     if (reached < cnt) {
       uint32_t a = b, z = 0;
       for (uint32_t q = b; q < e; ++q) {
@@ -115,16 +126,16 @@ class NestedDissection {
         if (level_[v] >= 0)
           idx_[a++] = v;
         else
-          tmp_[z++] = v;
+          tmp[z++] = v;
       }
-      std::copy(tmp_.begin(), tmp_.begin() + z, idx_.begin() + a);
+      std::copy(tmp, tmp + z, idx_.begin() + a);
       *na = a - b;
       *ns = 0;
       return 1;
     }
-    const uint32_t root = queue_[cnt - 1];
+    const uint32_t root = queue[cnt - 1];
     for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
-    bfs(root, id, &maxlev);
+    bfs(root, id, queue, &maxlev);
     if (maxlev < 2) return 0;
     // separator = the level where the running count first exceeds half
     std::vector<uint32_t> hist(maxlev + 2, 0);
@@ -140,18 +151,18 @@ class NestedDissection {
     if (sep == 0) sep = 1;
     if (sep >= maxlev) sep = maxlev - 1;
     uint32_t a = b, zb = 0, zs = 0;
-    uint32_t* sbuf = queue_.data();  // queue no longer needed
+    uint32_t* sbuf = queue;  // queue no longer needed
     for (uint32_t q = b; q < e; ++q) {
       const uint32_t v = idx_[q];
       const uint32_t l = (uint32_t)level_[v];
       if (l < sep)
         idx_[a++] = v;
       else if (l > sep)
-        tmp_[zb++] = v;
+        tmp[zb++] = v;
       else
         sbuf[zs++] = v;
     }
-    std::copy(tmp_.begin(), tmp_.begin() + zb, idx_.begin() + a);
+    std::copy(tmp, tmp + zb, idx_.begin() + a);
     std::copy(sbuf, sbuf + zs, idx_.begin() + a + zb);
     *na = a - b;
     *ns = zs;
@@ -182,13 +193,36 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   lap("ordering");
   std::vector<uint32_t> iperm0(n);
   for (uint32_t k = 0; k < n; ++k) iperm0[perm0[k]] = k;
+  // strictly lower pattern of P M P^T (row k: columns r < k), built in
+  // parallel so the sequential etree pass below streams contiguous rows
+  std::vector<uint32_t> lp((size_t)n + 1, 0), li;
+  {
+    parallel_for(n, 2048, [&](uint32_t k0, uint32_t k1, uint32_t) {
+      for (uint32_t k = k0; k < k1; ++k) {
+        const uint32_t ko = perm0[k];
+        uint32_t c = 0;
+        for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) c += iperm0[ci[q]] < k;
+        lp[k + 1] = c;
+      }
+    });
+    for (uint32_t k = 0; k < n; ++k) lp[k + 1] += lp[k];
+    li.resize(lp[n]);
+    parallel_for(n, 2048, [&](uint32_t k0, uint32_t k1, uint32_t) {
+      for (uint32_t k = k0; k < k1; ++k) {
+        const uint32_t ko = perm0[k];
+        uint32_t o = lp[k];
+        for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
+          const uint32_t r = iperm0[ci[q]];
+          if (r < k) li[o++] = r;
+        }
+      }
+    });
+  }
   // (2) elimination tree (Liu, path compression) of P M P^T
   std::vector<int32_t> par(n, -1), anc(n, -1);
   for (uint32_t k = 0; k < n; ++k) {
-    const uint32_t ko = perm0[k];
-    for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
-      int32_t r = (int32_t)iperm0[ci[q]];
-      if ((uint32_t)r >= k) continue;
+    for (uint32_t q = lp[k]; q < lp[k + 1]; ++q) {
+      int32_t r = (int32_t)li[q];
       while (anc[r] != -1 && anc[r] != (int32_t)k) {
         const int32_t nx = anc[r];
         anc[r] = (int32_t)k;
@@ -236,21 +270,93 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     const int32_t q = par[post[j]];
     parent[j] = q == -1 ? -1 : (int32_t)ipost[q];
   }
-  lap("etree+post");
-  // (4) column counts by row-subtree traversal (Davis, LDL symbolic)
-  std::vector<uint32_t> colcnt(n, 1);  // diagonal
+  // upper pattern + values in the final numbering: column j holds the rows
+  // i >= j (diagonal first is not required), used by the column counts,
+  // the front structures and the scatter list
+  std::vector<uint32_t> up((size_t)n + 1, 0), ui;
+  std::vector<float> uv;
   {
-    std::vector<int32_t> flag(n, -1);
-    for (uint32_t k = 0; k < n; ++k) {
-      flag[k] = (int32_t)k;
-      const uint32_t ko = p.perm[k];
-      for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
-        uint32_t i = p.iperm[ci[q]];
-        if (i >= k) continue;
-        for (; flag[i] != (int32_t)k; i = (uint32_t)parent[i]) {
-          colcnt[i]++;
-          flag[i] = (int32_t)k;
+    parallel_for(n, 2048, [&](uint32_t j0, uint32_t j1, uint32_t) {
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint32_t jo = p.perm[j];
+        uint32_t c = 0;
+        for (uint32_t q = rp[jo]; q < rp[jo + 1]; ++q) c += p.iperm[ci[q]] >= j;
+        up[j + 1] = c;
+      }
+    });
+    for (uint32_t j = 0; j < n; ++j) up[j + 1] += up[j];
+    ui.resize(up[n]);
+    uv.resize(up[n]);
+    parallel_for(n, 2048, [&](uint32_t j0, uint32_t j1, uint32_t) {
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint32_t jo = p.perm[j];
+        uint32_t o = up[j];
+        for (uint32_t q = rp[jo]; q < rp[jo + 1]; ++q) {
+          const uint32_t i = p.iperm[ci[q]];
+          if (i >= j) {
+            ui[o] = i;
+            uv[o++] = val[q];
+          }
         }
+      }
+    });
+  }
+  lap("etree+post");
+  // (4) column counts (Gilbert, Ng & Peyton 1994: row-subtree leaves and
+  // least common ancestors, near O(nnz(M))).  The matrix is already in
+  // postorder, so the postorder of the tree is the identity.
+  std::vector<uint32_t> colcnt(n, 0);
+  {
+    std::vector<int32_t> delta(n, 0), first(n, -1), maxfirst(n, -1), prevleaf(n, -1), anc(n);
+    for (uint32_t k = 0; k < n; ++k) {
+      delta[k] = first[k] == -1 ? 1 : 0;  // k is a leaf of the etree
+      for (int32_t j = (int32_t)k; j != -1 && first[j] == -1; j = parent[j]) first[j] = (int32_t)k;
+    }
+    for (uint32_t i = 0; i < n; ++i) anc[i] = (int32_t)i;
+    for (uint32_t j = 0; j < n; ++j) {
+      if (parent[j] != -1) delta[parent[j]]--;
+      for (uint32_t q = up[j]; q < up[j + 1]; ++q) {
+        const uint32_t i = ui[q];
+        // is j a leaf of the row subtree of i?
+        if (i <= j || first[j] <= maxfirst[i]) continue;
+        maxfirst[i] = first[j];
+        const int32_t jprev = prevleaf[i];
+        prevleaf[i] = (int32_t)j;
+        delta[j]++;
+        if (jprev == -1) continue;  // first leaf: lca is the subtree root i
+        int32_t lca = jprev;
+        while (lca != anc[lca]) lca = anc[lca];
+        for (int32_t s2 = jprev; s2 != lca;) {  // path compression
+          const int32_t nx = anc[s2];
+          anc[s2] = lca;
+          s2 = nx;
+        }
+        delta[lca]--;
+      }
+      if (parent[j] != -1) anc[j] = parent[j];
+    }
+    for (uint32_t j = 0; j < n; ++j)
+      if (parent[j] != -1) delta[parent[j]] += delta[j];
+    for (uint32_t j = 0; j < n; ++j) colcnt[j] = (uint32_t)delta[j];
+    static const bool check = std::getenv("DMCG_CHECK_SYMBOLIC") != nullptr;
+    if (check) {  // row-subtree traversal (Davis, LDL symbolic)
+      std::vector<uint32_t> cc(n, 1);
+      std::vector<int32_t> flag(n, -1);
+      for (uint32_t k = 0; k < n; ++k) {
+        flag[k] = (int32_t)k;
+        const uint32_t ko = p.perm[k];
+        for (uint32_t q = rp[ko]; q < rp[ko + 1]; ++q) {
+          uint32_t i = p.iperm[ci[q]];
+          if (i >= k) continue;
+          for (; flag[i] != (int32_t)k; i = (uint32_t)parent[i]) {
+            cc[i]++;
+            flag[i] = (int32_t)k;
+          }
+        }
+      }
+      if (cc != colcnt) {
+        std::fprintf(stderr, "dmcg: column-count mismatch\n");
+        std::abort();
       }
     }
   }
@@ -327,51 +433,19 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   for (uint32_t s = 0; s < NS; ++s)
     for (uint32_t j = p.first[s]; j < p.first[s + 1]; ++j) col_sup[j] = s;
   lap("supernodes");
-  // (7) row structures, postorder of supernodes = column order
+  // (7) supernodal tree (parent = supernode of the etree parent of the last
+  // column), children, levels; then the row structures, one tree level at a
+  // time with the supernodes of a level in parallel (a structure needs only
+  // its own columns of M and its children's structures).
   p.parent.assign(NS, -1);
   std::vector<std::vector<uint32_t>> kids(NS);
-  std::vector<int32_t> mark(n, -1);
-  p.str_ptr.assign(NS + 1, 0);
-  p.str_idx.clear();
-  p.str_idx.reserve((size_t)n * 40);
-  std::vector<uint32_t> rows;
   for (uint32_t s = 0; s < NS; ++s) {
-    const uint32_t f0 = p.first[s], f1 = p.first[s + 1];
-    rows.clear();
-    for (uint32_t j = f0; j < f1; ++j) {
-      rows.push_back(j);
-      mark[j] = (int32_t)s;
-    }
-    for (uint32_t j = f0; j < f1; ++j) {
-      const uint32_t jo = p.perm[j];
-      for (uint32_t q = rp[jo]; q < rp[jo + 1]; ++q) {
-        const uint32_t i = p.iperm[ci[q]];
-        if (i >= f1 && mark[i] != (int32_t)s) {
-          mark[i] = (int32_t)s;
-          rows.push_back(i);
-        }
-      }
-    }
-    for (uint32_t c : kids[s]) {
-      for (uint64_t q = p.str_ptr[c] + p.w(c); q < p.str_ptr[c + 1]; ++q) {
-        const uint32_t i = p.str_idx[q];
-        if (i >= f1 && mark[i] != (int32_t)s) {
-          mark[i] = (int32_t)s;
-          rows.push_back(i);
-        }
-      }
-    }
-    std::sort(rows.begin() + (f1 - f0), rows.end());
-    p.str_idx.insert(p.str_idx.end(), rows.begin(), rows.end());
-    p.str_ptr[s + 1] = p.str_idx.size();
-    if (rows.size() > f1 - f0) {
-      const uint32_t ps = col_sup[rows[f1 - f0]];
-      p.parent[s] = (int32_t)ps;
-      kids[ps].push_back(s);
+    const int32_t pc = parent[p.first[s + 1] - 1];
+    if (pc >= 0) {
+      p.parent[s] = (int32_t)col_sup[pc];
+      kids[p.parent[s]].push_back(s);
     }
   }
-  lap("structure");
-  // children lists, levels
   p.child_ptr.assign(NS + 1, 0);
   p.child_idx.clear();
   for (uint32_t s = 0; s < NS; ++s) {
@@ -393,6 +467,63 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     std::vector<uint32_t> fill(p.level_ptr.begin(), p.level_ptr.end() - 1);
     for (uint32_t s = 0; s < NS; ++s) p.level_sup[fill[lev[s]]++] = s;
   }
+  {
+    std::vector<std::vector<uint32_t>> str(NS);
+    std::vector<std::vector<int32_t>> marks(16);
+    for (uint32_t l = 0; l < p.nlevels; ++l) {
+      const uint32_t l0 = p.level_ptr[l], cnt = p.level_ptr[l + 1] - l0;
+      parallel_for(cnt, 16, [&](uint32_t q0, uint32_t q1, uint32_t c) {
+        std::vector<int32_t>& mark = marks[c];
+        if (mark.empty()) mark.assign(n, -1);
+        for (uint32_t t = q0; t < q1; ++t) {
+          const uint32_t s = p.level_sup[l0 + t];
+          const uint32_t f0 = p.first[s], f1 = p.first[s + 1];
+          std::vector<uint32_t>& rows = str[s];
+          for (uint32_t j = f0; j < f1; ++j) {
+            rows.push_back(j);
+            mark[j] = (int32_t)s;
+          }
+          for (uint32_t j = f0; j < f1; ++j)
+            for (uint32_t q = up[j]; q < up[j + 1]; ++q) {
+              const uint32_t i = ui[q];
+              if (i >= f1 && mark[i] != (int32_t)s) {
+                mark[i] = (int32_t)s;
+                rows.push_back(i);
+              }
+            }
+          for (uint32_t ch : kids[s]) {
+            const std::vector<uint32_t>& cr = str[ch];
+            for (size_t q = p.first[ch + 1] - p.first[ch]; q < cr.size(); ++q) {
+              const uint32_t i = cr[q];
+              if (i >= f1 && mark[i] != (int32_t)s) {
+                mark[i] = (int32_t)s;
+                rows.push_back(i);
+              }
+            }
+          }
+          std::sort(rows.begin() + (f1 - f0), rows.end());
+        }
+      });
+    }
+    p.str_ptr.assign(NS + 1, 0);
+    for (uint32_t s = 0; s < NS; ++s) p.str_ptr[s + 1] = p.str_ptr[s] + str[s].size();
+    p.str_idx.resize(p.str_ptr[NS]);
+    parallel_for(NS, 64, [&](uint32_t s0, uint32_t s1, uint32_t) {
+      for (uint32_t s = s0; s < s1; ++s)
+        std::copy(str[s].begin(), str[s].end(), p.str_idx.begin() + p.str_ptr[s]);
+    });
+    static const bool check = std::getenv("DMCG_CHECK_SYMBOLIC") != nullptr;
+    if (check)  // the tree from the etree matches the structures' first off-diagonal rows
+      for (uint32_t s = 0; s < NS; ++s) {
+        const uint32_t w = p.first[s + 1] - p.first[s];
+        const int32_t ps = str[s].size() > w ? (int32_t)col_sup[str[s][w]] : -1;
+        if (ps != p.parent[s]) {
+          std::fprintf(stderr, "dmcg: supernodal parent mismatch at %u\n", s);
+          std::abort();
+        }
+      }
+  }
+  lap("structure");
   // offsets and statistics
   p.front_off.assign(NS + 1, 0);
   p.inv_off.assign(NS + 1, 0);
@@ -416,41 +547,42 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   lap("levels+stats");
   // (8) extend-add maps: child update rows -> parent local rows
   p.rel_ptr.assign(NS + 1, 0);
-  p.rel_idx.clear();
-  for (uint32_t c = 0; c < NS; ++c) {
-    const int32_t ps = p.parent[c];
-    if (ps >= 0) {
+  for (uint32_t c = 0; c < NS; ++c)
+    p.rel_ptr[c + 1] = p.rel_ptr[c] + (p.parent[c] >= 0 ? p.m(c) - p.w(c) : 0);
+  p.rel_idx.resize(p.rel_ptr[NS]);
+  parallel_for(NS, 64, [&](uint32_t c0, uint32_t c1, uint32_t) {
+    for (uint32_t c = c0; c < c1; ++c) {
+      const int32_t ps = p.parent[c];
+      if (ps < 0) continue;
       const uint32_t* pb = &p.str_idx[p.str_ptr[ps]];
       const uint32_t pm = p.m((uint32_t)ps);
+      uint64_t o = p.rel_ptr[c];
+      const uint32_t* it = pb;
       for (uint64_t q = p.str_ptr[c] + p.w(c); q < p.str_ptr[c + 1]; ++q) {
-        const uint32_t r = p.str_idx[q];
-        const uint32_t* it = std::lower_bound(pb, pb + pm, r);
-        p.rel_idx.push_back((uint32_t)(it - pb));
+        it = std::lower_bound(it, pb + pm, p.str_idx[q]);  // rows are sorted
+        p.rel_idx[o++] = (uint32_t)(it - pb);
       }
     }
-    p.rel_ptr[c + 1] = p.rel_idx.size();
-  }
+  });
   lap("rel maps");
   // (9) scatter list of M into the fronts (lower part, column-major local)
   p.a_ptr.assign(NS + 1, 0);
-  p.a_pos.clear();
-  p.a_val.clear();
-  std::vector<int32_t> loc(n, -1);
-  for (uint32_t s = 0; s < NS; ++s) {
-    const uint32_t m = p.m(s), f0 = p.first[s], f1 = p.first[s + 1];
-    for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = (int32_t)t;
-    for (uint32_t j = f0; j < f1; ++j) {
-      const uint32_t jo = p.perm[j];
-      for (uint32_t q = rp[jo]; q < rp[jo + 1]; ++q) {
-        const uint32_t i = p.iperm[ci[q]];
-        if (i < j) continue;
-        p.a_pos.push_back((j - f0) * m + (uint32_t)loc[i]);
-        p.a_val.push_back(val[q]);
-      }
+  for (uint32_t s = 0; s < NS; ++s) p.a_ptr[s + 1] = up[p.first[s + 1]];
+  p.a_pos.resize(p.a_ptr[NS]);
+  p.a_val.resize(p.a_ptr[NS]);
+  parallel_for(NS, 64, [&](uint32_t s0, uint32_t s1, uint32_t) {
+    std::vector<int32_t> loc(n, -1);
+    for (uint32_t s = s0; s < s1; ++s) {
+      const uint32_t m = p.m(s), f0 = p.first[s], f1 = p.first[s + 1];
+      for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = (int32_t)t;
+      for (uint32_t j = f0; j < f1; ++j)
+        for (uint32_t q = up[j]; q < up[j + 1]; ++q) {
+          p.a_pos[q] = (j - f0) * m + (uint32_t)loc[ui[q]];
+          p.a_val[q] = uv[q];
+        }
+      for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = -1;
     }
-    p.a_ptr[s + 1] = p.a_pos.size();
-    for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = -1;
-  }
+  });
   lap("scatter");
 }
 

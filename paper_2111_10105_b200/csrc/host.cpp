@@ -9,11 +9,13 @@
 #include <cstring>
 #include <deque>
 #include <limits>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "internal.h"
 #include "kernels.h"
+#include "par.h"
 
 namespace dmcg {
 
@@ -161,40 +163,66 @@ Status validate_mesh(const MeshHost& m) {
 // symmetric and integer valued, so M's entries are small integers held
 // exactly in float.
 void build_normal_matrix(MeshHost* m) {
+  // Rows of M are independent: each chunk of rows is built into its own
+  // arrays by one host thread, then the chunks are concatenated.
   const uint32_t n = m->n;
-  std::vector<double> acc(n, 0.0);
-  std::vector<int64_t> mark(n, -1);
-  std::vector<uint32_t> list;
-  m->m_rp.assign((size_t)n + 1, 0);
-  m->m_ci.clear();
-  m->m_val.clear();
-  m->m_ci.reserve((size_t)n * 20);
-  m->m_val.reserve((size_t)n * 20);
+  const uint32_t grain = 2048;
+  const uint32_t nch = parallel_chunks(n, grain);
+  std::vector<std::vector<uint32_t>> cci(nch), crl(nch);
+  std::vector<std::vector<float>> cval(nch);
   auto lval = [&](uint32_t row, uint32_t p) -> double {
     return m->lap_ci[p] == row ? (double)(m->lap_rp[row + 1] - m->lap_rp[row] - 1) : -1.0;
   };
-  for (uint32_t i = 0; i < n; ++i) {
-    list.clear();
-    for (uint32_t p = m->lap_rp[i]; p < m->lap_rp[i + 1]; ++p) {
-      const uint32_t k = m->lap_ci[p];
-      const double a = lval(i, p);  // L^T(i,k) = L(k,i) = L(i,k)
-      for (uint32_t q = m->lap_rp[k]; q < m->lap_rp[k + 1]; ++q) {
-        const uint32_t j = m->lap_ci[q];
-        if (mark[j] != (int64_t)i) {
-          mark[j] = i;
-          acc[j] = 0.0;
-          list.push_back(j);
+  parallel_for(n, grain, [&](uint32_t r0, uint32_t r1, uint32_t c) {
+    std::unique_ptr<double[]> acc(new double[n]);  // valid where mark[j] == row
+    std::vector<int32_t> mark(n, -1);
+    std::vector<uint32_t> list, ci, rl;  // thread-local: no shared vector headers
+    std::vector<float> va;
+    ci.reserve((size_t)(r1 - r0) * 20);
+    va.reserve((size_t)(r1 - r0) * 20);
+    rl.reserve(r1 - r0);
+    for (uint32_t i = r0; i < r1; ++i) {
+      list.clear();
+      for (uint32_t p = m->lap_rp[i]; p < m->lap_rp[i + 1]; ++p) {
+        const uint32_t k = m->lap_ci[p];
+        const double a = lval(i, p);  // L^T(i,k) = L(k,i) = L(i,k)
+        for (uint32_t q = m->lap_rp[k]; q < m->lap_rp[k + 1]; ++q) {
+          const uint32_t j = m->lap_ci[q];
+          if (mark[j] != (int32_t)i) {
+            mark[j] = (int32_t)i;
+            acc[j] = 0.0;
+            list.push_back(j);
+          }
+          acc[j] += a * lval(k, q);
         }
-        acc[j] += a * lval(k, q);
       }
+      if (m->anchor_pos[i] >= 0) acc[i] += 1.0;
+      std::sort(list.begin(), list.end());
+      for (uint32_t j : list) {
+        ci.push_back(j);
+        va.push_back((float)acc[j]);
+      }
+      rl.push_back((uint32_t)list.size());
     }
-    if (m->anchor_pos[i] >= 0) acc[i] += 1.0;
-    std::sort(list.begin(), list.end());
-    for (uint32_t j : list) {
-      m->m_ci.push_back(j);
-      m->m_val.push_back((float)acc[j]);
+    cci[c] = std::move(ci);
+    cval[c] = std::move(va);
+    crl[c] = std::move(rl);
+  });
+  m->m_rp.assign((size_t)n + 1, 0);
+  size_t tot = 0;
+  for (uint32_t c = 0; c < nch; ++c) tot += cci[c].size();
+  m->m_ci.resize(tot);
+  m->m_val.resize(tot);
+  size_t o = 0;
+  uint32_t row = 0;
+  for (uint32_t c = 0; c < nch; ++c) {
+    std::copy(cci[c].begin(), cci[c].end(), m->m_ci.begin() + o);
+    std::copy(cval[c].begin(), cval[c].end(), m->m_val.begin() + o);
+    o += cci[c].size();
+    for (uint32_t len : crl[c]) {
+      m->m_rp[row + 1] = m->m_rp[row] + len;
+      ++row;
     }
-    m->m_rp[i + 1] = (uint32_t)m->m_ci.size();
   }
 }
 
@@ -509,7 +537,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_Q = (double*)get(3 * (size_t)F * kk * 8);
   p->d_Z = (double*)get(3 * (size_t)F * kk * 8);
   p->d_tau = (double*)get(3 * (size_t)F * 8);
-  p->d_H = (double*)get(3 * 2 * (size_t)F2 * F2 * 8);
+  p->d_H = (double*)get(3 * 2 * (size_t)F2 * (F2 + 1) * 8);  // jacobi: A (m2 x m2+1) + V per axis
   p->d_V = (double*)get(3 * FF * 8);
   p->d_qr_scr = (double*)get(3 * dmcg::qr_scratch_doubles((int)F, (int)kk) * 8);
   p->d_w = (double*)get(3 * (size_t)F * 8);
@@ -572,7 +600,9 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
 // decoder needs it; solver.cpp:25-39).
 dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
   if (p->d_m_rp) return Status::ok();
+  PhaseTimer tm("normal");
   build_normal_matrix(&p->mesh);
+  tm.lap("build");
   const MeshHost& m = p->mesh;
   p->stats.nnz_normal = (long long)m.m_ci.size();
   p->d_m_rp = (uint32_t*)plan_alloc(p, m.m_rp.size() * 4);
@@ -588,15 +618,18 @@ dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
   ok = ok && cudaMemcpyAsync(p->d_m_val, m.m_val.data(), m.m_val.size() * 4,
                              cudaMemcpyHostToDevice, s) == cudaSuccess;
   if (!ok) return {DMCG_E_CUDA, "CudaError: normal matrix upload failed"};
+  tm.lap("upload");
   return Status::ok();
 }
 
 dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   if (p->decode_ready) return Status::ok();
+  PhaseTimer tm("prepare");
   {
     Status sn = plan_prepare_normal(p);
     if (!sn.good()) return sn;
   }
+  tm.lap("normal matrix");
   const uint32_t n = p->n;
   const MeshHost& m = p->mesh;
   bool ok = true;
@@ -612,6 +645,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
     p->analyze_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
+  tm.lap("analyze");
   const CholPlan& cp = p->chol;
   const size_t nW = (size_t)n * p->W;
   p->d_rm_delta = (double*)get(nW * 8);
@@ -668,6 +702,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   p->stats.flops_factor = cp.flops_factor;
   p->stats.analyze_seconds = p->analyze_seconds;
   if (!ok) return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  tm.lap("alloc");
   cudaStream_t s = p->ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
@@ -689,6 +724,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   h2d((void*)cd.level_sup, cp.level_sup.data(), cp.level_sup.size() * 4);
   if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) return {DMCG_E_CUDA, "CudaError: decode plan upload failed"};
+  tm.lap("upload+sync");
   p->decode_ready = true;
   return Status::ok();
 }
@@ -936,12 +972,15 @@ extern "C" int dmcg_debug_chol(uint32_t n, const uint32_t* faces, uint32_t n_fac
                                const uint32_t* anchors, uint32_t W, const double* b, double* x,
                                double stats[8]) {
   MeshHost m;
+  PhaseTimer tm("debug_chol");
   Status st = build_mesh(faces, n_faces, n, &m);
   if (!st.good()) return st.code;
+  tm.lap("mesh");
   m.anchors.assign(anchors, anchors + n_c);
   m.anchor_pos.assign(n, -1);
   for (uint32_t t = 0; t < n_c; ++t) m.anchor_pos[anchors[t]] = (int32_t)t;
   build_normal_matrix(&m);
+  tm.lap("normal");
   CholPlan p;
   const auto t0 = std::chrono::steady_clock::now();
   chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p);

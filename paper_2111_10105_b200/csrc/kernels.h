@@ -33,7 +33,7 @@ cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
 cudaError_t launch_householder(cudaStream_t s, int nbatch, int m, int p, int c0, int ncols,
                                double* Z, double* tau, double* Qout);
 // Round-robin Jacobi eigensolver of symmetric m x m A (col-major, per
-// batch).  work: nbatch * 2 * m2 * m2 doubles (m2 = m + m%2).  Writes V
+// batch).  work: nbatch * 2 * m2 * (m2 + 1) doubles (m2 = m + m%2).  Writes V
 // (m x m) and w (m).  flags[3] set on non-convergence.
 cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
                           double* V, double* w, int* flags);

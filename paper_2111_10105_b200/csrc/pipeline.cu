@@ -11,9 +11,16 @@
 
 namespace dmcg {
 
+// DMCG_SYNC=1 synchronises after every launch so a fault names its kernel.
+static bool debug_sync() {
+  static const bool on = getenv("DMCG_SYNC") != nullptr;
+  return on;
+}
+
 #define DMCG_TRY(expr)                                                            \
   do {                                                                            \
     cudaError_t _e = (expr);                                                      \
+    if (_e == cudaSuccess && debug_sync()) _e = cudaDeviceSynchronize();          \
     if (_e != cudaSuccess)                                                        \
       return Status{DMCG_E_CUDA, std::string("CudaError: ") + cudaGetErrorString(_e) + \
                                      " at " #expr};                               \

@@ -130,8 +130,10 @@ def test_full_eigenbasis_mode_matches_reference_path(codec):
     check_parity(codec, spec.make(), spec, rounds=0)
 
 
-def test_basis_float_parity_and_orthonormality(codec):
-    spec = synth.CONFIGS["c0"]
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_basis_float_parity_and_orthonormality(codec, name):
+    """c1 has F - k > k: the completion's blocked-QR workspace is wider than the factor's."""
+    spec = synth.CONFIGS[name]
     s = spec.make()
     plan = C.Plan(codec, s.n, s.F, s.faces, _cfg(spec))
     import torch
