@@ -30,9 +30,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2111_10105_b200.shard import (dist_env, max_over_ranks, sequence_for_rank,  # noqa: E402
+                                         whole_job_rate)
+
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 FP64_DMMA_TFLOPS = 37.1  # profiles/r01_peaks.md (tools/peak_fp64.cu)
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_oi_fused launch (c1),
+# from the ncu --set full capture in profiles/ (None until captured)
+OI_TRAFFIC = 1379328  # profiles/r01_ncu_oi_full.md
 
 WORKLOADS = {
     "c0": "c0: icosphere L4 (2562 v), F=64, k=32, 10 OI rounds, 12-bit, fp64",
@@ -42,13 +48,6 @@ WORKLOADS = {
     "c3": "c3: grid 512x512 (262144 v), F=512, k=256, 20 OI rounds, 12-bit, fp32 storage",
     "c4": "c4: icosphere L5 (10242 v) sequences, F=128, k=64, 10 OI rounds, 12-bit, fp64",
 }
-
-
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
 
 
 class Clocks:
@@ -97,28 +96,13 @@ def load_peak():
         return FALLBACK_HBM_GBS, "fallback"
 
 
-def make_sequence(cfgname, rank):
-    from paper_2111_10105_b200 import synth
-    spec = synth.CONFIGS[cfgname]
-    if rank == 0:
-        return spec, spec.make(0)
-    # independent sequence per rank: same generator family, distinct seed
-    if cfgname == "c1":
-        return spec, synth.torus(96, 96, 200, seed=1 + 1000 * rank)
-    if cfgname == "c4":
-        return spec, spec.make(rank)
-    if cfgname == "c0":
-        return spec, synth.sphere(4, 64, 4, 0, seed=1000 * rank)
-    return spec, spec.make(0)
-
-
 def run_reference(args, rank, world):
     """CPU oracle port of the reference path on the host cores (rank 0)."""
     if rank != 0:
         return 0
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
-    spec, s = make_sequence(args.config, 0)
+    spec, s = sequence_for_rank(args.config, 0)
     threads = os.cpu_count() or 1
     vf = s.n * s.F
     times = []
@@ -184,7 +168,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    spec, s = make_sequence(args.config, rank)
+    spec, s = sequence_for_rank(args.config, rank)
     cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds)
     f32 = spec.dtype == "f32"
     npdt = np.float32 if f32 else np.float64
@@ -196,7 +180,7 @@ def main():
     d_out = [torch.empty_like(t) for t in d_in]
     stream = torch.cuda.ExternalStream(plan.stream())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    step_ms, fac_ms, sol_ms, launches = [], [], [], 0
+    step_ms, fac_ms, sol_ms, oi_ms, launches = [], [], [], [], 0
     for it in range(args.warmup):
         plan.encode_device([t.data_ptr() for t in d_in])
         plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
@@ -218,26 +202,28 @@ def main():
             st = plan.stats()
             fac_ms.append(st["ms_factor"])
             sol_ms.append(st["ms_solve"])
+            oi_ms.append(st["ms_oi"])
             launches += st["kernel_launches_encode"] + st["kernel_launches_decode"]
     torch.cuda.synchronize()
-    total_ms = float(sum(step_ms))
+    total_ms = max_over_ranks(float(sum(step_ms)), dist, "cuda")
     if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
     vf_step = s.n * s.F
-    value = vf_step * world * args.steps / (total_ms / 1e3)
+    value = whole_job_rate(vf_step, world, args.steps, total_ms)
 
-    # roofline of the dominant stage, the decode's direct solve (K7: supernodal
-    # Cholesky factor + 2 multi-RHS solves, DMMA): algorithmic flops per
-    # decode (CholPlan::flops_factor + flops_solve) over the
-    # K7 device time measured with CUDA events inside the plan.
+    # roofline of the dominant kernel, k_oi_fused (the fused orthogonal
+    # iterations, one CTA per axis): algorithmic flops per launch
+    # over its launch time, CUDA events around the launch on
+    # the plan stream (stats.ms_oi), median over the timed steps.  The
+    # decode's direct solve (K7) is reported beside it.
     st = plan.stats()
+    oi_flops = float(st["flops_oi"])
+    oi_sec = float(np.median(oi_ms)) / 1e3 if oi_ms else 0.0
+    peak = FP64_DMMA_TFLOPS
+    achieved = oi_flops / oi_sec / 1e12 if oi_sec > 0 else 0.0
     k7_flops = float(st["flops_factor"] + st["flops_solve"])
     k7_sec = float(np.median(fac_ms) + np.median(sol_ms)) / 1e3
-    peak = FP64_DMMA_TFLOPS
-    achieved = k7_flops / k7_sec / 1e12 if k7_sec > 0 else 0.0
+    k7_achieved = k7_flops / k7_sec / 1e12 if k7_sec > 0 else 0.0
 
     # ---- e2e through the drop-in C ABI from pinned host memory -------------
     pinned = [torch.from_numpy(np.ascontiguousarray(x, dtype=npdt)).pin_memory() for x in s.axes]
@@ -253,12 +239,8 @@ def main():
         dt = (time.perf_counter() - t0) * 1e3
         if it > 0:
             e2e_ms.append(dt)
-    e2e_total = float(sum(e2e_ms))
-    if dist:
-        t = torch.tensor([e2e_total], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    e2e_value = vf_step * world * len(e2e_ms) / (e2e_total / 1e3)
+    e2e_total = max_over_ranks(float(sum(e2e_ms)), dist, "cuda")
+    e2e_value = whole_job_rate(vf_step, world, len(e2e_ms), e2e_total)
     es = np.dtype(npdt).itemsize
     enc_bytes = sum(x.nbytes for x in enc.dict_q + enc.row_min + enc.row_max + enc.row_bits +
                     enc.coeff_q + enc.anchor_q) + enc.anchor_idx.nbytes
@@ -281,15 +263,20 @@ def main():
                        "l2": "256 MiB flush between timed steps",
                        "plan": "mesh plan (CSR, anchors, normal matrix) built once outside value; "
                                "inside e2e", "cg_rtol": args.rtol},
-            "roofline": {"kernel": "K7 direct solve (k_panel/k_trailing/k_inv_*/k_fwd*/k_bwd*)",
-                         "bound": "tensor", "achieved": achieved, "peak": peak,
-                         "peak_kind": "measured FP64 DMMA (profiles/r01_peaks.md)",
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
-                         "algorithmic_flops": k7_flops,
-                         "model": "sum over fronts of (m-t)^2 per pivot + w^3/3 inverse; "
-                                  "2 solves x 2(2w^2 + 4w(m-w)) per right-hand side",
-                         "ms_factor": float(np.median(fac_ms)), "ms_solve": float(np.median(sol_ms)),
-                         "supernodes": st["supernodes"], "nnz_factor": st["nnz_factor"]},
+            "roofline": {"kernel": "k_oi_fused", "bound": "tensor", "achieved": achieved,
+                         "peak": peak, "peak_kind": "measured FP64 DMMA, whole GPU (profiles/r01_peaks.md)",
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": OI_TRAFFIC,
+                         "launches_per_step": 1, "ctas": 3,
+                         "algorithmic_flops": oi_flops, "ms": oi_sec * 1e3,
+                         "share_of_step": oi_sec * 1e3 / (total_ms / args.steps),
+                         "model": "3 axes x ((rounds+1) x (2F^2k + 4Fk^2 - 4k^3/3) + 2Fk^2)",
+                         "note": "one CTA per axis (each round depends on the last): the ceiling "
+                                 "is 3/148 of the device peak; see DESIGN.md §5"},
+            "roofline_k7": {"kernel": "K7 direct solve (k_panel/k_trailing/k_inv_*/k_fwd*/k_bwd*)",
+                            "bound": "tensor", "achieved": k7_achieved, "peak": peak, "unit": "TFLOP/s",
+                            "frac": k7_achieved / peak, "algorithmic_flops": k7_flops,
+                            "ms_factor": float(np.median(fac_ms)), "ms_solve": float(np.median(sol_ms)),
+                            "supernodes": st["supernodes"], "nnz_factor": st["nnz_factor"]},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "vertex-frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_total / len(e2e_ms)},

@@ -210,6 +210,8 @@ typedef struct {
   long long nnz_factor;       /* stored entries of the Cholesky factor */
   double flops_factor, flops_solve;  /* per decode */
   double analyze_seconds;     /* host symbolic analysis (plan creation) */
+  float ms_oi;                /* fused orthogonal-iteration kernel (k_oi_fused), last encode */
+  double flops_oi;            /* its algorithmic flops */
 } dmcg_stats;
 int dmcg_plan_stats(const dmcg_plan* plan, dmcg_stats* out);
 /* Stats of the last drop-in dmcg_encode / dmcg_decode on this context. */

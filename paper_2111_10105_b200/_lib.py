@@ -87,7 +87,8 @@ class DmcgStats(ctypes.Structure):
                 ("ms_factor", ctypes.c_float), ("ms_solve", ctypes.c_float), ("solver", ctypes.c_int),
                 ("supernodes", ctypes.c_int), ("levels", ctypes.c_int),
                 ("nnz_factor", ctypes.c_longlong), ("flops_factor", ctypes.c_double),
-                ("flops_solve", ctypes.c_double), ("analyze_seconds", ctypes.c_double)]
+                ("flops_solve", ctypes.c_double), ("analyze_seconds", ctypes.c_double),
+                ("ms_oi", ctypes.c_float), ("flops_oi", ctypes.c_double)]
 
 
 _lib = None

@@ -889,6 +889,8 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
     ctx->last_stats.ms_basis = e.ms_basis;
     ctx->last_stats.ms_project = e.ms_project;
     ctx->last_stats.kernel_launches_encode = e.kernel_launches_encode;
+    ctx->last_stats.ms_oi = e.ms_oi;
+    ctx->last_stats.flops_oi = e.flops_oi;
   }
   dmcg_plan_destroy(p);
   return ctx->set_error(st);
@@ -956,6 +958,8 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
     ctx->last_stats.ms_basis = e.ms_basis;
     ctx->last_stats.ms_project = e.ms_project;
     ctx->last_stats.kernel_launches_encode = e.kernel_launches_encode;
+    ctx->last_stats.ms_oi = e.ms_oi;
+    ctx->last_stats.flops_oi = e.flops_oi;
   }
   dmcg_plan_destroy(p);
   return ctx->set_error(st);

@@ -137,6 +137,7 @@ struct dmcg_plan {
   double *d_rm_y = nullptr, *d_rm_xp = nullptr, *d_rm_r = nullptr;     // permuted / residual
   double analyze_seconds = 0.0;
   bool decode_ready = false;
+  bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
 
   cudaEvent_t ev[8] = {};
   dmcg_stats stats = {};

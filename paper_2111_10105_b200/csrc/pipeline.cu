@@ -163,8 +163,11 @@ Status basis(dmcg_plan* p) {
   // Q0 = qr(start); rounds x {Z = R Q; Q = qr(Z)}; H = Q^T R Q — one fused
   // kernel, one CTA per axis (basis.cu k_oi_fused).
   double* H = p->d_C;  // k x k scratch (coefficient buffer is free here)
+  DMCG_TRY(cudaEventRecord(p->ev[6], s));
   DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H,
                                   p->d_qr_scr));
+  DMCG_TRY(cudaEventRecord(p->ev[7], s));
+  p->oi_timed = true;
   DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
   double* Ws = p->d_Z;  // k x k sorted Ritz vectors (Z is free)
   DMCG_TRY(launch_sort_basis(s, 3, k, k, p->d_V, p->d_w, Ws, (long)k * k, p->d_evals, F));
@@ -229,6 +232,17 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   cudaEventElapsedTime(&p->stats.ms_gram, p->ev[1], p->ev[2]);
   cudaEventElapsedTime(&p->stats.ms_basis, p->ev[2], p->ev[3]);
   cudaEventElapsedTime(&p->stats.ms_project, p->ev[3], p->ev[4]);
+  p->stats.ms_oi = 0.0f;
+  p->stats.flops_oi = 0.0;
+  if (p->oi_timed) {
+    cudaEventElapsedTime(&p->stats.ms_oi, p->ev[6], p->ev[7]);
+    // per axis: (rounds + 1) x {Householder factor 2Fk^2 - 2k^3/3, thin Q 2Fk^2 - 2k^3/3}
+    // + (rounds + 1) x R Q (2F^2 k) + Q^T Z (2Fk^2)
+    const double F = p->F, k = p->k, r = p->rounds;
+    const double qr = 2.0 * (2.0 * F * k * k - 2.0 * k * k * k / 3.0);
+    p->stats.flops_oi = 3.0 * ((r + 1.0) * (qr + 2.0 * F * F * k) + 2.0 * F * k * k);
+    p->oi_timed = false;
+  }
   p->stats.kernel_launches_encode =
       1 + 2 + (p->rounds > 0 && k < F ? 2 * p->rounds + 12 : 3) + 1 + (k > 0 ? 3 : 0) + 1;
   if (flags[0]) {
