@@ -1,5 +1,6 @@
-// K3 — small dense kernels of the temporal basis: Householder QR (rank
-// safe), round-robin Jacobi eigensolver, descending sort, canonical signs.
+// K3 — small dense kernels of the temporal basis: fused orthogonal
+// iterations with a blocked Householder QR (rank safe), round-robin Jacobi
+// eigensolver, descending sort, canonical signs, orthogonal completion.
 // One CTA per axis; matrices are F x k / k x k (F <= 512) and live in L2 /
 // shared memory.  Same algorithms and formulas as the oracle restatement
 // (oracle/dmc_oracle.c: householder_factor, orc_jacobi_eig, orc_basis);
@@ -14,8 +15,7 @@ namespace dmcg {
 
 namespace {
 
-constexpr int kBasisThreads = 1024;
-constexpr int kOiThreads = 512;  // fused OI kernels: 128 registers per thread
+constexpr int kOiThreads = 256;  // fused OI kernels: register-resident QR panels
 
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -30,89 +30,6 @@ __device__ double block_sum(double v, double* red) {
   }
   __syncthreads();
   return red[32];
-}
-
-// Householder QR (Eigen::HouseholderQR / makeHouseholder semantics, see
-// oracle householder_factor): beta = -sign(c0)||x||, tau = (beta-c0)/beta,
-// v = [1; tail/(c0-beta)]; a vanishing tail gives tau = 0, so rank-deficient
-// inputs (the normal case) never divide by zero and Q
-// stays orthonormal.
-__global__ void __launch_bounds__(kBasisThreads)
-    k_householder(int m, int p, int c0, int ncols, double* Zall, double* tauall, double* Qall) {
-  __shared__ double red[33];
-  __shared__ double s_tau, s_den;
-  const int b = blockIdx.x;
-  double* Z = Zall + (size_t)b * m * p;
-  double* tau = tauall + (size_t)b * p;
-  double* Q = Qall + (size_t)b * m * ncols;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int pe = p < m ? p : m;
-  for (int j = 0; j < pe; ++j) {
-    double* x = Z + (size_t)j * m;
-    double part = 0.0;
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) part = __dadd_rn(part, __dmul_rn(x[i], x[i]));
-    const double tail = block_sum(part, red);
-    if (tid == 0) {
-      const double c = x[j];
-      if (tail <= DBL_MIN) {
-        s_tau = 0.0;
-        s_den = 0.0;
-      } else {
-        double bb = sqrt(c * c + tail);
-        if (c >= 0.0) bb = -bb;
-        s_den = c - bb;
-        s_tau = (bb - c) / bb;
-        x[j] = bb;
-      }
-      tau[j] = s_tau;
-    }
-    __syncthreads();
-    const double tj = s_tau, den = s_den;
-    if (tj == 0.0) {
-      for (int i = j + 1 + tid; i < m; i += blockDim.x) x[i] = 0.0;
-      __syncthreads();
-      continue;
-    }
-    for (int i = j + 1 + tid; i < m; i += blockDim.x) x[i] = x[i] / den;
-    __syncthreads();
-    for (int c = j + 1 + warp; c < p; c += nw) {
-      double* y = Z + (size_t)c * m;
-      double d = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) d += x[i] * y[i];
-      d = warp_sum(d);
-      d = tj * (y[j] + d);
-      __syncwarp();
-      if (lane == 0) y[j] = y[j] - d;
-      for (int i = j + 1 + lane; i < m; i += 32) y[i] = y[i] - d * x[i];
-    }
-    __syncthreads();
-  }
-  // Q = H_0 ... H_{p-1} [e_c0 ... e_{c0+ncols-1}], backward accumulation.
-  for (long t = tid; t < (long)m * ncols; t += blockDim.x) Q[t] = 0.0;
-  __syncthreads();
-  for (int c = tid; c < ncols; c += blockDim.x)
-    if (c0 + c < m) Q[(size_t)c * m + c0 + c] = 1.0;
-  __syncthreads();
-  for (int j = pe - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* v = Z + (size_t)j * m;
-    // columns whose identity seed sits above row j are untouched by H_j
-    // only if their current rows >= j are zero: true for c0 + c < j when
-    // c0 == 0 (thin Q); the completion (c0 >= p) touches every column.
-    const int cstart = (c0 == 0) ? (j < ncols ? j : ncols) : 0;
-    for (int c = cstart + warp; c < ncols; c += nw) {
-      double* y = Q + (size_t)c * m;
-      double d = 0.0;
-      for (int i = j + 1 + lane; i < m; i += 32) d += v[i] * y[i];
-      d = warp_sum(d);
-      d = tj * (y[j] + d);
-      __syncwarp();
-      if (lane == 0) y[j] = y[j] - d;
-      for (int i = j + 1 + lane; i < m; i += 32) y[i] = y[i] - d * v[i];
-    }
-    __syncthreads();
-  }
 }
 
 // Parallel (round-robin) cyclic Jacobi.  Every step applies m2/2 disjoint
@@ -349,176 +266,13 @@ __global__ void k_symmetrize(int m, double* Hall) {
 
 // ---------------------------------------------------------------------------
 // Fused orthogonal iterations: one CTA per axis runs every round
-//   Z = R Q  (SIMT, R from L2, Q in smem);  Q = thin Householder Q of Z
+//   Z = R Q  (DMMA, R from L2, Q in smem);  Q = thin Householder Q of Z
 // and the Rayleigh-Ritz matrix H = Q^T R Q, with Z and Q in shared memory
 // when 2 F k doubles fit (else in a global work area, L1/L2 resident).
-// The Householder QR needs one CTA barrier per column: the warp that
-// updates column j+1 in step j also computes column j+1's reflector, and
-// the scaling of reflector j is deferred to step j+1 (column j is read
-// unscaled, divided on the fly, during step j).
 // ---------------------------------------------------------------------------
 struct QrShared {
-  double tau[512], rinv[512];
+  double tau[512];
 };
-
-// Register-blocked warp primitives: a lane owns rows j+1+lane+32t,
-// t < MAXR (MAXR = ceil(F/32) <= 16), so all its loads issue back to back.
-
-// Reflector of column c (rows >= c) by one warp: tau and 1/(c0 - beta), the
-// diagonal set to beta (the oracle's householder_factor formulas; the GPU
-// scales by the reciprocal instead of dividing element by element, a
-// 1-ulp difference inside the P3 tolerance).
-template <int MAXR, typename P>
-__device__ __forceinline__ void qr_reflector(P Z, int m, int c, QrShared& q, int lane) {
-  P x = Z + c * m;
-  double p0 = 0.0, p1 = 0.0;
-#pragma unroll
-  for (int t = 0; t < MAXR; ++t) {
-    const int i = c + 1 + lane + 32 * t;
-    const double xi = i < m ? x[i] : 0.0;
-    if (t & 1)
-      p1 += xi * xi;
-    else
-      p0 += xi * xi;
-  }
-  const double tail = warp_sum(p0 + p1);
-  const double c0 = x[c];
-  double rinv = 0.0, tau = 0.0;
-  if (tail > DBL_MIN) {
-    const double s2 = c0 * c0 + tail;
-    const double r = rsqrt(s2);
-    const double nrm = s2 * r;
-    const double bb = c0 >= 0.0 ? -nrm : nrm;
-    const double ibb = c0 >= 0.0 ? -r : r;
-    rinv = __drcp_rn(c0 - bb);
-    tau = (bb - c0) * ibb;
-    __syncwarp();
-    if (lane == 0) x[c] = bb;
-  }
-  if (lane == 0) {
-    q.tau[c] = tau;
-    q.rinv[c] = rinv;
-  }
-  __syncwarp();
-}
-
-// y_c -= tau v (v^T y_c) for columns c = c0, c0 + stride, ... < cend (rows > j
-// of v are vs * v[i]; v[j] = 1 implicit), two columns per pass so their
-// warp reductions overlap.
-template <int MAXR, typename PY, typename PV>
-__device__ __forceinline__ void apply_reflector_cols(PY Y, int ld, int j, PV v, double vs,
-                                                     double tau, int c0, int cend, int stride,
-                                                     int lane, int m) {
-  if (c0 >= cend) return;
-  double vr[MAXR];
-#pragma unroll
-  for (int t = 0; t < MAXR; ++t) {
-    const int i = j + 1 + lane + 32 * t;
-    vr[t] = i < m ? v[i] * vs : 0.0;
-  }
-  for (int c = c0; c < cend; c += 2 * stride) {
-    const bool two = c + stride < cend;
-    PY ya = Y + c * ld;
-    PY yb = Y + (two ? c + stride : c) * ld;
-    double ra[MAXR], rb[MAXR];
-#pragma unroll
-    for (int t = 0; t < MAXR; ++t) {
-      const int i = j + 1 + lane + 32 * t;
-      ra[t] = i < m ? ya[i] : 0.0;
-      rb[t] = (two && i < m) ? yb[i] : 0.0;
-    }
-    double da0 = 0.0, da1 = 0.0, db0 = 0.0, db1 = 0.0;
-#pragma unroll
-    for (int t = 0; t < MAXR; ++t) {
-      if (t & 1) {
-        da1 += vr[t] * ra[t];
-        db1 += vr[t] * rb[t];
-      } else {
-        da0 += vr[t] * ra[t];
-        db0 += vr[t] * rb[t];
-      }
-    }
-    double da = da0 + da1, db = db0 + db1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      da += __shfl_xor_sync(0xffffffffu, da, o);
-      db += __shfl_xor_sync(0xffffffffu, db, o);
-    }
-    const double yja = ya[j], yjb = two ? yb[j] : 0.0;
-    da = tau * (yja + da);
-    db = tau * (yjb + db);
-    __syncwarp();
-    if (lane == 0) {
-      ya[j] = yja - da;
-      if (two) yb[j] = yjb - db;
-    }
-#pragma unroll
-    for (int t = 0; t < MAXR; ++t) {
-      const int i = j + 1 + lane + 32 * t;
-      if (i < m) {
-        ya[i] = ra[t] - da * vr[t];
-        if (two) yb[i] = rb[t] - db * vr[t];
-      }
-    }
-    __syncwarp();
-  }
-}
-
-template <typename P>
-__device__ __forceinline__ void qr_scale(P Z, int m, int j, const QrShared& q) {
-  P x = Z + j * m;
-  const double r = q.rinv[j];
-  const bool zero = q.tau[j] == 0.0;
-  for (int i = j + 1 + (int)threadIdx.x; i < m; i += blockDim.x) x[i] = zero ? 0.0 : x[i] * r;
-}
-
-// In-place Householder factorisation of the m x p column-major Z; on exit
-// column j below the diagonal holds the scaled reflector (Eigen layout).
-// One CTA barrier per column: reflector j+1 is computed by warp 0 right
-// after it updates column j+1, and the scaling of column j is deferred to
-// step j+1 (during step j the raw column is read and scaled on the fly).
-template <int MAXR, typename P>
-__device__ void qr_factor(P Z, int m, int p, QrShared& q) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int pe = p < m ? p : m;
-  if (pe <= 0) return;
-  if (warp == 0) qr_reflector<MAXR>(Z, m, 0, q, lane);
-  __syncthreads();
-  for (int j = 0; j < pe; ++j) {
-    const double tj = q.tau[j], rj = q.rinv[j];
-    if (j > 0) qr_scale(Z, m, j - 1, q);
-    // warp 0: column j+1 alone, then reflector j+1, then its share of the
-    // rest; columns j+2.. are spread over all warps.
-    if (warp == 0 && j + 1 < p) {
-      if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 1, j + 2, 1, lane, m);
-      if (j + 1 < pe) qr_reflector<MAXR>(Z, m, j + 1, q, lane);
-    }
-    if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 2 + warp, p, nw, lane, m);
-    __syncthreads();
-  }
-  qr_scale(Z, m, pe - 1, q);
-  __syncthreads();
-}
-
-// Qout (m x ncols, leading dimension ldq) = H_0 ... H_{pe-1} [e_c0 ...].
-template <int MAXR, typename PZ, typename PQ>
-__device__ void qr_form(PZ Z, int m, int p, int c0, int ncols, PQ Qo, int ldq, const QrShared& q) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int pe = p < m ? p : m;
-  for (int t = threadIdx.x; t < m * ncols; t += blockDim.x) {
-    const int c = t / m, r = t % m;
-    Qo[c * ldq + r] = (r == c0 + c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int j = pe - 1; j >= 0; --j) {
-    const double tj = q.tau[j];
-    if (tj == 0.0) continue;
-    PZ v = Z + j * m;
-    const int cstart = (c0 == 0) ? (j < ncols ? j : ncols) : 0;
-    apply_reflector_cols<MAXR>(Qo, ldq, j, v, 1.0, tj, cstart + warp, ncols, nw, lane, m);
-    __syncthreads();
-  }
-}
 
 // Z (F x k) = R (F x F, symmetric, global) * Q (F x k) on the FP64 tensor
 // pipe: each warp owns an 8-row block and up to 64 columns (8 DMMA tiles of
@@ -541,15 +295,23 @@ __device__ void warp_gemm_tn(int M, int N, int K, PA A, int lda, PB B, int ldb, 
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u][0] = acc[u][1] = 0.0;
     const int ia = i0 + (lane >> 2);
-    for (int k0 = 0; k0 < K; k0 += 4) {
-      const int ka = k0 + (lane & 3);
-      const double a = (ia < M && ka < K) ? A[ia * lda + ka] : 0.0;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      // the loads of four k-steps issue before their DMMAs (A may stream from L2)
+      double av[4], bv[4][8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int jb = j00 + u * 8 + (lane >> 2);
-        const double b = (jb < N && ka < K) ? B[jb * ldb + ka] : 0.0;
-        dmma884(acc[u], a, b);
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int ka = k0 + 4 * s4 + (lane & 3);
+        av[s4] = (ia < M && ka < K) ? A[ia * lda + ka] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int jb = j00 + u * 8 + (lane >> 2);
+          bv[s4][u] = (jb < N && ka < K) ? B[jb * ldb + ka] : 0.0;
+        }
       }
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dmma884(acc[u], av[s4], bv[s4][u]);
     }
     const int ir = i0 + (lane >> 2);
 #pragma unroll
@@ -565,175 +327,369 @@ __device__ void warp_gemm_tn(int M, int N, int K, PA A, int lda, PB B, int ldb, 
 // Z = R Q: Z(g, j) = sum_f R(g, f) Q(f, j) = sum_f R[g*F + f] Q[j*F + f]
 // (R symmetric, so its column g is its row g).
 template <typename P>
-__device__ void oi_apply(const double* __restrict__ R, int F, int k, P Q, P Z) {
-  warp_gemm_tn(F, k, F, R, F, Q, F, Z, F);
+__device__ void oi_apply(const double* __restrict__ R, int F, int k, P Q, int ld, P Z) {
+  warp_gemm_tn(F, k, F, R, F, Q, ld, Z, ld);
   __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
-// Blocked (compact-WY) Householder QR.  Columns are factored in panels of
-// QNB: only the panel sees per-column steps (one barrier each); the rest of
-// the matrix and the formation of Q are updated with small DMMA GEMMs,
-//   Y <- (I - V T V^T)^T Y,   Q <- (I - V T V^T) Q,
-// T being the LAPACK dlarft forward/columnwise triangular factor.  Scratch
-// (global, L1-resident): T of every panel, W (QNB x ncols), G (QNB x QNB).
+// Blocked (compact-WY) Householder QR with register-resident panels.
+// A panel of PW columns (rows >= its first column) is factored by warp 0
+// entirely in registers — a lane owns rows lane + 32 t — so a column step is
+// a handful of interleaved warp reductions with no CTA barrier.  The warp
+// also forms the panel's dlarft triangle T.  The trailing columns and the
+// thin Q are then updated by all warps with DMMA (mma.sync.m8n8k4.f64):
+//   W = V^T Y,  W = T^T W (factor) / T W (formation),  Y -= V W.
+// Scratch (shared memory when it fits): W (PW x wcols), T of every panel.
+// Reflector formulas are the oracle's householder_factor (tau, beta,
+// v = x / (x0 - beta)); the GPU multiplies by the reciprocal, a 1-ulp
+// difference inside the P3 tolerance.
 // ---------------------------------------------------------------------------
-constexpr int QNB = 16;
+#ifndef PANEL_STAMP
+#define PANEL_STAMP(i)
+#endif
+#ifndef FACT_STAMP
+#define FACT_STAMP(i)
+#endif
 
-// CTA GEMM on the FP64 tensor pipe with functor operands:
-//   for m < M, n < N:  st(m, n, sum_k la(m, k) * lb(k, n))
-template <class LA, class LB, class ST>
-__device__ void cta_gemm(int M, int N, int K, const LA& la, const LB& lb, const ST& st) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int mt = (M + 7) / 8, nt = (N + 31) / 32;
-  for (int t = warp; t < mt * nt; t += nw) {
-    const int m0 = (t % mt) * 8, n0 = (t / mt) * 32;
-    double acc[4][2];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = 0.0;
-    const int ma = m0 + (lane >> 2);
-    for (int k0 = 0; k0 < K; k0 += 4) {
-      const int ka = k0 + (lane & 3);
-      const double a = (ma < M && ka < K) ? la(ma, ka) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int nb = n0 + u * 8 + (lane >> 2);
-        const double b = (nb < N && ka < K) ? lb(ka, nb) : 0.0;
-        dmma884(acc[u], a, b);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int nc = n0 + u * 8 + (lane & 3) * 2 + e;
-        if (ma < M && nc < N) st(ma, nc, acc[u][e]);
-      }
-  }
-  __syncthreads();
-}
+template <int MAXR>
+struct QrPanel {
+  static constexpr int PW = MAXR <= 8 ? 8 : 4;  // a[MAXR][PW] stays in registers
+};
 
-// V(g, i) of the panel starting at column c0, g counted from row c0: unit
-// diagonal, zero above it, the stored (scaled) reflector below.
+// V(g, i) of the panel whose first column is c0 (g relative to row c0):
+// zero above the unit diagonal, the stored reflector below.
 template <typename P>
 struct PanelV {
   P Z;
-  int m, c0;
+  int ld, c0;  // leading dimension of Z, first column of the panel
   __device__ __forceinline__ double operator()(int g, int i) const {
-    return g < i ? 0.0 : (g == i ? 1.0 : Z[(c0 + i) * m + c0 + g]);
+    return g < i ? 0.0 : (g == i ? 1.0 : Z[(c0 + i) * ld + c0 + g]);
   }
 };
 
-// Unblocked factorisation of the panel columns [c0, ce), one barrier per column.
-template <int MAXR, typename P>
-__device__ void panel_factor(P Z, int m, int c0, int ce, QrShared& q) {
+// Leading dimension of F-row matrices in shared memory: odd, so the 8 rows
+// x 4 columns of a DMMA fragment fall on distinct banks.
+__host__ __device__ __forceinline__ int odd_ld(int F) { return F | 1; }
+
+template <int MAXR, int PW, typename P>
+__device__ __noinline__ void warp_panel_qr(P Z, int m, int ld, int c0, int pb, double* tau,
+                                           int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int M = m - c0;
+  P base = Z + c0 * ld + c0;
+  PANEL_STAMP(0);
+  double a[MAXR][PW];
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t)
+#pragma unroll
+    for (int c = 0; c < PW; ++c) {
+      const int g = lane + 32 * t;
+      a[t][c] = (c < pb && g < M) ? base[c * ld + g] : 0.0;
+    }
+  PANEL_STAMP(1);
+  double tv[PW];
+#pragma unroll
+  for (int j = 0; j < PW; ++j) {
+    // columns j >= pb are zero: their reflector is the identity (tail 0,
+    // tau 0), so no branch on pb is needed around the shuffles below
+    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int g = lane + 32 * t;
+      const double x = g > j ? a[t][j] : 0.0;
+      if (t & 1)
+        p1 = fma(x, x, p1);
+      else
+        p0 = fma(x, x, p0);
+    }
+    const double tail = warp_sum(p0 + p1);
+    const double x0 = __shfl_sync(FULL, a[0][j], j);
+    double rinv = 0.0, tj = 0.0, beta = x0;
+    if (tail > DBL_MIN) {
+      const double s2 = x0 * x0 + tail;
+      const double r = rsqrt(s2);
+      const double nrm = s2 * r;
+      beta = x0 >= 0.0 ? -nrm : nrm;
+      const double ibb = x0 >= 0.0 ? -r : r;
+      rinv = __drcp_rn(x0 - beta);
+      tj = (beta - x0) * ibb;
+    }
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int g = lane + 32 * t;
+      if (g > j) a[t][j] *= rinv;
+    }
+    if (lane == j) a[0][j] = beta;
+    tv[j] = tj;
+    // H_j applied to the panel columns l > j: d_l = y_l[j] + v^T y_l (rows > j)
+    double d[PW];
+#pragma unroll
+    for (int l = 0; l < PW; ++l) {
+      d[l] = 0.0;
+      if (l > j) {
+#pragma unroll
+        for (int t = 0; t < MAXR; ++t) {
+          const int g = lane + 32 * t;
+          if (g > j) d[l] = fma(a[t][j], a[t][l], d[l]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l > j) d[l] += __shfl_xor_sync(FULL, d[l], o);
+#pragma unroll
+    for (int l = 0; l < PW; ++l) {
+      if (l <= j) continue;
+      const double yj = __shfl_sync(FULL, a[0][l], j);
+      const double s = tj * (yj + d[l]);
+#pragma unroll
+      for (int t = 0; t < MAXR; ++t) {
+        const int g = lane + 32 * t;
+        if (g > j) a[t][l] = fma(-s, a[t][j], a[t][l]);
+      }
+      if (lane == j) a[0][l] -= s;
+    }
+  }
+  PANEL_STAMP(2);
+  PANEL_STAMP(3);
+  // write the factored panel back
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t)
+#pragma unroll
+    for (int c = 0; c < PW; ++c) {
+      const int g = lane + 32 * t;
+      if (c < pb && g < M) base[c * ld + g] = a[t][c];
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+      if (j < pb) tau[c0 + j] = tv[j];
+  PANEL_STAMP(4);
+}
+
+// dlarft: T (PW x PW row-major, upper) from G(l, i) = v_l^T v_i (row-major,
+// ld ldg) and tau; lane j of warp 0 forms row j:
+//   T(j, j) = tau_j,  T(j, i) = -tau_i sum_{l=j}^{i-1} T(j, l) G(l, i).
+template <int PW>
+__device__ void panel_T(const double* G, int ldg, const double* tau, int pb, double* T,
+                        int lane) {
+  if (lane >= PW) return;
+  const int j = lane;
+  double tr[PW];
+#pragma unroll
+  for (int i = 0; i < PW; ++i) {
+    double v = 0.0;
+    if (i < pb && i == j) v = tau[i];
+    if (i < pb && i > j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l < i && l >= j) acc = fma(tr[l], G[l * ldg + i], acc);
+      v = -tau[i] * acc;
+    }
+    tr[i] = j < pb ? v : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < PW; ++i) T[j * PW + i] = tr[i];
+}
+
+// Branch-free operand fetch: element g of column `col` (pointer to its row
+// c0) masked to V's shape — zero above the unit diagonal at `diag` (diag < 0:
+// a plain column) and zero past the M rows / outside the tile.
+__device__ __forceinline__ double vfetch(const double* col, int g, int M, int diag, bool valid) {
+  const double x = col[g < M ? g : M - 1];
+  const double v = diag < 0 ? x : (g > diag ? x : (g == diag ? 1.0 : 0.0));
+  return (valid && g < M) ? v : 0.0;
+}
+
+// W (PW x nc, row-major) = V^T [V_nv | Y] over the rows g < M of the panel:
+// the first nv right-hand columns are V's own (G = V^T V), the rest Y.  One
+// warp per 8-column tile; K = M in steps of 16 with the next step's
+// operands loaded before the current step's DMMAs (four accumulators).
+template <int PW, typename PZ, typename PY>
+__device__ void wy_vty(const PanelV<PZ>& V, int M, int pb, int nv, PY Y, int ldy, int nc,
+                       double* W) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (warp == 0) qr_reflector<MAXR>(Z, m, c0, q, lane);
-  __syncthreads();
-  for (int j = c0; j < ce; ++j) {
-    const double tj = q.tau[j], rj = q.rinv[j];
-    if (j > c0) qr_scale(Z, m, j - 1, q);
-    if (warp == 0 && j + 1 < ce) {
-      if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 1, j + 2, 1, lane, m);
-      qr_reflector<MAXR>(Z, m, j + 1, q, lane);
+  const int i = lane >> 2, q = lane & 3;
+  const int ic = i < pb ? i : pb - 1;
+  const double* acol = V.Z + (V.c0 + ic) * V.ld + V.c0;
+  const bool avalid = i < pb;
+  for (int ct = warp; ct * 8 < nc; ct += nw) {
+    const int c = ct * 8 + i;
+    const bool bvalid = c < nc;
+    const int cc = bvalid ? c : nc - 1;
+    const double* bcol = cc < nv ? V.Z + (V.c0 + cc) * V.ld + V.c0 : Y + (cc - nv) * ldy;
+    const int bdiag = cc < nv ? cc : -1;
+    double acc[4][2] = {};
+    double av[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      av[u] = vfetch(acol, 4 * u + q, M, ic, avalid);
+      bv[u] = vfetch(bcol, 4 * u + q, M, bdiag, bvalid);
     }
-    if (tj != 0.0) apply_reflector_cols<MAXR>(Z, m, j, Z + j * m, rj, tj, j + 2 + warp, ce, nw, lane, m);
-    __syncthreads();
-  }
-  qr_scale(Z, m, ce - 1, q);
-  __syncthreads();
-}
-
-// T (row-major QNB x QNB, upper) of the panel [c0, c0+pb): T(i,i) = tau_i,
-// T(0:i, i) = -tau_i T(0:i, 0:i) (V(:, 0:i)^T v_i).
-template <typename P>
-__device__ void panel_T(P Z, int m, int c0, int pb, const QrShared& q, double* T, double* G) {
-  PanelV<P> V{Z, m, c0};
-  cta_gemm(pb, pb, m - c0, [&](int a, int g) { return V(g, a); }, V,
-           [&](int a, int b, double v) { G[a * QNB + b] = v; });
-  if (threadIdx.x < 32) {
-    const int j = threadIdx.x;
-    for (int i = 0; i < pb; ++i) {
-      const double ti = q.tau[c0 + i];
-      if (j < i) {
-        double acc = 0.0;
-        for (int l = j; l < i; ++l) acc += T[j * QNB + l] * G[l * QNB + i];
-        T[j * QNB + i] = -ti * acc;
+    for (int k0 = 16; k0 < M + 16; k0 += 16) {
+      double an[4], bn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        an[u] = vfetch(acol, k0 + 4 * u + q, M, ic, avalid);
+        bn[u] = vfetch(bcol, k0 + 4 * u + q, M, bdiag, bvalid);
       }
-      if (j == i) T[i * QNB + i] = ti;
-      if (j > i && j < QNB) T[j * QNB + i] = 0.0;
-      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma884(acc[u], av[u], bv[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = an[u];
+        bv[u] = bn[u];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int co = ct * 8 + q * 2 + e;
+      if (i < PW && co < nc) W[i * nc + co] = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
     }
   }
-  __syncthreads();
 }
 
+// W <- T^T W (trans) or T W, T upper triangular (PW x PW row-major).
+template <int PW>
+__device__ void wy_tw(const double* T, int pb, double* W, int ldw, int nc, bool trans) {
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    double w[PW], o[PW];
+#pragma unroll
+    for (int i = 0; i < PW; ++i) w[i] = i < pb ? W[i * ldw + c] : 0.0;
+#pragma unroll
+    for (int i = 0; i < PW; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < PW; ++l) {
+        if (trans ? (l <= i) : (l >= i)) acc = fma(trans ? T[l * PW + i] : T[i * PW + l], w[l], acc);
+      }
+      o[i] = acc;
+    }
+#pragma unroll
+    for (int i = 0; i < PW; ++i)
+      if (i < pb) W[i * ldw + c] = o[i];
+  }
+}
+
+// Y (rows g < M, nc columns) -= V W; one warp per 8-row tile with the V
+// fragment in registers, the column tiles in groups of four whose W and Y
+// fragments are all loaded before their DMMAs.
+template <int PW, typename PZ, typename PY>
+__device__ void wy_update(const PanelV<PZ>& V, int M, int pb, PY Y, int ldy, int nc,
+                          const double* W, int ldw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int nct = (nc + 7) / 8;
+  for (int mt = warp; mt * 8 < M; mt += nw) {
+    const int g = mt * 8 + r;
+    double av[PW / 4];
+#pragma unroll
+    for (int u = 0; u < PW / 4; ++u) {
+      const int i = 4 * u + q;
+      const int icl = i < pb ? i : pb - 1;
+      av[u] = vfetch(V.Z + (V.c0 + icl) * V.ld + V.c0, g, M, icl, i < pb);
+    }
+    const int gc = g < M ? g : M - 1;
+    for (int ct0 = 0; ct0 < nct; ct0 += 4) {
+      double bw[4][PW / 4], yv[4][2], acc[4][2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+#pragma unroll
+        for (int u = 0; u < PW / 4; ++u) {
+          const int i = 4 * u + q, c = (ct0 + t) * 8 + r;
+          const bool ok = i < pb && c < nc;
+          bw[t][u] = ok ? W[(i < pb ? i : 0) * ldw + (c < nc ? c : 0)] : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = (ct0 + t) * 8 + 2 * q + e;
+          yv[t][e] = Y[(c < nc ? c : nc - 1) * ldy + gc];
+          acc[t][e] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < PW / 4; ++u) dmma884(acc[t], av[u], bw[t][u]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = (ct0 + t) * 8 + 2 * q + e;
+          if (g < M && c < nc) Y[c * ldy + g] = yv[t][e] - acc[t][e];
+        }
+    }
+  }
+}
+
+// Householder factor of the p columns of Z (m x p, in place): R on and
+// above the diagonal, V below, tau[j]; T of panel b at Ts + b PW^2.
 template <int MAXR, typename P>
-__device__ void bqr_factor(P Z, int m, int p, QrShared& q, double* scr, int wcols) {
+__device__ void wqr_factor(P Z, int m, int ld, int p, double* tau, double* scr, int wcols) {
+  constexpr int PW = QrPanel<MAXR>::PW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pe = p < m ? p : m;
-  double* G = scr;                 // QNB x QNB
-  double* W = G + QNB * QNB;       // QNB x wcols (wcols >= p)
-  double* Ts = W + QNB * wcols;    // T of every panel
-  for (int c0 = 0; c0 < pe; c0 += QNB) {
-    const int pb = min(QNB, pe - c0);
-    panel_factor<MAXR>(Z, m, c0, c0 + pb, q);
-    double* T = Ts + (c0 / QNB) * QNB * QNB;
-    panel_T(Z, m, c0, pb, q, T, G);
-    const int rem = p - (c0 + pb);
-    if (rem <= 0) continue;
-    PanelV<P> V{Z, m, c0};
-    P Y = Z + (c0 + pb) * m + c0;  // rows c0.., columns c0+pb..
-    // W = V^T Y
-    cta_gemm(pb, rem, m - c0, [&](int i, int g) { return V(g, i); },
-             [&](int g, int c) { return Y[c * m + g]; }, [&](int i, int c, double v) { W[i * rem + c] = v; });
-    // W <- T^T W  (row i needs rows l <= i: descending in place)
-    for (int c = threadIdx.x; c < rem; c += blockDim.x)
-      for (int i = pb - 1; i >= 0; --i) {
-        double acc = 0.0;
-        for (int l = 0; l <= i; ++l) acc += T[l * QNB + i] * W[l * rem + c];
-        W[i * rem + c] = acc;
-      }
+  double* W = scr;                   // PW x (pb + rem): [G | V^T Y]
+  double* Ts = scr + PW * (wcols + PW);
+  for (int c0 = 0; c0 < pe; c0 += PW) {
+    const int pb = min(PW, pe - c0);
+    double* T = Ts + (c0 / PW) * PW * PW;
+    FACT_STAMP(0);
+    if (warp == 0) warp_panel_qr<MAXR, PW>(Z, m, ld, c0, pb, tau, lane);
     __syncthreads();
-    // Y -= V W
-    cta_gemm(m - c0, rem, pb, V, [&](int i, int c) { return W[i * rem + c]; },
-             [&](int g, int c, double v) { Y[c * m + g] -= v; });
+    FACT_STAMP(1);
+    const int rem = p - (c0 + pb), ncw = pb + max(rem, 0);
+    const PanelV<P> V{Z, ld, c0};
+    P Y = Z + (c0 + pb) * ld + c0;
+    wy_vty<PW>(V, m - c0, pb, pb, Y, ld, ncw, W);   // one pass: G = V^T V and V^T Y
+    __syncthreads();
+    FACT_STAMP(2);
+    if (warp == 0) panel_T<PW>(W, ncw, tau + c0, pb, T, lane);
+    __syncthreads();
+    FACT_STAMP(3);
+    if (rem <= 0) continue;
+    wy_tw<PW>(T, pb, W + pb, ncw, rem, true);
+    __syncthreads();
+    FACT_STAMP(4);
+    wy_update<PW>(V, m - c0, pb, Y, ld, rem, W + pb, ncw);
+    __syncthreads();
+    FACT_STAMP(5);
   }
 }
 
-// Qout (m x ncols, leading dimension ldq) = H_0 ... H_{pe-1} [e_cid ...].
-template <typename PZ, typename PQ>
-__device__ void bqr_form(PZ Z, int m, int p, int cid, int ncols, PQ Qo, int ldq, double* scr,
-                         int wcols) {
+// Qout (m x ncols, leading dimension ldq) = H_0 ... H_{pe-1} [e_cid ...]
+// from the factor of wqr_factor (same scratch).
+template <int MAXR, typename PZ, typename PQ>
+__device__ void wqr_form(PZ Z, int m, int ldz, int p, int cid, int ncols, PQ Qo, int ldq,
+                         double* scr, int wcols) {
+  constexpr int PW = QrPanel<MAXR>::PW;
   const int pe = p < m ? p : m;
-  double* W = scr + QNB * QNB;     // QNB x wcols (wcols >= ncols)
-  const double* Ts = W + QNB * wcols;
+  double* W = scr;
+  const double* Ts = scr + PW * (wcols + PW);
   for (int t = threadIdx.x; t < m * ncols; t += blockDim.x) {
     const int c = t / m, r = t % m;
     Qo[c * ldq + r] = (r == cid + c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  const int npan = (pe + QNB - 1) / QNB;
+  const int npan = (pe + PW - 1) / PW;
   for (int pi = npan - 1; pi >= 0; --pi) {
-    const int c0 = pi * QNB, pb = min(QNB, pe - c0);
-    const double* T = Ts + pi * QNB * QNB;
-    PanelV<PZ> V{Z, m, c0};
-    // columns whose rows >= c0 are still zero are untouched (thin Q: c < c0)
+    const int c0 = pi * PW, pb = min(PW, pe - c0);
+    // thin Q: columns c < c0 are still e_c, zero on the rows this panel touches
     const int cs = (cid == 0) ? (c0 < ncols ? c0 : ncols) : 0;
     const int nc = ncols - cs;
     if (nc <= 0) continue;
+    const PanelV<PZ> V{Z, ldz, c0};
     PQ Y = Qo + cs * ldq + c0;
-    cta_gemm(pb, nc, m - c0, [&](int i, int g) { return V(g, i); },
-             [&](int g, int c) { return Y[c * ldq + g]; }, [&](int i, int c, double v) { W[i * nc + c] = v; });
-    // W <- T W  (row i needs rows l >= i: ascending in place)
-    for (int c = threadIdx.x; c < nc; c += blockDim.x)
-      for (int i = 0; i < pb; ++i) {
-        double acc = 0.0;
-        for (int l = i; l < pb; ++l) acc += T[i * QNB + l] * W[l * nc + c];
-        W[i * nc + c] = acc;
-      }
+    wy_vty<PW>(V, m - c0, pb, 0, Y, ldq, nc, W);
     __syncthreads();
-    cta_gemm(m - c0, nc, pb, V, [&](int i, int c) { return W[i * nc + c]; },
-             [&](int g, int c, double v) { Y[c * ldq + g] -= v; });
+    wy_tw<PW>(Ts + pi * PW * PW, pb, W, nc, nc, false);
+    __syncthreads();
+    wy_update<PW>(V, m - c0, pb, Y, ldq, nc, W, nc);
+    __syncthreads();
   }
 }
 
@@ -741,20 +697,20 @@ template <int MAXR, typename P>
 __device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
                         const double* __restrict__ start, P Z, P Q, double* Qo, double* H,
                         QrShared& q, double* scr) {
-  const int Fk = F * k;
-  for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = start[t];
+  const int ld = odd_ld(F);  // Z and Q: F x k, leading dimension ld
+  for (int t = threadIdx.x; t < F * k; t += blockDim.x) Z[(t / F) * ld + t % F] = start[t];
   __syncthreads();
-  bqr_factor<MAXR>(Z, F, k, q, scr, k);
-  bqr_form(Z, F, k, 0, k, Q, F, scr, k);
+  wqr_factor<MAXR>(Z, F, ld, k, q.tau, scr, k);
+  wqr_form<MAXR>(Z, F, ld, k, 0, k, Q, ld, scr, k);
   for (int r = 0; r < rounds; ++r) {
-    oi_apply(R, F, k, Q, Z);
-    bqr_factor<MAXR>(Z, F, k, q, scr, k);
-    bqr_form(Z, F, k, 0, k, Q, F, scr, k);
+    oi_apply(R, F, k, Q, ld, Z);
+    wqr_factor<MAXR>(Z, F, ld, k, q.tau, scr, k);
+    wqr_form<MAXR>(Z, F, ld, k, 0, k, Q, ld, scr, k);
   }
   // Rayleigh-Ritz: H = Q^T (R Q), symmetrised; Q out.
-  oi_apply(R, F, k, Q, Z);
+  oi_apply(R, F, k, Q, ld, Z);
   // H(i, j) = sum_g Q(g, i) Z(g, j), then symmetrised like the oracle
-  warp_gemm_tn(k, k, F, Q, F, Z, F, H, k);
+  warp_gemm_tn(k, k, F, Q, ld, Z, ld, H, k);
   __syncthreads();
   for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
     const int i = t % k, j = t / k;
@@ -763,7 +719,7 @@ __device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
     H[j * k + i] = sv;
     H[i * k + j] = sv;
   }
-  for (int t = threadIdx.x; t < Fk; t += blockDim.x) Qo[t] = Q[t];
+  for (int t = threadIdx.x; t < F * k; t += blockDim.x) Qo[t] = Q[(t / F) * ld + t % F];
 }
 
 template <bool SMEM, int MAXR>
@@ -774,14 +730,14 @@ __global__ void __launch_bounds__(kOiThreads)
   extern __shared__ double dyn[];
   __shared__ QrShared q;
   const int b = blockIdx.x;
-  const size_t Fk = (size_t)F * k;
+  const size_t Fk = (size_t)F * k, Lk = (size_t)odd_ld(F) * k;
   const double* R = Rall + (size_t)b * F * F;
-  double* scr = scr_smem ? dyn + (SMEM ? 2 * Fk : 0) : scr_all + b * scr_stride;
+  double* scr = scr_smem ? dyn + (SMEM ? 2 * Lk : 0) : scr_all + b * scr_stride;
   if (SMEM)
-    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Fk, Qall + b * Fk,
+    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Lk, Qall + b * Fk,
                   Hall + (size_t)b * k * k, q, scr);
   else
-    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Fk, work + b * 2 * Fk + Fk,
+    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Lk, work + b * 2 * Lk + Lk,
                   Qall + b * Fk, Hall + (size_t)b * k * k, q, scr);
 }
 
@@ -794,20 +750,15 @@ __global__ void __launch_bounds__(kOiThreads)
   extern __shared__ double dyn[];
   __shared__ QrShared q;
   const int b = blockIdx.x;
-  const int Fk = F * k;
-  double* Z = SMEM ? dyn : work + (size_t)b * Fk;
+  const int ld = odd_ld(F), Lk = ld * k;
+  double* Z = SMEM ? dyn : work + (size_t)b * Lk;
   double* U = Uall + (size_t)b * F * F;
-  double* scr = scr_smem ? dyn + (SMEM ? Fk : 0) : scr_all + b * scr_stride;
+  double* scr = scr_smem ? dyn + (SMEM ? Lk : 0) : scr_all + b * scr_stride;
   const int wc = k > F - k ? k : F - k;
-  for (int t = threadIdx.x; t < Fk; t += blockDim.x) Z[t] = U[t];
+  for (int t = threadIdx.x; t < F * k; t += blockDim.x) Z[(t / F) * ld + t % F] = U[t];
   __syncthreads();
-  if (SMEM) {
-    bqr_factor<MAXR>(dyn, F, k, q, scr, wc);
-    bqr_form(dyn, F, k, k, F - k, U + Fk, F, scr, wc);
-  } else {
-    bqr_factor<MAXR>(Z, F, k, q, scr, wc);
-    bqr_form(Z, F, k, k, F - k, U + Fk, F, scr, wc);
-  }
+  wqr_factor<MAXR>(Z, F, ld, k, q.tau, scr, wc);
+  wqr_form<MAXR>(Z, F, ld, k, k, F - k, U + (size_t)F * k, F, scr, wc);
 }
 
 __global__ void k_fill_zero(double* p, long count) {
@@ -817,11 +768,6 @@ __global__ void k_fill_zero(double* p, long count) {
 
 }  // namespace
 
-cudaError_t launch_householder(cudaStream_t s, int nbatch, int m, int p, int c0, int ncols,
-                               double* Z, double* tau, double* Qout) {
-  k_householder<<<nbatch, kBasisThreads, 0, s>>>(m, p, c0, ncols, Z, tau, Qout);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_sort_basis(cudaStream_t s, int nbatch, int m, int ncols_store, const double* V,
                               const double* w, double* Vs, long vs_bs, double* ws, long ws_bs) {
@@ -849,12 +795,12 @@ static cudaError_t set_smem_attr(const void* fn, size_t bytes) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-constexpr size_t kBasisSmemMax = 200 * 1024;  // + ~17 KB static QrShared <= 227 KB
 
-// Blocked-QR scratch: G (QNB^2) | W (QNB x wcols) | T of every panel.
+// Blocked-QR scratch: W (PW x (wcols + PW)) | T of every panel (PW = 8, or
+// 4 when F > 256: the bound below covers both).
 static size_t qr_scratch(int wcols, int k) {
-  const int npan = (k + QNB - 1) / QNB;
-  return (size_t)QNB * QNB + (size_t)QNB * wcols + (size_t)npan * QNB * QNB;
+  constexpr int PW = 8;
+  return (size_t)PW * (wcols + PW) + (size_t)((k + 3) / 4) * 16 + (size_t)((k + PW - 1) / PW) * PW * PW;
 }
 
 size_t qr_scratch_doubles(int F, int k) { return qr_scratch(F > k ? F : k, k); }
@@ -903,10 +849,10 @@ template <int MAXR>
 static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                  const double* R, const double* start, double* Q, double* H,
                                  double* work, double* scr) {
-  const size_t pair = (size_t)2 * F * k * sizeof(double);
+  const size_t pair = (size_t)2 * odd_ld(F) * k * sizeof(double);
   const size_t sbytes = qr_scratch(k, k) * sizeof(double);
   const size_t ss = qr_scratch_doubles(F, k);
-  if (pair <= kBasisSmemMax) {
+  if (pair <= smem_room((const void*)k_oi_fused<true, MAXR>)) {
     const void* fn = (const void*)k_oi_fused<true, MAXR>;
     const int in_smem = pair + sbytes <= smem_room(fn);
     const size_t smem = pair + (in_smem ? sbytes : 0);
@@ -938,10 +884,10 @@ cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds
 template <int MAXR>
 static cudaError_t complete_impl(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
                                  double* scr) {
-  const size_t zb = (size_t)F * k * sizeof(double);
+  const size_t zb = (size_t)odd_ld(F) * k * sizeof(double);
   const size_t sbytes = qr_scratch(k > F - k ? k : F - k, k) * sizeof(double);
   const size_t ss = qr_scratch_doubles(F, k);
-  if (zb <= kBasisSmemMax) {
+  if (zb <= smem_room((const void*)k_complete<true, MAXR>)) {
     const void* fn = (const void*)k_complete<true, MAXR>;
     const int in_smem = zb + sbytes <= smem_room(fn);
     const size_t smem = zb + (in_smem ? sbytes : 0);

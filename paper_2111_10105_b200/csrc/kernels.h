@@ -27,11 +27,7 @@ cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long 
 cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
                            const void* const x[3], bool f32, int bits, float* rng, uint16_t* q);
 
-// ---- basis.cu (compiled with --fmad=false) ------------------------------
-// Householder factor of p columns of Z (m x p, per batch, in place) and
-// Qout (m x ncols) = H_0 ... H_{p-1} [e_c0 ... e_{c0+ncols-1}].
-cudaError_t launch_householder(cudaStream_t s, int nbatch, int m, int p, int c0, int ncols,
-                               double* Z, double* tau, double* Qout);
+// ---- basis.cu --------------------------------------------------------------
 // Round-robin Jacobi eigensolver of symmetric m x m A (col-major, per
 // batch).  work: nbatch * 2 * m2 * (m2 + 1) doubles (m2 = m + m%2).  Writes V
 // (m x m) and w (m).  flags[3] set on non-convergence.
