@@ -7,9 +7,15 @@
 // reductions run in parallel order and use FMA, so results agree with the
 // oracle to rounding, not bit for bit (P3).
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace dmcg {
 
@@ -324,13 +330,6 @@ __device__ void warp_gemm_tn(int M, int N, int K, PA A, int lda, PB B, int ldb, 
   }
 }
 
-// Z = R Q: Z(g, j) = sum_f R(g, f) Q(f, j) = sum_f R[g*F + f] Q[j*F + f]
-// (R symmetric, so its column g is its row g).
-template <typename P>
-__device__ void oi_apply(const double* __restrict__ R, int F, int k, P Q, int ld, P Z) {
-  warp_gemm_tn(F, k, F, R, F, Q, ld, Z, ld);
-  __syncthreads();
-}
 
 // ---------------------------------------------------------------------------
 // Blocked (compact-WY) Householder QR with register-resident panels.
@@ -693,23 +692,209 @@ __device__ void wqr_form(PZ Z, int m, int ldz, int p, int cid, int ncols, PQ Qo,
   }
 }
 
-template <int MAXR, typename P>
+// ---------------------------------------------------------------------------
+// Z = R Q spread over a thread-block cluster of `cs` CTAs per axis.  The QR
+// is sequential and stays on the cluster's rank-0 CTA; the product (63 % of
+// an OI round's flops) is split by row blocks over the cluster.  Q goes out
+// through L2 (qbuf, written by rank 0), the Z blocks come back through
+// distributed shared memory; two cluster barriers per round (release /
+// acquire at cluster scope).
+// ---------------------------------------------------------------------------
+__device__ long long g_oi_prof[256];  // per-CTA cycle split of the last k_oi_fused (DMCG_DEBUG)
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Rows [8 mt0, 8 mt1) of Z = R Q: 8-row x 16-column DMMA tasks over the
+// warps of this CTA; A = rows 8 mt0.. of R (shared memory when staged, else
+// L2; loaded two 16-deep k-batches ahead of the DMMAs), B = Q.
+template <typename PQ, typename PZ>
+__device__ void rq_tasks(const double* R, int ldr, int F, int k, PQ Qb, int ldq, PZ Zo, int ldz,
+                         int mt0, int mt1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nt = (k + 15) / 16, ntask = (mt1 - mt0) * nt;
+  const int r = lane >> 2, q = lane & 3;
+  for (int t = warp; t < ntask; t += nw) {
+    const int m0 = (mt0 + t % (mt1 - mt0)) * 8, n0 = (t / (mt1 - mt0)) * 16;
+    const int g = m0 + r, gc = g < F ? g : F - 1;
+    const int c0 = n0 + r, c1 = n0 + 8 + r;
+    const int cc0 = c0 < k ? c0 : k - 1, cc1 = c1 < k ? c1 : k - 1;
+    // row g of R (= column g, R symmetric); R holds rows from 8 mt0 on
+    const double* Ar = R + (size_t)(gc - 8 * mt0) * ldr;
+    double acc[2][2][2] = {};
+    double a0[4], a1[4];
+    auto fetch_a = [&](int k0, double* a) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = k0 + 4 * u + q;
+        a[u] = kk < F ? Ar[kk] : 0.0;
+      }
+    };
+    fetch_a(0, a0);
+    fetch_a(16, a1);
+    for (int k0 = 0; k0 < F; k0 += 16) {
+      double an[4];
+      fetch_a(k0 + 32, an);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = k0 + 4 * u + q, kc = kk < F ? kk : F - 1;
+        const double y0 = kk < F ? Qb[cc0 * ldq + kc] : 0.0;
+        const double y1 = kk < F ? Qb[cc1 * ldq + kc] : 0.0;
+        dmma884(acc[u & 1][0], a0[u], y0);
+        dmma884(acc[u & 1][1], a0[u], y1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0[u] = a1[u];
+        a1[u] = an[u];
+      }
+    }
+    if (g < F)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = n0 + 8 * h + 2 * q + e;
+          if (c < k) Zo[c * ldz + g] = acc[0][h][e] + acc[1][h][e];
+        }
+  }
+}
+
+// Row block of the Z = R Q tasks owned by cluster rank `rank`: ranks 1..cs-1
+// split the 8-row tiles (rank 0 runs the QR); cs == 1: everything.
+__device__ __forceinline__ void rq_rows(int F, int rank, int cs, int* mt0, int* mt1) {
+  const int mt = (F + 7) / 8;
+  if (cs == 1) {
+    *mt0 = 0;
+    *mt1 = mt;
+    return;
+  }
+  *mt0 = (int)((long)mt * (rank - 1) / (cs - 1));
+  *mt1 = (int)((long)mt * rank / (cs - 1));
+}
+
+// All CTAs of the cluster call this (same arguments except rank).  Rank 0
+// publishes Q to L2 (qbuf); ranks > 0 copy it into their own shared memory
+// and compute their rows of Z from their resident rows of R (Rs, staged once
+// per kernel, leading dimension ldr), storing them straight into rank 0's Z
+// (distributed shared memory, or the global work area when Z does not fit
+// on chip).
+template <bool SMEM, int MAXR, typename P>
+__device__ void oi_apply_cluster(const double* R, int ldr, int F, int k, P Q, int ld, P Z,
+                                 double* qbuf, int rank, int cs) {
+  int mt0, mt1;
+  rq_rows(F, rank, cs, &mt0, &mt1);
+  if (cs == 1) {
+    rq_tasks(R, ldr, F, k, Q, ld, Z, ld, mt0, mt1);
+    __syncthreads();
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (rank == 0) {
+    for (int c = warp; c < k; c += nw) {
+      double v[MAXR];
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) {
+        const int r = lane + 32 * u;
+        v[u] = r < F ? Q[c * ld + r] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) {
+        const int r = lane + 32 * u;
+        if (r < F) qbuf[c * F + r] = v[u];
+      }
+    }
+    __threadfence();
+  }
+  cluster_sync_all();
+  if (rank != 0) {
+    const double* Qsrc = qbuf;
+    int ldqs = F;
+    if (SMEM) {
+      // this CTA's copy of Q (its own Q area is free): four columns in flight per warp
+      for (int c0 = warp * 4; c0 < k; c0 += nw * 4) {
+        double v[4][MAXR];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int u = 0; u < MAXR; ++u) {
+            const int r = lane + 32 * u, c = c0 + j;
+            v[j][u] = (r < F && c < k) ? __ldcg(qbuf + c * F + r) : 0.0;
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int u = 0; u < MAXR; ++u) {
+            const int r = lane + 32 * u, c = c0 + j;
+            if (r < F && c < k) Q[c * ld + r] = v[j][u];
+          }
+      }
+      __syncthreads();
+      Qsrc = Q;
+      ldqs = ld;
+    }
+    // (global path: Z, Q in the work area; read Q from L2, the barrier invalidated L1)
+    P Zdst = SMEM ? cg::this_cluster().map_shared_rank(Z, 0) : Z;
+    if (mt1 > mt0) rq_tasks(R, ldr, F, k, Qsrc, ldqs, Zdst, ld, mt0, mt1);
+  }
+  cluster_sync_all();
+}
+
+template <bool SMEM, int MAXR, typename P>
 __device__ void oi_body(int F, int k, int rounds, const double* __restrict__ R,
                         const double* __restrict__ start, P Z, P Q, double* Qo, double* H,
-                        QrShared& q, double* scr) {
+                        QrShared& q, double* scr, double* qbuf, int rank, int cs) {
   const int ld = odd_ld(F);  // Z and Q: F x k, leading dimension ld
-  for (int t = threadIdx.x; t < F * k; t += blockDim.x) Z[(t / F) * ld + t % F] = start[t];
-  __syncthreads();
-  wqr_factor<MAXR>(Z, F, ld, k, q.tau, scr, k);
-  wqr_form<MAXR>(Z, F, ld, k, 0, k, Q, ld, scr, k);
-  for (int r = 0; r < rounds; ++r) {
-    oi_apply(R, F, k, Q, ld, Z);
+  const bool lead = rank == 0;
+  if (lead) {
+    for (int t = threadIdx.x; t < F * k; t += blockDim.x) Z[(t / F) * ld + t % F] = start[t];
+    __syncthreads();
     wqr_factor<MAXR>(Z, F, ld, k, q.tau, scr, k);
     wqr_form<MAXR>(Z, F, ld, k, 0, k, Q, ld, scr, k);
   }
-  // Rayleigh-Ritz: H = Q^T (R Q), symmetrised; Q out.
-  oi_apply(R, F, k, Q, ld, Z);
-  // H(i, j) = sum_g Q(g, i) Z(g, j), then symmetrised like the oracle
+  // ranks > 0 keep their rows of R resident (their Z area is free)
+  const double* Rr = R;
+  int ldr = F;
+  if (SMEM && !lead) {
+    int mt0, mt1;
+    rq_rows(F, rank, cs, &mt0, &mt1);
+    const int r0 = 8 * mt0, nr = min(F, 8 * mt1) - r0;
+    if (nr > 0 && (size_t)nr * ld <= (size_t)ld * k) {
+      for (int t = threadIdx.x; t < nr * F; t += blockDim.x) Z[(t / F) * ld + t % F] = R[(size_t)r0 * F + t];
+      __syncthreads();
+      Rr = Z;
+      ldr = ld;
+    } else {
+      Rr = R + (size_t)r0 * F;
+    }
+  } else if (!lead) {
+    int mt0, mt1;
+    rq_rows(F, rank, cs, &mt0, &mt1);
+    Rr = R + (size_t)8 * mt0 * F;
+  }
+  long long t_rq = 0, t_f = 0, t_q = 0;
+  for (int r = 0; r <= rounds; ++r) {
+    const long long t0 = clock64();
+    oi_apply_cluster<SMEM, MAXR>(Rr, ldr, F, k, Q, ld, Z, qbuf, rank, cs);
+    const long long t1 = clock64();
+    t_rq += t1 - t0;
+    if (lead && r < rounds) {
+      wqr_factor<MAXR>(Z, F, ld, k, q.tau, scr, k);
+      const long long t2 = clock64();
+      wqr_form<MAXR>(Z, F, ld, k, 0, k, Q, ld, scr, k);
+      t_f += t2 - t1;
+      t_q += clock64() - t2;
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x < 64) {
+    g_oi_prof[blockIdx.x * 4 + 0] = t_rq;
+    g_oi_prof[blockIdx.x * 4 + 1] = t_f;
+    g_oi_prof[blockIdx.x * 4 + 2] = t_q;
+  }
+  if (!lead) return;
+  // Rayleigh-Ritz: H = Q^T (R Q), symmetrised like the oracle; Q out.
   warp_gemm_tn(k, k, F, Q, ld, Z, ld, H, k);
   __syncthreads();
   for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
@@ -726,19 +911,23 @@ template <bool SMEM, int MAXR>
 __global__ void __launch_bounds__(kOiThreads)
     k_oi_fused(int F, int k, int rounds, const double* __restrict__ Rall,
                const double* __restrict__ start, double* Qall, double* Hall, double* work,
-               double* scr_all, size_t scr_stride, int scr_smem) {
+               double* scr_all, size_t scr_stride, int scr_smem, int cs) {
   extern __shared__ double dyn[];
   __shared__ QrShared q;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x / cs, rank = blockIdx.x % cs;
   const size_t Fk = (size_t)F * k, Lk = (size_t)odd_ld(F) * k;
   const double* R = Rall + (size_t)b * F * F;
   double* scr = scr_smem ? dyn + (SMEM ? 2 * Lk : 0) : scr_all + b * scr_stride;
-  if (SMEM)
-    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Lk, Qall + b * Fk,
-                  Hall + (size_t)b * k * k, q, scr);
-  else
-    oi_body<MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Lk, work + b * 2 * Lk + Lk,
-                  Qall + b * Fk, Hall + (size_t)b * k * k, q, scr);
+  // Qo doubles as the L2 staging buffer of Q during the rounds
+  double* qbuf = Qall + b * Fk;
+  if (SMEM) {
+    oi_body<true, MAXR>(F, k, rounds, R, start + b * Fk, dyn, dyn + Lk, Qall + b * Fk,
+                        Hall + (size_t)b * k * k, q, scr, qbuf, rank, cs);
+  } else {
+    oi_body<false, MAXR>(F, k, rounds, R, start + b * Fk, work + b * 2 * Lk,
+                         work + b * 2 * Lk + Lk, Qall + b * Fk, Hall + (size_t)b * k * k, q, scr,
+                         qbuf, rank, cs);
+  }
 }
 
 // Completion: columns k..F-1 of the full Householder Q of U_k (F x k, the
@@ -845,6 +1034,57 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
   return cudaGetLastError();
 }
 
+// CTAs per axis for the distributed R Q (a portable cluster size).
+constexpr int kOiCluster = 8;
+
+template <bool SMEM, int MAXR>
+static cudaError_t oi_launch(cudaStream_t s, int nbatch, size_t smem, int F, int k, int rounds,
+                             const double* R, const double* start, double* Q, double* H,
+                             double* work, double* scr, size_t ss, int in_smem) {
+  const void* fn = (const void*)k_oi_fused<SMEM, MAXR>;
+  cudaError_t e = set_smem_attr(fn, smem);
+  if (e != cudaSuccess) return e;
+  int cs = kOiCluster;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(nbatch * cs);
+  cfg.blockDim = dim3(kOiThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k_oi_fused<SMEM, MAXR>, &cfg) != cudaSuccess ||
+      nclusters < 1) {
+    cudaGetLastError();
+    cs = 1;  // no room for a cluster of this size: one CTA per axis
+  }
+  static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "dmcg: k_oi_fused F=%d k=%d cluster %d (max active clusters %d)\n", F, k, cs, nclusters);
+  if (cs == 1) {
+    k_oi_fused<SMEM, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work,
+                                                            scr, ss, in_smem, 1);
+    return cudaGetLastError();
+  }
+  e = cudaLaunchKernelEx(&cfg, k_oi_fused<SMEM, MAXR>, F, k, rounds, R, start, Q, H, work, scr,
+                         ss, in_smem, cs);
+  if (dbg && e == cudaSuccess) {
+    long long h[256];
+    cudaStreamSynchronize(s);
+    (void)0;
+    cudaMemcpyFromSymbol(h, g_oi_prof, sizeof(h));
+    for (int c = 0; c < nbatch * cs && c < 32; c += 1)
+      fprintf(stderr, "  cta %d: rq %lld factor %lld form %lld | publish %lld sync %lld copy %lld tasks %lld\n",
+              c, h[4 * c], h[4 * c + 1], h[4 * c + 2], h[128 + 4 * c], h[129 + 4 * c], h[130 + 4 * c],
+              h[131 + 4 * c]);
+  }
+  return e;
+}
+
 template <int MAXR>
 static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                  const double* R, const double* start, double* Q, double* H,
@@ -853,23 +1093,13 @@ static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int r
   const size_t sbytes = qr_scratch(k, k) * sizeof(double);
   const size_t ss = qr_scratch_doubles(F, k);
   if (pair <= smem_room((const void*)k_oi_fused<true, MAXR>)) {
-    const void* fn = (const void*)k_oi_fused<true, MAXR>;
-    const int in_smem = pair + sbytes <= smem_room(fn);
-    const size_t smem = pair + (in_smem ? sbytes : 0);
-    cudaError_t e = set_smem_attr(fn, smem);
-    if (e != cudaSuccess) return e;
-    k_oi_fused<true, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work,
-                                                            scr, ss, in_smem);
-  } else {
-    const void* fn = (const void*)k_oi_fused<false, MAXR>;
-    const int in_smem = sbytes <= smem_room(fn);
-    const size_t smem = in_smem ? sbytes : 0;
-    cudaError_t e = set_smem_attr(fn, smem);
-    if (e != cudaSuccess) return e;
-    k_oi_fused<false, MAXR><<<nbatch, kOiThreads, smem, s>>>(F, k, rounds, R, start, Q, H, work,
-                                                             scr, ss, in_smem);
+    const int in_smem = pair + sbytes <= smem_room((const void*)k_oi_fused<true, MAXR>);
+    return oi_launch<true, MAXR>(s, nbatch, pair + (in_smem ? sbytes : 0), F, k, rounds, R, start,
+                                 Q, H, work, scr, ss, in_smem);
   }
-  return cudaGetLastError();
+  const int in_smem = sbytes <= smem_room((const void*)k_oi_fused<false, MAXR>);
+  return oi_launch<false, MAXR>(s, nbatch, in_smem ? sbytes : 0, F, k, rounds, R, start, Q, H,
+                                work, scr, ss, in_smem);
 }
 
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,

@@ -14,6 +14,10 @@
 #include <cfloat>
 
 #include "chol_dev.h"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include "gemm.cuh"
 
 namespace dmcg {
@@ -477,6 +481,38 @@ __global__ void k_residual(int n, int W, const uint32_t* __restrict__ rp,
 
 }  // namespace
 
+// DMCG_LEVEL_TIMING=1: CUDA events around the phases of every level, printed
+// after a stream sync (debugging aid; off by default).
+struct LevelTimer {
+  cudaStream_t s;
+  const char* what;
+  bool on;
+  std::vector<cudaEvent_t> ev;
+  LevelTimer(cudaStream_t st, const char* w, uint32_t nlev) : s(st), what(w) {
+    static const bool env = std::getenv("DMCG_LEVEL_TIMING") != nullptr;
+    on = env;
+    if (on) {
+      ev.resize((size_t)nlev * 5);
+      for (auto& e : ev) cudaEventCreate(&e);
+    }
+  }
+  void mark(uint32_t l, int k) {
+    if (on) cudaEventRecord(ev[(size_t)l * 5 + k], s);
+  }
+  void report(const CholLevels& lv, const char* a, const char* b, const char* c, bool split = false) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    for (uint32_t l = 0; l < lv.nlevels; ++l) {
+      float t[3];
+      const int a0[3] = {0, 1, split ? 3 : 2}, a1[3] = {1, 2, split ? 4 : 3};
+      for (int k = 0; k < 3; ++k) cudaEventElapsedTime(&t[k], ev[l * 5 + a0[k]], ev[l * 5 + a1[k]]);
+      std::fprintf(stderr, "  %s level %u: %u fronts, maxw %u maxm %u | %s %.3f %s %.3f %s %.3f ms\n", what,
+                   l, lv.count[l], lv.maxw[l], lv.maxm[l], a, t[0], b, t[1], c, t[2]);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+};
+
 cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevels& lv) {
   const int nb = 32;
   {
@@ -492,10 +528,13 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
   }
   cudaError_t e = cudaMemsetAsync(d.Linv, 0, d.linv_doubles * sizeof(double), s);
   if (e != cudaSuccess) return e;
+  LevelTimer lt(s, "factor", lv.nlevels);
   for (uint32_t l = 0; l < lv.nlevels; ++l) {
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
+    lt.mark(l, 0);
     k_assemble<<<dim3((lv.maxm[l] + kAsmCols - 1) / kAsmCols, cnt), 256, 0, s>>>(d, ls);
+    lt.mark(l, 1);
     for (uint32_t k0 = 0; k0 < lv.maxw[l]; k0 += nb) {
       k_panel<<<cnt, kPanelThreads, 0, s>>>(d, ls, (int)k0, nb);
       // bound over the level: a front whose last panel is partial (pw < nb)
@@ -506,10 +545,13 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
         k_trailing<<<dim3(nt * (nt + 1) / 2, cnt), kGemmThreads, 0, s>>>(d, ls, (int)k0, nb);
       }
     }
+    lt.mark(l, 2);
     const uint32_t nbk = (lv.maxw[l] + kIB - 1) / kIB;
     k_inv_diag<<<dim3(nbk, cnt), kIB, kInvDiagSmem, s>>>(d, ls);
     if (nbk > 1) k_inv_offdiag<<<dim3(nbk, cnt), kGemmThreads, 0, s>>>(d, ls, d.scratch);
+    lt.mark(l, 3);
   }
+  lt.report(lv, "assemble", "panels", "inverse");
   return cudaGetLastError();
 }
 
@@ -526,20 +568,27 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
                               const double* b, double* y, double* x) {
   const int W = (int)d.W;
   const unsigned tn = (unsigned)((W + kBN - 1) / kBN);
+  LevelTimer lt(s, "solve", lv.nlevels);
   for (uint32_t l = 0; l < lv.nlevels; ++l) {
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
+    lt.mark(l, 0);
     k_solve_gather<<<dim3((lv.maxm[l] + 31) / 32, (W + 63) / 64, cnt), 256, 0, s>>>(d, ls, b);
     k_fwd1<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y);
+    lt.mark(l, 1);
     if (lv.maxu[l] > 0)
       k_fwd2<<<dim3((lv.maxu[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y);
+    lt.mark(l, 2);
   }
   for (int l = (int)lv.nlevels - 1; l >= 0; --l) {
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
+    lt.mark(l, 3);
     k_bwd1<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x);
     k_bwd2<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x);
+    lt.mark(l, 4);
   }
+  lt.report(lv, "gather+fwd1", "fwd2", "bwd", true);
   return cudaGetLastError();
 }
 

@@ -454,6 +454,8 @@ void dmcg_plan_destroy(dmcg_plan* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
   cudaStreamSynchronize(p->ctx->stream);
+  for (auto* g : {&p->g_encode, &p->g_decode})
+    if (g->exec) cudaGraphExecDestroy(g->exec);
   for (auto& kv : p->owned) p->ctx->pool.put(kv.first, kv.second);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
@@ -736,6 +738,7 @@ int dmcg_plan_create(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uin
   if (!ctx || !plan || !cfg) return DMCG_E_CONFIG;
   cudaSetDevice(ctx->device);
   Status st = plan_create_impl(ctx, n, F, dtype, faces, n_faces, cfg, nullptr, 0, plan);
+  if (st.good()) (*plan)->use_graphs = true;  // reused across calls: replay CUDA graphs
   return ctx->set_error(st);
 }
 

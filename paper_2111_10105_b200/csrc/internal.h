@@ -82,6 +82,16 @@ struct dmcg_ctx {
   }
 };
 
+namespace dmcg {
+// An instantiated CUDA graph of one plan call, keyed by the caller's
+// pointers / options (pipeline.cu run_graph).
+struct PlanGraph {
+  cudaGraphExec_t exec = nullptr;
+  const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
+  int opt_key = 0;
+};
+}  // namespace dmcg
+
 struct dmcg_plan {
   dmcg_ctx* ctx = nullptr;
   // geometry / config
@@ -138,6 +148,8 @@ struct dmcg_plan {
   double analyze_seconds = 0.0;
   bool decode_ready = false;
   bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
+  bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
+  dmcg::PlanGraph g_encode, g_decode;
 
   cudaEvent_t ev[8] = {};
   dmcg_stats stats = {};

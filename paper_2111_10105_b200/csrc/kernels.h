@@ -44,8 +44,9 @@ cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int nc
                                long bs);
 cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H);
 // Fused orthogonal iterations (one CTA per axis): Q0 = qr(start), `rounds`
-// x {Z = R Q; Q = qr(Z)}, then H = Q^T R Q (symmetrised).  work: nbatch *
-// 2 F k doubles (used when the pair does not fit in shared memory).
+// x {Z = R Q; Q = qr(Z)}, then H = Q^T R Q (symmetrised); R Q is spread over a
+// cluster of CTAs per axis (Q doubles as its L2 staging buffer).  work:
+// nbatch * 2 (F|1) k doubles (used when the pair does not fit in shared memory).
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
                             const double* start, double* Q, double* H, double* work, double* scr);
 // U[:, k:F] = columns k..F-1 of the full Householder Q of U[:, :k].

@@ -28,6 +28,15 @@ static bool debug_sync() {
 
 namespace {
 
+// Event record that stays a timing point inside a CUDA graph capture.
+cudaError_t record_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(s, &cs);
+  if (err != cudaSuccess) return err;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, s);
+}
+
 // ---- GEMM operand loaders / epilogues specific to the codec --------------
 
 // Projection epilogue (codec.cpp:420 + the row min/max of codec.cpp:253):
@@ -163,11 +172,10 @@ Status basis(dmcg_plan* p) {
   // Q0 = qr(start); rounds x {Z = R Q; Q = qr(Z)}; H = Q^T R Q — one fused
   // kernel, one CTA per axis (basis.cu k_oi_fused).
   double* H = p->d_C;  // k x k scratch (coefficient buffer is free here)
-  DMCG_TRY(cudaEventRecord(p->ev[6], s));
+  DMCG_TRY(record_event(p->ev[6], s));
   DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H,
                                   p->d_qr_scr));
-  DMCG_TRY(cudaEventRecord(p->ev[7], s));
-  p->oi_timed = true;
+  DMCG_TRY(record_event(p->ev[7], s));
   DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
   double* Ws = p->d_Z;  // k x k sorted Ritz vectors (Z is free)
   DMCG_TRY(launch_sort_basis(s, 3, k, k, p->d_V, p->d_w, Ws, (long)k * k, p->d_evals, F));
@@ -186,25 +194,26 @@ Status basis(dmcg_plan* p) {
 
 }  // namespace
 
-// Host-side wrapper used by host.cpp.
-Status plan_encode(dmcg_plan* p, const void* const x[3]) {
+// Every kernel of one encode on the plan stream (no host synchronisation:
+// capturable into a CUDA graph).
+static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
   const bool f32 = p->dtype == DMCG_F32;
   const long FF = (long)F * F;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
-  DMCG_TRY(cudaEventRecord(p->ev[0], s));
+  DMCG_TRY(record_event(p->ev[0], s));
   // K1 delta coordinates (codec.cpp:419).
   DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
-  DMCG_TRY(cudaEventRecord(p->ev[1], s));
+  DMCG_TRY(record_event(p->ev[1], s));
   // K2 autocorrelation (spectral.cpp:35-39).
   Status st = f32 ? gram<float>(p, x) : gram<double>(p, x);
   if (!st.good()) return st;
-  DMCG_TRY(cudaEventRecord(p->ev[2], s));
+  DMCG_TRY(record_event(p->ev[2], s));
   // K3 basis.
   st = basis(p);
   if (!st.good()) return st;
-  DMCG_TRY(cudaEventRecord(p->ev[3], s));
+  DMCG_TRY(record_event(p->ev[3], s));
   // K5a dictionary levels (encode_dictionaries first block).
   DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
   // K4 projection coeffs = U_k^T delta^T (codec.cpp:420) + row min/max, then
@@ -217,11 +226,68 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
     DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
                                p->d_row_max, p->d_row_bits, p->d_coeff_q));
   }
-  DMCG_TRY(cudaEventRecord(p->ev[4], s));
+  DMCG_TRY(record_event(p->ev[4], s));
   // K5b anchors (codec.cpp:444-471).
   DMCG_TRY(launch_anchors(s, (int)p->n_c, F, p->d_anchor_idx, x, f32, p->anchor_bits,
                           p->d_anchor_rng, p->d_anchor_q));
-  DMCG_TRY(cudaEventRecord(p->ev[5], s));
+  DMCG_TRY(record_event(p->ev[5], s));
+  return Status::ok();
+}
+
+// CUDA graphs for plans that are reused (dmcg_plan_*): the ~50 encode and
+// ~300 decode launches are replayed from one instantiated graph instead of
+// being re-issued one by one (the stream launch rate, ~3.5 us per kernel on
+// this host, would otherwise bound the small-kernel phases).  A graph is
+// keyed by the caller's device pointers and options and re-captured when
+// they change.  Off for the one-shot drop-in plans and under the debugging
+// switches (DMCG_SYNC, DMCG_LEVEL_TIMING, DMCG_NO_GRAPH).
+static bool graphs_allowed(const dmcg_plan* p) {
+  static const bool env_off = getenv("DMCG_NO_GRAPH") || getenv("DMCG_SYNC") ||
+                              getenv("DMCG_LEVEL_TIMING") || getenv("DMCG_DEBUG");
+  return p->use_graphs && !env_off;
+}
+
+template <class Fn>
+static Status run_graph(dmcg_plan* p, PlanGraph& g, const void* const key[4], int opt_key,
+                        const Fn& enqueue) {
+  cudaStream_t s = p->ctx->stream;
+  if (!graphs_allowed(p)) return enqueue();
+  bool hit = g.exec != nullptr && g.opt_key == opt_key;
+  for (int i = 0; i < 4 && hit; ++i) hit = g.key[i] == key[i];
+  if (!hit) {
+    if (g.exec) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    DMCG_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    Status st = enqueue();
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (!st.good()) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    DMCG_TRY(e);
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    DMCG_TRY(e);
+    for (int i = 0; i < 4; ++i) g.key[i] = key[i];
+    g.opt_key = opt_key;
+  }
+  DMCG_TRY(cudaGraphLaunch(g.exec, s));
+  return Status::ok();
+}
+
+// Host-side wrapper used by host.cpp.
+Status plan_encode(dmcg_plan* p, const void* const x[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int k = (int)p->k, F = (int)p->F;
+  const void* key[4] = {x[0], x[1], x[2], nullptr};
+  {
+    Status st = run_graph(p, p->g_encode, key, 0, [&] { return enqueue_encode(p, x); });
+    if (!st.good()) return st;
+  }
+  p->oi_timed = p->rounds > 0 && k < F && k > 0;
   int flags[8];
   DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
   DMCG_TRY(cudaStreamSynchronize(s));
@@ -259,13 +325,12 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
 
 // Direct decode: K6 into the row-major n x 3F layout, rhs, supernodal
 // Cholesky factor + solve + refinement (solver.cpp:43-58, 82-90).
-static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
-                                 void* const out[3]) {
+static Status enqueue_decode_direct(dmcg_plan* p, int refine, void* const out[3]) {
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k, W = (int)p->W;
   const bool f32 = p->dtype == DMCG_F32;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
-  DMCG_TRY(cudaEventRecord(p->ev[0], s));
+  DMCG_TRY(record_event(p->ev[0], s));
   const size_t nW = (size_t)n * W;
   if (k > 0) {
     DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
@@ -281,21 +346,34 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   DMCG_TRY(launch_rhs_rm(s, n, F, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos, (int)p->n_c,
                          p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_rm_delta, p->d_rm_b,
                          p->d_flags + 1));
-  DMCG_TRY(cudaEventRecord(p->ev[1], s));
+  DMCG_TRY(record_event(p->ev[1], s));
   DMCG_TRY(chol_factor_device(s, p->cdev, p->levels));
-  DMCG_TRY(cudaEventRecord(p->ev[2], s));
+  DMCG_TRY(record_event(p->ev[2], s));
   DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
   DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, false));
-  const int refine = opt ? opt->refine : 1;
   for (int r = 0; r < refine; ++r) {
     DMCG_TRY(normal_residual(s, n, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b, p->d_rm_x,
                              p->d_rm_r));
     DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp));
     DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, true));
   }
-  DMCG_TRY(cudaEventRecord(p->ev[3], s));
+  DMCG_TRY(record_event(p->ev[3], s));
   DMCG_TRY(launch_output_rm(s, n, F, p->d_rm_x, out, f32));
-  DMCG_TRY(cudaEventRecord(p->ev[4], s));
+  DMCG_TRY(record_event(p->ev[4], s));
+  return Status::ok();
+}
+
+static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
+                                 void* const out[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int k = (int)p->k, W = (int)p->W;
+  const int refine = opt ? opt->refine : 1;
+  const void* key[4] = {out[0], out[1], out[2], nullptr};
+  {
+    Status st = run_graph(p, p->g_decode, key, refine,
+                          [&] { return enqueue_decode_direct(p, refine, out); });
+    if (!st.good()) return st;
+  }
   int flags[8];
   DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
   DMCG_TRY(cudaStreamSynchronize(s));
@@ -345,7 +423,7 @@ Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out
     if (!sn.good()) return sn;
   }
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
-  DMCG_TRY(cudaEventRecord(p->ev[0], s));
+  DMCG_TRY(record_event(p->ev[0], s));
   // K6: dequantise + reconstruct delta~ = (U~ c~)^T (codec.cpp:528-533)
   // straight into the CG layout; rows >= k_l are exactly zero in the
   // reference, so the contraction runs over r < k_l only.
@@ -362,15 +440,15 @@ Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out
   DMCG_TRY(launch_rhs(s, n, F, (int)p->W, (int)p->nblk, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos,
                       (int)p->n_c, p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_cg_q,
                       p->d_cg_r, p->d_flags + 1));
-  DMCG_TRY(cudaEventRecord(p->ev[1], s));
+  DMCG_TRY(record_event(p->ev[1], s));
   // K7 CG.
   const double rtol = opt ? opt->cg_rtol : 1e-10;
   const int maxit = opt ? opt->cg_max_iter : 20000;
   DMCG_TRY(launch_cg(s, n, (int)p->W, (int)p->nblk, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_cg_x,
                      p->d_cg_r, p->d_cg_p, p->d_cg_q, rtol, maxit, p->d_cg_iters, p->d_cg_res));
-  DMCG_TRY(cudaEventRecord(p->ev[2], s));
+  DMCG_TRY(record_event(p->ev[2], s));
   DMCG_TRY(launch_output(s, n, F, p->d_cg_x, out, f32));
-  DMCG_TRY(cudaEventRecord(p->ev[3], s));
+  DMCG_TRY(record_event(p->ev[3], s));
   int flags[8];
   DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
   std::vector<int> iters(p->W);

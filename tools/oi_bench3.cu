@@ -5,14 +5,14 @@
 #include <vector>
 
 __device__ long long g_stamp[8];
-#define PANEL_STAMP(i)                                            \
+#define PANEL_STAMP_X(i)                                            \
   do {                                                           \
     __syncwarp();                                                \
     if (lane == 0) g_stamp[i] += clock64();                      \
   } while (0)
 __device__ long long g_fs[8];
 __device__ long long* g_acc;  // generic pointer to the probe kernel's shared accumulators
-#define FACT_STAMP(i)                                            \
+#define FACT_STAMP_X(i)                                            \
   do {                                                           \
     if (threadIdx.x == 0) {                                      \
       long long* acc_ = g_acc;                                   \
@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(256) k_probe(int F, int k, const double* R, co
   long long c1 = clock64();
   wqr_form<8>(Z, F, L, k, 0, k, Q, L, scr, k);
   long long c2 = clock64();
-  oi_apply(R, F, k, Q, L, Z);
+  oi_apply_cluster<true, 8>(R, F, F, k, Q, L, Z, (double*)nullptr, 0, 1);
   long long c3 = clock64();
   // the register panels alone (warp 0)
   if (threadIdx.x < 32)
