@@ -74,10 +74,25 @@ __global__ void __launch_bounds__(256) k_assemble(CholDev d, const uint32_t* lsu
     const uint32_t* rel = d.rel_idx + d.rel_ptr[c];
     const uint32_t b0 = lower_bound_u32(rel, uc, cc0);
     const uint32_t b1 = lower_bound_u32(rel, uc, cc1);
-    for (uint32_t b = b0; b < b1; ++b) {
-      const double* src = C + (size_t)(wc + b) * mc + wc;
-      double* dst = A + (size_t)rel[b] * m;
-      for (uint32_t a = b + threadIdx.x; a < uc; a += blockDim.x) dst[rel[a]] += src[a];
+    // (b, a) over columns b in [b0, b1) x rows a in [b, uc): eight updates
+    // per thread are loaded before any is stored (distinct targets)
+    const uint32_t nb = b1 - b0;
+    const long tot = (long)nb * uc;
+    for (long t0 = threadIdx.x; t0 < tot; t0 += 8L * blockDim.x) {
+      double sv[8], dv[8];
+      double* dp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long t = t0 + (long)u * blockDim.x;
+        const uint32_t b = b0 + (uint32_t)(t / uc), a = (uint32_t)(t % uc);
+        const bool ok = t < tot && a >= b;
+        dp[u] = ok ? A + (size_t)rel[b] * m + rel[a] : nullptr;
+        sv[u] = ok ? C[(size_t)(wc + b) * mc + wc + a] : 0.0;
+        dv[u] = ok ? *dp[u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (dp[u]) *dp[u] = dv[u] + sv[u];
     }
     __syncthreads();
   }
@@ -161,11 +176,27 @@ struct LoadPanel {
     return A[(size_t)(k0 + k) * m + off + i];
   }
 };
+// Epilogues that read the destination load every target first and store
+// afterwards: a load -> subtract -> store loop on one pointer issues in
+// order and would wait one L2 round trip per element (the compiler cannot
+// hoist the next load above a possibly aliasing store).
 struct SubLower {
   double* A;
   int m, off;
   __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
                                              const WarpTile& wt) const {
+    double v[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int mi = mb + r, ni = nb + c;
+          v[i][j][e] = (mi < M && ni < N && mi >= ni) ? A[(size_t)(off + ni) * m + off + mi] : 0.0;
+        }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -176,7 +207,7 @@ struct SubLower {
           frag_rc(i, j, e, lane, &r, &c);
           const int mi = mb + r, ni = nb + c;
           if (mi < M && ni < N && mi >= ni)
-            A[(size_t)(off + ni) * m + off + mi] -= wt.acc[i][j][e];
+            A[(size_t)(off + ni) * m + off + mi] = v[i][j][e] - wt.acc[i][j][e];
         }
   }
 };
@@ -343,10 +374,23 @@ __global__ void __launch_bounds__(256) k_solve_gather(CholDev d, const uint32_t*
     const double* Rc = d.R + (d.rhs_off[ch] + wc) * W;
     const uint32_t* rel = d.rel_idx + d.rel_ptr[ch];
     const uint32_t a0 = lower_bound_u32(rel, uc, r0), a1 = lower_bound_u32(rel, uc, r1);
-    for (long t = threadIdx.x; t < (long)(a1 - a0) * cw; t += blockDim.x) {
-      const uint32_t a = a0 + (uint32_t)(t / cw);
-      const int c = c0 + (int)(t % cw);
-      R[(size_t)rel[a] * W + c] += Rc[(size_t)a * W + c];
+    const long tot = (long)(a1 - a0) * cw;
+    for (long t0 = threadIdx.x; t0 < tot; t0 += 8L * blockDim.x) {
+      double sv[8], dv[8];
+      double* dp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const long t = t0 + (long)u * blockDim.x;
+        const bool ok = t < tot;
+        const uint32_t a = a0 + (uint32_t)(ok ? t / cw : 0);
+        const int c = c0 + (int)(ok ? t % cw : 0);
+        dp[u] = ok ? R + (size_t)rel[a] * W + c : nullptr;
+        sv[u] = ok ? Rc[(size_t)a * W + c] : 0.0;
+        dv[u] = ok ? *dp[u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (dp[u]) *dp[u] = dv[u] + sv[u];
     }
     __syncthreads();
   }
@@ -385,6 +429,21 @@ struct StoreRows {
   int W;
   __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
                                              const WarpTile& wt) const {
+    double v[4][4][2];
+    if (MODE != 0) {  // all reads before the first store (see SubLower)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            int r, c;
+            frag_rc(i, j, e, lane, &r, &c);
+            const int mi = mb + r, ni = nb + c;
+            const size_t o = (size_t)mi * W + ni;
+            v[i][j][e] = (mi < M && ni < N) ? (MODE == 1 ? out[o] : base[o]) : 0.0;
+          }
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -396,9 +455,7 @@ struct StoreRows {
           const int mi = mb + r, ni = nb + c;
           if (mi < M && ni < N) {
             const size_t o = (size_t)mi * W + ni;
-            if (MODE == 0) out[o] = wt.acc[i][j][e];
-            if (MODE == 1) out[o] -= wt.acc[i][j][e];
-            if (MODE == 2) out[o] = base[o] - wt.acc[i][j][e];
+            out[o] = MODE == 0 ? wt.acc[i][j][e] : v[i][j][e] - wt.acc[i][j][e];
           }
         }
   }
@@ -535,8 +592,22 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
     lt.mark(l, 0);
     k_assemble<<<dim3((lv.maxm[l] + kAsmCols - 1) / kAsmCols, cnt), 256, 0, s>>>(d, ls);
     lt.mark(l, 1);
+    static const bool per_launch = std::getenv("DMCG_LEVEL_TIMING") &&
+                                   std::getenv("DMCG_LEVEL_TIMING")[0] == '2';
+    std::vector<cudaEvent_t> pe;
+    const bool pl = per_launch && l + 1 == lv.nlevels;
     for (uint32_t k0 = 0; k0 < lv.maxw[l]; k0 += nb) {
+      if (pl) {
+        pe.emplace_back();
+        cudaEventCreate(&pe.back());
+        cudaEventRecord(pe.back(), s);
+      }
       k_panel<<<cnt, kPanelThreads, 0, s>>>(d, ls, (int)k0, nb);
+      if (pl) {
+        pe.emplace_back();
+        cudaEventCreate(&pe.back());
+        cudaEventRecord(pe.back(), s);
+      }
       // bound over the level: a front whose last panel is partial (pw < nb)
       // has a trailing block of m - k0 - pw rows
       const uint32_t T = lv.maxm[l] > k0 + 1 ? lv.maxm[l] - k0 - 1 : 0;
@@ -544,6 +615,19 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
         const uint32_t nt = (T + kBM - 1) / kBM;
         k_trailing<<<dim3(nt * (nt + 1) / 2, cnt), kGemmThreads, 0, s>>>(d, ls, (int)k0, nb);
       }
+    }
+    if (pl) {
+      pe.emplace_back();
+      cudaEventCreate(&pe.back());
+      cudaEventRecord(pe.back(), s);
+      cudaStreamSynchronize(s);
+      for (size_t i = 0; i + 2 < pe.size(); i += 2) {
+        float a, b;
+        cudaEventElapsedTime(&a, pe[i], pe[i + 1]);
+        cudaEventElapsedTime(&b, pe[i + 1], pe[i + 2]);
+        std::fprintf(stderr, "    root panel %zu: k_panel %.1f us, k_trailing %.1f us\n", i / 2, a * 1e3, b * 1e3);
+      }
+      for (auto e : pe) cudaEventDestroy(e);
     }
     lt.mark(l, 2);
     const uint32_t nbk = (lv.maxw[l] + kIB - 1) / kIB;
