@@ -175,6 +175,9 @@ struct LoadPanel {
   __device__ __forceinline__ double operator()(int, int k, int i) const {
     return A[(size_t)(k0 + k) * m + off + i];
   }
+  __device__ __forceinline__ const double* addr(int, int k, int i) const {
+    return A + (size_t)(k0 + k) * m + off + i;
+  }
 };
 // Epilogues that read the destination load every target first and store
 // afterwards: a load -> subtract -> store loop on one pointer issues in
@@ -278,6 +281,9 @@ struct LoadLinvRM {  // X(k, c) = V[(r0 + k) * w + c0 + c]
   __device__ __forceinline__ double operator()(int, int k, int c) const {
     return V[(size_t)(r0 + k) * w + c0 + c];
   }
+  __device__ __forceinline__ const double* addr(int, int k, int c) const {
+    return V + (size_t)(r0 + k) * w + c0 + c;
+  }
 };
 struct LoadLinvRowsK {  // X(k, r) = V[(r0 + r) * w + c0 + k]   (k contiguous)
   static constexpr bool kKContig = true;
@@ -285,6 +291,9 @@ struct LoadLinvRowsK {  // X(k, r) = V[(r0 + r) * w + c0 + k]   (k contiguous)
   int w, r0, c0;
   __device__ __forceinline__ double operator()(int, int k, int r) const {
     return V[(size_t)(r0 + r) * w + c0 + k];
+  }
+  __device__ __forceinline__ const double* addr(int, int k, int r) const {
+    return V + (size_t)(r0 + r) * w + c0 + k;
   }
 };
 struct LoadFrontCM {  // X(k, r) = A[(c0 + k) * m + r0 + r]
@@ -294,6 +303,9 @@ struct LoadFrontCM {  // X(k, r) = A[(c0 + k) * m + r0 + r]
   __device__ __forceinline__ double operator()(int, int k, int r) const {
     return A[(size_t)(c0 + k) * m + r0 + r];
   }
+  __device__ __forceinline__ const double* addr(int, int k, int r) const {
+    return A + (size_t)(c0 + k) * m + r0 + r;
+  }
 };
 struct LoadColMajorT {  // X(k, i) = p[k * ld + i]
   static constexpr bool kKContig = false;
@@ -301,6 +313,9 @@ struct LoadColMajorT {  // X(k, i) = p[k * ld + i]
   int ld;
   __device__ __forceinline__ double operator()(int, int k, int i) const {
     return p[(size_t)k * ld + i];
+  }
+  __device__ __forceinline__ const double* addr(int, int k, int i) const {
+    return p + (size_t)k * ld + i;
   }
 };
 struct StoreTile {  // out[r * ld + c] = sign * v
@@ -353,6 +368,9 @@ __global__ void __launch_bounds__(kGemmThreads) k_inv_offdiag(CholDev d, const u
 // rows landing in the chunk form a contiguous range (rel is increasing).
 __global__ void __launch_bounds__(256) k_solve_gather(CholDev d, const uint32_t* lsup,
                                                       const double* __restrict__ b) {
+  // R_s = [P b rows of s; 0] + sum of the children's update rows, in the
+  // pull form of the extend-add (CholPlan::pull_*): every element is formed
+  // independently, children in a fixed order (deterministic), no barriers.
   const uint32_t s = lsup[blockIdx.z];
   const int W = (int)d.W;
   const int c0 = blockIdx.y * 64;
@@ -361,38 +379,15 @@ __global__ void __launch_bounds__(256) k_solve_gather(CholDev d, const uint32_t*
   const uint32_t r0 = blockIdx.x * 32;
   if (r0 >= m) return;
   const uint32_t r1 = min(m, r0 + 32);
-  double* R = d.R + d.rhs_off[s] * W;
+  const unsigned long long g0 = d.rhs_off[s];
   for (long t = threadIdx.x; t < (long)(r1 - r0) * cw; t += blockDim.x) {
     const uint32_t r = r0 + (uint32_t)(t / cw);
     const int c = c0 + (int)(t % cw);
-    R[(size_t)r * W + c] = r < w ? b[(size_t)d.perm[f0 + r] * W + c] : 0.0;
-  }
-  __syncthreads();
-  for (uint32_t q = d.child_ptr[s]; q < d.child_ptr[s + 1]; ++q) {
-    const uint32_t ch = d.child_idx[q];
-    const uint32_t wc = front_w(d, ch), uc = front_m(d, ch) - wc;
-    const double* Rc = d.R + (d.rhs_off[ch] + wc) * W;
-    const uint32_t* rel = d.rel_idx + d.rel_ptr[ch];
-    const uint32_t a0 = lower_bound_u32(rel, uc, r0), a1 = lower_bound_u32(rel, uc, r1);
-    const long tot = (long)(a1 - a0) * cw;
-    for (long t0 = threadIdx.x; t0 < tot; t0 += 8L * blockDim.x) {
-      double sv[8], dv[8];
-      double* dp[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const long t = t0 + (long)u * blockDim.x;
-        const bool ok = t < tot;
-        const uint32_t a = a0 + (uint32_t)(ok ? t / cw : 0);
-        const int c = c0 + (int)(ok ? t % cw : 0);
-        dp[u] = ok ? R + (size_t)rel[a] * W + c : nullptr;
-        sv[u] = ok ? Rc[(size_t)a * W + c] : 0.0;
-        dv[u] = ok ? *dp[u] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (dp[u]) *dp[u] = dv[u] + sv[u];
-    }
-    __syncthreads();
+    const size_t g = g0 + r;
+    double v = r < w ? b[(size_t)d.perm[f0 + r] * W + c] : 0.0;
+    const uint32_t e0 = d.pull_ptr[g], e1 = d.pull_ptr[g + 1];
+    for (uint32_t e = e0; e < e1; ++e) v += d.R[(size_t)d.pull_src[e] * W + c];
+    d.R[g * W + c] = v;
   }
 }
 
@@ -403,6 +398,9 @@ struct LoadRowMajor {  // X(k, i) = p[i * ld + k]   (k contiguous)
   __device__ __forceinline__ double operator()(int, int k, int i) const {
     return p[(size_t)i * ld + k];
   }
+  __device__ __forceinline__ const double* addr(int, int k, int i) const {
+    return p + (size_t)i * ld + k;
+  }
 };
 struct LoadColMajor {  // X(k, i) = p[k * ld + i]   (i contiguous)
   static constexpr bool kKContig = false;
@@ -410,6 +408,9 @@ struct LoadColMajor {  // X(k, i) = p[k * ld + i]   (i contiguous)
   int ld;
   __device__ __forceinline__ double operator()(int, int k, int i) const {
     return p[(size_t)k * ld + i];
+  }
+  __device__ __forceinline__ const double* addr(int, int k, int i) const {
+    return p + (size_t)k * ld + i;
   }
 };
 struct LoadGatherRows {  // X(k, c) = x[rows[k] * W + c]
@@ -419,6 +420,9 @@ struct LoadGatherRows {  // X(k, c) = x[rows[k] * W + c]
   int W;
   __device__ __forceinline__ double operator()(int, int k, int c) const {
     return x[(size_t)rows[k] * W + c];
+  }
+  __device__ __forceinline__ const double* addr(int, int k, int c) const {
+    return x + (size_t)rows[k] * W + c;
   }
 };
 // out[(row0 + i) * W + c] (=, -=, or = base - v)
@@ -509,6 +513,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_bwd2(CholDev d, const uint32_t
   gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadColMajor{V, w},
             LoadColMajor{T, W}, StoreRows<0>{x + (size_t)d.first[s] * W, nullptr, W});
 }
+
 
 // out[perm[j]] (+)= x[j]
 __global__ void k_unpermute(int n, int W, const uint32_t* perm, const double* __restrict__ xp,

@@ -29,6 +29,11 @@ struct CholPlan {
   std::vector<uint64_t> rhs_off;          // nsup + 1, m_s rows each (times W columns)
   std::vector<uint64_t> rel_ptr;          // nsup + 1 (indexed by child)
   std::vector<uint32_t> rel_idx;          // child update row -> local row in the parent
+  // "pull" form of the extend-add for the solves: front row g (global
+  // numbering rhs_off[s] + r) sums the child update rows pull_src[pull_ptr[g]
+  // .. pull_ptr[g+1]) (global rows), children in order: every row can be
+  // formed independently and deterministically.
+  std::vector<uint32_t> pull_ptr, pull_src;
   std::vector<uint64_t> a_ptr;            // nsup + 1
   std::vector<uint32_t> a_pos;            // local index (col * m + row) in the front
   std::vector<float> a_val;               // value of M

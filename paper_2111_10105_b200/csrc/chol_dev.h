@@ -24,6 +24,10 @@ struct CholDev {
   const unsigned long long* rhs_off = nullptr;
   const uint32_t* perm = nullptr;
   const uint32_t* level_sup = nullptr;
+  const uint32_t* level_ptr = nullptr;  // nlevels + 1 offsets into level_sup
+  const uint32_t* pull_ptr = nullptr;   // extend-add pull lists (chol.h)
+  const uint32_t* pull_src = nullptr;
+  uint32_t nlevels = 0;
   double* F = nullptr;     // fronts (factor in place)
   double* Linv = nullptr;  // L11^{-1}, row-major per front
   double* R = nullptr;     // per-front right-hand-side buffers (m_s x W)

@@ -564,6 +564,29 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       }
     }
   });
+  // pull lists (see chol.h): count per parent row, then fill child by child
+  {
+    const uint64_t R = p.rhs_off[NS];
+    p.pull_ptr.assign(R + 1, 0);
+    for (uint32_t c = 0; c < NS; ++c) {
+      const int32_t ps = p.parent[c];
+      if (ps < 0) continue;
+      for (uint64_t q = p.rel_ptr[c]; q < p.rel_ptr[c + 1]; ++q)
+        p.pull_ptr[p.rhs_off[ps] + p.rel_idx[q] + 1]++;
+    }
+    for (uint64_t g = 0; g < R; ++g) p.pull_ptr[g + 1] += p.pull_ptr[g];
+    p.pull_src.resize(p.pull_ptr[R]);
+    std::vector<uint32_t> fill(p.pull_ptr.begin(), p.pull_ptr.end() - 1);
+    for (uint32_t s = 0; s < NS; ++s)
+      for (uint32_t q = p.child_ptr[s]; q < p.child_ptr[s + 1]; ++q) {
+        const uint32_t c = p.child_idx[q];
+        const uint32_t wc = p.w(c);
+        for (uint64_t e = p.rel_ptr[c]; e < p.rel_ptr[c + 1]; ++e) {
+          const uint64_t g = p.rhs_off[s] + p.rel_idx[e];
+          p.pull_src[fill[g]++] = (uint32_t)(p.rhs_off[c] + wc + (e - p.rel_ptr[c]));
+        }
+      }
+  }
   lap("rel maps");
   // (9) scatter list of M into the fronts (lower part, column-major local)
   p.a_ptr.assign(NS + 1, 0);

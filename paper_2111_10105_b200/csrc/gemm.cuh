@@ -12,6 +12,8 @@
 // and written through epilogue functors (strided store, split-K partial,
 // row min/max, CG column-block layout).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace dmcg {
@@ -45,9 +47,117 @@ __device__ __forceinline__ GemmSmem& gemm_smem() {
   return sm;
 }
 
+// Loaders that are plain address maps (`addr(b, k, m)`, no transform) take
+// the cp.async path below: a 4-stage shared-memory ring filled straight
+// from global memory (no register staging), so three k-slices of loads are
+// in flight while one is multiplied.
+template <class T, class = void>
+struct RawLoader : std::false_type {};
+template <class T>
+struct RawLoader<T, std::void_t<decltype(&T::addr)>> : std::true_type {};
+
+constexpr int kAStages = 4, kABK = 8;
+struct GemmSmemAsync {
+  double As[kAStages][kABK][kBM + 4];
+  double Bs[kAStages][kABK][kBN + 4];
+};
+__device__ __forceinline__ GemmSmemAsync& gemm_smem_async() {
+  __shared__ GemmSmemAsync sm;
+  return sm;
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <class LA, class LB, class EP>
+__device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int n0, int kbeg,
+                                                int kend, int split, const LA& la, const LB& lb,
+                                                const EP& ep) {
+  GemmSmemAsync& sm = gemm_smem_async();
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wm = w >> 1, wn = w & 1;
+  WarpTile wt;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) wt.acc[i][j][0] = wt.acc[i][j][1] = 0.0;
+  const int nk = kend > kbeg ? (kend - kbeg + kABK - 1) / kABK : 0;
+  if (nk > 0) {
+    const double* adummy = la.addr(b, kbeg, m0);
+    const double* bdummy = lb.addr(b, kbeg, n0);
+    auto issue = [&](int it) {
+      const int buf = it % kAStages, kt = kbeg + it * kABK;
+#pragma unroll
+      for (int q = 0; q < (kABK * kBM) / kGemmThreads; ++q) {
+        const int e = t + q * kGemmThreads;
+        int k, m;
+        if (LA::kKContig) {
+          k = e % kABK;
+          m = e / kABK;
+        } else {
+          m = e % kBM;
+          k = e / kBM;
+        }
+        const bool ok = kt + k < kend && m0 + m < M;
+        cp_async8(&sm.As[buf][k][m], ok ? la.addr(b, kt + k, m0 + m) : adummy, ok);
+        int kb, nb;
+        if (LB::kKContig) {
+          kb = e % kABK;
+          nb = e / kABK;
+        } else {
+          nb = e % kBN;
+          kb = e / kBN;
+        }
+        const bool okb = kt + kb < kend && n0 + nb < N;
+        cp_async8(&sm.Bs[buf][kb][nb], okb ? lb.addr(b, kt + kb, n0 + nb) : bdummy, okb);
+      }
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < kAStages - 1; ++s0) {
+      if (s0 < nk) issue(s0);
+      cp_async_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+      cp_async_wait<kAStages - 2>();
+      __syncthreads();
+      if (it + kAStages - 1 < nk) issue(it + kAStages - 1);
+      cp_async_commit();
+      const int buf = it % kAStages;
+#pragma unroll
+      for (int kk = 0; kk < kABK / 4; ++kk) {
+        const int kr = kk * 4 + (lane & 3);
+        double a[4], bb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sm.As[buf][kr][wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bb[j] = sm.Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(wt.acc[i][j], a[i], bb[j]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the ring may be refilled by a following tile
+  }
+  ep(b, split, m0 + wm * 32, n0 + wn * 32, lane, M, N, wt);
+}
+
 template <class LA, class LB, class EP>
 __device__ __forceinline__ void gemm_tile(int b, int M, int N, int m0, int n0, int kbeg, int kend,
                                           int split, const LA& la, const LB& lb, const EP& ep) {
+  if constexpr (RawLoader<LA>::value && RawLoader<LB>::value) {
+    gemm_tile_async(b, M, N, m0, n0, kbeg, kend, split, la, lb, ep);
+    return;
+  }
   GemmSmem& sm = gemm_smem();
   auto& As = sm.As;
   auto& Bs = sm.Bs;

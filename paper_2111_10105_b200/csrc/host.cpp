@@ -675,6 +675,10 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   cd.rhs_off = (const unsigned long long*)get(cp.rhs_off.size() * 8);
   cd.perm = (const uint32_t*)get(cp.perm.size() * 4);
   cd.level_sup = (const uint32_t*)get(cp.level_sup.size() * 4 + 4);
+  cd.level_ptr = (const uint32_t*)get(cp.level_ptr.size() * 4 + 4);
+  cd.pull_ptr = (const uint32_t*)get(cp.pull_ptr.size() * 4 + 4);
+  cd.pull_src = (const uint32_t*)get(cp.pull_src.size() * 4 + 4);
+  cd.nlevels = cp.nlevels;
   cd.F = (double*)get(cp.front_off[cp.nsup] * 8);
   cd.Linv = (double*)get(cp.inv_off[cp.nsup] * 8 + 8);
   cd.R = (double*)get(cp.rhs_off[cp.nsup] * p->W * 8);
@@ -724,6 +728,9 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   h2d((void*)cd.rhs_off, cp.rhs_off.data(), cp.rhs_off.size() * 8);
   h2d((void*)cd.perm, cp.perm.data(), cp.perm.size() * 4);
   h2d((void*)cd.level_sup, cp.level_sup.data(), cp.level_sup.size() * 4);
+  h2d((void*)cd.level_ptr, cp.level_ptr.data(), cp.level_ptr.size() * 4);
+  h2d((void*)cd.pull_ptr, cp.pull_ptr.data(), cp.pull_ptr.size() * 4);
+  h2d((void*)cd.pull_src, cp.pull_src.data(), cp.pull_src.size() * 4);
   if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) return {DMCG_E_CUDA, "CudaError: decode plan upload failed"};
   tm.lap("upload+sync");

@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(kGemmThreads) k_probe(double* A, int m, int k0
   } else if (mode == 7) {
     gemm_tile(0, T, T, ti * kBM, tj * kBN, 0, 16, 0, lp, lp, EpiSum{A + (size_t)m * m});
   } else if (mode == 6) {
-    gemm_tile_probe(T, T, ti * kBM, tj * kBN, 16, lp, lp, A + (size_t)m * m);
   } else {  // loads only
     double acc = 0.0;
     for (int i = threadIdx.x; i < 32 * 64; i += blockDim.x) acc += lp(0, i / 64, ti * 64 + i % 64);
