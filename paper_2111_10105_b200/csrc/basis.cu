@@ -46,7 +46,8 @@ __device__ double block_sum(double v, double* red) {
 // deterministic) A updates and rotates only its slice of V rows, so no
 // inter-CTA traffic is needed.  a_smem = 0 keeps A and V in `work`
 // (gridDim.y must then be 1).
-constexpr int kJacThreads = 512;
+constexpr int kJacThreads = 1024;
+__device__ int g_jacobi_sweeps[8];  // sweeps of the last k_jacobi per matrix (DMCG_DEBUG)
 
 __global__ void __launch_bounds__(kJacThreads)
     k_jacobi(int m, const double* __restrict__ Aall, double* work, double* Vall, double* wall,
@@ -86,6 +87,31 @@ __global__ void __launch_bounds__(kJacThreads)
   // per-thread task cursors (square h x h for A blocks, h x nr for V rows)
   const int da = NT / h, db = NT % h;
   const int dva = nr > 0 ? NT / nr : 0, dvr = nr > 0 ? NT % nr : 0;
+  // Fast path: the tasks of a thread are the same every round, so their
+  // (pair, pair) / (pair, row) indices are computed once here (upper
+  // triangle of the h x h block grid incl. its diagonal; h x nr V rows).
+  constexpr int kTA = 4, kTV = 8;
+  const int ntri = h * (h + 1) / 2, nvt = h * nr;
+  const bool fast = ntri <= kTA * NT && nvt <= kTV * NT;
+  int ta[kTA], tb[kTA], va[kTV], vr[kTV];
+#pragma unroll
+  for (int k = 0; k < kTA; ++k) {
+    const int t = tid + k * NT;
+    int a = 0, off = 0;
+    if (t < ntri)
+      while (off + (h - a) <= t) {
+        off += h - a;
+        ++a;
+      }
+    ta[k] = t < ntri ? a : -1;
+    tb[k] = t < ntri ? a + (t - off) : 0;
+  }
+#pragma unroll
+  for (int k = 0; k < kTV; ++k) {
+    const int t = tid + k * NT;
+    va[k] = (nr > 0 && t < nvt) ? t / nr : -1;
+    vr[k] = (nr > 0 && t < nvt) ? t % nr : 0;
+  }
   bool converged = (m2 <= 1);
   for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
     int any = 0;
@@ -111,16 +137,19 @@ __global__ void __launch_bounds__(kJacThreads)
         Qi[i] = q;
         const double app = A[p * ld + p], aqq = A[q * ld + q];
         const double apq = A[q * ld + p];
-        const double rel = 1e-17 * sqrt(fabs(app) * fabs(aqq));
-        const double thresh = rel > abs_thresh ? rel : abs_thresh;
+        // |apq| > max(1e-17 sqrt(|app aqq|), abs_thresh), compared in squares
+        const double rel2 = 1e-34 * fabs(app) * fabs(aqq);
+        const double apq2 = apq * apq;
         double c = 1.0, sv = 0.0, tt = 0.0;
-        if (fabs(apq) > thresh) {
-          const double theta = (aqq - app) / (2.0 * apq);
-          if (fabs(theta) > 1e150)
-            tt = 0.5 / theta;
+        if (apq2 > rel2 && fabs(apq) > abs_thresh) {
+          // reciprocal forms of the oracle's divisions (last-ulp differences)
+          const double theta = (aqq - app) * (0.5 * __drcp_rn(apq));
+          const double at = fabs(theta);
+          if (at > 1e150)
+            tt = 0.5 * __drcp_rn(theta);
           else
-            tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          c = rsqrt(tt * tt + 1.0);
+            tt = (theta >= 0.0 ? 1.0 : -1.0) * __drcp_rn(at + sqrt(fma(theta, theta, 1.0)));
+          c = rsqrt(fma(tt, tt, 1.0));
           sv = tt * c;
           on = 1;
         }
@@ -130,6 +159,58 @@ __global__ void __launch_bounds__(kJacThreads)
       }
       if (!__syncthreads_or(on)) continue;  // nothing to rotate at this step
       any = 1;
+      if (fast) {
+#pragma unroll
+        for (int k = 0; k < kTA; ++k) {
+          const int a = ta[k], bb = tb[k];
+          if (a < 0) continue;
+          const int p1 = P[a], q1 = Qi[a];
+          if (a == bb) {
+            const double t = tn[a];
+            if (t != 0.0) {
+              const double apq = A[q1 * ld + p1];
+              A[p1 * ld + p1] = A[p1 * ld + p1] - t * apq;
+              A[q1 * ld + q1] = A[q1 * ld + q1] + t * apq;
+              A[q1 * ld + p1] = 0.0;
+              A[p1 * ld + q1] = 0.0;
+            }
+            continue;
+          }
+          const double sa = sn[a], sb = sn[bb];
+          if (sa == 0.0 && sb == 0.0) continue;
+          const int p2 = P[bb], q2 = Qi[bb];
+          const double ca = cs[a], cb = cs[bb];
+          const double b00 = A[p2 * ld + p1], b01 = A[q2 * ld + p1];
+          const double b10 = A[p2 * ld + q1], b11 = A[q2 * ld + q1];
+          const double r00 = ca * b00 - sa * b10, r01 = ca * b01 - sa * b11;
+          const double r10 = sa * b00 + ca * b10, r11 = sa * b01 + ca * b11;
+          const double n00 = cb * r00 - sb * r01, n01 = sb * r00 + cb * r01;
+          const double n10 = cb * r10 - sb * r11, n11 = sb * r10 + cb * r11;
+          A[p2 * ld + p1] = n00;
+          A[p1 * ld + p2] = n00;
+          A[q2 * ld + p1] = n01;
+          A[p1 * ld + q2] = n01;
+          A[p2 * ld + q1] = n10;
+          A[q1 * ld + p2] = n10;
+          A[q2 * ld + q1] = n11;
+          A[q1 * ld + q2] = n11;
+        }
+#pragma unroll
+        for (int k = 0; k < kTV; ++k) {
+          const int a = va[k], r = vr[k];
+          if (a < 0) continue;
+          const double sa = sn[a];
+          if (sa == 0.0) continue;
+          const double ca = cs[a];
+          double* vp = V + P[a] * ldv;
+          double* vq = V + Qi[a] * ldv;
+          const double x = vp[r], y = vq[r];
+          vp[r] = ca * x - sa * y;
+          vq[r] = sa * x + ca * y;
+        }
+        __syncthreads();
+        continue;
+      }
       {
         int a = tid / h, bb = tid % h;
         for (; a < h; a += da, bb += db) {
@@ -192,6 +273,22 @@ __global__ void __launch_bounds__(kJacThreads)
       __syncthreads();
     }
     converged = !any;
+    if (!converged) {
+      // A sweep that rotated is followed by a rotation-free one only if no
+      // pair is above its threshold now (A does not change during a sweep
+      // without rotations, and a sweep visits every pair): test that
+      // directly instead of running the empty sweep.
+      int hot = 0;
+      for (int t = tid; t < m2 * m2; t += NT) {
+        const int p = t % m2, q = t / m2;
+        if (p >= q) continue;
+        const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[q * ld + p];
+        const double rel = 1e-17 * sqrt(fabs(app) * fabs(aqq));
+        if (fabs(apq) > (rel > abs_thresh ? rel : abs_thresh)) hot = 1;
+      }
+      converged = !__syncthreads_or(hot);
+    }
+    if (threadIdx.x == 0 && sp == 0 && b < 8) g_jacobi_sweeps[b] = sweep + 1;
   }
   double* Vo = Vall + (size_t)b * m * m;
   for (int c = 0; c < m; ++c)
@@ -1028,6 +1125,13 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
     cudaError_t e = set_smem_attr((const void*)k_jacobi, smem);
     if (e != cudaSuccess) return e;
     k_jacobi<<<dim3(nbatch, nsplit), kJacThreads, smem, s>>>(m, A, work, V, w, flags, 1, vr);
+    static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
+    if (dbg) {
+      int sw[8] = {};
+      cudaStreamSynchronize(s);
+      cudaMemcpyFromSymbol(sw, g_jacobi_sweeps, sizeof(sw));
+      fprintf(stderr, "dmcg: k_jacobi m=%d split %d sweeps %d %d %d\n", m, nsplit, sw[0], sw[1], sw[2]);
+    }
   } else {
     k_jacobi<<<dim3(nbatch, 1), kJacThreads, 0, s>>>(m, A, work, V, w, flags, 0, m2);
   }
