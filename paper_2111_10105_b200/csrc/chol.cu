@@ -115,9 +115,19 @@ __global__ void __launch_bounds__(kPanelThreads)
   if (k0 >= w) return;
   const int pw = min(nb, w - k0);
   double* A = d.F + d.front_off[s];
-  for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
-    const int c = t / pw, r = t % pw;
-    D[r][c] = r >= c ? A[(size_t)(k0 + c) * m + k0 + r] : 0.0;
+  {  // the kNB x kNB diagonal block: all loads of a thread issued together
+    constexpr int kPer = kNB * kNB / kPanelThreads;
+    double v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = threadIdx.x + u * kPanelThreads, c = t / kNB, r = t % kNB;
+      v[u] = (r < pw && c < pw && r >= c) ? A[(size_t)(k0 + c) * m + k0 + r] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int t = threadIdx.x + u * kPanelThreads, c = t / kNB, r = t % kNB;
+      D[r][c] = v[u];
+    }
   }
   __syncthreads();
   // Right-looking Cholesky of D with one barrier per pivot: columns stay
@@ -253,7 +263,20 @@ __global__ void __launch_bounds__(kIB) k_inv_diag(CholDev d, const uint32_t* lsu
   const double* A = d.F + d.front_off[s];
   double* V = d.Linv + d.inv_off[s];
   const int c = threadIdx.x;
-  for (int r = 0; r < bs; ++r) Ls[r][c] = (c < bs && c <= r) ? A[(size_t)(b0 + c) * m + b0 + r] : 0.0;
+  __shared__ double rdiag[kIB];
+  // thread = row, 16 column loads in flight (column-major front)
+  for (int c8 = 0; c8 < kIB; c8 += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int cc = c8 + u;
+      v[u] = (c < bs && cc < bs && cc <= c) ? A[(size_t)(b0 + cc) * m + b0 + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) Ls[c][c8 + u] = v[u];
+  }
+  __syncthreads();
+  if (c < bs) rdiag[c] = 1.0 / Ls[c][c];
   __syncthreads();
   if (c < bs) {
     for (int r = 0; r < bs; ++r) {
@@ -261,9 +284,15 @@ __global__ void __launch_bounds__(kIB) k_inv_diag(CholDev d, const uint32_t* lsu
         Xs[r][c] = 0.0;
         continue;
       }
-      double acc = (r == c) ? 1.0 : 0.0;
-      for (int k = c; k < r; ++k) acc -= Ls[r][k] * Xs[k][c];
-      Xs[r][c] = acc / Ls[r][r];
+      // two partial sums so the chain over k is half as long
+      double a0 = (r == c) ? 1.0 : 0.0, a1 = 0.0;
+      int k = c;
+      for (; k + 1 < r; k += 2) {
+        a0 -= Ls[r][k] * Xs[k][c];
+        a1 -= Ls[r][k + 1] * Xs[k + 1][c];
+      }
+      if (k < r) a0 -= Ls[r][k] * Xs[k][c];
+      Xs[r][c] = (a0 + a1) * rdiag[r];
     }
   }
   __syncthreads();
