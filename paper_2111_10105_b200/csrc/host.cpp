@@ -226,6 +226,15 @@ void build_normal_matrix(MeshHost* m) {
   }
 }
 
+uint64_t hash_faces(const uint32_t* faces, uint32_t n_faces) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the index words
+  for (size_t t = 0; t < 3 * (size_t)n_faces; ++t) {
+    h ^= faces[t];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
 // ---- anchors (src/codec.cpp:199-242) ----------------------------------------
 namespace {
 struct Mt64 {  // MT19937-64, the engine std::mt19937_64 specifies
@@ -352,6 +361,7 @@ int dmcg_create(dmcg_ctx** out, int device) {
 void dmcg_destroy(dmcg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  c->pending.reset();
   cudaStreamSynchronize(c->stream);
   c->pool.release_all();
   cudaStreamDestroy(c->stream);
@@ -603,7 +613,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
 dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
   if (p->d_m_rp) return Status::ok();
   PhaseTimer tm("normal");
-  build_normal_matrix(&p->mesh);
+  if (!p->chol_given) build_normal_matrix(&p->mesh);
   tm.lap("build");
   const MeshHost& m = p->mesh;
   p->stats.nnz_normal = (long long)m.m_ci.size();
@@ -643,9 +653,11 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   // direct solver: symbolic analysis of M (host) + device structures
   {
     const auto t0 = std::chrono::steady_clock::now();
-    chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p->chol);
-    p->analyze_seconds =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (!p->chol_given) chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p->chol);
+    p->analyze_seconds = p->chol_given
+                             ? p->analyze_seconds
+                             : std::chrono::duration<double>(std::chrono::steady_clock::now() - t0)
+                                   .count();
   }
   tm.lap("analyze");
   const CholPlan& cp = p->chol;
@@ -877,6 +889,30 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
                                nullptr, 0, &p);
   if (!st.good()) return ctx->set_error(st);
+  {  // the decoder's analysis of this mesh, overlapped with the GPU encode
+    ctx->pending.reset();
+    static const bool off = std::getenv("DMCG_NO_OVERLAP") != nullptr;
+    if (!off) {
+      auto pa = std::make_unique<PendingAnalysis>();
+      pa->n = seq->n;
+      pa->n_faces = seq->n_faces;
+      pa->faces_hash = hash_faces(seq->faces, seq->n_faces);
+      pa->anchors = p->mesh.anchors;
+      pa->mesh.n = p->mesh.n;
+      pa->mesh.lap_rp = p->mesh.lap_rp;
+      pa->mesh.lap_ci = p->mesh.lap_ci;
+      pa->mesh.anchor_pos = p->mesh.anchor_pos;
+      PendingAnalysis* raw = pa.get();
+      pa->th = std::thread([raw] {
+        const auto t0 = std::chrono::steady_clock::now();
+        build_normal_matrix(&raw->mesh);
+        chol_analyze(raw->n, raw->mesh.m_rp, raw->mesh.m_ci, raw->mesh.m_val, &raw->chol);
+        raw->seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      });
+      ctx->pending = std::move(pa);
+    }
+  }
   tm.lap("plan");
   const size_t bytes = (size_t)seq->n * seq->F * (seq->dtype == DMCG_F32 ? 4 : 8);
   for (int a = 0; a < 3 && st.good(); ++a)
@@ -941,6 +977,19 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
                                in->anchor_idx, in->n_c, &p);
   if (!st.good()) return ctx->set_error(st);
   PhaseTimer tm("decode");
+  if (ctx->pending) {  // analysis started by the last dmcg_encode: used once if it matches
+    std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
+    if (pa->n == in->n && pa->n_faces == in->n_faces &&
+        pa->anchors == p->mesh.anchors && pa->faces_hash == hash_faces(in->faces, in->n_faces)) {
+      if (pa->th.joinable()) pa->th.join();
+      p->mesh.m_rp = std::move(pa->mesh.m_rp);
+      p->mesh.m_ci = std::move(pa->mesh.m_ci);
+      p->mesh.m_val = std::move(pa->mesh.m_val);
+      p->chol = std::move(pa->chol);
+      p->analyze_seconds = pa->seconds;
+      p->chol_given = true;
+    }
+  }
   tm.lap("plan");
   st = upload_impl(p, in);
   tm.lap("upload");

@@ -5,7 +5,9 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dmcg.h"
@@ -70,8 +72,30 @@ Status plan_prepare_decode(dmcg_plan* p);
 Status plan_prepare_normal(dmcg_plan* p);
 }  // namespace dmcg
 
+namespace dmcg {
+// The decoder's host analysis (normal matrix M = L^T L + S^T S and the
+// symbolic Cholesky of M) depends only on the mesh and the anchor set, both
+// known when dmcg_encode starts.  The drop-in encode therefore runs it on a
+// host thread while its GPU work executes; the next dmcg_decode on the same
+// mesh and anchors takes the result (once) instead of recomputing it.
+struct PendingAnalysis {
+  uint32_t n = 0, n_faces = 0;
+  uint64_t faces_hash = 0;
+  std::vector<uint32_t> anchors;
+  MeshHost mesh;    // lap_rp / lap_ci / anchor_pos in, m_rp / m_ci / m_val out
+  CholPlan chol;
+  double seconds = 0.0;
+  std::thread th;
+  ~PendingAnalysis() {
+    if (th.joinable()) th.join();
+  }
+};
+uint64_t hash_faces(const uint32_t* faces, uint32_t n_faces);
+}  // namespace dmcg
+
 struct dmcg_ctx {
   int device = 0;
+  std::unique_ptr<dmcg::PendingAnalysis> pending;  // see PendingAnalysis
   cudaStream_t stream = nullptr;
   std::string err;
   dmcg::DevicePool pool;
@@ -147,6 +171,7 @@ struct dmcg_plan {
   double *d_rm_y = nullptr, *d_rm_xp = nullptr, *d_rm_r = nullptr;     // permuted / residual
   double analyze_seconds = 0.0;
   bool decode_ready = false;
+  bool chol_given = false;          // chol / mesh.m_* were filled by a PendingAnalysis
   bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
   dmcg::PlanGraph g_encode, g_decode;

@@ -282,3 +282,21 @@ def test_config3_full_size_properties(codec):
     bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
     err = max(np.abs(x[a] - s.axes[a]).max() for a in range(3))
     assert err < 1e-2 * bbox
+
+
+def test_overlapped_analysis_is_used_once_and_only_for_its_mesh(codec):
+    """dmcg_encode starts the decoder's mesh analysis on a host thread; the next
+    dmcg_decode takes it only when mesh and anchors match, and only once."""
+    s1 = synth.CONFIGS["c0"].make()
+    s2 = synth.sphere(3, 32, 4, 0, seed=9)
+    cfg = C.EncoderConfig(k_l=16, row_bits=[12] * 16, oi_rounds=6)
+    g1 = codec.encode(s1, cfg)
+    x_pending = codec.decode(g1)          # takes the analysis started by encode(s1)
+    x_fresh = codec.decode(g1)            # nothing pending: analyses itself
+    g2 = codec.encode(s2, cfg)            # pending analysis now belongs to s2's mesh
+    x_mismatch = codec.decode(g1)         # must ignore it
+    x2 = codec.decode(g2)                 # pending was consumed above: analyses itself
+    for a in range(3):
+        assert np.array_equal(x_pending[a], x_fresh[a])
+        assert np.array_equal(x_mismatch[a], x_fresh[a])
+    assert x2[0].shape == (s2.n, s2.F)
