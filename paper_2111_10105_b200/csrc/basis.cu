@@ -1148,7 +1148,8 @@ static cudaError_t oi_launch(cudaStream_t s, int nbatch, size_t smem, int F, int
   const void* fn = (const void*)k_oi_fused<SMEM, MAXR>;
   cudaError_t e = set_smem_attr(fn, smem);
   if (e != cudaSuccess) return e;
-  int cs = kOiCluster;
+  static const int cs_env = getenv("DMCG_OI_CLUSTER") ? atoi(getenv("DMCG_OI_CLUSTER")) : 0;
+  int cs = cs_env >= 1 && cs_env <= 8 ? cs_env : kOiCluster;  // override for tests
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1162,7 +1163,8 @@ static cudaError_t oi_launch(cudaStream_t s, int nbatch, size_t smem, int F, int
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, k_oi_fused<SMEM, MAXR>, &cfg) != cudaSuccess ||
+  if (cs == 1 ||
+      cudaOccupancyMaxActiveClusters(&nclusters, k_oi_fused<SMEM, MAXR>, &cfg) != cudaSuccess ||
       nclusters < 1) {
     cudaGetLastError();
     cs = 1;  // no room for a cluster of this size: one CTA per axis

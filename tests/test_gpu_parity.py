@@ -300,3 +300,29 @@ def test_overlapped_analysis_is_used_once_and_only_for_its_mesh(codec):
         assert np.array_equal(x_pending[a], x_fresh[a])
         assert np.array_equal(x_mismatch[a], x_fresh[a])
     assert x2[0].shape == (s2.n, s2.F)
+
+
+def test_single_cta_oi_fallback_matches():
+    """The one-CTA-per-axis OI path (used when no cluster of 8 fits) gives the
+    same basis as the cluster path to rounding (subprocess: the override is
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path[:0] = ['.', 'oracle'];"
+        "from paper_2111_10105_b200 import codec as C, synth;"
+        "s = synth.CONFIGS['c1']; q = s.make(); cd = C.Codec(0);"
+        "g = cd.encode(q, C.EncoderConfig(k_l=s.k, row_bits=[s.bits]*s.k, oi_rounds=s.rounds));"
+        "np.save(sys.argv[1], np.stack([g.dict_q[a][:8] for a in range(3)]))")
+    outs = []
+    for cs in ("1", "8"):
+        path = f"/tmp/dmcg_oi_cs{cs}.npy"
+        env = dict(os.environ, DMCG_OI_CLUSTER=cs)
+        r = subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path).astype(np.int64))
+    # the 8 leading dictionary columns (well separated on c1) agree to +-1 level
+    assert np.abs(outs[0] - outs[1]).max() <= 1
