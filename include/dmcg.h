@@ -218,6 +218,13 @@ int dmcg_plan_stats(const dmcg_plan* plan, dmcg_stats* out);
 int dmcg_ctx_stats(const dmcg_ctx* ctx, dmcg_stats* out);
 /* Stream the plan runs on (cudaStream_t), for event timing by callers. */
 void* dmcg_plan_stream(dmcg_plan* plan);
+/* serialize() of the plan's device-resident symbols: the
+ * bit-packed payload sections (dictionary, coefficient and anchor levels;
+ * reference BitWriter, src/quantize.cpp:50-69) are packed on the GPU, the
+ * header / row headers / indices on the host; bytes identical to
+ * dmcg_serialize of dmcg_plan_download's result.  out == NULL queries the
+ * size.  Returns the stream size, 0 on error (cap too small / CUDA). */
+size_t dmcg_plan_serialize(dmcg_plan* plan, uint8_t* out, size_t cap, dmcg_sections* s);
 
 /* ---- diagnostics (host only, no GPU) ----------------------------------
  * Symbolic analysis of the anchored normal matrix of a mesh and, when W > 0,

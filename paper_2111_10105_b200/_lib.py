@@ -21,6 +21,7 @@ intp = ctypes.POINTER(ctypes.c_int)
 vp = ctypes.c_void_p
 
 DMCG_OK = 0
+DMCG_E_CUDA = 10
 DMCG_F64, DMCG_F32 = 0, 1
 DMCG_PCA_QP = 4
 
@@ -32,6 +33,7 @@ EXPORTS = [
     "dmcg_anchor_count", "dmcg_select_anchors", "dmcg_plan_create", "dmcg_plan_destroy",
     "dmcg_plan_encode_device", "dmcg_plan_decode_device", "dmcg_plan_download", "dmcg_plan_upload",
     "dmcg_plan_basis", "dmcg_plan_stats", "dmcg_ctx_stats", "dmcg_plan_stream", "dmcg_debug_chol",
+    "dmcg_plan_serialize",
 ]
 
 
@@ -146,5 +148,7 @@ def lib():
     L.dmcg_ctx_stats.argtypes = [vp, ctypes.POINTER(DmcgStats)]
     L.dmcg_plan_stream.argtypes = [vp]
     L.dmcg_plan_stream.restype = vp
+    L.dmcg_plan_serialize.restype = ctypes.c_size_t
+    L.dmcg_plan_serialize.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.POINTER(DmcgSections)]
     _lib = L
     return L

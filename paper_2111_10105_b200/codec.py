@@ -286,6 +286,20 @@ class Plan:
     def stream(self) -> int:
         return L.lib().dmcg_plan_stream(self._p) or 0
 
+    def serialize(self):
+        """DMC1 bytes of the device-resident symbols, payload bit-packed on the
+        GPU (dmcg_plan_serialize): (bytes, SectionSizes dict), identical to
+        serialize(self.download())."""
+        s = L.DmcgSections()
+        size = L.lib().dmcg_plan_serialize(self._p, None, 0, ctypes.byref(s))
+        if size == 0:
+            _check(self.codec.handle, L.DMCG_E_CUDA)
+        buf = np.zeros(size, np.uint8)
+        got = L.lib().dmcg_plan_serialize(self._p, buf.ctypes.data_as(L.u8p), size, ctypes.byref(s))
+        if got != size:
+            _check(self.codec.handle, L.DMCG_E_CUDA)
+        return buf.tobytes(), {f: getattr(s, f) for f, _ in L.DmcgSections._fields_}
+
 
 # ---- stream / metrics / helpers (host C++ in libdmcg.so) --------------------
 

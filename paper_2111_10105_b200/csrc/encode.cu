@@ -224,3 +224,65 @@ cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
 }
 
 }  // namespace dmcg
+
+// ---- f1: DMC1 payload bit packing on the device (stream.cpp BitWriter) ------
+namespace dmcg {
+namespace {
+
+// ORs symbol v (b bits, MSB first) into the stream at bit position P; bytes
+// are little-endian inside the 32-bit words of `out` (byte B at word B/4).
+__device__ __forceinline__ void put_bits(uint32_t* out, unsigned long long P, uint32_t v, int b) {
+  const unsigned long long end = P + (unsigned)b;
+  for (unsigned long long B = P >> 3; B <= (end - 1) >> 3; ++B) {
+    const unsigned long long lo = P > B * 8 ? P : B * 8;
+    const unsigned long long hi = end < B * 8 + 8 ? end : B * 8 + 8;
+    const int nb = (int)(hi - lo);
+    const uint32_t part = (v >> (unsigned)(end - hi)) & ((1u << nb) - 1u);
+    const uint32_t byte = part << (unsigned)(B * 8 + 8 - hi);
+    atomicOr(&out[B >> 2], byte << (8 * (unsigned)(B & 3)));
+  }
+}
+
+__global__ void k_pack_uniform(const uint16_t* __restrict__ sym, long count, int bits,
+                               unsigned long long base_bit, uint32_t* out) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  put_bits(out, base_bit + (unsigned long long)t * bits, sym[t], bits);
+}
+
+// Rows of n symbols; row r starts at row_bitoff[r] (~0: row carries no payload).
+__global__ void k_pack_rows(const uint16_t* __restrict__ sym, long n, int rows,
+                            const uint8_t* __restrict__ row_bits,
+                            const unsigned long long* __restrict__ row_bitoff,
+                            unsigned long long base_bit, uint32_t* out) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= n * rows) return;
+  const int r = (int)(t / n);
+  const long i = t % n;
+  const unsigned long long off = row_bitoff[r];
+  if (off == ~0ull) return;
+  const int b = row_bits[r];
+  put_bits(out, base_bit + off + (unsigned long long)i * b, sym[t], b);
+}
+
+}  // namespace
+
+cudaError_t launch_pack_uniform(cudaStream_t s, const uint16_t* sym, long count, int bits,
+                                unsigned long long base_byte, uint32_t* out) {
+  if (count <= 0) return cudaSuccess;
+  k_pack_uniform<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(sym, count, bits, base_byte * 8,
+                                                                 out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_rows(cudaStream_t s, const uint16_t* sym, long n, int rows,
+                             const uint8_t* row_bits, const unsigned long long* row_bitoff,
+                             unsigned long long base_byte, uint32_t* out) {
+  if (n <= 0 || rows <= 0) return cudaSuccess;
+  const long tot = n * rows;
+  k_pack_rows<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(sym, n, rows, row_bits, row_bitoff,
+                                                            base_byte * 8, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dmcg

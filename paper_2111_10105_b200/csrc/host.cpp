@@ -752,6 +752,18 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
 
 extern "C" {
 
+static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_sections* sec,
+                                  size_t* size);
+
+size_t dmcg_plan_serialize(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_sections* sec) {
+  if (!p) return 0;
+  cudaSetDevice(p->ctx->device);
+  size_t size = 0;
+  Status st = plan_serialize_impl(p, out, cap, sec, &size);
+  p->ctx->set_error(st);
+  return st.good() ? size : 0;
+}
+
 int dmcg_plan_create(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uint32_t* faces,
                      uint32_t n_faces, const dmcg_config* cfg, dmcg_plan** plan) {
   if (!ctx || !plan || !cfg) return DMCG_E_CONFIG;
@@ -823,6 +835,95 @@ int dmcg_plan_download(dmcg_plan* p, dmcg_encoded* out) {
   if (!p || !out) return DMCG_E_CONFIG;
   cudaSetDevice(p->ctx->device);
   return p->ctx->set_error(download_impl(p, out));
+}
+
+// dmcg_plan_serialize: host frame + device payload packing (see dmcg.h).
+static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_sections* sec,
+                                  size_t* size) {
+  cudaStream_t s = p->ctx->stream;
+  const size_t n = p->n, F = p->F, k = p->k;
+  std::vector<float> rmin(3 * k + 1), rmax(3 * k + 1);
+  std::vector<uint8_t> rbits(3 * k + 1);
+  float rng[6];
+  if (k) {
+    CUDA_OK(cudaMemcpyAsync(rmin.data(), p->d_row_min, 3 * k * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(rmax.data(), p->d_row_max, 3 * k * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(cudaMemcpyAsync(rbits.data(), p->d_row_bits, 3 * k, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaStreamSynchronize(s));
+  dmcg_encoded m;
+  std::memset(&m, 0, sizeof(m));
+  m.n = p->n;
+  m.F = p->F;
+  m.k_l = p->k;
+  m.n_c = p->n_c;
+  m.n_faces = p->n_faces;
+  m.variant = DMCG_PCA_QP;
+  m.anchor_bits = (uint8_t)p->anchor_bits;
+  m.dict_bits = (uint8_t)p->dict_bits;
+  m.diff_bits = (uint8_t)p->diff_bits;
+  m.faces = p->faces.data();
+  m.anchor_idx = p->mesh.anchors.data();
+  for (int a = 0; a < 3; ++a) {
+    m.row_min[a] = rmin.data() + a * k;
+    m.row_max[a] = rmax.data() + a * k;
+    m.row_bits[a] = rbits.data() + a * k;
+    m.anchor_min[a] = rng[2 * a];
+    m.anchor_max[a] = rng[2 * a + 1];
+  }
+  PayloadSpans sp;
+  const size_t total = serialize_stream(&m, nullptr, 0, sec, &sp);
+  *size = total;
+  if (!out) return Status::ok();
+  if (cap < total) return {DMCG_E_CONFIG, "ConfigError: serialize buffer too small"};
+  serialize_stream(&m, out, cap, sec, &sp);  // header, faces, row headers, indices, ranges
+  // payload bit offsets of the coefficient rows (degenerate rows carry none)
+  std::vector<unsigned long long> off(3 * k + 1, ~0ull);
+  for (int a = 0; a < 3; ++a) {
+    unsigned long long bit = 0;
+    for (size_t r = 0; r < k; ++r)
+      if (rmin[a * k + r] != rmax[a * k + r]) {
+        off[a * k + r] = bit;
+        bit += (unsigned long long)n * rbits[a * k + r];
+      }
+  }
+  const size_t words = (total + 3) / 4;
+  if (p->stream_cap < words) {
+    p->d_stream = (uint32_t*)plan_alloc(p, words * 4);
+    p->stream_cap = p->d_stream ? words : 0;
+  }
+  if (!p->d_row_bitoff) p->d_row_bitoff = (unsigned long long*)plan_alloc(p, (3 * k + 1) * 8);
+  if (!p->d_stream || !p->d_row_bitoff)
+    return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  CUDA_OK(cudaMemsetAsync(p->d_stream, 0, words * 4, s));
+  if (k)
+    CUDA_OK(cudaMemcpyAsync(p->d_row_bitoff, off.data(), 3 * k * 8, cudaMemcpyHostToDevice, s));
+  const size_t FF = F * F;
+  for (int a = 0; a < 3; ++a) {
+    CUDA_OK(launch_pack_uniform(s, p->d_dict_q + a * FF, (long)FF, p->dict_bits, sp.dict[a],
+                                p->d_stream));
+    if (k)
+      CUDA_OK(launch_pack_rows(s, p->d_coeff_q + a * k * n, (long)n, (int)k, p->d_row_bits + a * k,
+                               p->d_row_bitoff + a * k, sp.coeff[a], p->d_stream));
+    CUDA_OK(launch_pack_uniform(s, p->d_anchor_q + a * (size_t)p->n_c * F, (long)p->n_c * F,
+                                p->anchor_bits, sp.anchor[a], p->d_stream));
+  }
+  const uint8_t* dev = (const uint8_t*)p->d_stream;
+  auto span_copy = [&](size_t off0, size_t bytes) -> cudaError_t {
+    return bytes ? cudaMemcpyAsync(out + off0, dev + off0, bytes, cudaMemcpyDeviceToHost, s)
+                 : cudaSuccess;
+  };
+  for (int a = 0; a < 3; ++a) {
+    size_t cbits = 0;
+    for (size_t r = 0; r < k; ++r)
+      if (rmin[a * k + r] != rmax[a * k + r]) cbits += n * rbits[a * k + r];
+    CUDA_OK(span_copy(sp.dict[a], (FF * p->dict_bits + 7) / 8));
+    CUDA_OK(span_copy(sp.coeff[a], (cbits + 7) / 8));
+    CUDA_OK(span_copy(sp.anchor[a], ((size_t)p->n_c * F * p->anchor_bits + 7) / 8));
+  }
+  CUDA_OK(cudaStreamSynchronize(s));
+  return Status::ok();
 }
 
 static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {

@@ -91,6 +91,13 @@ struct PendingAnalysis {
   }
 };
 uint64_t hash_faces(const uint32_t* faces, uint32_t n_faces);
+
+// Byte offsets of the bit-packed payload sections of a DMC1 stream.
+struct PayloadSpans {
+  size_t dict[3], coeff[3], anchor[3];
+};
+size_t serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sections* s,
+                        PayloadSpans* spans);
 }  // namespace dmcg
 
 struct dmcg_ctx {
@@ -160,6 +167,9 @@ struct dmcg_plan {
   uint16_t* d_anchor_q = nullptr;  // 3 x n_c x F
   // decode
   double* d_rowp = nullptr;        // 3 x k x 2 (min_, width) dequantiser params
+  uint32_t* d_stream = nullptr;    // device DMC1 image for dmcg_plan_serialize
+  size_t stream_cap = 0;
+  unsigned long long* d_row_bitoff = nullptr;  // 3 x k payload bit offsets
   double *d_cg_x = nullptr, *d_cg_r = nullptr, *d_cg_p = nullptr, *d_cg_q = nullptr;
   int* d_cg_iters = nullptr;       // per column
   double* d_cg_res = nullptr;      // per column relative residual

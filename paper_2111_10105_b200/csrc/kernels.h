@@ -27,6 +27,15 @@ cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long 
 cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
                            const void* const x[3], bool f32, int bits, float* rng, uint16_t* q);
 
+// DMC1 payload bit packing (stream.cpp BitWriter, MSB first) into a zeroed
+// byte buffer viewed as 32-bit words; base_byte = the section's byte offset.
+cudaError_t launch_pack_uniform(cudaStream_t s, const uint16_t* sym, long count, int bits,
+                                unsigned long long base_byte, uint32_t* out);
+// rows x n symbols; row r at bit row_bitoff[r] of the section (~0: no payload).
+cudaError_t launch_pack_rows(cudaStream_t s, const uint16_t* sym, long n, int rows,
+                             const uint8_t* row_bits, const unsigned long long* row_bitoff,
+                             unsigned long long base_byte, uint32_t* out);
+
 // ---- basis.cu --------------------------------------------------------------
 // Round-robin Jacobi eigensolver of symmetric m x m A (col-major, per
 // batch).  work: nbatch * 2 * m2 * (m2 + 1) doubles (m2 = m + m%2).  Writes V

@@ -116,12 +116,20 @@ void unpack(const uint8_t* src, size_t count, int bits, uint16_t* out) {
 
 size_t packed_bytes(size_t count, int bits) { return (count * (size_t)bits + 7) / 8; }
 
+// Skips `bytes` payload bytes (their content is written elsewhere).
+void skip(ByteOut& w, size_t bytes) {
+  if (w.o && w.pos + bytes > w.cap) w.overflow = true;
+  w.pos += bytes;
+}
+
 }  // namespace
 
-extern "C" {
-
-size_t dmcg_serialize(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sections* s) {
-  if (!e) return 0;
+// Writes the DMC1 stream of e.  With spans == nullptr the payload sections
+// (dictionary, coefficient and anchor levels) are bit-packed here; otherwise
+// they are only sized and their byte offsets reported in spans (the GPU
+// packer fills them: dmcg_plan_serialize).
+size_t dmcg::serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sections* s,
+                             PayloadSpans* spans) {
   dmcg_sections sz;
   std::memset(&sz, 0, sizeof(sz));
   ByteOut w{out, cap};
@@ -147,7 +155,10 @@ size_t dmcg_serialize(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sect
   const size_t FF = (size_t)e->F * e->F;
   for (int a = 0; a < 3; ++a) {
     size_t start = w.pos;
-    {
+    if (spans) {
+      spans->dict[a] = w.pos;
+      skip(w, packed_bytes(FF, e->dict_bits));
+    } else {
       BitOut b(w);
       for (size_t t = 0; t < FF; ++t) b.put(e->dict_q[a][t], e->dict_bits);
       b.flush();
@@ -161,7 +172,13 @@ size_t dmcg_serialize(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sect
     }
     sz.coeff_headers += w.pos - start;
     start = w.pos;
-    {
+    if (spans) {
+      spans->coeff[a] = w.pos;
+      size_t bits = 0;
+      for (uint32_t r = 0; r < e->k_l; ++r)
+        if (e->row_min[a][r] != e->row_max[a][r]) bits += (size_t)e->n * e->row_bits[a][r];
+      skip(w, (bits + 7) / 8);
+    } else {
       BitOut b(w);
       for (uint32_t r = 0; r < e->k_l; ++r) {
         if (e->row_min[a][r] == e->row_max[a][r]) continue;  // no payload (stream.cpp:114)
@@ -182,14 +199,26 @@ size_t dmcg_serialize(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sect
     w.f32(e->anchor_max[a]);
     sz.anchor_ranges += w.pos - start;
     start = w.pos;
-    BitOut b(w);
-    for (size_t t = 0; t < (size_t)e->n_c * e->F; ++t) b.put(e->anchor_q[a][t], e->anchor_bits);
-    b.flush();
+    if (spans) {
+      spans->anchor[a] = w.pos;
+      skip(w, packed_bytes((size_t)e->n_c * e->F, e->anchor_bits));
+    } else {
+      BitOut b(w);
+      for (size_t t = 0; t < (size_t)e->n_c * e->F; ++t) b.put(e->anchor_q[a][t], e->anchor_bits);
+      b.flush();
+    }
     sz.anchor_payload += w.pos - start;
   }
   if (s) *s = sz;
   if (w.overflow) return 0;
   return w.pos;
+}
+
+extern "C" {
+
+size_t dmcg_serialize(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_sections* s) {
+  if (!e) return 0;
+  return dmcg::serialize_stream(e, out, cap, s, nullptr);
 }
 
 // Header fields + the reference's header checks (stream.cpp:299-336).

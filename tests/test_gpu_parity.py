@@ -326,3 +326,35 @@ def test_single_cta_oi_fallback_matches():
         outs.append(np.load(path).astype(np.int64))
     # the 8 leading dictionary columns (well separated on c1) agree to +-1 level
     assert np.abs(outs[0] - outs[1]).max() <= 1
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_gpu_serialize_matches_host_bytes(codec, name):
+    """the DMC1 payload bit-packed on the GPU (dmcg_plan_serialize)
+    is byte-identical to the host serializer on the downloaded symbols."""
+    import torch
+    spec = synth.CONFIGS[name]
+    s = spec.make()
+    plan = C.Plan(codec, s.n, s.F, s.faces, _cfg(spec))
+    d = [torch.from_numpy(x).cuda() for x in s.axes]
+    plan.encode_device([t.data_ptr() for t in d])
+    gpu_bytes, gpu_sec = plan.serialize()
+    host_bytes, host_sec = C.serialize(plan.download())
+    assert gpu_sec == host_sec
+    assert gpu_bytes == host_bytes
+    assert C.serialize(C.parse(gpu_bytes))[0] == gpu_bytes
+
+
+def test_gpu_serialize_degenerate_and_mixed_bits(codec):
+    """Degenerate (min == max) rows carry no payload and per-row bit depths vary:
+    the GPU bit offsets must follow the host layout exactly."""
+    import torch
+    s = synth.sphere(2, 24, 3, 0, seed=4)
+    static = synth.Sequence(s.faces, [np.repeat(x[:, :1], s.F, axis=1) for x in s.axes])
+    for seq, bits in ((s, [3, 7, 12, 16, 1, 9]), (static, [5, 11, 2, 13, 8, 4])):
+        cfg = C.EncoderConfig(k_l=len(bits), row_bits=bits, oi_rounds=4, dict_bits=11,
+                              anchor_bits=13)
+        plan = C.Plan(codec, seq.n, seq.F, seq.faces, cfg)
+        d = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in seq.axes]
+        plan.encode_device([t.data_ptr() for t in d])
+        assert plan.serialize()[0] == C.serialize(plan.download())[0]
