@@ -101,6 +101,10 @@ typedef struct {
                                1: conjugate gradients */
   int refine;               /* refinement passes after the direct solve
                                (default 1, like refine_anchored, solver.cpp:43-58) */
+  int reuse_factor;         /* plans only: keep the numeric factor of M (it depends on
+                               the mesh and anchors alone, both fixed by the plan) and
+                               skip refactoring on later decodes (default 0: factor
+                               on every decode, like the reference) */
 } dmcg_decode_options;
 
 void dmcg_decode_options_default(dmcg_decode_options* opt);

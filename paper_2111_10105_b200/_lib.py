@@ -49,7 +49,7 @@ class DmcgConfig(ctypes.Structure):
 
 class DmcgDecodeOptions(ctypes.Structure):
     _fields_ = [("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int),
-                ("solver", ctypes.c_int), ("refine", ctypes.c_int)]
+                ("solver", ctypes.c_int), ("refine", ctypes.c_int), ("reuse_factor", ctypes.c_int)]
 
 
 class DmcgSeq(ctypes.Structure):

@@ -129,10 +129,11 @@ class CompressedAnimation:
         self.anchor_max = [float(e.anchor_max[a]) for a in range(3)]
 
 
-def _decode_opts(rtol, max_iter, solver, refine):
+def _decode_opts(rtol, max_iter, solver, refine, reuse_factor=False):
     if solver not in ("direct", "cg"):
         raise ValueError(f"solver must be 'direct' or 'cg', not {solver!r}")
-    return L.DmcgDecodeOptions(rtol, max_iter, 0 if solver == "direct" else 1, refine)
+    return L.DmcgDecodeOptions(rtol, max_iter, 0 if solver == "direct" else 1, refine,
+                               1 if reuse_factor else 0)
 
 
 def _check(ctx, rc):
@@ -252,8 +253,11 @@ class Plan:
         ptrs = (ctypes.c_void_p * 3)(*[int(p) for p in d_axes])
         _check(self.codec.handle, L.lib().dmcg_plan_encode_device(self._p, ptrs))
 
-    def decode_device(self, d_out, rtol=1e-10, max_iter=20000, solver="direct", refine=1):
-        opt = _decode_opts(rtol, max_iter, solver, refine)
+    def decode_device(self, d_out, rtol=1e-10, max_iter=20000, solver="direct", refine=1,
+                      reuse_factor=False):
+        """reuse_factor: keep the plan's numeric factor of M across decodes (many
+        sequences on one mesh); off by default (the reference factors every call)."""
+        opt = _decode_opts(rtol, max_iter, solver, refine, reuse_factor)
         ptrs = (ctypes.c_void_p * 3)(*[int(p) for p in d_out])
         _check(self.codec.handle, L.lib().dmcg_plan_decode_device(self._p, ctypes.byref(opt), ptrs))
 

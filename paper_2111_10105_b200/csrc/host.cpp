@@ -393,6 +393,7 @@ void dmcg_decode_options_default(dmcg_decode_options* o) {
   o->cg_max_iter = 20000;
   o->solver = 0;
   o->refine = 1;
+  o->reuse_factor = 0;
 }
 
 uint32_t dmcg_anchor_count(uint32_t n, double fraction) {

@@ -181,7 +181,8 @@ struct dmcg_plan {
   double *d_rm_y = nullptr, *d_rm_xp = nullptr, *d_rm_r = nullptr;     // permuted / residual
   double analyze_seconds = 0.0;
   bool decode_ready = false;
-  bool chol_given = false;          // chol / mesh.m_* were filled by a PendingAnalysis
+  bool chol_given = false;
+  bool factor_valid = false;        // cdev.F / Linv hold the numeric factor of M          // chol / mesh.m_* were filled by a PendingAnalysis
   bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
   dmcg::PlanGraph g_encode, g_decode;

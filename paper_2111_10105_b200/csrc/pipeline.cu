@@ -325,7 +325,7 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
 
 // Direct decode: K6 into the row-major n x 3F layout, rhs, supernodal
 // Cholesky factor + solve + refinement (solver.cpp:43-58, 82-90).
-static Status enqueue_decode_direct(dmcg_plan* p, int refine, void* const out[3]) {
+static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void* const out[3]) {
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k, W = (int)p->W;
   const bool f32 = p->dtype == DMCG_F32;
@@ -347,7 +347,7 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, void* const out[3]
                          p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_rm_delta, p->d_rm_b,
                          p->d_flags + 1));
   DMCG_TRY(record_event(p->ev[1], s));
-  DMCG_TRY(chol_factor_device(s, p->cdev, p->levels));
+  if (factor) DMCG_TRY(chol_factor_device(s, p->cdev, p->levels));
   DMCG_TRY(record_event(p->ev[2], s));
   DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
   DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, false));
@@ -368,10 +368,11 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   cudaStream_t s = p->ctx->stream;
   const int k = (int)p->k, W = (int)p->W;
   const int refine = opt ? opt->refine : 1;
+  const bool factor = !(opt && opt->reuse_factor && p->factor_valid);
   const void* key[4] = {out[0], out[1], out[2], nullptr};
   {
-    Status st = run_graph(p, p->g_decode, key, refine,
-                          [&] { return enqueue_decode_direct(p, refine, out); });
+    Status st = run_graph(p, p->g_decode, key, refine * 2 + (factor ? 1 : 0),
+                          [&] { return enqueue_decode_direct(p, refine, factor, out); });
     if (!st.good()) return st;
   }
   int flags[8];
@@ -393,9 +394,13 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
                                     refine + 1;
   p->stats.flops_solve = (1 + refine) * p->chol.flops_solve_per_rhs * W;
   if (flags[1]) return Status{DMCG_E_CORRUPT, "CorruptPayload: packed value out of range"};
-  if (flags[4])
+  if (flags[4]) {
+    p->factor_valid = false;
     return Status{DMCG_E_NUMERICAL,
                   "SingularSystem: anchored normal equations are not positive definite"};
+  }
+  p->factor_valid = true;
+  if (!factor) p->stats.ms_factor = 0.0f;
   return Status::ok();
 }
 

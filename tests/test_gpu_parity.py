@@ -358,3 +358,22 @@ def test_gpu_serialize_degenerate_and_mixed_bits(codec):
         d = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in seq.axes]
         plan.encode_device([t.data_ptr() for t in d])
         assert plan.serialize()[0] == C.serialize(plan.download())[0]
+
+
+def test_plan_factor_reuse_gives_identical_frames(codec):
+    """decode_device(reuse_factor=True) skips refactoring M on later decodes of
+    the plan (M depends only on mesh + anchors); the frames are bit-identical."""
+    import torch
+    spec = synth.CONFIGS["c4"]
+    s1, s2 = spec.make(0), spec.make(1)
+    plan = C.Plan(codec, s1.n, s1.F, s1.faces, _cfg(spec))
+    outs = []
+    for s, reuse in ((s1, False), (s2, True), (s2, False)):
+        d = [torch.from_numpy(x).cuda() for x in s.axes]
+        o = [torch.empty_like(t) for t in d]
+        plan.encode_device([t.data_ptr() for t in d])
+        plan.decode_device([t.data_ptr() for t in o], reuse_factor=reuse)
+        outs.append([t.cpu().numpy() for t in o])
+    st = plan.stats()
+    for a in range(3):
+        assert np.array_equal(outs[1][a], outs[2][a])
