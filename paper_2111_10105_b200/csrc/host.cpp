@@ -100,32 +100,42 @@ Status build_mesh(const uint32_t* faces, uint32_t n_faces, uint32_t n, MeshHost*
       col[fill[f[j]]++] = f[(j + 2) % 3];
     }
   }
-  out->adj_rp.assign((size_t)n + 1, 0);
-  out->adj_ci.clear();
-  out->adj_ci.reserve(col.size() / 2 + 1);
-  for (uint32_t i = 0; i < n; ++i) {
-    auto b = col.begin() + cnt[i], e = col.begin() + cnt[i + 1];
-    std::sort(b, e);
-    auto u = std::unique(b, e);
-    out->adj_ci.insert(out->adj_ci.end(), b, u);
-    out->adj_rp[i + 1] = (uint32_t)out->adj_ci.size();
-  }
-  // Laplacian structure (laplacian.cpp:21-37): diagonal in sorted position.
-  out->lap_rp.assign((size_t)n + 1, 0);
-  out->lap_ci.clear();
-  out->lap_ci.reserve(out->adj_ci.size() + n);
-  for (uint32_t i = 0; i < n; ++i) {
-    bool placed = false;
-    for (uint32_t p = out->adj_rp[i]; p < out->adj_rp[i + 1]; ++p) {
-      if (!placed && out->adj_ci[p] > i) {
-        out->lap_ci.push_back(i);
-        placed = true;
-      }
-      out->lap_ci.push_back(out->adj_ci[p]);
+  // per vertex: sort + deduplicate its neighbour list in place (parallel),
+  // then the CSR of the one-ring and of the Laplacian (diagonal in sorted
+  // position) by prefix sums
+  std::vector<uint32_t> deg(n, 0);
+  parallel_for(n, 1024, [&](uint32_t v0, uint32_t v1, uint32_t) {
+    for (uint32_t i = v0; i < v1; ++i) {
+      auto b = col.begin() + cnt[i], e = col.begin() + cnt[i + 1];
+      std::sort(b, e);
+      deg[i] = (uint32_t)(std::unique(b, e) - b);
     }
-    if (!placed) out->lap_ci.push_back(i);
-    out->lap_rp[i + 1] = (uint32_t)out->lap_ci.size();
+  });
+  out->adj_rp.assign((size_t)n + 1, 0);
+  out->lap_rp.assign((size_t)n + 1, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    out->adj_rp[i + 1] = out->adj_rp[i] + deg[i];
+    out->lap_rp[i + 1] = out->lap_rp[i] + deg[i] + 1;
   }
+  out->adj_ci.resize(out->adj_rp[n]);
+  out->lap_ci.resize(out->lap_rp[n]);
+  parallel_for(n, 1024, [&](uint32_t v0, uint32_t v1, uint32_t) {
+    for (uint32_t i = v0; i < v1; ++i) {
+      const uint32_t* src = col.data() + cnt[i];
+      std::copy(src, src + deg[i], out->adj_ci.begin() + out->adj_rp[i]);
+      // Laplacian structure (laplacian.cpp:21-37): diagonal in sorted position
+      uint32_t o = out->lap_rp[i];
+      bool placed = false;
+      for (uint32_t t = 0; t < deg[i]; ++t) {
+        if (!placed && src[t] > i) {
+          out->lap_ci[o++] = i;
+          placed = true;
+        }
+        out->lap_ci[o++] = src[t];
+      }
+      if (!placed) out->lap_ci[o++] = i;
+    }
+  });
   return Status::ok();
 }
 
@@ -486,9 +496,12 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->F = F;
   p->dtype = dtype;
   p->n_faces = n_faces;
+  PhaseTimer tm("plan");
   p->faces.assign(faces, faces + 3 * (size_t)n_faces);
   Status st = build_mesh(faces, n_faces, n, &p->mesh);
+  tm.lap("mesh");
   if (st.good() && !anchors_given) st = validate_mesh(p->mesh);
+  tm.lap("validate");
   if (st.good()) st = check_config(*cfg, n, F, &p->row_bits);
   if (!st.good()) {
     delete p;
@@ -572,6 +585,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     dmcg_plan_destroy(p);
     return {DMCG_E_CUDA, "CudaError: device allocation failed"};
   }
+  tm.lap("alloc");
   for (auto& e : p->ev) cudaEventCreate(&e);
   cudaStream_t s = ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
@@ -593,8 +607,10 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
       for (size_t t = 0; t < (size_t)F * k; ++t)
         start[a * (size_t)F * k + t] = (double)(splitmix64(&st64) >> 11) * 0x1.0p-52 - 1.0;
     }
+  tm.lap("events+start");
   h2d(p->d_start, start.data(), start.size() * 8);
   if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
+  tm.lap("upload+sync");
   if (!ok) {
     dmcg_plan_destroy(p);
     return {DMCG_E_CUDA, "CudaError: plan upload failed"};
