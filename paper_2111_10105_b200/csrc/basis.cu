@@ -355,17 +355,6 @@ __global__ void k_canon_signs(int m, int c0, int ncols, double* Uall, long bs) {
     for (int i = lane; i < m; i += 32) u[i] = -u[i];
 }
 
-// H <- 0.5 (H + H^T) (Rayleigh-Ritz matrix).
-__global__ void k_symmetrize(int m, double* Hall) {
-  double* H = Hall + (size_t)blockIdx.y * m * m;
-  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= (long)m * m) return;
-  const int j = (int)(t / m), i = (int)(t % m);
-  if (i >= j) return;
-  const double s = 0.5 * (H[(size_t)j * m + i] + H[(size_t)i * m + j]);
-  H[(size_t)j * m + i] = s;
-  H[(size_t)i * m + j] = s;
-}
 
 // ---------------------------------------------------------------------------
 // Fused orthogonal iterations: one CTA per axis runs every round
@@ -1071,11 +1060,6 @@ cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int nc
   return cudaGetLastError();
 }
 
-cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H) {
-  dim3 grid((unsigned)(((long)m * m + 255) / 256), nbatch);
-  k_symmetrize<<<grid, 256, 0, s>>>(m, H);
-  return cudaGetLastError();
-}
 
 static cudaError_t set_smem_attr(const void* fn, size_t bytes) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);

@@ -51,7 +51,6 @@ cudaError_t launch_sort_basis(cudaStream_t s, int nbatch, int m, int ncols_store
 // m-row column-major U (batch stride bs).
 cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int ncols, double* U,
                                long bs);
-cudaError_t launch_symmetrize(cudaStream_t s, int nbatch, int m, double* H);
 // Fused orthogonal iterations (one CTA per axis): Q0 = qr(start), `rounds`
 // x {Z = R Q; Q = qr(Z)}, then H = Q^T R Q (symmetrised); R Q is spread over a
 // cluster of CTAs per axis (Q doubles as its L2 staging buffer).  work:
