@@ -48,6 +48,7 @@ __device__ double block_sum(double v, double* red) {
 // (gridDim.y must then be 1).
 constexpr int kJacThreads = 1024;
 __device__ int g_jacobi_sweeps[8];  // sweeps of the last k_jacobi per matrix (DMCG_DEBUG)
+__device__ long long g_jacobi_cyc[64];  // cycles per sweep of matrix 0 (DMCG_DEBUG)
 
 __global__ void __launch_bounds__(kJacThreads)
     k_jacobi(int m, const double* __restrict__ Aall, double* work, double* Vall, double* wall,
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kJacThreads)
   }
   bool converged = (m2 <= 1);
   for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
+    const long long sw_t0 = clock64();
     int any = 0;
     for (int s = 0; s + 1 < m2; ++s) {
       int on = 0;
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(kJacThreads)
       converged = !__syncthreads_or(hot);
     }
     if (threadIdx.x == 0 && sp == 0 && b < 8) g_jacobi_sweeps[b] = sweep + 1;
+    if (threadIdx.x == 0 && sp == 0 && b == 0 && sweep < 64) g_jacobi_cyc[sweep] = clock64() - sw_t0;
   }
   double* Vo = Vall + (size_t)b * m * m;
   for (int c = 0; c < m; ++c)
@@ -476,27 +479,42 @@ __device__ __noinline__ void warp_panel_qr(P Z, int m, int ld, int c0, int pb, d
   double tv[PW];
 #pragma unroll
   for (int j = 0; j < PW; ++j) {
-    // columns j >= pb are zero: their reflector is the identity (tail 0,
-    // tau 0), so no branch on pb is needed around the shuffles below
-    double p0 = 0.0, p1 = 0.0;
+    // Columns j >= pb are zero: their reflector is the identity (tail 0,
+    // tau 0), so no branch on pb is needed around the shuffles below.
+    // One reduction round per column: the norm of the tail of column j and
+    // the raw products x^T y_l with the later columns are summed together;
+    // v = x / (x0 - beta) only rescales them (d_l = tau (y_l[j] + rinv x^T y_l)).
+    double r[PW + 1];
+#pragma unroll
+    for (int l = 0; l <= PW; ++l) r[l] = 0.0;
 #pragma unroll
     for (int t = 0; t < MAXR; ++t) {
       const int g = lane + 32 * t;
       const double x = g > j ? a[t][j] : 0.0;
-      if (t & 1)
-        p1 = fma(x, x, p1);
-      else
-        p0 = fma(x, x, p0);
+      r[PW] = fma(x, x, r[PW]);
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l > j) r[l] = fma(x, a[t][l], r[l]);
     }
-    const double tail = warp_sum(p0 + p1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r[PW] += __shfl_xor_sync(FULL, r[PW], o);
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l > j) r[l] += __shfl_xor_sync(FULL, r[l], o);
+    }
+    const double tail = r[PW];
     const double x0 = __shfl_sync(FULL, a[0][j], j);
+    double yj[PW];
+#pragma unroll
+    for (int l = 0; l < PW; ++l) yj[l] = l > j ? __shfl_sync(FULL, a[0][l], j) : 0.0;
     double rinv = 0.0, tj = 0.0, beta = x0;
     if (tail > DBL_MIN) {
       const double s2 = x0 * x0 + tail;
-      const double r = rsqrt(s2);
-      const double nrm = s2 * r;
+      const double rs = rsqrt(s2);
+      const double nrm = s2 * rs;
       beta = x0 >= 0.0 ? -nrm : nrm;
-      const double ibb = x0 >= 0.0 ? -r : r;
+      const double ibb = x0 >= 0.0 ? -rs : rs;
       rinv = __drcp_rn(x0 - beta);
       tj = (beta - x0) * ibb;
     }
@@ -507,35 +525,17 @@ __device__ __noinline__ void warp_panel_qr(P Z, int m, int ld, int c0, int pb, d
     }
     if (lane == j) a[0][j] = beta;
     tv[j] = tj;
-    // H_j applied to the panel columns l > j: d_l = y_l[j] + v^T y_l (rows > j)
-    double d[PW];
-#pragma unroll
-    for (int l = 0; l < PW; ++l) {
-      d[l] = 0.0;
-      if (l > j) {
-#pragma unroll
-        for (int t = 0; t < MAXR; ++t) {
-          const int g = lane + 32 * t;
-          if (g > j) d[l] = fma(a[t][j], a[t][l], d[l]);
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int l = 0; l < PW; ++l)
-        if (l > j) d[l] += __shfl_xor_sync(FULL, d[l], o);
+    // H_j applied to the panel columns l > j
 #pragma unroll
     for (int l = 0; l < PW; ++l) {
       if (l <= j) continue;
-      const double yj = __shfl_sync(FULL, a[0][l], j);
-      const double s = tj * (yj + d[l]);
+      const double sl = tj * fma(rinv, r[l], yj[l]);
 #pragma unroll
       for (int t = 0; t < MAXR; ++t) {
         const int g = lane + 32 * t;
-        if (g > j) a[t][l] = fma(-s, a[t][j], a[t][l]);
+        if (g > j) a[t][l] = fma(-sl, a[t][j], a[t][l]);
       }
-      if (lane == j) a[0][l] -= s;
+      if (lane == j) a[0][l] -= sl;
     }
   }
   PANEL_STAMP(2);
@@ -1115,6 +1115,9 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
       cudaStreamSynchronize(s);
       cudaMemcpyFromSymbol(sw, g_jacobi_sweeps, sizeof(sw));
       fprintf(stderr, "dmcg: k_jacobi m=%d split %d sweeps %d %d %d\n", m, nsplit, sw[0], sw[1], sw[2]);
+      long long cy[64];
+      cudaMemcpyFromSymbol(cy, g_jacobi_cyc, sizeof(cy));
+      for (int i = 0; i < sw[0] && i < 64; ++i) fprintf(stderr, "  sweep %d: %lld cycles\n", i, cy[i]);
     }
   } else {
     k_jacobi<<<dim3(nbatch, 1), kJacThreads, 0, s>>>(m, A, work, V, w, flags, 0, m2);
