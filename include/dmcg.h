@@ -229,6 +229,13 @@ void* dmcg_plan_stream(dmcg_plan* plan);
  * dmcg_serialize of dmcg_plan_download's result.  out == NULL queries the
  * size.  Returns the stream size, 0 on error (cap too small / CUDA). */
 size_t dmcg_plan_serialize(dmcg_plan* plan, uint8_t* out, size_t cap, dmcg_sections* s);
+/* distortion_report (src/metrics.cpp:67-129) on the device for
+ * two device-resident sequences of the plan's shape and dtype: per-frame RMS
+ * vertex error (frame_rms) and NMSVE with the normalised Laplacian into host
+ * arrays of F doubles, and the per-vertex mean error into n doubles
+ * (vertex_mean_error may be NULL). */
+int dmcg_plan_distortion(dmcg_plan* plan, const void* const d_orig[3], const void* const d_recon[3],
+                         double* frame_rms, double* nmsve, double* vertex_mean_error);
 
 /* ---- diagnostics (host only, no GPU) ----------------------------------
  * Symbolic analysis of the anchored normal matrix of a mesh and, when W > 0,

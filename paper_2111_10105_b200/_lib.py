@@ -33,7 +33,7 @@ EXPORTS = [
     "dmcg_anchor_count", "dmcg_select_anchors", "dmcg_plan_create", "dmcg_plan_destroy",
     "dmcg_plan_encode_device", "dmcg_plan_decode_device", "dmcg_plan_download", "dmcg_plan_upload",
     "dmcg_plan_basis", "dmcg_plan_stats", "dmcg_ctx_stats", "dmcg_plan_stream", "dmcg_debug_chol",
-    "dmcg_plan_serialize",
+    "dmcg_plan_serialize", "dmcg_plan_distortion",
 ]
 
 
@@ -150,5 +150,6 @@ def lib():
     L.dmcg_plan_stream.restype = vp
     L.dmcg_plan_serialize.restype = ctypes.c_size_t
     L.dmcg_plan_serialize.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.POINTER(DmcgSections)]
+    L.dmcg_plan_distortion.argtypes = [vp, vp * 3, vp * 3, f64p, f64p, f64p]
     _lib = L
     return L

@@ -290,6 +290,19 @@ class Plan:
     def stream(self) -> int:
         return L.lib().dmcg_plan_stream(self._p) or 0
 
+    def distortion(self, d_orig, d_recon, vertex_errors=False):
+        """distortion_report (src/metrics.cpp:67-129) on the GPU for two device
+        sequences of this plan's shape: (frame_rms[F], nmsve[F], vertex_mean_error[n] or None)."""
+        rms = np.zeros(self.F)
+        nm = np.zeros(self.F)
+        vme = np.zeros(self.n) if vertex_errors else None
+        a = (ctypes.c_void_p * 3)(*[int(p) for p in d_orig])
+        b = (ctypes.c_void_p * 3)(*[int(p) for p in d_recon])
+        _check(self.codec.handle, L.lib().dmcg_plan_distortion(
+            self._p, a, b, rms.ctypes.data_as(L.f64p), nm.ctypes.data_as(L.f64p),
+            vme.ctypes.data_as(L.f64p) if vme is not None else None))
+        return rms, nm, vme
+
     def serialize(self):
         """DMC1 bytes of the device-resident symbols, payload bit-packed on the
         GPU (dmcg_plan_serialize): (bytes, SectionSizes dict), identical to

@@ -348,3 +348,92 @@ cudaError_t launch_output(cudaStream_t s, int n, int F, const double* X, void* c
 }
 
 }  // namespace dmcg
+
+// ---- f3: distortion metrics on the device (src/metrics.cpp:67-129) --------
+namespace dmcg {
+namespace {
+
+template <typename T>
+__global__ void k_distortion_terms(int n, int F, const uint32_t* __restrict__ lap_rp,
+                                   const uint32_t* __restrict__ lap_ci, const T* __restrict__ a0,
+                                   const T* __restrict__ a1, const T* __restrict__ a2,
+                                   const T* __restrict__ b0, const T* __restrict__ b1,
+                                   const T* __restrict__ b2, double* err2, double* enorm,
+                                   double* gnorm) {
+  // per (vertex i, frame f): |d|^2, |d|, |(L_norm d)_i| with d = orig - recon
+  // and L_norm = I - D^{-1} A (LaplacianKind::Normalized, laplacian.cpp:21-37)
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)n * F) return;
+  const int i = (int)(t / F), f = (int)(t % F);
+  const size_t o = (size_t)i * F + f;
+  const double d0 = (double)a0[o] - (double)b0[o], d1 = (double)a1[o] - (double)b1[o],
+               d2 = (double)a2[o] - (double)b2[o];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  const uint32_t p0 = lap_rp[i], p1 = lap_rp[i + 1];
+  for (uint32_t p = p0; p < p1; ++p) {
+    const uint32_t j = lap_ci[p];
+    if ((int)j == i) continue;
+    const size_t oj = (size_t)j * F + f;
+    s0 += (double)a0[oj] - (double)b0[oj];
+    s1 += (double)a1[oj] - (double)b1[oj];
+    s2 += (double)a2[oj] - (double)b2[oj];
+  }
+  const double inv = 1.0 / (double)(p1 - p0 - 1);
+  const double g0 = d0 - inv * s0, g1 = d1 - inv * s1, g2 = d2 - inv * s2;
+  const double q = d0 * d0 + d1 * d1 + d2 * d2;
+  err2[o] = q;
+  enorm[o] = sqrt(q);
+  gnorm[o] = sqrt(g0 * g0 + g1 * g1 + g2 * g2);
+}
+
+// column sums over the vertices (thread = frame, ascending i: deterministic)
+__global__ void k_frame_sums(int n, int F, const double* __restrict__ err2,
+                             const double* __restrict__ enorm, const double* __restrict__ gnorm,
+                             double* rms, double* nmsve) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= F) return;
+  double s2 = 0.0, se = 0.0, sg = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const size_t o = (size_t)i * F + f;
+    s2 += err2[o];
+    se += enorm[o];
+    sg += gnorm[o];
+  }
+  rms[f] = sqrt(s2 / n);
+  nmsve[f] = (se + sg) / (2.0 * n);
+}
+
+// vertex_mean_error(i) = mean over frames of |d|
+__global__ void k_vertex_means(int n, int F, const double* __restrict__ enorm, double* vme) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int f = 0; f < F; ++f) s += enorm[(size_t)i * F + f];
+  vme[i] = s / F;
+}
+
+}  // namespace
+
+cudaError_t launch_distortion(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
+                              const uint32_t* lap_ci, const void* const a[3],
+                              const void* const b[3], bool f32, double* work, double* rms,
+                              double* nmsve, double* vme) {
+  const long tot = (long)n * F;
+  double* err2 = work;
+  double* en = work + tot;
+  double* gn = work + 2 * tot;
+  const unsigned g = (unsigned)((tot + 255) / 256);
+  if (f32)
+    k_distortion_terms<float><<<g, 256, 0, s>>>(
+        n, F, lap_rp, lap_ci, (const float*)a[0], (const float*)a[1], (const float*)a[2],
+        (const float*)b[0], (const float*)b[1], (const float*)b[2], err2, en, gn);
+  else
+    k_distortion_terms<double><<<g, 256, 0, s>>>(
+        n, F, lap_rp, lap_ci, (const double*)a[0], (const double*)a[1], (const double*)a[2],
+        (const double*)b[0], (const double*)b[1], (const double*)b[2], err2, en, gn);
+  k_frame_sums<<<(F + 127) / 128, 128, 0, s>>>(n, F, err2, en, gn, rms, nmsve);
+  if (vme) k_vertex_means<<<(n + 255) / 256, 256, 0, s>>>(n, F, en, vme);
+  return cudaGetLastError();
+}
+
+}  // namespace dmcg

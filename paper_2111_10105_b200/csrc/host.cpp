@@ -772,6 +772,30 @@ extern "C" {
 static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_sections* sec,
                                   size_t* size);
 
+int dmcg_plan_distortion(dmcg_plan* p, const void* const d_orig[3], const void* const d_recon[3],
+                         double* frame_rms, double* nmsve, double* vertex_mean_error) {
+  if (!p || !d_orig || !d_recon || !frame_rms || !nmsve) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  const size_t n = p->n, F = p->F;
+  if (!p->d_metric) p->d_metric = (double*)plan_alloc(p, (3 * n * F + 2 * F + n) * 8);
+  if (!p->d_metric) return p->ctx->set_error({DMCG_E_CUDA, "CudaError: device allocation failed"});
+  cudaStream_t s = p->ctx->stream;
+  double* rms = p->d_metric + 3 * n * F;
+  double* nm = rms + F;
+  double* vme = nm + F;
+  cudaError_t e = launch_distortion(s, (int)n, (int)F, p->d_lap_rp, p->d_lap_ci, d_orig, d_recon,
+                                    p->dtype == DMCG_F32, p->d_metric, rms, nm,
+                                    vertex_mean_error ? vme : nullptr);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(frame_rms, rms, F * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(nmsve, nm, F * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && vertex_mean_error)
+    e = cudaMemcpyAsync(vertex_mean_error, vme, n * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess)
+    return p->ctx->set_error({DMCG_E_CUDA, std::string("CudaError: ") + cudaGetErrorString(e)});
+  return DMCG_OK;
+}
+
 size_t dmcg_plan_serialize(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_sections* sec) {
   if (!p) return 0;
   cudaSetDevice(p->ctx->device);

@@ -168,6 +168,7 @@ struct dmcg_plan {
   // decode
   double* d_rowp = nullptr;        // 3 x k x 2 (min_, width) dequantiser params
   uint32_t* d_stream = nullptr;    // device DMC1 image for dmcg_plan_serialize
+  double* d_metric = nullptr;      // 3 n F + F + F + n doubles (dmcg_plan_distortion)
   size_t stream_cap = 0;
   unsigned long long* d_row_bitoff = nullptr;  // 3 x k payload bit offsets
   double *d_cg_x = nullptr, *d_cg_r = nullptr, *d_cg_p = nullptr, *d_cg_q = nullptr;

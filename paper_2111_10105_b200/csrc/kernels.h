@@ -79,6 +79,13 @@ cudaError_t launch_cg(cudaStream_t s, int n, int W, int nblk, const uint32_t* m_
                       double* Q, double rtol, int maxit, int* iters, double* res);
 cudaError_t launch_output(cudaStream_t s, int n, int F, const double* X, void* const out[3],
                           bool f32);
+// distortion_report terms (metrics.cpp:67-129) of orig a vs recon b (3 axes,
+// vertex-major n x F, f32 or f64): per-frame RMS and NMSVE (normalised
+// Laplacian), per-vertex mean error (vme may be null).  work: 3 n F doubles.
+cudaError_t launch_distortion(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
+                              const uint32_t* lap_ci, const void* const a[3],
+                              const void* const b[3], bool f32, double* work, double* rms,
+                              double* nmsve, double* vme);
 // Row-major (n x 3F) variants used by the direct solver.
 cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
                           const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
