@@ -360,7 +360,8 @@ int dmcg_create(dmcg_ctx** out, int device) {
   if (cudaSetDevice(device) != cudaSuccess) return DMCG_E_CUDA;
   auto* c = new dmcg_ctx();
   c->device = device;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return DMCG_E_CUDA;
   }
@@ -374,6 +375,8 @@ void dmcg_destroy(dmcg_ctx* c) {
   c->pending.reset();
   cudaStreamSynchronize(c->stream);
   c->pool.release_all();
+  cudaStreamSynchronize(c->aux);
+  cudaStreamDestroy(c->aux);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -479,6 +482,8 @@ void dmcg_plan_destroy(dmcg_plan* p) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
   for (auto& kv : p->owned) p->ctx->pool.put(kv.first, kv.second);
   for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : {p->ev_fork, p->ev_join})
     if (e) cudaEventDestroy(e);
   delete p;
 }
@@ -587,6 +592,8 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   }
   tm.lap("alloc");
   for (auto& e : p->ev) cudaEventCreate(&e);
+  cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
   cudaStream_t s = ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;

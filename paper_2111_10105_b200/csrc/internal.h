@@ -104,6 +104,7 @@ struct dmcg_ctx {
   int device = 0;
   std::unique_ptr<dmcg::PendingAnalysis> pending;  // see PendingAnalysis
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // fork/join side stream (independent encode / decode phases)
   std::string err;
   dmcg::DevicePool pool;
   dmcg_stats last_stats = {};  // stats of the last drop-in encode / decode
@@ -189,5 +190,7 @@ struct dmcg_plan {
   dmcg::PlanGraph g_encode, g_decode;
 
   cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // ctx->stream <-> ctx->aux
+  bool forked = false;
   dmcg_stats stats = {};
 };

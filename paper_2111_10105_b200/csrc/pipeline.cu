@@ -184,11 +184,18 @@ Status basis(dmcg_plan* p) {
   LoadDense<double, true> lW{Ws, (long)k * k, 1L, (long)k};
   DMCG_TRY(launch_gemm(s, 3, F, k, k, 1, lQm, lW, StoreStrided{p->d_U, FF, 1L, (long)F}));
   DMCG_TRY(launch_canon_signs(s, 3, F, 0, k, p->d_U, FF));
-  // Completion to F x F: columns k..F-1 of the full Householder Q of U_k.
-  DMCG_TRY(launch_complete(s, 3, F, k, p->d_U, p->d_H, p->d_qr_scr));
-  DMCG_TRY(launch_canon_signs(s, 3, F, k, F - k, p->d_U, FF));
+  // Completion to F x F: columns k..F-1 of the full Householder Q of U_k, on
+  // the side stream (it only feeds the dictionary levels; the projection
+  // needs U_k alone).  enqueue_encode joins before quant_dict.
+  cudaStream_t s2 = p->ctx->aux;
+  DMCG_TRY(cudaEventRecord(p->ev_fork, s));
+  DMCG_TRY(cudaStreamWaitEvent(s2, p->ev_fork, 0));
+  DMCG_TRY(launch_complete(s2, 3, F, k, p->d_U, p->d_H, p->d_qr_scr));
+  DMCG_TRY(launch_canon_signs(s2, 3, F, k, F - k, p->d_U, FF));
   for (int a = 0; a < 3; ++a)
-    DMCG_TRY(launch_fill_zero(s, p->d_evals + (long)a * F + k, F - k));
+    DMCG_TRY(launch_fill_zero(s2, p->d_evals + (long)a * F + k, F - k));
+  DMCG_TRY(cudaEventRecord(p->ev_join, s2));
+  p->forked = true;
   return Status::ok();
 }
 
@@ -211,11 +218,10 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   if (!st.good()) return st;
   DMCG_TRY(record_event(p->ev[2], s));
   // K3 basis.
+  p->forked = false;
   st = basis(p);
   if (!st.good()) return st;
   DMCG_TRY(record_event(p->ev[3], s));
-  // K5a dictionary levels (encode_dictionaries first block).
-  DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
   // K4 projection coeffs = U_k^T delta^T (codec.cpp:420) + row min/max, then
   // quantize_rows (codec.cpp:426).
   if (k > 0) {
@@ -230,6 +236,10 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   // K5b anchors (codec.cpp:444-471).
   DMCG_TRY(launch_anchors(s, (int)p->n_c, F, p->d_anchor_idx, x, f32, p->anchor_bits,
                           p->d_anchor_rng, p->d_anchor_q));
+  // K5a dictionary levels (encode_dictionaries first block), after the
+  // completion joined back from the side stream.
+  if (p->forked) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
+  DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
   DMCG_TRY(record_event(p->ev[5], s));
   return Status::ok();
 }
@@ -332,6 +342,13 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
   DMCG_TRY(record_event(p->ev[0], s));
   const size_t nW = (size_t)n * W;
+  // The right-hand sides (dequantise + reconstruct + L^T delta~ + S^T a) do
+  // not depend on the factor of M: they run on the side stream while the
+  // main stream factors, and join before the solves.
+  cudaStream_t s1 = s;
+  s = p->ctx->aux;
+  DMCG_TRY(cudaEventRecord(p->ev_fork, s1));
+  DMCG_TRY(cudaStreamWaitEvent(s, p->ev_fork, 0));
   if (k > 0) {
     DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
     LoadCoeffDeq la{p->d_coeff_q, p->d_rowp, p->d_row_bits, p->d_flags + 1, n, k};
@@ -347,8 +364,12 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
                          p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_rm_delta, p->d_rm_b,
                          p->d_flags + 1));
   DMCG_TRY(record_event(p->ev[1], s));
+  DMCG_TRY(cudaEventRecord(p->ev_join, s));
+  s = s1;
   if (factor) DMCG_TRY(chol_factor_device(s, p->cdev, p->levels));
   DMCG_TRY(record_event(p->ev[2], s));
+  DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
+  DMCG_TRY(record_event(p->ev[5], s));
   DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
   DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, false));
   for (int r = 0; r < refine; ++r) {
@@ -379,9 +400,10 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
   DMCG_TRY(cudaStreamSynchronize(s));
   cudaEventElapsedTime(&p->stats.ms_decode, p->ev[0], p->ev[4]);
+  // reconstruct (side stream) and factor (main stream) both start at ev0
   cudaEventElapsedTime(&p->stats.ms_reconstruct, p->ev[0], p->ev[1]);
-  cudaEventElapsedTime(&p->stats.ms_factor, p->ev[1], p->ev[2]);
-  cudaEventElapsedTime(&p->stats.ms_solve, p->ev[2], p->ev[3]);
+  cudaEventElapsedTime(&p->stats.ms_factor, p->ev[0], p->ev[2]);
+  cudaEventElapsedTime(&p->stats.ms_solve, p->ev[5], p->ev[3]);
   p->stats.ms_cg = 0.0f;
   p->stats.solver = 0;
   p->stats.cg_iterations_max = 0;
