@@ -212,7 +212,7 @@ def main():
     value = whole_job_rate(vf_step, world, args.steps, total_ms)
 
     # roofline of the dominant kernel, k_oi_fused (the fused orthogonal
-    # iterations, one CTA per axis): algorithmic flops per launch
+    # iterations, one 8-CTA cluster per axis): algorithmic flops per launch
     # over its launch time, CUDA events around the launch on
     # the plan stream (stats.ms_oi), median over the timed steps.  The
     # decode's direct solve (K7) is reported beside it.
@@ -266,12 +266,14 @@ def main():
             "roofline": {"kernel": "k_oi_fused", "bound": "tensor", "achieved": achieved,
                          "peak": peak, "peak_kind": "measured FP64 DMMA, whole GPU (profiles/r01_peaks.md)",
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": OI_TRAFFIC,
-                         "launches_per_step": 1, "ctas": 3,
+                         "launches_per_step": 1, "ctas": 24, "cluster": 8,
                          "algorithmic_flops": oi_flops, "ms": oi_sec * 1e3,
                          "share_of_step": oi_sec * 1e3 / (total_ms / args.steps),
                          "model": "3 axes x ((rounds+1) x (2F^2k + 4Fk^2 - 4k^3/3) + 2Fk^2)",
-                         "note": "one CTA per axis (each round depends on the last): the ceiling "
-                                 "is 3/148 of the device peak; see DESIGN.md §5"},
+                         "note": "one 8-CTA cluster per axis; each round's Householder QR is "
+                                 "sequential on the cluster's rank 0 (the other 7 CTAs compute "
+                                 "Z = R Q), so the ceiling is a few SMs' DMMA rate, not the "
+                                 "device peak; see DESIGN.md §5"},
             "roofline_k7": {"kernel": "K7 direct solve (k_panel/k_trailing/k_inv_*/k_fwd*/k_bwd*)",
                             "bound": "tensor", "achieved": k7_achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": k7_achieved / peak, "algorithmic_flops": k7_flops,
