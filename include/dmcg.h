@@ -105,6 +105,13 @@ typedef struct {
                                the mesh and anchors alone, both fixed by the plan) and
                                skip refactoring on later decodes (default 0: factor
                                on every decode, like the reference) */
+  uint32_t frame_begin;     /* direct solver: decode frames [frame_begin, frame_begin +
+                               frame_count) only and write just those columns of the
+                               output (frame_count 0 = all frames).  The solve is
+                               column-separable, so a window gives the same bits as the
+                               full decode; the multi-GPU decoder splits frames across
+                               ranks this way. */
+  uint32_t frame_count;
 } dmcg_decode_options;
 
 void dmcg_decode_options_default(dmcg_decode_options* opt);
@@ -236,6 +243,59 @@ size_t dmcg_plan_serialize(dmcg_plan* plan, uint8_t* out, size_t cap, dmcg_secti
  * (vertex_mean_error may be NULL). */
 int dmcg_plan_distortion(dmcg_plan* plan, const void* const d_orig[3], const void* const d_recon[3],
                          double* frame_rms, double* nmsve, double* vertex_mean_error);
+
+/* ---- multi-GPU: vertex-row shards of one sequence ----------
+ * The reference is single-threaded with no parallel path; these entry points
+ * are the B200 addition for sequences too large for one GPU (BASELINE
+ * config 3).  One process per GPU.  Rank q of N owns vertex rows
+ * [q n / N, (q+1) n / N); its local input (n_loc x F per axis, the plan dtype)
+ * holds the owned rows followed by the halo rows listed by
+ * dmcg_shard_info_get.  Encode collectives: allreduce(sum) of the Gram
+ * partials, allreduce(max) of the row / anchor range keys, and an
+ * all-gather of every rank's symbols, after which each rank holds the full
+ * encoded stream (dmcg_plan_download / dmcg_plan_serialize work as usual).
+ * Decode splits frames across ranks with dmcg_decode_options.frame_begin /
+ * frame_count (no exchange).  Results equal a single-GPU encode up to the
+ * summation order of the Gram. */
+typedef struct dmcg_comm dmcg_comm;
+/* ncclGetUniqueId on one rank; share the 128 bytes with the others. */
+int dmcg_comm_unique_id(uint8_t id[128]);
+/* ncclCommInitRank (NCCL is dlopen'ed; DMCG_E_UNSUPPORTED if absent). */
+int dmcg_comm_create(int device, const uint8_t id[128], int nranks, int rank, dmcg_comm** out);
+void dmcg_comm_destroy(dmcg_comm* comm);
+
+typedef struct {
+  int nranks, rank;
+  uint32_t row_begin, row_end;      /* owned vertex rows */
+  uint32_t n_own, n_halo, n_loc;    /* local input rows = n_own + n_halo */
+  uint32_t anchor_begin, anchor_end;/* owned anchor slots */
+  uint64_t stage_begin, stage_count;/* this rank's symbols in the gather buffer (u16) */
+  uint64_t gather_count;            /* gather buffer length (u16) */
+} dmcg_shard_info;
+
+/* Host only (no GPU): the layout rank `rank` of `nranks` would use.  halo
+ * (n_halo entries, may be NULL) receives the global ids of the halo rows in
+ * local-row order. */
+int dmcg_shard_layout(uint32_t n, uint32_t F, const uint32_t* faces, uint32_t n_faces,
+                      const dmcg_config* cfg, int nranks, int rank, dmcg_shard_info* info,
+                      uint32_t* halo);
+/* A plan for rank `rank` of `nranks`; comm may be NULL (phase-by-phase use). */
+int dmcg_plan_create_shard(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uint32_t* faces,
+                           uint32_t n_faces, const dmcg_config* cfg, int nranks, int rank,
+                           dmcg_comm* comm, dmcg_plan** plan);
+int dmcg_shard_info_get(const dmcg_plan* plan, dmcg_shard_info* info, uint32_t* halo);
+/* Whole sharded encode on the plan stream, collectives included. */
+int dmcg_shard_encode_device(dmcg_plan* plan, const void* const d_loc_axes[3]);
+/* The same encode one phase at a time, for callers that run the
+ * collectives themselves: phase 0 (delta + Gram partial) -> sum-reduce
+ * DMCG_SHARD_GRAM; phase 1 (basis + projection + range keys) -> max-reduce
+ * DMCG_SHARD_KEYS; phase 2 (quantise own rows / anchors into the gather
+ * buffer at stage_begin) -> all-gather DMCG_SHARD_SYMBOLS; phase 3 (unpack
+ * the gathered symbols into the plan's encoded arrays). */
+int dmcg_shard_encode_phase(dmcg_plan* plan, int phase, const void* const d_loc_axes[3]);
+enum { DMCG_SHARD_GRAM = 0, DMCG_SHARD_KEYS = 1, DMCG_SHARD_SYMBOLS = 2 };
+/* Device pointer and element count of a collective buffer (f64 / u64 / u16). */
+int dmcg_shard_buffer(dmcg_plan* plan, int which, void** dptr, size_t* count);
 
 /* ---- diagnostics (host only, no GPU) ----------------------------------
  * Symbolic analysis of the anchored normal matrix of a mesh and, when W > 0,

@@ -49,7 +49,17 @@ class DmcgConfig(ctypes.Structure):
 
 class DmcgDecodeOptions(ctypes.Structure):
     _fields_ = [("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int),
-                ("solver", ctypes.c_int), ("refine", ctypes.c_int), ("reuse_factor", ctypes.c_int)]
+                ("solver", ctypes.c_int), ("refine", ctypes.c_int), ("reuse_factor", ctypes.c_int),
+                ("frame_begin", ctypes.c_uint32), ("frame_count", ctypes.c_uint32)]
+
+
+class DmcgShardInfo(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int), ("rank", ctypes.c_int),
+                ("row_begin", ctypes.c_uint32), ("row_end", ctypes.c_uint32),
+                ("n_own", ctypes.c_uint32), ("n_halo", ctypes.c_uint32), ("n_loc", ctypes.c_uint32),
+                ("anchor_begin", ctypes.c_uint32), ("anchor_end", ctypes.c_uint32),
+                ("stage_begin", ctypes.c_uint64), ("stage_count", ctypes.c_uint64),
+                ("gather_count", ctypes.c_uint64)]
 
 
 class DmcgSeq(ctypes.Structure):
@@ -151,5 +161,21 @@ def lib():
     L.dmcg_plan_serialize.restype = ctypes.c_size_t
     L.dmcg_plan_serialize.argtypes = [vp, u8p, ctypes.c_size_t, ctypes.POINTER(DmcgSections)]
     L.dmcg_plan_distortion.argtypes = [vp, vp * 3, vp * 3, f64p, f64p, f64p]
+    # multi-GPU vertex-row shards
+    L.dmcg_comm_unique_id.argtypes = [u8p]
+    L.dmcg_comm_create.argtypes = [ctypes.c_int, u8p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    L.dmcg_comm_destroy.argtypes = [vp]
+    L.dmcg_comm_destroy.restype = None
+    L.dmcg_shard_layout.argtypes = [ctypes.c_uint32, ctypes.c_uint32, u32p, ctypes.c_uint32,
+                                    ctypes.POINTER(DmcgConfig), ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(DmcgShardInfo), u32p]
+    L.dmcg_plan_create_shard.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int, u32p,
+                                         ctypes.c_uint32, ctypes.POINTER(DmcgConfig), ctypes.c_int,
+                                         ctypes.c_int, vp, ctypes.POINTER(vp)]
+    L.dmcg_shard_info_get.argtypes = [vp, ctypes.POINTER(DmcgShardInfo), u32p]
+    L.dmcg_shard_encode_device.argtypes = [vp, vp * 3]
+    L.dmcg_shard_encode_phase.argtypes = [vp, ctypes.c_int, vp * 3]
+    L.dmcg_shard_buffer.argtypes = [vp, ctypes.c_int, ctypes.POINTER(vp),
+                                    ctypes.POINTER(ctypes.c_size_t)]
     _lib = L
     return L

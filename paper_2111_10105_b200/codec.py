@@ -129,11 +129,12 @@ class CompressedAnimation:
         self.anchor_max = [float(e.anchor_max[a]) for a in range(3)]
 
 
-def _decode_opts(rtol, max_iter, solver, refine, reuse_factor=False):
+def _decode_opts(rtol, max_iter, solver, refine, reuse_factor=False, frames=None):
     if solver not in ("direct", "cg"):
         raise ValueError(f"solver must be 'direct' or 'cg', not {solver!r}")
+    f0, fc = (0, 0) if frames is None else (int(frames[0]), int(frames[1]) - int(frames[0]))
     return L.DmcgDecodeOptions(rtol, max_iter, 0 if solver == "direct" else 1, refine,
-                               1 if reuse_factor else 0)
+                               1 if reuse_factor else 0, f0, fc)
 
 
 def _check(ctx, rc):
@@ -196,11 +197,12 @@ class Codec:
         return out
 
     def decode(self, c: CompressedAnimation, rtol: float = 1e-10, max_iter: int = 20000,
-               dtype=np.float64, solver: str = "direct", refine: int = 1, out=None):
+               dtype=np.float64, solver: str = "direct", refine: int = 1, out=None, frames=None):
         """dmc::decode (include/dmc/codec.hpp:91; src/codec.cpp:475-552).
         Returns the three (n, F) axis arrays.  solver "direct" (supernodal
-        Cholesky + refine passes, the reference scheme) or "cg"."""
-        opt = _decode_opts(rtol, max_iter, solver, refine)
+        Cholesky + refine passes, the reference scheme) or "cg".  frames=(f0, f1)
+        decodes only those frames (other columns of `out` are left untouched)."""
+        opt = _decode_opts(rtol, max_iter, solver, refine, frames=frames)
         if out is None:
             out = [np.empty((c.n, c.F), dtype=dtype) for _ in range(3)]
         else:  # caller-provided (e.g. pinned) host buffers
@@ -254,10 +256,12 @@ class Plan:
         _check(self.codec.handle, L.lib().dmcg_plan_encode_device(self._p, ptrs))
 
     def decode_device(self, d_out, rtol=1e-10, max_iter=20000, solver="direct", refine=1,
-                      reuse_factor=False):
+                      reuse_factor=False, frames=None):
         """reuse_factor: keep the plan's numeric factor of M across decodes (many
-        sequences on one mesh); off by default (the reference factors every call)."""
-        opt = _decode_opts(rtol, max_iter, solver, refine, reuse_factor)
+        sequences on one mesh); off by default (the reference factors every call).
+        frames=(f0, f1): decode only frames f0..f1-1 (direct solver; writes only
+        those columns of d_out) -- the multi-GPU decoder's frame split."""
+        opt = _decode_opts(rtol, max_iter, solver, refine, reuse_factor, frames)
         ptrs = (ctypes.c_void_p * 3)(*[int(p) for p in d_out])
         _check(self.codec.handle, L.lib().dmcg_plan_decode_device(self._p, ctypes.byref(opt), ptrs))
 

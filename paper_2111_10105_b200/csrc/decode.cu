@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kCgThreads)
 
 // Row-major variants for the direct solver: vectors are n x W, row i =
 // [x frames | y frames | z frames] of vertex i.
-__global__ void k_rhs_rm(int n, int F, int W, const uint32_t* __restrict__ rp,
+__global__ void k_rhs_rm(int n, int F, int W, int F_all, int f_off, const uint32_t* __restrict__ rp,
                          const uint32_t* __restrict__ ci, const int32_t* __restrict__ apos, int n_c,
                          const uint16_t* __restrict__ aq, const float* __restrict__ arng, int abits,
                          const double* __restrict__ D, double* __restrict__ B, int* flags) {
@@ -251,7 +251,7 @@ __global__ void k_rhs_rm(int n, int F, int W, const uint32_t* __restrict__ rp,
   if (slot >= 0) {
     const int a = c / F, f = c % F;
     const QParams q = make_qparams(arng[2 * a], arng[2 * a + 1], abits);
-    const uint32_t lv = aq[((size_t)a * n_c + slot) * F + f];
+    const uint32_t lv = aq[((size_t)a * n_c + slot) * F_all + f_off + f];
     if (lv >= q.levels) atomicOr(flags, 1);
     acc = __dadd_rn(acc, dequantize_level(q.min_, q.width, q.degenerate, lv));
   }
@@ -259,7 +259,8 @@ __global__ void k_rhs_rm(int n, int F, int W, const uint32_t* __restrict__ rp,
 }
 
 template <typename T>
-__global__ void k_output_rm(int n, int F, const double* __restrict__ X, T* o0, T* o1, T* o2) {
+__global__ void k_output_rm(int n, int F, int F_all, int f_off, const double* __restrict__ X, T* o0,
+                            T* o1, T* o2) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   const long nF = (long)n * F;
   if (t >= 3 * nF) return;
@@ -267,7 +268,7 @@ __global__ void k_output_rm(int n, int F, const double* __restrict__ X, T* o0, T
   const long rem = t % nF;
   const int i = (int)(rem / F), f = (int)(rem % F);
   T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
-  o[rem] = (T)X[(size_t)i * 3 * F + (size_t)a * F + f];
+  o[(size_t)i * F_all + f_off + f] = (T)X[(size_t)i * 3 * F + (size_t)a * F + f];
 }
 
 template <typename T>
@@ -311,27 +312,28 @@ cudaError_t launch_cg(cudaStream_t s, int n, int W, int nblk, const uint32_t* m_
   return cudaGetLastError();
 }
 
-cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
-                          const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
-                          const uint16_t* anchor_q, const float* anchor_rng, int anchor_bits,
-                          const double* D, double* B, int* flags) {
+cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
+                          const uint32_t* lap_rp, const uint32_t* lap_ci, const int32_t* anchor_pos,
+                          int n_c, const uint16_t* anchor_q, const float* anchor_rng,
+                          int anchor_bits, const double* D, double* B, int* flags) {
   const long total = 3L * n * F;
-  k_rhs_rm<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, F, 3 * F, lap_rp, lap_ci, anchor_pos,
+  k_rhs_rm<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, F, 3 * F, F_all, f_off, lap_rp,
+                                                           lap_ci, anchor_pos,
                                                            n_c, anchor_q, anchor_rng, anchor_bits,
                                                            D, B, flags);
   return cudaGetLastError();
 }
 
-cudaError_t launch_output_rm(cudaStream_t s, int n, int F, const double* X, void* const out[3],
-                             bool f32) {
+cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
+                             void* const out[3], bool f32) {
   const long total = 3L * n * F;
   const unsigned grid = (unsigned)((total + 255) / 256);
   if (f32)
-    k_output_rm<float><<<grid, 256, 0, s>>>(n, F, X, (float*)out[0], (float*)out[1],
+    k_output_rm<float><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (float*)out[0], (float*)out[1],
                                             (float*)out[2]);
   else
-    k_output_rm<double><<<grid, 256, 0, s>>>(n, F, X, (double*)out[0], (double*)out[1],
-                                             (double*)out[2]);
+    k_output_rm<double><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (double*)out[0],
+                                             (double*)out[1], (double*)out[2]);
   return cudaGetLastError();
 }
 

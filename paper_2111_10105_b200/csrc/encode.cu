@@ -168,6 +168,67 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// ---- vertex-row shards: the anchor payload split in two ------
+// The global anchor range is a min/max over every anchor trajectory, so a
+// shard first reduces its own anchors into ordered keys (combined across
+// ranks by one MAX allreduce with the min half complemented), then quantises
+// its anchors with the global widened range.  min/max are exact, so the
+// levels equal the single-GPU k_anchors bits.
+template <typename T>
+__global__ void __launch_bounds__(1024)
+    k_anchor_keys(int na, int F, const uint32_t* __restrict__ rows, const T* __restrict__ x0,
+                  const T* __restrict__ x1, const T* __restrict__ x2,
+                  unsigned long long* keys) {
+  const int a = blockIdx.x;
+  const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
+  const long total = (long)na * F;
+  double lo = INFINITY, hi = -INFINITY;
+  for (long t = threadIdx.x; t < total; t += blockDim.x) {
+    const double v = (double)X[(size_t)rows[t / F] * F + t % F];
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0 && lo <= hi) {
+    atomicMin(&keys[2 * a], ordered_key(lo));
+    atomicMax(&keys[2 * a + 1], ordered_key(hi));
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+    k_anchor_quant(int na, int F, const uint32_t* __restrict__ rows, const T* __restrict__ x0,
+                   const T* __restrict__ x1, const T* __restrict__ x2, int bits,
+                   const unsigned long long* __restrict__ keys, float* rng,
+                   uint16_t* __restrict__ q) {
+  const int a = blockIdx.x;
+  const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
+  float flo, fhi;
+  widened_range(key_to_double(keys[2 * a]), key_to_double(keys[2 * a + 1]), &flo, &fhi);
+  if (threadIdx.x == 0) {
+    rng[2 * a] = flo;
+    rng[2 * a + 1] = fhi;
+  }
+  const QParams qp = make_qparams(flo, fhi, bits);
+  const long total = (long)na * F;
+  uint16_t* o = q + (size_t)a * total;
+  for (long t = threadIdx.x; t < total; t += blockDim.x) {
+    const double v = (double)X[(size_t)rows[t / F] * F + t % F];
+    o[t] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v);
+  }
+}
+
+// keys[2 r] <- ~keys[2 r]: turns the running-min half into a max-reducible key
+// (and back), so one NCCL MAX allreduce combines both halves.
+__global__ void k_flip_min_keys(long rows, unsigned long long* keys) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t < rows) keys[2 * t] = ~keys[2 * t];
+}
+
 }  // namespace
 
 cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
@@ -220,6 +281,37 @@ cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
   else
     k_anchors<double><<<3, 1024, 0, s>>>(n_c, F, idx, (const double*)x[0], (const double*)x[1],
                                          (const double*)x[2], bits, rng, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_anchor_keys(cudaStream_t s, int na, int F, const uint32_t* rows,
+                               const void* const x[3], bool f32, unsigned long long* keys) {
+  if (na <= 0) return cudaSuccess;
+  if (f32)
+    k_anchor_keys<float><<<3, 1024, 0, s>>>(na, F, rows, (const float*)x[0], (const float*)x[1],
+                                            (const float*)x[2], keys);
+  else
+    k_anchor_keys<double><<<3, 1024, 0, s>>>(na, F, rows, (const double*)x[0],
+                                             (const double*)x[1], (const double*)x[2], keys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_anchor_quant(cudaStream_t s, int na, int F, const uint32_t* rows,
+                                const void* const x[3], bool f32, int bits,
+                                const unsigned long long* keys, float* rng, uint16_t* q) {
+  if (f32)
+    k_anchor_quant<float><<<3, 1024, 0, s>>>(na, F, rows, (const float*)x[0], (const float*)x[1],
+                                             (const float*)x[2], bits, keys, rng, q);
+  else
+    k_anchor_quant<double><<<3, 1024, 0, s>>>(na, F, rows, (const double*)x[0],
+                                              (const double*)x[1], (const double*)x[2], bits, keys,
+                                              rng, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flip_min_keys(cudaStream_t s, long rows, unsigned long long* keys) {
+  if (rows <= 0) return cudaSuccess;
+  k_flip_min_keys<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(rows, keys);
   return cudaGetLastError();
 }
 

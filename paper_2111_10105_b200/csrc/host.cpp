@@ -407,6 +407,8 @@ void dmcg_decode_options_default(dmcg_decode_options* o) {
   o->solver = 0;
   o->refine = 1;
   o->reuse_factor = 0;
+  o->frame_begin = 0;
+  o->frame_count = 0;
 }
 
 uint32_t dmcg_anchor_count(uint32_t n, double fraction) {
@@ -821,6 +823,48 @@ int dmcg_plan_create(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uin
   return ctx->set_error(st);
 }
 
+int dmcg_plan_create_shard(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, const uint32_t* faces,
+                           uint32_t n_faces, const dmcg_config* cfg, int nranks, int rank,
+                           dmcg_comm* comm, dmcg_plan** plan) {
+  if (!ctx || !plan || !cfg || nranks < 1 || rank < 0 || rank >= nranks) return DMCG_E_CONFIG;
+  if (n < (uint32_t)nranks)
+    return ctx->set_error({DMCG_E_CONFIG, "ConfigError: fewer vertices than ranks"});
+  if (comm && (comm_size(comm) != nranks || comm_rank(comm) != rank))
+    return ctx->set_error({DMCG_E_CONFIG, "ConfigError: communicator does not match rank"});
+  cudaSetDevice(ctx->device);
+  Status st = plan_create_impl(ctx, n, F, dtype, faces, n_faces, cfg, nullptr, 0, plan);
+  if (!st.good()) return ctx->set_error(st);
+  dmcg_plan* p = *plan;
+  p->use_graphs = true;  // decode graphs; the sharded encode launches directly
+  p->shard.reset(new ShardState());
+  ShardState& sh = *p->shard;
+  shard_layout(p->mesh, F, p->k, nranks, rank, &sh);
+  sh.comm = comm;
+  const uint32_t na = sh.a0[rank + 1] - sh.a0[rank];
+  std::vector<uint32_t> loc_anchor(na);
+  for (uint32_t t = 0; t < na; ++t) loc_anchor[t] = p->mesh.anchors[sh.a0[rank] + t] - sh.r0[rank];
+  sh.d_loc_rp = (uint32_t*)plan_get(p, sh.loc_rp.size() * 4);
+  sh.d_loc_ci = (uint32_t*)plan_get(p, sh.loc_ci.size() * 4);
+  sh.d_loc_anchor = (uint32_t*)plan_get(p, (size_t)na * 4);
+  sh.d_keys = (unsigned long long*)plan_get(p, (3 * (size_t)p->k + 3) * 2 * 8);
+  sh.d_gather = (uint16_t*)plan_get(p, sh.stage_off[nranks] * 2);
+  bool ok = sh.d_loc_rp && sh.d_loc_ci && sh.d_loc_anchor && sh.d_keys && sh.d_gather;
+  cudaStream_t s = ctx->stream;
+  auto h2d = [&](void* d, const void* h, size_t bytes) {
+    if (bytes && ok) ok = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  };
+  h2d(sh.d_loc_rp, sh.loc_rp.data(), sh.loc_rp.size() * 4);
+  h2d(sh.d_loc_ci, sh.loc_ci.data(), sh.loc_ci.size() * 4);
+  h2d(sh.d_loc_anchor, loc_anchor.data(), (size_t)na * 4);
+  if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
+  if (!ok) {
+    dmcg_plan_destroy(p);
+    *plan = nullptr;
+    return ctx->set_error({DMCG_E_CUDA, "CudaError: shard plan allocation / upload failed"});
+  }
+  return ctx->set_error(Status::ok());
+}
+
 int dmcg_plan_encode_device(dmcg_plan* p, const void* const d_axes[3]) {
   if (!p) return DMCG_E_CONFIG;
   cudaSetDevice(p->ctx->device);
@@ -1149,10 +1193,15 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   tm.lap("prepare(analyze)");
   if (st.good()) st = plan_decode(p, &o, p->d_x_out);
   tm.lap("kernels");
-  const size_t bytes = (size_t)in->n * in->F * (out_dtype == DMCG_F32 ? 4 : 8);
+  // D2H of the decoded frame window only (all frames by default): columns
+  // outside the window of the caller's arrays are left untouched.
+  const size_t es = out_dtype == DMCG_F32 ? 4 : 8;
+  const size_t f0 = o.frame_count ? o.frame_begin : 0;
+  const size_t fw = o.frame_count ? o.frame_count : in->F;
   for (int a = 0; a < 3 && st.good(); ++a)
-    if (cudaMemcpyAsync(out_axes[a], p->d_x_out[a], bytes, cudaMemcpyDeviceToHost, ctx->stream) !=
-        cudaSuccess)
+    if (cudaMemcpy2DAsync((uint8_t*)out_axes[a] + f0 * es, in->F * es,
+                          (const uint8_t*)p->d_x_out[a] + f0 * es, in->F * es, fw * es, in->n,
+                          cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
       st = {DMCG_E_CUDA, "CudaError: D2H copy failed"};
   if (st.good() && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
     st = {DMCG_E_CUDA, "CudaError: stream sync failed"};

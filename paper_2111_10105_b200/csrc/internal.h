@@ -120,12 +120,49 @@ namespace dmcg {
 struct PlanGraph {
   cudaGraphExec_t exec = nullptr;
   const void* key[4] = {nullptr, nullptr, nullptr, nullptr};
-  int opt_key = 0;
+  long long opt_key = 0;
 };
+}  // namespace dmcg
+
+struct dmcg_comm;  // NCCL communicator (shard.cpp)
+namespace dmcg {
+// Vertex-row shard of one large sequence.  Rank q owns the
+// contiguous rows [r0[q], r0[q+1]); its local input holds those rows
+// followed by the halo rows (one-ring neighbours owned by other ranks) that
+// K1 needs.  The local Laplacian CSR keeps each row's global column order, so
+// the shard's delta rows equal the single-GPU rows bit for bit.
+struct ShardState {
+  int nranks = 1, rank = 0;
+  std::vector<uint32_t> r0;                  // nranks + 1 row boundaries
+  std::vector<uint32_t> a0;                  // nranks + 1 anchor-slot boundaries
+  std::vector<unsigned long long> stage_off; // nranks + 1 offsets (u16) into the gather buffer
+  uint32_t n_own = 0, n_loc = 0;
+  std::vector<uint32_t> halo;                // global ids of local rows n_own..n_loc-1
+  std::vector<uint32_t> loc_rp, loc_ci;      // local CSR of the owned rows
+  uint32_t* d_loc_rp = nullptr;
+  uint32_t* d_loc_ci = nullptr;
+  uint32_t* d_loc_anchor = nullptr;          // local rows of the owned anchors
+  unsigned long long* d_keys = nullptr;      // (3 k + 3) x (min, max) ordered keys
+  uint16_t* d_gather = nullptr;              // every rank's symbols (rank q at stage_off[q])
+  dmcg_comm* comm = nullptr;                 // not owned
+};
+// Row split, halo and local CSR of rank `rank` (needs m.lap_* and m.anchors).
+void shard_layout(const MeshHost& m, uint32_t F, uint32_t k, int nranks, int rank,
+                  ShardState* out);
+// Collectives on the plan stream (NCCL, shard.cpp).
+Status comm_allreduce_sum_f64(dmcg_comm* c, double* buf, size_t count, cudaStream_t s);
+Status comm_allreduce_max_u64(dmcg_comm* c, unsigned long long* buf, size_t count,
+                              cudaStream_t s);
+// Every rank q broadcasts buf[off[q] .. off[q+1]) (u16) in place to all ranks.
+Status comm_allgatherv_u16(dmcg_comm* c, uint16_t* buf, const unsigned long long* off,
+                           cudaStream_t s);
+int comm_size(const dmcg_comm* c);
+int comm_rank(const dmcg_comm* c);
 }  // namespace dmcg
 
 struct dmcg_plan {
   dmcg_ctx* ctx = nullptr;
+  std::unique_ptr<dmcg::ShardState> shard;  // vertex-row shard plans only
   // geometry / config
   uint32_t n = 0, F = 0, k = 0, n_c = 0, n_faces = 0;
   int dtype = DMCG_F64;

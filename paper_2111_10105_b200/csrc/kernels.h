@@ -26,6 +26,16 @@ cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long 
 // Anchor quantisation (codec.cpp:444-471), one CTA per axis.
 cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
                            const void* const x[3], bool f32, int bits, float* rng, uint16_t* q);
+// Vertex-row shards: anchor min/max keys of the rows[na] local
+// anchor rows (keys: 3 x (min, max) ordered keys), then their levels with
+// the (allreduced) global widened range -> rng (3 x 2), q (3 x na x F).
+cudaError_t launch_anchor_keys(cudaStream_t s, int na, int F, const uint32_t* rows,
+                               const void* const x[3], bool f32, unsigned long long* keys);
+cudaError_t launch_anchor_quant(cudaStream_t s, int na, int F, const uint32_t* rows,
+                                const void* const x[3], bool f32, int bits,
+                                const unsigned long long* keys, float* rng, uint16_t* q);
+// keys[2 r] = ~keys[2 r] for r < rows (min half <-> max-reducible).
+cudaError_t launch_flip_min_keys(cudaStream_t s, long rows, unsigned long long* keys);
 
 // DMC1 payload bit packing (stream.cpp BitWriter, MSB first) into a zeroed
 // byte buffer viewed as 32-bit words; base_byte = the section's byte offset.
@@ -86,12 +96,14 @@ cudaError_t launch_distortion(cudaStream_t s, int n, int F, const uint32_t* lap_
                               const uint32_t* lap_ci, const void* const a[3],
                               const void* const b[3], bool f32, double* work, double* rms,
                               double* nmsve, double* vme);
-// Row-major (n x 3F) variants used by the direct solver.
-cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
-                          const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,
-                          const uint16_t* anchor_q, const float* anchor_rng, int anchor_bits,
-                          const double* D, double* B, int* flags);
-cudaError_t launch_output_rm(cudaStream_t s, int n, int F, const double* X, void* const out[3],
-                             bool f32);
+// Row-major (n x 3F) variants used by the direct solver.  F = frames in the
+// decoded window [f_off, f_off + F) of the F_all-frame sequence (anchor
+// levels and the output arrays are indexed with F_all).
+cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
+                          const uint32_t* lap_rp, const uint32_t* lap_ci, const int32_t* anchor_pos,
+                          int n_c, const uint16_t* anchor_q, const float* anchor_rng,
+                          int anchor_bits, const double* D, double* B, int* flags);
+cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
+                             void* const out[3], bool f32);
 
 }  // namespace dmcg

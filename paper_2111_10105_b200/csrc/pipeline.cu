@@ -102,8 +102,9 @@ struct LoadDictDeq {
   uint32_t levels;
   int F;
   int* flags;
+  int f0;  // first decoded frame (frame window, dmcg_decode_options)
   __device__ __forceinline__ double operator()(int b, int r, int f) const {
-    const uint32_t lv = q[((long)b * F + r) * F + f];
+    const uint32_t lv = q[((long)b * F + r) * F + f0 + f];
     if (lv >= levels) atomicOr(flags, 1);
     return dequantize_level(-1.0, width, false, lv);
   }
@@ -142,9 +143,9 @@ int pick_splits(int tiles, int nbatch, int K) {
 }
 
 template <typename T>
-Status gram(dmcg_plan* p, const void* const x[3]) {
+Status gram(dmcg_plan* p, const void* const x[3], int n) {
   cudaStream_t s = p->ctx->stream;
-  const int F = (int)p->F, n = (int)p->n;
+  const int F = (int)p->F;
   const int tiles = ((F + kBM - 1) / kBM) * ((F + kBN - 1) / kBN);
   int splits = pick_splits(tiles, 3, n);
   const long maxs = (long)(p->part_elems / (3L * F * F));
@@ -214,7 +215,7 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
   DMCG_TRY(record_event(p->ev[1], s));
   // K2 autocorrelation (spectral.cpp:35-39).
-  Status st = f32 ? gram<float>(p, x) : gram<double>(p, x);
+  Status st = f32 ? gram<float>(p, x, n) : gram<double>(p, x, n);
   if (!st.good()) return st;
   DMCG_TRY(record_event(p->ev[2], s));
   // K3 basis.
@@ -258,7 +259,7 @@ static bool graphs_allowed(const dmcg_plan* p) {
 }
 
 template <class Fn>
-static Status run_graph(dmcg_plan* p, PlanGraph& g, const void* const key[4], int opt_key,
+static Status run_graph(dmcg_plan* p, PlanGraph& g, const void* const key[4], long long opt_key,
                         const Fn& enqueue) {
   cudaStream_t s = p->ctx->stream;
   if (!graphs_allowed(p)) return enqueue();
@@ -333,11 +334,132 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   return Status::ok();
 }
 
+
+// ---- vertex-row shards (shard.cpp has the layout and NCCL) -----
+// Phase 0: K1 delta of the owned rows (local CSR over owned + halo rows) and
+// the symmetrised Gram partial of the owned rows into d_R.
+// Phase 1: basis from the (allreduced) d_R, projection of the owned rows
+// with per-row min / max keys, anchor keys; min halves complemented so one
+// MAX allreduce combines every key.
+// Phase 2: keys restored; owned rows and anchors quantised into this rank's
+// slot of the gather buffer; dictionary levels.
+// Phase 3: every rank's symbols (after the all-gather) unpacked into the
+// plan's [3][k][n] / [3][n_c][F] encoded arrays; waits for the stream and
+// checks the flags.
+static Status shard_finish_stats(dmcg_plan* p);
+Status shard_phase(dmcg_plan* p, int phase, const void* const x[3]) {
+  ShardState& sh = *p->shard;
+  cudaStream_t s = p->ctx->stream;
+  const int F = (int)p->F, k = (int)p->k, n_own = (int)sh.n_own;
+  const bool f32 = p->dtype == DMCG_F32;
+  const long FF = (long)F * F;
+  const long krows = 3L * k + 3;
+  const int q = sh.rank;
+  const int na = (int)(sh.a0[q + 1] - sh.a0[q]);
+  switch (phase) {
+    case 0: {
+      DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
+      DMCG_TRY(record_event(p->ev[0], s));
+      DMCG_TRY(launch_delta(s, n_own, F, sh.d_loc_rp, sh.d_loc_ci, x, f32, p->d_delta,
+                            p->d_flags));
+      DMCG_TRY(record_event(p->ev[1], s));
+      Status st = f32 ? gram<float>(p, x, n_own) : gram<double>(p, x, n_own);
+      if (!st.good()) return st;
+      return Status::ok();
+    }
+    case 1: {
+      DMCG_TRY(record_event(p->ev[2], s));
+      p->forked = false;
+      Status st = basis(p);
+      if (!st.good()) return st;
+      DMCG_TRY(record_event(p->ev[3], s));
+      DMCG_TRY(launch_init_keys(s, krows, sh.d_keys));
+      if (k > 0) {
+        LoadDense<double, true> lU{p->d_U, FF, 1L, (long)F};
+        LoadDense<double, true> lD{p->d_delta, (long)n_own * F, 1L, (long)F};
+        DMCG_TRY(launch_gemm(s, 3, k, n_own, F, 1, lU, lD, StoreCoeffMinMax{p->d_C, sh.d_keys}));
+      }
+      DMCG_TRY(launch_anchor_keys(s, na, F, sh.d_loc_anchor, x, f32, sh.d_keys + 6L * k));
+      DMCG_TRY(launch_flip_min_keys(s, krows, sh.d_keys));
+      return Status::ok();
+    }
+    case 2: {
+      DMCG_TRY(launch_flip_min_keys(s, krows, sh.d_keys));
+      uint16_t* stage = sh.d_gather + sh.stage_off[q];
+      if (k > 0)
+        DMCG_TRY(launch_quant_rows(s, k, n_own, sh.d_keys, p->d_row_bits + 3 * k, p->d_C,
+                                   p->d_row_min, p->d_row_max, p->d_row_bits, stage));
+      DMCG_TRY(launch_anchor_quant(s, na, F, sh.d_loc_anchor, x, f32, p->anchor_bits,
+                                   sh.d_keys + 6L * k, p->d_anchor_rng,
+                                   stage + 3L * k * n_own));
+      DMCG_TRY(record_event(p->ev[4], s));
+      if (p->forked) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
+      DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
+      return Status::ok();
+    }
+    case 3: {
+      const size_t n = p->n, n_c = p->n_c;
+      for (int r = 0; r < sh.nranks; ++r) {
+        const size_t own = sh.r0[r + 1] - sh.r0[r], nar = sh.a0[r + 1] - sh.a0[r];
+        const uint16_t* src = sh.d_gather + sh.stage_off[r];
+        if (k > 0 && own)
+          DMCG_TRY(cudaMemcpy2DAsync(p->d_coeff_q + sh.r0[r], n * 2, src, own * 2, own * 2,
+                                     3 * (size_t)k, cudaMemcpyDeviceToDevice, s));
+        if (nar)
+          DMCG_TRY(cudaMemcpy2DAsync(p->d_anchor_q + (size_t)sh.a0[r] * F, n_c * F * 2,
+                                     src + 3 * (size_t)k * own, nar * F * 2, nar * F * 2, 3,
+                                     cudaMemcpyDeviceToDevice, s));
+      }
+      DMCG_TRY(record_event(p->ev[5], s));
+      return shard_finish_stats(p);
+    }
+  }
+  return Status{DMCG_E_CONFIG, "ConfigError: bad shard phase"};
+}
+
+static Status shard_finish_stats(dmcg_plan* p) {
+  cudaStream_t s = p->ctx->stream;
+  int flags[8];
+  DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  DMCG_TRY(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&p->stats.ms_encode, p->ev[0], p->ev[5]);
+  cudaEventElapsedTime(&p->stats.ms_delta, p->ev[0], p->ev[1]);
+  cudaEventElapsedTime(&p->stats.ms_gram, p->ev[1], p->ev[2]);    // incl. the allreduce
+  cudaEventElapsedTime(&p->stats.ms_basis, p->ev[2], p->ev[3]);
+  cudaEventElapsedTime(&p->stats.ms_project, p->ev[3], p->ev[4]); // incl. the key allreduce
+  if (flags[0])
+    return Status{DMCG_E_INDEX, "ValidationError: non-finite coordinate in the local rows"};
+  if (flags[3])
+    return Status{DMCG_E_NUMERICAL,
+                  "ConvergenceFailure: symmetric eigendecomposition did not converge"};
+  return Status::ok();
+}
+
+Status shard_encode(dmcg_plan* p, const void* const x[3]) {
+  ShardState& sh = *p->shard;
+  cudaStream_t s = p->ctx->stream;
+  const size_t FF = (size_t)p->F * p->F;
+  Status st = shard_phase(p, 0, x);
+  if (st.good()) st = comm_allreduce_sum_f64(sh.comm, p->d_R, 3 * FF, s);
+  if (st.good()) st = shard_phase(p, 1, x);
+  if (st.good()) st = comm_allreduce_max_u64(sh.comm, sh.d_keys, (3ull * p->k + 3) * 2, s);
+  if (st.good()) st = shard_phase(p, 2, x);
+  if (st.good()) st = comm_allgatherv_u16(sh.comm, sh.d_gather, sh.stage_off.data(), s);
+  if (st.good()) st = shard_phase(p, 3, x);
+  return st;
+}
+
 // Direct decode: K6 into the row-major n x 3F layout, rhs, supernodal
 // Cholesky factor + solve + refinement (solver.cpp:43-58, 82-90).
-static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void* const out[3]) {
+// Frames [f0, f0 + Fw) only (the solve is column-separable: each frame
+// column's result does not depend on the others, so a window decodes to the
+// same bits as the full decode).
+static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void* const out[3],
+                                    int f0, int Fw) {
   cudaStream_t s = p->ctx->stream;
-  const int n = (int)p->n, F = (int)p->F, k = (int)p->k, W = (int)p->W;
+  const int n = (int)p->n, F = Fw, F_all = (int)p->F, k = (int)p->k, W = 3 * Fw;
+  CholDev cdev = p->cdev;
+  cdev.W = (uint32_t)W;
   const bool f32 = p->dtype == DMCG_F32;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
   DMCG_TRY(record_event(p->ev[0], s));
@@ -353,33 +475,33 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
     DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
     LoadCoeffDeq la{p->d_coeff_q, p->d_rowp, p->d_row_bits, p->d_flags + 1, n, k};
     const uint32_t levels = 1u << p->dict_bits;
-    LoadDictDeq lb{p->d_dict_q, 2.0 / (double)levels, levels, F, p->d_flags + 1};
+    LoadDictDeq lb{p->d_dict_q, 2.0 / (double)levels, levels, F_all, p->d_flags + 1, f0};
     // delta~ (i, a*F + f): batch b = axis, rows = vertices, cols = frames
     DMCG_TRY(launch_gemm(s, 3, n, F, k, 1, la, lb,
                          StoreStrided{p->d_rm_delta, (long)F, (long)W, 1L}));
   } else {
     DMCG_TRY(cudaMemsetAsync(p->d_rm_delta, 0, nW * sizeof(double), s));
   }
-  DMCG_TRY(launch_rhs_rm(s, n, F, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos, (int)p->n_c,
+  DMCG_TRY(launch_rhs_rm(s, n, F, F_all, f0, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos, (int)p->n_c,
                          p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_rm_delta, p->d_rm_b,
                          p->d_flags + 1));
   DMCG_TRY(record_event(p->ev[1], s));
   DMCG_TRY(cudaEventRecord(p->ev_join, s));
   s = s1;
-  if (factor) DMCG_TRY(chol_factor_device(s, p->cdev, p->levels));
+  if (factor) DMCG_TRY(chol_factor_device(s, cdev, p->levels));
   DMCG_TRY(record_event(p->ev[2], s));
   DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
   DMCG_TRY(record_event(p->ev[5], s));
-  DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
-  DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, false));
+  DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
+  DMCG_TRY(chol_unpermute(s, n, W, cdev.perm, p->d_rm_xp, p->d_rm_x, false));
   for (int r = 0; r < refine; ++r) {
     DMCG_TRY(normal_residual(s, n, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b, p->d_rm_x,
                              p->d_rm_r));
-    DMCG_TRY(chol_solve_device(s, p->cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp));
-    DMCG_TRY(chol_unpermute(s, n, W, p->cdev.perm, p->d_rm_xp, p->d_rm_x, true));
+    DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp));
+    DMCG_TRY(chol_unpermute(s, n, W, cdev.perm, p->d_rm_xp, p->d_rm_x, true));
   }
   DMCG_TRY(record_event(p->ev[3], s));
-  DMCG_TRY(launch_output_rm(s, n, F, p->d_rm_x, out, f32));
+  DMCG_TRY(launch_output_rm(s, n, F, F_all, f0, p->d_rm_x, out, f32));
   DMCG_TRY(record_event(p->ev[4], s));
   return Status::ok();
 }
@@ -387,13 +509,24 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
 static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
                                  void* const out[3]) {
   cudaStream_t s = p->ctx->stream;
-  const int k = (int)p->k, W = (int)p->W;
+  const int k = (int)p->k;
   const int refine = opt ? opt->refine : 1;
   const bool factor = !(opt && opt->reuse_factor && p->factor_valid);
+  uint32_t f0 = opt ? opt->frame_begin : 0, Fw = opt ? opt->frame_count : 0;
+  if (Fw == 0) {
+    f0 = 0;
+    Fw = p->F;
+  }
+  if (f0 >= p->F || Fw > p->F - f0)
+    return Status{DMCG_E_CONFIG, "DimensionMismatch: frame window outside the sequence"};
+  const int W = 3 * (int)Fw;
   const void* key[4] = {out[0], out[1], out[2], nullptr};
   {
-    Status st = run_graph(p, p->g_decode, key, refine * 2 + (factor ? 1 : 0),
-                          [&] { return enqueue_decode_direct(p, refine, factor, out); });
+    const long long okey = ((long long)f0 << 40) | ((long long)Fw << 16) | (refine * 2) |
+                           (factor ? 1 : 0);
+    Status st = run_graph(p, p->g_decode, key, okey, [&] {
+      return enqueue_decode_direct(p, refine, factor, out, (int)f0, (int)Fw);
+    });
     if (!st.good()) return st;
   }
   int flags[8];
