@@ -12,6 +12,10 @@ Contract: one JSON line on rank 0.
     D2H of the encoded symbols, H2D for decode, D2H of the vertices.
   * N > 1 (torchrun): every rank codes its own independent sequence (seed
     offset by rank) with no data-path collective -> scaling "weak".
+  * --rows (c3): ONE sequence sharded by vertex rows across the N ranks
+    (libdmcg shard ABI: NCCL allreduce of the Gram partials and range keys,
+    all-gather of the symbols; decode split by frame windows) -> scaling
+    "strong" (the whole job is one sequence per step).
   * --impl reference: the CPU oracle port (kind "port", the reference itself
     cannot be built here: Eigen3 absent) on the host cores; rank 0 only.
 """
@@ -144,6 +148,147 @@ def cpu_baseline(args, spec, s):
                       f"{threads} threads, {dt:.2f} s"}
 
 
+class _DevArray:
+    """__cuda_array_interface__ view of a libdmcg device buffer (for torch)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3}
+
+
+def run_rows(args, rank, world, local, dist):
+    """One sequence, vertex rows sharded over the ranks."""
+    import torch
+    from paper_2111_10105_b200 import codec as C
+    from paper_2111_10105_b200 import shard, synth
+
+    spec = synth.CONFIGS[args.config]
+    s = spec.make(0)
+    cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds)
+    f32 = spec.dtype == "f32"
+    npdt = np.float32 if f32 else np.float64
+    tdt = torch.float32 if f32 else torch.float64
+    codec = C.Codec(local)
+    comm = shard.Comm(local, world, rank, dist)
+    plan = shard.ShardPlan(codec, s.n, s.F, s.faces, cfg, world, rank, comm, dtype=npdt)
+    info = plan.info
+    loc_host = plan.local_rows([np.asarray(a, dtype=npdt) for a in s.axes])
+    d_loc = [torch.from_numpy(a).cuda() for a in loc_host]
+    d_out = [torch.zeros((s.n, s.F), dtype=tdt, device="cuda") for _ in range(3)]
+    f0, f1 = plan.frames()
+    stream = torch.cuda.ExternalStream(plan.stream())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        plan.encode_device([t.data_ptr() for t in d_loc])
+        plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol, frames=(f0, f1))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms, stages, launches = [], [], 0
+    with Clocks(local) as clk:
+        for it in range(args.steps):
+            flush.fill_(it & 0xFF)
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            st = plan.stats()
+            stages.append({k: v for k, v in st.items() if k.startswith("ms_")})
+            launches += st["kernel_launches_encode"] + st["kernel_launches_decode"]
+    total_ms = max_over_ranks(float(sum(step_ms)), dist, "cuda")
+    value = s.n * s.F * args.steps / (total_ms / 1e3)
+
+    # e2e: pinned host local rows -> H2D, sharded encode, D2H of this rank's
+    # symbols (its share of the compressed stream), frame-window decode, D2H of
+    # the window's frames.
+    pin_in = [torch.from_numpy(a).pin_memory() for a in loc_host]
+    sym_ptr, _ = plan.buffer(shard.SHARD_SYMBOLS)
+    sb, sc = info["stage_begin"], info["stage_count"]
+    syms = torch.as_tensor(_DevArray(sym_ptr, info["gather_count"], "<i2"), device="cuda")
+    pin_sym = torch.empty(sc, dtype=torch.int16).pin_memory()
+    pin_out = [torch.empty((s.n, f1 - f0), dtype=tdt).pin_memory() for _ in range(3)]
+    e2e_ms = []
+    for it in range(max(2, args.steps) + 1):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            for a in range(3):
+                d_loc[a].copy_(pin_in[a], non_blocking=True)
+        plan.encode_device([t.data_ptr() for t in d_loc])
+        with torch.cuda.stream(stream):
+            pin_sym.copy_(syms[sb:sb + sc], non_blocking=True)
+        plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol, frames=(f0, f1))
+        with torch.cuda.stream(stream):
+            for a in range(3):
+                pin_out[a].copy_(d_out[a][:, f0:f1], non_blocking=True)
+        stream.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        if it > 0:
+            e2e_ms.append(dt)
+    e2e_total = max_over_ranks(float(sum(e2e_ms)), dist, "cuda")
+    e2e_value = s.n * s.F * len(e2e_ms) / (e2e_total / 1e3)
+    es = np.dtype(npdt).itemsize
+    h2d = sum(a.nbytes for a in loc_host)
+    d2h = sc * 2 + 3 * s.n * (f1 - f0) * es
+    out = [t.cpu().numpy() for t in d_out]
+    bbox = float(np.linalg.norm([a.max() - a.min() for a in s.axes]))
+    err = max(float(np.abs(out[a][:, f0:f1].astype(np.float64) - s.axes[a][:, f0:f1]).max())
+              for a in range(3))
+    st = plan.stats()
+    if rank == 0:
+        med = {k: float(np.median([d[k] for d in stages])) for k in stages[0]}
+        oi_flops = float(st["flops_oi"])
+        oi_ms = med.get("ms_oi", 0.0)
+        achieved = oi_flops / (oi_ms / 1e3) / 1e12 if oi_ms > 0 else 0.0
+        line = {
+            "metric": "encode+decode vertex-frames/sec", "value": value, "unit": "vertex-frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64" if not f32 else "f64 (f32 storage)",
+            "data": "synthetic (seeded generator, DESIGN.md §2)",
+            "config": {"workload": WORKLOADS[args.config], "per_gpu": "1/N of one sequence per step",
+                       "parallelism": f"vertex rows x{world} (encode: NCCL allreduce of Gram "
+                                      "partials + range keys, all-gather of symbols; decode: "
+                                      "frame windows, replicated factor)",
+                       "rows_per_rank": info["n_own"], "halo_rows": info["n_halo"],
+                       "frames_decoded_per_rank": f1 - f0,
+                       "l2": "256 MiB flush between timed steps", "cg_rtol": args.rtol},
+            "roofline": {"kernel": "k_oi_fused", "bound": "tensor", "achieved": achieved,
+                         "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_DMMA_TFLOPS, "traffic": None,
+                         "algorithmic_flops": oi_flops, "ms": oi_ms,
+                         "share_of_step": oi_ms / (total_ms / args.steps)},
+            "cpu_baseline": None,
+            "e2e": {"value": e2e_value, "unit": "vertex-frames/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_total / len(e2e_ms),
+                    "note": "per rank: pinned local rows in, own symbols + own frame window out; "
+                            "plan (mesh, halo, symbolic analysis) built once outside"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "quality": {"max_err_over_bbox_rank0_window": err / bbox},
+            "stage_ms_rank0": med,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    comm.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -153,6 +298,8 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rows", action="store_true",
+                    help="shard one sequence by vertex rows across the ranks (SURVEY §8e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     rank, world, local = dist_env()
@@ -167,6 +314,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if args.rows:
+        return run_rows(args, rank, world, local, dist)
 
     spec, s = sequence_for_rank(args.config, rank)
     cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds)

@@ -33,7 +33,9 @@ EXPORTS = [
     "dmcg_anchor_count", "dmcg_select_anchors", "dmcg_plan_create", "dmcg_plan_destroy",
     "dmcg_plan_encode_device", "dmcg_plan_decode_device", "dmcg_plan_download", "dmcg_plan_upload",
     "dmcg_plan_basis", "dmcg_plan_stats", "dmcg_ctx_stats", "dmcg_plan_stream", "dmcg_debug_chol",
-    "dmcg_plan_serialize", "dmcg_plan_distortion",
+    "dmcg_plan_serialize", "dmcg_plan_distortion", "dmcg_comm_unique_id", "dmcg_comm_create",
+    "dmcg_comm_destroy", "dmcg_shard_layout", "dmcg_plan_create_shard", "dmcg_shard_info_get",
+    "dmcg_shard_encode_device", "dmcg_shard_encode_phase", "dmcg_shard_buffer",
 ]
 
 

@@ -427,6 +427,8 @@ static Status shard_finish_stats(dmcg_plan* p) {
   cudaEventElapsedTime(&p->stats.ms_gram, p->ev[1], p->ev[2]);    // incl. the allreduce
   cudaEventElapsedTime(&p->stats.ms_basis, p->ev[2], p->ev[3]);
   cudaEventElapsedTime(&p->stats.ms_project, p->ev[3], p->ev[4]); // incl. the key allreduce
+  const bool oi = p->rounds > 0 && p->k < p->F && p->k > 0;
+  p->stats.kernel_launches_encode = 1 + 2 + (oi ? 10 : 3) + 1 + (p->k > 0 ? 2 : 0) + 1 + 2 + 1 + 1;
   if (flags[0])
     return Status{DMCG_E_INDEX, "ValidationError: non-finite coordinate in the local rows"};
   if (flags[3])
