@@ -428,6 +428,14 @@ static Status shard_finish_stats(dmcg_plan* p) {
   cudaEventElapsedTime(&p->stats.ms_basis, p->ev[2], p->ev[3]);
   cudaEventElapsedTime(&p->stats.ms_project, p->ev[3], p->ev[4]); // incl. the key allreduce
   const bool oi = p->rounds > 0 && p->k < p->F && p->k > 0;
+  p->stats.ms_oi = 0.0f;
+  p->stats.flops_oi = 0.0;
+  if (oi) {
+    cudaEventElapsedTime(&p->stats.ms_oi, p->ev[6], p->ev[7]);
+    const double F = p->F, k = p->k, r = p->rounds;
+    const double qr = 2.0 * (2.0 * F * k * k - 2.0 * k * k * k / 3.0);
+    p->stats.flops_oi = 3.0 * ((r + 1.0) * (qr + 2.0 * F * F * k) + 2.0 * F * k * k);
+  }
   p->stats.kernel_launches_encode = 1 + 2 + (oi ? 10 : 3) + 1 + (p->k > 0 ? 2 : 0) + 1 + 2 + 1 + 1;
   if (flags[0])
     return Status{DMCG_E_INDEX, "ValidationError: non-finite coordinate in the local rows"};
