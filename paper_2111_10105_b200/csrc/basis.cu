@@ -555,6 +555,113 @@ __device__ __noinline__ void warp_panel_qr(P Z, int m, int ld, int c0, int pb, d
   PANEL_STAMP(4);
 }
 
+// warp_panel_qr + dlarft in the same reduction rounds (panel = the whole
+// block, B == PW): at column j the round that sums the tail norm and x^T y_l
+// (l > j) also sums x^T v_l for the earlier reflectors l < j, which gives
+// G(l, j) = v_l^T v_j = v_l(j) + rinv x^T v_l; lane l then extends row l of T:
+//   T(l, j) = -tau_j sum_{m=l}^{j-1} T(l, m) G(m, j),  T(j, j) = tau_j.
+// Z points at the block's diagonal row; T row-major PW x PW.
+template <int MAXR, int PW, typename P>
+__device__ __noinline__ void warp_panel_qr_T(P Z, int m, int ld, int pb, double* tau, double* T,
+                                             int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int M = m;
+  double a[MAXR][PW];
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t)
+#pragma unroll
+    for (int c = 0; c < PW; ++c) {
+      const int g = lane + 32 * t;
+      a[t][c] = (c < pb && g < M) ? Z[c * ld + g] : 0.0;
+    }
+  double tv[PW], tr[PW];
+#pragma unroll
+  for (int i = 0; i < PW; ++i) tr[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < PW; ++j) {
+    double r[PW + 1];
+#pragma unroll
+    for (int l = 0; l <= PW; ++l) r[l] = 0.0;
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int g = lane + 32 * t;
+      const double x = g > j ? a[t][j] : 0.0;
+      r[PW] = fma(x, x, r[PW]);
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l != j) r[l] = fma(x, a[t][l], r[l]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r[PW] += __shfl_xor_sync(FULL, r[PW], o);
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l != j) r[l] += __shfl_xor_sync(FULL, r[l], o);
+    }
+    const double tail = r[PW];
+    const double x0 = __shfl_sync(FULL, a[0][j], j);
+    double yj[PW];
+#pragma unroll
+    for (int l = 0; l < PW; ++l) yj[l] = l != j ? __shfl_sync(FULL, a[0][l], j) : 0.0;
+    double rinv = 0.0, tj = 0.0, beta = x0;
+    if (tail > DBL_MIN) {
+      const double s2 = x0 * x0 + tail;
+      const double rs = rsqrt(s2);
+      const double nrm = s2 * rs;
+      beta = x0 >= 0.0 ? -nrm : nrm;
+      const double ibb = x0 >= 0.0 ? -rs : rs;
+      rinv = __drcp_rn(x0 - beta);
+      tj = (beta - x0) * ibb;
+    }
+    // G(l, j) for l < j (yj[l] = v_l(j), the stored reflector entry in row j)
+    double gcol[PW];
+#pragma unroll
+    for (int l = 0; l < PW; ++l) gcol[l] = l < j ? fma(rinv, r[l], yj[l]) : 0.0;
+    {
+      double acc = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < PW; ++mm)
+        if (mm < j && mm >= lane) acc = fma(tr[mm], gcol[mm], acc);
+      const double tl = lane < j ? -tj * acc : (lane == j ? tj : 0.0);
+#pragma unroll
+      for (int i = 0; i < PW; ++i)
+        if (i == j) tr[i] = j < pb ? tl : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < MAXR; ++t) {
+      const int g = lane + 32 * t;
+      if (g > j) a[t][j] *= rinv;
+    }
+    if (lane == j) a[0][j] = beta;
+    tv[j] = tj;
+#pragma unroll
+    for (int l = 0; l < PW; ++l) {
+      if (l <= j) continue;
+      const double sl = tj * fma(rinv, r[l], yj[l]);
+#pragma unroll
+      for (int t = 0; t < MAXR; ++t) {
+        const int g = lane + 32 * t;
+        if (g > j) a[t][l] = fma(-sl, a[t][j], a[t][l]);
+      }
+      if (lane == j) a[0][l] -= sl;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t)
+#pragma unroll
+    for (int c = 0; c < PW; ++c) {
+      const int g = lane + 32 * t;
+      if (c < pb && g < M) Z[c * ld + g] = a[t][c];
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+      if (j < pb) tau[j] = tv[j];
+  if (lane < PW)
+#pragma unroll
+    for (int i = 0; i < PW; ++i) T[lane * PW + i] = lane < pb ? tr[i] : 0.0;
+}
+
 // dlarft: T (PW x PW row-major, upper) from G(l, i) = v_l^T v_i (row-major,
 // ld ldg) and tau; lane j of warp 0 forms row j:
 //   T(j, j) = tau_j,  T(j, i) = -tau_i sum_{l=j}^{i-1} T(j, l) G(l, i).
@@ -1041,6 +1148,319 @@ __global__ void k_fill_zero(double* p, long count) {
   if (t < count) p[t] = 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Column-distributed orthogonal iterations (k_oi_cluster): the cluster's cs
+// CTAs of one axis each own a block of B columns of Z and Q (F x B in
+// shared memory), so both the QR and Z = R Q spread over the cluster:
+//   * Z_c = R Q_c needs only the CTA's own Q block (R streams from L2);
+//   * the Householder QR is a wavefront over the blocks: CTA c applies the
+//     block reflectors H_p (p < c) of the earlier CTAs to its block as soon
+//     as each is published (V_p read over distributed shared memory), then
+//     factors its own block, forms T_c (dlarft) and publishes it with a
+//     release flag — no cluster-wide barrier per panel;
+//   * the thin Q block Q_c = H_0 ... H_c E_c needs only the published
+//     reflectors, so every CTA forms its block independently;
+//   * one cluster barrier per round (all remote reads of V done before the
+//     next R Q overwrites Z).
+// Same reflector formulas as the single-CTA path (warp_panel_qr /
+// wqr_factor), so the result agrees with the oracle's householder_factor to
+// rounding (P3).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire_cluster(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cluster(int* p, int v) {
+  asm volatile("st.release.cluster.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Masked element of a unit-lower-trapezoidal block V (M x nb, column i at
+// Vb + i ldv, row 0 = the block's diagonal row).
+__device__ __forceinline__ double vmask(const double* Vb, int ldv, int g, int i, int M, int nb) {
+  const int gc = g < M ? g : M - 1, ic = i < nb ? i : nb - 1;
+  const double x = Vb[ic * ldv + gc];
+  const double v = g > i ? x : (g == i ? 1.0 : 0.0);
+  return (g < M && i < nb) ? v : 0.0;
+}
+
+// W (nb x nc, row-major ld B) = V^T Y over M rows (Y: column j at Yb + j ldy;
+// y_is_v: Y is V itself, masked the same way -> G = V^T V).  8 x 8 DMMA
+// tiles; K split over the warps left after one warp per tile, partial tiles
+// summed in `part` (nw x 64 doubles).
+template <int B>
+__device__ void blk_vty(const double* Vb, int ldv, int nb, const double* Yb, int ldy, int nc,
+                        bool y_is_v, int M, double* W, double* part, const double* T = nullptr,
+                        bool trans = false) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  constexpr int TR = B / 8;
+  const int tc = (nc + 7) / 8, ntile = TR * tc;
+  const int nk = nw / ntile > 0 ? nw / ntile : 1;
+  const int i = lane >> 2, q = lane & 3;
+  if (warp < ntile * nk) {
+    const int tile = warp % ntile, kc = warp / ntile;
+    const int ti = tile % TR, tj = tile / TR;
+    const int ksteps = (M + 3) / 4;
+    const int k0 = (int)((long)ksteps * kc / nk) * 4, k1 = (int)((long)ksteps * (kc + 1) / nk) * 4;
+    double acc[2][2] = {};
+    const int ia = ti * 8 + i, jb = tj * 8 + i;
+    for (int kk = k0; kk < k1; kk += 8) {
+      const int g0 = kk + q, g1 = kk + 4 + q;
+      const double a0 = vmask(Vb, ldv, g0, ia, M, nb);
+      const double a1 = g1 < k1 ? vmask(Vb, ldv, g1, ia, M, nb) : 0.0;
+      double b0, b1;
+      if (y_is_v) {
+        b0 = vmask(Yb, ldy, g0, jb, M, nc);
+        b1 = g1 < k1 ? vmask(Yb, ldy, g1, jb, M, nc) : 0.0;
+      } else {
+        const int jc = jb < nc ? jb : nc - 1;
+        b0 = (g0 < M && jb < nc) ? Yb[jc * ldy + g0] : 0.0;
+        b1 = (g1 < M && g1 < k1 && jb < nc) ? Yb[jc * ldy + g1] : 0.0;
+      }
+      dmma884(acc[0], a0, b0);
+      dmma884(acc[1], a1, b1);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) part[warp * 64 + i * 8 + q * 2 + e] = acc[0][e] + acc[1][e];
+  }
+  __syncthreads();
+  if (T) {  // W = T^T (V^T Y) or T (V^T Y): one thread per column
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      double w[B];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        const int tile = (r / 8) + TR * (c / 8);
+        double s = 0.0;
+        for (int kc = 0; kc < nk; ++kc) s += part[(tile + kc * ntile) * 64 + (r % 8) * 8 + (c % 8)];
+        w[r] = r < nb ? s : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < B; ++l)
+          if (trans ? (l <= i) : (l >= i)) acc = fma(trans ? T[l * B + i] : T[i * B + l], w[l], acc);
+        if (i < nb) W[i * B + c] = acc;
+      }
+    }
+  } else {
+    for (int t = threadIdx.x; t < nb * nc; t += blockDim.x) {
+      const int r = t / nc, c = t % nc;
+      const int tile = (r / 8) + TR * (c / 8);
+      double s = 0.0;
+      for (int kc = 0; kc < nk; ++kc) s += part[(tile + kc * ntile) * 64 + (r % 8) * 8 + (c % 8)];
+      W[r * B + c] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Y (M x nc) -= V (M x nb) W (nb x nc): 8-row tiles over the warps, all
+// nc / 8 column tiles of a row tile at once (K = nb <= B).
+template <int B>
+__device__ void blk_update(const double* Vb, int ldv, int nb, double* Yb, int ldy, int nc, int M,
+                           const double* W) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  constexpr int KT = B / 4, CT = B / 8;
+  double bw[CT][KT];
+#pragma unroll
+  for (int t = 0; t < CT; ++t)
+#pragma unroll
+    for (int u = 0; u < KT; ++u) {
+      const int i = 4 * u + q, c = t * 8 + r;
+      bw[t][u] = (i < nb && c < nc) ? W[i * B + c] : 0.0;
+    }
+  for (int mt = warp; mt * 8 < M; mt += nw) {
+    const int g = mt * 8 + r;
+    double av[KT];
+#pragma unroll
+    for (int u = 0; u < KT; ++u) av[u] = vmask(Vb, ldv, g, 4 * u + q, M, nb);
+    double acc[CT][2] = {};
+#pragma unroll
+    for (int t = 0; t < CT; ++t)
+#pragma unroll
+      for (int u = 0; u < KT; ++u) dmma884(acc[t], av[u], bw[t][u]);
+#pragma unroll
+    for (int t = 0; t < CT; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = t * 8 + 2 * q + e;
+        if (g < M && c < nc) Yb[c * ldy + g] -= acc[t][e];
+      }
+  }
+  __syncthreads();
+}
+
+// Y <- (I - V T^(T) V^T) Y for one block reflector (W, part: scratch).
+// A remote V / T (another CTA's shared memory) is first copied into the
+// local staging buffers with every thread's loads in flight at once, so the
+// DMMA passes read local shared memory only.
+template <int B>
+__device__ void blk_apply(const double* Vb, int ldv, int nb, const double* T, bool trans,
+                          double* Yb, int ldy, int nc, int M, double* W, double* part,
+                          double* vstage, double* tstage, bool remote) {
+  if (remote) {
+    constexpr int U = 8;
+    const int total = (nb - 1) * ldv + M;  // columns of M rows, ld ldv
+    for (int t0 = threadIdx.x; t0 < total; t0 += U * blockDim.x) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * blockDim.x;
+        v[u] = t < total ? Vb[t] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u * blockDim.x;
+        if (t < total) vstage[t] = v[u];
+      }
+    }
+    for (int t = threadIdx.x; t < B * B; t += blockDim.x) tstage[t] = T[t];
+    __syncthreads();
+    Vb = vstage;
+    T = tstage;
+  }
+  blk_vty<B>(Vb, ldv, nb, Yb, ldy, nc, false, M, W, part, T, trans);
+  blk_update<B>(Vb, ldv, nb, Yb, ldy, nc, M, W);
+}
+
+__device__ long long g_oic_prof[64 * 8];  // per-CTA cycle split of k_oi_cluster (DMCG_DEBUG)
+
+template <int MAXR, int B>
+__global__ void __launch_bounds__(kOiThreads)
+    k_oi_cluster(int F, int k, int rounds, const double* __restrict__ Rall,
+                 const double* __restrict__ start, double* Qall, double* Hall) {
+  extern __shared__ double dyn[];
+  __shared__ double s_tau[B];
+  __shared__ double s_T[B * B];
+  __shared__ double s_W[B * B];
+  __shared__ double s_part[(kOiThreads / 32) * 64];
+  __shared__ int s_ready;
+  constexpr int PW = QrPanel<MAXR>::PW;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int b = blockIdx.x / cs;
+  const int ld = odd_ld(F);
+  double* Zb = dyn;
+  double* Qb = dyn + (size_t)ld * B;
+  double* Vs = Qb + (size_t)ld * B;   // staging copy of a remote block reflector
+  double* Ts = Vs + (size_t)ld * B;   // and its T
+  double* scr = Ts + B * B;           // wqr_factor scratch (B > PW)
+  const int c0 = rank * B, nb = min(B, k - c0);
+  const double* R = Rall + (size_t)b * F * F;
+  const double* S = start + (size_t)b * F * k;
+  for (int t = threadIdx.x; t < F * B; t += blockDim.x) {
+    const int j = t / F, i = t % F;
+    Zb[j * ld + i] = j < nb ? S[(size_t)(c0 + j) * F + i] : 0.0;
+  }
+  if (threadIdx.x == 0) s_ready = 0;
+  cluster_sync_all();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  long long t_wait = 0, t_app = 0, t_fac = 0, t_form = 0, t_sync = 0, t_rq = 0;
+  for (int r = 0;; ++r) {
+    const int epoch = r + 1;
+    long long t0 = clock64();
+    // ---- factor: apply the published reflectors of the earlier blocks ----
+    for (int p = 0; p < rank; ++p) {
+      if (threadIdx.x == 0) {
+        const int* f = cl.map_shared_rank(&s_ready, p);
+        while (ld_acquire_cluster(f) < epoch) {
+        }
+      }
+      __syncthreads();
+      long long t1 = clock64();
+      t_wait += t1 - t0;
+      const double* Vp = cl.map_shared_rank(Zb, p);
+      const double* Tp = cl.map_shared_rank(s_T, p);
+      blk_apply<B>(Vp + p * B, ld, B, Tp, true, Zb + p * B, ld, nb, F - p * B, s_W, s_part,
+                   Vs + p * B, Ts, true);
+      t0 = clock64();
+      t_app += t0 - t1;
+    }
+    // ---- own block: Householder factor, T = dlarft(V, tau), publish ------
+    if (nb > 0) {
+      if (B == PW) {
+        if (warp == 0) warp_panel_qr_T<MAXR, PW>(Zb + c0, F - c0, ld, nb, s_tau, s_T, lane);
+        __syncthreads();
+      } else {
+        wqr_factor<MAXR>(Zb + c0, F - c0, ld, nb, s_tau, scr, nb);
+        blk_vty<B>(Zb + c0, ld, nb, Zb + c0, ld, nb, true, F - c0, s_W, s_part);
+      }
+      if (B != PW && warp == 0) {
+        // dlarft row j on lane j from G = s_W (row-major, ld B)
+        if (lane < B) {
+          const int j = lane;
+          double tr[B];
+#pragma unroll
+          for (int i = 0; i < B; ++i) {
+            double v = 0.0;
+            if (i < nb && i == j) v = s_tau[i];
+            if (i < nb && i > j) {
+              double acc = 0.0;
+#pragma unroll
+              for (int l = 0; l < B; ++l)
+                if (l < i && l >= j) acc = fma(tr[l], s_W[l * B + i], acc);
+              v = -s_tau[i] * acc;
+            }
+            tr[i] = j < nb ? v : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < B; ++i) s_T[j * B + i] = tr[i];
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) st_release_cluster(&s_ready, epoch);
+    long long t1 = clock64();
+    t_fac += t1 - t0;
+    // ---- thin Q block: Q_c = H_0 ... H_c E_c ------------------------------
+    for (int t = threadIdx.x; t < F * B; t += blockDim.x) {
+      const int j = t / F, i = t % F;
+      Qb[j * ld + i] = (j < nb && i == c0 + j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int p = rank; p >= 0 && nb > 0; --p) {
+      const bool own = p == rank;
+      const double* Vp = own ? Zb : cl.map_shared_rank(Zb, p);
+      const double* Tp = own ? s_T : cl.map_shared_rank(s_T, p);
+      blk_apply<B>(Vp + p * B, ld, own ? nb : B, Tp, false, Qb + p * B, ld, nb, F - p * B, s_W,
+                   s_part, Vs + p * B, Ts, !own);
+    }
+    t0 = clock64();
+    t_form += t0 - t1;
+    cluster_sync_all();  // every remote read of this round's V is done
+    t1 = clock64();
+    t_sync += t1 - t0;
+    // ---- Z_c = R Q_c --------------------------------------------------------
+    if (nb > 0) rq_tasks(R, F, F, nb, Qb, ld, Zb, ld, 0, (F + 7) / 8);
+    __syncthreads();
+    t_rq += clock64() - t1;
+    if (r == rounds) break;
+  }
+  if (threadIdx.x == 0 && blockIdx.x < 64) {
+    long long* g = g_oic_prof + blockIdx.x * 8;
+    g[0] = t_wait; g[1] = t_app; g[2] = t_fac; g[3] = t_form; g[4] = t_sync; g[5] = t_rq;
+  }
+  // Q out; H = Q^T (R Q) by column blocks, symmetrised like the oracle.
+  double* Qo = Qall + (size_t)b * F * k;
+  double* H = Hall + (size_t)b * k * k;
+  for (int t = threadIdx.x; t < F * nb; t += blockDim.x) {
+    const int j = t / F, i = t % F;
+    Qo[(size_t)(c0 + j) * F + i] = Qb[j * ld + i];
+  }
+  cluster_sync_all();
+  if (nb > 0) warp_gemm_tn(k, nb, F, Qo, F, Zb, ld, H + (size_t)c0 * k, k);
+  cluster_sync_all();
+  for (int t = threadIdx.x; t < k * nb; t += blockDim.x) {
+    const int i = t % k, j = c0 + t / k;
+    if (i >= j) continue;
+    const double sv = 0.5 * (__ldcg(H + (size_t)j * k + i) + __ldcg(H + (size_t)i * k + j));
+    H[(size_t)j * k + i] = sv;
+    H[(size_t)i * k + j] = sv;
+  }
+}
+
 }  // namespace
 
 
@@ -1195,9 +1615,89 @@ static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int r
                                 work, scr, ss, in_smem);
 }
 
+// Column-distributed OI (k_oi_cluster): B columns per CTA, cs = ceil(k / B)
+// CTAs per axis in one cluster (up to 16, the non-portable maximum).
+template <int MAXR, int B>
+static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, int rounds,
+                                     const double* R, const double* start, double* Q, double* H,
+                                     bool* launched) {
+  *launched = false;
+  const int cs = (k + B - 1) / B;
+  constexpr int PW = QrPanel<MAXR>::PW;
+  const size_t smem =
+      ((size_t)3 * odd_ld(F) * B + B * B + (B > PW ? qr_scratch(B, B) : 0)) * sizeof(double);
+  const void* fn = (const void*)k_oi_cluster<MAXR, B>;
+  if (smem > smem_room(fn)) return cudaSuccess;
+  cudaError_t e = set_smem_attr(fn, smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return cudaSuccess;
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(nbatch * cs);
+  cfg.blockDim = dim3(kOiThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k_oi_cluster<MAXR, B>, &cfg) != cudaSuccess ||
+      nclusters < 1) {
+    cudaGetLastError();
+    return cudaSuccess;
+  }
+  static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "dmcg: k_oi_cluster F=%d k=%d B=%d cluster %d smem %zu (max active %d)\n", F,
+            k, B, cs, smem, nclusters);
+  e = cudaLaunchKernelEx(&cfg, k_oi_cluster<MAXR, B>, F, k, rounds, R, start, Q, H);
+  *launched = e == cudaSuccess;
+  if (dbg && e == cudaSuccess) {
+    long long h[64 * 8];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_oic_prof, sizeof(h));
+    for (int c = 0; c < cs && c < 64; ++c)
+      fprintf(stderr, "  cta %d: wait %lld apply %lld factor %lld form %lld sync %lld rq %lld\n", c,
+              h[8 * c], h[8 * c + 1], h[8 * c + 2], h[8 * c + 3], h[8 * c + 4], h[8 * c + 5]);
+  }
+  return e;
+}
+
+template <int MAXR>
+static cudaError_t oi_cluster_dispatch(cudaStream_t s, int nbatch, int F, int k, int rounds,
+                                       const double* R, const double* start, double* Q, double* H,
+                                       bool* launched) {
+  *launched = false;
+  if (k <= 0 || k >= F) return cudaSuccess;
+  if ((k + 7) / 8 <= 16)
+    return oi_cluster_launch<MAXR, 8>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
+  if ((k + 15) / 16 <= 16)
+    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
+  return cudaSuccess;
+}
+
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
                             const double* start, double* Q, double* H, double* work, double* scr) {
   if (F > 512) return cudaErrorInvalidValue;
+  static const bool legacy = getenv("DMCG_OI_LEGACY") != nullptr;
+  if (!legacy) {
+    bool done = false;
+    cudaError_t e = cudaSuccess;
+    if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
+    else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
+    else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
+    else e = oi_cluster_dispatch<16>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
+    if (e != cudaSuccess || done) return e;
+  }
   if (F <= 64) return oi_fused_impl<2>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);
   if (F <= 128) return oi_fused_impl<4>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);
   if (F <= 256) return oi_fused_impl<8>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);

@@ -302,10 +302,12 @@ def test_overlapped_analysis_is_used_once_and_only_for_its_mesh(codec):
     assert x2[0].shape == (s2.n, s2.F)
 
 
-def test_single_cta_oi_fallback_matches():
-    """The one-CTA-per-axis OI path (used when no cluster of 8 fits) gives the
-    same basis as the cluster path to rounding (subprocess: the override is
-    read once per process)."""
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_oi_paths_agree(name):
+    """The three OI kernels give the same basis to rounding: the column-
+    distributed k_oi_cluster (default), the row-split k_oi_fused with a cluster
+    of 8 (DMCG_OI_LEGACY) and its one-CTA fallback (DMCG_OI_CLUSTER=1).
+    Subprocesses: the switches are read once per process."""
     import os
     import subprocess
     import sys
@@ -313,19 +315,21 @@ def test_single_cta_oi_fallback_matches():
     code = (
         "import sys, numpy as np; sys.path[:0] = ['.', 'oracle'];"
         "from paper_2111_10105_b200 import codec as C, synth;"
-        "s = synth.CONFIGS['c1']; q = s.make(); cd = C.Codec(0);"
+        f"s = synth.CONFIGS['{name}']; q = s.make(); cd = C.Codec(0);"
         "g = cd.encode(q, C.EncoderConfig(k_l=s.k, row_bits=[s.bits]*s.k, oi_rounds=s.rounds));"
         "np.save(sys.argv[1], np.stack([g.dict_q[a][:8] for a in range(3)]))")
     outs = []
-    for cs in ("1", "8"):
-        path = f"/tmp/dmcg_oi_cs{cs}.npy"
-        env = dict(os.environ, DMCG_OI_CLUSTER=cs)
+    for tag, extra in (("dist", {}), ("rows8", {"DMCG_OI_LEGACY": "1"}),
+                       ("one", {"DMCG_OI_LEGACY": "1", "DMCG_OI_CLUSTER": "1"})):
+        path = f"/tmp/dmcg_oi_{name}_{tag}.npy"
+        env = dict(os.environ, **extra)
         r = subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env,
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path).astype(np.int64))
-    # the 8 leading dictionary columns (well separated on c1) agree to +-1 level
+    # the 8 leading dictionary columns (well separated) agree to +-1 level
     assert np.abs(outs[0] - outs[1]).max() <= 1
+    assert np.abs(outs[0] - outs[2]).max() <= 1
 
 
 @pytest.mark.parametrize("name", ["c0", "c1"])
