@@ -1325,6 +1325,291 @@ __device__ void blk_apply(const double* Vb, int ldv, int nb, const double* T, bo
   blk_update<B>(Vb, ldv, nb, Yb, ldy, nc, M, W);
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster Jacobi for matrices too large for one CTA's shared memory
+// (k_jacobi_cluster, m2 = 2h <= 256): the parallel cyclic Jacobi of k_jacobi
+// with the columns of A and V distributed over the cs CTAs of a cluster.
+// Pairs follow the round-robin (circle) tournament: pair i is (top[i],
+// bot[i]); CTA q owns pairs [q P, (q+1) P) and the 2P columns of A and V in
+// those slots.  A step:
+//   1. each CTA computes the rotations of its own pairs (their 2 x 2 blocks
+//      are local) and writes them into every CTA's parameter table (DSMEM);
+//      cluster barrier;
+//   2. rows p, q of every own column rotate by pair (p, q), then the own
+//      pairs' columns of A and V; the rotated 2 x 2 blocks get the tangent
+//      formulas and exact zeros (same formulas as k_jacobi);
+//   3. the tournament moves one column to each neighbouring CTA (pushed into
+//      its inbox over DSMEM); cluster barrier; inboxes land in the buffers
+//      the outgoing columns freed.
+// A sweep is 2h - 1 steps.  Convergence: the k_jacobi threshold test on every
+// off-diagonal entry, each CTA on its own columns (the diagonal is gathered
+// into every CTA first), OR-ed through DSMEM.
+// ---------------------------------------------------------------------------
+constexpr int kJcThreads = 256;
+constexpr int kJcMaxH = 128;
+constexpr int kJcMaxP = 32;  // pairs per CTA
+
+struct JcShared {
+  double c[kJcMaxH], s[kJcMaxH], t[kJcMaxH], app[kJcMaxH], aqq[kJcMaxH], apq[kJcMaxH];
+  double diag[2 * kJcMaxH];
+  int p[kJcMaxH], q[kJcMaxH], on[kJcMaxH];
+  int slot_buf[2 * kJcMaxP];  // local slot -> column buffer
+  int slot_col[2 * kJcMaxP];  // local slot -> logical column
+  int in_col[2];              // logical column arriving in inbox 0 (left) / 1 (right)
+  int out_buf[2];             // buffers leaving to the right / left (-1: none)
+  int hot;
+  double fro2;
+  double red[33];
+};
+
+__global__ void __launch_bounds__(kJcThreads)
+    k_jacobi_cluster(int m, const double* __restrict__ Aall, double* Vall, double* wall,
+                     int* flags) {
+  extern __shared__ double dyn[];
+  __shared__ JcShared sh;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  const int b = blockIdx.x / cs;
+  const int m2 = m + (m & 1), h = m2 / 2, P = h / cs, P0 = q * P;
+  const int nslot = 2 * P, tid = threadIdx.x, NT = blockDim.x;
+  // column buffer j (A then V, m2 doubles each); buffers nslot, nslot + 1 are
+  // the inboxes (from the left / right neighbour)
+  auto Acol = [&](int j) { return dyn + (size_t)j * 2 * m2; };
+  auto Vcol = [&](int j) { return dyn + (size_t)j * 2 * m2 + m2; };
+  const double* Ain = Aall + (size_t)b * m * m;
+  for (int s = tid; s < nslot; s += NT) {  // initial pairs (2i, 2i + 1)
+    const int i = P0 + (s < P ? s : s - P);
+    sh.slot_buf[s] = s;
+    sh.slot_col[s] = s < P ? 2 * i : 2 * i + 1;
+  }
+  if (tid == 0) {
+    sh.fro2 = 0.0;
+    sh.hot = 0;
+  }
+  __syncthreads();
+  double part = 0.0;
+  for (int t = tid; t < nslot * m2; t += NT) {
+    const int s = t / m2, r = t % m2, c = sh.slot_col[s];
+    const double v = (r < m && c < m) ? Ain[(size_t)c * m + r] : 0.0;
+    Acol(s)[r] = v;
+    Vcol(s)[r] = (r == c) ? 1.0 : 0.0;
+    part += v * v;
+  }
+  part = block_sum(part, sh.red);
+  cluster_sync_all();
+  if (tid == 0)
+    for (int r = 0; r < cs; ++r) atomicAdd(&cl.map_shared_rank(&sh, r)->fro2, part);
+  cluster_sync_all();
+  const double abs_thresh = sqrt(sh.fro2) * 1e-22 + DBL_MIN;
+  bool converged = (m2 <= 1);
+  int sweep = 0;
+  for (; sweep < 60 && !converged; ++sweep) {
+    int any = 0;
+    for (int step = 0; step + 1 < m2; ++step) {
+      // 1. rotations of the own pairs -> every CTA's table
+      if (tid < P) {
+        const int i = P0 + tid;
+        const int ct = sh.slot_col[tid], cb = sh.slot_col[tid + P];
+        const bool tp = ct < cb;
+        const int p = tp ? ct : cb, qq = tp ? cb : ct;
+        const double* Ap = Acol(sh.slot_buf[tp ? tid : tid + P]);
+        const double* Aq = Acol(sh.slot_buf[tp ? tid + P : tid]);
+        const double app = Ap[p], aqq = Aq[qq], apq = Aq[p];
+        const double rel2 = 1e-34 * fabs(app) * fabs(aqq);
+        double c = 1.0, sv = 0.0, tt = 0.0;
+        int on = 0;
+        if (apq * apq > rel2 && fabs(apq) > abs_thresh) {
+          const double theta = (aqq - app) * (0.5 * __drcp_rn(apq));
+          const double at = fabs(theta);
+          if (at > 1e150)
+            tt = 0.5 * __drcp_rn(theta);
+          else
+            tt = (theta >= 0.0 ? 1.0 : -1.0) * __drcp_rn(at + sqrt(fma(theta, theta, 1.0)));
+          c = rsqrt(fma(tt, tt, 1.0));
+          sv = tt * c;
+          on = 1;
+        }
+        for (int r = 0; r < cs; ++r) {
+          JcShared* o = cl.map_shared_rank(&sh, r);
+          o->c[i] = c;
+          o->s[i] = sv;
+          o->t[i] = tt;
+          o->app[i] = app;
+          o->aqq[i] = aqq;
+          o->apq[i] = apq;
+          o->p[i] = p;
+          o->q[i] = qq;
+          o->on[i] = on;
+        }
+      }
+      cluster_sync_all();
+      int step_on = 0;
+      for (int i = tid; i < h; i += NT) step_on |= sh.on[i];
+      if (__syncthreads_or(step_on)) {  // the same answer on every CTA
+        any = 1;
+        // 2a. rows p, q of every own column
+        for (int t = tid; t < nslot * h; t += NT) {
+          const int s = t / h, i = t % h;
+          if (!sh.on[i]) continue;
+          double* A = Acol(sh.slot_buf[s]);
+          const int p = sh.p[i], qq = sh.q[i];
+          const double c = sh.c[i], sv = sh.s[i];
+          const double x = A[p], y = A[qq];
+          A[p] = c * x - sv * y;
+          A[qq] = sv * x + c * y;
+        }
+        __syncthreads();
+        // 2b. columns p, q of the own pairs (A and V)
+        for (int t = tid; t < P * m2; t += NT) {
+          const int j = t / m2, r = t % m2, i = P0 + j;
+          if (!sh.on[i]) continue;
+          const bool tp = sh.slot_col[j] == sh.p[i];
+          const int bp = sh.slot_buf[tp ? j : j + P], bq = sh.slot_buf[tp ? j + P : j];
+          const double c = sh.c[i], sv = sh.s[i];
+          double* Ap = Acol(bp);
+          double* Aq = Acol(bq);
+          const double x = Ap[r], y = Aq[r];
+          Ap[r] = c * x - sv * y;
+          Aq[r] = sv * x + c * y;
+          double* Vp = Vcol(bp);
+          double* Vq = Vcol(bq);
+          const double vx = Vp[r], vy = Vq[r];
+          Vp[r] = c * vx - sv * vy;
+          Vq[r] = sv * vx + c * vy;
+        }
+        __syncthreads();
+        // 2c. tangent formulas on the rotated 2 x 2 blocks
+        if (tid < P && sh.on[P0 + tid]) {
+          const int i = P0 + tid;
+          const bool tp = sh.slot_col[tid] == sh.p[i];
+          double* Ap = Acol(sh.slot_buf[tp ? tid : tid + P]);
+          double* Aq = Acol(sh.slot_buf[tp ? tid + P : tid]);
+          const int p = sh.p[i], qq = sh.q[i];
+          const double tt = sh.t[i], apq = sh.apq[i];
+          Ap[p] = sh.app[i] - tt * apq;
+          Aq[qq] = sh.aqq[i] + tt * apq;
+          Ap[qq] = 0.0;
+          Aq[p] = 0.0;
+        }
+      }
+      // 3. tournament: new_top[0] = top[0], new_top[1] = bot[0],
+      //    new_top[i] = top[i-1] (i >= 2), new_bot[i] = bot[i+1] (i < h-1),
+      //    new_bot[h-1] = top[h-1].
+      if (tid == 0) {
+        sh.out_buf[0] = -1;
+        sh.out_buf[1] = -1;
+        if (q < cs - 1) {  // top[P0 + P - 1] -> right neighbour's top slot 0
+          sh.out_buf[0] = sh.slot_buf[P - 1];
+          cl.map_shared_rank(&sh, q + 1)->in_col[0] = sh.slot_col[P - 1];
+        }
+        if (q > 0) {  // bot[P0] -> left neighbour's last bot slot
+          sh.out_buf[1] = sh.slot_buf[P];
+          cl.map_shared_rank(&sh, q - 1)->in_col[1] = sh.slot_col[P];
+        }
+      }
+      __syncthreads();
+      if (sh.out_buf[0] >= 0) {
+        double* dst = cl.map_shared_rank(dyn, q + 1) + (size_t)(nslot + 0) * 2 * m2;
+        const double* src = Acol(sh.out_buf[0]);
+        for (int r = tid; r < 2 * m2; r += NT) dst[r] = src[r];
+      }
+      if (sh.out_buf[1] >= 0) {
+        double* dst = cl.map_shared_rank(dyn, q - 1) + (size_t)(nslot + 1) * 2 * m2;
+        const double* src = Acol(sh.out_buf[1]);
+        for (int r = tid; r < 2 * m2; r += NT) dst[r] = src[r];
+      }
+      cluster_sync_all();
+      // inboxes: from the left into the buffer the right-going column freed
+      // (the last CTA has none: the left-going one), and vice versa
+      const int ob_r = sh.out_buf[0], ob_l = sh.out_buf[1];
+      const int dst_left = ob_r >= 0 ? ob_r : ob_l, dst_right = ob_l >= 0 ? ob_l : ob_r;
+      if (q > 0) {
+        const double* src = dyn + (size_t)(nslot + 0) * 2 * m2;
+        double* dst = Acol(dst_left);
+        for (int r = tid; r < 2 * m2; r += NT) dst[r] = src[r];
+      }
+      if (q < cs - 1) {
+        const double* src = dyn + (size_t)(nslot + 1) * 2 * m2;
+        double* dst = Acol(dst_right);
+        for (int r = tid; r < 2 * m2; r += NT) dst[r] = src[r];
+      }
+      if (tid == 0) {
+        int nb[2 * kJcMaxP], nc[2 * kJcMaxP];
+        for (int s = 0; s < P; ++s) {  // tops
+          const int g = P0 + s;
+          if (g == 0) {
+            nb[s] = sh.slot_buf[0];
+            nc[s] = sh.slot_col[0];
+          } else if (g == 1) {
+            nb[s] = sh.slot_buf[P];
+            nc[s] = sh.slot_col[P];
+          } else if (s == 0) {
+            nb[s] = dst_left;
+            nc[s] = sh.in_col[0];
+          } else {
+            nb[s] = sh.slot_buf[s - 1];
+            nc[s] = sh.slot_col[s - 1];
+          }
+        }
+        for (int s = 0; s < P; ++s) {  // bots
+          const int g = P0 + s;
+          if (g == h - 1) {
+            nb[P + s] = sh.slot_buf[P - 1];
+            nc[P + s] = sh.slot_col[P - 1];
+          } else if (s == P - 1) {
+            nb[P + s] = dst_right;
+            nc[P + s] = sh.in_col[1];
+          } else {
+            nb[P + s] = sh.slot_buf[P + s + 1];
+            nc[P + s] = sh.slot_col[P + s + 1];
+          }
+        }
+        for (int s = 0; s < nslot; ++s) {
+          sh.slot_buf[s] = nb[s];
+          sh.slot_col[s] = nc[s];
+        }
+      }
+      __syncthreads();
+    }
+    converged = !any;
+    if (!converged) {
+      // a sweep that rotated: converged iff no off-diagonal entry is above
+      // its threshold now (k_jacobi's direct test)
+      for (int s = tid; s < nslot; s += NT) {
+        const int c = sh.slot_col[s];
+        const double d = Acol(sh.slot_buf[s])[c];
+        for (int r = 0; r < cs; ++r) cl.map_shared_rank(&sh, r)->diag[c] = d;
+      }
+      if (tid == 0) sh.hot = 0;
+      cluster_sync_all();
+      int hot = 0;
+      for (int t = tid; t < nslot * m2; t += NT) {
+        const int s = t / m2, r = t % m2, c = sh.slot_col[s];
+        if (r == c) continue;
+        const double arc = Acol(sh.slot_buf[s])[r];
+        const double rel = 1e-17 * sqrt(fabs(sh.diag[r]) * fabs(sh.diag[c]));
+        if (fabs(arc) > (rel > abs_thresh ? rel : abs_thresh)) hot = 1;
+      }
+      hot = __syncthreads_or(hot);
+      if (tid == 0 && hot)
+        for (int r = 0; r < cs; ++r) atomicOr(&cl.map_shared_rank(&sh, r)->hot, 1);
+      cluster_sync_all();
+      converged = !sh.hot;
+      cluster_sync_all();  // every CTA has read hot before the next reset
+    }
+  }
+  if (threadIdx.x == 0 && q == 0 && b < 8) g_jacobi_sweeps[b] = sweep;
+  double* Vo = Vall + (size_t)b * m * m;
+  double* wo = wall + (size_t)b * m;
+  for (int t = tid; t < nslot * m2; t += NT) {
+    const int s = t / m2, r = t % m2, c = sh.slot_col[s];
+    if (c < m && r < m) Vo[(size_t)c * m + r] = Vcol(sh.slot_buf[s])[r];
+    if (c < m && r == 0) wo[c] = Acol(sh.slot_buf[s])[c];
+  }
+  if (!converged && tid == 0 && q == 0) atomicOr(flags, 1);
+}
+
 __device__ long long g_oic_prof[64 * 8];  // per-CTA cycle split of k_oi_cluster (DMCG_DEBUG)
 
 template <int MAXR, int B>
@@ -1516,7 +1801,8 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
   const size_t abytes = (size_t)m2 * (m2 + 1) * sizeof(double);
   const size_t room = smem_room((const void*)k_jacobi);
   int nsplit = 0;
-  for (int sp = 1; sp <= 8 && abytes < room; sp *= 2) {
+  static const bool force_cluster = getenv("DMCG_JACOBI_CLUSTER") != nullptr;  // tests
+  for (int sp = 1; sp <= 8 && abytes < room && !force_cluster; sp *= 2) {
     const int vr = (m2 + sp - 1) / sp;
     if (abytes + (size_t)m2 * vr * sizeof(double) <= room) {
       nsplit = sp;
@@ -1540,6 +1826,45 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
       for (int i = 0; i < sw[0] && i < 64; ++i) fprintf(stderr, "  sweep %d: %lld cycles\n", i, cy[i]);
     }
   } else {
+    // A does not fit one CTA: the cluster kernel (columns of A and V spread
+    // over the cluster), else the global-memory fallback.
+    static const bool legacy = getenv("DMCG_JACOBI_LEGACY") != nullptr;
+    const int h = m2 / 2;
+    int cs = 0;
+    for (int c = 8; c >= 2 && !legacy; c /= 2)
+      if (h % c == 0 && h / c >= 2 && h / c <= kJcMaxP && h <= kJcMaxH) {
+        cs = c;
+        break;
+      }
+    if (cs > 0) {
+      const size_t smem = (size_t)(2 * (h / cs) + 2) * 2 * m2 * sizeof(double);
+      const void* fn = (const void*)k_jacobi_cluster;
+      if (smem <= smem_room(fn) && set_smem_attr(fn, smem) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(nbatch * cs);
+        cfg.blockDim = dim3(kJcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_jacobi_cluster, m, A, V, w, flags);
+        static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
+        if (dbg && e == cudaSuccess) {
+          int sw[8] = {};
+          cudaStreamSynchronize(s);
+          cudaMemcpyFromSymbol(sw, g_jacobi_sweeps, sizeof(sw));
+          fprintf(stderr, "dmcg: k_jacobi_cluster m=%d cluster %d sweeps %d %d %d\n", m, cs, sw[0],
+                  sw[1], sw[2]);
+        }
+        return e;
+      }
+      cudaGetLastError();
+    }
     k_jacobi<<<dim3(nbatch, 1), kJacThreads, 0, s>>>(m, A, work, V, w, flags, 0, m2);
   }
   return cudaGetLastError();

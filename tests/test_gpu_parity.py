@@ -124,6 +124,24 @@ def test_config2_parity_f32(codec):
     check_parity(codec, s, spec, f32_out=True)
 
 
+def test_cluster_jacobi_full_eigenbasis_parity():
+    """k_jacobi_cluster (the distributed Jacobi used when the matrix does not
+    fit one CTA) on the reference's full-eigenbasis path, forced at F = 64 and
+    checked with the full parity contract (subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path[:0] = ['tests', '.', 'oracle'];"
+            "import test_gpu_parity as T;"
+            "from paper_2111_10105_b200 import codec as C, synth;"
+            "spec = synth.CONFIGS['c0']; cd = C.Codec(0);"
+            "T.check_parity(cd, spec.make(), spec, rounds=0); print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=600, env=dict(os.environ, DMCG_JACOBI_CLUSTER="1"))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
 def test_full_eigenbasis_mode_matches_reference_path(codec):
     """oi_rounds = 0 is the reference's own n_b = 1 path (codec.cpp:158-159)."""
     spec = synth.CONFIGS["c0"]
@@ -320,7 +338,8 @@ def test_oi_paths_agree(name):
         "np.save(sys.argv[1], np.stack([g.dict_q[a][:8] for a in range(3)]))")
     outs = []
     for tag, extra in (("dist", {}), ("rows8", {"DMCG_OI_LEGACY": "1"}),
-                       ("one", {"DMCG_OI_LEGACY": "1", "DMCG_OI_CLUSTER": "1"})):
+                       ("one", {"DMCG_OI_LEGACY": "1", "DMCG_OI_CLUSTER": "1"}),
+                       ("jacc", {"DMCG_JACOBI_CLUSTER": "1"})):
         path = f"/tmp/dmcg_oi_{name}_{tag}.npy"
         env = dict(os.environ, **extra)
         r = subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env,
@@ -330,6 +349,7 @@ def test_oi_paths_agree(name):
     # the 8 leading dictionary columns (well separated) agree to +-1 level
     assert np.abs(outs[0] - outs[1]).max() <= 1
     assert np.abs(outs[0] - outs[2]).max() <= 1
+    assert np.abs(outs[0] - outs[3]).max() <= 1   # cluster Jacobi (Rayleigh-Ritz)
 
 
 @pytest.mark.parametrize("name", ["c0", "c1"])
