@@ -71,6 +71,14 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
                "r"(pred ? 8 : 0));
 }
+__device__ __forceinline__ void cp_async_el(double* smem, const double* gmem, bool pred) {
+  cp_async8(smem, gmem, pred);
+}
+__device__ __forceinline__ void cp_async_el(float* smem, const float* gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(pred ? 4 : 0));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -81,7 +89,16 @@ template <class LA, class LB, class EP>
 __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int n0, int kbeg,
                                                 int kend, int split, const LA& la, const LB& lb,
                                                 const EP& ep) {
-  GemmSmemAsync& sm = gemm_smem_async();
+  // operand element types (double, or float upcast when fragments load):
+  // the ring is declared for doubles and reinterpreted for narrower types
+  using TA = std::remove_cv_t<std::remove_pointer_t<decltype(la.addr(0, 0, 0))>>;
+  using TB = std::remove_cv_t<std::remove_pointer_t<decltype(lb.addr(0, 0, 0))>>;
+  GemmSmemAsync& smd = gemm_smem_async();
+  struct Ring {
+    TA (*As)[kABK][kBM + 4];
+    TB (*Bs)[kABK][kBN + 4];
+  } sm{reinterpret_cast<TA(*)[kABK][kBM + 4]>(smd.As),
+       reinterpret_cast<TB(*)[kABK][kBN + 4]>(smd.Bs)};
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int wm = w >> 1, wn = w & 1;
   WarpTile wt;
@@ -91,8 +108,8 @@ __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int
     for (int j = 0; j < 4; ++j) wt.acc[i][j][0] = wt.acc[i][j][1] = 0.0;
   const int nk = kend > kbeg ? (kend - kbeg + kABK - 1) / kABK : 0;
   if (nk > 0) {
-    const double* adummy = la.addr(b, kbeg, m0);
-    const double* bdummy = lb.addr(b, kbeg, n0);
+    const TA* adummy = la.addr(b, kbeg, m0);
+    const TB* bdummy = lb.addr(b, kbeg, n0);
     auto issue = [&](int it) {
       const int buf = it % kAStages, kt = kbeg + it * kABK;
 #pragma unroll
@@ -107,7 +124,7 @@ __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int
           k = e / kBM;
         }
         const bool ok = kt + k < kend && m0 + m < M;
-        cp_async8(&sm.As[buf][k][m], ok ? la.addr(b, kt + k, m0 + m) : adummy, ok);
+        cp_async_el(&sm.As[buf][k][m], ok ? la.addr(b, kt + k, m0 + m) : adummy, ok);
         int kb, nb;
         if (LB::kKContig) {
           kb = e % kABK;
@@ -117,7 +134,7 @@ __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int
           kb = e / kBN;
         }
         const bool okb = kt + kb < kend && n0 + nb < N;
-        cp_async8(&sm.Bs[buf][kb][nb], okb ? lb.addr(b, kt + kb, n0 + nb) : bdummy, okb);
+        cp_async_el(&sm.Bs[buf][kb][nb], okb ? lb.addr(b, kt + kb, n0 + nb) : bdummy, okb);
       }
     };
 #pragma unroll
@@ -136,9 +153,9 @@ __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int
         const int kr = kk * 4 + (lane & 3);
         double a[4], bb[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sm.As[buf][kr][wm * 32 + i * 8 + (lane >> 2)];
+        for (int i = 0; i < 4; ++i) a[i] = (double)sm.As[buf][kr][wm * 32 + i * 8 + (lane >> 2)];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bb[j] = sm.Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2)];
+        for (int j = 0; j < 4; ++j) bb[j] = (double)sm.Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2)];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -262,6 +279,9 @@ struct LoadDense {
   __device__ __forceinline__ double operator()(int b, int k, int i) const {
     return (double)p[b * sb + (long)k * sk + (long)i * si];
   }
+  __device__ __forceinline__ const T* addr(int b, int k, int i) const {
+    return p + b * sb + (long)k * sk + (long)i * si;
+  }
 };
 
 // Per-batch pointer table variant (independent axis buffers).
@@ -275,6 +295,9 @@ struct LoadDense3 {
   __device__ __forceinline__ double operator()(int b, int k, int i) const {
     const T* p = b == 0 ? p0 : (b == 1 ? p1 : p2);
     return (double)p[(long)k * sk + (long)i * si];
+  }
+  __device__ __forceinline__ const T* addr(int b, int k, int i) const {
+    return (b == 0 ? p0 : (b == 1 ? p1 : p2)) + (long)k * sk + (long)i * si;
   }
 };
 
