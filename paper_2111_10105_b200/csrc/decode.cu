@@ -27,6 +27,42 @@ __global__ void k_row_params(int rows, const float* rmin, const float* rmax, con
   rowp[2 * t + 1] = q.degenerate ? 0.0 : q.width;
 }
 
+// dequantize_rows (codec.cpp:267-288) of all 3 k retained rows into f64
+// (row r of axis a at out[(a k + r) n]); a level beyond 2^bits flags a
+// corrupt payload.  Memory-bound pre-pass of the reconstruction GEMM, which
+// then streams plain f64 tiles through its cp.async ring.
+__global__ void k_dequant_rows(int n, const uint16_t* __restrict__ q, const double* __restrict__ rowp,
+                               const uint8_t* __restrict__ rbits, int* flags,
+                               double* __restrict__ out) {
+  const long row = blockIdx.y;
+  const double min_ = rowp[2 * row], width = rowp[2 * row + 1];
+  const uint32_t levels = 1u << rbits[row];
+  const uint16_t* qr = q + row * n;
+  double* o = out + row * n;
+  bool bad = false;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t lv = qr[i];
+    bad |= width != 0.0 && lv >= levels;
+    o[i] = width == 0.0 ? min_ : dequantize_level(min_, width, false, lv);
+  }
+  if (bad) atomicOr(flags, 1);
+}
+
+// decode_dictionaries (codec.cpp:330-349): columns r < k of U~ over the
+// frame window [f0, f0 + Fw) -> out[(a k + r) Fw + f].
+__global__ void k_dequant_dict(int F, int k, int f0, int Fw, const uint16_t* __restrict__ q,
+                               double width, uint32_t levels, int* flags, double* __restrict__ out) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long total = 3L * k * Fw;
+  if (t >= total) return;
+  const int f = (int)(t % Fw);
+  const long ar = t / Fw;  // a k + r
+  const int a = (int)(ar / k), r = (int)(ar % k);
+  const uint32_t lv = q[((long)a * F + r) * F + f0 + f];
+  if (lv >= levels) atomicOr(flags, 1);
+  out[t] = dequantize_level(-1.0, width, false, lv);
+}
+
 // rhs = L^T delta~ + S^T a  (solver.cpp:77-80).  One thread per (row,
 // column block); Laplacian values implicit; anchors dequantised on the fly
 // (anchor_matrix, codec.cpp:174-195).
@@ -291,6 +327,24 @@ cudaError_t launch_row_params(cudaStream_t s, int rows, const float* rmin, const
                               const uint8_t* rbits, double* rowp) {
   if (rows <= 0) return cudaSuccess;
   k_row_params<<<(rows + 255) / 256, 256, 0, s>>>(rows, rmin, rmax, rbits, rowp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_rows(cudaStream_t s, int rows, int n, const uint16_t* q,
+                                const double* rowp, const uint8_t* rbits, int* flags, double* out) {
+  if (rows <= 0 || n <= 0) return cudaSuccess;
+  const int bx = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
+  k_dequant_rows<<<dim3(bx, rows), 256, 0, s>>>(n, q, rowp, rbits, flags, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dequant_dict(cudaStream_t s, int F, int k, int f0, int Fw, const uint16_t* q,
+                                int bits, int* flags, double* out) {
+  const long total = 3L * k * Fw;
+  if (total <= 0) return cudaSuccess;
+  const uint32_t levels = 1u << bits;
+  k_dequant_dict<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(F, k, f0, Fw, q, 2.0 / (double)levels,
+                                                               levels, flags, out);
   return cudaGetLastError();
 }
 

@@ -694,6 +694,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   p->d_rm_y = (double*)get(nW * 8);
   p->d_rm_xp = (double*)get(nW * 8);
   p->d_rm_r = (double*)get(nW * 8);
+  p->d_Ud = (double*)get(3 * (size_t)std::max<uint32_t>(p->k, 1) * p->F * 8);
   CholDev& cd = p->cdev;
   cd.n = n;
   cd.nsup = cp.nsup;

@@ -205,6 +205,7 @@ struct dmcg_plan {
   uint16_t* d_anchor_q = nullptr;  // 3 x n_c x F
   // decode
   double* d_rowp = nullptr;        // 3 x k x 2 (min_, width) dequantiser params
+  double* d_Ud = nullptr;          // 3 x k x F dequantised dictionary columns (decode)
   uint32_t* d_stream = nullptr;    // device DMC1 image for dmcg_plan_serialize
   double* d_metric = nullptr;      // 3 n F + F + F + n doubles (dmcg_plan_distortion)
   size_t stream_cap = 0;

@@ -78,6 +78,13 @@ cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count);
 // Dequantiser parameters per retained row (QParams of quantize.cpp:15-20).
 cudaError_t launch_row_params(cudaStream_t s, int k, const float* rmin, const float* rmax,
                               const uint8_t* rbits, double* rowp);
+// dequantize_rows of the 3 k retained rows (q: 3k x n levels) into f64 out
+// (3k x n); decode_dictionaries of U~[:, :k] over frames [f0, f0 + Fw) into
+// out (3 x k x Fw).  flags |= 1 on a level out of range (CorruptPayload).
+cudaError_t launch_dequant_rows(cudaStream_t s, int rows, int n, const uint16_t* q,
+                                const double* rowp, const uint8_t* rbits, int* flags, double* out);
+cudaError_t launch_dequant_dict(cudaStream_t s, int F, int k, int f0, int Fw, const uint16_t* q,
+                                int bits, int* flags, double* out);
 // rhs = L^T delta~ + S^T a (solver.cpp:77-80) in the CG column-block layout.
 cudaError_t launch_rhs(cudaStream_t s, int n, int F, int W, int nblk, const uint32_t* lap_rp,
                        const uint32_t* lap_ci, const int32_t* anchor_pos, int n_c,

@@ -483,9 +483,15 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
   DMCG_TRY(cudaStreamWaitEvent(s, p->ev_fork, 0));
   if (k > 0) {
     DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
-    LoadCoeffDeq la{p->d_coeff_q, p->d_rowp, p->d_row_bits, p->d_flags + 1, n, k};
-    const uint32_t levels = 1u << p->dict_bits;
-    LoadDictDeq lb{p->d_dict_q, 2.0 / (double)levels, levels, F_all, p->d_flags + 1, f0};
+    // dequantised coefficients (3 k x n, into the encode's coefficient
+    // buffer) and U~[:, :k] over the window, then a plain f64 GEMM
+    double* Cd = p->d_C;
+    double* Ud = p->d_Ud;
+    DMCG_TRY(launch_dequant_rows(s, 3 * k, n, p->d_coeff_q, p->d_rowp, p->d_row_bits,
+                                 p->d_flags + 1, Cd));
+    DMCG_TRY(launch_dequant_dict(s, F_all, k, f0, F, p->d_dict_q, p->dict_bits, p->d_flags + 1, Ud));
+    LoadDense<double, false> la{Cd, (long)k * n, (long)n, 1L};   // A(r, i) = c~(r, i)
+    LoadDense<double, false> lb{Ud, (long)k * F, (long)F, 1L};   // B(r, f) = U~(f0 + f, r)
     // delta~ (i, a*F + f): batch b = axis, rows = vertices, cols = frames
     DMCG_TRY(launch_gemm(s, 3, n, F, k, 1, la, lb,
                          StoreStrided{p->d_rm_delta, (long)F, (long)W, 1L}));
