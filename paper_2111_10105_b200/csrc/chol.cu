@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <vector>
 #include "gemm.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace dmcg {
 
@@ -98,11 +100,13 @@ __global__ void __launch_bounds__(256) k_assemble(CholDev d, const uint32_t* lsu
   }
 }
 
-// Panel [k0, k0 + pw) of a front: the CTA factors the pw x pw diagonal
-// block in shared memory (one barrier per pivot), then every thread solves
-// its own rows of the panel below against it (row-wise TRSM, no barriers).
-// Pivots are applied as reciprocal square roots (the CPU reference divides
-// by the square root; results agree to rounding).
+// Panel [k0, k0 + pw) of a front: warp 0 factors the pw x pw diagonal block
+// in registers (left-looking, lane = row, shuffles instead of barriers),
+// then every thread solves rows of the panel below against it (row-wise
+// TRSM).  The rows below are split over a cluster of up to 8 CTAs per front
+// (grid.y); each refactors the small block, and one cluster barrier keeps
+// rank 0's write-back after every rank's read.  Pivots are applied as reciprocal square roots (the CPU
+// reference divides by the square root; results agree to rounding).
 constexpr int kPanelThreads = 256;  // 32 panel values per thread stay in registers
 constexpr int kNB = 32;
 
@@ -115,51 +119,49 @@ __global__ void __launch_bounds__(kPanelThreads)
   if (k0 >= w) return;
   const int pw = min(nb, w - k0);
   double* A = d.F + d.front_off[s];
-  {  // the kNB x kNB diagonal block: all loads of a thread issued together
-    constexpr int kPer = kNB * kNB / kPanelThreads;
-    double v[kPer];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  cg::cluster_group cl = cg::this_cluster();
+  const int ny = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  if (warp == 0) {
+    // Right-looking Cholesky of the kNB x kNB diagonal block in registers,
+    // redundantly in every CTA of the cluster: lane r holds row r; pivot j's
+    // column is broadcast by independent shuffles (no barrier, no chain).
+    double a[kNB];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int t = threadIdx.x + u * kPanelThreads, c = t / kNB, r = t % kNB;
-      v[u] = (r < pw && c < pw && r >= c) ? A[(size_t)(k0 + c) * m + k0 + r] : 0.0;
-    }
+    for (int c = 0; c < kNB; ++c)
+      a[c] = (lane < pw && c < pw && c <= lane) ? A[(size_t)(k0 + c) * m + k0 + lane] : 0.0;
+    bool bad = false;
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int t = threadIdx.x + u * kPanelThreads, c = t / kNB, r = t % kNB;
-      D[r][c] = v[u];
+    for (int j = 0; j < kNB; ++j) {
+      const double djj = __shfl_sync(0xffffffffu, a[j], j);
+      const double ip = rsqrt(fmax(djj, DBL_MIN));
+      if (j < pw && !(djj > 0.0)) bad = true;
+      const double lj = lane > j ? a[j] * ip : (lane == j ? djj * ip : 0.0);
+      a[j] = lj;
+      if (lane == 0 && j < pw) dinv[j] = ip;
+#pragma unroll
+      for (int c = j + 1; c < kNB; ++c) a[c] = fma(-lj, __shfl_sync(0xffffffffu, lj, c), a[c]);
     }
+    if (bad && lane == 0 && rank == 0) atomicOr(d.flags, 1);
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) D[lane][c] = c <= lane ? a[c] : 0.0;
+    if (ny > 1) {
+      // every CTA of the cluster has read the block before rank 0 rewrites it
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+    if (rank == 0 && lane < pw)
+#pragma unroll
+      for (int c = 0; c < kNB; ++c)
+        if (c < pw && c <= lane) A[(size_t)(k0 + c) * m + k0 + lane] = a[c];
+  } else if (ny > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
   __syncthreads();
-  // Right-looking Cholesky of D with one barrier per pivot: columns stay
-  // unscaled while they are read (L(r, j) = D[r][j] / sqrt(D[j][j]) is
-  // formed on the fly) and are scaled once at the end.
-  for (int j = 0; j < pw; ++j) {
-    const double djj = D[j][j];
-    const double ip = rsqrt(fmax(djj, DBL_MIN));
-    if (threadIdx.x == 0) {
-      if (!(djj > 0.0)) atomicOr(d.flags, 1);
-      dinv[j] = ip;
-    }
-    const int rem = pw - 1 - j;
-    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
-      const int r = j + 1 + t / rem, c = j + 1 + t % rem;
-      if (c <= r) D[r][c] -= (D[r][j] * ip) * (D[c][j] * ip);
-    }
-    __syncthreads();
-  }
-  for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
-    const int c = t / pw, r = t % pw;
-    if (r > c) D[r][c] *= dinv[c];
-    if (r == c) D[r][c] = 1.0 / dinv[c];
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < pw * pw; t += blockDim.x) {
-    const int c = t / pw, r = t % pw;
-    if (r >= c) A[(size_t)(k0 + c) * m + k0 + r] = D[r][c];
-  }
   // rows below: x = a L^{-T}; column-oriented substitution so the updates
   // of one pivot are independent (ILP) instead of one long FMA chain.
-  for (int i = k0 + pw + threadIdx.x; i < m; i += blockDim.x) {
+  for (int i = k0 + pw + rank * kPanelThreads + threadIdx.x; i < m; i += ny * kPanelThreads) {
     double x[kNB];
 #pragma unroll
     for (int c = 0; c < kNB; ++c) x[c] = c < pw ? A[(size_t)(k0 + c) * m + i] : 0.0;
@@ -636,7 +638,25 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
         cudaEventCreate(&pe.back());
         cudaEventRecord(pe.back(), s);
       }
-      k_panel<<<cnt, kPanelThreads, 0, s>>>(d, ls, (int)k0, nb);
+      const uint32_t below = lv.maxm[l] > k0 ? lv.maxm[l] - k0 : 1;
+      const uint32_t ny = std::min<uint32_t>(8, (below + kPanelThreads - 1) / kPanelThreads);
+      if (ny == 1) {
+        k_panel<<<cnt, kPanelThreads, 0, s>>>(d, ls, (int)k0, nb);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = ny;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cnt, ny);
+        cfg.blockDim = dim3(kPanelThreads);
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_panel, d, ls, (int)k0, nb);
+        if (e != cudaSuccess) return e;
+      }
       if (pl) {
         pe.emplace_back();
         cudaEventCreate(&pe.back());
