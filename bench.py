@@ -40,9 +40,9 @@ from paper_2111_10105_b200.shard import (dist_env, max_over_ranks, sequence_for_
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 FP64_DMMA_TFLOPS = 37.1  # profiles/r01_peaks.md (tools/peak_fp64.cu)
-# dram__bytes_read.sum + dram__bytes_write.sum of one k_oi_fused launch (c1),
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_oi_cluster launch (c1),
 # from the ncu --set full capture in profiles/ (None until captured)
-OI_TRAFFIC = 1379328  # profiles/r01_ncu_oi_full.md
+OI_TRAFFIC = 1403136  # profiles/r01_ncu_oi_cluster_full.md
 
 WORKLOADS = {
     "c0": "c0: icosphere L4 (2562 v), F=64, k=32, 10 OI rounds, 12-bit, fp64",
@@ -265,7 +265,7 @@ def run_rows(args, rank, world, local, dist):
                        "rows_per_rank": info["n_own"], "halo_rows": info["n_halo"],
                        "frames_decoded_per_rank": f1 - f0,
                        "l2": "256 MiB flush between timed steps", "cg_rtol": args.rtol},
-            "roofline": {"kernel": "k_oi_fused", "bound": "tensor", "achieved": achieved,
+            "roofline": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
                          "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_TFLOPS, "traffic": None,
                          "algorithmic_flops": oi_flops, "ms": oi_ms,
@@ -361,8 +361,8 @@ def main():
     vf_step = s.n * s.F
     value = whole_job_rate(vf_step, world, args.steps, total_ms)
 
-    # roofline of the dominant kernel, k_oi_fused (the fused orthogonal
-    # iterations, one 8-CTA cluster per axis): algorithmic flops per launch
+    # roofline of the dominant kernel, k_oi_cluster (the fused orthogonal
+    # iterations, one cluster of k/8 CTAs per axis): algorithmic flops per launch
     # over its launch time, CUDA events around the launch on
     # the plan stream (stats.ms_oi), median over the timed steps.  The
     # decode's direct solve (K7) is reported beside it.
@@ -413,17 +413,18 @@ def main():
                        "l2": "256 MiB flush between timed steps",
                        "plan": "mesh plan (CSR, anchors, normal matrix) built once outside value; "
                                "inside e2e", "cg_rtol": args.rtol},
-            "roofline": {"kernel": "k_oi_fused", "bound": "tensor", "achieved": achieved,
+            "roofline": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
                          "peak": peak, "peak_kind": "measured FP64 DMMA, whole GPU (profiles/r01_peaks.md)",
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": OI_TRAFFIC,
-                         "launches_per_step": 1, "ctas": 24, "cluster": 8,
+                         "launches_per_step": 1, "ctas": 3 * ((spec.k + 7) // 8),
+                         "cluster": (spec.k + 7) // 8,
                          "algorithmic_flops": oi_flops, "ms": oi_sec * 1e3,
                          "share_of_step": oi_sec * 1e3 / (total_ms / args.steps),
                          "model": "3 axes x ((rounds+1) x (2F^2k + 4Fk^2 - 4k^3/3) + 2Fk^2)",
-                         "note": "one 8-CTA cluster per axis; each round's Householder QR is "
-                                 "sequential on the cluster's rank 0 (the other 7 CTAs compute "
-                                 "Z = R Q), so the ceiling is a few SMs' DMMA rate, not the "
-                                 "device peak; see DESIGN.md §5"},
+                         "note": "one cluster per axis, 8 columns of Z / Q per CTA; every OI "
+                                 "round is a wavefront of dependent block-Householder steps "
+                                 "(latency-bound on a 200 x 64 problem), so the ceiling is the "
+                                 "cluster's SMs, not the device peak; see DESIGN.md §5"},
             "roofline_k7": {"kernel": "K7 direct solve (k_panel/k_trailing/k_inv_*/k_fwd*/k_bwd*)",
                             "bound": "tensor", "achieved": k7_achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": k7_achieved / peak, "algorithmic_flops": k7_flops,
