@@ -2003,6 +2003,9 @@ static cudaError_t oi_cluster_dispatch(cudaStream_t s, int nbatch, int F, int k,
                                        bool* launched) {
   *launched = false;
   if (k <= 0 || k >= F) return cudaSuccess;
+  static const int bsel = getenv("DMCG_OI_B") ? atoi(getenv("DMCG_OI_B")) : 0;  // experiments
+  if (bsel == 16 && (k + 15) / 16 <= 16)
+    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
   if ((k + 7) / 8 <= 16)
     return oi_cluster_launch<MAXR, 8>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
   if ((k + 15) / 16 <= 16)

@@ -490,10 +490,14 @@ void dmcg_plan_destroy(dmcg_plan* p) {
   delete p;
 }
 
+// mesh_given: Laplacian structure of these faces already built (the decoder
+// reuses the encoder's, see dmcg_decode); encode_side = false skips the
+// encode-only set-up (OI start matrices).
 static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
                                const uint32_t* faces, uint32_t n_faces, const dmcg_config* cfg,
                                const uint32_t* anchors_given, uint32_t n_c_given,
-                               dmcg_plan** out) {
+                               dmcg_plan** out, MeshHost* mesh_given = nullptr,
+                               bool encode_side = true) {
   *out = nullptr;
   if (n == 0 || F == 0) return {DMCG_E_INDEX, "ValidationError: sequence is empty"};
   if (dtype != DMCG_F64 && dtype != DMCG_F32) return {DMCG_E_CONFIG, "ConfigError: bad dtype"};
@@ -505,7 +509,14 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->n_faces = n_faces;
   PhaseTimer tm("plan");
   p->faces.assign(faces, faces + 3 * (size_t)n_faces);
-  Status st = build_mesh(faces, n_faces, n, &p->mesh);
+  Status st;
+  if (mesh_given) {
+    p->mesh.n = n;
+    p->mesh.lap_rp = std::move(mesh_given->lap_rp);
+    p->mesh.lap_ci = std::move(mesh_given->lap_ci);
+  } else {
+    st = build_mesh(faces, n_faces, n, &p->mesh);
+  }
   tm.lap("mesh");
   if (st.good() && !anchors_given) st = validate_mesh(p->mesh);
   tm.lap("validate");
@@ -610,14 +621,14 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   // OI start matrices: SplitMix64 uniform in [-1, 1), column-major F x k,
   // axis a seeded with oi_seed + a (same stream as oracle orc_start_matrix).
   std::vector<double> start(3 * (size_t)F * kk, 0.0);
-  if (k > 0)
+  if (k > 0 && encode_side)
     for (int a = 0; a < 3; ++a) {
       uint64_t st64 = p->oi_seed + (uint64_t)a;
       for (size_t t = 0; t < (size_t)F * k; ++t)
         start[a * (size_t)F * k + t] = (double)(splitmix64(&st64) >> 11) * 0x1.0p-52 - 1.0;
     }
   tm.lap("events+start");
-  h2d(p->d_start, start.data(), start.size() * 8);
+  if (encode_side) h2d(p->d_start, start.data(), start.size() * 8);
   if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
   tm.lap("upload+sync");
   if (!ok) {
@@ -1166,23 +1177,28 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   cfg.anchor_bits = in->anchor_bits;
   cfg.dict_bits = in->dict_bits;
   cfg.diff_bits = in->diff_bits ? in->diff_bits : 8;
+  // The analysis started by the last dmcg_encode (normal matrix, symbolic
+  // Cholesky, and the Laplacian structure it was built from) is taken once,
+  // and only when mesh and anchors match.
+  std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
+  if (pa && !(pa->n == in->n && pa->n_faces == in->n_faces &&
+              pa->anchors.size() == in->n_c &&
+              std::equal(pa->anchors.begin(), pa->anchors.end(), in->anchor_idx) &&
+              pa->faces_hash == hash_faces(in->faces, in->n_faces)))
+    pa.reset();
+  if (pa && pa->th.joinable()) pa->th.join();
   dmcg_plan* p = nullptr;
   Status st = plan_create_impl(ctx, in->n, in->F, out_dtype, in->faces, in->n_faces, &cfg,
-                               in->anchor_idx, in->n_c, &p);
+                               in->anchor_idx, in->n_c, &p, pa ? &pa->mesh : nullptr, false);
   if (!st.good()) return ctx->set_error(st);
   PhaseTimer tm("decode");
-  if (ctx->pending) {  // analysis started by the last dmcg_encode: used once if it matches
-    std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
-    if (pa->n == in->n && pa->n_faces == in->n_faces &&
-        pa->anchors == p->mesh.anchors && pa->faces_hash == hash_faces(in->faces, in->n_faces)) {
-      if (pa->th.joinable()) pa->th.join();
-      p->mesh.m_rp = std::move(pa->mesh.m_rp);
-      p->mesh.m_ci = std::move(pa->mesh.m_ci);
-      p->mesh.m_val = std::move(pa->mesh.m_val);
-      p->chol = std::move(pa->chol);
-      p->analyze_seconds = pa->seconds;
-      p->chol_given = true;
-    }
+  if (pa) {
+    p->mesh.m_rp = std::move(pa->mesh.m_rp);
+    p->mesh.m_ci = std::move(pa->mesh.m_ci);
+    p->mesh.m_val = std::move(pa->mesh.m_val);
+    p->chol = std::move(pa->chol);
+    p->analyze_seconds = pa->seconds;
+    p->chol_given = true;
   }
   tm.lap("plan");
   st = upload_impl(p, in);
