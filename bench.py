@@ -164,7 +164,8 @@ def run_rows(args, rank, world, local, dist):
 
     spec = synth.CONFIGS[args.config]
     s = spec.make(0)
-    cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds)
+    cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds,
+                          oi_implicit=args.implicit)
     f32 = spec.dtype == "f32"
     npdt = np.float32 if f32 else np.float64
     tdt = torch.float32 if f32 else torch.float64
@@ -259,6 +260,8 @@ def run_rows(args, rank, world, local, dist):
             "vs_baseline": None, "dtype": "f64" if not f32 else "f64 (f32 storage)",
             "data": "synthetic (seeded generator, DESIGN.md §2)",
             "config": {"workload": WORKLOADS[args.config], "per_gpu": "1/N of one sequence per step",
+                       "covariance": "implicit X^T (X Q), partials allreduced per round"
+                       if args.implicit else "explicit R = X^T X (allreduced once)",
                        "parallelism": f"vertex rows x{world} (encode: NCCL allreduce of Gram "
                                       "partials + range keys, all-gather of symbols; decode: "
                                       "frame windows, replicated factor)",
@@ -298,6 +301,8 @@ def main():
     ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--implicit", action="store_true",
+                    help="implicit OI: Z = X^T (X Q) per round, R never formed")
     ap.add_argument("--rows", action="store_true",
                     help="shard one sequence by vertex rows across the ranks (SURVEY §8e)")
     args = ap.parse_args()
@@ -319,7 +324,8 @@ def main():
         return run_rows(args, rank, world, local, dist)
 
     spec, s = sequence_for_rank(args.config, rank)
-    cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds)
+    cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds,
+                          oi_implicit=args.implicit)
     f32 = spec.dtype == "f32"
     npdt = np.float32 if f32 else np.float64
     codec = C.Codec(local)
@@ -409,6 +415,8 @@ def main():
             "vs_baseline": None, "dtype": "f64" if not f32 else "f64 (f32 storage)",
             "data": "synthetic (seeded generator, DESIGN.md §2)",
             "config": {"workload": WORKLOADS[args.config], "per_gpu": "one sequence per step",
+                       "covariance": "implicit X^T (X Q) per round" if args.implicit
+                       else "explicit R = X^T X",
                        "parallelism": f"sequences x{world}, no collective",
                        "l2": "256 MiB flush between timed steps",
                        "plan": "mesh plan (CSR, anchors, normal matrix) built once outside value; "

@@ -93,6 +93,7 @@ struct EncoderConfig {  // reference codec.hpp:30-49 (+ B200 basis controls)
   bool raw_payload = false;
   int oi_rounds = 0;       // 0 = full eigenbasis (reference n_b = 1 path)
   uint64_t oi_seed = 0;
+  int oi_implicit = 0;
 };
 
 struct QuantRow {  // stream.hpp:86-93
@@ -160,6 +161,7 @@ inline CompressedAnimation encode(const MeshSequence& s, const EncoderConfig& cf
   c.raw_payload = cfg.raw_payload;
   c.oi_rounds = cfg.oi_rounds;
   c.oi_seed = cfg.oi_seed;
+  c.oi_implicit = cfg.oi_implicit;
   const uint32_t n = (uint32_t)s.n(), F = (uint32_t)s.k();
   dmcg_sizes sz;
   detail::check(dmcg_encoded_sizes(n, F, &c, &sz));

@@ -87,6 +87,12 @@ typedef struct {
    * + Rayleigh-Ritz + Householder completion (K3). */
   int oi_rounds;
   uint64_t oi_seed;         /* start matrix seed (axis a uses oi_seed + a) */
+  int oi_implicit;          /* 1: never form R = X^T X; every round computes
+                               Z = X^T (X Q) as two GEMMs over the vertex rows and
+                               H = (X Q)^T (X Q) (BASELINE config 3's "covariance
+                               applied implicitly"; on vertex-row shards the X^T (X Q)
+                               partials are allreduced every round).  Same
+                               iteration as the explicit R Q; 0 (default): form R. */
 } dmcg_config;
 
 void dmcg_config_default(dmcg_config* cfg);

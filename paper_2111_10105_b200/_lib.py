@@ -46,7 +46,8 @@ class DmcgConfig(ctypes.Structure):
                 ("dict_bits", ctypes.c_int), ("diff_bits", ctypes.c_int),
                 ("anchor_strategy", ctypes.c_int), ("seed", ctypes.c_uint64),
                 ("laplacian", ctypes.c_int), ("raw_payload", ctypes.c_int),
-                ("oi_rounds", ctypes.c_int), ("oi_seed", ctypes.c_uint64)]
+                ("oi_rounds", ctypes.c_int), ("oi_seed", ctypes.c_uint64),
+                ("oi_implicit", ctypes.c_int)]
 
 
 class DmcgDecodeOptions(ctypes.Structure):

@@ -51,6 +51,7 @@ class EncoderConfig:
     raw_payload: bool = False
     oi_rounds: int = 0             # 0 = full eigenbasis (reference n_b = 1 path)
     oi_seed: int = 0
+    oi_implicit: bool = False      # Z = X^T (X Q) per round instead of R Q (R never formed)
 
     def to_c(self):
         c = L.DmcgConfig()
@@ -64,6 +65,7 @@ class EncoderConfig:
         c.anchor_strategy, c.seed, c.laplacian = self.anchor_strategy, self.seed, self.laplacian
         c.raw_payload = int(self.raw_payload)
         c.oi_rounds, c.oi_seed = self.oi_rounds, self.oi_seed
+        c.oi_implicit = int(self.oi_implicit)
         return c
 
 

@@ -1633,7 +1633,9 @@ __global__ void __launch_bounds__(kOiThreads)
   double* Ts = Vs + (size_t)ld * B;   // and its T
   double* scr = Ts + B * B;           // wqr_factor scratch (B > PW)
   const int c0 = rank * B, nb = min(B, k - c0);
-  const double* R = Rall + (size_t)b * F * F;
+  // Rall == nullptr: QR only (Q of the start matrices, no R Q / H) — one
+  // round of the implicit X (X^T Q) iteration, whose products run as GEMMs
+  const double* R = Rall ? Rall + (size_t)b * F * F : nullptr;
   const double* S = start + (size_t)b * F * k;
   for (int t = threadIdx.x; t < F * B; t += blockDim.x) {
     const int j = t / F, i = t % F;
@@ -1718,6 +1720,7 @@ __global__ void __launch_bounds__(kOiThreads)
     t1 = clock64();
     t_sync += t1 - t0;
     // ---- Z_c = R Q_c --------------------------------------------------------
+    if (!R) break;
     if (nb > 0) rq_tasks(R, F, F, nb, Qb, ld, Zb, ld, 0, (F + 7) / 8);
     __syncthreads();
     t_rq += clock64() - t1;
@@ -1729,11 +1732,12 @@ __global__ void __launch_bounds__(kOiThreads)
   }
   // Q out; H = Q^T (R Q) by column blocks, symmetrised like the oracle.
   double* Qo = Qall + (size_t)b * F * k;
-  double* H = Hall + (size_t)b * k * k;
+  double* H = Hall ? Hall + (size_t)b * k * k : nullptr;
   for (int t = threadIdx.x; t < F * nb; t += blockDim.x) {
     const int j = t / F, i = t % F;
     Qo[(size_t)(c0 + j) * F + i] = Qb[j * ld + i];
   }
+  if (!R) return;
   cluster_sync_all();
   if (nb > 0) warp_gemm_tn(k, nb, F, Qo, F, Zb, ld, H + (size_t)c0 * k, k);
   cluster_sync_all();
@@ -2011,6 +2015,19 @@ static cudaError_t oi_cluster_dispatch(cudaStream_t s, int nbatch, int F, int k,
   if ((k + 15) / 16 <= 16)
     return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
   return cudaSuccess;
+}
+
+cudaError_t launch_qr_cluster(cudaStream_t s, int nbatch, int F, int k, const double* Z,
+                              double* Q) {
+  if (F > 512 || k <= 0 || k >= F) return cudaErrorInvalidValue;
+  bool done = false;
+  cudaError_t e = cudaSuccess;
+  if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
+  else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
+  else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
+  else e = oi_cluster_dispatch<16>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
+  if (e == cudaSuccess && !done) e = cudaErrorNotSupported;  // no cluster of this size fits
+  return e;
 }
 
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,

@@ -78,6 +78,20 @@ __global__ void k_reduce_sym(int F, int splits, int nbatch, const double* __rest
   R[b * FF + (long)g * F + f] = __dmul_rn(0.5, __dadd_rn(s1, s2));
 }
 
+// Split-K partials (row-major M x N per split and batch) summed in split
+// order into column-major out[b][n M + m] (the implicit OI's Z = X^T P).
+__global__ void k_reduce_sum(int M, int N, int splits, int nbatch, const double* __restrict__ part,
+                             double* __restrict__ out) {
+  const long MN = (long)M * N;
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (t >= MN) return;
+  const int n = (int)(t / M), m = (int)(t % M);
+  double s = 0.0;
+  for (int sp = 0; sp < splits; ++sp) s += part[((long)sp * nbatch + b) * MN + (long)m * N + n];
+  out[b * MN + t] = s;
+}
+
 // pack_matrix with UniformQuantizer(-1.0f, 1.0f, dict_bits) (codec.cpp:122-129).
 __global__ void k_quant_dict(long count, int bits, const double* __restrict__ U,
                              uint16_t* __restrict__ q) {
@@ -251,6 +265,14 @@ cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, con
   const long FF = (long)F * F;
   dim3 grid((unsigned)((FF + 255) / 256), nbatch);
   k_reduce_sym<<<grid, 256, 0, s>>>(F, splits, nbatch, part, R);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_sum(cudaStream_t s, int M, int N, int splits, int nbatch,
+                              const double* part, double* out) {
+  const long MN = (long)M * N;
+  dim3 grid((unsigned)((MN + 255) / 256), nbatch);
+  k_reduce_sum<<<grid, 256, 0, s>>>(M, N, splits, nbatch, part, out);
   return cudaGetLastError();
 }
 

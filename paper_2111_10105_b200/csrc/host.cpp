@@ -399,6 +399,7 @@ void dmcg_config_default(dmcg_config* cfg) {
   cfg->raw_payload = 0;
   cfg->oi_rounds = 0;
   cfg->oi_seed = 0;
+  cfg->oi_implicit = 0;
 }
 
 void dmcg_decode_options_default(dmcg_decode_options* o) {
@@ -528,6 +529,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->k = cfg->k_l;
   p->rounds = cfg->oi_rounds;
   p->oi_seed = cfg->oi_seed;
+  p->implicit = cfg->oi_implicit != 0;
   p->anchor_bits = cfg->anchor_bits;
   p->dict_bits = cfg->dict_bits;
   p->diff_bits = cfg->diff_bits;

@@ -169,6 +169,7 @@ struct dmcg_plan {
   int rounds = 0;
   int anchor_bits = 16, dict_bits = 16, diff_bits = 8;
   uint64_t oi_seed = 0;
+  bool implicit = false;            // dmcg_config.oi_implicit
   std::vector<int> row_bits;
   std::vector<uint32_t> faces;
   dmcg::MeshHost mesh;

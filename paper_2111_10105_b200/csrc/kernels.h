@@ -16,6 +16,9 @@ cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
 // Sum split-K Gram partials in split order and symmetrise (spectral.cpp:37-38).
 cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, const double* part,
                               double* R);
+// Sum of split-K partials (row-major M x N) into column-major out (M x N).
+cudaError_t launch_reduce_sum(cudaStream_t s, int M, int N, int splits, int nbatch,
+                              const double* part, double* out);
 // Dictionary levels over [-1, 1] (codec.cpp:122-129, 300-301).
 cudaError_t launch_quant_dict(cudaStream_t s, long count, int bits, const double* U, uint16_t* q);
 cudaError_t launch_init_keys(cudaStream_t s, long rows, unsigned long long* keys);
@@ -67,6 +70,10 @@ cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int nc
 // nbatch * 2 (F|1) k doubles (used when the pair does not fit in shared memory).
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
                             const double* start, double* Q, double* H, double* work, double* scr);
+// Q (F x k per batch) = thin Householder Q of Z (same kernel as the fused
+// OI, QR only): one round of the implicit X (X^T Q) iteration.
+cudaError_t launch_qr_cluster(cudaStream_t s, int nbatch, int F, int k, const double* Z,
+                              double* Q);
 // U[:, k:F] = columns k..F-1 of the full Householder Q of U[:, :k].
 cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
                             double* scr);

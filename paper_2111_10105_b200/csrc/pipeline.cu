@@ -158,7 +158,68 @@ Status gram(dmcg_plan* p, const void* const x[3], int n) {
   return Status::ok();
 }
 
-Status basis(dmcg_plan* p) {
+bool implicit_oi(const dmcg_plan* p) {
+  return p->implicit && p->rounds > 0 && p->k > 0 && p->k < p->F;
+}
+
+// Algorithmic flops of the OI: explicit (rounds + 1) x {QR,
+// R Q} + Q^T Z; implicit (rounds + 1) x {QR, X Q} + rounds x X^T P + P^T P
+// over the plan's (or shard's) vertex rows.
+double oi_flops(const dmcg_plan* p, double F, double k, double r, double qr) {
+  if (!implicit_oi(p)) return 3.0 * ((r + 1.0) * (qr + 2.0 * F * F * k) + 2.0 * F * k * k);
+  const double n = p->shard ? (double)p->shard->n_own : (double)p->n;
+  return 3.0 * ((r + 1.0) * (qr + 2.0 * n * F * k) + r * 2.0 * n * F * k + 2.0 * n * k * k);
+}
+
+// The implicit orthogonal iterations (dmcg_config.oi_implicit; BASELINE
+// config 3): R = X^T X is never formed.  Q0 = qr(start); every round
+//   P = X Q (n x k, GEMM over frames),  Z = X^T P (F x k, split-K GEMM over
+//   the vertex rows),  Q = qr(Z)  (k_oi_cluster in QR-only mode),
+// then P = X Q and H = P^T P (= Q^T R Q, symmetrised like the oracle).  On a
+// vertex-row shard X is the rank's rows and the Z / H partials are
+// allreduced (sum) every round.  P lives in the coefficient buffer.
+template <typename T>
+Status implicit_oi(dmcg_plan* p, const void* const x[3], int nrows, dmcg_comm* comm, double* H) {
+  cudaStream_t s = p->ctx->stream;
+  const int F = (int)p->F, k = (int)p->k;
+  const long Fk = (long)F * k, nk = (long)nrows * k;
+  double* P = p->d_C;
+  LoadDense3<T, true> lxk{(const T*)x[0], (const T*)x[1], (const T*)x[2], 1L, (long)F};   // X(i, f) by f
+  LoadDense3<T, false> lxm{(const T*)x[0], (const T*)x[1], (const T*)x[2], (long)F, 1L};  // X(i, f) by i
+  LoadDense<double, true> lq{p->d_Q, Fk, 1L, (long)F};
+  LoadDense<double, true> lp{P, nk, 1L, (long)nrows};
+  auto splits_for = [&](int M, int N) {
+    const int tiles = ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN);
+    long sp = pick_splits(tiles, 3, nrows);
+    const long cap = (long)(p->part_elems / (3L * M * N));
+    if (sp > cap) sp = cap;
+    return gemm_splits(nrows, (int)(sp < 1 ? 1 : sp), nullptr);
+  };
+  DMCG_TRY(launch_qr_cluster(s, 3, F, k, p->d_start, p->d_Q));
+  for (int r = 0; r <= p->rounds; ++r) {
+    // P = X Q: M = rows, N = k, K = F
+    DMCG_TRY(launch_gemm(s, 3, nrows, k, F, 1, lxk, lq, StoreStrided{P, nk, 1L, (long)nrows}));
+    if (r == p->rounds) break;
+    // Z = X^T P: M = F, N = k, K = rows (split-K)
+    const int sz = splits_for(F, k);
+    DMCG_TRY(launch_gemm(s, 3, F, k, nrows, sz, lxm, lp, StorePartial{p->d_part, 3}));
+    DMCG_TRY(launch_reduce_sum(s, F, k, sz, 3, p->d_part, p->d_Z));
+    if (comm) {
+      Status st = comm_allreduce_sum_f64(comm, p->d_Z, 3 * (size_t)Fk, s);
+      if (!st.good()) return st;
+    }
+    DMCG_TRY(launch_qr_cluster(s, 3, F, k, p->d_Z, p->d_Q));
+  }
+  // H = P^T P: M = N = k, K = rows (split-K), symmetrised
+  const int sh = splits_for(k, k);
+  DMCG_TRY(launch_gemm(s, 3, k, k, nrows, sh, lp, lp, StorePartial{p->d_part, 3}));
+  DMCG_TRY(launch_reduce_sym(s, k, sh, 3, p->d_part, H));
+  if (comm) return comm_allreduce_sum_f64(comm, H, 3 * (size_t)k * k, s);
+  return Status::ok();
+}
+
+Status basis(dmcg_plan* p, const void* const x[3] = nullptr, int nrows = 0,
+             dmcg_comm* comm = nullptr) {
   cudaStream_t s = p->ctx->stream;
   const int F = (int)p->F, k = (int)p->k;
   const long FF = (long)F * F;
@@ -174,8 +235,15 @@ Status basis(dmcg_plan* p) {
   // kernel, one CTA per axis (basis.cu k_oi_fused).
   double* H = p->d_C;  // k x k scratch (coefficient buffer is free here)
   DMCG_TRY(record_event(p->ev[6], s));
-  DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H,
-                                  p->d_qr_scr));
+  if (implicit_oi(p)) {
+    H = p->d_Z;  // the coefficient buffer holds P; Z is dead after the last QR
+    Status st = p->dtype == DMCG_F32 ? implicit_oi<float>(p, x, nrows, comm, H)
+                                     : implicit_oi<double>(p, x, nrows, comm, H);
+    if (!st.good()) return st;
+  } else {
+    DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H,
+                             p->d_qr_scr));
+  }
   DMCG_TRY(record_event(p->ev[7], s));
   DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
   double* Ws = p->d_Z;  // k x k sorted Ritz vectors (Z is free)
@@ -214,13 +282,14 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   // K1 delta coordinates (codec.cpp:419).
   DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
   DMCG_TRY(record_event(p->ev[1], s));
-  // K2 autocorrelation (spectral.cpp:35-39).
-  Status st = f32 ? gram<float>(p, x, n) : gram<double>(p, x, n);
+  // K2 autocorrelation (spectral.cpp:35-39); the implicit OI never forms it.
+  Status st = Status::ok();
+  if (!implicit_oi(p)) st = f32 ? gram<float>(p, x, n) : gram<double>(p, x, n);
   if (!st.good()) return st;
   DMCG_TRY(record_event(p->ev[2], s));
   // K3 basis.
   p->forked = false;
-  st = basis(p);
+  st = basis(p, x, n);
   if (!st.good()) return st;
   DMCG_TRY(record_event(p->ev[3], s));
   // K4 projection coeffs = U_k^T delta^T (codec.cpp:420) + row min/max, then
@@ -317,7 +386,7 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
     // + (rounds + 1) x R Q (2F^2 k) + Q^T Z (2Fk^2)
     const double F = p->F, k = p->k, r = p->rounds;
     const double qr = 2.0 * (2.0 * F * k * k - 2.0 * k * k * k / 3.0);
-    p->stats.flops_oi = 3.0 * ((r + 1.0) * (qr + 2.0 * F * F * k) + 2.0 * F * k * k);
+    p->stats.flops_oi = oi_flops(p, F, k, r, qr);
     p->oi_timed = false;
   }
   p->stats.kernel_launches_encode =
@@ -363,6 +432,7 @@ Status shard_phase(dmcg_plan* p, int phase, const void* const x[3]) {
       DMCG_TRY(launch_delta(s, n_own, F, sh.d_loc_rp, sh.d_loc_ci, x, f32, p->d_delta,
                             p->d_flags));
       DMCG_TRY(record_event(p->ev[1], s));
+      if (implicit_oi(p)) return Status::ok();
       Status st = f32 ? gram<float>(p, x, n_own) : gram<double>(p, x, n_own);
       if (!st.good()) return st;
       return Status::ok();
@@ -370,7 +440,11 @@ Status shard_phase(dmcg_plan* p, int phase, const void* const x[3]) {
     case 1: {
       DMCG_TRY(record_event(p->ev[2], s));
       p->forked = false;
-      Status st = basis(p);
+      if (implicit_oi(p) && !sh.comm && sh.nranks > 1)
+        return Status{DMCG_E_CONFIG,
+                      "ConfigError: the implicit OI allreduces every round: shard it with a "
+                      "communicator (dmcg_shard_encode_device)"};
+      Status st = basis(p, x, n_own, sh.comm);
       if (!st.good()) return st;
       DMCG_TRY(record_event(p->ev[3], s));
       DMCG_TRY(launch_init_keys(s, krows, sh.d_keys));
@@ -434,7 +508,7 @@ static Status shard_finish_stats(dmcg_plan* p) {
     cudaEventElapsedTime(&p->stats.ms_oi, p->ev[6], p->ev[7]);
     const double F = p->F, k = p->k, r = p->rounds;
     const double qr = 2.0 * (2.0 * F * k * k - 2.0 * k * k * k / 3.0);
-    p->stats.flops_oi = 3.0 * ((r + 1.0) * (qr + 2.0 * F * F * k) + 2.0 * F * k * k);
+    p->stats.flops_oi = oi_flops(p, F, k, r, qr);
   }
   p->stats.kernel_launches_encode = 1 + 2 + (oi ? 10 : 3) + 1 + (p->k > 0 ? 2 : 0) + 1 + 2 + 1 + 1;
   if (flags[0])
@@ -450,7 +524,7 @@ Status shard_encode(dmcg_plan* p, const void* const x[3]) {
   cudaStream_t s = p->ctx->stream;
   const size_t FF = (size_t)p->F * p->F;
   Status st = shard_phase(p, 0, x);
-  if (st.good()) st = comm_allreduce_sum_f64(sh.comm, p->d_R, 3 * FF, s);
+  if (st.good() && !implicit_oi(p)) st = comm_allreduce_sum_f64(sh.comm, p->d_R, 3 * FF, s);
   if (st.good()) st = shard_phase(p, 1, x);
   if (st.good()) st = comm_allreduce_max_u64(sh.comm, sh.d_keys, (3ull * p->k + 3) * 2, s);
   if (st.good()) st = shard_phase(p, 2, x);

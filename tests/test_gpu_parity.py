@@ -21,9 +21,10 @@ from paper_2111_10105_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def _cfg(cfgspec, rounds=None):
+def _cfg(cfgspec, rounds=None, implicit=False):
     return C.EncoderConfig(k_l=cfgspec.k, row_bits=[cfgspec.bits] * cfgspec.k,
-                           oi_rounds=cfgspec.rounds if rounds is None else rounds)
+                           oi_rounds=cfgspec.rounds if rounds is None else rounds,
+                           oi_implicit=implicit)
 
 
 def _agreeing_columns(ev, k):
@@ -56,9 +57,9 @@ def _oracle_stream_of(g, s):
     return og
 
 
-def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3):
+def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3, implicit=False):
     rounds = spec.rounds if rounds is None else rounds
-    ec = _cfg(spec, rounds)
+    ec = _cfg(spec, rounds, implicit)
     g = codec.encode(s, ec)
     o = O.encode(s, spec.k, spec.bits, rounds=rounds, seed=0, nthreads=8)
     n, F, k = s.n, s.F, spec.k
@@ -106,6 +107,15 @@ def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3):
 def test_config_parity(codec, name):
     spec = synth.CONFIGS[name]
     check_parity(codec, spec.make(), spec)
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2f32"])
+def test_implicit_oi_parity(codec, name):
+    """oi_implicit: Z = X^T (X Q) per round, R never formed (BASELINE config 3's
+    'covariance applied implicitly') — the same iteration as the oracle's R Q, so the
+    full parity contract holds."""
+    spec = synth.CONFIGS[name]
+    check_parity(codec, spec.make(), spec, implicit=True, f32_out=spec.dtype == "f32")
 
 
 def test_config4_sequence_parity(codec):

@@ -134,6 +134,24 @@ def test_one_rank_nccl_path_is_bit_identical_to_plan(codec):
     comm.close()
 
 
+def test_one_rank_nccl_path_implicit_oi(codec):
+    """The sharded implicit OI (X^T (X Q) partials allreduced every round) with
+    one rank equals the single-GPU implicit plan bit for bit."""
+    spec = synth.CONFIGS["c1"]
+    s = spec.make()
+    ec = _cfg(spec, implicit=True)
+    comm = shard.Comm(0, 1, 0)
+    sp = shard.ShardPlan(codec, s.n, s.F, s.faces, ec, 1, 0, comm)
+    d_in = [torch.from_numpy(a).cuda() for a in s.axes]
+    sp.encode_device([t.data_ptr() for t in d_in])
+    p = C.Plan(codec, s.n, s.F, s.faces, ec)
+    p.encode_device([t.data_ptr() for t in d_in])
+    _assert_same_stream(sp.download(), p.download())
+    assert p.stats()["ms_gram"] < 0.05      # R is never formed
+    sp.close()
+    comm.close()
+
+
 def test_frame_windows_reproduce_full_decode(codec):
     spec = synth.CONFIGS["c1"]
     s = spec.make()
