@@ -376,6 +376,8 @@ void dmcg_destroy(dmcg_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->pool.release_all();
   cudaStreamSynchronize(c->aux);
+  for (auto e : c->ev_timing) cudaEventDestroy(e);
+  for (auto e : c->ev_plain) cudaEventDestroy(e);
   cudaStreamDestroy(c->aux);
   cudaStreamDestroy(c->stream);
   delete c;
@@ -484,10 +486,8 @@ void dmcg_plan_destroy(dmcg_plan* p) {
   for (auto* g : {&p->g_encode, &p->g_decode})
     if (g->exec) cudaGraphExecDestroy(g->exec);
   for (auto& kv : p->owned) p->ctx->pool.put(kv.first, kv.second);
-  for (auto& e : p->ev)
-    if (e) cudaEventDestroy(e);
-  for (auto e : {p->ev_fork, p->ev_join})
-    if (e) cudaEventDestroy(e);
+  for (auto& e : p->ev) p->ctx->give_event(e, true);
+  for (auto e : {p->ev_fork, p->ev_join}) p->ctx->give_event(e, false);
   delete p;
 }
 
@@ -553,7 +553,6 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->W = 3 * F;
   p->W_pad = (p->W + kColBlock - 1) / kColBlock * kColBlock;
   p->nblk = p->W_pad / kColBlock;
-  const size_t es = dtype == DMCG_F32 ? 4 : 8;
   const size_t nF = (size_t)n * F, FF = (size_t)F * F;
   const uint32_t F2 = F + (F & 1);
   const size_t kk = (size_t)std::max<uint32_t>(k, 1);
@@ -568,10 +567,6 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_lap_ci = (uint32_t*)get(m.lap_ci.size() * 4);
   p->d_anchor_idx = (uint32_t*)get((size_t)p->n_c * 4);
   p->d_anchor_pos = (int32_t*)get((size_t)n * 4);
-  for (int a = 0; a < 3; ++a) {
-    p->d_x_in[a] = get(nF * es);
-    p->d_x_out[a] = get(nF * es);
-  }
   p->d_delta = (double*)get(3 * nF * 8);
   p->d_R = (double*)get(3 * FF * 8);
   const int tiles = ((F + 63) / 64) * ((F + 63) / 64);
@@ -606,9 +601,9 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     return {DMCG_E_CUDA, "CudaError: device allocation failed"};
   }
   tm.lap("alloc");
-  for (auto& e : p->ev) cudaEventCreate(&e);
-  cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming);
+  for (auto& e : p->ev) e = ctx->take_event(true);
+  p->ev_fork = ctx->take_event(false);
+  p->ev_join = ctx->take_event(false);
   cudaStream_t s = ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
@@ -1092,6 +1087,33 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   if (!ctx || !seq || !cfg || !out) return DMCG_E_CONFIG;
   cudaSetDevice(ctx->device);
   PhaseTimer tm("encode");
+  // The input upload goes first, into pool buffers: with pinned host memory
+  // it runs on the copy engine while the host builds the mesh (CSR,
+  // validation, anchors) for the plan below.
+  const size_t in_bytes =
+      (seq->n && seq->F) ? (size_t)seq->n * seq->F * (seq->dtype == DMCG_F32 ? 4 : 8) : 0;
+  void* d_in[3] = {nullptr, nullptr, nullptr};
+  struct InGuard {
+    dmcg_ctx* c;
+    void** d;
+    size_t bytes;
+    ~InGuard() {
+      cudaStreamSynchronize(c->stream);
+      for (int a = 0; a < 3; ++a)
+        if (d[a]) c->pool.put(d[a], bytes);
+    }
+  } in_guard{ctx, d_in, in_bytes};
+  if (in_bytes && seq->axes[0] && seq->axes[1] && seq->axes[2] &&
+      (seq->dtype == DMCG_F64 || seq->dtype == DMCG_F32)) {
+    bool ok = true;
+    for (int a = 0; a < 3 && ok; ++a) {
+      d_in[a] = ctx->pool.get(in_bytes);
+      ok = d_in[a] && cudaMemcpyAsync(d_in[a], seq->axes[a], in_bytes, cudaMemcpyHostToDevice,
+                                      ctx->stream) == cudaSuccess;
+    }
+    if (!ok) return ctx->set_error({DMCG_E_CUDA, "CudaError: H2D copy failed"});
+  }
+  tm.lap("h2d issue");
   dmcg_plan* p = nullptr;
   Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
                                nullptr, 0, &p);
@@ -1121,12 +1143,7 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
     }
   }
   tm.lap("plan");
-  const size_t bytes = (size_t)seq->n * seq->F * (seq->dtype == DMCG_F32 ? 4 : 8);
-  for (int a = 0; a < 3 && st.good(); ++a)
-    if (cudaMemcpyAsync(p->d_x_in[a], seq->axes[a], bytes, cudaMemcpyHostToDevice, ctx->stream) !=
-        cudaSuccess)
-      st = {DMCG_E_CUDA, "CudaError: H2D copy failed"};
-  if (st.good()) st = plan_encode(p, p->d_x_in);
+  if (st.good()) st = plan_encode(p, d_in);
   tm.lap("h2d+kernels");
   if (st.good()) {
     if (!out->faces) out->faces = seq->faces;
@@ -1210,6 +1227,10 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   if (opt) o = *opt;
   if (st.good() && o.solver == 0) st = plan_prepare_decode(p);
   tm.lap("prepare(analyze)");
+  for (int a = 0; a < 3 && st.good(); ++a) {  // output staging (drop-in decode only)
+    p->d_x_out[a] = plan_alloc(p, (size_t)in->n * in->F * (out_dtype == DMCG_F32 ? 4 : 8));
+    if (!p->d_x_out[a]) st = {DMCG_E_CUDA, "CudaError: device allocation failed"};
+  }
   if (st.good()) st = plan_decode(p, &o, p->d_x_out);
   tm.lap("kernels");
   // D2H of the decoded frame window only (all frames by default): columns
