@@ -132,7 +132,8 @@ typedef struct {
   uint32_t n_faces;
 } dmcg_seq;
 
-/* Compressed animation, pca_qp / n_b = 1 subset of dmc::CompressedAnimation
+/* Compressed animation, n_b = 1 subset of dmc::CompressedAnimation for the
+ * variants on the B200 path: pca, pca_q, v2v, pca_qs, pca_qp
  * (include/dmc/stream.hpp:130-155).  All arrays are caller-allocated with
  * the sizes from dmcg_encoded_sizes(); levels are 16-bit because every bit
  * depth is limited to 1..16 (codec.cpp:82-86,114-118).
@@ -152,11 +153,13 @@ typedef struct {
   uint32_t* anchor_idx;
   float anchor_min[3], anchor_max[3];
   uint16_t* anchor_q[3];
+  float* means[3];          /* F per-frame vertex means, variants pca / pca_q only
+                               (codec.cpp:432-441; may be NULL otherwise) */
 } dmcg_encoded;
 
 /* Element counts of each dmcg_encoded array for (n, F, cfg). */
 typedef struct {
-  size_t dict_q, rows, coeff_q, anchor_idx, anchor_q;
+  size_t dict_q, rows, coeff_q, anchor_idx, anchor_q, means;
 } dmcg_sizes;
 int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_sizes* out);
 

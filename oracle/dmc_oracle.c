@@ -1236,6 +1236,103 @@ int orc_solve_anchored(uint32_t n, const uint32_t* lrow, const uint32_t* lcol, c
   return rc;
 }
 
+/* Nested-dissection ordering + sparse LDL^T of an SPD CSR matrix (the
+ * SimplicialLDLT stand-in shared by both solvers).  0 on success. */
+static int ldl_build(csr* M, ldl_factor* f) {
+  const uint32_t n = M->n;
+  f->n = n;
+  f->perm = malloc((size_t)n * sizeof(uint32_t));
+  f->pinv = malloc((size_t)n * sizeof(uint32_t));
+  nd_state st;
+  st.M = M;
+  st.part = calloc(n, sizeof(int32_t));
+  st.level = malloc((size_t)n * sizeof(int32_t));
+  st.queue = malloc((size_t)n * sizeof(uint32_t));
+  st.perm = f->perm;
+  st.nperm = 0;
+  st.next_id = 1;
+  uint32_t* all = malloc((size_t)n * sizeof(uint32_t));
+  for (uint32_t i = 0; i < n; ++i) all[i] = i;
+  nd_recurse(&st, all, n, 0);
+  free(all);
+  free(st.part);
+  free(st.level);
+  free(st.queue);
+  for (uint32_t k = 0; k < n; ++k) f->pinv[f->perm[k]] = k;
+  return ldl_factorize(M, f);
+}
+
+static void ldl_release(ldl_factor* f, int factored) {
+  free(f->perm);
+  free(f->pinv);
+  if (factored) {
+    free(f->Lp);
+    free(f->Li);
+    free(f->Lx);
+    free(f->D);
+  }
+}
+
+int orc_solve_mean_constrained(uint32_t n, const uint32_t* lrow, const uint32_t* lcol,
+                               const double* lval, uint32_t W, const double* delta,
+                               const double* means, double* X, int nthreads) {
+  if (n < 2) return ORC_E_CONFIG;
+  /* reduced = L[:, 1:]; normal = reduced^T reduced = (L^T L)[1:, 1:] (solver.cpp:116-117) */
+  csr M = normal_matrix(n, lrow, lcol, lval, 0, NULL);
+  csr Rm;
+  Rm.n = n - 1;
+  Rm.rp = malloc((size_t)n * sizeof(uint32_t));
+  Rm.ci = malloc((size_t)M.rp[n] * sizeof(uint32_t));
+  Rm.v = malloc((size_t)M.rp[n] * sizeof(double));
+  uint32_t q = 0;
+  Rm.rp[0] = 0;
+  for (uint32_t i = 1; i < n; ++i) {
+    for (uint32_t p = M.rp[i]; p < M.rp[i + 1]; ++p)
+      if (M.ci[p] > 0) {
+        Rm.ci[q] = M.ci[p] - 1;
+        Rm.v[q++] = M.v[p];
+      }
+    Rm.rp[i] = q;
+  }
+  csr_free(&M);
+  ldl_factor f;
+  int rc = ldl_build(&Rm, &f);
+  if (rc == 0) {
+    const size_t nW = (size_t)n * W, mW = (size_t)(n - 1) * W;
+    double* full = malloc(nW * sizeof(double));
+    double* rhs = malloc(nW * sizeof(double));
+    double* z = malloc(mW * sizeof(double));
+    double* dz = malloc(mW * sizeof(double));
+    /* z = solve(reduced^T delta); reduced^T = rows 1.. of L^T = L (solver.cpp:124) */
+    spmm(n, lrow, lcol, lval, delta, rhs, W, nthreads);
+    ldl_solve_multi(&f, rhs + W, z, W, nthreads);
+    /* z += solve(reduced^T (delta - reduced z)); reduced z = L [0; z] (solver.cpp:125) */
+    for (uint32_t c = 0; c < W; ++c) full[c] = 0.0;
+    memcpy(full + W, z, mW * sizeof(double));
+    spmm(n, lrow, lcol, lval, full, rhs, W, nthreads);
+    for (size_t t = 0; t < nW; ++t) full[t] = delta[t] - rhs[t];
+    spmm(n, lrow, lcol, lval, full, rhs, W, nthreads);
+    ldl_solve_multi(&f, rhs + W, dz, W, nthreads);
+    for (size_t t = 0; t < mW; ++t) z[t] += dz[t];
+    /* x = [0; z], each column shifted to its mean (solver.cpp:126-131) */
+    for (uint32_t c = 0; c < W; ++c) X[c] = 0.0;
+    memcpy(X + W, z, mW * sizeof(double));
+    for (uint32_t c = 0; c < W; ++c) {
+      double sum = 0.0;
+      for (uint32_t i = 0; i < n; ++i) sum += X[(size_t)i * W + c];
+      const double shift = means[c] - sum / (double)n;
+      for (uint32_t i = 0; i < n; ++i) X[(size_t)i * W + c] += shift;
+    }
+    free(full);
+    free(rhs);
+    free(z);
+    free(dz);
+  }
+  csr_free(&Rm);
+  ldl_release(&f, rc == 0);
+  return rc;
+}
+
 /* ======================================================================== */
 /* encode / decode (src/codec.cpp:351-552)                                   */
 /* ======================================================================== */
@@ -1244,6 +1341,20 @@ int orc_encode(uint32_t n, uint32_t F, const double* const axes[3], const uint32
                uint32_t n_faces, uint32_t k_l, const int* row_bits, double anchor_fraction,
                int anchor_bits, int dict_bits, int rounds, uint64_t basis_seed, orc_encoded* out,
                double* U_out, double* evals_out, orc_timing* tm, int nthreads) {
+  return orc_encode_variant(4, n, F, axes, faces, n_faces, k_l, row_bits, anchor_fraction,
+                            anchor_bits, dict_bits, rounds, basis_seed, out, U_out, evals_out, tm,
+                            nthreads);
+}
+
+static int uses_anchors(int v) { return v == 3 || v == 4; }  /* stream.hpp:77-79 (n_b = 1) */
+static int uses_means(int v) { return v == 0 || v == 1; }    /* stream.hpp:80-82 */
+
+int orc_encode_variant(int variant, uint32_t n, uint32_t F, const double* const axes[3],
+                       const uint32_t* faces, uint32_t n_faces, uint32_t k_l, const int* row_bits,
+                       double anchor_fraction, int anchor_bits, int dict_bits, int rounds,
+                       uint64_t basis_seed, orc_encoded* out, double* U_out, double* evals_out,
+                       orc_timing* tm, int nthreads) {
+  if (variant < 0 || variant > 4) return ORC_E_CONFIG;
   orc_timing dummy;
   if (!tm) tm = &dummy;
   memset(tm, 0, sizeof(*tm));
@@ -1258,7 +1369,8 @@ int orc_encode(uint32_t n, uint32_t F, const double* const axes[3], const uint32
   out->n = n;
   out->F = F;
   out->k_l = k_l;
-  out->n_c = orc_anchor_count(n, anchor_fraction);
+  out->variant = variant;
+  out->n_c = uses_anchors(variant) ? orc_anchor_count(n, anchor_fraction) : 0;
   out->n_faces = n_faces;
   out->faces = faces;
   out->anchor_bits = anchor_bits;
@@ -1294,8 +1406,17 @@ int orc_encode(uint32_t n, uint32_t F, const double* const axes[3], const uint32
     for (size_t t = 0; t < (size_t)F * F; ++t)
       out->dict_q[a][t] = orc_quantize(-1.0f, 1.0f, dict_bits, U[t]);
     t0 = now_s();
-    orc_delta(n, F, lrow, lcol, lval, X, delta);
+    if (variant == 2)  /* v2v: the trajectories themselves (codec.cpp:416-417) */
+      memcpy(delta, X, (size_t)n * F * sizeof(double));
+    else
+      orc_delta(n, F, lrow, lcol, lval, X, delta);
     tm->t_delta += now_s() - t0;
+    if (uses_means(variant))  /* traj.row(f).mean() as float (codec.cpp:432-441) */
+      for (uint32_t f = 0; f < F; ++f) {
+        double sum = 0.0;
+        for (uint32_t i = 0; i < n; ++i) sum += X[(size_t)i * F + f];
+        out->means[a][f] = (float)(sum / (double)n);
+      }
     /* coeffs = U^T delta^T, rows r < k_l (codec.cpp:420) */
     t0 = now_s();
 #ifdef _OPENMP
@@ -1318,8 +1439,8 @@ int orc_encode(uint32_t n, uint32_t F, const double* const axes[3], const uint32
   }
   /* anchors (codec.cpp:444-471) */
   t0 = now_s();
-  if (!rc) rc = orc_select_anchors(n, out->n_c, 0, 0, out->anchor_idx);
-  for (int a = 0; a < 3 && !rc; ++a) {
+  if (!rc && out->n_c) rc = orc_select_anchors(n, out->n_c, 0, 0, out->anchor_idx);
+  for (int a = 0; a < 3 && !rc && out->n_c; ++a) {
     const double* X = axes[a];
     double lo = INFINITY, hi = -INFINITY;
     for (uint32_t t = 0; t < out->n_c; ++t) {
@@ -1422,11 +1543,24 @@ int orc_decode(const orc_encoded* in, double* const axes_out[3], orc_timing* tm,
   if (!rc) {
     /* solve_anchored, Parallel (codec.cpp:537-539): the reference factors M
      * once per axis; M does not depend on the axis, so all 3F columns are
-     * solved against one factorisation here. */
+     * solved against one factorisation here.  pca_qs (Serial) refactors per
+     * column (solver.cpp:92-100): the same factor and column-separable solves.
+     * v2v needs no solve (codec.cpp:520-524); pca / pca_q the mean-
+     * constrained one (codec.cpp:540-546). */
     t0 = now_s();
     double* X = malloc((size_t)n * W * sizeof(double));
-    rc = orc_solve_anchored(n, lrow, lcol, lval, W, delta, n_c, in->anchor_idx, anchors, X,
-                            nthreads);
+    if (in->variant == 2) {
+      memcpy(X, delta, (size_t)n * W * sizeof(double));
+    } else if (uses_means(in->variant)) {
+      double* mw = malloc((size_t)W * sizeof(double));
+      for (int a = 0; a < 3; ++a)
+        for (uint32_t f = 0; f < F; ++f) mw[(size_t)a * F + f] = (double)in->means[a][f];
+      rc = orc_solve_mean_constrained(n, lrow, lcol, lval, W, delta, mw, X, nthreads);
+      free(mw);
+    } else {
+      rc = orc_solve_anchored(n, lrow, lcol, lval, W, delta, n_c, in->anchor_idx, anchors, X,
+                              nthreads);
+    }
     for (int a = 0; a < 3 && !rc; ++a)
       for (uint32_t i = 0; i < n; ++i)
         memcpy(axes_out[a] + (size_t)i * F, X + (size_t)i * W + (size_t)a * F,
@@ -1501,7 +1635,7 @@ size_t orc_serialize(const orc_encoded* e, uint8_t* o, orc_sections* s) {
   const char magic[4] = {'D', 'M', 'C', '1'};
   for (int i = 0; i < 4; ++i) put_u8(o, &p, (uint8_t)magic[i]);
   put_u16(o, &p, 1);  /* version */
-  put_u8(o, &p, 4);   /* Variant::PcaQp */
+  put_u8(o, &p, (uint8_t)e->variant);
   put_u8(o, &p, 0);   /* flags */
   put_u32(o, &p, e->n);
   put_u32(o, &p, e->F);
@@ -1543,6 +1677,15 @@ size_t orc_serialize(const orc_encoded* e, uint8_t* o, orc_sections* s) {
     bw_flush(&w);
     p = w.pos;
     sz.coeff_payload += p - start;
+    if (uses_means(e->variant)) {  /* stream.cpp:255-263 */
+      start = p;
+      for (uint32_t f = 0; f < e->F; ++f) put_f32(o, &p, e->means[a][f]);
+      sz.means += p - start;
+    }
+  }
+  if (!uses_anchors(e->variant)) {
+    if (s) *s = sz;
+    return p;
   }
   size_t start = p;
   for (uint32_t t = 0; t < e->n_c; ++t) put_u32(o, &p, e->anchor_idx[t]);

@@ -140,6 +140,8 @@ typedef struct {
   uint32_t* anchor_idx;       /* n_c */
   float anchor_min[3], anchor_max[3];
   uint32_t* anchor_q[3];      /* n_c*F anchor-major */
+  int variant;                /* stream.hpp:60-68: 0 pca, 1 pca_q, 2 v2v, 3 pca_qs, 4 pca_qp */
+  float* means[3];            /* F per-frame vertex means (pca / pca_q), else unused */
 } orc_encoded;
 
 typedef struct {
@@ -157,6 +159,21 @@ int orc_encode(uint32_t n, uint32_t F, const double* const axes[3], const uint32
                int nthreads);
 int orc_decode(const orc_encoded* in, double* const axes_out[3], orc_timing* timing,
                int nthreads);
+/* encode for any n_b = 1 variant 0-4 (codec.cpp:351-473): v2v projects the
+ * trajectories instead of delta (codec.cpp:416-417); pca / pca_q store the
+ * per-frame vertex means (codec.cpp:432-441) and no anchors; pca_qs codes like
+ * pca_qp.  orc_encode == orc_encode_variant(4, ...). */
+int orc_encode_variant(int variant, uint32_t n, uint32_t F, const double* const axes[3],
+                       const uint32_t* faces, uint32_t n_faces, uint32_t k_l, const int* row_bits,
+                       double anchor_fraction, int anchor_bits, int dict_bits, int rounds,
+                       uint64_t basis_seed, orc_encoded* out, double* U_out, double* evals_out,
+                       orc_timing* timing, int nthreads);
+/* solve_mean_constrained (src/solver.cpp:105-133): vertex 0 pinned, normal
+ * equations of L[:, 1:] by sparse LDL^T, one refinement, per-column mean
+ * shift to means[c].  delta, X: n x W vertex-major. */
+int orc_solve_mean_constrained(uint32_t n, const uint32_t* lrow, const uint32_t* lcol,
+                               const double* lval, uint32_t W, const double* delta,
+                               const double* means, double* X, int nthreads);
 
 /* ---- stream.cpp / metrics.cpp ------------------------------------------ */
 typedef struct {

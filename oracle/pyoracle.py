@@ -30,7 +30,7 @@ class OrcEncoded(ctypes.Structure):
                 ("dict_q", u32p * 3), ("row_min", f32p * 3), ("row_max", f32p * 3),
                 ("row_bits", u8p * 3), ("coeff_q", u32p * 3), ("anchor_idx", u32p),
                 ("anchor_min", ctypes.c_float * 3), ("anchor_max", ctypes.c_float * 3),
-                ("anchor_q", u32p * 3)]
+                ("anchor_q", u32p * 3), ("variant", ctypes.c_int), ("means", f32p * 3)]
 
 
 class OrcTiming(ctypes.Structure):
@@ -90,6 +90,9 @@ def lib():
                                  f64p, ctypes.POINTER(OrcTiming), ctypes.c_int]
         L.orc_decode.argtypes = [ctypes.POINTER(OrcEncoded), f64p * 3, ctypes.POINTER(OrcTiming),
                                  ctypes.c_int]
+        L.orc_encode_variant.argtypes = [ctypes.c_int] + L.orc_encode.argtypes
+        L.orc_solve_mean_constrained.argtypes = [ctypes.c_uint32, u32p, u32p, f64p,
+                                                 ctypes.c_uint32, f64p, f64p, f64p, ctypes.c_int]
         L.orc_serialize.restype = ctypes.c_size_t
         L.orc_serialize.argtypes = [ctypes.POINTER(OrcEncoded), u8p, ctypes.POINTER(OrcSections)]
         L.orc_rate_exact.argtypes = [ctypes.POINTER(OrcSections), ctypes.c_uint32, ctypes.c_uint32,
@@ -275,10 +278,24 @@ def solve_anchored(faces, n, delta: np.ndarray, idx, anchors, nthreads=1):
     return X
 
 
+def solve_mean_constrained(faces, n, delta: np.ndarray, means, nthreads=1):
+    """solve_mean_constrained (src/solver.cpp:105-133) via orc_solve_mean_constrained."""
+    lrow, lcol, lval = laplacian(faces, n)
+    delta = np.ascontiguousarray(delta, np.float64)
+    W = delta.shape[1]
+    means = np.ascontiguousarray(means, np.float64)
+    X = np.zeros((n, W))
+    rc = lib().orc_solve_mean_constrained(n, P(lrow, u32p), P(lcol, u32p), P(lval, f64p), W,
+                                          P(delta, f64p), P(means, f64p), P(X, f64p), nthreads)
+    if rc:
+        raise ArithmeticError(f"solve_mean_constrained code {rc}")
+    return X
+
+
 class Encoded:
     """Owner of the numpy buffers behind an OrcEncoded view."""
 
-    def __init__(self, n, F, k_l, n_c, faces, anchor_bits=16, dict_bits=16):
+    def __init__(self, n, F, k_l, n_c, faces, anchor_bits=16, dict_bits=16, variant=4):
         self.faces = np.ascontiguousarray(faces, dtype=np.uint32)
         self.dict_q = [np.zeros((F, F), np.uint32) for _ in range(3)]   # [col][row] = col-major
         self.row_min = [np.zeros(max(k_l, 1), np.float32) for _ in range(3)]
@@ -287,7 +304,9 @@ class Encoded:
         self.coeff_q = [np.zeros((max(k_l, 1), n), np.uint32) for _ in range(3)]
         self.anchor_idx = np.zeros(max(n_c, 1), np.uint32)
         self.anchor_q = [np.zeros((max(n_c, 1), F), np.uint32) for _ in range(3)]
+        self.means = [np.zeros(F, np.float32) for _ in range(3)]
         s = OrcEncoded()
+        s.variant = variant
         s.n, s.F, s.k_l, s.n_c, s.n_faces = n, F, k_l, n_c, len(self.faces)
         s.anchor_bits, s.dict_bits, s.diff_bits = anchor_bits, dict_bits, 8
         s.faces = P(self.faces, u32p)
@@ -298,6 +317,7 @@ class Encoded:
             s.row_bits[a] = P(self.row_bits[a], u8p)
             s.coeff_q[a] = P(self.coeff_q[a], u32p)
             s.anchor_q[a] = P(self.anchor_q[a], u32p)
+            s.means[a] = P(self.means[a], f32p)
         s.anchor_idx = P(self.anchor_idx, u32p)
         self.s = s
 
@@ -310,18 +330,24 @@ class Encoded:
         return list(self.s.anchor_max)
 
 
+VARIANTS = {"pca": 0, "pca_q": 1, "v2v": 2, "pca_qs": 3, "pca_qp": 4}
+
+
 def encode(seq, k_l, bits, rounds=0, seed=0, anchor_fraction=0.01, anchor_bits=16, dict_bits=16,
-           nthreads=1, timing=None):
+           nthreads=1, timing=None, variant=4):
+    """codec.cpp:351-473 for the n_b = 1 variants 0-4 (default pca_qp)."""
     n, F = seq.axes[0].shape
+    variant = VARIANTS.get(variant, variant)
     axes = [np.ascontiguousarray(a, dtype=np.float64) for a in seq.axes]
-    n_c = anchor_count(n, anchor_fraction)
-    enc = Encoded(n, F, k_l, n_c, seq.faces, anchor_bits, dict_bits)
+    n_c = anchor_count(n, anchor_fraction) if variant in (3, 4) else 0
+    enc = Encoded(n, F, k_l, n_c, seq.faces, anchor_bits, dict_bits, variant)
     rb = np.full(max(k_l, 1), bits, dtype=np.int32) if np.isscalar(bits) else \
         np.ascontiguousarray(bits, np.int32)
     U = np.zeros((3, F, F))  # per axis, [col][row] => U[a].T is the matrix
     ev = np.zeros((3, F))
     tm = OrcTiming()
-    rc = lib().orc_encode(n, F, (f64p * 3)(*[P(a, f64p) for a in axes]), P(enc.faces, u32p),
+    rc = lib().orc_encode_variant(variant, n, F, (f64p * 3)(*[P(a, f64p) for a in axes]),
+                                  P(enc.faces, u32p),
                           len(enc.faces), k_l, P(rb, intp), anchor_fraction, anchor_bits, dict_bits,
                           rounds, seed, ctypes.byref(enc.s), P(U, f64p), P(ev, f64p),
                           ctypes.byref(tm), nthreads)

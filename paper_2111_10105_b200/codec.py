@@ -71,10 +71,12 @@ class EncoderConfig:
 
 @dataclass
 class CompressedAnimation:
-    """pca_qp / n_b = 1 subset of dmc::CompressedAnimation (stream.hpp:130-155).
+    """n_b = 1 subset of dmc::CompressedAnimation (stream.hpp:130-155) for the
+    variants pca, pca_q, v2v, pca_qs, pca_qp.
 
     dict_q[a] is (F, F) with dict_q[a][j, i] = level of U(i, j) (column-major
-    pack order); coeff_q[a] is (k_l, n); anchor_q[a] is (n_c, F)."""
+    pack order); coeff_q[a] is (k_l, n); anchor_q[a] is (n_c, F) (anchored
+    variants); means[a] is (F,) float32 (pca / pca_q)."""
     n: int
     F: int
     k_l: int
@@ -93,6 +95,7 @@ class CompressedAnimation:
     anchor_min: list = field(default_factory=lambda: [0.0] * 3)
     anchor_max: list = field(default_factory=lambda: [0.0] * 3)
     anchor_q: list = field(default_factory=list)
+    means: list = field(default_factory=list)
 
     @classmethod
     def allocate(cls, n, F, k_l, n_c, faces, **kw):
@@ -104,6 +107,7 @@ class CompressedAnimation:
         c.coeff_q = [np.zeros((max(k_l, 1), n), np.uint16) for _ in range(3)]
         c.anchor_idx = np.zeros(max(n_c, 1), np.uint32)
         c.anchor_q = [np.zeros((max(n_c, 1), F), np.uint16) for _ in range(3)]
+        c.means = [np.zeros(F, np.float32) for _ in range(3)]
         return c
 
     def to_c(self) -> L.DmcgEncoded:
@@ -123,6 +127,8 @@ class CompressedAnimation:
             e.anchor_q[a] = self.anchor_q[a].ctypes.data_as(L.u16p)
             e.anchor_min[a] = self.anchor_min[a]
             e.anchor_max[a] = self.anchor_max[a]
+            if len(self.means) == 3:
+                e.means[a] = self.means[a].ctypes.data_as(L.f32p)
         e.anchor_idx = self.anchor_idx.ctypes.data_as(L.u32p)
         return e
 
@@ -191,7 +197,7 @@ class Codec:
         L.lib().dmcg_encoded_sizes(n, F, ctypes.byref(cc), ctypes.byref(sizes))
         out = CompressedAnimation.allocate(n, F, cfg.k_l, sizes.anchor_idx, faces,
                                            anchor_bits=cfg.anchor_bits, dict_bits=cfg.dict_bits,
-                                           diff_bits=cfg.diff_bits)
+                                           diff_bits=cfg.diff_bits, variant=cfg.variant)
         e = out.to_c()
         _check(self._ctx, L.lib().dmcg_encode(self._ctx, ctypes.byref(s), ctypes.byref(cc),
                                               ctypes.byref(e)))
@@ -238,7 +244,7 @@ class Plan:
                                                       self.faces.ctypes.data_as(L.u32p),
                                                       len(self.faces), ctypes.byref(self._cfg),
                                                       ctypes.byref(self._p)))
-        self.n_c = L.lib().dmcg_anchor_count(n, cfg.anchor_fraction)
+        self.n_c = _n_anchors(n, cfg)
         self.cfg = cfg
         codec._plans.add(self)
 
@@ -271,7 +277,7 @@ class Plan:
         out = CompressedAnimation.allocate(self.n, self.F, self.k_l, self.n_c, self.faces,
                                            anchor_bits=self.cfg.anchor_bits,
                                            dict_bits=self.cfg.dict_bits,
-                                           diff_bits=self.cfg.diff_bits)
+                                           diff_bits=self.cfg.diff_bits, variant=self.cfg.variant)
         e = out.to_c()
         _check(self.codec.handle, L.lib().dmcg_plan_download(self._p, ctypes.byref(e)))
         out.refresh_from_c(e)
@@ -347,7 +353,7 @@ def parse(data: bytes) -> CompressedAnimation:
     c = CompressedAnimation.allocate(hdr.n, hdr.F, hdr.k_l, hdr.n_c,
                                      np.zeros((hdr.n_faces, 3), np.uint32),
                                      anchor_bits=hdr.anchor_bits, dict_bits=hdr.dict_bits,
-                                     diff_bits=hdr.diff_bits)
+                                     diff_bits=hdr.diff_bits, variant=hdr.variant)
     e = c.to_c()
     rc = L.lib().dmcg_parse(buf.ctypes.data_as(L.u8p), len(buf), ctypes.byref(e), None)
     if rc:
@@ -364,6 +370,12 @@ def rate_exact(c: CompressedAnimation) -> dict:
     out = np.zeros(5)
     L.lib().dmcg_rate_exact(ctypes.byref(s), c.n, c.F, out.ctypes.data_as(L.f64p))
     return dict(zip(("q", "q_a", "q_d", "aux", "q_s"), out.tolist()))
+
+
+def _n_anchors(n, cfg) -> int:
+    """n_c of an encode (codec.cpp:374): anchored variants only."""
+    return anchor_count(n, cfg.anchor_fraction) if cfg.variant in (L.DMCG_PCA_QS, L.DMCG_PCA_QP) \
+        else 0
 
 
 def anchor_count(n: int, fraction: float = 0.01) -> int:

@@ -27,6 +27,55 @@ __global__ void k_row_params(int rows, const float* rmin, const float* rmax, con
   rowp[2 * t + 1] = q.degenerate ? 0.0 : q.width;
 }
 
+// Column sums of a row-major rows x cols block (leading dimension ld,
+// batch z via blockIdx.z), deterministic: CTA (x, y) sums rows y, y + R, ...
+// of 32 columns with a fixed 8-way split, partial[z][y][c]; the finalisers
+// below add the R partials in order.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_colsum_partial(int rows, int cols, long ld, const T* __restrict__ X0,
+                     const T* __restrict__ X1, const T* __restrict__ X2, double* partial) {
+  __shared__ double red[8][33];
+  const int z = blockIdx.z;
+  const T* X = z == 0 ? X0 : (z == 1 ? X1 : X2);
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int R = gridDim.y;
+  double s = 0.0;
+  if (c < cols)
+    for (int i = blockIdx.y * 8 + threadIdx.y; i < rows; i += R * 8) s += (double)X[(size_t)i * ld + c];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    double t = 0.0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+    partial[((size_t)z * R + blockIdx.y) * cols + c] = t;
+  }
+}
+
+// traj.row(f).mean() as float (codec.cpp:432-441): means[z][f].
+__global__ void k_means_final(int rows, int cols, int R, const double* __restrict__ partial,
+                              float* means) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, z = blockIdx.y;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int y = 0; y < R; ++y) s += partial[((size_t)z * R + y) * cols + c];
+  means[(size_t)z * cols + c] = (float)(s / (double)rows);
+}
+
+// solve_mean_constrained's shift (solver.cpp:129-131): column c = a Fw + f of
+// the n x 3Fw solution moves to the stored mean of frame f0 + f of axis a.
+__global__ void k_shift_final(int rows, int Fw, int F_all, int f0, int R,
+                              const double* __restrict__ partial, const float* __restrict__ means,
+                              double* shift) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, W = 3 * Fw;
+  if (c >= W) return;
+  double s = 0.0;
+  for (int y = 0; y < R; ++y) s += partial[(size_t)y * W + c];
+  const int a = c / Fw, f = c % Fw;
+  shift[c] = (double)means[(size_t)a * F_all + f0 + f] - s / (double)rows;
+}
+
 // dequantize_rows (codec.cpp:267-288) of all 3 k retained rows into f64
 // (row r of axis a at out[(a k + r) n]); a level beyond 2^bits flags a
 // corrupt payload.  Memory-bound pre-pass of the reconstruction GEMM, which
@@ -296,7 +345,7 @@ __global__ void k_rhs_rm(int n, int F, int W, int F_all, int f_off, const uint32
 
 template <typename T>
 __global__ void k_output_rm(int n, int F, int F_all, int f_off, const double* __restrict__ X, T* o0,
-                            T* o1, T* o2) {
+                            T* o1, T* o2, const double* __restrict__ shift) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   const long nF = (long)n * F;
   if (t >= 3 * nF) return;
@@ -304,7 +353,8 @@ __global__ void k_output_rm(int n, int F, int F_all, int f_off, const double* __
   const long rem = t % nF;
   const int i = (int)(rem / F), f = (int)(rem % F);
   T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
-  o[(size_t)i * F_all + f_off + f] = (T)X[(size_t)i * 3 * F + (size_t)a * F + f];
+  const double v = X[(size_t)i * 3 * F + (size_t)a * F + f];
+  o[(size_t)i * F_all + f_off + f] = (T)(shift ? v + shift[a * F + f] : v);
 }
 
 template <typename T>
@@ -327,6 +377,35 @@ cudaError_t launch_row_params(cudaStream_t s, int rows, const float* rmin, const
                               const uint8_t* rbits, double* rowp) {
   if (rows <= 0) return cudaSuccess;
   k_row_params<<<(rows + 255) / 256, 256, 0, s>>>(rows, rmin, rmax, rbits, rowp);
+  return cudaGetLastError();
+}
+
+static int colsum_split(int rows) {
+  const int r = (rows + 8191) / 8192;
+  return r < 1 ? 1 : (r > 64 ? 64 : r);
+}
+
+cudaError_t launch_frame_means(cudaStream_t s, int n, int F, const void* const x[3], bool f32,
+                               double* partial, float* means) {
+  const int R = colsum_split(n);
+  const dim3 grid((F + 31) / 32, R, 3), block(32, 8);
+  if (f32)
+    k_colsum_partial<float><<<grid, block, 0, s>>>(n, F, F, (const float*)x[0], (const float*)x[1],
+                                                   (const float*)x[2], partial);
+  else
+    k_colsum_partial<double><<<grid, block, 0, s>>>(n, F, F, (const double*)x[0],
+                                                    (const double*)x[1], (const double*)x[2],
+                                                    partial);
+  k_means_final<<<dim3((F + 127) / 128, 3), 128, 0, s>>>(n, F, R, partial, means);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mean_shift(cudaStream_t s, int n, int Fw, int F_all, int f0, const double* X,
+                              const float* means, double* partial, double* shift) {
+  const int W = 3 * Fw, R = colsum_split(n);
+  k_colsum_partial<double><<<dim3((W + 31) / 32, R, 1), dim3(32, 8), 0, s>>>(n, W, W, X, X, X,
+                                                                             partial);
+  k_shift_final<<<(W + 127) / 128, 128, 0, s>>>(n, Fw, F_all, f0, R, partial, means, shift);
   return cudaGetLastError();
 }
 
@@ -379,15 +458,15 @@ cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
 }
 
 cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
-                             void* const out[3], bool f32) {
+                             void* const out[3], bool f32, const double* shift) {
   const long total = 3L * n * F;
   const unsigned grid = (unsigned)((total + 255) / 256);
   if (f32)
     k_output_rm<float><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (float*)out[0], (float*)out[1],
-                                            (float*)out[2]);
+                                            (float*)out[2], shift);
   else
     k_output_rm<double><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (double*)out[0],
-                                             (double*)out[1], (double*)out[2]);
+                                             (double*)out[1], (double*)out[2], shift);
   return cudaGetLastError();
 }
 

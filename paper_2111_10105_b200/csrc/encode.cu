@@ -2,6 +2,7 @@
 // Compiled with --fmad=false (and explicit _rn intrinsics) because the
 // reference Release build has no FMA contraction (CMakeLists.txt:7-9).
 #include <cfloat>
+#include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -58,6 +59,19 @@ __global__ void __launch_bounds__(kDeltaWarps * 32)
     }
   }
   if (bad) atomicOr(flags, 1 << a);
+}
+
+// validate_sequence's finiteness check for the variants without K1 (v2v),
+// which otherwise rides on k_delta.
+template <typename T>
+__global__ void k_check_finite(long nF, const T* __restrict__ x0, const T* __restrict__ x1,
+                               const T* __restrict__ x2, int* flags) {
+  const int a = blockIdx.y;
+  const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
+  bool bad = false;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < nF; t += (long)gridDim.x * blockDim.x)
+    bad |= !isfinite((double)X[t]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, 1 << a);
 }
 
 // Gram reduction: S = sum of split-K partials in split order, then
@@ -257,6 +271,19 @@ cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
     k_delta<double><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const double*)x[0],
                                                       (const double*)x[1], (const double*)x[2],
                                                       delta, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(cudaStream_t s, int n, int F, const void* const x[3], bool f32,
+                                int* flags) {
+  const long nF = (long)n * F;
+  const dim3 grid((unsigned)std::min<long>((nF + 255) / 256, 1024), 3);
+  if (f32)
+    k_check_finite<float><<<grid, 256, 0, s>>>(nF, (const float*)x[0], (const float*)x[1],
+                                               (const float*)x[2], flags);
+  else
+    k_check_finite<double><<<grid, 256, 0, s>>>(nF, (const double*)x[0], (const double*)x[1],
+                                                (const double*)x[2], flags);
   return cudaGetLastError();
 }
 

@@ -236,6 +236,26 @@ void build_normal_matrix(MeshHost* m) {
   }
 }
 
+void build_reduced_normal(MeshHost* m) {
+  build_normal_matrix(m);  // L^T L: no anchors on the anchor-free variants
+  const uint32_t n = m->n;
+  std::vector<uint32_t> rp(n, 0), ci;
+  std::vector<float> va;
+  ci.reserve(m->m_ci.size());
+  va.reserve(m->m_ci.size());
+  for (uint32_t i = 1; i < n; ++i) {
+    for (uint32_t p = m->m_rp[i]; p < m->m_rp[i + 1]; ++p)
+      if (m->m_ci[p] > 0) {
+        ci.push_back(m->m_ci[p] - 1);
+        va.push_back(m->m_val[p]);
+      }
+    rp[i] = (uint32_t)ci.size();
+  }
+  m->m_rp = std::move(rp);
+  m->m_ci = std::move(ci);
+  m->m_val = std::move(va);
+}
+
 uint64_t hash_faces(const uint32_t* faces, uint32_t n_faces) {
   uint64_t h = 1469598103934665603ull;  // FNV-1a over the index words
   for (size_t t = 0; t < 3 * (size_t)n_faces; ++t) {
@@ -326,8 +346,10 @@ Status check_config(const dmcg_config& cfg, uint32_t n, uint32_t k, std::vector<
       return {DMCG_E_CONFIG,
               "InvalidBits: row bit depth " + std::to_string(bits) + " outside 1..16"};
   // Scope of the B200 path.
-  if (cfg.variant != DMCG_PCA_QP)
-    return {DMCG_E_UNSUPPORTED, "Unsupported: only variant pca_qp is on the B200 path"};
+  if (cfg.variant < DMCG_PCA || cfg.variant > DMCG_PCA_QP)
+    return {DMCG_E_UNSUPPORTED,
+            "Unsupported: only the n_b = 1 variants pca, pca_q, v2v, pca_qs, pca_qp are on the "
+            "B200 path"};
   if (cfg.raw_payload) return {DMCG_E_UNSUPPORTED, "Unsupported: raw_payload debug mode"};
   if (cfg.laplacian != 0)
     return {DMCG_E_UNSUPPORTED, "Unsupported: only the combinatorial Laplacian"};
@@ -455,8 +477,10 @@ int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_size
   out->dict_q = (size_t)F * F;
   out->rows = cfg->k_l;
   out->coeff_q = (size_t)cfg->k_l * n;
-  out->anchor_idx = dmcg_anchor_count(n, cfg->anchor_fraction);
+  out->anchor_idx =
+      variant_uses_anchors(cfg->variant) ? dmcg_anchor_count(n, cfg->anchor_fraction) : 0;
   out->anchor_q = out->anchor_idx * (size_t)F;
+  out->means = variant_uses_means(cfg->variant) ? F : 0;
   return DMCG_OK;
 }
 
@@ -527,6 +551,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     return st;
   }
   p->k = cfg->k_l;
+  p->variant = cfg->variant;
   p->rounds = cfg->oi_rounds;
   p->oi_seed = cfg->oi_seed;
   p->implicit = cfg->oi_implicit != 0;
@@ -534,7 +559,9 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->dict_bits = cfg->dict_bits;
   p->diff_bits = cfg->diff_bits;
   // anchors (codec.cpp:374, 445)
-  if (anchors_given) {
+  if (!variant_uses_anchors(p->variant)) {
+    p->n_c = 0;  // anchor-free variants (codec.cpp:374)
+  } else if (anchors_given) {
     p->n_c = n_c_given;
     p->mesh.anchors.assign(anchors_given, anchors_given + n_c_given);
   } else {
@@ -592,6 +619,8 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_row_bits = (uint8_t*)get(4 * kk);
   p->d_coeff_q = (uint16_t*)get(3 * kk * n * 2);
   p->d_anchor_rng = (float*)get(6 * 4);
+  p->d_means = (float*)get(3 * (size_t)F * 4);
+  p->d_colsum = (double*)get(3 * 64 * 3 * (size_t)F * 8);
   p->d_anchor_q = (uint16_t*)get(3 * (size_t)p->n_c * F * 2);
   p->d_rowp = (double*)get(3 * kk * 2 * 8);
   p->d_cg_iters = (int*)get(p->W_pad * 4);
@@ -647,7 +676,12 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
 dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
   if (p->d_m_rp) return Status::ok();
   PhaseTimer tm("normal");
-  if (!p->chol_given) build_normal_matrix(&p->mesh);
+  if (!p->chol_given) {
+    if (variant_uses_means(p->variant))
+      build_reduced_normal(&p->mesh);
+    else
+      build_normal_matrix(&p->mesh);
+  }
   tm.lap("build");
   const MeshHost& m = p->mesh;
   p->stats.nnz_normal = (long long)m.m_ci.size();
@@ -671,12 +705,22 @@ dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
 dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   if (p->decode_ready) return Status::ok();
   PhaseTimer tm("prepare");
+  if (p->variant == DMCG_V2V) {  // no solve: the reconstruction buffers only
+    const size_t nW = (size_t)p->n * p->W;
+    p->d_rm_delta = (double*)plan_alloc(p, nW * 8);
+    p->d_Ud = (double*)plan_alloc(p, 3 * (size_t)std::max<uint32_t>(p->k, 1) * p->F * 8);
+    if (!p->d_rm_delta || !p->d_Ud) return {DMCG_E_CUDA, "CudaError: device allocation failed"};
+    p->decode_ready = true;
+    return Status::ok();
+  }
   {
     Status sn = plan_prepare_normal(p);
     if (!sn.good()) return sn;
   }
   tm.lap("normal matrix");
   const uint32_t n = p->n;
+  // the anchor-free variants solve with vertex 0 pinned: n - 1 unknowns
+  const uint32_t nm = variant_uses_means(p->variant) ? n - 1 : n;
   const MeshHost& m = p->mesh;
   bool ok = true;
   auto get = [&](size_t bytes) {
@@ -687,7 +731,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   // direct solver: symbolic analysis of M (host) + device structures
   {
     const auto t0 = std::chrono::steady_clock::now();
-    if (!p->chol_given) chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p->chol);
+    if (!p->chol_given) chol_analyze(nm, m.m_rp, m.m_ci, m.m_val, &p->chol);
     p->analyze_seconds = p->chol_given
                              ? p->analyze_seconds
                              : std::chrono::duration<double>(std::chrono::steady_clock::now() - t0)
@@ -704,7 +748,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   p->d_rm_r = (double*)get(nW * 8);
   p->d_Ud = (double*)get(3 * (size_t)std::max<uint32_t>(p->k, 1) * p->F * 8);
   CholDev& cd = p->cdev;
-  cd.n = n;
+  cd.n = nm;
   cd.nsup = cp.nsup;
   cd.W = p->W;
   cd.first = (const uint32_t*)get(cp.first.size() * 4);
@@ -838,6 +882,10 @@ int dmcg_plan_create_shard(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, con
   if (!ctx || !plan || !cfg || nranks < 1 || rank < 0 || rank >= nranks) return DMCG_E_CONFIG;
   if (n < (uint32_t)nranks)
     return ctx->set_error({DMCG_E_CONFIG, "ConfigError: fewer vertices than ranks"});
+  if (variant_uses_means(cfg->variant))
+    return ctx->set_error({DMCG_E_UNSUPPORTED,
+                           "Unsupported: vertex-row shards of the pca / pca_q variants (their "
+                           "frame means need a cross-rank reduction)"});
   if (comm && (comm_size(comm) != nranks || comm_rank(comm) != rank))
     return ctx->set_error({DMCG_E_CONFIG, "ConfigError: communicator does not match rank"});
   cudaSetDevice(ctx->device);
@@ -897,7 +945,7 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
   e->k_l = p->k;
   e->n_c = p->n_c;
   e->n_faces = p->n_faces;
-  e->variant = DMCG_PCA_QP;
+  e->variant = (uint8_t)p->variant;
   e->flags = 0;
   e->anchor_bits = (uint8_t)p->anchor_bits;
   e->dict_bits = (uint8_t)p->dict_bits;
@@ -913,12 +961,17 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
       CUDA_OK(cudaMemcpyAsync(e->coeff_q[a], p->d_coeff_q + a * k * n, k * n * 2,
                               cudaMemcpyDeviceToHost, s));
     }
-    CUDA_OK(cudaMemcpyAsync(e->anchor_q[a], p->d_anchor_q + a * (size_t)p->n_c * F,
-                            (size_t)p->n_c * F * 2, cudaMemcpyDeviceToHost, s));
+    if (p->n_c)
+      CUDA_OK(cudaMemcpyAsync(e->anchor_q[a], p->d_anchor_q + a * (size_t)p->n_c * F,
+                              (size_t)p->n_c * F * 2, cudaMemcpyDeviceToHost, s));
+    if (variant_uses_means(p->variant) && e->means[a])
+      CUDA_OK(cudaMemcpyAsync(e->means[a], p->d_means + a * F, F * 4, cudaMemcpyDeviceToHost, s));
   }
-  CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
+  std::memset(rng, 0, sizeof(rng));
+  if (p->n_c)
+    CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaStreamSynchronize(s));
-  std::memcpy(e->anchor_idx, p->mesh.anchors.data(), (size_t)p->n_c * 4);
+  if (p->n_c) std::memcpy(e->anchor_idx, p->mesh.anchors.data(), (size_t)p->n_c * 4);
   for (int a = 0; a < 3; ++a) {
     e->anchor_min[a] = rng[2 * a];
     e->anchor_max[a] = rng[2 * a + 1];
@@ -945,13 +998,16 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
   const size_t n = p->n, F = p->F, k = p->k;
   std::vector<float> rmin(3 * k + 1), rmax(3 * k + 1);
   std::vector<uint8_t> rbits(3 * k + 1);
-  float rng[6];
+  float rng[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<float> means(3 * F);
   if (k) {
     CUDA_OK(cudaMemcpyAsync(rmin.data(), p->d_row_min, 3 * k * 4, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaMemcpyAsync(rmax.data(), p->d_row_max, 3 * k * 4, cudaMemcpyDeviceToHost, s));
     CUDA_OK(cudaMemcpyAsync(rbits.data(), p->d_row_bits, 3 * k, cudaMemcpyDeviceToHost, s));
   }
-  CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
+  if (p->n_c) CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
+  if (variant_uses_means(p->variant))
+    CUDA_OK(cudaMemcpyAsync(means.data(), p->d_means, 3 * F * 4, cudaMemcpyDeviceToHost, s));
   CUDA_OK(cudaStreamSynchronize(s));
   dmcg_encoded m;
   std::memset(&m, 0, sizeof(m));
@@ -960,7 +1016,7 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
   m.k_l = p->k;
   m.n_c = p->n_c;
   m.n_faces = p->n_faces;
-  m.variant = DMCG_PCA_QP;
+  m.variant = (uint8_t)p->variant;
   m.anchor_bits = (uint8_t)p->anchor_bits;
   m.dict_bits = (uint8_t)p->dict_bits;
   m.diff_bits = (uint8_t)p->diff_bits;
@@ -972,8 +1028,9 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
     m.row_bits[a] = rbits.data() + a * k;
     m.anchor_min[a] = rng[2 * a];
     m.anchor_max[a] = rng[2 * a + 1];
+    m.means[a] = means.data() + a * F;
   }
-  PayloadSpans sp;
+  PayloadSpans sp{};
   const size_t total = serialize_stream(&m, nullptr, 0, sec, &sp);
   *size = total;
   if (!out) return Status::ok();
@@ -1007,8 +1064,9 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
     if (k)
       CUDA_OK(launch_pack_rows(s, p->d_coeff_q + a * k * n, (long)n, (int)k, p->d_row_bits + a * k,
                                p->d_row_bitoff + a * k, sp.coeff[a], p->d_stream));
-    CUDA_OK(launch_pack_uniform(s, p->d_anchor_q + a * (size_t)p->n_c * F, (long)p->n_c * F,
-                                p->anchor_bits, sp.anchor[a], p->d_stream));
+    if (p->n_c)
+      CUDA_OK(launch_pack_uniform(s, p->d_anchor_q + a * (size_t)p->n_c * F, (long)p->n_c * F,
+                                  p->anchor_bits, sp.anchor[a], p->d_stream));
   }
   const uint8_t* dev = (const uint8_t*)p->d_stream;
   auto span_copy = [&](size_t off0, size_t bytes) -> cudaError_t {
@@ -1040,8 +1098,13 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
       CUDA_OK(cudaMemcpyAsync(p->d_coeff_q + a * k * n, e->coeff_q[a], k * n * 2,
                               cudaMemcpyHostToDevice, s));
     }
-    CUDA_OK(cudaMemcpyAsync(p->d_anchor_q + a * (size_t)p->n_c * F, e->anchor_q[a],
-                            (size_t)p->n_c * F * 2, cudaMemcpyHostToDevice, s));
+    if (p->n_c)
+      CUDA_OK(cudaMemcpyAsync(p->d_anchor_q + a * (size_t)p->n_c * F, e->anchor_q[a],
+                              (size_t)p->n_c * F * 2, cudaMemcpyHostToDevice, s));
+    if (variant_uses_means(p->variant)) {
+      if (!e->means[a]) return {DMCG_E_CORRUPT, "CorruptPayload: missing frame means"};
+      CUDA_OK(cudaMemcpyAsync(p->d_means + a * F, e->means[a], F * 4, cudaMemcpyHostToDevice, s));
+    }
     rng[2 * a] = e->anchor_min[a];
     rng[2 * a + 1] = e->anchor_max[a];
   }
@@ -1121,7 +1184,7 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   {  // the decoder's analysis of this mesh, overlapped with the GPU encode
     ctx->pending.reset();
     static const bool off = std::getenv("DMCG_NO_OVERLAP") != nullptr;
-    if (!off) {
+    if (!off && cfg->variant != DMCG_V2V) {  // v2v decodes without a solve
       auto pa = std::make_unique<PendingAnalysis>();
       pa->n = seq->n;
       pa->n_faces = seq->n_faces;
@@ -1131,11 +1194,16 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
       pa->mesh.lap_rp = p->mesh.lap_rp;
       pa->mesh.lap_ci = p->mesh.lap_ci;
       pa->mesh.anchor_pos = p->mesh.anchor_pos;
+      pa->reduced = variant_uses_means(cfg->variant);
       PendingAnalysis* raw = pa.get();
       pa->th = std::thread([raw] {
         const auto t0 = std::chrono::steady_clock::now();
-        build_normal_matrix(&raw->mesh);
-        chol_analyze(raw->n, raw->mesh.m_rp, raw->mesh.m_ci, raw->mesh.m_val, &raw->chol);
+        if (raw->reduced)
+          build_reduced_normal(&raw->mesh);
+        else
+          build_normal_matrix(&raw->mesh);
+        chol_analyze(raw->n - (raw->reduced ? 1 : 0), raw->mesh.m_rp, raw->mesh.m_ci,
+                     raw->mesh.m_val, &raw->chol);
         raw->seconds =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       });
@@ -1172,17 +1240,24 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   cudaSetDevice(ctx->device);
   // Header sanity (the same bounds parse() enforces, stream.cpp:322-336).
   if (in->n < 1 || in->F < 1) return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: empty animation"});
-  if (in->variant != DMCG_PCA_QP)
-    return ctx->set_error({DMCG_E_UNSUPPORTED, "Unsupported: only variant pca_qp is on the B200 path"});
+  if (in->variant > DMCG_PCA_QP)
+    return ctx->set_error({DMCG_E_UNSUPPORTED,
+                           "Unsupported: only the n_b = 1 variants pca, pca_q, v2v, pca_qs, pca_qp "
+                           "are on the B200 path"});
   if (in->k_l > in->F)
     return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: retained row count exceeds dictionary dimension"});
-  if (in->n_c < 1 || in->n_c > in->n)
+  if (variant_uses_anchors(in->variant) ? (in->n_c < 1 || in->n_c > in->n) : in->n_c != 0)
     return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: anchor count out of range"});
+  if (variant_uses_means(in->variant))
+    for (int a = 0; a < 3; ++a)
+      if (!in->means[a])
+        return ctx->set_error({DMCG_E_CORRUPT, "CorruptPayload: missing frame means"});
   for (uint32_t t = 0; t < in->n_c; ++t)
     if (in->anchor_idx[t] >= in->n || (t && in->anchor_idx[t] <= in->anchor_idx[t - 1]))
       return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: anchor indices invalid"});
   dmcg_config cfg;
   dmcg_config_default(&cfg);
+  cfg.variant = in->variant;
   cfg.k_l = in->k_l;
   std::vector<int> rb(in->k_l, 16);
   for (uint32_t r = 0; r < in->k_l; ++r) {
@@ -1201,6 +1276,7 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   // and only when mesh and anchors match.
   std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
   if (pa && !(pa->n == in->n && pa->n_faces == in->n_faces &&
+              pa->reduced == variant_uses_means(in->variant) &&
               pa->anchors.size() == in->n_c &&
               std::equal(pa->anchors.begin(), pa->anchors.end(), in->anchor_idx) &&
               pa->faces_hash == hash_faces(in->faces, in->n_faces)))

@@ -16,6 +16,11 @@
 
 namespace dmcg {
 
+// Variant predicates (include/dmc/stream.hpp:77-84), n_b = 1 variants.
+inline bool variant_uses_anchors(int v) { return v == DMCG_PCA_QS || v == DMCG_PCA_QP; }
+inline bool variant_uses_means(int v) { return v == DMCG_PCA || v == DMCG_PCA_Q; }
+inline bool variant_uses_delta(int v) { return v != DMCG_V2V; }
+
 struct Status {
   int code = 0;
   std::string msg;
@@ -52,6 +57,9 @@ struct MeshHost {
 Status build_mesh(const uint32_t* faces, uint32_t n_faces, uint32_t n, MeshHost* out);
 Status validate_mesh(const MeshHost& m);   // isolated / connected (mesh.cpp:108-136)
 void build_normal_matrix(MeshHost* m);     // needs anchors set
+// (L^T L)[1:, 1:]: the normal matrix of solve_mean_constrained
+// (solver.cpp:116-117), n - 1 rows (vertex i at row i - 1).
+void build_reduced_normal(MeshHost* m);
 
 }  // namespace dmcg
 
@@ -80,6 +88,7 @@ namespace dmcg {
 // mesh and anchors takes the result (once) instead of recomputing it.
 struct PendingAnalysis {
   uint32_t n = 0, n_faces = 0;
+  bool reduced = false;  // (L^T L)[1:, 1:] of the anchor-free variants, else L^T L + S^T S
   uint64_t faces_hash = 0;
   std::vector<uint32_t> anchors;
   MeshHost mesh;    // lap_rp / lap_ci / anchor_pos in, m_rp / m_ci / m_val out
@@ -187,6 +196,7 @@ struct dmcg_plan {
   int rounds = 0;
   int anchor_bits = 16, dict_bits = 16, diff_bits = 8;
   uint64_t oi_seed = 0;
+  int variant = DMCG_PCA_QP;        // pca / pca_q / v2v / pca_qs / pca_qp
   bool implicit = false;            // dmcg_config.oi_implicit
   std::vector<int> row_bits;
   std::vector<uint32_t> faces;
@@ -220,6 +230,8 @@ struct dmcg_plan {
   uint8_t* d_row_bits = nullptr;   // 3 x k
   uint16_t* d_coeff_q = nullptr;   // 3 x k x n
   float* d_anchor_rng = nullptr;   // 3 x 2
+  float* d_means = nullptr;        // 3 x F per-frame vertex means (pca / pca_q)
+  double* d_colsum = nullptr;      // column-sum partials (3 x 64 x 3F) of the means / shift
   uint16_t* d_anchor_q = nullptr;  // 3 x n_c x F
   // decode
   double* d_rowp = nullptr;        // 3 x k x 2 (min_, width) dequantiser params

@@ -13,6 +13,9 @@ namespace dmcg {
 cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
                          const uint32_t* lap_ci, const void* const x[3], bool f32, double* delta,
                          int* flags);
+// flags[0] |= 1 << axis on a non-finite coordinate (v2v: no K1 pass).
+cudaError_t launch_check_finite(cudaStream_t s, int n, int F, const void* const x[3], bool f32,
+                                int* flags);
 // Sum split-K Gram partials in split order and symmetrise (spectral.cpp:37-38).
 cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, const double* part,
                               double* R);
@@ -118,6 +121,14 @@ cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
                           int n_c, const uint16_t* anchor_q, const float* anchor_rng,
                           int anchor_bits, const double* D, double* B, int* flags);
 cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
-                             void* const out[3], bool f32);
+                             void* const out[3], bool f32, const double* shift = nullptr);
+// Anchor-free variants (pca / pca_q): per-frame vertex means of the input
+// (codec.cpp:432-441) -> means (3 x F floats); the per-column shift of the
+// mean-constrained solution (solver.cpp:129-131) -> shift (3 Fw doubles).
+// partial: scratch of 3 x 64 x max(F, 3 Fw) doubles.
+cudaError_t launch_frame_means(cudaStream_t s, int n, int F, const void* const x[3], bool f32,
+                               double* partial, float* means);
+cudaError_t launch_mean_shift(cudaStream_t s, int n, int Fw, int F_all, int f0, const double* X,
+                              const float* means, double* partial, double* shift);
 
 }  // namespace dmcg

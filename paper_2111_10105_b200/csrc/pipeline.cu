@@ -279,8 +279,11 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   const long FF = (long)F * F;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
   DMCG_TRY(record_event(p->ev[0], s));
-  // K1 delta coordinates (codec.cpp:419).
-  DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
+  // K1 delta coordinates (codec.cpp:419); v2v codes the trajectories.
+  if (variant_uses_delta(p->variant))
+    DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
+  else
+    DMCG_TRY(launch_check_finite(s, n, F, x, f32, p->d_flags));
   DMCG_TRY(record_event(p->ev[1], s));
   // K2 autocorrelation (spectral.cpp:35-39); the implicit OI never forms it.
   Status st = Status::ok();
@@ -297,15 +300,29 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   if (k > 0) {
     DMCG_TRY(launch_init_keys(s, 3L * k, p->d_keys));
     LoadDense<double, true> lU{p->d_U, FF, 1L, (long)F};
-    LoadDense<double, true> lD{p->d_delta, (long)n * F, 1L, (long)F};
-    DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lD, StoreCoeffMinMax{p->d_C, p->d_keys}));
+    StoreCoeffMinMax ep{p->d_C, p->d_keys};
+    if (variant_uses_delta(p->variant)) {
+      LoadDense<double, true> lD{p->d_delta, (long)n * F, 1L, (long)F};
+      DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lD, ep));
+    } else if (f32) {  // v2v: coeffs = U^T traj (codec.cpp:416-417)
+      LoadDense3<float, true> lX{(const float*)x[0], (const float*)x[1], (const float*)x[2], 1L,
+                                 (long)F};
+      DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lX, ep));
+    } else {
+      LoadDense3<double, true> lX{(const double*)x[0], (const double*)x[1], (const double*)x[2],
+                                  1L, (long)F};
+      DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lX, ep));
+    }
     DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
                                p->d_row_max, p->d_row_bits, p->d_coeff_q));
   }
   DMCG_TRY(record_event(p->ev[4], s));
-  // K5b anchors (codec.cpp:444-471).
-  DMCG_TRY(launch_anchors(s, (int)p->n_c, F, p->d_anchor_idx, x, f32, p->anchor_bits,
-                          p->d_anchor_rng, p->d_anchor_q));
+  // K5b anchors (codec.cpp:444-471) or the per-frame means (codec.cpp:432-441).
+  if (p->n_c)
+    DMCG_TRY(launch_anchors(s, (int)p->n_c, F, p->d_anchor_idx, x, f32, p->anchor_bits,
+                            p->d_anchor_rng, p->d_anchor_q));
+  if (variant_uses_means(p->variant))
+    DMCG_TRY(launch_frame_means(s, n, F, x, f32, p->d_colsum, p->d_means));
   // K5a dictionary levels (encode_dictionaries first block), after the
   // completion joined back from the side stream.
   if (p->forked) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
@@ -429,8 +446,11 @@ Status shard_phase(dmcg_plan* p, int phase, const void* const x[3]) {
     case 0: {
       DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
       DMCG_TRY(record_event(p->ev[0], s));
-      DMCG_TRY(launch_delta(s, n_own, F, sh.d_loc_rp, sh.d_loc_ci, x, f32, p->d_delta,
-                            p->d_flags));
+      if (variant_uses_delta(p->variant))
+        DMCG_TRY(launch_delta(s, n_own, F, sh.d_loc_rp, sh.d_loc_ci, x, f32, p->d_delta,
+                              p->d_flags));
+      else
+        DMCG_TRY(launch_check_finite(s, n_own, F, x, f32, p->d_flags));
       DMCG_TRY(record_event(p->ev[1], s));
       if (implicit_oi(p)) return Status::ok();
       Status st = f32 ? gram<float>(p, x, n_own) : gram<double>(p, x, n_own);
@@ -450,8 +470,19 @@ Status shard_phase(dmcg_plan* p, int phase, const void* const x[3]) {
       DMCG_TRY(launch_init_keys(s, krows, sh.d_keys));
       if (k > 0) {
         LoadDense<double, true> lU{p->d_U, FF, 1L, (long)F};
-        LoadDense<double, true> lD{p->d_delta, (long)n_own * F, 1L, (long)F};
-        DMCG_TRY(launch_gemm(s, 3, k, n_own, F, 1, lU, lD, StoreCoeffMinMax{p->d_C, sh.d_keys}));
+        StoreCoeffMinMax ep{p->d_C, sh.d_keys};
+        if (variant_uses_delta(p->variant)) {
+          LoadDense<double, true> lD{p->d_delta, (long)n_own * F, 1L, (long)F};
+          DMCG_TRY(launch_gemm(s, 3, k, n_own, F, 1, lU, lD, ep));
+        } else if (f32) {  // v2v: the owned rows of the trajectories
+          LoadDense3<float, true> lX{(const float*)x[0], (const float*)x[1], (const float*)x[2],
+                                     1L, (long)F};
+          DMCG_TRY(launch_gemm(s, 3, k, n_own, F, 1, lU, lX, ep));
+        } else {
+          LoadDense3<double, true> lX{(const double*)x[0], (const double*)x[1],
+                                      (const double*)x[2], 1L, (long)F};
+          DMCG_TRY(launch_gemm(s, 3, k, n_own, F, 1, lU, lX, ep));
+        }
       }
       DMCG_TRY(launch_anchor_keys(s, na, F, sh.d_loc_anchor, x, f32, sh.d_keys + 6L * k));
       DMCG_TRY(launch_flip_min_keys(s, krows, sh.d_keys));
@@ -572,6 +603,18 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
   } else {
     DMCG_TRY(cudaMemsetAsync(p->d_rm_delta, 0, nW * sizeof(double), s));
   }
+  if (p->variant == DMCG_V2V) {  // axes = U~ c~ (codec.cpp:520-524): no solve
+    DMCG_TRY(record_event(p->ev[1], s));
+    DMCG_TRY(cudaEventRecord(p->ev_join, s));
+    s = s1;
+    DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
+    for (int e : {2, 5, 3}) DMCG_TRY(record_event(p->ev[e], s));
+    DMCG_TRY(launch_output_rm(s, n, F, F_all, f0, p->d_rm_delta, out, f32));
+    DMCG_TRY(record_event(p->ev[4], s));
+    return Status::ok();
+  }
+  // rhs = L^T delta~ (+ S^T a): every row of L delta~ (anchor slots -1 on the
+  // anchor-free variants, whose reduced system uses rows 1.. only).
   DMCG_TRY(launch_rhs_rm(s, n, F, F_all, f0, p->d_lap_rp, p->d_lap_ci, p->d_anchor_pos, (int)p->n_c,
                          p->d_anchor_q, p->d_anchor_rng, p->anchor_bits, p->d_rm_delta, p->d_rm_b,
                          p->d_flags + 1));
@@ -582,16 +625,28 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
   DMCG_TRY(record_event(p->ev[2], s));
   DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
   DMCG_TRY(record_event(p->ev[5], s));
-  DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_b, p->d_rm_y, p->d_rm_xp));
-  DMCG_TRY(chol_unpermute(s, n, W, cdev.perm, p->d_rm_xp, p->d_rm_x, false));
+  // solve_anchored (solver.cpp:62-90) on all n rows, or solve_mean_constrained
+  // (solver.cpp:105-133): vertex 0 pinned, unknowns = rows 1.. (offset W).
+  const bool mc = variant_uses_means(p->variant);
+  const int nm = (int)cdev.n;
+  const size_t o = mc ? (size_t)W : 0;
+  DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_b + o, p->d_rm_y, p->d_rm_xp));
+  DMCG_TRY(chol_unpermute(s, nm, W, cdev.perm, p->d_rm_xp, p->d_rm_x + o, false));
   for (int r = 0; r < refine; ++r) {
-    DMCG_TRY(normal_residual(s, n, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b, p->d_rm_x,
-                             p->d_rm_r));
+    DMCG_TRY(normal_residual(s, nm, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b + o,
+                             p->d_rm_x + o, p->d_rm_r));
     DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp));
-    DMCG_TRY(chol_unpermute(s, n, W, cdev.perm, p->d_rm_xp, p->d_rm_x, true));
+    DMCG_TRY(chol_unpermute(s, nm, W, cdev.perm, p->d_rm_xp, p->d_rm_x + o, true));
   }
   DMCG_TRY(record_event(p->ev[3], s));
-  DMCG_TRY(launch_output_rm(s, n, F, F_all, f0, p->d_rm_x, out, f32));
+  const double* shift = nullptr;
+  if (mc) {  // x = [0; z], each column moved to its stored mean
+    DMCG_TRY(cudaMemsetAsync(p->d_rm_x, 0, (size_t)W * sizeof(double), s));
+    double* sh = p->d_colsum + 64 * (size_t)W;  // after the (<= 64) row-chunk partials
+    DMCG_TRY(launch_mean_shift(s, n, F, F_all, f0, p->d_rm_x, p->d_means, p->d_colsum, sh));
+    shift = sh;
+  }
+  DMCG_TRY(launch_output_rm(s, n, F, F_all, f0, p->d_rm_x, out, f32, shift));
   DMCG_TRY(record_event(p->ev[4], s));
   return Status::ok();
 }
@@ -650,6 +705,9 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
 }
 
 Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]) {
+  if (opt && opt->solver != 0 && !variant_uses_anchors(p->variant))
+    return Status{DMCG_E_UNSUPPORTED,
+                  "Unsupported: the CG solver serves the anchored variants only (pca_qp, pca_qs)"};
   if (!opt || opt->solver == 0) {
     Status st = plan_prepare_decode(p);
     if (!st.good()) return st;

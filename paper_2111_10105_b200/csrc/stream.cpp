@@ -136,7 +136,7 @@ size_t dmcg::serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, d
   const char magic[4] = {'D', 'M', 'C', '1'};
   for (char c : magic) w.u8((uint8_t)c);
   w.u16(1);  // kStreamVersion
-  w.u8(DMCG_PCA_QP);
+  w.u8(e->variant);
   w.u8(0);   // flags
   w.u32(e->n);
   w.u32(e->F);
@@ -189,6 +189,15 @@ size_t dmcg::serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, d
       b.flush();
     }
     sz.coeff_payload += w.pos - start;
+    if (variant_uses_means(e->variant)) {  // stream.cpp:255-263
+      start = w.pos;
+      for (uint32_t f = 0; f < e->F; ++f) w.f32(e->means[a][f]);
+      sz.means += w.pos - start;
+    }
+  }
+  if (!variant_uses_anchors(e->variant)) {
+    if (s) *s = sz;
+    return w.overflow ? 0 : w.pos;
   }
   size_t start = w.pos;
   for (uint32_t t = 0; t < e->n_c; ++t) w.u32(e->anchor_idx[t]);
@@ -267,8 +276,9 @@ static int parse_header_impl(ByteIn& r, dmcg_encoded* c, std::string* msg) {
   }
   if (!(db >= 1 && db <= 16)) return corrupt("dictionary bit depth outside 1..16");
   if (!(fb >= 1 && fb <= 16)) return corrupt("difference bit depth outside 1..16");
-  if (variant != DMCG_PCA_QP || n_b != 1 || flags != 0) {
-    *msg = "Unsupported: only pca_qp, n_b = 1, quantised streams are on the B200 path";
+  if (variant > DMCG_PCA_QP || n_b != 1 || flags != 0) {
+    *msg = "Unsupported: only the n_b = 1 variants pca, pca_q, v2v, pca_qs, pca_qp with "
+           "quantised payloads are on the B200 path";
     return DMCG_E_UNSUPPORTED;
   }
   c->n = n;
@@ -370,6 +380,20 @@ int dmcg_parse(const uint8_t* data, size_t size, dmcg_encoded* c, dmcg_sections*
       }
     }
     sz.coeff_payload += r.pos - start;
+    if (dmcg::variant_uses_means(c->variant)) {
+      start = r.pos;
+      for (uint32_t f = 0; f < c->F; ++f) {
+        const float m = r.f32();
+        if (c->means[a]) c->means[a][f] = m;
+      }
+      if (!r.err.empty()) return corrupt(r.err);
+      sz.means += r.pos - start;
+    }
+  }
+  if (!dmcg::variant_uses_anchors(c->variant)) {
+    if (r.pos != size) return corrupt("trailing bytes after stream end");
+    if (s) *s = sz;
+    return DMCG_OK;
   }
   size_t start = r.pos;
   uint32_t prev = 0;

@@ -143,7 +143,8 @@ def _shard_plan_class():
                 codec.handle, n, F, self.dtype, self.faces.ctypes.data_as(L.u32p),
                 len(self.faces), ctypes.byref(self._cfg), nranks, rank,
                 comm.handle if comm is not None else None, ctypes.byref(self._p)))
-            self.n_c = L.lib().dmcg_anchor_count(n, cfg.anchor_fraction)
+            self.n_c = L.lib().dmcg_anchor_count(n, cfg.anchor_fraction) \
+                if cfg.variant in (L.DMCG_PCA_QS, L.DMCG_PCA_QP) else 0
             self.cfg = cfg
             codec._plans.add(self)
             info = L.DmcgShardInfo()

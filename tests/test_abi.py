@@ -139,10 +139,40 @@ def test_parse_strictness():  # stream.cpp:294-469, SPEC.md:527 (acceptance 7)
 
 def test_parse_rejects_other_variants():
     data = bytearray(G["stream"].tobytes())
-    data[6] = 3  # pca_qs: valid in the reference, outside the B200 path
+    data[6] = 5  # blocks: valid in the reference, outside the B200 path
     with pytest.raises(C.DmcError) as e:
         C.parse(bytes(data))
     assert e.value.code == 11
+    data[6] = 6  # per_mesh_gft: anchor-free, so these header bytes are corrupt for it
+    with pytest.raises(C.DmcError) as e:
+        C.parse(bytes(data))
+    assert e.value.code == 6 and "anchor count nonzero" in str(e.value)
+
+
+def test_parse_accepts_pca_qs_stream():
+    """pca_qs (variant 3) has pca_qp's layout; only the solve mode differs."""
+    data = bytearray(G["stream"].tobytes())
+    data[6] = 3
+    c = C.parse(bytes(data))
+    assert c.variant == 3 and C.serialize(c)[0] == bytes(data)
+
+
+@pytest.mark.parametrize("variant", ["pca", "pca_q", "v2v", "pca_qs"])
+def test_variant_streams_match_oracle_bytes(variant):
+    """dmcg_parse / dmcg_serialize of the anchor-free and serial variants
+    (stream.cpp:245-292, 410-469) round-trip the oracle's DMC1 bytes."""
+    import pyoracle as O
+    from paper_2111_10105_b200 import synth
+    s = synth.sphere(2, 16, 3, 0, seed=11)
+    o = O.encode(s, 8, 12, rounds=4, variant=variant)
+    ob, osec = O.serialize(o)
+    c = C.parse(ob)
+    assert c.variant == O.VARIANTS[variant] and c.n_c == (2 if variant == "pca_qs" else 0)
+    cb, csec = C.serialize(c)
+    assert cb == ob and csec == osec
+    if variant in ("pca", "pca_q"):
+        assert osec["means"] == 3 * 16 * 4
+        assert all(np.array_equal(c.means[a], o.means[a]) for a in range(3))
 
 
 def test_codec_without_gpu_fails_loudly():

@@ -21,10 +21,10 @@ from paper_2111_10105_b200 import synth
 pytestmark = pytest.mark.gpu
 
 
-def _cfg(cfgspec, rounds=None, implicit=False):
+def _cfg(cfgspec, rounds=None, implicit=False, variant=4):
     return C.EncoderConfig(k_l=cfgspec.k, row_bits=[cfgspec.bits] * cfgspec.k,
                            oi_rounds=cfgspec.rounds if rounds is None else rounds,
-                           oi_implicit=implicit)
+                           oi_implicit=implicit, variant=variant)
 
 
 def _agreeing_columns(ev, k):
@@ -42,7 +42,7 @@ def _agreeing_columns(ev, k):
 
 
 def _oracle_stream_of(g, s):
-    og = O.Encoded(g.n, g.F, g.k_l, g.n_c, s.faces, g.anchor_bits, g.dict_bits)
+    og = O.Encoded(g.n, g.F, g.k_l, g.n_c, s.faces, g.anchor_bits, g.dict_bits, g.variant)
     for a in range(3):
         og.dict_q[a][:] = g.dict_q[a]
         if g.k_l:
@@ -51,23 +51,35 @@ def _oracle_stream_of(g, s):
             og.row_bits[a][:] = g.row_bits[a][:g.k_l]
             og.coeff_q[a][:] = g.coeff_q[a][:g.k_l]
         og.anchor_q[a][:] = g.anchor_q[a]
+        og.means[a][:] = g.means[a]
         og.s.anchor_min[a] = g.anchor_min[a]
         og.s.anchor_max[a] = g.anchor_max[a]
     og.anchor_idx[:] = g.anchor_idx
     return og
 
 
-def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3, implicit=False):
+def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3, implicit=False,
+                 variant=4):
     rounds = spec.rounds if rounds is None else rounds
-    ec = _cfg(spec, rounds, implicit)
+    ec = _cfg(spec, rounds, implicit, variant)
     g = codec.encode(s, ec)
-    o = O.encode(s, spec.k, spec.bits, rounds=rounds, seed=0, nthreads=8)
+    o = O.encode(s, spec.k, spec.bits, rounds=rounds, seed=0, nthreads=8, variant=variant)
     n, F, k = s.n, s.F, spec.k
-    # P1 / P2
-    assert np.array_equal(g.anchor_idx, o.anchor_idx)
+    assert g.variant == variant and g.n_c == o.s.n_c
+    # P1 / P2 (anchored variants)
+    if g.n_c:
+        assert np.array_equal(g.anchor_idx, o.anchor_idx)
     for a in range(3):
-        assert np.array_equal(g.anchor_q[a], o.anchor_q[a])
-        assert g.anchor_min[a] == o.s.anchor_min[a] and g.anchor_max[a] == o.s.anchor_max[a]
+        if g.n_c:
+            assert np.array_equal(g.anchor_q[a], o.anchor_q[a])
+            assert g.anchor_min[a] == o.s.anchor_min[a] and g.anchor_max[a] == o.s.anchor_max[a]
+        if variant in (0, 1):  # frame means: a sum over n vertices in another order;
+            # near-zero means (symmetric meshes) can differ by many float ulps, so
+            # the bound is absolute: a few double roundings of the coordinate scale
+            dm = np.abs(g.means[a].astype(np.float64) - o.means[a].astype(np.float64))
+            scale = np.abs(np.asarray(s.axes[a], np.float64)).max()
+            ulp = np.spacing(np.abs(o.means[a])).astype(np.float64)
+            assert np.all(dm <= np.maximum(ulp, 1e-13 * scale)), (a, dm.max())
     gb, gs = C.serialize(g)
     ob, os_ = O.serialize(o)
     assert gs == os_ and len(gb) == len(ob)
@@ -116,6 +128,18 @@ def test_implicit_oi_parity(codec, name):
     full parity contract holds."""
     spec = synth.CONFIGS[name]
     check_parity(codec, spec.make(), spec, implicit=True, f32_out=spec.dtype == "f32")
+
+
+@pytest.mark.parametrize("variant", ["v2v", "pca_q", "pca", "pca_qs"])
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_variant_parity(codec, name, variant):
+    """The other n_b = 1 variants: v2v codes the trajectories
+    and decodes without a solve; pca / pca_q store frame means and decode by
+    solve_mean_constrained (vertex 0 pinned, normal matrix of L[:, 1:] on the
+    GPU Cholesky path, mean shift); pca_qs is pca_qp with the serial solve
+    mode.  Full parity contract against the oracle."""
+    spec = synth.CONFIGS[name]
+    check_parity(codec, spec.make(), spec, variant=O.VARIANTS[variant])
 
 
 def test_config4_sequence_parity(codec):
@@ -281,9 +305,14 @@ def test_errors(codec):
     with pytest.raises(C.DmcError) as e:
         codec.encode(s, C.EncoderConfig(k_l=4, anchor_bits=17))
     assert e.value.code == 5
-    with pytest.raises(C.DmcError) as e:
-        codec.encode(s, C.EncoderConfig(k_l=4, variant=3))
+    with pytest.raises(C.DmcError) as e:  # blocks (n_b > 1): outside the B200 path
+        codec.encode(s, C.EncoderConfig(k_l=4, variant=5, n_b=2))
     assert e.value.code == 11
+    bad_v2v = [ax.copy() for ax in s.axes]  # v2v has no K1 pass: its own finiteness check
+    bad_v2v[2][1, 1] = np.inf
+    with pytest.raises(C.DmcError) as e:
+        codec.encode(synth.Sequence(s.faces, bad_v2v), C.EncoderConfig(k_l=4, variant=2))
+    assert e.value.code == 4 and "axis z" in str(e.value)
     two = synth.Sequence(np.array([[0, 1, 2], [3, 4, 5]], np.uint32),
                          [np.random.default_rng(0).normal(size=(6, 3)) for _ in range(3)])
     with pytest.raises(C.DmcError) as e:

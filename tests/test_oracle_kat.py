@@ -327,3 +327,58 @@ def test_frame_rms_examples():
 def _golden():
     import os
     return os.path.join(os.path.dirname(__file__), "golden", "small_ico1.npz")
+
+
+# ---- anchor-free variants ---------------------------------
+
+def test_solve_mean_constrained_dense():  # solver.cpp:105-133
+    """Pinned vertex 0, least squares on L[:, 1:], one refinement, mean shift:
+    equals the dense numpy restatement."""
+    d = np.load(_golden())
+    faces = d["faces"]
+    L = O.dense_laplacian(faces, 42)
+    rng = np.random.default_rng(3)
+    delta = rng.normal(size=(42, 5))
+    means = rng.normal(size=5)
+    x = O.solve_mean_constrained(faces, 42, delta, means)
+    z = np.linalg.lstsq(L[:, 1:], delta, rcond=None)[0]
+    ref = np.vstack([np.zeros((1, 5)), z])
+    ref += means - ref.mean(axis=0)
+    np.testing.assert_allclose(x, ref, atol=1e-9)
+    np.testing.assert_allclose(x.mean(axis=0), means, atol=1e-12)
+
+
+def test_solve_mean_constrained_exact_inputs():  # a sequence's own delta and means
+    d = np.load(_golden())
+    faces, X = d["faces"], d["axes"][0]
+    L = O.dense_laplacian(faces, 42)
+    x = O.solve_mean_constrained(faces, 42, L @ X, X.mean(axis=0))
+    assert np.abs(x - X).max() / np.abs(X).max() < 1e-8
+
+
+@pytest.mark.parametrize("variant", ["v2v", "pca_q", "pca", "pca_qs"])
+def test_variant_roundtrip_lossless_limit(variant):  # codec.cpp:416-441, 520-546
+    d = np.load(_golden())
+    s = seq_from(d["faces"], list(d["axes"]))
+    enc = O.encode(s, 12, 16, rounds=0, anchor_fraction=0.05, variant=variant)
+    out = O.decode(enc)
+    bbox = np.linalg.norm([a.max() - a.min() for a in s.axes])
+    assert O.frame_rms(s.axes, out).max() < 1e-3 * bbox
+    if variant in ("pca", "pca_q"):
+        for a in range(3):  # traj.row(f).mean() as float
+            np.testing.assert_array_equal(enc.means[a], s.axes[a].mean(axis=0).astype(np.float32))
+
+
+def test_v2v_decode_is_dictionary_times_coefficients():  # codec.cpp:520-524
+    d = np.load(_golden())
+    s = seq_from(d["faces"], list(d["axes"]))
+    enc = O.encode(s, 6, 12, rounds=0, variant="v2v")
+    out = O.decode(enc)
+    F = s.axes[0].shape[1]
+    for a in range(3):
+        U = np.array([[O.dequantize(-1.0, 1.0, 16, int(enc.dict_q[a][j, i])) for j in range(F)]
+                      for i in range(F)])
+        C = np.array([[O.dequantize(float(enc.row_min[a][r]), float(enc.row_max[a][r]),
+                                    int(enc.row_bits[a][r]), int(enc.coeff_q[a][r, i]))
+                       for i in range(42)] for r in range(6)])
+        np.testing.assert_allclose(out[a], (U[:, :6] @ C).T, atol=1e-12)
