@@ -102,7 +102,7 @@ struct QuantRow {  // stream.hpp:86-93
   std::vector<uint32_t> q;  // empty when min == max
 };
 
-struct CompressedAnimation {  // stream.hpp:130-155, pca_qp / n_b = 1
+struct CompressedAnimation {  // stream.hpp:130-155, n_b = 1: pca, pca_q, v2v, pca_qs, pca_qp
   Variant variant = Variant::PcaQp;
   uint32_t n = 0, k = 0, k_l = 0, n_c = 0;
   uint8_t anchor_bits = 16, dict_bits = 16, diff_bits = 8;
@@ -112,6 +112,7 @@ struct CompressedAnimation {  // stream.hpp:130-155, pca_qp / n_b = 1
   std::vector<uint32_t> anchor_indices;
   std::array<float, 3> anchor_min{}, anchor_max{};
   std::array<std::vector<uint32_t>, 3> anchor_q;     // n_c*k, anchor-major
+  std::array<std::vector<float>, 3> means;           // k per-frame means (pca / pca_q)
 };
 
 namespace detail {
@@ -175,6 +176,8 @@ inline CompressedAnimation encode(const MeshSequence& s, const EncoderConfig& cf
   out.anchor_indices.resize(sz.anchor_idx);
   dmcg_encoded e{};
   for (int a = 0; a < 3; ++a) {
+    out.means[a].resize(sz.means);
+    e.means[a] = sz.means ? out.means[a].data() : nullptr;
     dq[a].resize(sz.dict_q);
     cq[a].resize(sz.coeff_q + 1);
     aq[a].resize(sz.anchor_q);
@@ -193,7 +196,7 @@ inline CompressedAnimation encode(const MeshSequence& s, const EncoderConfig& cf
   dmcg_seq q{n, F, DMCG_F64, {s.axis(0).data(), s.axis(1).data(), s.axis(2).data()},
              faces.data(), (uint32_t)s.faces().size()};
   detail::check(dmcg_encode(detail::Ctx::get().c, &q, &c, &e));
-  out.variant = Variant::PcaQp;
+  out.variant = cfg.variant;
   out.n = n;
   out.k = F;
   out.k_l = cfg.k_l;
@@ -243,8 +246,10 @@ inline MeshSequence decode(const CompressedAnimation& c, double cg_rtol = 1e-10)
   e.anchor_idx = idx.data();
   for (int a = 0; a < 3; ++a) {
     if (c.dict_first[a].size() != (size_t)F * F || c.coeffs[a].size() != c.k_l ||
-        c.anchor_q[a].size() != (size_t)c.n_c * F)
+        c.anchor_q[a].size() != (size_t)c.n_c * F ||
+        ((c.variant == Variant::Pca || c.variant == Variant::PcaQ) && c.means[a].size() != F))
       throw Error(6, "CorruptPayload: payload has wrong element count");
+    e.means[a] = c.means[a].empty() ? nullptr : const_cast<float*>(c.means[a].data());
     dq[a].assign(c.dict_first[a].begin(), c.dict_first[a].end());
     aq[a].assign(c.anchor_q[a].begin(), c.anchor_q[a].end());
     cq[a].assign((size_t)c.k_l * n + 1, 0);
