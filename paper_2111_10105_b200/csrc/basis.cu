@@ -1818,7 +1818,12 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
     const size_t smem = abytes + (size_t)m2 * vr * sizeof(double);
     cudaError_t e = set_smem_attr((const void*)k_jacobi, smem);
     if (e != cudaSuccess) return e;
-    k_jacobi<<<dim3(nbatch, nsplit), kJacThreads, smem, s>>>(m, A, work, V, w, flags, 1, vr);
+    // (DMCG_JAC_THREADS: experiments; at m = 64 fewer threads measured slower:
+    // 1024 / 512 / 256 -> 0.90 / 0.98 / 1.18 ms for the three c1 axes)
+    static const int env_nt = getenv("DMCG_JAC_THREADS") ? atoi(getenv("DMCG_JAC_THREADS")) : 0;
+    int nt = kJacThreads;
+    if (env_nt >= 64 && env_nt <= kJacThreads && env_nt % 32 == 0) nt = env_nt;
+    k_jacobi<<<dim3(nbatch, nsplit), nt, smem, s>>>(m, A, work, V, w, flags, 1, vr);
     static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
     if (dbg) {
       int sw[8] = {};
