@@ -56,10 +56,13 @@ class EncoderConfig:
     def to_c(self):
         c = L.DmcgConfig()
         L.lib().dmcg_config_default(ctypes.byref(c))
-        self._rb = np.ascontiguousarray(list(self.row_bits), dtype=np.int32)
+        # the row-bit array lives as long as the struct that points at it (no
+        # shared state on self: concurrent encodes may share one config)
+        rb = np.ascontiguousarray(list(self.row_bits), dtype=np.int32)
+        c._row_bits_keep = rb
         c.variant, c.k_l, c.n_b, c.t_max = self.variant, self.k_l, self.n_b, self.t_max
-        c.row_bits = self._rb.ctypes.data_as(L.intp) if len(self._rb) else None
-        c.n_row_bits = len(self._rb)
+        c.row_bits = rb.ctypes.data_as(L.intp) if len(rb) else None
+        c.n_row_bits = len(rb)
         c.anchor_fraction = self.anchor_fraction
         c.anchor_bits, c.dict_bits, c.diff_bits = self.anchor_bits, self.dict_bits, self.diff_bits
         c.anchor_strategy, c.seed, c.laplacian = self.anchor_strategy, self.seed, self.laplacian

@@ -47,6 +47,9 @@ __device__ double block_sum(double v, double* red) {
 // inter-CTA traffic is needed.  a_smem = 0 keeps A and V in `work`
 // (gridDim.y must then be 1).
 constexpr int kJacThreads = 1024;
+// Relative rotation threshold |a_pq| > rel sqrt(|a_pp a_qq|) (the oracle's
+// orc_jacobi_eig uses 1e-17; DMCG_JAC_REL overrides it for experiments).
+__constant__ double c_jac_rel = 1e-17, c_jac_rel2 = 1e-34;
 __device__ int g_jacobi_sweeps[8];  // sweeps of the last k_jacobi per matrix (DMCG_DEBUG)
 __device__ long long g_jacobi_cyc[64];  // cycles per sweep of matrix 0 (DMCG_DEBUG)
 
@@ -139,8 +142,8 @@ __global__ void __launch_bounds__(kJacThreads)
         Qi[i] = q;
         const double app = A[p * ld + p], aqq = A[q * ld + q];
         const double apq = A[q * ld + p];
-        // |apq| > max(1e-17 sqrt(|app aqq|), abs_thresh), compared in squares
-        const double rel2 = 1e-34 * fabs(app) * fabs(aqq);
+        // |apq| > max(rel sqrt(|app aqq|), abs_thresh), compared in squares
+        const double rel2 = c_jac_rel2 * fabs(app) * fabs(aqq);
         const double apq2 = apq * apq;
         double c = 1.0, sv = 0.0, tt = 0.0;
         if (apq2 > rel2 && fabs(apq) > abs_thresh) {
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(kJacThreads)
         const int p = t % m2, q = t / m2;
         if (p >= q) continue;
         const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[q * ld + p];
-        const double rel = 1e-17 * sqrt(fabs(app) * fabs(aqq));
+        const double rel = c_jac_rel * sqrt(fabs(app) * fabs(aqq));
         if (fabs(apq) > (rel > abs_thresh ? rel : abs_thresh)) hot = 1;
       }
       converged = !__syncthreads_or(hot);
@@ -1416,7 +1419,7 @@ __global__ void __launch_bounds__(kJcThreads)
         const double* Ap = Acol(sh.slot_buf[tp ? tid : tid + P]);
         const double* Aq = Acol(sh.slot_buf[tp ? tid + P : tid]);
         const double app = Ap[p], aqq = Aq[qq], apq = Aq[p];
-        const double rel2 = 1e-34 * fabs(app) * fabs(aqq);
+        const double rel2 = c_jac_rel2 * fabs(app) * fabs(aqq);
         double c = 1.0, sv = 0.0, tt = 0.0;
         int on = 0;
         if (apq * apq > rel2 && fabs(apq) > abs_thresh) {
@@ -1588,7 +1591,7 @@ __global__ void __launch_bounds__(kJcThreads)
         const int s = t / m2, r = t % m2, c = sh.slot_col[s];
         if (r == c) continue;
         const double arc = Acol(sh.slot_buf[s])[r];
-        const double rel = 1e-17 * sqrt(fabs(sh.diag[r]) * fabs(sh.diag[c]));
+        const double rel = c_jac_rel * sqrt(fabs(sh.diag[r]) * fabs(sh.diag[c]));
         if (fabs(arc) > (rel > abs_thresh ? rel : abs_thresh)) hot = 1;
       }
       hot = __syncthreads_or(hot);
@@ -1800,6 +1803,15 @@ static size_t smem_room(const void* fn) {
 
 cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
                           double* V, double* w, int* flags) {
+  static bool rel_set = false;
+  if (!rel_set) {
+    rel_set = true;
+    if (const char* e = getenv("DMCG_JAC_REL")) {
+      const double r = atof(e), r2 = r * r;
+      cudaMemcpyToSymbol(c_jac_rel, &r, sizeof(r));
+      cudaMemcpyToSymbol(c_jac_rel2, &r2, sizeof(r2));
+    }
+  }
   if (m > 512) return cudaErrorInvalidValue;
   const int m2 = m + (m & 1);
   const size_t abytes = (size_t)m2 * (m2 + 1) * sizeof(double);
