@@ -84,11 +84,14 @@ def _assert_same_stream(g, h):
 
 
 def _check_against_oracle(g, s, spec):
-    o = O.encode(s, spec.k, spec.bits, rounds=spec.rounds, seed=0, nthreads=8)
-    assert np.array_equal(g.anchor_idx, o.anchor_idx)
+    o = O.encode(s, spec.k, spec.bits, rounds=spec.rounds, seed=0, nthreads=8, variant=g.variant)
+    assert g.n_c == o.s.n_c
+    if g.n_c:
+        assert np.array_equal(g.anchor_idx, o.anchor_idx)
     for a in range(3):
-        assert np.array_equal(g.anchor_q[a], o.anchor_q[a])   # P2: bit-exact
-        assert g.anchor_min[a] == o.s.anchor_min[a] and g.anchor_max[a] == o.s.anchor_max[a]
+        if g.n_c:
+            assert np.array_equal(g.anchor_q[a], o.anchor_q[a])   # P2: bit-exact
+            assert g.anchor_min[a] == o.s.anchor_min[a] and g.anchor_max[a] == o.s.anchor_max[a]
         for j in _agreeing_columns(o.evals[a], spec.k):       # P3 / P4
             dq = np.abs(g.dict_q[a][j].astype(np.int64) - o.dict_q[a][j].astype(np.int64))
             assert dq.max() <= 1 and np.count_nonzero(dq) <= 2, (a, j)
@@ -99,11 +102,12 @@ def _check_against_oracle(g, s, spec):
     return o
 
 
-@pytest.mark.parametrize("name,S", [("c0", 3), ("c1", 4)])
-def test_virtual_ranks_encode_matches_oracle(codec, name, S):
+@pytest.mark.parametrize("name,S,variant", [("c0", 3, 4), ("c1", 4, 4), ("c0", 2, 2)])
+def test_virtual_ranks_encode_matches_oracle(codec, name, S, variant):
+    """pca_qp (4) and v2v (2, the trajectories projected row-block by row-block)."""
     spec = synth.CONFIGS[name]
     s = spec.make()
-    plans = _virtual_ranks_encode(codec, s, _cfg(spec), S)
+    plans = _virtual_ranks_encode(codec, s, _cfg(spec, variant=variant), S)
     streams = [p.download() for p in plans]
     for h in streams[1:]:
         _assert_same_stream(streams[0], h)      # every rank holds the same stream
@@ -132,6 +136,14 @@ def test_one_rank_nccl_path_is_bit_identical_to_plan(codec):
     assert sp.serialize()[0] == p.serialize()[0]
     sp.close()
     comm.close()
+
+
+def test_shard_refuses_mean_variants(codec):
+    spec = synth.CONFIGS["c0"]
+    s = spec.make()
+    with pytest.raises(C.DmcError) as e:
+        shard.ShardPlan(codec, s.n, s.F, s.faces, _cfg(spec, variant=1), 2, 0, None)
+    assert e.value.code == 11
 
 
 def test_one_rank_nccl_path_implicit_oi(codec):
