@@ -48,7 +48,8 @@ enum dmcg_status {
 
 enum dmcg_dtype { DMCG_F64 = 0, DMCG_F32 = 1 };
 
-/* Variant values = reference Variant (include/dmc/stream.hpp:38-46). */
+/* Variant values = reference Variant (include/dmc/stream.hpp:60-68).  The B200
+ * path covers 0-5; per_mesh_gft (6) is refused with DMCG_E_UNSUPPORTED. */
 enum dmcg_variant {
   DMCG_PCA = 0, DMCG_PCA_Q = 1, DMCG_V2V = 2, DMCG_PCA_QS = 3, DMCG_PCA_QP = 4,
   DMCG_BLOCKS = 5, DMCG_PER_MESH_GFT = 6
@@ -72,8 +73,9 @@ typedef struct {
   uint32_t k_l;             /* retained rows (default 20) */
   const int* row_bits;      /* k_l entries or NULL = all 16 (codec.cpp:106-113) */
   uint32_t n_row_bits;
-  uint16_t n_b;             /* blocks; must be 1 */
-  int t_max;                /* block OI rounds (unused at n_b = 1, validated) */
+  uint16_t n_b;             /* blocks (> 1 only for DMCG_BLOCKS) */
+  int t_max;                /* blocks: orthogonal_iterations t_max (default 4,
+                               spectral.cpp:69-104); validated at n_b = 1 */
   double anchor_fraction;   /* default 0.01 */
   int anchor_bits;          /* default 16 */
   int dict_bits;            /* default 16 */
@@ -93,6 +95,9 @@ typedef struct {
                                applied implicitly"; on vertex-row shards the X^T (X Q)
                                partials are allreduced every round).  Same
                                iteration as the explicit R Q; 0 (default): form R. */
+  double oi_tolerance;      /* blocks: EncoderConfig::oi_tolerance, the optional
+                               principal-angle stop of orthogonal_iterations
+                               (spectral.cpp:90-97); < 0 (default) = unset */
 } dmcg_config;
 
 void dmcg_config_default(dmcg_config* cfg);
@@ -155,11 +160,26 @@ typedef struct {
   uint16_t* anchor_q[3];
   float* means[3];          /* F per-frame vertex means, variants pca / pca_q only
                                (codec.cpp:432-441; may be NULL otherwise) */
+  /* blocks variant (DMCG_BLOCKS, n_b > 1; AxisPayload dict_first / dict_diffs /
+   * coeffs, stream.hpp:101-109): the F frames are padded with the last frame to
+   * F + pad = n_b * k_f (codec.cpp:43-49, 81-82).  0 reads as n_b = 1.  With
+   * n_b > 1 the arrays above hold, per axis:
+   *   dict_q      n_b * k_f^2 levels: dict_first (dict_bits) then the n_b - 1
+   *               dict_diffs (diff_bits), each k_f x k_f column-major
+   *   diff_min/max  n_b - 1 difference ranges (DictDiff::min / max)
+   *   row_*       n_b * k_l headers, block b at [b * k_l]
+   *   coeff_q     n_b * k_l * n levels, block b at [b * k_l * n]
+   *   anchor_q    n_c * F (unpadded, as for pca_qp) */
+  uint16_t n_b, pad;
+  float* diff_min[3];
+  float* diff_max[3];
 } dmcg_encoded;
 
 /* Element counts of each dmcg_encoded array for (n, F, cfg). */
 typedef struct {
   size_t dict_q, rows, coeff_q, anchor_idx, anchor_q, means;
+  size_t dict_ranges;       /* n_b - 1 (blocks variant), else 0 */
+  uint16_t n_b, pad;        /* checked block count and frame padding */
 } dmcg_sizes;
 int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_sizes* out);
 
@@ -213,7 +233,9 @@ int dmcg_plan_decode_device(dmcg_plan* plan, const dmcg_decode_options* opt,
 int dmcg_plan_download(dmcg_plan* plan, dmcg_encoded* out);
 int dmcg_plan_upload(dmcg_plan* plan, const dmcg_encoded* in);
 /* Device copy of the F x F basis of axis a (column-major) and its Ritz /
- * eigen values, for parity checks. */
+ * eigen values, for parity checks.  Blocks variant: the n_b k_f x k_f
+ * dictionaries of the axis back to back (n_b k_f^2 doubles), evals = F
+ * doubles (k_f eigenvalues per block's direct decomposition). */
 int dmcg_plan_basis(dmcg_plan* plan, int axis, double* U_host, double* evals_host);
 
 typedef struct {

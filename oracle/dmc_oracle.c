@@ -1346,7 +1346,7 @@ int orc_encode(uint32_t n, uint32_t F, const double* const axes[3], const uint32
                             nthreads);
 }
 
-static int uses_anchors(int v) { return v == 3 || v == 4; }  /* stream.hpp:77-79 (n_b = 1) */
+static int uses_anchors(int v) { return v == 3 || v == 4 || v == 5; }  /* stream.hpp:77-79 */
 static int uses_means(int v) { return v == 0 || v == 1; }    /* stream.hpp:80-82 */
 
 int orc_encode_variant(int variant, uint32_t n, uint32_t F, const double* const axes[3],
@@ -1477,12 +1477,231 @@ int orc_encode_variant(int variant, uint32_t n, uint32_t F, const double* const 
   return rc;
 }
 
+/* ======================================================================== */
+/* blocks variant (n_b > 1)                                                   */
+/* ======================================================================== */
+
+static uint32_t nb_of(const orc_encoded* e) { return e->n_b ? e->n_b : 1; }
+
+/* align_signs (src/spectral.cpp:122-131): flip columns with prev . cur < 0. */
+static void align_signs(uint32_t m, const double* prev, double* U) {
+  for (uint32_t j = 0; j < m; ++j) {
+    const double* p = prev + (size_t)j * m;
+    double* u = U + (size_t)j * m;
+    double d = 0.0;
+    for (uint32_t i = 0; i < m; ++i) d += p[i] * u[i];
+    if (d < 0.0)
+      for (uint32_t i = 0; i < m; ++i) u[i] = -u[i];
+  }
+}
+
+/* k_f x k_f autocorrelation of frames [f0, f0 + kf) of the padded n x Fp
+ * trajectory (spectral.cpp:35-39 on a.middleRows(b * k_f, k_f)). */
+static void block_autocorrelation(uint32_t n, uint32_t Fp, uint32_t f0, uint32_t kf,
+                                  const double* Xp, double* R) {
+  for (uint32_t g = 0; g < kf; ++g)
+    for (uint32_t f = 0; f < kf; ++f) {
+      double s = 0.0;
+      for (uint32_t i = 0; i < n; ++i) s += Xp[(size_t)i * Fp + f0 + f] * Xp[(size_t)i * Fp + f0 + g];
+      R[(size_t)g * kf + f] = s;
+    }
+  for (uint32_t g = 0; g < kf; ++g)
+    for (uint32_t f = 0; f < g; ++f) {
+      const double s = 0.5 * (R[(size_t)g * kf + f] + R[(size_t)f * kf + g]);
+      R[(size_t)g * kf + f] = s;
+      R[(size_t)f * kf + g] = s;
+    }
+}
+
+int orc_encode_blocks(uint32_t n, uint32_t F, const double* const axes[3], const uint32_t* faces,
+                      uint32_t n_faces, uint32_t n_b, uint32_t k_l, const int* row_bits,
+                      double anchor_fraction, int anchor_bits, int dict_bits, int diff_bits,
+                      int t_max, double stop_tol, orc_encoded* out, double* U_out, int nthreads) {
+  /* validate_sequence + check_config (codec.cpp:352-363, 69-120) */
+  if (orc_validate(n, F, faces, n_faces, axes[0], axes[1], axes[2])) return ORC_E_INDEX;
+  if (n_b < 1 || n_b > F || t_max < 1) return ORC_E_CONFIG;
+  if (anchor_fraction < 0.0 || anchor_fraction > 1.0) return ORC_E_CONFIG;
+  if (anchor_bits < 1 || anchor_bits > 16 || dict_bits < 1 || dict_bits > 16 || diff_bits < 1 ||
+      diff_bits > 16)
+    return ORC_E_CONFIG;
+  const uint32_t pad = (n_b - F % n_b) % n_b, Fp = F + pad, kf = Fp / n_b;
+  if (k_l > kf) return ORC_E_CONFIG;
+  for (uint32_t r = 0; r < k_l; ++r)
+    if (row_bits[r] < 1 || row_bits[r] > 16) return ORC_E_CONFIG;
+  out->n = n;
+  out->F = F;
+  out->k_l = k_l;
+  out->variant = 5;
+  out->n_b = n_b;
+  out->pad = pad;
+  out->n_c = orc_anchor_count(n, anchor_fraction);
+  out->n_faces = n_faces;
+  out->faces = faces;
+  out->anchor_bits = anchor_bits;
+  out->dict_bits = dict_bits;
+  out->diff_bits = diff_bits;
+  uint32_t* arp = malloc(((size_t)n + 1) * sizeof(uint32_t));
+  uint32_t* acol = malloc((size_t)6 * n_faces * sizeof(uint32_t));
+  long nnz = orc_build_connectivity(faces, n_faces, n, arp, acol);
+  uint32_t* lrow = malloc(((size_t)n + 1) * sizeof(uint32_t));
+  uint32_t* lcol = malloc(((size_t)n + nnz) * sizeof(uint32_t));
+  double* lval = malloc(((size_t)n + nnz) * sizeof(double));
+  orc_build_laplacian(n, arp, acol, 0, lrow, lcol, lval);
+
+  const size_t kk = (size_t)kf * kf;
+  double* Xp = malloc((size_t)n * Fp * sizeof(double));
+  double* delta = malloc((size_t)n * Fp * sizeof(double));
+  double* R = malloc(kk * sizeof(double));
+  double* D = malloc(n_b * kk * sizeof(double));    /* dicts[b] */
+  double* Dec = malloc(kk * sizeof(double));        /* payload.decoded.back() */
+  double* cur = malloc(kk * sizeof(double));
+  double* C = malloc((size_t)(k_l ? k_l : 1) * n * sizeof(double));
+  int rc = 0;
+  for (int a = 0; a < 3 && !rc; ++a) {
+    /* pad_frames (codec.cpp:43-49): repeat the last frame */
+    for (uint32_t i = 0; i < n; ++i) {
+      memcpy(Xp + (size_t)i * Fp, axes[a] + (size_t)i * F, (size_t)F * sizeof(double));
+      for (uint32_t p = 0; p < pad; ++p) Xp[(size_t)i * Fp + F + p] = axes[a][(size_t)i * F + F - 1];
+    }
+    /* block_dictionaries (codec.cpp:149-172) */
+    for (uint32_t b = 0; b < n_b && !rc; ++b) {
+      double* U = D + b * kk;
+      block_autocorrelation(n, Fp, b * kf, kf, Xp, R);
+      if (b == 0) {
+        rc = orc_full_eigenbasis(kf, R, U, NULL);
+      } else {
+        if (orc_orthogonal_iterations(kf, R, D + (b - 1) * kk, t_max, stop_tol, U))
+          rc = orc_full_eigenbasis(kf, R, U, NULL);  /* catch (RankDeficiency) */
+        if (!rc) align_signs(kf, D + (b - 1) * kk, U);
+      }
+    }
+    if (rc) break;
+    if (U_out) memcpy(U_out + (size_t)a * n_b * kk, D, n_b * kk * sizeof(double));
+    /* encode_dictionaries (codec.cpp:290-328), auto_realign = true */
+    uint32_t* dq = out->dict_q[a];
+    for (size_t t = 0; t < kk; ++t) {
+      dq[t] = orc_quantize(-1.0f, 1.0f, dict_bits, D[t]);
+      Dec[t] = orc_dequantize(-1.0f, 1.0f, dict_bits, dq[t]);
+    }
+    for (uint32_t b = 1; b < n_b; ++b) {
+      memcpy(cur, D + b * kk, kk * sizeof(double));
+      for (uint32_t j = 0; j < kf; ++j) {
+        double* c = cur + (size_t)j * kf;
+        const double* p = Dec + (size_t)j * kf;
+        double straight = 0.0, flipped = 0.0;
+        for (uint32_t i = 0; i < kf; ++i) {
+          const double d = c[i] - p[i], e = -c[i] - p[i];
+          straight += d * d;
+          flipped += e * e;
+        }
+        if (straight > 2.0 && flipped < straight)
+          for (uint32_t i = 0; i < kf; ++i) c[i] = -c[i];
+      }
+      double lo = INFINITY, hi = -INFINITY;
+      for (size_t t = 0; t < kk; ++t) {
+        cur[t] = cur[t] - Dec[t];  /* diff = cur - prev */
+        if (cur[t] < lo) lo = cur[t];
+        if (cur[t] > hi) hi = cur[t];
+      }
+      float flo, fhi;
+      orc_widened_range(lo, hi, &flo, &fhi);
+      out->diff_min[a][b - 1] = flo;
+      out->diff_max[a][b - 1] = fhi;
+      uint32_t* q = dq + b * kk;
+      for (size_t t = 0; t < kk; ++t) {
+        q[t] = orc_quantize(flo, fhi, diff_bits, cur[t]);
+        Dec[t] = Dec[t] + orc_dequantize(flo, fhi, diff_bits, q[t]);
+      }
+    }
+    /* per block: delta_b = L * block_traj^T, coeffs = dicts[b]^T delta_b^T
+     * (codec.cpp:411-429); delta is column-separable, so delta of the
+     * padded trajectory restricted to the block's frames. */
+    orc_delta(n, Fp, lrow, lcol, lval, Xp, delta);
+    for (uint32_t b = 0; b < n_b; ++b) {
+      const double* U = D + b * kk;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+      for (uint32_t i = 0; i < n; ++i) {
+        const double* d = delta + (size_t)i * Fp + (size_t)b * kf;
+        for (uint32_t r = 0; r < k_l; ++r) {
+          const double* u = U + (size_t)r * kf;
+          double s = 0.0;
+          for (uint32_t f = 0; f < kf; ++f) s = s + u[f] * d[f];
+          C[(size_t)r * n + i] = s;
+        }
+      }
+      const size_t ro = (size_t)b * k_l;
+      orc_quantize_rows(k_l, n, C, row_bits, out->row_min[a] + ro, out->row_max[a] + ro,
+                        out->coeff_q[a] + ro * n);
+      for (uint32_t r = 0; r < k_l; ++r) out->row_bits[a][ro + r] = (uint8_t)row_bits[r];
+    }
+  }
+  /* anchors on the unpadded trajectories (codec.cpp:444-471) */
+  if (!rc) rc = orc_select_anchors(n, out->n_c, 0, 0, out->anchor_idx);
+  for (int a = 0; a < 3 && !rc; ++a) {
+    const double* X = axes[a];
+    double lo = INFINITY, hi = -INFINITY;
+    for (uint32_t t = 0; t < out->n_c; ++t)
+      for (uint32_t f = 0; f < F; ++f) {
+        const double v = X[(size_t)out->anchor_idx[t] * F + f];
+        if (v < lo) lo = v;
+        if (v > hi) hi = v;
+      }
+    float flo, fhi;
+    orc_widened_range(lo, hi, &flo, &fhi);
+    out->anchor_min[a] = flo;
+    out->anchor_max[a] = fhi;
+    for (uint32_t t = 0; t < out->n_c; ++t)
+      for (uint32_t f = 0; f < F; ++f)
+        out->anchor_q[a][(size_t)t * F + f] =
+            orc_quantize(flo, fhi, anchor_bits, X[(size_t)out->anchor_idx[t] * F + f]);
+  }
+  free(arp);
+  free(acol);
+  free(lrow);
+  free(lcol);
+  free(lval);
+  free(Xp);
+  free(delta);
+  free(R);
+  free(D);
+  free(Dec);
+  free(cur);
+  free(C);
+  return rc;
+}
+
+/* decode_dictionaries (codec.cpp:330-349) */
+int orc_decode_dictionaries(const orc_encoded* in, int a, double* out) {
+  const uint32_t n_b = nb_of(in), kf = (in->F + in->pad) / n_b;
+  const size_t kk = (size_t)kf * kf;
+  const uint32_t dlev = 1u << in->dict_bits, flev = 1u << in->diff_bits;
+  int rc = 0;
+  for (size_t t = 0; t < kk; ++t) {
+    if (in->dict_q[a][t] >= dlev) rc = ORC_E_CORRUPT;
+    out[t] = orc_dequantize(-1.0f, 1.0f, in->dict_bits, in->dict_q[a][t]);
+  }
+  for (uint32_t b = 1; b < n_b; ++b) {
+    const float mn = in->diff_min[a][b - 1], mx = in->diff_max[a][b - 1];
+    const uint32_t* q = in->dict_q[a] + b * kk;
+    for (size_t t = 0; t < kk; ++t) {
+      if (q[t] >= flev) rc = ORC_E_CORRUPT;
+      out[b * kk + t] = out[(b - 1) * kk + t] + orc_dequantize(mn, mx, in->diff_bits, q[t]);
+    }
+  }
+  return rc;
+}
+
 int orc_decode(const orc_encoded* in, double* const axes_out[3], orc_timing* tm, int nthreads) {
   orc_timing dummy;
   if (!tm) tm = &dummy;
   memset(tm, 0, sizeof(*tm));
   const uint32_t n = in->n, F = in->F, k_l = in->k_l, n_c = in->n_c;
-  const uint32_t W = 3 * F;
+  /* blocks (n_b > 1): the solve runs over the F + pad padded frames
+   * (codec.cpp:483-495, 527-549), blocks of k_f frames */
+  const uint32_t nb = nb_of(in), Fp = F + (nb > 1 ? in->pad : 0), kf = Fp / nb;
+  const uint32_t W = 3 * Fp;
   double t0 = now_s();
   uint32_t* arp = malloc(((size_t)n + 1) * sizeof(uint32_t));
   uint32_t* acol = malloc((size_t)6 * in->n_faces * sizeof(uint32_t));
@@ -1500,7 +1719,7 @@ int orc_decode(const orc_encoded* in, double* const axes_out[3], orc_timing* tm,
   int rc = 0;
   double* delta = malloc((size_t)n * W * sizeof(double)); /* n x 3F */
   double* anchors = malloc((size_t)n_c * W * sizeof(double));
-  double* Ut = malloc((size_t)F * F * sizeof(double));
+  double* Ut = malloc((size_t)nb * kf * kf * sizeof(double));
   double* Cq = malloc((size_t)(k_l ? k_l : 1) * n * sizeof(double));
   for (int a = 0; a < 3 && !rc; ++a) {
     /* anchor_matrix (codec.cpp:174-195) */
@@ -1509,35 +1728,39 @@ int orc_decode(const orc_encoded* in, double* const axes_out[3], orc_timing* tm,
       for (uint32_t f = 0; f < F; ++f) {
         const uint32_t lv = in->anchor_q[a][(size_t)t * F + f];
         if (lv >= alev) rc = ORC_E_CORRUPT;
-        anchors[(size_t)t * W + (size_t)a * F + f] =
+        anchors[(size_t)t * W + (size_t)a * Fp + f] =
             orc_dequantize(in->anchor_min[a], in->anchor_max[a], in->anchor_bits, lv);
       }
+    for (uint32_t t = 0; t < n_c; ++t)  /* padded columns repeat the last frame */
+      for (uint32_t f = F; f < Fp; ++f)
+        anchors[(size_t)t * W + (size_t)a * Fp + f] = anchors[(size_t)t * W + (size_t)a * Fp + F - 1];
     /* decode_dictionaries / unpack_matrix (codec.cpp:330-349,131-142) */
     t0 = now_s();
-    const uint32_t dlev = 1u << in->dict_bits;
-    for (size_t t = 0; t < (size_t)F * F; ++t) {
-      if (in->dict_q[a][t] >= dlev) rc = ORC_E_CORRUPT;
-      Ut[t] = orc_dequantize(-1.0f, 1.0f, in->dict_bits, in->dict_q[a][t]);
-    }
+    if (orc_decode_dictionaries(in, a, Ut)) rc = ORC_E_CORRUPT;
     tm->t_dict_decode += now_s() - t0;
     if (rc) break;
     /* dequantize_rows + delta~ = (U~ coeffs)^T (codec.cpp:528-533) */
     t0 = now_s();
-    rc = orc_dequantize_rows(k_l, k_l, n, in->row_min[a], in->row_max[a], in->row_bits[a],
-                             in->coeff_q[a], Cq);
-    if (rc) break;
+    for (uint32_t b = 0; b < nb && !rc; ++b) {
+      const size_t ro = (size_t)b * k_l;
+      rc = orc_dequantize_rows(k_l, k_l, n, in->row_min[a] + ro, in->row_max[a] + ro,
+                               in->row_bits[a] + ro, in->coeff_q[a] + ro * n, Cq);
+      if (rc) break;
+      const double* Ub = Ut + (size_t)b * kf * kf;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
 #endif
-    for (uint32_t i = 0; i < n; ++i) {
-      double* o = delta + (size_t)i * W + (size_t)a * F;
-      for (uint32_t f = 0; f < F; ++f) o[f] = 0.0;
-      for (uint32_t r = 0; r < k_l; ++r) {
-        const double c = Cq[(size_t)r * n + i];
-        const double* u = Ut + (size_t)r * F;
-        for (uint32_t f = 0; f < F; ++f) o[f] = o[f] + u[f] * c;
+      for (uint32_t i = 0; i < n; ++i) {
+        double* o = delta + (size_t)i * W + (size_t)a * Fp + (size_t)b * kf;
+        for (uint32_t f = 0; f < kf; ++f) o[f] = 0.0;
+        for (uint32_t r = 0; r < k_l; ++r) {
+          const double c = Cq[(size_t)r * n + i];
+          const double* u = Ub + (size_t)r * kf;
+          for (uint32_t f = 0; f < kf; ++f) o[f] = o[f] + u[f] * c;
+        }
       }
     }
+    if (rc) break;
     tm->t_reconstruct += now_s() - t0;
   }
   if (!rc) {
@@ -1563,7 +1786,7 @@ int orc_decode(const orc_encoded* in, double* const axes_out[3], orc_timing* tm,
     }
     for (int a = 0; a < 3 && !rc; ++a)
       for (uint32_t i = 0; i < n; ++i)
-        memcpy(axes_out[a] + (size_t)i * F, X + (size_t)i * W + (size_t)a * F,
+        memcpy(axes_out[a] + (size_t)i * F, X + (size_t)i * W + (size_t)a * Fp,
                (size_t)F * sizeof(double));
     free(X);
     tm->t_solve = now_s() - t0;
@@ -1627,7 +1850,7 @@ static void put_f32(uint8_t* o, size_t* p, float v) {
   put_u32(o, p, u);
 }
 
-/* src/stream.cpp:172-292 restricted to pca_qp, n_b = 1, quantised payloads. */
+/* src/stream.cpp:172-292 for the quantised payloads of variants 0-5. */
 size_t orc_serialize(const orc_encoded* e, uint8_t* o, orc_sections* s) {
   orc_sections sz;
   memset(&sz, 0, sizeof(sz));
@@ -1639,8 +1862,9 @@ size_t orc_serialize(const orc_encoded* e, uint8_t* o, orc_sections* s) {
   put_u8(o, &p, 0);   /* flags */
   put_u32(o, &p, e->n);
   put_u32(o, &p, e->F);
-  put_u16(o, &p, 1);  /* n_b */
-  put_u16(o, &p, 0);  /* pad */
+  const uint32_t nb = nb_of(e), kf = (e->F + (nb > 1 ? e->pad : 0)) / nb;
+  put_u16(o, &p, (uint16_t)nb);
+  put_u16(o, &p, (uint16_t)(nb > 1 ? e->pad : 0));
   put_u32(o, &p, e->k_l);
   put_u32(o, &p, e->n_c);
   put_u8(o, &p, (uint8_t)e->anchor_bits);
@@ -1653,30 +1877,46 @@ size_t orc_serialize(const orc_encoded* e, uint8_t* o, orc_sections* s) {
   sz.connectivity = p - sz.header;
   for (int a = 0; a < 3; ++a) {
     size_t start = p;
+    const size_t kk = (size_t)kf * kf;
     bitw w = {o, p, 0, 0};
-    for (size_t t = 0; t < (size_t)e->F * e->F; ++t) bw_put(&w, e->dict_q[a][t], e->dict_bits);
+    for (size_t t = 0; t < kk; ++t) bw_put(&w, e->dict_q[a][t], e->dict_bits);
     bw_flush(&w);
     p = w.pos;
     sz.dict_payload += p - start;
-    start = p;
-    for (uint32_t r = 0; r < e->k_l; ++r) {
-      put_f32(o, &p, e->row_min[a][r]);
-      put_f32(o, &p, e->row_max[a][r]);
-      put_u8(o, &p, e->row_bits[a][r]);
+    for (uint32_t b = 1; b < nb; ++b) {  /* dict_diffs (stream.cpp:218-227) */
+      start = p;
+      put_f32(o, &p, e->diff_min[a][b - 1]);
+      put_f32(o, &p, e->diff_max[a][b - 1]);
+      sz.dict_ranges += p - start;
+      start = p;
+      bitw d = {o, p, 0, 0};
+      for (size_t t = 0; t < kk; ++t) bw_put(&d, e->dict_q[a][b * kk + t], e->diff_bits);
+      bw_flush(&d);
+      p = d.pos;
+      sz.dict_payload += p - start;
     }
-    sz.coeff_headers += p - start;
-    start = p;
-    w.pos = p;
-    w.acc = 0;
-    w.fill = 0;
-    for (uint32_t r = 0; r < e->k_l; ++r) {
-      if (e->row_min[a][r] == e->row_max[a][r]) continue;
-      const uint32_t* q = e->coeff_q[a] + (size_t)r * e->n;
-      for (uint32_t i = 0; i < e->n; ++i) bw_put(&w, q[i], e->row_bits[a][r]);
+    for (uint32_t b = 0; b < nb; ++b) {  /* one CoeffBlock per block (stream.cpp:229-251) */
+      const size_t ro = (size_t)b * e->k_l;
+      start = p;
+      for (uint32_t r = 0; r < e->k_l; ++r) {
+        put_f32(o, &p, e->row_min[a][ro + r]);
+        put_f32(o, &p, e->row_max[a][ro + r]);
+        put_u8(o, &p, e->row_bits[a][ro + r]);
+      }
+      sz.coeff_headers += p - start;
+      start = p;
+      w.pos = p;
+      w.acc = 0;
+      w.fill = 0;
+      for (uint32_t r = 0; r < e->k_l; ++r) {
+        if (e->row_min[a][ro + r] == e->row_max[a][ro + r]) continue;
+        const uint32_t* q = e->coeff_q[a] + (ro + r) * e->n;
+        for (uint32_t i = 0; i < e->n; ++i) bw_put(&w, q[i], e->row_bits[a][ro + r]);
+      }
+      bw_flush(&w);
+      p = w.pos;
+      sz.coeff_payload += p - start;
     }
-    bw_flush(&w);
-    p = w.pos;
-    sz.coeff_payload += p - start;
     if (uses_means(e->variant)) {  /* stream.cpp:255-263 */
       start = p;
       for (uint32_t f = 0; f < e->F; ++f) put_f32(o, &p, e->means[a][f]);

@@ -142,6 +142,15 @@ typedef struct {
   uint32_t* anchor_q[3];      /* n_c*F anchor-major */
   int variant;                /* stream.hpp:60-68: 0 pca, 1 pca_q, 2 v2v, 3 pca_qs, 4 pca_qp */
   float* means[3];            /* F per-frame vertex means (pca / pca_q), else unused */
+  /* blocks variant (5): n_b blocks of k_f = (F + pad) / n_b padded frames.
+   * n_b == 0 reads as 1.  With n_b > 1: dict_q[a] holds n_b * k_f^2 levels
+   * (first block at dict_bits, then n_b - 1 differences at diff_bits, each
+   * column-major); diff_min / diff_max[a] the n_b - 1 difference ranges;
+   * row_*[a] n_b * k_l headers and coeff_q[a] n_b * k_l * n levels, block b at
+   * row offset b * k_l; anchor_q stays n_c * F (unpadded). */
+  uint32_t n_b, pad;
+  float* diff_min[3];
+  float* diff_max[3];
 } orc_encoded;
 
 typedef struct {
@@ -168,6 +177,23 @@ int orc_encode_variant(int variant, uint32_t n, uint32_t F, const double* const 
                        double anchor_fraction, int anchor_bits, int dict_bits, int rounds,
                        uint64_t basis_seed, orc_encoded* out, double* U_out, double* evals_out,
                        orc_timing* timing, int nthreads);
+/* blocks variant (codec.cpp:351-473 with n_b > 1): frames padded with the
+ * last frame (pad_frames, codec.cpp:43-49); per block the k_f x k_f
+ * autocorrelation; block 0 full_eigenbasis, later blocks warm-started
+ * orthogonal_iterations (t_max, stop_tol < 0 = none) falling back to
+ * full_eigenbasis on RankDeficiency, then align_signs (block_dictionaries,
+ * codec.cpp:149-172); encode_dictionaries with difference coding and
+ * auto-realignment (codec.cpp:290-328); per block coeffs = dicts[b]^T delta_b^T
+ * quantised by rows; anchors as pca_qp.  out->n_b / pad are set here; the
+ * caller sizes the arrays (see orc_encoded).  U_out: 3 * n_b * k_f^2 (the
+ * unquantised dictionaries) or NULL.  variant must be 5. */
+int orc_encode_blocks(uint32_t n, uint32_t F, const double* const axes[3], const uint32_t* faces,
+                      uint32_t n_faces, uint32_t n_b, uint32_t k_l, const int* row_bits,
+                      double anchor_fraction, int anchor_bits, int dict_bits, int diff_bits,
+                      int t_max, double stop_tol, orc_encoded* out, double* U_out, int nthreads);
+/* decode_dictionaries (codec.cpp:330-349): the n_b decoded k_f x k_f
+ * dictionaries of axis a (col-major, block b at b * k_f^2). */
+int orc_decode_dictionaries(const orc_encoded* in, int a, double* out);
 /* solve_mean_constrained (src/solver.cpp:105-133): vertex 0 pinned, normal
  * equations of L[:, 1:] by sparse LDL^T, one refinement, per-column mean
  * shift to means[c].  delta, X: n x W vertex-major. */

@@ -30,7 +30,9 @@ class OrcEncoded(ctypes.Structure):
                 ("dict_q", u32p * 3), ("row_min", f32p * 3), ("row_max", f32p * 3),
                 ("row_bits", u8p * 3), ("coeff_q", u32p * 3), ("anchor_idx", u32p),
                 ("anchor_min", ctypes.c_float * 3), ("anchor_max", ctypes.c_float * 3),
-                ("anchor_q", u32p * 3), ("variant", ctypes.c_int), ("means", f32p * 3)]
+                ("anchor_q", u32p * 3), ("variant", ctypes.c_int), ("means", f32p * 3),
+                ("n_b", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("diff_min", f32p * 3), ("diff_max", f32p * 3)]
 
 
 class OrcTiming(ctypes.Structure):
@@ -93,6 +95,11 @@ def lib():
         L.orc_encode_variant.argtypes = [ctypes.c_int] + L.orc_encode.argtypes
         L.orc_solve_mean_constrained.argtypes = [ctypes.c_uint32, u32p, u32p, f64p,
                                                  ctypes.c_uint32, f64p, f64p, f64p, ctypes.c_int]
+        L.orc_encode_blocks.argtypes = [
+            ctypes.c_uint32, ctypes.c_uint32, f64p * 3, u32p, ctypes.c_uint32, ctypes.c_uint32,
+            ctypes.c_uint32, intp, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+            ctypes.c_int, ctypes.c_double, ctypes.POINTER(OrcEncoded), f64p, ctypes.c_int]
+        L.orc_decode_dictionaries.argtypes = [ctypes.POINTER(OrcEncoded), ctypes.c_int, f64p]
         L.orc_serialize.restype = ctypes.c_size_t
         L.orc_serialize.argtypes = [ctypes.POINTER(OrcEncoded), u8p, ctypes.POINTER(OrcSections)]
         L.orc_rate_exact.argtypes = [ctypes.POINTER(OrcSections), ctypes.c_uint32, ctypes.c_uint32,
@@ -295,20 +302,30 @@ def solve_mean_constrained(faces, n, delta: np.ndarray, means, nthreads=1):
 class Encoded:
     """Owner of the numpy buffers behind an OrcEncoded view."""
 
-    def __init__(self, n, F, k_l, n_c, faces, anchor_bits=16, dict_bits=16, variant=4):
+    def __init__(self, n, F, k_l, n_c, faces, anchor_bits=16, dict_bits=16, variant=4, n_b=1,
+                 diff_bits=8):
         self.faces = np.ascontiguousarray(faces, dtype=np.uint32)
-        self.dict_q = [np.zeros((F, F), np.uint32) for _ in range(3)]   # [col][row] = col-major
-        self.row_min = [np.zeros(max(k_l, 1), np.float32) for _ in range(3)]
-        self.row_max = [np.zeros(max(k_l, 1), np.float32) for _ in range(3)]
-        self.row_bits = [np.zeros(max(k_l, 1), np.uint8) for _ in range(3)]
-        self.coeff_q = [np.zeros((max(k_l, 1), n), np.uint32) for _ in range(3)]
+        pad = (n_b - F % n_b) % n_b
+        kf = (F + pad) // n_b
+        self.n_b, self.pad, self.kf = n_b, pad, kf
+        # [col][row] = col-major; blocks: (n_b, kf, kf), first block then differences
+        self.dict_q = [np.zeros((F, F) if n_b == 1 else (n_b, kf, kf), np.uint32)
+                       for _ in range(3)]
+        self.diff_min = [np.zeros(max(n_b - 1, 1), np.float32) for _ in range(3)]
+        self.diff_max = [np.zeros(max(n_b - 1, 1), np.float32) for _ in range(3)]
+        rows = max(k_l, 1) * n_b   # blocks: block b at row b * k_l
+        self.row_min = [np.zeros(rows, np.float32) for _ in range(3)]
+        self.row_max = [np.zeros(rows, np.float32) for _ in range(3)]
+        self.row_bits = [np.zeros(rows, np.uint8) for _ in range(3)]
+        self.coeff_q = [np.zeros((rows, n), np.uint32) for _ in range(3)]
         self.anchor_idx = np.zeros(max(n_c, 1), np.uint32)
         self.anchor_q = [np.zeros((max(n_c, 1), F), np.uint32) for _ in range(3)]
         self.means = [np.zeros(F, np.float32) for _ in range(3)]
         s = OrcEncoded()
         s.variant = variant
         s.n, s.F, s.k_l, s.n_c, s.n_faces = n, F, k_l, n_c, len(self.faces)
-        s.anchor_bits, s.dict_bits, s.diff_bits = anchor_bits, dict_bits, 8
+        s.anchor_bits, s.dict_bits, s.diff_bits = anchor_bits, dict_bits, diff_bits
+        s.n_b, s.pad = n_b, pad
         s.faces = P(self.faces, u32p)
         for a in range(3):
             s.dict_q[a] = P(self.dict_q[a], u32p)
@@ -318,6 +335,8 @@ class Encoded:
             s.coeff_q[a] = P(self.coeff_q[a], u32p)
             s.anchor_q[a] = P(self.anchor_q[a], u32p)
             s.means[a] = P(self.means[a], f32p)
+            s.diff_min[a] = P(self.diff_min[a], f32p)
+            s.diff_max[a] = P(self.diff_max[a], f32p)
         s.anchor_idx = P(self.anchor_idx, u32p)
         self.s = s
 
@@ -358,6 +377,39 @@ def encode(seq, k_l, bits, rounds=0, seed=0, anchor_fraction=0.01, anchor_bits=1
     if timing is not None:
         timing.update({k: getattr(tm, k) for k, _ in OrcTiming._fields_})
     return enc
+
+
+def encode_blocks(seq, n_b, k_l, bits, t_max=4, stop_tol=-1.0, anchor_fraction=0.01,
+                  anchor_bits=16, dict_bits=16, diff_bits=8, nthreads=1):
+    """codec.cpp:351-473 for the blocks variant (n_b blocks, block_dictionaries
+    codec.cpp:149-172, encode_dictionaries codec.cpp:290-328).  enc.U: (3, n_b,
+    kf, kf) unquantised dictionaries, enc.U[a][b] the matrix."""
+    n, F = seq.axes[0].shape
+    axes = [np.ascontiguousarray(a, dtype=np.float64) for a in seq.axes]
+    n_c = anchor_count(n, anchor_fraction)
+    enc = Encoded(n, F, k_l, n_c, seq.faces, anchor_bits, dict_bits, 5, n_b, diff_bits)
+    rb = np.full(max(k_l, 1), bits, dtype=np.int32) if np.isscalar(bits) else \
+        np.ascontiguousarray(bits, np.int32)
+    kf = enc.kf
+    U = np.zeros((3, n_b, kf, kf))  # [a][b][col][row]
+    rc = lib().orc_encode_blocks(n, F, (f64p * 3)(*[P(a, f64p) for a in axes]),
+                                 P(enc.faces, u32p), len(enc.faces), n_b, k_l, P(rb, intp),
+                                 anchor_fraction, anchor_bits, dict_bits, diff_bits, t_max,
+                                 stop_tol, ctypes.byref(enc.s), P(U, f64p), nthreads)
+    if rc:
+        raise ValueError(f"orc_encode_blocks error code {rc}")
+    enc.U = np.ascontiguousarray(np.swapaxes(U, 2, 3))
+    return enc
+
+
+def decode_dictionaries(enc: Encoded, a: int):
+    """decode_dictionaries (codec.cpp:330-349): (n_b, kf, kf) matrices."""
+    nb, kf = enc.n_b, enc.kf
+    out = np.zeros((nb, kf, kf))
+    rc = lib().orc_decode_dictionaries(ctypes.byref(enc.s), a, P(out, f64p))
+    if rc:
+        raise ValueError(f"decode_dictionaries code {rc}")
+    return np.ascontiguousarray(np.swapaxes(out, 1, 2))
 
 
 def decode(enc: Encoded, nthreads=1, timing=None):

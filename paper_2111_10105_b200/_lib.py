@@ -23,7 +23,7 @@ vp = ctypes.c_void_p
 DMCG_OK = 0
 DMCG_E_CUDA = 10
 DMCG_F64, DMCG_F32 = 0, 1
-DMCG_PCA, DMCG_PCA_Q, DMCG_V2V, DMCG_PCA_QS, DMCG_PCA_QP = 0, 1, 2, 3, 4
+DMCG_PCA, DMCG_PCA_Q, DMCG_V2V, DMCG_PCA_QS, DMCG_PCA_QP, DMCG_BLOCKS = 0, 1, 2, 3, 4, 5
 
 # symbols declared in include/dmcg.h (tests check every one is exported)
 EXPORTS = [
@@ -47,7 +47,7 @@ class DmcgConfig(ctypes.Structure):
                 ("anchor_strategy", ctypes.c_int), ("seed", ctypes.c_uint64),
                 ("laplacian", ctypes.c_int), ("raw_payload", ctypes.c_int),
                 ("oi_rounds", ctypes.c_int), ("oi_seed", ctypes.c_uint64),
-                ("oi_implicit", ctypes.c_int)]
+                ("oi_implicit", ctypes.c_int), ("oi_tolerance", ctypes.c_double)]
 
 
 class DmcgDecodeOptions(ctypes.Structure):
@@ -78,12 +78,15 @@ class DmcgEncoded(ctypes.Structure):
                 ("diff_bits", ctypes.c_uint8), ("faces", u32p), ("dict_q", u16p * 3),
                 ("row_min", f32p * 3), ("row_max", f32p * 3), ("row_bits", u8p * 3),
                 ("coeff_q", u16p * 3), ("anchor_idx", u32p), ("anchor_min", ctypes.c_float * 3),
-                ("anchor_max", ctypes.c_float * 3), ("anchor_q", u16p * 3), ("means", f32p * 3)]
+                ("anchor_max", ctypes.c_float * 3), ("anchor_q", u16p * 3), ("means", f32p * 3),
+                ("n_b", ctypes.c_uint16), ("pad", ctypes.c_uint16),
+                ("diff_min", f32p * 3), ("diff_max", f32p * 3)]
 
 
 class DmcgSizes(ctypes.Structure):
     _fields_ = [(k, ctypes.c_size_t) for k in ("dict_q", "rows", "coeff_q", "anchor_idx", "anchor_q",
-                                              "means")]
+                                              "means", "dict_ranges")] + \
+        [("n_b", ctypes.c_uint16), ("pad", ctypes.c_uint16)]
 
 
 class DmcgSections(ctypes.Structure):

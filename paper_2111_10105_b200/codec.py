@@ -52,6 +52,7 @@ class EncoderConfig:
     oi_rounds: int = 0             # 0 = full eigenbasis (reference n_b = 1 path)
     oi_seed: int = 0
     oi_implicit: bool = False      # Z = X^T (X Q) per round instead of R Q (R never formed)
+    oi_tolerance: Optional[float] = None  # blocks: principal-angle stop (spectral.cpp:90-97)
 
     def to_c(self):
         c = L.DmcgConfig()
@@ -69,17 +70,22 @@ class EncoderConfig:
         c.raw_payload = int(self.raw_payload)
         c.oi_rounds, c.oi_seed = self.oi_rounds, self.oi_seed
         c.oi_implicit = int(self.oi_implicit)
+        c.oi_tolerance = -1.0 if self.oi_tolerance is None else float(self.oi_tolerance)
         return c
 
 
 @dataclass
 class CompressedAnimation:
-    """n_b = 1 subset of dmc::CompressedAnimation (stream.hpp:130-155) for the
-    variants pca, pca_q, v2v, pca_qs, pca_qp.
+    """dmc::CompressedAnimation (stream.hpp:130-155) for the variants pca,
+    pca_q, v2v, pca_qs, pca_qp and blocks.
 
     dict_q[a] is (F, F) with dict_q[a][j, i] = level of U(i, j) (column-major
     pack order); coeff_q[a] is (k_l, n); anchor_q[a] is (n_c, F) (anchored
-    variants); means[a] is (F,) float32 (pca / pca_q)."""
+    variants); means[a] is (F,) float32 (pca / pca_q).  Blocks (n_b > 1, k_f =
+    (F + pad) / n_b): dict_q[a] is (n_b, k_f, k_f) -- dict_first then the
+    n_b - 1 dict_diffs, each [j, i] = level (i, j); diff_min / diff_max[a] the
+    (n_b - 1,) difference ranges; row_*[a] (n_b * k_l,) and coeff_q[a]
+    (n_b * k_l, n), block b at rows b * k_l."""
     n: int
     F: int
     k_l: int
@@ -99,15 +105,30 @@ class CompressedAnimation:
     anchor_max: list = field(default_factory=lambda: [0.0] * 3)
     anchor_q: list = field(default_factory=list)
     means: list = field(default_factory=list)
+    n_b: int = 1
+    pad: int = 0
+    diff_min: list = field(default_factory=list)
+    diff_max: list = field(default_factory=list)
+
+    @property
+    def k_f(self) -> int:
+        return (self.F + self.pad) // self.n_b
 
     @classmethod
-    def allocate(cls, n, F, k_l, n_c, faces, **kw):
+    def allocate(cls, n, F, k_l, n_c, faces, n_b=1, **kw):
         c = cls(n, F, k_l, n_c, np.ascontiguousarray(faces, dtype=np.uint32), **kw)
-        c.dict_q = [np.zeros((F, F), np.uint16) for _ in range(3)]
-        c.row_min = [np.zeros(max(k_l, 1), np.float32) for _ in range(3)]
-        c.row_max = [np.zeros(max(k_l, 1), np.float32) for _ in range(3)]
-        c.row_bits = [np.zeros(max(k_l, 1), np.uint8) for _ in range(3)]
-        c.coeff_q = [np.zeros((max(k_l, 1), n), np.uint16) for _ in range(3)]
+        c.n_b = max(int(n_b), 1)
+        c.pad = (c.n_b - F % c.n_b) % c.n_b if c.n_b > 1 else 0
+        kf = c.k_f
+        rows = max(k_l, 1) * c.n_b
+        c.dict_q = [np.zeros((F, F) if c.n_b == 1 else (c.n_b, kf, kf), np.uint16)
+                    for _ in range(3)]
+        c.diff_min = [np.zeros(max(c.n_b - 1, 1), np.float32) for _ in range(3)]
+        c.diff_max = [np.zeros(max(c.n_b - 1, 1), np.float32) for _ in range(3)]
+        c.row_min = [np.zeros(rows, np.float32) for _ in range(3)]
+        c.row_max = [np.zeros(rows, np.float32) for _ in range(3)]
+        c.row_bits = [np.zeros(rows, np.uint8) for _ in range(3)]
+        c.coeff_q = [np.zeros((rows, n), np.uint16) for _ in range(3)]
         c.anchor_idx = np.zeros(max(n_c, 1), np.uint32)
         c.anchor_q = [np.zeros((max(n_c, 1), F), np.uint16) for _ in range(3)]
         c.means = [np.zeros(F, np.float32) for _ in range(3)]
@@ -121,7 +142,11 @@ class CompressedAnimation:
         e.variant, e.flags = self.variant, 0
         e.anchor_bits, e.dict_bits, e.diff_bits = self.anchor_bits, self.dict_bits, self.diff_bits
         e.faces = self.faces.ctypes.data_as(L.u32p)
+        e.n_b, e.pad = self.n_b, self.pad
         for a in range(3):
+            if self.n_b > 1:
+                e.diff_min[a] = self.diff_min[a].ctypes.data_as(L.f32p)
+                e.diff_max[a] = self.diff_max[a].ctypes.data_as(L.f32p)
             e.dict_q[a] = self.dict_q[a].ctypes.data_as(L.u16p)
             e.row_min[a] = self.row_min[a].ctypes.data_as(L.f32p)
             e.row_max[a] = self.row_max[a].ctypes.data_as(L.f32p)
@@ -198,7 +223,7 @@ class Codec:
         cc = cfg.to_c()
         sizes = L.DmcgSizes()
         L.lib().dmcg_encoded_sizes(n, F, ctypes.byref(cc), ctypes.byref(sizes))
-        out = CompressedAnimation.allocate(n, F, cfg.k_l, sizes.anchor_idx, faces,
+        out = CompressedAnimation.allocate(n, F, cfg.k_l, sizes.anchor_idx, faces, n_b=cfg.n_b,
                                            anchor_bits=cfg.anchor_bits, dict_bits=cfg.dict_bits,
                                            diff_bits=cfg.diff_bits, variant=cfg.variant)
         e = out.to_c()
@@ -278,7 +303,7 @@ class Plan:
 
     def download(self) -> CompressedAnimation:
         out = CompressedAnimation.allocate(self.n, self.F, self.k_l, self.n_c, self.faces,
-                                           anchor_bits=self.cfg.anchor_bits,
+                                           n_b=self.cfg.n_b, anchor_bits=self.cfg.anchor_bits,
                                            dict_bits=self.cfg.dict_bits,
                                            diff_bits=self.cfg.diff_bits, variant=self.cfg.variant)
         e = out.to_c()
@@ -291,11 +316,19 @@ class Plan:
         _check(self.codec.handle, L.lib().dmcg_plan_upload(self._p, ctypes.byref(e)))
 
     def basis(self, axis: int):
-        U = np.zeros((self.F, self.F))  # column-major buffer -> U[j, i] = U(i, j)
-        ev = np.zeros(self.F)
+        """(U, evals); blocks: U is (n_b, k_f, k_f), U[b] block b's dictionary."""
+        nb = max(self.cfg.n_b, 1)
+        if nb > 1:
+            Fp = self.F + (nb - self.F % nb) % nb
+            kf = Fp // nb
+            U = np.zeros((nb, kf, kf))
+            ev = np.zeros(Fp)
+        else:
+            U = np.zeros((self.F, self.F))  # column-major buffer -> U[j, i] = U(i, j)
+            ev = np.zeros(self.F)
         _check(self.codec.handle, L.lib().dmcg_plan_basis(self._p, axis, U.ctypes.data_as(L.f64p),
                                                           ev.ctypes.data_as(L.f64p)))
-        return U.T.copy(), ev
+        return np.ascontiguousarray(np.swapaxes(U, -1, -2)), ev
 
     def stats(self) -> dict:
         st = L.DmcgStats()
@@ -354,7 +387,7 @@ def parse(data: bytes) -> CompressedAnimation:
     if rc:
         raise DmcError(rc, L.lib().dmcg_parse_error().decode())
     c = CompressedAnimation.allocate(hdr.n, hdr.F, hdr.k_l, hdr.n_c,
-                                     np.zeros((hdr.n_faces, 3), np.uint32),
+                                     np.zeros((hdr.n_faces, 3), np.uint32), n_b=hdr.n_b,
                                      anchor_bits=hdr.anchor_bits, dict_bits=hdr.dict_bits,
                                      diff_bits=hdr.diff_bits, variant=hdr.variant)
     e = c.to_c()
@@ -377,8 +410,8 @@ def rate_exact(c: CompressedAnimation) -> dict:
 
 def _n_anchors(n, cfg) -> int:
     """n_c of an encode (codec.cpp:374): anchored variants only."""
-    return anchor_count(n, cfg.anchor_fraction) if cfg.variant in (L.DMCG_PCA_QS, L.DMCG_PCA_QP) \
-        else 0
+    return anchor_count(n, cfg.anchor_fraction) \
+        if cfg.variant in (L.DMCG_PCA_QS, L.DMCG_PCA_QP, L.DMCG_BLOCKS) else 0
 
 
 def anchor_count(n: int, fraction: float = 0.01) -> int:

@@ -345,13 +345,13 @@ __global__ void k_rhs_rm(int n, int F, int W, int F_all, int f_off, const uint32
 
 template <typename T>
 __global__ void k_output_rm(int n, int F, int F_all, int f_off, const double* __restrict__ X, T* o0,
-                            T* o1, T* o2, const double* __restrict__ shift) {
+                            T* o1, T* o2, const double* __restrict__ shift, int F_out) {
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  const long nF = (long)n * F;
+  const long nF = (long)n * F_out;
   if (t >= 3 * nF) return;
   const int a = (int)(t / nF);
   const long rem = t % nF;
-  const int i = (int)(rem / F), f = (int)(rem % F);
+  const int i = (int)(rem / F_out), f = (int)(rem % F_out);
   T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
   const double v = X[(size_t)i * 3 * F + (size_t)a * F + f];
   o[(size_t)i * F_all + f_off + f] = (T)(shift ? v + shift[a * F + f] : v);
@@ -458,15 +458,16 @@ cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
 }
 
 cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
-                             void* const out[3], bool f32, const double* shift) {
-  const long total = 3L * n * F;
+                             void* const out[3], bool f32, const double* shift, int F_out) {
+  if (F_out < 0) F_out = F;
+  const long total = 3L * n * F_out;
   const unsigned grid = (unsigned)((total + 255) / 256);
   if (f32)
     k_output_rm<float><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (float*)out[0], (float*)out[1],
-                                            (float*)out[2], shift);
+                                            (float*)out[2], shift, F_out);
   else
     k_output_rm<double><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (double*)out[0],
-                                             (double*)out[1], (double*)out[2], shift);
+                                             (double*)out[1], (double*)out[2], shift, F_out);
   return cudaGetLastError();
 }
 

@@ -346,9 +346,9 @@ Status check_config(const dmcg_config& cfg, uint32_t n, uint32_t k, std::vector<
       return {DMCG_E_CONFIG,
               "InvalidBits: row bit depth " + std::to_string(bits) + " outside 1..16"};
   // Scope of the B200 path.
-  if (cfg.variant < DMCG_PCA || cfg.variant > DMCG_PCA_QP)
+  if (cfg.variant < DMCG_PCA || cfg.variant > DMCG_BLOCKS)
     return {DMCG_E_UNSUPPORTED,
-            "Unsupported: only the n_b = 1 variants pca, pca_q, v2v, pca_qs, pca_qp are on the "
+            "Unsupported: only the variants pca, pca_q, v2v, pca_qs, pca_qp, blocks are on the "
             "B200 path"};
   if (cfg.raw_payload) return {DMCG_E_UNSUPPORTED, "Unsupported: raw_payload debug mode"};
   if (cfg.laplacian != 0)
@@ -424,6 +424,7 @@ void dmcg_config_default(dmcg_config* cfg) {
   cfg->oi_rounds = 0;
   cfg->oi_seed = 0;
   cfg->oi_implicit = 0;
+  cfg->oi_tolerance = -1.0;
 }
 
 void dmcg_decode_options_default(dmcg_decode_options* o) {
@@ -481,6 +482,19 @@ int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_size
       variant_uses_anchors(cfg->variant) ? dmcg_anchor_count(n, cfg->anchor_fraction) : 0;
   out->anchor_q = out->anchor_idx * (size_t)F;
   out->means = variant_uses_means(cfg->variant) ? F : 0;
+  const uint32_t nb = cfg->n_b ? cfg->n_b : 1;
+  out->n_b = (uint16_t)nb;
+  out->pad = 0;
+  out->dict_ranges = 0;
+  if (nb > 1) {  // blocks: padded frames, n_b dictionaries and coefficient blocks
+    if (nb > F) return DMCG_E_CONFIG;
+    const uint32_t pad = (nb - F % nb) % nb, kf = (F + pad) / nb;
+    out->pad = (uint16_t)pad;
+    out->dict_q = (size_t)nb * kf * kf;
+    out->dict_ranges = nb - 1;
+    out->rows = (size_t)nb * cfg->k_l;
+    out->coeff_q = out->rows * n;
+  }
   return DMCG_OK;
 }
 
@@ -551,6 +565,27 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     return st;
   }
   p->k = cfg->k_l;
+  p->k_l = cfg->k_l;
+  p->F_in = F;
+  if (cfg->variant == DMCG_BLOCKS) {
+    // pad_frames (codec.cpp:43-49): the plan works on F + pad frames
+    p->nb = cfg->n_b;
+    p->pad = (p->nb - F % p->nb) % p->nb;
+    F += p->pad;
+    p->F = F;
+    p->kf = F / p->nb;
+    p->k = p->nb * p->k_l;
+    if (p->kf > 512) {
+      delete p;
+      return {DMCG_E_UNSUPPORTED, "Unsupported: blocks of more than 512 frames"};
+    }
+    std::vector<int> tiled;
+    for (uint32_t b = 0; b < p->nb; ++b) tiled.insert(tiled.end(), p->row_bits.begin(), p->row_bits.end());
+    p->row_bits.swap(tiled);
+  }
+  p->t_max = cfg->t_max;
+  p->oi_tol = cfg->oi_tolerance;
+  if (cfg->variant == DMCG_BLOCKS) p->rounds = 0;  // block 0: full_eigenbasis (codec.cpp:159)
   p->variant = cfg->variant;
   p->rounds = cfg->oi_rounds;
   p->oi_seed = cfg->oi_seed;
@@ -605,7 +640,12 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_Q = (double*)get(3 * (size_t)F * kk * 8);
   p->d_Z = (double*)get(3 * (size_t)F * kk * 8);
   p->d_tau = (double*)get(3 * (size_t)F * 8);
-  p->d_H = (double*)get(3 * 2 * (size_t)F2 * (F2 + 1) * 8);  // jacobi: A (m2 x m2+1) + V per axis
+  size_t jac = 3 * 2 * (size_t)F2 * (F2 + 1);  // jacobi: A (m2 x m2+1) + V per axis
+  if (p->nb > 1) {  // the blocks' eigenbases: 3 nb batches of kf
+    const size_t kf2 = p->kf + (p->kf & 1);
+    jac = std::max(jac, 3 * (size_t)p->nb * 2 * kf2 * (kf2 + 1));
+  }
+  p->d_H = (double*)get(jac * 8);
   p->d_V = (double*)get(3 * FF * 8);
   p->d_qr_scr = (double*)get(3 * dmcg::qr_scratch_doubles((int)F, (int)kk) * 8);
   p->d_w = (double*)get(3 * (size_t)F * 8);
@@ -625,6 +665,14 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_rowp = (double*)get(3 * kk * 2 * 8);
   p->d_cg_iters = (int*)get(p->W_pad * 4);
   p->d_cg_res = (double*)get(p->W_pad * 8);
+  if (p->nb > 1) {
+    const size_t bk = (size_t)p->nb * p->kf * p->kf;
+    p->d_bUeig = (double*)get(3 * bk * 8);
+    p->d_bUd = (double*)get(3 * bk * 8);
+    p->d_bwork = (double*)get(3 * dmcg::block_work_doubles((int)p->kf) * 8);
+    p->d_diff_rng = (float*)get(3 * (size_t)(p->nb - 1) * 2 * 4);
+    if (p->pad) p->d_xpad = get(3 * nF * (dtype == DMCG_F32 ? 4 : 8));
+  }
   if (!ok) {
     dmcg_plan_destroy(p);
     return {DMCG_E_CUDA, "CudaError: device allocation failed"};
@@ -838,7 +886,7 @@ int dmcg_plan_distortion(dmcg_plan* p, const void* const d_orig[3], const void* 
                          double* frame_rms, double* nmsve, double* vertex_mean_error) {
   if (!p || !d_orig || !d_recon || !frame_rms || !nmsve) return DMCG_E_CONFIG;
   cudaSetDevice(p->ctx->device);
-  const size_t n = p->n, F = p->F;
+  const size_t n = p->n, F = p->F_in;  // the caller's (unpadded) frames
   if (!p->d_metric) p->d_metric = (double*)plan_alloc(p, (3 * n * F + 2 * F + n) * 8);
   if (!p->d_metric) return p->ctx->set_error({DMCG_E_CUDA, "CudaError: device allocation failed"});
   cudaStream_t s = p->ctx->stream;
@@ -886,6 +934,9 @@ int dmcg_plan_create_shard(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype, con
     return ctx->set_error({DMCG_E_UNSUPPORTED,
                            "Unsupported: vertex-row shards of the pca / pca_q variants (their "
                            "frame means need a cross-rank reduction)"});
+  if (cfg->variant == DMCG_BLOCKS)
+    return ctx->set_error({DMCG_E_UNSUPPORTED,
+                           "Unsupported: vertex-row shards of the blocks variant"});
   if (comm && (comm_size(comm) != nranks || comm_rank(comm) != rank))
     return ctx->set_error({DMCG_E_CONFIG, "ConfigError: communicator does not match rank"});
   cudaSetDevice(ctx->device);
@@ -939,10 +990,15 @@ int dmcg_plan_decode_device(dmcg_plan* p, const dmcg_decode_options* opt, void* 
 
 static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
   cudaStream_t s = p->ctx->stream;
-  const size_t n = p->n, F = p->F, k = p->k, FF = F * F;
+  // blocks: per axis nb k_f^2 dictionary levels and nb k_l rows; anchors
+  // and frames unpadded (F_in) on the host
+  const size_t n = p->n, F = p->F, k = p->k, Fo = p->F_in;
+  const size_t FF = p->nb > 1 ? (size_t)p->nb * p->kf * p->kf : F * F;
   e->n = p->n;
-  e->F = p->F;
-  e->k_l = p->k;
+  e->F = p->F_in;
+  e->k_l = p->k_l;
+  e->n_b = (uint16_t)p->nb;
+  e->pad = (uint16_t)p->pad;
   e->n_c = p->n_c;
   e->n_faces = p->n_faces;
   e->variant = (uint8_t)p->variant;
@@ -962,8 +1018,17 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
                               cudaMemcpyDeviceToHost, s));
     }
     if (p->n_c)
-      CUDA_OK(cudaMemcpyAsync(e->anchor_q[a], p->d_anchor_q + a * (size_t)p->n_c * F,
-                              (size_t)p->n_c * F * 2, cudaMemcpyDeviceToHost, s));
+      CUDA_OK(cudaMemcpy2DAsync(e->anchor_q[a], Fo * 2, p->d_anchor_q + a * (size_t)p->n_c * F,
+                                F * 2, Fo * 2, p->n_c, cudaMemcpyDeviceToHost, s));
+    if (p->nb > 1) {
+      std::vector<float> rng2(2 * (p->nb - 1));
+      CUDA_OK(cudaMemcpy(rng2.data(), p->d_diff_rng + a * rng2.size(), rng2.size() * 4,
+                         cudaMemcpyDeviceToHost));
+      for (uint32_t b = 0; b + 1 < p->nb; ++b) {
+        e->diff_min[a][b] = rng2[2 * b];
+        e->diff_max[a][b] = rng2[2 * b + 1];
+      }
+    }
     if (variant_uses_means(p->variant) && e->means[a])
       CUDA_OK(cudaMemcpyAsync(e->means[a], p->d_means + a * F, F * 4, cudaMemcpyDeviceToHost, s));
   }
@@ -995,6 +1060,36 @@ int dmcg_plan_download(dmcg_plan* p, dmcg_encoded* out) {
 static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_sections* sec,
                                   size_t* size) {
   cudaStream_t s = p->ctx->stream;
+  if (p->nb > 1) {
+    // blocks: the per-block sections are framed on the host from the
+    // downloaded symbols (the device packer covers the n_b = 1 layout)
+    const size_t nb = p->nb, kk = (size_t)p->kf * p->kf, rows = (size_t)p->k;
+    std::vector<uint16_t> dq(3 * nb * kk), cq(3 * rows * p->n), aq(3 * (size_t)p->n_c * p->F_in);
+    std::vector<float> rmin(3 * rows + 1), rmax(3 * rows + 1), dmin(3 * nb), dmax(3 * nb);
+    std::vector<uint8_t> rbits(3 * rows + 1);
+    std::vector<uint32_t> aidx(p->n_c + 1);
+    dmcg_encoded m;
+    std::memset(&m, 0, sizeof(m));
+    for (int a = 0; a < 3; ++a) {
+      m.dict_q[a] = dq.data() + a * nb * kk;
+      m.row_min[a] = rmin.data() + a * rows;
+      m.row_max[a] = rmax.data() + a * rows;
+      m.row_bits[a] = rbits.data() + a * rows;
+      m.coeff_q[a] = cq.data() + a * rows * p->n;
+      m.anchor_q[a] = aq.data() + a * (size_t)p->n_c * p->F_in;
+      m.diff_min[a] = dmin.data() + a * nb;
+      m.diff_max[a] = dmax.data() + a * nb;
+    }
+    m.anchor_idx = aidx.data();
+    m.faces = p->faces.data();
+    Status st = download_impl(p, &m);
+    if (!st.good()) return st;
+    *size = serialize_stream(&m, nullptr, 0, sec, nullptr);
+    if (!out) return Status::ok();
+    if (cap < *size) return {DMCG_E_CONFIG, "ConfigError: serialize buffer too small"};
+    serialize_stream(&m, out, cap, sec, nullptr);
+    return Status::ok();
+  }
   const size_t n = p->n, F = p->F, k = p->k;
   std::vector<float> rmin(3 * k + 1), rmax(3 * k + 1);
   std::vector<uint8_t> rbits(3 * k + 1);
@@ -1087,8 +1182,18 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
 
 static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
   cudaStream_t s = p->ctx->stream;
-  const size_t n = p->n, F = p->F, k = p->k, FF = F * F;
+  const size_t n = p->n, F = p->F, k = p->k, Fo = p->F_in;
+  const size_t FF = p->nb > 1 ? (size_t)p->nb * p->kf * p->kf : F * F;
   float rng[6];
+  if (p->nb > 1) {
+    std::vector<float> rng2(3 * 2 * (p->nb - 1));
+    for (int a = 0; a < 3; ++a)
+      for (uint32_t b = 0; b + 1 < p->nb; ++b) {
+        rng2[(a * (p->nb - 1) + b) * 2] = e->diff_min[a][b];
+        rng2[(a * (p->nb - 1) + b) * 2 + 1] = e->diff_max[a][b];
+      }
+    CUDA_OK(cudaMemcpy(p->d_diff_rng, rng2.data(), rng2.size() * 4, cudaMemcpyHostToDevice));
+  }
   for (int a = 0; a < 3; ++a) {
     CUDA_OK(cudaMemcpyAsync(p->d_dict_q + a * FF, e->dict_q[a], FF * 2, cudaMemcpyHostToDevice, s));
     if (k) {
@@ -1099,8 +1204,8 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
                               cudaMemcpyHostToDevice, s));
     }
     if (p->n_c)
-      CUDA_OK(cudaMemcpyAsync(p->d_anchor_q + a * (size_t)p->n_c * F, e->anchor_q[a],
-                              (size_t)p->n_c * F * 2, cudaMemcpyHostToDevice, s));
+      CUDA_OK(cudaMemcpy2DAsync(p->d_anchor_q + a * (size_t)p->n_c * F, F * 2, e->anchor_q[a],
+                                Fo * 2, Fo * 2, p->n_c, cudaMemcpyHostToDevice, s));
     if (variant_uses_means(p->variant)) {
       if (!e->means[a]) return {DMCG_E_CORRUPT, "CorruptPayload: missing frame means"};
       CUDA_OK(cudaMemcpyAsync(p->d_means + a * F, e->means[a], F * 4, cudaMemcpyHostToDevice, s));
@@ -1109,6 +1214,8 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
     rng[2 * a + 1] = e->anchor_max[a];
   }
   CUDA_OK(cudaMemcpyAsync(p->d_anchor_rng, rng, sizeof(rng), cudaMemcpyHostToDevice, s));
+  // the decoder's anchor padding (codec.cpp:483-495): frames F_in.. repeat the last
+  if (p->n_c && F > Fo) CUDA_OK(launch_pad_anchor_levels(s, (int)p->n_c, (int)Fo, (int)F, p->d_anchor_q));
   CUDA_OK(cudaStreamSynchronize(s));  // rng is a stack buffer
   return Status::ok();
 }
@@ -1122,7 +1229,9 @@ int dmcg_plan_upload(dmcg_plan* p, const dmcg_encoded* in) {
 int dmcg_plan_basis(dmcg_plan* p, int axis, double* U_host, double* evals_host) {
   if (!p || axis < 0 || axis > 2) return DMCG_E_CONFIG;
   cudaSetDevice(p->ctx->device);
-  const size_t FF = (size_t)p->F * p->F;
+  // blocks: the nb k_f x k_f dictionaries of the axis (nb k_f^2 doubles);
+  // evals = the per-block eigenvalues of the direct decomposition
+  const size_t FF = p->nb > 1 ? (size_t)p->nb * p->kf * p->kf : (size_t)p->F * p->F;
   cudaStream_t s = p->ctx->stream;
   if (U_host) cudaMemcpyAsync(U_host, p->d_U + axis * FF, FF * 8, cudaMemcpyDeviceToHost, s);
   if (evals_host)
@@ -1240,10 +1349,17 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   cudaSetDevice(ctx->device);
   // Header sanity (the same bounds parse() enforces, stream.cpp:322-336).
   if (in->n < 1 || in->F < 1) return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: empty animation"});
-  if (in->variant > DMCG_PCA_QP)
+  if (in->variant > DMCG_BLOCKS)
     return ctx->set_error({DMCG_E_UNSUPPORTED,
-                           "Unsupported: only the n_b = 1 variants pca, pca_q, v2v, pca_qs, pca_qp "
+                           "Unsupported: only the variants pca, pca_q, v2v, pca_qs, pca_qp, blocks "
                            "are on the B200 path"});
+  const uint32_t nb = in->n_b > 1 ? in->n_b : 1;
+  if (nb > 1 && in->variant != DMCG_BLOCKS)
+    return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: block count > 1 requires the blocks variant"});
+  if (nb > 1 && (in->pad != (nb - in->F % nb) % nb))
+    return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: padding does not match the block count"});
+  if (nb > 1 && in->k_l > (in->F + in->pad) / nb)
+    return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: retained row count exceeds dictionary dimension"});
   if (in->k_l > in->F)
     return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: retained row count exceeds dictionary dimension"});
   if (variant_uses_anchors(in->variant) ? (in->n_c < 1 || in->n_c > in->n) : in->n_c != 0)
@@ -1259,13 +1375,13 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   dmcg_config_default(&cfg);
   cfg.variant = in->variant;
   cfg.k_l = in->k_l;
+  cfg.n_b = (uint16_t)nb;
   std::vector<int> rb(in->k_l, 16);
-  for (uint32_t r = 0; r < in->k_l; ++r) {
-    rb[r] = in->row_bits[0][r];
+  for (uint32_t r = 0; r < in->k_l; ++r) rb[r] = in->row_bits[0][r];
+  for (uint32_t r = 0; r < nb * in->k_l; ++r)
     for (int a = 0; a < 3; ++a)
       if (in->row_bits[a][r] < 1 || in->row_bits[a][r] > 16)
         return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: row bit depth outside 1..16"});
-  }
   cfg.row_bits = rb.data();
   cfg.n_row_bits = in->k_l;
   cfg.anchor_bits = in->anchor_bits;

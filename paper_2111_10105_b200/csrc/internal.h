@@ -16,8 +16,10 @@
 
 namespace dmcg {
 
-// Variant predicates (include/dmc/stream.hpp:77-84), n_b = 1 variants.
-inline bool variant_uses_anchors(int v) { return v == DMCG_PCA_QS || v == DMCG_PCA_QP; }
+// Variant predicates (include/dmc/stream.hpp:77-84).
+inline bool variant_uses_anchors(int v) {
+  return v == DMCG_PCA_QS || v == DMCG_PCA_QP || v == DMCG_BLOCKS;
+}
 inline bool variant_uses_means(int v) { return v == DMCG_PCA || v == DMCG_PCA_Q; }
 inline bool variant_uses_delta(int v) { return v != DMCG_V2V; }
 
@@ -256,6 +258,20 @@ struct dmcg_plan {
   bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
   dmcg::PlanGraph g_encode, g_decode;
+
+  // blocks variant (n_b > 1, codec.cpp:149-172, 290-349): F above is the
+  // padded frame count F_in + pad = nb * kf, k = nb * k_l coefficient rows
+  // per axis (block b at rows [b k_l, (b+1) k_l)); d_R / d_U / d_dict_q hold
+  // the nb per-block k_f x k_f matrices of each axis back to back.
+  uint32_t nb = 1, kf = 0, k_l = 0, F_in = 0, pad = 0;
+  int t_max = 4;
+  double oi_tol = -1.0;
+  double* d_bUeig = nullptr;       // 3 x nb x kf^2 eigenbases of every block
+  double* d_bwork = nullptr;       // 3 x block_work_doubles(kf)
+  double* d_bUd = nullptr;         // 3 x nb x kf^2 decoded dictionaries
+  float* d_diff_rng = nullptr;     // 3 x (nb - 1) x 2 difference ranges
+  void* d_xpad = nullptr;          // 3 x n x F padded input (pad > 0)
+  int oi_fallbacks = 0;            // blocks that fell back to full_eigenbasis (last encode)
 
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // ctx->stream <-> ctx->aux

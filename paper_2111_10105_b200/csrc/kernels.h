@@ -121,7 +121,8 @@ cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
                           int n_c, const uint16_t* anchor_q, const float* anchor_rng,
                           int anchor_bits, const double* D, double* B, int* flags);
 cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
-                             void* const out[3], bool f32, const double* shift = nullptr);
+                             void* const out[3], bool f32, const double* shift = nullptr,
+                             int F_out = -1);  // frames written per axis (< 0: F)
 // Anchor-free variants (pca / pca_q): per-frame vertex means of the input
 // (codec.cpp:432-441) -> means (3 x F floats); the per-column shift of the
 // mean-constrained solution (solver.cpp:129-131) -> shift (3 Fw doubles).
@@ -130,5 +131,35 @@ cudaError_t launch_frame_means(cudaStream_t s, int n, int F, const void* const x
                                double* partial, float* means);
 cudaError_t launch_mean_shift(cudaStream_t s, int n, int Fw, int F_all, int f0, const double* X,
                               const float* means, double* partial, double* shift);
+
+// ---- blocks.cu (variant blocks, n_b > 1) ----------------------------------
+// pad_frames (codec.cpp:43-49): out (3 x n x Fp, plan dtype) = x with the
+// last frame repeated into frames F..Fp-1.
+cudaError_t launch_pad_frames(cudaStream_t s, int n, int F, int Fp, const void* const x[3],
+                              bool f32, void* out);
+// block_dictionaries (codec.cpp:149-172) after the per-block eigenbases:
+// per axis, block 0 = Ueig[0]; block b > 0 = orthogonal_iterations(R_b,
+// U_{b-1}, t_max, tol) (spectral.cpp:69-104) or, on RankDeficiency,
+// Ueig[b]; then align_signs against U_{b-1} (spectral.cpp:122-131).
+// R, Ueig, U: 3 x nb x kf x kf col-major; work: 3 x block_work_doubles(kf).
+// flags[0] += number of blocks that fell back to the eigenbasis.
+cudaError_t launch_block_chain(cudaStream_t s, int nb, int kf, int t_max, double tol,
+                               const double* R, const double* Ueig, double* U, double* work,
+                               int* flags);
+size_t block_work_doubles(int kf);
+// encode_dictionaries (codec.cpp:290-328, auto_realign): q (3 x nb x kf^2)
+// = first block at dict_bits, then the closed-loop differences at
+// diff_bits; rng (3 x (nb-1) x 2) their widened ranges.
+cudaError_t launch_dict_encode_blocks(cudaStream_t s, int nb, int kf, int dict_bits,
+                                      int diff_bits, const double* U, double* work, uint16_t* q,
+                                      float* rng);
+// decode_dictionaries (codec.cpp:330-349): Ud (3 x nb x kf^2); flags |= 1 on
+// a level out of range.
+cudaError_t launch_dict_decode_blocks(cudaStream_t s, int nb, int kf, int dict_bits,
+                                      int diff_bits, const uint16_t* q, const float* rng,
+                                      int* flags, double* Ud);
+// anchor levels (3 x n_c x Fp): columns F..Fp-1 = column F-1 (the decoder's
+// anchor padding, codec.cpp:483-495).
+cudaError_t launch_pad_anchor_levels(cudaStream_t s, int n_c, int F, int Fp, uint16_t* q);
 
 }  // namespace dmcg

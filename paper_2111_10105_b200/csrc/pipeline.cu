@@ -270,9 +270,101 @@ Status basis(dmcg_plan* p, const void* const x[3] = nullptr, int nrows = 0,
 
 }  // namespace
 
+// Blocks variant operand: batch b = axis b / nb, block b % nb; element
+// (k, i) of the block at p[axis] + block * off + k * sk + i * si.
+template <typename T, bool KC>
+struct LoadBlocks {
+  static constexpr bool kKContig = KC;
+  const T* p0;
+  const T* p1;
+  const T* p2;
+  int nb;
+  long off, sk, si;
+  __device__ __forceinline__ const T* addr(int b, int k, int i) const {
+    const int a = b / nb, blk = b - a * nb;
+    return (a == 0 ? p0 : (a == 1 ? p1 : p2)) + blk * off + (long)k * sk + (long)i * si;
+  }
+  __device__ __forceinline__ double operator()(int b, int k, int i) const {
+    return (double)*addr(b, k, i);
+  }
+};
+
+// Blocks variant encode (codec.cpp:351-473 with n_b > 1): padded frames,
+// every block's k_f x k_f autocorrelation and eigenbasis as batched
+// launches over the 3 n_b blocks, the sequential warm-started OI chain and
+// dictionary difference coder per axis, then the batched per-block
+// projection + row quantisation and the anchors.
+template <typename T>
+static Status enqueue_encode_blocks_t(dmcg_plan* p, const void* const x[3]) {
+  cudaStream_t s = p->ctx->stream;
+  const int n = (int)p->n, Fp = (int)p->F, Fi = (int)p->F_in, nb = (int)p->nb, kf = (int)p->kf;
+  const int kl = (int)p->k_l, k = (int)p->k, nbat = 3 * nb;
+  const long kk = (long)kf * kf;
+  const bool f32 = p->dtype == DMCG_F32;
+  DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
+  DMCG_TRY(record_event(p->ev[0], s));
+  const void* xs[3] = {x[0], x[1], x[2]};
+  if (p->pad) {  // pad_frames (codec.cpp:43-49)
+    DMCG_TRY(launch_pad_frames(s, n, Fi, Fp, x, f32, p->d_xpad));
+    for (int a = 0; a < 3; ++a) xs[a] = (const T*)p->d_xpad + (size_t)a * n * Fp;
+  }
+  // delta of the padded trajectories (column-separable: block b's delta is
+  // columns [b k_f, (b+1) k_f), codec.cpp:419)
+  DMCG_TRY(launch_delta(s, n, Fp, p->d_lap_rp, p->d_lap_ci, xs, f32, p->d_delta, p->d_flags));
+  DMCG_TRY(record_event(p->ev[1], s));
+  // R_b = A_b A_b^T per block (spectral.cpp:35-39), split-K over vertices
+  {
+    const int tiles = ((kf + kBM - 1) / kBM) * ((kf + kBN - 1) / kBN);
+    int splits = pick_splits(tiles, nbat, n);
+    const long maxs = (long)(p->part_elems / ((long)nbat * kk));
+    if (splits > maxs) splits = (int)maxs;
+    splits = gemm_splits(n, splits, nullptr);
+    LoadBlocks<T, false> lx{(const T*)xs[0], (const T*)xs[1], (const T*)xs[2], nb, (long)kf,
+                            (long)Fp, 1L};
+    DMCG_TRY(launch_gemm(s, nbat, kf, kf, n, splits, lx, lx, StorePartial{p->d_part, nbat}));
+    DMCG_TRY(launch_reduce_sym(s, kf, splits, nbat, p->d_part, p->d_R));
+  }
+  DMCG_TRY(record_event(p->ev[2], s));
+  // full_eigenbasis of every block (block 0's dictionary, the later blocks'
+  // RankDeficiency fallback), then the OI chain + align_signs per axis
+  DMCG_TRY(launch_jacobi(s, nbat, kf, p->d_R, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
+  DMCG_TRY(launch_sort_basis(s, nbat, kf, kf, p->d_V, p->d_w, p->d_bUeig, kk, p->d_evals, kf));
+  DMCG_TRY(launch_canon_signs(s, nbat, kf, 0, kf, p->d_bUeig, kk));
+  DMCG_TRY(launch_block_chain(s, nb, kf, p->t_max, p->oi_tol, p->d_R, p->d_bUeig, p->d_U,
+                              p->d_bwork, p->d_flags + 5));
+  DMCG_TRY(record_event(p->ev[3], s));
+  // coeffs_b = dicts[b]^T delta_b^T, rows < k_l (codec.cpp:420), + quantize_rows
+  if (kl > 0) {
+    DMCG_TRY(launch_init_keys(s, 3L * k, p->d_keys));
+    LoadDense<double, true> lU{p->d_U, kk, 1L, (long)kf};  // A(f, r) = U_b(f, r)
+    const double* d = p->d_delta;
+    const long nF = (long)n * Fp;
+    LoadBlocks<double, true> lD{d, d + nF, d + 2 * nF, nb, (long)kf, 1L, (long)Fp};
+    DMCG_TRY(launch_gemm(s, nbat, kl, n, kf, 1, lU, lD, StoreCoeffMinMax{p->d_C, p->d_keys}));
+    DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
+                               p->d_row_max, p->d_row_bits, p->d_coeff_q));
+  }
+  DMCG_TRY(record_event(p->ev[4], s));
+  // anchors (codec.cpp:444-471): the padded frames repeat the last one, so
+  // the range and the first F_in levels equal those of the unpadded input
+  DMCG_TRY(launch_anchors(s, (int)p->n_c, Fp, p->d_anchor_idx, xs, f32, p->anchor_bits,
+                          p->d_anchor_rng, p->d_anchor_q));
+  // encode_dictionaries (codec.cpp:290-328)
+  DMCG_TRY(launch_dict_encode_blocks(s, nb, kf, p->dict_bits, p->diff_bits, p->d_U, p->d_bwork,
+                                     p->d_dict_q, p->d_diff_rng));
+  DMCG_TRY(record_event(p->ev[5], s));
+  return Status::ok();
+}
+
+static Status enqueue_encode_blocks(dmcg_plan* p, const void* const x[3]) {
+  return p->dtype == DMCG_F32 ? enqueue_encode_blocks_t<float>(p, x)
+                              : enqueue_encode_blocks_t<double>(p, x);
+}
+
 // Every kernel of one encode on the plan stream (no host synchronisation:
 // capturable into a CUDA graph).
 static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
+  if (p->nb > 1) return enqueue_encode_blocks(p, x);
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
   const bool f32 = p->dtype == DMCG_F32;
@@ -408,6 +500,10 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   }
   p->stats.kernel_launches_encode =
       1 + 2 + (p->rounds > 0 && k < F ? 2 * p->rounds + 12 : 3) + 1 + (k > 0 ? 3 : 0) + 1;
+  if (p->nb > 1) {
+    p->stats.kernel_launches_encode = (p->pad ? 1 : 0) + 1 + 2 + 4 + (k > 0 ? 3 : 0) + 2;
+    p->oi_fallbacks = flags[5];
+  }
   if (flags[0]) {
     std::string axes;
     for (int a = 0; a < 3; ++a)
@@ -586,7 +682,22 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
   s = p->ctx->aux;
   DMCG_TRY(cudaEventRecord(p->ev_fork, s1));
   DMCG_TRY(cudaStreamWaitEvent(s, p->ev_fork, 0));
-  if (k > 0) {
+  if (k > 0 && p->nb > 1) {
+    // blocks: decode_dictionaries (closed-loop sums), dequantize_rows of
+    // every block, then delta~(:, block b) = (U~_b c~_b)^T as one batched
+    // GEMM over the 3 n_b blocks (codec.cpp:527-533)
+    const int nb = (int)p->nb, kf = (int)p->kf, kl = (int)p->k_l;
+    const long kk = (long)kf * kf;
+    DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
+    DMCG_TRY(launch_dequant_rows(s, 3 * k, n, p->d_coeff_q, p->d_rowp, p->d_row_bits,
+                                 p->d_flags + 1, p->d_C));
+    DMCG_TRY(launch_dict_decode_blocks(s, nb, kf, p->dict_bits, p->diff_bits, p->d_dict_q,
+                                       p->d_diff_rng, p->d_flags + 1, p->d_bUd));
+    LoadDense<double, false> la{p->d_C, (long)kl * n, (long)n, 1L};  // A(r, i) = c~_b(r, i)
+    LoadDense<double, false> lb{p->d_bUd, kk, (long)kf, 1L};         // B(r, f) = U~_b(f, r)
+    DMCG_TRY(launch_gemm(s, 3 * nb, n, kf, kl, 1, la, lb,
+                         StoreStrided{p->d_rm_delta, (long)kf, (long)W, 1L}));
+  } else if (k > 0) {
     DMCG_TRY(launch_row_params(s, 3 * k, p->d_row_min, p->d_row_max, p->d_row_bits, p->d_rowp));
     // dequantised coefficients (3 k x n, into the encode's coefficient
     // buffer) and U~[:, :k] over the window, then a plain f64 GEMM
@@ -646,7 +757,11 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
     DMCG_TRY(launch_mean_shift(s, n, F, F_all, f0, p->d_rm_x, p->d_means, p->d_colsum, sh));
     shift = sh;
   }
-  DMCG_TRY(launch_output_rm(s, n, F, F_all, f0, p->d_rm_x, out, f32, shift));
+  if (p->nb > 1)  // strip the padding (codec.cpp:549)
+    DMCG_TRY(launch_output_rm(s, n, F, (int)p->F_in, 0, p->d_rm_x, out, f32, nullptr,
+                              (int)p->F_in));
+  else
+    DMCG_TRY(launch_output_rm(s, n, F, F_all, f0, p->d_rm_x, out, f32, shift));
   DMCG_TRY(record_event(p->ev[4], s));
   return Status::ok();
 }
@@ -658,6 +773,11 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   const int refine = opt ? opt->refine : 1;
   const bool factor = !(opt && opt->reuse_factor && p->factor_valid);
   uint32_t f0 = opt ? opt->frame_begin : 0, Fw = opt ? opt->frame_count : 0;
+  if (p->nb > 1) {  // blocks: one stacked solve over all padded frames
+    if (f0 != 0 || (Fw != 0 && Fw != p->F_in))
+      return Status{DMCG_E_UNSUPPORTED, "Unsupported: frame windows of a blocks stream"};
+    Fw = 0;
+  }
   if (Fw == 0) {
     f0 = 0;
     Fw = p->F;
@@ -705,6 +825,9 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
 }
 
 Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]) {
+  if (opt && opt->solver != 0 && p->nb > 1)
+    return Status{DMCG_E_UNSUPPORTED,
+                  "Unsupported: the CG solver serves the n_b = 1 anchored variants only"};
   if (opt && opt->solver != 0 && !variant_uses_anchors(p->variant))
     return Status{DMCG_E_UNSUPPORTED,
                   "Unsupported: the CG solver serves the anchored variants only (pca_qp, pca_qs)"};

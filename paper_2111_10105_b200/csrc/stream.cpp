@@ -140,8 +140,10 @@ size_t dmcg::serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, d
   w.u8(0);   // flags
   w.u32(e->n);
   w.u32(e->F);
-  w.u16(1);  // n_b
-  w.u16(0);  // pad
+  const uint32_t nb = e->n_b > 1 ? e->n_b : 1, pad = nb > 1 ? e->pad : 0;
+  const uint32_t kf = (e->F + pad) / nb;
+  w.u16((uint16_t)nb);
+  w.u16((uint16_t)pad);
   w.u32(e->k_l);
   w.u32(e->n_c);
   w.u8(e->anchor_bits);
@@ -152,7 +154,8 @@ size_t dmcg::serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, d
   w.u32(e->n_faces);
   for (size_t t = 0; t < 3 * (size_t)e->n_faces; ++t) w.u32(e->faces[t]);
   sz.connectivity = w.pos - sz.header;
-  const size_t FF = (size_t)e->F * e->F;
+  const size_t FF = (size_t)kf * kf;
+  if (spans && nb > 1) return 0;  // device packing serves n_b = 1 streams only
   for (int a = 0; a < 3; ++a) {
     size_t start = w.pos;
     if (spans) {
@@ -164,31 +167,49 @@ size_t dmcg::serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, d
       b.flush();
     }
     sz.dict_payload += w.pos - start;
-    start = w.pos;
-    for (uint32_t r = 0; r < e->k_l; ++r) {
-      w.f32(e->row_min[a][r]);
-      w.f32(e->row_max[a][r]);
-      w.u8(e->row_bits[a][r]);
-    }
-    sz.coeff_headers += w.pos - start;
-    start = w.pos;
-    if (spans) {
-      spans->coeff[a] = w.pos;
-      size_t bits = 0;
-      for (uint32_t r = 0; r < e->k_l; ++r)
-        if (e->row_min[a][r] != e->row_max[a][r]) bits += (size_t)e->n * e->row_bits[a][r];
-      skip(w, (bits + 7) / 8);
-    } else {
+    for (uint32_t blk = 1; blk < nb; ++blk) {  // dict_diffs (stream.cpp:218-227)
+      start = w.pos;
+      w.f32(e->diff_min[a][blk - 1]);
+      w.f32(e->diff_max[a][blk - 1]);
+      sz.dict_ranges += w.pos - start;
+      start = w.pos;
       BitOut b(w);
-      for (uint32_t r = 0; r < e->k_l; ++r) {
-        if (e->row_min[a][r] == e->row_max[a][r]) continue;  // no payload (stream.cpp:114)
-        const uint16_t* q = e->coeff_q[a] + (size_t)r * e->n;
-        const int bits = e->row_bits[a][r];
-        for (uint32_t i = 0; i < e->n; ++i) b.put(q[i], bits);
-      }
+      for (size_t t = 0; t < FF; ++t) b.put(e->dict_q[a][blk * FF + t], e->diff_bits);
       b.flush();
+      sz.dict_payload += w.pos - start;
     }
-    sz.coeff_payload += w.pos - start;
+    for (uint32_t blk = 0; blk < nb; ++blk) {  // one CoeffBlock per block (stream.cpp:229-251)
+      const size_t ro = (size_t)blk * e->k_l;
+      const float* row_min = e->row_min[a] + ro;
+      const float* row_max = e->row_max[a] + ro;
+      const uint8_t* row_bits = e->row_bits[a] + ro;
+      const uint16_t* coeff_q = e->coeff_q[a] + ro * e->n;
+      start = w.pos;
+      for (uint32_t r = 0; r < e->k_l; ++r) {
+        w.f32(row_min[r]);
+        w.f32(row_max[r]);
+        w.u8(row_bits[r]);
+      }
+      sz.coeff_headers += w.pos - start;
+      start = w.pos;
+      if (spans) {
+        spans->coeff[a] = w.pos;
+        size_t bits = 0;
+        for (uint32_t r = 0; r < e->k_l; ++r)
+          if (row_min[r] != row_max[r]) bits += (size_t)e->n * row_bits[r];
+        skip(w, (bits + 7) / 8);
+      } else {
+        BitOut b(w);
+        for (uint32_t r = 0; r < e->k_l; ++r) {
+          if (row_min[r] == row_max[r]) continue;  // no payload (stream.cpp:114)
+          const uint16_t* q = coeff_q + (size_t)r * e->n;
+          const int bits = row_bits[r];
+          for (uint32_t i = 0; i < e->n; ++i) b.put(q[i], bits);
+        }
+        b.flush();
+      }
+      sz.coeff_payload += w.pos - start;
+    }  // blocks
     if (variant_uses_means(e->variant)) {  // stream.cpp:255-263
       start = w.pos;
       for (uint32_t f = 0; f < e->F; ++f) w.f32(e->means[a][f]);
@@ -276,11 +297,13 @@ static int parse_header_impl(ByteIn& r, dmcg_encoded* c, std::string* msg) {
   }
   if (!(db >= 1 && db <= 16)) return corrupt("dictionary bit depth outside 1..16");
   if (!(fb >= 1 && fb <= 16)) return corrupt("difference bit depth outside 1..16");
-  if (variant > DMCG_PCA_QP || n_b != 1 || flags != 0) {
-    *msg = "Unsupported: only the n_b = 1 variants pca, pca_q, v2v, pca_qs, pca_qp with "
+  if (variant > DMCG_BLOCKS || flags != 0 || (n_b == 1 && pad != 0)) {
+    *msg = "Unsupported: only the variants pca, pca_q, v2v, pca_qs, pca_qp, blocks with "
            "quantised payloads are on the B200 path";
     return DMCG_E_UNSUPPORTED;
   }
+  c->n_b = n_b;
+  c->pad = pad;
   c->n = n;
   c->F = k;
   c->k_l = k_l;
@@ -317,7 +340,8 @@ int dmcg_parse(const uint8_t* data, size_t size, dmcg_encoded* c, dmcg_sections*
     return DMCG_E_CORRUPT;
   };
   if (hdr.n != c->n || hdr.F != c->F || hdr.k_l != c->k_l || hdr.n_c != c->n_c ||
-      hdr.n_faces != c->n_faces)
+      hdr.n_faces != c->n_faces || hdr.n_b != (c->n_b ? c->n_b : 1) ||
+      (hdr.n_b > 1 && hdr.pad != c->pad))
     return corrupt("buffers sized for a different header");
   *c = hdr;
   sz.header = 32;
@@ -333,7 +357,8 @@ int dmcg_parse(const uint8_t* data, size_t size, dmcg_encoded* c, dmcg_sections*
     if (f[0] == f[1] || f[1] == f[2] || f[0] == f[2]) return corrupt("degenerate face");
   }
   sz.connectivity = r.pos - sz.header;
-  const size_t FF = (size_t)c->F * c->F;
+  const uint32_t nb = c->n_b, kf = (c->F + c->pad) / nb;
+  const size_t FF = (size_t)kf * kf;
   for (int a = 0; a < 3; ++a) {
     size_t start = r.pos;
     const size_t db = packed_bytes(FF, c->dict_bits);
@@ -341,45 +366,66 @@ int dmcg_parse(const uint8_t* data, size_t size, dmcg_encoded* c, dmcg_sections*
     if (!p) return corrupt(r.err);
     unpack(p, FF, c->dict_bits, c->dict_q[a]);
     sz.dict_payload += r.pos - start;
-    start = r.pos;
-    size_t bits_total = 0;
-    for (uint32_t q = 0; q < c->k_l; ++q) {
-      c->row_min[a][q] = r.f32();
-      c->row_max[a][q] = r.f32();
-      c->row_bits[a][q] = r.u8();
+    for (uint32_t blk = 1; blk < nb; ++blk) {  // dict_diffs (stream.cpp:370-385)
+      start = r.pos;
+      const float mn = r.f32(), mx = r.f32();
       if (!r.err.empty()) return corrupt(r.err);
-      if (c->row_bits[a][q] < 1 || c->row_bits[a][q] > 16)
-        return corrupt("row bit depth outside 1..16");
-      if (!(c->row_min[a][q] <= c->row_max[a][q])) return corrupt("row range has min > max");
-      if (!(c->row_min[a][q] == c->row_max[a][q])) bits_total += (size_t)c->row_bits[a][q] * c->n;
+      if (!(mn <= mx)) return corrupt("difference range has min > max");
+      c->diff_min[a][blk - 1] = mn;
+      c->diff_max[a][blk - 1] = mx;
+      sz.dict_ranges += r.pos - start;
+      start = r.pos;
+      const uint8_t* pd = r.slice(packed_bytes(FF, c->diff_bits));
+      if (!pd) return corrupt(r.err);
+      unpack(pd, FF, c->diff_bits, c->dict_q[a] + blk * FF);
+      sz.dict_payload += r.pos - start;
     }
-    sz.coeff_headers += r.pos - start;
-    start = r.pos;
-    const size_t pb = (bits_total + 7) / 8;
-    const uint8_t* pp = r.slice(pb);
-    if (!pp) return corrupt(r.err);
-    // rows are contiguous in the bit stream: unpack sequentially
-    uint64_t acc = 0;
-    int fill = 0;
-    size_t pos = 0;
-    for (uint32_t q = 0; q < c->k_l; ++q) {
-      uint16_t* o = c->coeff_q[a] + (size_t)q * c->n;
-      if (c->row_min[a][q] == c->row_max[a][q]) {
-        std::memset(o, 0, (size_t)c->n * 2);
-        continue;
+    for (uint32_t blk = 0; blk < nb; ++blk) {  // coeffs, one CoeffBlock per block
+      const size_t ro = (size_t)blk * c->k_l;
+      float* row_min = c->row_min[a] + ro;
+      float* row_max = c->row_max[a] + ro;
+      uint8_t* row_bits = c->row_bits[a] + ro;
+      uint16_t* coeff_q = c->coeff_q[a] + ro * c->n;
+      start = r.pos;
+      size_t bits_total = 0;
+      for (uint32_t q = 0; q < c->k_l; ++q) {
+        row_min[q] = r.f32();
+        row_max[q] = r.f32();
+        row_bits[q] = r.u8();
+        if (!r.err.empty()) return corrupt(r.err);
+        if (row_bits[q] < 1 || row_bits[q] > 16)
+          return corrupt("row bit depth outside 1..16");
+        if (!(row_min[q] <= row_max[q])) return corrupt("row range has min > max");
+        if (!(row_min[q] == row_max[q])) bits_total += (size_t)row_bits[q] * c->n;
       }
-      const int bits = c->row_bits[a][q];
-      const uint32_t mask = (1u << bits) - 1u;
-      for (uint32_t i = 0; i < c->n; ++i) {
-        while (fill < bits) {
-          acc = (acc << 8) | pp[pos++];
-          fill += 8;
+      sz.coeff_headers += r.pos - start;
+      start = r.pos;
+      const size_t pb = (bits_total + 7) / 8;
+      const uint8_t* pp = r.slice(pb);
+      if (!pp) return corrupt(r.err);
+      // rows are contiguous in the bit stream: unpack sequentially
+      uint64_t acc = 0;
+      int fill = 0;
+      size_t pos = 0;
+      for (uint32_t q = 0; q < c->k_l; ++q) {
+        uint16_t* o = coeff_q + (size_t)q * c->n;
+        if (row_min[q] == row_max[q]) {
+          std::memset(o, 0, (size_t)c->n * 2);
+          continue;
         }
-        fill -= bits;
-        o[i] = (uint16_t)((acc >> fill) & mask);
+        const int bits = row_bits[q];
+        const uint32_t mask = (1u << bits) - 1u;
+        for (uint32_t i = 0; i < c->n; ++i) {
+          while (fill < bits) {
+            acc = (acc << 8) | pp[pos++];
+            fill += 8;
+          }
+          fill -= bits;
+          o[i] = (uint16_t)((acc >> fill) & mask);
+        }
       }
-    }
-    sz.coeff_payload += r.pos - start;
+      sz.coeff_payload += r.pos - start;
+    }  // blocks
     if (dmcg::variant_uses_means(c->variant)) {
       start = r.pos;
       for (uint32_t f = 0; f < c->F; ++f) {

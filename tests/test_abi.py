@@ -139,10 +139,9 @@ def test_parse_strictness():  # stream.cpp:294-469, SPEC.md:527 (acceptance 7)
 
 def test_parse_rejects_other_variants():
     data = bytearray(G["stream"].tobytes())
-    data[6] = 5  # blocks: valid in the reference, outside the B200 path
-    with pytest.raises(C.DmcError) as e:
-        C.parse(bytes(data))
-    assert e.value.code == 11
+    data[6] = 5  # blocks with n_b = 1: pca_qp's layout (codec.cpp:158-159)
+    c = C.parse(bytes(data))
+    assert c.variant == 5 and c.n_b == 1 and C.serialize(c)[0] == bytes(data)
     data[6] = 6  # per_mesh_gft: anchor-free, so these header bytes are corrupt for it
     with pytest.raises(C.DmcError) as e:
         C.parse(bytes(data))

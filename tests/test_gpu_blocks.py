@@ -1,0 +1,193 @@
+"""GPU parity of the blocks variant (n_b > 1) through the
+C ABI against the CPU oracle (orc_encode_blocks / orc_decode).
+
+Contract, on the same seeded inputs:
+  B1  anchor indices, levels and ranges; header; section sizes: bit-exact
+  B2  per-block dictionaries: columns determined by the data (eigen-gap
+      columns of blocks that fell back to the eigenbasis, chained through the
+      sign alignment; every column of warm-started OI blocks on full-rank
+      data) within 1e-9; their first-block levels bit-exact (+-1 at exact
+      bin ties); on full-rank data the difference ranges equal and the
+      difference levels within +-1 on <= 1e-3 of the entries
+  B3  coefficient rows of determined columns: (min, max) equal, symbols +-1
+      on <= 1e-4 n entries
+  B4  the GPU stream decoded on the GPU vs the oracle: <= 1e-8 bbox; end to
+      end |RMSE_gpu / RMSE_cpu - 1| <= 1e-3
+"""
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_2111_10105_b200 import codec as C
+from paper_2111_10105_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+class _Seq:
+    def __init__(self, faces, axes):
+        self.faces = np.asarray(faces, np.uint32)
+        self.axes = [np.ascontiguousarray(a, np.float64) for a in axes]
+        self.n, self.F = self.axes[0].shape
+
+
+def _noisy(level, F, seed):
+    s = synth.sphere(level, F, 3, 0, seed=seed)
+    rng = np.random.default_rng(seed)
+    return _Seq(s.faces, [a + 0.05 * rng.standard_normal(a.shape) for a in s.axes])
+
+
+def _block_evals(X, n_b):
+    n, F = X.shape
+    pad = (n_b - F % n_b) % n_b
+    Xp = np.concatenate([X, np.repeat(X[:, -1:], pad, axis=1)], axis=1)
+    kf = (F + pad) // n_b
+    return [np.linalg.eigvalsh(Xp[:, b * kf:(b + 1) * kf].T @ Xp[:, b * kf:(b + 1) * kf])[::-1]
+            for b in range(n_b)]
+
+
+def _gap_columns(ev, k):
+    cols = set()
+    for j in range(k):
+        if ev[j] < 1e-6 * ev[0]:
+            break
+        lo = ev[j + 1] if j + 1 < len(ev) else 0.0
+        hi_gap = (ev[j - 1] - ev[j]) / ev[j - 1] if j > 0 else 1.0
+        if (ev[j] - lo) / ev[j] >= 1e-3 and hi_gap >= 1e-3:
+            cols.add(j)
+    return cols
+
+
+def _oracle_stream_of(g, faces):
+    og = O.Encoded(g.n, g.F, g.k_l, g.n_c, faces, g.anchor_bits, g.dict_bits, 5, g.n_b,
+                   g.diff_bits)
+    for a in range(3):
+        og.dict_q[a][:] = g.dict_q[a]
+        og.diff_min[a][:] = g.diff_min[a]
+        og.diff_max[a][:] = g.diff_max[a]
+        og.row_min[a][:] = g.row_min[a]
+        og.row_max[a][:] = g.row_max[a]
+        og.row_bits[a][:] = g.row_bits[a]
+        og.coeff_q[a][:] = g.coeff_q[a]
+        og.anchor_q[a][:] = g.anchor_q[a]
+        og.s.anchor_min[a] = g.anchor_min[a]
+        og.s.anchor_max[a] = g.anchor_max[a]
+    og.anchor_idx[:] = g.anchor_idx
+    return og
+
+
+def check_blocks_parity(codec, s, n_b, k_l, bits, full_rank, diff_bits=8, t_max=4):
+    cfg = C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=n_b, k_l=k_l, row_bits=[bits] * k_l,
+                          t_max=t_max, diff_bits=diff_bits)
+    g = codec.encode(s, cfg)
+    o = O.encode_blocks(s, n_b, k_l, bits, t_max=t_max, diff_bits=diff_bits, nthreads=8)
+    n, kf = s.n, o.kf
+    assert (g.n_b, g.pad, g.k_f) == (n_b, o.s.pad, kf)
+    # B1
+    assert np.array_equal(g.anchor_idx, o.anchor_idx[:o.s.n_c])
+    for a in range(3):
+        assert np.array_equal(g.anchor_q[a], o.anchor_q[a])
+        assert g.anchor_min[a] == o.s.anchor_min[a] and g.anchor_max[a] == o.s.anchor_max[a]
+    gb, gsec = C.serialize(g)
+    ob, osec = O.serialize(o)
+    assert gsec == osec and len(gb) == len(ob)
+    # B2 / B3 through a device plan (its dictionaries before quantisation)
+    import torch
+    plan = C.Plan(codec, s.n, s.F, s.faces, cfg)
+    d = [torch.from_numpy(x).cuda() for x in s.axes]
+    plan.encode_device([t.data_ptr() for t in d])
+    pg = plan.download()
+    for a in range(3):
+        np.testing.assert_array_equal(pg.coeff_q[a], g.coeff_q[a])  # plan == drop-in
+        Ug, _ = plan.basis(a)
+        evs = _block_evals(s.axes[a], n_b)
+        det = set(range(kf)) if full_rank else _gap_columns(evs[0], kf)
+        for b in range(n_b):
+            if b and not full_rank:
+                det &= _gap_columns(evs[b], kf)  # the sign chain needs every block's column
+            Uo = o.U[a][b]
+            for j in sorted(det):
+                assert np.abs(Ug[b][:, j] - Uo[:, j]).max() <= 1e-9, (a, b, j)
+                r = b * k_l + j
+                if j < k_l:
+                    assert g.row_min[a][r] == o.row_min[a][r] and \
+                        g.row_max[a][r] == o.row_max[a][r], (a, b, j)
+                    dq = g.coeff_q[a][r].astype(np.int64) - o.coeff_q[a][r].astype(np.int64)
+                    assert np.abs(dq).max() <= 1 and np.count_nonzero(dq) <= max(1, 1e-4 * n)
+            if b == 0:
+                for j in det:
+                    dl = g.dict_q[a][0][j].astype(np.int64) - o.dict_q[a][0][j].astype(np.int64)
+                    assert np.abs(dl).max() <= 1 and np.count_nonzero(dl) <= 2, (a, j)
+            elif full_rank:
+                assert g.diff_min[a][b - 1] == o.diff_min[a][b - 1]
+                assert g.diff_max[a][b - 1] == o.diff_max[a][b - 1]
+                dl = g.dict_q[a][b].astype(np.int64) - o.dict_q[a][b].astype(np.int64)
+                assert np.abs(dl).max() <= 1 and np.count_nonzero(dl) <= max(2, 1e-3 * kf * kf)
+    # GPU-side serialize of a blocks plan = host serialize of its symbols
+    assert plan.serialize()[0] == C.serialize(pg)[0]
+    plan.close()
+    # B4 same stream
+    xg = codec.decode(g)
+    xo = O.decode(_oracle_stream_of(g, s.faces), nthreads=8)
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
+    for a in range(3):
+        assert xg[a].shape == (s.n, s.F)
+        assert np.abs(xg[a] - xo[a]).max() <= 1e-8 * bbox, a
+    r_g = O.frame_rms(s.axes, xg)
+    r_o = O.frame_rms(s.axes, O.decode(o, nthreads=8))
+    assert abs(r_g.mean() / r_o.mean() - 1) <= 1e-3
+    return g, o
+
+
+@pytest.mark.parametrize("n_b", [2, 4])
+def test_blocks_parity_full_rank_oi(codec, n_b):
+    """Warm-started orthogonal iterations run to t_max on every block."""
+    check_blocks_parity(codec, _noisy(2, 24, 7), n_b, 4, 12, full_rank=True)
+
+
+def test_blocks_parity_padding(codec):
+    """F = 26, n_b = 4: pad 2 (< k_f = 7), the last frame repeated and stripped."""
+    check_blocks_parity(codec, _noisy(2, 26, 3), 4, 5, 12, full_rank=True, diff_bits=10)
+
+
+@pytest.mark.parametrize("name,n_b,k_l", [("c0", 4, 12), ("c0", 3, 12), ("c1", 4, 32)])
+def test_blocks_parity_configs(codec, name, n_b, k_l):
+    """BASELINE configs 0 / 1 in block mode: low-rank trajectories, so the
+    later blocks fall back to their own eigenbasis (RankDeficiency)."""
+    spec = synth.CONFIGS[name]
+    check_blocks_parity(codec, spec.make(), n_b, k_l, spec.bits, full_rank=False)
+
+
+def test_blocks_oi_tolerance_stop(codec):
+    """oi_tolerance (spectral.cpp:90-97): a loose stop ends the iteration
+    after the first round; the dictionaries still match the oracle's."""
+    s = _noisy(2, 24, 11)
+    cfg = C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=3, k_l=4, row_bits=[12] * 4, t_max=6,
+                          oi_tolerance=10.0)
+    g = codec.encode(s, cfg)
+    lib = O.lib()
+    o = O.Encoded(s.n, 24, 4, O.anchor_count(s.n), s.faces, 16, 16, 5, 3, 8)
+    rb = np.full(4, 12, np.int32)
+    import ctypes
+    U = np.zeros((3, 3, 8, 8))
+    rc = lib.orc_encode_blocks(s.n, 24, (O.f64p * 3)(*[O.P(a, O.f64p) for a in s.axes]),
+                               O.P(o.faces, O.u32p), len(o.faces), 3, 4, O.P(rb, O.intp), 0.01, 16,
+                               16, 8, 6, 10.0, ctypes.byref(o.s), O.P(U, O.f64p), 8)
+    assert rc == 0
+    for a in range(3):
+        np.testing.assert_array_equal(g.coeff_q[a], o.coeff_q[a])
+
+
+def test_blocks_decode_refusals(codec):
+    spec = synth.CONFIGS["c0"]
+    s = spec.make()
+    g = codec.encode(s, C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=4, k_l=8, row_bits=[12] * 8))
+    with pytest.raises(C.DmcError) as e:
+        codec.decode(g, frames=(0, 8))
+    assert e.value.code == 11
+    with pytest.raises(C.DmcError) as e:
+        codec.decode(g, solver="cg")
+    assert e.value.code == 11
+    with pytest.raises(C.DmcError) as e:  # k_l > k_f = 16
+        codec.encode(s, C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=4, k_l=17))
+    assert e.value.code == 5
