@@ -305,9 +305,12 @@ def test_errors(codec):
     with pytest.raises(C.DmcError) as e:
         codec.encode(s, C.EncoderConfig(k_l=4, anchor_bits=17))
     assert e.value.code == 5
-    with pytest.raises(C.DmcError) as e:  # blocks (n_b > 1): outside the B200 path
-        codec.encode(s, C.EncoderConfig(k_l=4, variant=5, n_b=2))
+    with pytest.raises(C.DmcError) as e:  # per_mesh_gft: outside the B200 path
+        codec.encode(s, C.EncoderConfig(k_l=4, variant=6))
     assert e.value.code == 11
+    with pytest.raises(C.DmcError) as e:  # n_b > 1 needs the blocks variant (codec.cpp:71-73)
+        codec.encode(s, C.EncoderConfig(k_l=4, n_b=2))
+    assert e.value.code == 5
     bad_v2v = [ax.copy() for ax in s.axes]  # v2v has no K1 pass: its own finiteness check
     bad_v2v[2][1, 1] = np.inf
     with pytest.raises(C.DmcError) as e:
