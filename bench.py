@@ -313,6 +313,9 @@ def main():
                     help="independent sequences in flight per GPU (one context / CUDA stream / "
                          "host thread each); default 4 for sequences of <= 4 M vertex-frames "
                          "(c0, c1, c4), else 1")
+    ap.add_argument("--n-b", type=int, default=1,
+                    help="blocks variant with this many frame blocks (SURVEY 8f f2); "
+                         "k_l = min(config k, k_f); default 1 = the pca_qp hot path")
     ap.add_argument("--rows", action="store_true",
                     help="shard one sequence by vertex rows across the ranks (SURVEY §8e)")
     args = ap.parse_args()
@@ -336,6 +339,11 @@ def main():
     spec, s = sequence_for_rank(args.config, rank)
     cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds,
                           oi_implicit=args.implicit)
+    if args.n_b > 1:  # blocks variant: n_b dictionaries of k_f frames
+        kf = (s.F + (args.n_b - s.F % args.n_b) % args.n_b) // args.n_b
+        kl = min(spec.k, kf)
+        cfg = C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=args.n_b, k_l=kl,
+                              row_bits=[spec.bits] * kl)
     f32 = spec.dtype == "f32"
     npdt = np.float32 if f32 else np.float64
     codec = C.Codec(local)
@@ -512,7 +520,9 @@ def main():
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if not f32 else "f64 (f32 storage)",
             "data": "synthetic (seeded generator, DESIGN.md §2)",
-            "config": {"workload": WORKLOADS[args.config],
+            "config": {"workload": WORKLOADS[args.config] + (
+                           f"; blocks variant n_b={args.n_b}, k_l={cfg.k_l}, t_max=4"
+                           if args.n_b > 1 else ""),
                        "per_gpu": (f"{K} independent sequences in flight per step (one context / "
                                    "CUDA stream / host thread each)") if K > 1
                        else "one sequence per step",

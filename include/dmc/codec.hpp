@@ -8,7 +8,11 @@
 //     data()/operator()) because Eigen3 is unavailable (reference
 //     CMakeLists.txt:11); the memory layout is identical, so a reference
 //     caller can pass Eigen::MatrixXd::data() buffers straight through.
-//   * CompressedAnimation holds the pca_qp / n_b = 1 fields only.
+//   * CompressedAnimation holds the quantised-payload fields of the variants
+//     pca, pca_q, v2v, pca_qs, pca_qp and blocks; the coefficient blocks of
+//     an axis are one flat row list (block b at rows [b k_l, (b+1) k_l)).
+//   * EncoderConfig::oi_tolerance is a double (< 0 = unset) instead of
+//     std::optional<double>.
 //   * EncoderConfig gains oi_rounds / oi_seed (B200 rank-k basis) and
 //     decode() takes optional CG controls.
 #pragma once
@@ -94,6 +98,7 @@ struct EncoderConfig {  // reference codec.hpp:30-49 (+ B200 basis controls)
   int oi_rounds = 0;       // 0 = full eigenbasis (reference n_b = 1 path)
   uint64_t oi_seed = 0;
   int oi_implicit = 0;
+  double oi_tolerance = -1.0;  // blocks: principal-angle stop (< 0 = unset)
 };
 
 struct QuantRow {  // stream.hpp:86-93
@@ -102,13 +107,21 @@ struct QuantRow {  // stream.hpp:86-93
   std::vector<uint32_t> q;  // empty when min == max
 };
 
-struct CompressedAnimation {  // stream.hpp:130-155, n_b = 1: pca, pca_q, v2v, pca_qs, pca_qp
+struct DictDiff {  // stream.hpp:95-101
+  float min = 0.0f, max = 0.0f;
+  std::vector<uint32_t> q;  // k_f * k_f levels at diff_bits, column-major
+};
+
+struct CompressedAnimation {  // stream.hpp:130-155, quantised payloads of variants 0-5
   Variant variant = Variant::PcaQp;
   uint32_t n = 0, k = 0, k_l = 0, n_c = 0;
+  uint16_t n_b = 1, pad = 0;
   uint8_t anchor_bits = 16, dict_bits = 16, diff_bits = 8;
   std::vector<Face> faces;
-  std::array<std::vector<uint32_t>, 3> dict_first;   // k*k levels, column-major
-  std::array<std::vector<QuantRow>, 3> coeffs;       // k_l rows per axis
+  std::array<std::vector<uint32_t>, 3> dict_first;   // k_f*k_f levels, column-major
+  std::array<std::vector<DictDiff>, 3> dict_diffs;   // blocks 2..n_b
+  std::array<std::vector<QuantRow>, 3> coeffs;       // n_b * k_l rows per axis
+  uint32_t k_f() const { return (k + pad) / n_b; }
   std::vector<uint32_t> anchor_indices;
   std::array<float, 3> anchor_min{}, anchor_max{};
   std::array<std::vector<uint32_t>, 3> anchor_q;     // n_c*k, anchor-major
@@ -163,6 +176,7 @@ inline CompressedAnimation encode(const MeshSequence& s, const EncoderConfig& cf
   c.oi_rounds = cfg.oi_rounds;
   c.oi_seed = cfg.oi_seed;
   c.oi_implicit = cfg.oi_implicit;
+  c.oi_tolerance = cfg.oi_tolerance;
   const uint32_t n = (uint32_t)s.n(), F = (uint32_t)s.k();
   dmcg_sizes sz;
   detail::check(dmcg_encoded_sizes(n, F, &c, &sz));
@@ -172,10 +186,15 @@ inline CompressedAnimation encode(const MeshSequence& s, const EncoderConfig& cf
   std::array<std::vector<uint16_t>, 3> dq, cq, aq;
   std::array<std::vector<float>, 3> rmin, rmax;
   std::array<std::vector<uint8_t>, 3> rbits;
+  std::array<std::vector<float>, 3> dmin, dmax;
   CompressedAnimation out;
   out.anchor_indices.resize(sz.anchor_idx);
   dmcg_encoded e{};
   for (int a = 0; a < 3; ++a) {
+    dmin[a].resize(sz.dict_ranges + 1);
+    dmax[a].resize(sz.dict_ranges + 1);
+    e.diff_min[a] = dmin[a].data();
+    e.diff_max[a] = dmax[a].data();
     out.means[a].resize(sz.means);
     e.means[a] = sz.means ? out.means[a].data() : nullptr;
     dq[a].resize(sz.dict_q);
@@ -200,18 +219,28 @@ inline CompressedAnimation encode(const MeshSequence& s, const EncoderConfig& cf
   out.n = n;
   out.k = F;
   out.k_l = cfg.k_l;
+  out.n_b = sz.n_b;
+  out.pad = sz.pad;
   out.n_c = e.n_c;
   out.anchor_bits = e.anchor_bits;
   out.dict_bits = e.dict_bits;
   out.diff_bits = e.diff_bits;
   out.faces = s.faces();
+  const size_t kk = (size_t)out.k_f() * out.k_f(), rows = (size_t)out.n_b * cfg.k_l;
   for (int a = 0; a < 3; ++a) {
-    out.dict_first[a].assign(dq[a].begin(), dq[a].end());
+    out.dict_first[a].assign(dq[a].begin(), dq[a].begin() + kk);
+    for (uint32_t b = 1; b < out.n_b; ++b) {
+      DictDiff d;
+      d.min = dmin[a][b - 1];
+      d.max = dmax[a][b - 1];
+      d.q.assign(dq[a].begin() + b * kk, dq[a].begin() + (b + 1) * kk);
+      out.dict_diffs[a].push_back(std::move(d));
+    }
     out.anchor_q[a].assign(aq[a].begin(), aq[a].end());
     out.anchor_min[a] = e.anchor_min[a];
     out.anchor_max[a] = e.anchor_max[a];
-    out.coeffs[a].resize(cfg.k_l);
-    for (uint32_t r = 0; r < cfg.k_l; ++r) {
+    out.coeffs[a].resize(rows);
+    for (uint32_t r = 0; r < rows; ++r) {
       QuantRow& row = out.coeffs[a][r];
       row.min = rmin[a][r];
       row.max = rmax[a][r];
@@ -231,11 +260,16 @@ inline MeshSequence decode(const CompressedAnimation& c, double cg_rtol = 1e-10)
   std::array<std::vector<uint16_t>, 3> dq, cq, aq;
   std::array<std::vector<float>, 3> rmin, rmax;
   std::array<std::vector<uint8_t>, 3> rbits;
+  std::array<std::vector<float>, 3> dmin, dmax;
   std::vector<uint32_t> idx(c.anchor_indices);
+  const uint32_t nb = c.n_b ? c.n_b : 1;
+  const size_t kk = (size_t)((F + c.pad) / nb) * ((F + c.pad) / nb), rows = (size_t)nb * c.k_l;
   dmcg_encoded e{};
   e.n = n;
   e.F = F;
   e.k_l = c.k_l;
+  e.n_b = (uint16_t)nb;
+  e.pad = c.pad;
   e.n_c = c.n_c;
   e.n_faces = (uint32_t)c.faces.size();
   e.variant = (uint8_t)c.variant;
@@ -245,18 +279,30 @@ inline MeshSequence decode(const CompressedAnimation& c, double cg_rtol = 1e-10)
   e.faces = faces.data();
   e.anchor_idx = idx.data();
   for (int a = 0; a < 3; ++a) {
-    if (c.dict_first[a].size() != (size_t)F * F || c.coeffs[a].size() != c.k_l ||
+    if (c.dict_first[a].size() != kk || c.dict_diffs[a].size() != nb - 1 ||
+        c.coeffs[a].size() != rows ||
         c.anchor_q[a].size() != (size_t)c.n_c * F ||
         ((c.variant == Variant::Pca || c.variant == Variant::PcaQ) && c.means[a].size() != F))
       throw Error(6, "CorruptPayload: payload has wrong element count");
     e.means[a] = c.means[a].empty() ? nullptr : const_cast<float*>(c.means[a].data());
     dq[a].assign(c.dict_first[a].begin(), c.dict_first[a].end());
+    dmin[a].resize(nb);
+    dmax[a].resize(nb);
+    for (uint32_t b = 1; b < nb; ++b) {
+      const DictDiff& d = c.dict_diffs[a][b - 1];
+      if (d.q.size() != kk) throw Error(6, "CorruptPayload: dictionary payload has wrong element count");
+      dq[a].insert(dq[a].end(), d.q.begin(), d.q.end());
+      dmin[a][b - 1] = d.min;
+      dmax[a][b - 1] = d.max;
+    }
+    e.diff_min[a] = dmin[a].data();
+    e.diff_max[a] = dmax[a].data();
     aq[a].assign(c.anchor_q[a].begin(), c.anchor_q[a].end());
-    cq[a].assign((size_t)c.k_l * n + 1, 0);
-    rmin[a].resize(c.k_l + 1);
-    rmax[a].resize(c.k_l + 1);
-    rbits[a].resize(c.k_l + 1);
-    for (uint32_t r = 0; r < c.k_l; ++r) {
+    cq[a].assign(rows * n + 1, 0);
+    rmin[a].resize(rows + 1);
+    rmax[a].resize(rows + 1);
+    rbits[a].resize(rows + 1);
+    for (uint32_t r = 0; r < rows; ++r) {
       const QuantRow& row = c.coeffs[a][r];
       rmin[a][r] = row.min;
       rmax[a][r] = row.max;

@@ -30,4 +30,6 @@ def test_dropin_roundtrip_on_gpu():
     assert out.returncode == 0, out.stdout + out.stderr
     lines = out.stdout.split("\n")
     assert lines[0].startswith("rms ") and float(lines[0].split()[1]) < 1e-3
-    assert lines[1].startswith("error 5 ConfigError")
+    blk = lines[1].split()
+    assert blk[:4] == ["blocks", "3", "1", "2"] and float(blk[5]) < 1e-3, lines[1]
+    assert lines[2].startswith("error 5 ConfigError")

@@ -37,6 +37,23 @@ int main() {
           err += d * d;
         }
     std::printf("rms %.3e\n", std::sqrt(err / (3.0 * n * F)));
+    // blocks variant: 3 blocks of k_f = 3 frames (one padded frame)
+    dmc::EncoderConfig bc;
+    bc.variant = dmc::Variant::Blocks;
+    bc.n_b = 3;
+    bc.k_l = 3;
+    bc.diff_bits = 16;
+    dmc::CompressedAnimation cb = dmc::encode(seq, bc);
+    dmc::MeshSequence ob = dmc::decode(cb);
+    double eb = 0.0;
+    for (int a = 0; a < 3; ++a)
+      for (int f = 0; f < F; ++f)
+        for (int i = 0; i < n; ++i) {
+          const double d = ob.axis(a)(f, i) - seq.axis(a)(f, i);
+          eb += d * d;
+        }
+    std::printf("blocks %u %u %zu rms %.3e\n", (unsigned)cb.n_b, (unsigned)cb.pad,
+                cb.dict_diffs[0].size(), std::sqrt(eb / (3.0 * n * F)));
     dmc::EncoderConfig bad = cfg;
     bad.k_l = F + 1;
     try {
