@@ -81,23 +81,29 @@ __device__ void qr_factor(int m, double* Z, double* tau, double* beta, double* s
       }
     }
     __syncthreads();
+    // v = x / denom is formed on the fly by the column updates (the same
+    // __ddiv_rn as the stored essential part) and written back to column j
+    // after the barrier below: one barrier per column instead of two.
     const double denom = sc[0];
-    for (int i = j + 1 + (int)threadIdx.x; i < m; i += kChainThreads)
-      x[i] = denom == 0.0 ? 0.0 : __ddiv_rn(x[i], denom);
-    __syncthreads();
-    if (threadIdx.x == 0 && denom != 0.0) x[j] = beta[j];
     const double tj = tau[j];
     if (tj != 0.0)
       for (int c = j + 1 + w; c < m; c += kWarps) {
         double* y = Z + (long)c * m;
         double d = 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) d = __dadd_rn(d, __dmul_rn(x[i], y[i]));
+        for (int i = j + 1 + lane; i < m; i += 32)
+          d = __dadd_rn(d, __dmul_rn(__ddiv_rn(x[i], denom), y[i]));
         d = __dadd_rn(warp_sum(d), y[j]);
         d = __dmul_rn(tj, d);
         if (lane == 0) y[j] = __dsub_rn(y[j], d);
-        for (int i = j + 1 + lane; i < m; i += 32) y[i] = __dsub_rn(y[i], __dmul_rn(d, x[i]));
+        for (int i = j + 1 + lane; i < m; i += 32)
+          y[i] = __dsub_rn(y[i], __dmul_rn(d, __ddiv_rn(x[i], denom)));
       }
     __syncthreads();
+    for (int i = j + 1 + (int)threadIdx.x; i < m; i += kChainThreads)
+      x[i] = denom == 0.0 ? 0.0 : __ddiv_rn(x[i], denom);
+    if (threadIdx.x == 0 && denom != 0.0) x[j] = beta[j];
+    // (column j is not read again in this factorisation: the next step's
+    // warp-0 reduction reads column j + 1, after the barrier at its end)
   }
 }
 
@@ -159,22 +165,28 @@ __device__ void canon_columns(int m, double* U) {
 
 __global__ void __launch_bounds__(kChainThreads)
     k_block_chain(int nb, int kf, int t_max, double tol, const double* __restrict__ R,
-                  const double* __restrict__ Ueig, double* U, double* work, int* flags) {
+                  const double* __restrict__ Ueig, double* U, double* work, int* flags,
+                  int use_smem) {
   __shared__ double tau[512], beta[512], red[kWarps], sc[2];
   __shared__ int s_def;
+  extern __shared__ double dsm[];  // use_smem: Z, N and the working dictionary
   const int a = blockIdx.x, m = kf, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const long kk = (long)m * m;
   const double* Ra = R + (long)a * nb * kk;
   const double* Ea = Ueig + (long)a * nb * kk;
   double* Ua = U + (long)a * nb * kk;
-  double* Z = work + (long)a * 2 * kk;
-  double* N = Z + kk;
+  // Every QR phase reads what other warps wrote in the previous one: with
+  // the k_f x k_f operands in shared memory (k_f <= 93) those round trips
+  // cost ~30 cycles instead of an L2 round trip.
+  double* Z = use_smem ? dsm : work + (long)a * 2 * kk;
+  double* N = use_smem ? dsm + kk : Z + kk;
   for (long e = threadIdx.x; e < kk; e += kChainThreads) Ua[e] = Ea[e];  // full_eigenbasis
   __syncthreads();
   for (int b = 1; b < nb; ++b) {
     const double* Rb = Ra + b * kk;
     const double* prev = Ua + (b - 1) * kk;
-    double* cur = Ua + b * kk;
+    double* const out = Ua + b * kk;
+    double* cur = use_smem ? dsm + 2 * kk : out;
     for (long e = threadIdx.x; e < kk; e += kChainThreads) cur[e] = prev[e];
     if (threadIdx.x == 0) s_def = 0;
     __syncthreads();
@@ -229,6 +241,10 @@ __global__ void __launch_bounds__(kChainThreads)
         for (int i = lane; i < m; i += 32) cur[(long)c * m + i] = -cur[(long)c * m + i];
     }
     __syncthreads();
+    if (use_smem) {
+      for (long e = threadIdx.x; e < kk; e += kChainThreads) out[e] = cur[e];
+      __syncthreads();
+    }
   }
 }
 
@@ -349,7 +365,15 @@ cudaError_t launch_block_chain(cudaStream_t s, int nb, int kf, int t_max, double
                                const double* R, const double* Ueig, double* U, double* work,
                                int* flags) {
   if (kf > 512) return cudaErrorInvalidValue;
-  k_block_chain<<<3, kChainThreads, 0, s>>>(nb, kf, t_max, tol, R, Ueig, U, work, flags);
+  const size_t smem = 3 * (size_t)kf * kf * sizeof(double);
+  const bool use_smem = smem <= 200 * 1024;
+  if (use_smem) {
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_block_chain,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_block_chain<<<3, kChainThreads, use_smem ? smem : 0, s>>>(nb, kf, t_max, tol, R, Ueig, U, work,
+                                                              flags, use_smem ? 1 : 0);
   return cudaGetLastError();
 }
 
