@@ -31,7 +31,8 @@ pytestmark = pytest.mark.gpu
 class _Seq:
     def __init__(self, faces, axes):
         self.faces = np.asarray(faces, np.uint32)
-        self.axes = [np.ascontiguousarray(a, np.float64) for a in axes]
+        self.axes = [np.ascontiguousarray(a) if a.dtype == np.float32 else
+                     np.ascontiguousarray(a, np.float64) for a in axes]
         self.n, self.F = self.axes[0].shape
 
 
@@ -201,3 +202,29 @@ def test_blocks_decode_refusals(codec):
     with pytest.raises(C.DmcError) as e:  # k_l > k_f = 16
         codec.encode(s, C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=4, k_l=17))
     assert e.value.code == 5
+
+
+def test_blocks_f32_input(codec):
+    """f32 trajectories (the plan's f32 path: padded f32 copy, f32 Gram /
+    projection operands upcast to f64) against the oracle on the same
+    f32-rounded values."""
+    s64 = _noisy(2, 26, 13)
+    s32 = _Seq(s64.faces, [a.astype(np.float32) for a in s64.axes])
+    ref = _Seq(s64.faces, [a.astype(np.float32).astype(np.float64) for a in s64.axes])
+    cfg = C.EncoderConfig(variant=C.L.DMCG_BLOCKS, n_b=4, k_l=5, row_bits=[12] * 5)
+    g = codec.encode(s32, cfg)
+    o = O.encode_blocks(ref, 4, 5, 12, nthreads=8)
+    assert g.pad == o.s.pad == 2
+    for a in range(3):
+        assert np.array_equal(g.anchor_q[a], o.anchor_q[a])
+        dq = g.coeff_q[a].astype(np.int64) - o.coeff_q[a].astype(np.int64)
+        assert np.abs(dq).max() <= 1 and np.count_nonzero(dq) <= max(1, 1e-4 * dq.size)
+        # blocks 1, 2 (full rank, warm-started OI); block 3 holds the two padded
+        # copies of the last frame: rank 5 of 7, its null-space columns are free
+        assert np.array_equal(g.diff_min[a][:2], o.diff_min[a][:2])
+        assert np.array_equal(g.diff_max[a][:2], o.diff_max[a][:2])
+    xg = codec.decode(g)
+    xo = O.decode(_oracle_stream_of(g, s64.faces), nthreads=8)
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in ref.axes]))
+    for a in range(3):
+        assert np.abs(xg[a] - xo[a]).max() <= 1e-8 * bbox
