@@ -213,6 +213,14 @@ void dmcg_rate_exact(const dmcg_sections* s, uint32_t n, uint32_t F, double out[
 
 /* ---- host helpers mirroring reference free functions -------------------- */
 uint32_t dmcg_anchor_count(uint32_t n, double fraction);               /* codec.cpp:199 */
+/* build_connectivity (include/dmc/mesh.hpp:69, src/mesh.cpp:60-86): the sorted,
+ * deduplicated one-ring of every vertex as CSR (row_ptr n + 1 entries, col cap
+ * entries; cap >= 6 * n_faces always suffices; *nnz = neighbour count).
+ * IndexOutOfRange / DegenerateFace / empty face list -> code 4, message in
+ * dmcg_host_error(). */
+int dmcg_build_connectivity(const uint32_t* faces, uint32_t n_faces, uint32_t n, uint32_t* row_ptr,
+                            uint32_t* col, size_t cap, size_t* nnz);
+const char* dmcg_host_error(void);
 int dmcg_select_anchors(uint32_t n, uint32_t n_c, int strategy, uint64_t seed,
                         uint32_t* out);                                 /* codec.cpp:204 */
 

@@ -6,6 +6,7 @@
 // (oracle/dmc_oracle.c: householder_factor, orc_jacobi_eig, orc_basis);
 // reductions run in parallel order and use FMA, so results agree with the
 // oracle to rounding, not bit for bit (P3).
+#include <mutex>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -1789,13 +1790,15 @@ size_t qr_scratch_doubles(int F, int k) { return qr_scratch(F > k ? F : k, k); }
 
 // Dynamic shared memory left for `fn` next to its static shared memory.
 static size_t smem_room(const void* fn) {
-  static int optin = -1;
-  if (optin < 0) {
-    int dev = 0;
+  // initialised once, thread-safe (magic static): contexts on several host
+  // threads call the launchers concurrently
+  static const int optin = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
-      optin = 227 * 1024;
-  }
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      v = 227 * 1024;
+    return v;
+  }();
   cudaFuncAttributes fa{};
   if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return 0;
   return (size_t)optin > fa.sharedSizeBytes + 256 ? optin - fa.sharedSizeBytes - 256 : 0;
@@ -1803,15 +1806,14 @@ static size_t smem_room(const void* fn) {
 
 cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
                           double* V, double* w, int* flags) {
-  static bool rel_set = false;
-  if (!rel_set) {
-    rel_set = true;
+  static std::once_flag rel_once;
+  std::call_once(rel_once, [] {
     if (const char* e = getenv("DMCG_JAC_REL")) {
       const double r = atof(e), r2 = r * r;
       cudaMemcpyToSymbol(c_jac_rel, &r, sizeof(r));
       cudaMemcpyToSymbol(c_jac_rel2, &r2, sizeof(r2));
     }
-  }
+  });
   if (m > 512) return cudaErrorInvalidValue;
   const int m2 = m + (m & 1);
   const size_t abytes = (size_t)m2 * (m2 + 1) * sizeof(double);

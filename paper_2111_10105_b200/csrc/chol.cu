@@ -11,6 +11,7 @@
 // are grouped DMMA GEMMs per level over (front, 64-row tile, 64-column tile).
 // Reference semantics: SimplicialLDLT factor + solve + one refinement pass
 // (src/solver.cpp:43-58, 82-90); the refinement is done by the caller.
+#include <atomic>
 #include <cfloat>
 
 #include "chol_dev.h"
@@ -609,14 +610,15 @@ struct LevelTimer {
 cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevels& lv) {
   const int nb = 32;
   {
-    static unsigned long long attr_set = 0;  // one bit per device
+    static std::atomic<unsigned long long> attr_set{0};  // one bit per device
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(attr_set & (1ull << dev))) {
+    if (!(attr_set.load() & (1ull << dev))) {
+      // idempotent: two threads racing here both set the same attribute
       cudaError_t e = cudaFuncSetAttribute(k_inv_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kInvDiagSmem);
       if (e != cudaSuccess) return e;
-      attr_set |= 1ull << dev;
+      attr_set.fetch_or(1ull << dev);
     }
   }
   cudaError_t e = cudaMemsetAsync(d.Linv, 0, d.linv_doubles * sizeof(double), s);

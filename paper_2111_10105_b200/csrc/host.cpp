@@ -585,9 +585,10 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   }
   p->t_max = cfg->t_max;
   p->oi_tol = cfg->oi_tolerance;
-  if (cfg->variant == DMCG_BLOCKS) p->rounds = 0;  // block 0: full_eigenbasis (codec.cpp:159)
   p->variant = cfg->variant;
-  p->rounds = cfg->oi_rounds;
+  // blocks: block 0 is always the full eigenbasis (codec.cpp:159); oi_rounds
+  // only applies to the n_b = 1 rank-k path
+  p->rounds = cfg->variant == DMCG_BLOCKS ? 0 : cfg->oi_rounds;
   p->oi_seed = cfg->oi_seed;
   p->implicit = cfg->oi_implicit != 0;
   p->anchor_bits = cfg->anchor_bits;
@@ -1022,8 +1023,9 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
                                 F * 2, Fo * 2, p->n_c, cudaMemcpyDeviceToHost, s));
     if (p->nb > 1) {
       std::vector<float> rng2(2 * (p->nb - 1));
-      CUDA_OK(cudaMemcpy(rng2.data(), p->d_diff_rng + a * rng2.size(), rng2.size() * 4,
-                         cudaMemcpyDeviceToHost));
+      // pageable destination: returns once the copy (ordered on the plan stream) is done
+      CUDA_OK(cudaMemcpyAsync(rng2.data(), p->d_diff_rng + a * rng2.size(), rng2.size() * 4,
+                              cudaMemcpyDeviceToHost, s));
       for (uint32_t b = 0; b + 1 < p->nb; ++b) {
         e->diff_min[a][b] = rng2[2 * b];
         e->diff_max[a][b] = rng2[2 * b + 1];
@@ -1192,7 +1194,8 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
         rng2[(a * (p->nb - 1) + b) * 2] = e->diff_min[a][b];
         rng2[(a * (p->nb - 1) + b) * 2 + 1] = e->diff_max[a][b];
       }
-    CUDA_OK(cudaMemcpy(p->d_diff_rng, rng2.data(), rng2.size() * 4, cudaMemcpyHostToDevice));
+    // pageable source: staged before return, so rng2 may go out of scope
+    CUDA_OK(cudaMemcpyAsync(p->d_diff_rng, rng2.data(), rng2.size() * 4, cudaMemcpyHostToDevice, s));
   }
   for (int a = 0; a < 3; ++a) {
     CUDA_OK(cudaMemcpyAsync(p->d_dict_q + a * FF, e->dict_q[a], FF * 2, cudaMemcpyHostToDevice, s));
@@ -1453,6 +1456,30 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   dmcg_plan_destroy(p);
   return ctx->set_error(st);
 }
+
+// build_connectivity (src/mesh.cpp:60-86): sorted, deduplicated one-ring CSR.
+// row_ptr: n + 1 entries; col: cap entries (cap >= 6 * n_faces always
+// suffices); *nnz receives the neighbour count.  Errors as build_mesh, the
+// message in dmcg_host_error().
+static thread_local std::string g_host_error;
+int dmcg_build_connectivity(const uint32_t* faces, uint32_t n_faces, uint32_t n, uint32_t* row_ptr,
+                            uint32_t* col, size_t cap, size_t* nnz) {
+  MeshHost m;
+  Status st = build_mesh(faces, n_faces, n, &m);
+  if (!st.good()) {
+    g_host_error = st.msg;
+    return st.code;
+  }
+  if (nnz) *nnz = m.adj_ci.size();
+  if (m.adj_ci.size() > cap) {
+    g_host_error = "DimensionMismatch: neighbour buffer too small";
+    return DMCG_E_CONFIG;
+  }
+  std::copy(m.adj_rp.begin(), m.adj_rp.end(), row_ptr);
+  std::copy(m.adj_ci.begin(), m.adj_ci.end(), col);
+  return 0;
+}
+const char* dmcg_host_error(void) { return g_host_error.c_str(); }
 
 }  // extern "C"
 

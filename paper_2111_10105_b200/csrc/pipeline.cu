@@ -476,7 +476,7 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
     Status st = run_graph(p, p->g_encode, key, 0, [&] { return enqueue_encode(p, x); });
     if (!st.good()) return st;
   }
-  p->oi_timed = p->rounds > 0 && k < F && k > 0;
+  p->oi_timed = p->nb == 1 && p->rounds > 0 && k < F && k > 0;
   int flags[8];
   DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
   DMCG_TRY(cudaStreamSynchronize(s));
