@@ -11,6 +11,7 @@ import pytest
 import pyoracle as O
 from paper_2111_10105_b200 import _lib as L
 from paper_2111_10105_b200 import codec as C
+from paper_2111_10105_b200 import synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = np.load(os.path.join(ROOT, "tests", "golden", "small_ico1.npz"))
@@ -181,3 +182,44 @@ def test_codec_without_gpu_fails_loudly():
     with pytest.raises(C.DmcError) as e:
         C.Codec(0)
     assert e.value.code == 10
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_build_connectivity_matches_oracle(name):
+    """dmcg_build_connectivity (build_connectivity, src/mesh.cpp:60-86): sorted,
+    deduplicated one-ring CSR identical to the oracle's; bad faces raise the
+    reference codes."""
+    import ctypes
+    s = synth.CONFIGS[name].make()
+    faces = np.ascontiguousarray(s.faces, np.uint32)
+    rp = np.zeros(s.n + 1, np.uint32)
+    col = np.zeros(6 * len(faces), np.uint32)
+    nnz = ctypes.c_size_t()
+    rc = L.lib().dmcg_build_connectivity(faces.ctypes.data_as(L.u32p), len(faces), s.n,
+                                         rp.ctypes.data_as(L.u32p), col.ctypes.data_as(L.u32p),
+                                         len(col), ctypes.byref(nnz))
+    assert rc == 0
+    orp, ocol = O.connectivity(faces, s.n)
+    assert np.array_equal(rp, orp) and np.array_equal(col[:nnz.value], ocol)
+    bad = np.array([[0, 1, 1]], np.uint32)
+    rc = L.lib().dmcg_build_connectivity(bad.ctypes.data_as(L.u32p), 1, 3, rp.ctypes.data_as(L.u32p),
+                                         col.ctypes.data_as(L.u32p), len(col), ctypes.byref(nnz))
+    assert rc == 4 and L.lib().dmcg_host_error().decode().startswith("DegenerateFace")
+
+
+@pytest.mark.parametrize("n,n_c,seed", [(10, 3, 0), (1000, 37, 42), (9216, 92, 7),
+                                        (262144, 2621, 123456789)])
+def test_seeded_random_anchors_pinned_to_std_mt19937_64(n, n_c, seed, tmp_path):
+    """SeededRandom anchors (codec.cpp:229-237): libdmcg's Mt64 and the oracle's
+    mt64 against the real std::mt19937_64 (tests/golden/mt64_anchors.cpp,
+    compiled here), whose own 10000th output is the [rand.predef] constant."""
+    import subprocess
+    exe = str(tmp_path / "mt64_anchors")
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    subprocess.run([cxx, "-O2", "-std=c++17", os.path.join(ROOT, "tests", "golden", "mt64_anchors.cpp"),
+                    "-o", exe], check=True)
+    assert subprocess.run([exe], capture_output=True, text=True).stdout.strip() == "9981545732273789042"
+    ref = np.array(subprocess.run([exe, str(n), str(n_c), str(seed)], capture_output=True,
+                                  text=True).stdout.split(), dtype=np.uint32)
+    assert np.array_equal(C.select_anchors(n, n_c, 1, seed), ref)
+    assert np.array_equal(O.select_anchors(n, n_c, 1, seed), ref)

@@ -5,12 +5,17 @@ seeded inputs.  Tolerances:
   P3     basis columns j with lambda_j >= 1e-6 lambda_1 and relative gaps
          >= 1e-3 to both neighbours: max|u_gpu - u_cpu| <= 1e-9, and their
          16-bit dictionary levels bit-exact
-  P4     coefficient symbols on those rows: bit-exact except <= 1e-4 of a
-         row with |delta| = 1 (fp64 boundary ties); row (min, max) equal
+  P4     coefficient symbols on those rows: |delta| <= 1 and at most
+         max(1, 1e-6 x compared symbols) mismatches over all of them (fp64
+         boundary ties); row (min, max) equal.  The measured
+         counts are appended to $DMCG_PARITY_LOG (profiles/r02_parity_counts.jsonl)
   P5     same stream decoded: max|x_gpu - x_cpu| <= 1e-8 bbox (f64, CG rtol
          1e-10) / 1e-4 bbox (f32 output); end to end |RMSE_gpu/RMSE_cpu - 1| <= 1e-3
   P6     bvpv identical
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -58,12 +63,25 @@ def _oracle_stream_of(g, s):
     return og
 
 
+NTHREADS = os.cpu_count() or 1
+
+
+def _log_counts(rec):
+    path = os.environ.get("DMCG_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
 def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3, implicit=False,
-                 variant=4):
+                 variant=4, oracle=None, oracle_x=None, tag=None):
+    """Full P1-P6 contract.  oracle / oracle_x: a precomputed oracle encode of
+    the same (s, spec, rounds, variant) and its decode (c3 reuses them)."""
     rounds = spec.rounds if rounds is None else rounds
     ec = _cfg(spec, rounds, implicit, variant)
     g = codec.encode(s, ec)
-    o = O.encode(s, spec.k, spec.bits, rounds=rounds, seed=0, nthreads=8, variant=variant)
+    o = oracle if oracle is not None else \
+        O.encode(s, spec.k, spec.bits, rounds=rounds, seed=0, nthreads=NTHREADS, variant=variant)
     n, F, k = s.n, s.F, spec.k
     assert g.variant == variant and g.n_c == o.s.n_c
     # P1 / P2 (anchored variants)
@@ -86,6 +104,7 @@ def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3, impli
     # P6
     assert C.rate_exact(g) == pytest.approx(O.rate_exact(o), rel=0, abs=0)
     # P3 / P4
+    mism, compared, per_axis = 0, 0, []
     for a in range(3):
         cols = _agreeing_columns(o.evals[a], k)
         assert cols and cols[0] == 0
@@ -99,16 +118,23 @@ def check_parity(codec, s, spec, rounds=None, f32_out=False, e2e_tol=1e-3, impli
                     abs(t - round(t)) < 1e-9, (a, j, i)
             assert g.row_min[a][j] == o.row_min[a][j] and g.row_max[a][j] == o.row_max[a][j], (a, j)
             d = g.coeff_q[a][j].astype(np.int64) - o.coeff_q[a][j].astype(np.int64)
-            assert np.abs(d).max() <= 1 and np.count_nonzero(d) <= max(1, 1e-4 * n), (a, j)
+            assert np.abs(d).max() <= 1, (a, j)
+            mism += int(np.count_nonzero(d))
+            compared += n
+        per_axis.append(len(cols))
+    _log_counts({"case": tag or spec.name, "rounds": rounds, "implicit": implicit,
+                 "variant": variant, "agreeing_columns": per_axis,
+                 "symbols_compared": compared, "symbol_mismatches": mism})
+    assert mism <= max(1, 1e-6 * compared), (mism, compared)
     # P5 same stream
     xg = codec.decode(g, rtol=1e-10, dtype=np.float32 if f32_out else np.float64)
-    xo = O.decode(_oracle_stream_of(g, s), nthreads=8)
+    xo = O.decode(_oracle_stream_of(g, s), nthreads=NTHREADS)
     bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
     tol = (1e-4 if f32_out else 1e-8) * bbox
     for a in range(3):
         assert np.abs(xg[a].astype(np.float64) - xo[a]).max() <= tol
     # P5 end to end
-    xoo = O.decode(o, nthreads=8)
+    xoo = oracle_x if oracle_x is not None else O.decode(o, nthreads=NTHREADS)
     r_g = O.frame_rms([np.asarray(x, np.float64) for x in s.axes], [x.astype(np.float64) for x in xg])
     r_o = O.frame_rms([np.asarray(x, np.float64) for x in s.axes], xoo)
     assert abs(r_g.mean() / r_o.mean() - 1) <= e2e_tol
@@ -176,10 +202,65 @@ def test_cluster_jacobi_full_eigenbasis_parity():
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
 
-def test_full_eigenbasis_mode_matches_reference_path(codec):
-    """oi_rounds = 0 is the reference's own n_b = 1 path (codec.cpp:158-159)."""
-    spec = synth.CONFIGS["c0"]
-    check_parity(codec, spec.make(), spec, rounds=0)
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c4"])
+def test_full_eigenbasis_mode_matches_reference_path(codec, name):
+    """oi_rounds = 0 is the reference's own n_b = 1 path: block 0 always takes
+    the full F x F eigenbasis (codec.cpp:158-159, spectral.cpp:49-67).  Full
+    parity contract on every fp64 config (c2: F = 256 runs the cluster Jacobi)."""
+    spec = synth.CONFIGS[name]
+    check_parity(codec, spec.make(), spec, rounds=0, tag=f"{name}-eigenbasis")
+
+
+def leading_gap_rank(ev, k):
+    """Largest r <= k with lambda_r / lambda_{r+1} >= 1.5 and lambda_r > 1e-10
+    lambda_1: the leading columns whose span is determined."""
+    ev = np.asarray(ev, float)
+    r = 0
+    for j in range(min(k, len(ev) - 1)):
+        if ev[j] <= 1e-10 * ev[0]:
+            break
+        if ev[j] >= 1.5 * max(ev[j + 1], 0.0):
+            r = j + 1
+    return r
+
+
+def principal_angle(U, V):
+    s = np.linalg.svd(U.T @ V, compute_uv=False)
+    return float(np.arccos(np.clip(s.min(), -1.0, 1.0)))
+
+
+def oi_vs_eigenbasis_angles(plan, s, k):
+    """Largest principal angle between the GPU rank-k orthogonal-iteration
+    basis and the full eigenbasis of R = A A^T (numpy eigh, fp64), on the
+    gap-separated leading columns, per axis."""
+    out = []
+    for a in range(3):
+        X = np.asarray(s.axes[a], np.float64)
+        R = X.T @ X
+        ev, V = np.linalg.eigh(R)
+        ev, V = ev[::-1], V[:, ::-1]
+        r = leading_gap_rank(ev, k)
+        Ug, _ = plan.basis(a)
+        out.append((r, principal_angle(Ug[:, :r], V[:, :r]) if r else 0.0))
+    return out
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c2f32", "c4"])
+def test_oi_basis_within_spec_angle_of_full_eigenbasis(codec, name):
+    """The BASELINE configs' N-round rank-k basis vs the reference's full
+    eigenbasis (codec.cpp:158-159): principal angle < 1e-3 rad on the
+    gap-separated leading columns."""
+    import torch
+    spec = synth.CONFIGS[name]
+    s = spec.make()
+    dt = np.float32 if spec.dtype == "f32" else np.float64
+    plan = C.Plan(codec, s.n, s.F, s.faces, _cfg(spec), dtype=dt)
+    d = [torch.from_numpy(np.ascontiguousarray(x, dtype=dt)).cuda() for x in s.axes]
+    plan.encode_device([t.data_ptr() for t in d])
+    angles = oi_vs_eigenbasis_angles(plan, s, spec.k)
+    _log_counts({"case": name, "oi_vs_eigenbasis": angles})
+    for r, ang in angles:
+        assert r >= 1 and ang < 1e-3, angles
 
 
 @pytest.mark.parametrize("name", ["c0", "c1"])
@@ -327,21 +408,6 @@ def test_errors(codec):
     with pytest.raises(C.DmcError) as e:
         codec.decode(g)
     assert e.value.code == 6
-
-
-@pytest.mark.slow
-def test_config3_full_size_properties(codec):
-    """C3 is too large for the oracle; check size-independent properties."""
-    spec = synth.CONFIGS["c3"]
-    s = spec.make()
-    g = codec.encode(s, _cfg(spec))
-    data, _ = C.serialize(g)
-    assert abs(C.rate_exact(g)["q_s"] - 18.948) < 2e-3   # BASELINE.md §2 analytic
-    assert C.serialize(C.parse(data))[0] == data
-    x = codec.decode(g, dtype=np.float32)
-    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
-    err = max(np.abs(x[a] - s.axes[a]).max() for a in range(3))
-    assert err < 1e-2 * bbox
 
 
 def test_overlapped_analysis_is_used_once_and_only_for_its_mesh(codec):

@@ -68,7 +68,7 @@ def test_golden_encode_stream_bytes():
     assert data == G["stream"].tobytes()
 
 
-@pytest.mark.parametrize("name", ["c0"])
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
 def test_config_eigh_and_splu_crosscheck(name):
     import scipy.sparse as sp
     import scipy.sparse.linalg as spl
