@@ -1,31 +1,36 @@
 """bench.py — encode+decode vertex-frames/s of the pca_qp hot path on B200.
 
-Contract (see DESIGN.md §6): one JSON line on rank 0.
-  * workload: BASELINE.json configs[1] (torus 96x96, F=200, k=64, 15 OI
-    rounds, 12-bit, fp64) unless --config says otherwise; one "step" = one
-    full encode + decode of each of K independent sequences per GPU
-    (--inflight K, default 8 for sequences of <= 4 M vertex-frames: one
-    sequence is a latency chain that leaves most SMs idle, so K contexts /
-    CUDA streams / host threads keep K sequences in flight).  The same
-    sequence timed alone is reported as config.ms_one_sequence_alone.
+Contract (DESIGN.md §7): one JSON line on rank 0.
+  * workload (N = 1): BASELINE.json configs[3] — the largest single-GPU
+    config (512 x 512 grid, 262 144 vertices, F = 512, k = 256, 20 OI rounds,
+    12-bit, fp32 storage) unless --config says otherwise; a "step" = one full
+    encode + decode of ONE sequence.  configs[3] names the covariance
+    "applied implicitly as X(X^T Q)"; the explicit R = X^T X (same iteration,
+    2 F^2 n flops once instead of 4 F n k per round) is the headline and the
+    implicit form is reported beside it (key "implicit_covariance").
   * value: device-resident (inputs already in HBM, mesh plan built once
-    outside the timed region), CUDA events (one start event every plan
-    stream waits on, the last plan stream's end event), L2 flushed between
-    steps (outside the events); max over ranks.
+    outside the timed region), CUDA events on the plan stream, L2 flushed
+    (256 MiB write) between steps outside the events; max over ranks.
   * e2e: the same metric through the drop-in C ABI (dmcg_encode +
-    dmcg_decode, one host thread per in-flight sequence) from pinned host
-    buffers: H2D of the inputs, plan build, D2H of the encoded symbols, H2D
-    for decode, D2H of the vertices.  With K > 1 the K workers run in steady
-    state (no barrier between steps), so copies and host phases of one
-    sequence overlap kernels of another; ms_per_step = wall / pairs per worker.
-  * N > 1 (torchrun): every rank codes its own independent sequences (seeds
-    offset by rank) with no data-path collective -> scaling "weak".
-  * --rows (c3): ONE sequence sharded by vertex rows across the N ranks
-    (libdmcg shard ABI: NCCL allreduce of the Gram partials and range keys,
-    all-gather of the symbols; decode split by frame windows) -> scaling
-    "strong" (the whole job is one sequence per step).
-  * --impl reference: the CPU oracle port (kind "port", the reference itself
-    cannot be built here: Eigen3 absent) on the host cores; rank 0 only.
+    dmcg_decode) from pinned host buffers: H2D of the inputs, mesh build,
+    D2H of the encoded symbols, H2D for decode, normal matrix + symbolic
+    analysis, D2H of the vertices — all inside the timed region.
+  * cpu_baseline: the oracle port (kind "port"; the reference itself needs
+    Eigen3, absent) on a bounded sample of the same workload — the config's
+    generator at a smaller vertex count with the same F / k / rounds / bits —
+    single-thread (the reference is single-threaded) and on all host cores,
+    with per-stage times.
+  * N > 1 (torchrun, or --gpus N which re-launches itself under
+    torch.distributed.run): default --mode rows — ONE c3 sequence sharded by
+    vertex rows across the N ranks (libdmcg shard ABI: NCCL allreduce of the
+    Gram partials and range keys, all-gather of the symbols; decode split by
+    frame windows) -> scaling "strong".  --mode sequences: every rank codes
+    its own independent sequences, no data-path collective -> "weak".
+  * small configs (<= 4 M vertex-frames: c0, c1, c4) keep K independent
+    sequences in flight per GPU (--inflight, default 8 there) — one sequence
+    of those is a latency chain that leaves most SMs idle.
+  * --impl reference: the CPU oracle port on all host cores, rank 0 only,
+    each step the bounded sample above.
 """
 from __future__ import annotations
 
@@ -48,9 +53,26 @@ from paper_2111_10105_b200.shard import (dist_env, max_over_ranks, sequence_for_
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 FP64_DMMA_TFLOPS = 37.1  # profiles/r01_peaks.md (tools/peak_fp64.cu)
-# dram__bytes_read.sum + dram__bytes_write.sum of one k_oi_cluster launch (c1),
-# from the ncu --set full capture in profiles/ (None until captured)
-OI_TRAFFIC = 1403136  # profiles/r01_ncu_oi_cluster_full.md
+# dram__bytes_read.sum + dram__bytes_write.sum per launch, per config and
+# kernel, from the committed ncu captures (tools/kernel_roofline.py --traffic-json)
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+
+# Bounded CPU samples (cpu_baseline and --impl reference): the config's own
+# generator at a smaller size, same F / k / OI rounds / bits / dtype.
+CPU_SAMPLES = {
+    "c3": {1: ("grid", 64, 64), 0: ("grid", 256, 256)},   # 0 = all host cores
+}
+
+
+def traffic_of(cfgname, kernel_prefix):
+    try:
+        data = json.load(open(TRAFFIC_PATH))[cfgname]
+    except Exception:
+        return None
+    for name, b in data.items():
+        if name.replace("void ", "").startswith(kernel_prefix):
+            return int(b)
+    return None
 
 WORKLOADS = {
     "c0": "c0: icosphere L4 (2562 v), F=64, k=32, 10 OI rounds, 12-bit, fp64",
@@ -108,34 +130,69 @@ def load_peak():
         return FALLBACK_HBM_GBS, "fallback"
 
 
-def run_reference(args, rank, world):
-    """CPU oracle port of the reference path on the host cores (rank 0)."""
-    if rank != 0:
-        return 0
+def cpu_sample(cfgname, threads):
+    """(sequence, description) of the bounded CPU sample of a config: c3 uses
+    its generator at 64 x 64 (one thread) / 256 x 256 (all cores) vertices with
+    the same F, k, OI rounds, bits and dtype; the small configs run whole."""
+    from paper_2111_10105_b200 import synth
+    spec = synth.CONFIGS[cfgname]
+    samp = CPU_SAMPLES.get(cfgname)
+    if samp is None:
+        return spec, spec.make(0), f"the full {cfgname} sequence"
+    kind, nx, ny = samp[1 if threads == 1 else 0]
+    s = synth.grid(nx, ny, 512, seed=3)
+    return spec, s, (f"{cfgname} generator at {nx}x{ny} = {s.n} vertices (full config 512x512), "
+                     f"same F={s.F}, k={spec.k}, {spec.rounds} OI rounds, {spec.bits}-bit, "
+                     "fp32 storage")
+
+
+def time_oracle(cfgname, threads, steps=1):
+    """Oracle port (oracle/dmc_oracle.c) encode + decode of the bounded
+    sample: vertex-frames/s and per-stage seconds (median over `steps`)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
-    spec, s = sequence_for_rank(args.config, 0)
-    threads = os.cpu_count() or 1
-    vf = s.n * s.F
-    times = []
-    for it in range(args.warmup + args.steps):
+    spec, s, desc = cpu_sample(cfgname, threads)
+    walls, stages = [], []
+    for _ in range(steps):
+        te, td = {}, {}
         t0 = time.perf_counter()
-        enc = O.encode(s, spec.k, spec.bits, rounds=spec.rounds, nthreads=threads)
-        O.decode(enc, nthreads=threads)
-        dt = time.perf_counter() - t0
-        if it >= args.warmup:
-            times.append(dt)
-    tot = sum(times)
-    value = vf * len(times) / tot
+        enc = O.encode(s, spec.k, spec.bits, rounds=spec.rounds, nthreads=threads, timing=te)
+        O.decode(enc, nthreads=threads, timing=td)
+        walls.append(time.perf_counter() - t0)
+        stages.append({"connectivity": te["t_connectivity"] + td["t_connectivity"],
+                       "gram": te["t_gram"], "eigen_oi": te["t_eigen"], "delta": te["t_delta"],
+                       "projection": te["t_project"], "quantize": te["t_quantize"],
+                       "anchors": te["t_anchors"], "dict_decode": td["t_dict_decode"],
+                       "reconstruct": td["t_reconstruct"], "anchored_solve": td["t_solve"]})
+    wall = float(np.median(walls))
+    st = {k: round(float(np.median([d[k] for d in stages])), 4) for k in stages[0]}
+    return {"value": s.n * s.F / wall, "unit": "vertex-frames/s", "threads": threads,
+            "seconds": wall, "vertex_frames": s.n * s.F, "sample": desc, "stage_s": st,
+            "walls": walls}
+
+
+def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle port of the reference path (the
+    reference itself needs Eigen3, absent) on all host cores, rank 0 only;
+    each step one encode + decode of the bounded sample."""
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    r = time_oracle(args.config, threads, steps=args.warmup + args.steps)
+    walls = r["walls"][args.warmup:]
+    tot = sum(walls)
+    value = r["vertex_frames"] * len(walls) / tot
     line = {
         "impl": "reference", "metric": "encode+decode vertex-frames/sec", "value": value,
         "unit": "vertex-frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * tot / len(walls), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, DESIGN.md §2)",
         "config": {"workload": WORKLOADS[args.config], "solver": "sparse LDL^T + 1 refinement"},
         "cpu_baseline": {"value": value, "unit": "vertex-frames/s", "cores": threads, "kind": "port",
-                         "sample": f"full {args.config} sequence per step (oracle/dmc_oracle.c; "
-                                   "reference needs Eigen3, absent)"},
+                         "sample": r["sample"] + " per step (oracle/dmc_oracle.c; the reference "
+                                                 "needs Eigen3, absent)",
+                         "stage_s": r["stage_s"]},
         "e2e": {"value": value, "unit": "vertex-frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -143,17 +200,17 @@ def run_reference(args, rank, world):
     return 0
 
 
-def cpu_baseline(args, spec, s):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import pyoracle as O
+def cpu_baseline(args):
+    """Two rows on the box's host cores: single-thread (like the reference) and
+    all cores; each its own bounded sample, per-stage seconds."""
     threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    enc = O.encode(s, spec.k, spec.bits, rounds=spec.rounds, nthreads=threads)
-    O.decode(enc, nthreads=threads)
-    dt = time.perf_counter() - t0
-    return {"value": s.n * s.F / dt, "unit": "vertex-frames/s", "cores": threads, "kind": "port",
-            "sample": f"one full {args.config} encode+decode ({s.n}x{s.F}), oracle/dmc_oracle.c, "
-                      f"{threads} threads, {dt:.2f} s"}
+    rows = [time_oracle(args.config, 1), time_oracle(args.config, threads)]
+    for r in rows:
+        r.pop("walls")
+    allc = rows[1]
+    return {"value": allc["value"], "unit": "vertex-frames/s", "cores": threads, "kind": "port",
+            "sample": allc["sample"] + f"; {allc['seconds']:.2f} s on {threads} threads",
+            "rows": rows}
 
 
 class _DevArray:
@@ -278,7 +335,8 @@ def run_rows(args, rank, world, local, dist):
                        "l2": "256 MiB flush between timed steps", "cg_rtol": args.rtol},
             "roofline": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
                          "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_DMMA_TFLOPS, "traffic": None,
+                         "frac": achieved / FP64_DMMA_TFLOPS,
+                         "traffic": traffic_of(args.config, "k_oi_cluster"),
                          "algorithmic_flops": oi_flops, "ms": oi_ms,
                          "share_of_step": oi_ms / (total_ms / args.steps)},
             "cpu_baseline": None,
@@ -300,17 +358,63 @@ def run_rows(args, rank, world, local, dist):
     return 0
 
 
+def time_plan(plan, d_in, d_out, args, stream, flush, dist, local):
+    """W untimed warm-up steps, then K steps each bracketed by CUDA events on
+    the plan stream (the L2 flush and the host sync sit outside the events).
+    Returns (per-step ms, per-step plan stats, launches, Clocks)."""
+    import torch
+    for _ in range(args.warmup):
+        plan.encode_device([t.data_ptr() for t in d_in])
+        plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms, stats, launches = [], [], 0
+    with Clocks(local) as clk:
+        for it in range(args.steps):
+            flush.fill_(it & 0xFF)               # L2 flush, outside the timed events
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plan.encode_device([t.data_ptr() for t in d_in])
+            plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            st = plan.stats()
+            stats.append(st)
+            launches += st["kernel_launches_encode"] + st["kernel_launches_decode"]
+    torch.cuda.synchronize()
+    return step_ms, stats, launches, clk
+
+
+def relaunch_under_torchrun(n):
+    """`python bench.py --gpus N` without a torchrun environment: re-exec this
+    script under torch.distributed.run with N ranks on this node (loopback
+    rendezvous) and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c1", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--rtol", type=float, default=1e-10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-implicit", action="store_true",
+                    help="skip the extra implicit-covariance measurement (c3)")
     ap.add_argument("--implicit", action="store_true",
-                    help="implicit OI: Z = X^T (X Q) per round, R never formed")
+                    help="headline with the implicit OI: Z = X^T (X Q) per round, R never formed")
     ap.add_argument("--inflight", type=int, default=None,
                     help="independent sequences in flight per GPU (one context / CUDA stream / "
                          "host thread each); default 8 for sequences of <= 4 M vertex-frames "
@@ -318,13 +422,24 @@ def main():
     ap.add_argument("--n-b", type=int, default=1,
                     help="blocks variant with this many frame blocks (SURVEY 8f f2); "
                          "k_l = min(config k, k_f); default 1 = the pca_qp hot path")
-    ap.add_argument("--rows", action="store_true",
-                    help="shard one sequence by vertex rows across the ranks (SURVEY §8e)")
+    ap.add_argument("--mode", choices=["rows", "sequences"], default=None,
+                    help="N > 1: rows = one sequence sharded by vertex rows (default), "
+                         "sequences = independent sequences per rank")
+    ap.add_argument("--rows", action="store_true", help="same as --mode rows")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        return 2
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.rows:
+        args.mode = "rows"
+    if args.mode is None:
+        args.mode = "rows" if world > 1 and args.n_b == 1 else "sequences"
 
     import torch
     from paper_2111_10105_b200 import codec as C
@@ -332,10 +447,12 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator / NVLS lines
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    if args.rows:
+    if args.mode == "rows":
         return run_rows(args, rank, world, local, dist)
 
     spec, s = sequence_for_rank(args.config, rank)
@@ -356,34 +473,31 @@ def main():
     d_out = [torch.empty_like(t) for t in d_in]
     stream = torch.cuda.ExternalStream(plan.stream())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    step_ms, fac_ms, sol_ms, oi_ms, launches = [], [], [], [], 0
-    for it in range(args.warmup):
-        plan.encode_device([t.data_ptr() for t in d_in])
-        plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    with Clocks(local) as clk:
-        for it in range(args.steps):
-            flush.fill_(it & 0xFF)               # L2 flush, outside the timed events
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            plan.encode_device([t.data_ptr() for t in d_in])
-            plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
-            e1.record(stream)
-            e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            st = plan.stats()
-            fac_ms.append(st["ms_factor"])
-            sol_ms.append(st["ms_solve"])
-            oi_ms.append(st["ms_oi"])
-            launches += st["kernel_launches_encode"] + st["kernel_launches_decode"]
-    torch.cuda.synchronize()
+    step_ms, stats, launches, clk = time_plan(plan, d_in, d_out, args, stream, flush, dist, local)
+    fac_ms = [st["ms_factor"] for st in stats]
+    sol_ms = [st["ms_solve"] for st in stats]
+    oi_ms = [st["ms_oi"] for st in stats]
     total_ms = max_over_ranks(float(sum(step_ms)), dist, "cuda")
     if dist:
         dist.barrier()
+
+    # ---- the implicit covariance of configs[3] (extra key) ------------------
+    implicit = None
+    if args.config == "c3" and not args.implicit and not args.no_implicit and args.n_b == 1:
+        icfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds,
+                               oi_implicit=True)
+        iplan = C.Plan(codec, s.n, s.F, s.faces, icfg, dtype=npdt)
+        istream = torch.cuda.ExternalStream(iplan.stream())
+        i_ms, i_stats, i_launch, i_clk = time_plan(iplan, d_in, d_out, args, istream, flush, dist,
+                                                   local)
+        i_total = max_over_ranks(float(sum(i_ms)), dist, "cuda")
+        implicit = {"value": whole_job_rate(s.n * s.F, world, args.steps, i_total),
+                    "ms_per_step": i_total / args.steps,
+                    "covariance": "implicit: every OI round P = X Q, Z = X^T P (R never formed)",
+                    "gpu_launches": i_launch, "clocks": i_clk.summary(),
+                    "stage_ms": {k: float(np.median([d[k] for d in i_stats]))
+                                 for k in i_stats[0] if k.startswith("ms_")}}
+        iplan.close()
     vf_step = s.n * s.F
     value = whole_job_rate(vf_step, world, args.steps, total_ms)
     single_ms = total_ms / args.steps   # one sequence at a time (latency of one encode+decode)
@@ -531,7 +645,7 @@ def main():
                                  for a in range(3)])) * np.sqrt(3))
 
     if rank == 0:
-        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(args, spec, s)
+        cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(args)
         line = {
             "metric": "encode+decode vertex-frames/sec", "value": value, "unit": "vertex-frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -554,17 +668,20 @@ def main():
                                "inside e2e", "cg_rtol": args.rtol},
             "roofline": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
                          "peak": peak, "peak_kind": "measured FP64 DMMA, whole GPU (profiles/r01_peaks.md)",
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": OI_TRAFFIC,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic_of(args.config, "k_oi_cluster"),
+                         "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per "
+                                           f"launch, {args.config} (profiles/roofline_traffic.json)",
                          "launches_per_step": 1, "ctas": 3 * ((spec.k + 7) // 8),
                          "cluster": (spec.k + 7) // 8,
                          "algorithmic_flops": oi_flops, "ms": oi_sec * 1e3,
                          "share_of_step": oi_sec * 1e3 / single_ms,
                          "share_basis": "of one sequence's encode+decode timed alone",
                          "model": "3 axes x ((rounds+1) x (2F^2k + 4Fk^2 - 4k^3/3) + 2Fk^2)",
-                         "note": "one cluster per axis, 8 columns of Z / Q per CTA; every OI "
-                                 "round is a wavefront of dependent block-Householder steps "
-                                 "(latency-bound on a 200 x 64 problem), so the ceiling is the "
-                                 "cluster's SMs, not the device peak; see DESIGN.md §5"},
+                         "note": "one cluster per axis, 8 or 16 columns of Z / Q per CTA; every "
+                                 "OI round is a wavefront of dependent block-Householder steps "
+                                 "(latency-bound), so the ceiling is the cluster's SMs, not the "
+                                 "device peak; see DESIGN.md §5"},
             "roofline_k7": {"kernel": "K7 direct solve (k_panel/k_trailing/k_inv_*/k_fwd*/k_bwd*)",
                             "bound": "tensor", "achieved": k7_achieved, "peak": peak, "unit": "TFLOP/s",
                             "frac": k7_achieved / peak, "algorithmic_flops": k7_flops,
@@ -580,7 +697,9 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "quality": {"rmse_over_bbox": rms / bbox},
-            "stage_ms": {k: v for k, v in plan.stats().items() if k.startswith("ms_")},
+            "stage_ms": {k: float(np.median([d[k] for d in stats])) for k in stats[0]
+                         if k.startswith("ms_")},
+            "implicit_covariance": implicit,
         }
         print(json.dumps(line), flush=True)
     if dist:

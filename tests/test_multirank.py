@@ -73,3 +73,25 @@ def test_reference_arm_under_torchrun_prints_on_rank0_only():
     rec = json.loads(lines[0])
     assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["value"] > 0
     assert rec["e2e"]["h2d_bytes_per_step"] == 0 and rec["cpu_baseline"]["kind"] == "port"
+
+
+def test_gpus_flag_relaunches_itself_under_torchrun():
+    """`python bench.py --gpus 2` with no torchrun environment re-executes itself
+    under torch.distributed.run with 2 ranks (loopback rendezvous) instead of
+    silently running one process; rank 0 alone prints the line."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    cmd = [sys.executable, "bench.py", "--impl", "reference", "--config", "c0", "--gpus", "2",
+           "--steps", "1", "--warmup", "0"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_gpus_mismatch_fails_loudly():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c0",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE=1" in out.stdout

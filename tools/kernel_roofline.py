@@ -1,10 +1,21 @@
 """Per-kernel roofline table from an ncu --csv metrics log (time, DRAM bytes,
-tensor / fp64 pipe activity, SM-time): python tools/kernel_roofline.py log.csv"""
+tensor / fp64 pipe activity, SM-time):
+
+    python tools/kernel_roofline.py log.csv [--traffic-json profiles/roofline_traffic.json CFG]
+
+--traffic-json merges {CFG: {kernel: DRAM bytes per launch}} into the given
+file; bench.py reads roofline.traffic from it (per config, per kernel)."""
 import collections
 import csv
+import json
+import os
 import sys
 
-HBM = 6548.8  # GB/s, MEASURED_PEAKS.json (copy kernel)
+_PEAKS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+try:
+    HBM = float(json.load(open(_PEAKS))["hbm_gbs"])   # GB/s, measured copy kernel
+except Exception:
+    HBM = 6650.0                                      # B200_PROFILING.md fallback
 
 rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
@@ -39,3 +50,10 @@ for name, a in sorted(agg.items(), key=lambda x: -x[1]["t"])[:24]:
     print(f"| `{name}` | {int(a['n'])} | {a['t'] * 1e3:.3f} | {a['t'] / tot * 100:.1f}% | "
           f"{a['bytes'] / 1e6:.1f} | {gbs:.0f} | {gbs / HBM * 100:.1f} | "
           f"{a['tensor'] / a['t']:.1f} | {a['fp64'] / a['t']:.1f} |")
+
+if "--traffic-json" in sys.argv:
+    i = sys.argv.index("--traffic-json")
+    path, cfg = sys.argv[i + 1], sys.argv[i + 2]
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    data[cfg] = {name: a["bytes"] / a["n"] for name, a in agg.items()}
+    json.dump(data, open(path, "w"), indent=1, sort_keys=True)
