@@ -336,6 +336,14 @@ enum { DMCG_SHARD_GRAM = 0, DMCG_SHARD_KEYS = 1, DMCG_SHARD_SYMBOLS = 2 };
 /* Device pointer and element count of a collective buffer (f64 / u64 / u16). */
 int dmcg_shard_buffer(dmcg_plan* plan, int which, void** dptr, size_t* count);
 
+/* ---- Ozaki INT8 tensor-core GEMM (csrc/ozaki.cu) ---------
+ * C (M x N, row-major f64, device) = A B^T on the current device and stream 0,
+ * A: M x K, B: N x K device matrices (f32 or f64) with element (r, k) at
+ * [r * rs + k * ks]; s = slices per operand (3..7).  Synchronous; used by the
+ * parity tests to pin the tcgen05 kernel against an fp64 GEMM. */
+int dmcg_ozaki_gemm(const void* dA, int a_f32, long a_rs, long a_ks, int M, const void* dB,
+                    int b_f32, long b_rs, long b_ks, int N, int K, int s, double* dC);
+
 /* ---- diagnostics (host only, no GPU) ----------------------------------
  * Symbolic analysis of the anchored normal matrix of a mesh and, when W > 0,
  * a CPU solve M x = b (b, x: n x W row-major) with the same supernodal data

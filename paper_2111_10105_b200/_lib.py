@@ -36,6 +36,7 @@ EXPORTS = [
     "dmcg_plan_serialize", "dmcg_plan_distortion", "dmcg_comm_unique_id", "dmcg_comm_create",
     "dmcg_comm_destroy", "dmcg_shard_layout", "dmcg_plan_create_shard", "dmcg_shard_info_get",
     "dmcg_shard_encode_device", "dmcg_shard_encode_phase", "dmcg_shard_buffer",
+    "dmcg_build_connectivity", "dmcg_host_error", "dmcg_ozaki_gemm",
 ]
 
 
@@ -148,6 +149,13 @@ def lib():
     L.dmcg_rate_exact.argtypes = [ctypes.POINTER(DmcgSections), ctypes.c_uint32, ctypes.c_uint32,
                                   f64p]
     L.dmcg_rate_exact.restype = None
+    L.dmcg_build_connectivity.argtypes = [u32p, ctypes.c_uint32, ctypes.c_uint32, u32p, u32p,
+                                          ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
+    L.dmcg_host_error.restype = ctypes.c_char_p
+    L.dmcg_ozaki_gemm.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_long, ctypes.c_long,
+                                  ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_long,
+                                  ctypes.c_long, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_void_p]
     L.dmcg_anchor_count.restype = ctypes.c_uint32
     L.dmcg_anchor_count.argtypes = [ctypes.c_uint32, ctypes.c_double]
     L.dmcg_select_anchors.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
