@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "ozaki.h"
 #include "kernels.h"
 #include "par.h"
 
@@ -634,8 +635,22 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_R = (double*)get(3 * FF * 8);
   const int tiles = ((F + 63) / 64) * ((F + 63) / 64);
   size_t splits = std::max<size_t>(1, (2 * 148 + tiles * 3 - 1) / (tiles * 3));
+  // Ozaki INT8 tensor-core Gram for fp32 storage: its split-K
+  // partials need the larger of the two partial counts
+  p->oz_slices = 0;
+  if (dtype == DMCG_F32 && p->nb == 1 && !getenv("DMCG_NO_OZAKI")) {
+    const char* e = getenv("DMCG_OZ_SLICES");
+    p->oz_slices = e ? std::max(3, std::min(7, atoi(e))) : 5;
+    const size_t ozs = (size_t)dmcg::oz_gram_splits((int)F, (int)n, p->oz_slices);
+    splits = std::max(splits, ozs);
+  }
   p->part_elems = splits * 3 * FF;
   p->d_part = (double*)get(p->part_elems * 8);
+  if (p->oz_slices) {
+    const size_t fp = dmcg::oz_rows_pad((int)F), kp = dmcg::oz_k_pad((int)n);
+    p->d_oz_q = (int8_t*)get(3 * (size_t)p->oz_slices * fp * kp);
+    p->d_oz_max = (unsigned long long*)get(3 * fp * 8);
+  }
   p->d_U = (double*)get(3 * FF * 8);
   p->d_evals = (double*)get(3 * (size_t)F * 8);
   p->d_Q = (double*)get(3 * (size_t)F * kk * 8);

@@ -217,6 +217,11 @@ struct dmcg_plan {
   double* d_R = nullptr;           // 3 x F x F
   double* d_part = nullptr;        // split-K partials
   size_t part_elems = 0;
+  // Ozaki INT8 tensor-core Gram (ozaki.h; f32 storage, n_b = 1): the s
+  // slices of X (rows = frames, K = vertex rows) and their row maxima
+  int oz_slices = 0;               // 0: DMMA Gram
+  int8_t* d_oz_q = nullptr;        // 3 x s x F_pad x n_pad
+  unsigned long long* d_oz_max = nullptr;  // 3 x F_pad
   double* d_U = nullptr;           // 3 x F x F (col-major)
   double* d_evals = nullptr;       // 3 x F
   double *d_Q = nullptr, *d_Z = nullptr, *d_tau = nullptr;  // 3 x F x k, 3 x F

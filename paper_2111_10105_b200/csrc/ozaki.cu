@@ -25,6 +25,19 @@ namespace {
 
 // ---- slicing ------------------------------------------------------------------
 
+// Slice exponent of a row with max |x| = mx: the smallest e with
+// mx 2^-e < 127.5 / 128, so the first balanced digit rint(128 x 2^-e) stays
+// within [-127, 127] and every later digit (a remainder in [-1/2, 1/2]
+// scaled by 128) within [-64, 64].  Rounded (balanced) digits make the
+// truncation and the dropped diagonals (p, q >= 2 only) zero-mean, so their
+// errors cancel like fp64 rounding instead of accumulating with n.
+__device__ __forceinline__ int oz_exp(double mx) {
+  if (!(mx > 0.0)) return 0;
+  int e;
+  const double f = frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+  return f >= 127.5 / 128.0 ? e + 1 : e;
+}
+
 template <typename T>
 __device__ __forceinline__ double oz_ld(const OzOperand& op, int b, long r, long k) {
   const T* base = (const T*)op.base[b];
@@ -80,21 +93,19 @@ __global__ void __launch_bounds__(256) k_oz_slice(OzOperand op, OzSlices sl) {
   const int r = t >> 2, kq = (t & 3) * 16;
   const long gk = k0 + kq;
   if (gk >= sl.K_pad) return;
-  const double mx = __longlong_as_double((long long)sl.maxbits[(long)b * sl.rows_pad + r0 + r]);
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);
+  const int e = oz_exp(__longlong_as_double((long long)sl.maxbits[(long)b * sl.rows_pad + r0 + r]));
   uint32_t w[kOzMaxS][4];
 #pragma unroll
   for (int p = 0; p < kOzMaxS; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    double y = ldexp(tile[r][kq + j], -e);  // |y| < 1, exact
+    double y = ldexp(tile[r][kq + j], -e);  // |y| < 127.5 / 128, exact
 #pragma unroll
     for (int p = 0; p < kOzMaxS; ++p) {
       if (p < sl.s) {
         y *= 128.0;
-        const double a = trunc(y);  // in [-127, 127]
-        y -= a;                     // exact
+        const double a = rint(y);  // balanced digits: |a_1| <= 127, |a_p| <= 64 (p > 1)
+        y -= a;                    // exact, |y| <= 1/2
         w[p][j >> 2] |= (uint32_t)(uint8_t)(int8_t)(int)a << (8 * (j & 3));
       }
     }
@@ -308,10 +319,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(smem_u32(&bars[2 * C::kStages]), 0u);
       tc_fence_after();
     }
-    const double amax = __longlong_as_double((long long)g.a_max[(long)b * g.a_rows_pad +
-                                                                 min(mrow, g.a_rows_pad - 1)]);
-    int ea = 0;
-    if (amax > 0.0) frexp(amax, &ea);
+    const int ea = oz_exp(__longlong_as_double(
+        (long long)g.a_max[(long)b * g.a_rows_pad + min(mrow, g.a_rows_pad - 1)]));
     const uint32_t lane_addr = tbase + ((uint32_t)(quarter * 32) << 16);
 #pragma unroll 1
     for (int c = 0; c < kOzBN / 16; ++c) {
@@ -334,9 +343,8 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < 16; ++j) {
           const int ncol = tn * kOzBN + c * 16 + j;
           if (ncol < g.N) {
-            const double bmax = __longlong_as_double((long long)g.b_max[(long)b * g.b_rows_pad + ncol]);
-            int eb = 0;
-            if (bmax > 0.0) frexp(bmax, &eb);
+            const int eb =
+                oz_exp(__longlong_as_double((long long)g.b_max[(long)b * g.b_rows_pad + ncol]));
             dst[(long)ncol * g.out.sn] = ldexp(v[j], ea + eb);
           }
         }
@@ -429,6 +437,38 @@ int oz_splits(const OzSlices& A, int min_splits) {
   int splits = (kb_total + kb_chunk - 1) / kb_chunk;
   if (min_splits > splits) splits = min_splits < kb_total ? min_splits : kb_total;
   return splits < 1 ? 1 : splits;
+}
+
+static int gram_min_splits(int F) {
+  const int tiles = ((F + kOzBM - 1) / kOzBM) * ((F + kOzBN - 1) / kOzBN);
+  return (2 * 148 + 3 * tiles - 1) / (3 * tiles);
+}
+
+int oz_gram_splits(int F, int n, int s) {
+  OzSlices sl;
+  sl.K = n;
+  sl.K_pad = oz_k_pad(n);
+  sl.s = s;
+  return oz_splits(sl, gram_min_splits(F));
+}
+
+cudaError_t oz_gram(cudaStream_t st, const void* const x[3], bool f32, int n, int F, int s,
+                    int8_t* q, unsigned long long* maxbits, double* part, int* splits) {
+  OzOperand op{{x[0], x[1], x[2]}, f32, 1L, (long)F, F, n, 3};
+  OzSlices sl;
+  sl.q = q;
+  sl.maxbits = maxbits;
+  sl.rows = F;
+  sl.rows_pad = oz_rows_pad(F);
+  sl.K = n;
+  sl.K_pad = oz_k_pad(n);
+  sl.s = s;
+  sl.batch = 3;
+  cudaError_t e = oz_slice(st, op, sl);
+  if (e != cudaSuccess) return e;
+  const long FF = (long)F * F;
+  OzStore out{part, FF, 3 * FF, (long)F, 1L};
+  return oz_gemm(st, sl, sl, out, gram_min_splits(F), splits);
 }
 
 cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const OzStore& out,

@@ -7,13 +7,15 @@
 // ~4.5 POPS dense and their int32 accumulation is EXACT, so a matrix product
 // whose operands are cut into s signed 7-bit slices,
 //
-//   x = 2^e(row) * sum_{p=1..s} a_p 2^(-7p),    a_p in [-127, 127],
+//   x = 2^e(row) * sum_{p=1..s} a_p 2^(-7p),    a_1 in [-127, 127],
+//   a_p in [-64, 64] for p > 1 (balanced, round-to-nearest digits),
 //
 // is recovered as  C = 2^(eA + eB) sum_{d=2}^{s+1} 2^(-7d) D_d,
 //   D_d = sum_{p+q=d} A_p B_q^T   (exact int32 GEMMs, one TMEM accumulator
 // per diagonal d, combined in fp64 in the epilogue).  The dropped terms
-// (p + q > s + 1) and the slice truncation bound the error by about
-// 2^(-7s) |x|_max |y|_max per product term — s = 5 (35 bits) covers fp32
+// (p + q > s + 1, both digits balanced) and the rounded slice tails bound the
+// error by about 2^(-7s) |x|_max |y|_max per product term, zero-mean, so
+// the error of a K-term sum grows like sqrt(K) — s = 5 (35 bits) covers fp32
 // inputs with headroom, s = 7 (49 bits) approaches fp64.
 //
 // Operands are "rows x K" views of fp32 / fp64 matrices with arbitrary
@@ -34,7 +36,7 @@ constexpr int kOzBM = 128;   // UMMA M (TMEM lanes)
 constexpr int kOzBN = 64;    // UMMA N per diagonal accumulator
 constexpr int kOzBK = 32;    // one kind::i8 MMA consumes K = 32 bytes
 constexpr int kOzMaxS = 7;
-constexpr int kOzKChunk = 16384;  // K per split: S * 127^2 * K < 2^31 for S <= 8
+constexpr int kOzKChunk = 16384;  // K per split: |D_d| <= S * 127 * 64 * K < 2^31
 
 // A batch (<= 3) of "rows x K" matrices: element (r, k) of batch b at
 // base[b][r * row_stride + k * k_stride], fp32 or fp64.
@@ -76,5 +78,14 @@ cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const
 
 // Splits oz_gemm will use for (A, B, min_splits).
 int oz_splits(const OzSlices& A, int min_splits);
+
+// The Gram R = X^T X of a batch of 3 n x F fp32 / fp64 axis matrices
+// (x[i*F + f]; rows = frames, K = vertex rows): slices X into q / maxbits
+// (3 x s x oz_rows_pad(F) x oz_k_pad(n) bytes, 3 x oz_rows_pad(F)) and writes
+// the split-K partials part[(split * 3 + b) F^2 + f F + g]; returns the
+// split count in *splits.  oz_gram_splits() = that count (for sizing part).
+int oz_gram_splits(int F, int n, int s);
+cudaError_t oz_gram(cudaStream_t st, const void* const x[3], bool f32, int n, int F, int s,
+                    int8_t* q, unsigned long long* maxbits, double* part, int* splits);
 
 }  // namespace dmcg

@@ -7,6 +7,7 @@
 
 #include "gemm.cuh"
 #include "internal.h"
+#include "ozaki.h"
 #include "kernels.h"
 
 namespace dmcg {
@@ -146,6 +147,15 @@ template <typename T>
 Status gram(dmcg_plan* p, const void* const x[3], int n) {
   cudaStream_t s = p->ctx->stream;
   const int F = (int)p->F;
+  if (p->oz_slices) {
+    // INT8 tensor cores, Ozaki slices (ozaki.h): exact int32 slice products,
+    // fp64 combination; the partials go through the same ordered reduction
+    int splits = 0;
+    DMCG_TRY(oz_gram(s, x, std::is_same<T, float>::value, n, F, p->oz_slices, p->d_oz_q,
+                     p->d_oz_max, p->d_part, &splits));
+    DMCG_TRY(launch_reduce_sym(s, F, splits, 3, p->d_part, p->d_R));
+    return Status::ok();
+  }
   const int tiles = ((F + kBM - 1) / kBM) * ((F + kBN - 1) / kBN);
   int splits = pick_splits(tiles, 3, n);
   const long maxs = (long)(p->part_elems / (3L * F * F));
