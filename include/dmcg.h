@@ -245,6 +245,10 @@ int dmcg_plan_upload(dmcg_plan* plan, const dmcg_encoded* in);
  * dictionaries of the axis back to back (n_b k_f^2 doubles), evals = F
  * doubles (k_f eigenvalues per block's direct decomposition). */
 int dmcg_plan_basis(dmcg_plan* plan, int axis, double* U_host, double* evals_host);
+/* K1's delta coordinates of the last device encode, axis-major (n x F
+ * vertex-major per axis, f64) into host memory: the delta_coordinates
+ * parity check (laplacian.cpp:39-46) at full size.  Not for blocks plans. */
+int dmcg_plan_delta(dmcg_plan* plan, int axis, double* delta_host);
 
 typedef struct {
   int cg_iterations_max;     /* max over columns in the last decode */

@@ -36,7 +36,7 @@ EXPORTS = [
     "dmcg_plan_serialize", "dmcg_plan_distortion", "dmcg_comm_unique_id", "dmcg_comm_create",
     "dmcg_comm_destroy", "dmcg_shard_layout", "dmcg_plan_create_shard", "dmcg_shard_info_get",
     "dmcg_shard_encode_device", "dmcg_shard_encode_phase", "dmcg_shard_buffer",
-    "dmcg_build_connectivity", "dmcg_host_error", "dmcg_ozaki_gemm",
+    "dmcg_build_connectivity", "dmcg_host_error", "dmcg_ozaki_gemm", "dmcg_plan_delta",
 ]
 
 
@@ -169,6 +169,7 @@ def lib():
     L.dmcg_plan_download.argtypes = [vp, ctypes.POINTER(DmcgEncoded)]
     L.dmcg_plan_upload.argtypes = [vp, ctypes.POINTER(DmcgEncoded)]
     L.dmcg_plan_basis.argtypes = [vp, ctypes.c_int, f64p, f64p]
+    L.dmcg_plan_delta.argtypes = [vp, ctypes.c_int, f64p]
     L.dmcg_plan_stats.argtypes = [vp, ctypes.POINTER(DmcgStats)]
     L.dmcg_ctx_stats.argtypes = [vp, ctypes.POINTER(DmcgStats)]
     L.dmcg_plan_stream.argtypes = [vp]

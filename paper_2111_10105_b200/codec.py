@@ -315,6 +315,12 @@ class Plan:
         e = c.to_c()
         _check(self.codec.handle, L.lib().dmcg_plan_upload(self._p, ctypes.byref(e)))
 
+    def delta(self, axis: int):
+        """K1's delta coordinates (n x F, f64) of the last device encode."""
+        d = np.zeros((self.n, self.F))
+        _check(self.codec.handle, L.lib().dmcg_plan_delta(self._p, axis, d.ctypes.data_as(L.f64p)))
+        return d
+
     def basis(self, axis: int):
         """(U, evals); blocks: U is (n_b, k_f, k_f), U[b] block b's dictionary."""
         nb = max(self.cfg.n_b, 1)

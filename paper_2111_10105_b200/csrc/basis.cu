@@ -1614,6 +1614,365 @@ __global__ void __launch_bounds__(kJcThreads)
   if (!converged && tid == 0 && q == 0) atomicOr(flags, 1);
 }
 
+// ---------------------------------------------------------------------------
+// Block Jacobi over a cluster (k_jacobi_blk, m <= 256; the default for
+// matrices too large for one CTA).  The m2 = 16 bw columns (bw = ceil(m/16),
+// zero padded: a zero column never rotates with a real one) form 16 blocks;
+// CTA q of the 8-CTA cluster holds one block pair (top, bottom) = 2 bw full
+// columns of A in shared memory, and the pairs follow the round-robin
+// tournament over blocks (15 block steps per sweep).  A block step:
+//   1. the own 2bw x 2bw diagonal block S = A[R_q, R_q] gets one parallel
+//      cyclic Jacobi sweep (k_jacobi's rotation formulas, threshold and
+//      exact zeros), accumulating J_q (S' = J_q^T S J_q);  cluster barrier;
+//   2. A <- J^T A J with J = blockdiag(J_0 .. J_7): every CTA updates its own
+//      columns (A[:, own] J_q, then rows R_p by J_p^T for every pair p, J_p
+//      read over DSMEM; its own diagonal block becomes S' exactly), and the
+//      eigenvector columns V[:, own] J_q in global memory;  cluster barrier;
+//   3. the blocks move to their next pair (pulled from the neighbours'
+//      buffers into the other half of a double buffer).
+// Two cluster barriers per block step instead of two per rotation step, so
+// a sweep costs 30 cluster barriers instead of 2 (m2 - 1).  Convergence:
+// k_jacobi's direct test on every off-diagonal entry after each sweep.
+// Same eigenproblem, same rotation formulas: the eigenvectors agree with the
+// oracle's orc_jacobi_eig to rounding on separated eigenvalues (P3).
+// ---------------------------------------------------------------------------
+constexpr int kJbThreads = 256;
+constexpr int kJbCs = 8;
+constexpr int kJbNblk = 2 * kJbCs;
+constexpr int kJbMaxBw = 16;
+constexpr int kJbMaxS = 2 * kJbMaxBw;
+
+__device__ long long g_jb_prof[8];
+struct JbShared {
+  double S[kJbMaxS][kJbMaxS + 1];
+  double J[kJbMaxS][kJbMaxS + 1];
+  double c[kJbMaxBw], s[kJbMaxBw], t[kJbMaxBw];
+  int P[kJbMaxBw], Q[kJbMaxBw];
+  double diag[kJbNblk * kJbMaxBw];
+  int top[kJbCs], bot[kJbCs];
+  int hot;
+  double fro2;
+  double red[33];
+};
+
+__global__ void __launch_bounds__(kJbThreads, 1)
+    k_jacobi_blk(int m, const double* __restrict__ Aall, double* Vg_all, double* Vall,
+                 double* wall, int* flags) {
+  extern __shared__ double dyn[];
+  __shared__ JbShared sh;
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int b = blockIdx.x / kJbCs;
+  constexpr int bw = kJbMaxBw, m2 = kJbNblk * bw, n2 = 2 * bw, h2 = bw;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  // A column buffers: [phase][slot][bw][m2]; slot 0 = top block, 1 = bottom
+  auto Acol = [&](int ph, int j) {  // local column j < n2 of phase ph
+    return dyn + ((size_t)(ph * 2 + (j >= bw)) * bw + (j >= bw ? j - bw : j)) * m2;
+  };
+  double* Vg = Vg_all + (size_t)b * m2 * m2;  // V(r, c) = Vg[c m2 + r]
+  const double* Ain = Aall + (size_t)b * m * m;
+  if (tid < kJbCs) {
+    sh.top[tid] = 2 * tid;
+    sh.bot[tid] = 2 * tid + 1;
+  }
+  if (tid == 0) {
+    sh.fro2 = 0.0;
+    sh.hot = 0;
+  }
+  __syncthreads();
+  auto lcol = [&](int pair, int j) {  // logical column of local index j of a pair
+    return j < bw ? sh.top[pair] * bw + j : sh.bot[pair] * bw + j - bw;
+  };
+  double part = 0.0;
+  for (int t = tid; t < n2 * m2; t += NT) {
+    const int j = t / m2, r = t % m2, c = lcol(q, j);
+    const double v = (r < m && c < m) ? Ain[(size_t)c * m + r] : 0.0;
+    Acol(0, j)[r] = v;
+    Vg[(size_t)c * m2 + r] = (r == c) ? 1.0 : 0.0;
+    part += v * v;
+  }
+  part = block_sum(part, sh.red);
+  cluster_sync_all();
+  if (tid == 0)
+    for (int r = 0; r < kJbCs; ++r) atomicAdd(&cl.map_shared_rank(&sh, r)->fro2, part);
+  cluster_sync_all();
+  const double abs_thresh = sqrt(sh.fro2) * 1e-22 + DBL_MIN;
+  // inner 2x2-block tasks (a <= b over the h2 pairs), one or two per thread
+  const int ntri = h2 * (h2 + 1) / 2;
+  int ta[2], tb[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int t = tid + k * NT;
+    int a = 0, off = 0;
+    if (t < ntri)
+      while (off + (h2 - a) <= t) {
+        off += h2 - a;
+        ++a;
+      }
+    ta[k] = t < ntri ? a : -1;
+    tb[k] = t < ntri ? a + (t - off) : 0;
+  }
+  int ph = 0;
+  bool converged = false;
+  int sweep = 0;
+  for (; sweep < 60 && !converged; ++sweep) {
+    for (int bstep = 0; bstep < kJbNblk - 1; ++bstep) {
+      long long tp0 = clock64();
+      // ---- 1. inner sweep on S = A[R_q, R_q] ----
+      for (int t = tid; t < n2 * n2; t += NT) {
+        const int i = t % n2, j = t / n2;
+        sh.S[i][j] = Acol(ph, j)[lcol(q, i)];
+        sh.J[i][j] = (i == j) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      const int rr = n2 - 1;
+      for (int st = 0; st < rr; ++st) {
+        int on = 0;
+        if (tid < h2) {
+          const int i = tid;
+          int x, y;
+          if (i == 0) {
+            x = 0;
+            y = st + rr - 1;
+            if (y >= rr) y -= rr;
+            ++y;
+          } else {
+            x = i + st - 1;
+            if (x >= rr) x -= rr;
+            ++x;
+            y = rr - i + st - 1;
+            if (y >= rr) y -= rr;
+            ++y;
+          }
+          const int p = x < y ? x : y, qq = x < y ? y : x;
+          sh.P[i] = p;
+          sh.Q[i] = qq;
+          const double app = sh.S[p][p], aqq = sh.S[qq][qq], apq = sh.S[qq][p];
+          const double rel2 = c_jac_rel2 * fabs(app) * fabs(aqq);
+          double c = 1.0, sv = 0.0, tt = 0.0;
+          if (apq * apq > rel2 && fabs(apq) > abs_thresh) {
+            const double theta = (aqq - app) * (0.5 * __drcp_rn(apq));
+            const double at = fabs(theta);
+            if (at > 1e150)
+              tt = 0.5 * __drcp_rn(theta);
+            else
+              tt = (theta >= 0.0 ? 1.0 : -1.0) * __drcp_rn(at + sqrt(fma(theta, theta, 1.0)));
+            c = rsqrt(fma(tt, tt, 1.0));
+            sv = tt * c;
+            on = 1;
+          }
+          sh.c[i] = c;
+          sh.s[i] = sv;
+          sh.t[i] = tt;
+        }
+        if (!__syncthreads_or(on)) continue;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int a = ta[k], bb = tb[k];
+          if (a < 0) continue;
+          const int p1 = sh.P[a], q1 = sh.Q[a];
+          if (a == bb) {
+            const double t = sh.t[a];
+            if (t != 0.0) {
+              const double apq = sh.S[q1][p1];
+              sh.S[p1][p1] = sh.S[p1][p1] - t * apq;
+              sh.S[q1][q1] = sh.S[q1][q1] + t * apq;
+              sh.S[q1][p1] = 0.0;
+              sh.S[p1][q1] = 0.0;
+            }
+            continue;
+          }
+          const double sa = sh.s[a], sb = sh.s[bb];
+          if (sa == 0.0 && sb == 0.0) continue;
+          const int p2 = sh.P[bb], q2 = sh.Q[bb];
+          const double ca = sh.c[a], cb = sh.c[bb];
+          const double b00 = sh.S[p1][p2], b01 = sh.S[p1][q2];
+          const double b10 = sh.S[q1][p2], b11 = sh.S[q1][q2];
+          const double r00 = ca * b00 - sa * b10, r01 = ca * b01 - sa * b11;
+          const double r10 = sa * b00 + ca * b10, r11 = sa * b01 + ca * b11;
+          const double n00 = cb * r00 - sb * r01, n01 = sb * r00 + cb * r01;
+          const double n10 = cb * r10 - sb * r11, n11 = sb * r10 + cb * r11;
+          sh.S[p1][p2] = n00;
+          sh.S[p2][p1] = n00;
+          sh.S[p1][q2] = n01;
+          sh.S[q2][p1] = n01;
+          sh.S[q1][p2] = n10;
+          sh.S[p2][q1] = n10;
+          sh.S[q1][q2] = n11;
+          sh.S[q2][q1] = n11;
+        }
+        for (int t = tid; t < h2 * n2; t += NT) {  // J <- J G (columns p, q)
+          const int a = t / n2, r = t % n2;
+          const double sa = sh.s[a];
+          if (sa == 0.0) continue;
+          const double ca = sh.c[a];
+          const int p = sh.P[a], qq = sh.Q[a];
+          const double x = sh.J[r][p], y = sh.J[r][qq];
+          sh.J[r][p] = ca * x - sa * y;
+          sh.J[r][qq] = sa * x + ca * y;
+        }
+        __syncthreads();
+      }
+      long long tp1 = clock64();
+      cluster_sync_all();  // every J_p published
+      long long tp2 = clock64();
+      // ---- 2a. own columns: A[:, own] <- A[:, own] J_q ; V likewise ----
+      for (int r = tid; r < 2 * m2; r += NT) {
+        const bool isv = r >= m2;
+        const int rr2 = isv ? r - m2 : r;
+        double a[n2];
+#pragma unroll
+        for (int j = 0; j < n2; ++j)
+          a[j] = isv ? Vg[(size_t)lcol(q, j) * m2 + rr2] : Acol(ph, j)[rr2];
+#pragma unroll
+        for (int c0 = 0; c0 < n2; c0 += 8) {
+          double o[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < n2; ++j) acc = fma(a[j], sh.J[j][c0 + c], acc);
+            o[c] = acc;
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (isv)
+              Vg[(size_t)lcol(q, c0 + c) * m2 + rr2] = o[c];
+            else
+              Acol(ph, c0 + c)[rr2] = o[c];
+          }
+        }
+      }
+      __syncthreads();
+      long long tp3 = clock64();
+      // ---- 2b. rows R_p of the own columns <- J_p^T (every pair p) ----
+      {
+        // stage every other pair's J (DSMEM) at once: one barrier, not one per pair
+        typedef double JT[kJbMaxS][kJbMaxS + 1];
+        JT* Js = reinterpret_cast<JT*>(dyn + (size_t)4 * bw * m2);
+        for (int t = tid; t < kJbCs * n2 * n2; t += NT) {
+          const int pp = t / (n2 * n2), e = t % (n2 * n2), i = e % n2, j = e / n2;
+          if (pp != q) Js[pp][i][j] = cl.map_shared_rank(&sh, pp)->J[i][j];
+        }
+        __syncthreads();
+        // thread: (pair, column j, rows i = i0 + 8 u): all reads of a
+        // column's pair rows precede its writes (the 8 threads of a
+        // (pair, column) are consecutive lanes; __syncwarp between)
+        for (int t = tid; t < kJbCs * n2 * 8; t += NT) {
+          const int pp = t / (n2 * 8), j = (t >> 3) % n2, i0 = t & 7;
+          double* col = Acol(ph, j);
+          if (pp == q) {  // own diagonal block: the inner result, exactly
+#pragma unroll
+            for (int u = 0; u < n2 / 8; ++u) col[lcol(q, i0 + 8 * u)] = sh.S[i0 + 8 * u][j];
+            continue;
+          }
+          double a[n2];
+#pragma unroll
+          for (int k = 0; k < n2; ++k) a[k] = col[lcol(pp, k)];
+          double o4[n2 / 8];
+#pragma unroll
+          for (int u = 0; u < n2 / 8; ++u) {
+            const int i = i0 + 8 * u;
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < n2; ++k) acc = fma(Js[pp][k][i], a[k], acc);
+            o4[u] = acc;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < n2 / 8; ++u) col[lcol(pp, i0 + 8 * u)] = o4[u];
+        }
+        __syncthreads();
+      }
+      long long tp4 = clock64();
+      cluster_sync_all();  // every update done, every J read
+      long long tp5 = clock64();
+      // ---- 3. tournament: pull the next pair into the other phase ----
+      {
+        const int nph = ph ^ 1;
+        // new top: q == 0 keeps its top; q == 1 takes pair 0's bottom;
+        // q >= 2 takes pair q-1's top.  New bottom: q < 7 takes pair q+1's
+        // bottom; q == 7 takes its own top.
+        const int st_rank = q == 0 ? 0 : (q == 1 ? 0 : q - 1), st_slot = q == 1 ? 1 : 0;
+        const int sb_rank = q < kJbCs - 1 ? q + 1 : q, sb_slot = q < kJbCs - 1 ? 1 : 0;
+        const double* srct =
+            cl.map_shared_rank(dyn, st_rank) + ((size_t)(ph * 2 + st_slot) * bw) * m2;
+        const double* srcb =
+            cl.map_shared_rank(dyn, sb_rank) + ((size_t)(ph * 2 + sb_slot) * bw) * m2;
+        double* dstt = dyn + ((size_t)(nph * 2 + 0) * bw) * m2;
+        double* dstb = dyn + ((size_t)(nph * 2 + 1) * bw) * m2;
+        const int tot = bw * m2;
+        for (int t0 = tid; t0 < tot; t0 += 8 * NT) {
+          double vt[8], vb[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int t = t0 + u * NT;
+            vt[u] = t < tot ? srct[t] : 0.0;
+            vb[u] = t < tot ? srcb[t] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int t = t0 + u * NT;
+            if (t < tot) {
+              dstt[t] = vt[u];
+              dstb[t] = vb[u];
+            }
+          }
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int nt[kJbCs], nb[kJbCs];
+          for (int i = 0; i < kJbCs; ++i) {
+            nt[i] = i == 0 ? sh.top[0] : (i == 1 ? sh.bot[0] : sh.top[i - 1]);
+            nb[i] = i < kJbCs - 1 ? sh.bot[i + 1] : sh.top[kJbCs - 1];
+          }
+          for (int i = 0; i < kJbCs; ++i) {
+            sh.top[i] = nt[i];
+            sh.bot[i] = nb[i];
+          }
+        }
+        ph = nph;
+        __syncthreads();
+      }
+      if (tid == 0 && q == 0 && b == 2) {
+        g_jb_prof[0] += tp1 - tp0; g_jb_prof[1] += tp2 - tp1; g_jb_prof[2] += tp3 - tp2;
+        g_jb_prof[3] += tp4 - tp3; g_jb_prof[4] += tp5 - tp4; g_jb_prof[5] += clock64() - tp5;
+      }
+    }
+    // ---- convergence: k_jacobi's direct test on every off-diagonal entry ----
+    for (int j = tid; j < n2; j += NT) {
+      const int c = lcol(q, j);
+      const double d = Acol(ph, j)[c];
+      for (int r = 0; r < kJbCs; ++r) cl.map_shared_rank(&sh, r)->diag[c] = d;
+    }
+    if (tid == 0) sh.hot = 0;
+    cluster_sync_all();
+    int hot = 0;
+    for (int t = tid; t < n2 * m2; t += NT) {
+      const int j = t / m2, r = t % m2, c = lcol(q, j);
+      if (r == c) continue;
+      const double arc = Acol(ph, j)[r];
+      const double rel = c_jac_rel * sqrt(fabs(sh.diag[r]) * fabs(sh.diag[c]));
+      if (fabs(arc) > (rel > abs_thresh ? rel : abs_thresh)) hot = 1;
+    }
+    hot = __syncthreads_or(hot);
+    if (tid == 0 && hot)
+      for (int r = 0; r < kJbCs; ++r) atomicOr(&cl.map_shared_rank(&sh, r)->hot, 1);
+    cluster_sync_all();
+    converged = !sh.hot;
+    cluster_sync_all();
+  }
+  if (threadIdx.x == 0 && q == 0 && b < 8) g_jacobi_sweeps[b] = sweep;
+  double* Vo = Vall + (size_t)b * m * m;
+  double* wo = wall + (size_t)b * m;
+  for (int t = tid; t < n2 * m2; t += NT) {
+    const int j = t / m2, r = t % m2, c = lcol(q, j);
+    if (c < m && r < m) Vo[(size_t)c * m + r] = Vg[(size_t)c * m2 + r];
+    if (c < m && r == 0) wo[c] = Acol(ph, j)[c];
+  }
+  if (!converged && tid == 0 && q == 0) atomicOr(flags, 1);
+}
+
 __device__ long long g_oic_prof[64 * 8];  // per-CTA cycle split of k_oi_cluster (DMCG_DEBUG)
 
 template <int MAXR, int B>
@@ -1852,6 +2211,44 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
     // A does not fit one CTA: the cluster kernel (columns of A and V spread
     // over the cluster), else the global-memory fallback.
     static const bool legacy = getenv("DMCG_JACOBI_LEGACY") != nullptr;
+    static const bool cols = getenv("DMCG_JACOBI_COLS") != nullptr;  // the rotation-step cluster kernel
+    if (!legacy && !cols && m <= kJbNblk * kJbMaxBw) {
+      const int bw = kJbMaxBw;  // zero padded to 256 (padding never rotates)
+      const int mb2 = kJbNblk * bw;
+      const size_t smem =
+          ((size_t)4 * bw * mb2 + (size_t)kJbCs * kJbMaxS * (kJbMaxS + 1)) * sizeof(double);
+      const void* fn = (const void*)k_jacobi_blk;
+      if (smem <= smem_room(fn) && set_smem_attr(fn, smem) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kJbCs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(nbatch * kJbCs);
+        cfg.blockDim = dim3(kJbThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // V accumulates in work (nbatch x mb2 x mb2 doubles: the caller's
+        // jacobi scratch holds 2 m2 (m2 + 1) per batch)
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_jacobi_blk, m, A, work, V, w, flags);
+        static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
+        if (dbg && e == cudaSuccess) {
+          int sw[8] = {};
+          cudaStreamSynchronize(s);
+          cudaMemcpyFromSymbol(sw, g_jacobi_sweeps, sizeof(sw));
+          fprintf(stderr, "dmcg: k_jacobi_blk m=%d bw %d sweeps %d %d %d\n", m, bw, sw[0], sw[1], sw[2]);
+          long long pr[8];
+          cudaMemcpyFromSymbol(pr, g_jb_prof, sizeof(pr));
+          fprintf(stderr, "  blk prof (cycles, cumulative): inner %lld bar1 %lld 2a %lld 2b %lld bar2 %lld pull %lld\n",
+                  pr[0], pr[1], pr[2], pr[3], pr[4], pr[5]);
+        }
+        return e;
+      }
+      cudaGetLastError();
+    }
     const int h = m2 / 2;
     int cs = 0;
     for (int c = 8; c >= 2 && !legacy; c /= 2)

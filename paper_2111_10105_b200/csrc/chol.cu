@@ -393,47 +393,109 @@ __global__ void __launch_bounds__(kGemmThreads) k_inv_offdiag(CholDev d, const u
   }
 }
 
-// ---- solves -------------------------------------------------------------
+// ---- solve operator -----------------------------------------------------
+// P_s = [L11^{-1}; -L21 L11^{-1}] (m x w, column-major, ld = m).  With it one
+// supernode's forward step is ONE product and its backward step another:
+//   forward   [y_s; U_s] = P_s r_s + [0; pulled child updates]
+//             (y_s = L11^{-1} r_s,  U_s = R_s[w:m] - L21 y_s)
+//   backward  x_s = P_s^T [y_s; x_below]
+//             (= L11^{-T} (y_s - L21^T x_below))
+// so no per-front right-hand-side panel is materialised: r_s (own rows) is
+// gathered into the x buffer, U_s is written once by the forward epilogue
+// and read once by the parent.
 
-// R_s = [b(perm) for own columns; 0] + extend-add of the children's updates.
-// Parallel over (row chunk of 32, column tile of 64, front); each child's
-// rows landing in the chunk form a contiguous range (rel is increasing).
-__global__ void __launch_bounds__(256) k_solve_gather(CholDev d, const uint32_t* lsup,
-                                                      const double* __restrict__ b) {
-  // R_s = [P b rows of s; 0] + sum of the children's update rows, in the
-  // pull form of the extend-add (CholPlan::pull_*): every element is formed
-  // independently, children in a fixed order (deterministic), no barriers.
-  const uint32_t s = lsup[blockIdx.z];
-  const int W = (int)d.W;
-  const int c0 = blockIdx.y * 64;
-  const int cw = min(64, W - c0);
-  const uint32_t m = front_m(d, s), w = front_w(d, s), f0 = d.first[s];
-  const uint32_t r0 = blockIdx.x * 32;
-  if (r0 >= m) return;
-  const uint32_t r1 = min(m, r0 + 32);
-  const unsigned long long g0 = d.rhs_off[s];
-  for (long t = threadIdx.x; t < (long)(r1 - r0) * cw; t += blockDim.x) {
-    const uint32_t r = r0 + (uint32_t)(t / cw);
-    const int c = c0 + (int)(t % cw);
-    const size_t g = g0 + r;
-    double v = r < w ? b[(size_t)d.perm[f0 + r] * W + c] : 0.0;
-    const uint32_t e0 = d.pull_ptr[g], e1 = d.pull_ptr[g + 1];
-    for (uint32_t e = e0; e < e1; ++e) v += d.R[(size_t)d.pull_src[e] * W + c];
-    d.R[g * W + c] = v;
+// Top block: P[j m + i] = Linv[i w + j] (lower triangle, zeros above).
+__global__ void __launch_bounds__(256) k_form_p_top(CholDev d, const uint32_t* lsup) {
+  const uint32_t s = lsup[blockIdx.y];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s);
+  const double* V = d.Linv + d.inv_off[s];
+  double* P = d.P + d.op_off[s];
+  // one 32 x 32 tile per CTA through shared memory (coalesced both ways)
+  __shared__ double t[32][33];
+  const int tiles = (w + 31) / 32;
+  for (int tt = blockIdx.x; tt < tiles * tiles; tt += gridDim.x) {
+    const int ti = tt / tiles, tj = tt % tiles;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) {
+      const int i = ti * 32 + r, j = tj * 32 + tx;
+      t[r][tx] = (i < w && j < w) ? V[(size_t)i * w + j] : 0.0;
+    }
+    __syncthreads();
+    for (int c = ty; c < 32; c += 8) {
+      const int j = tj * 32 + c, i = ti * 32 + tx;
+      if (i < w && j < w) P[(size_t)j * m + i] = t[tx][c];
+    }
+    __syncthreads();
   }
 }
 
-struct LoadRowMajor {  // X(k, i) = p[i * ld + k]   (k contiguous)
-  static constexpr bool kKContig = true;
-  const double* p;
-  int ld;
-  __device__ __forceinline__ double operator()(int, int k, int i) const {
-    return p[(size_t)i * ld + k];
-  }
-  __device__ __forceinline__ const double* addr(int, int k, int i) const {
-    return p + (size_t)i * ld + k;
+struct StoreNegCM {  // P[(n) * ld + off + m] = -v
+  double* P;
+  int ld, off;
+  __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int r, c;
+          frag_rc(i, j, e, lane, &r, &c);
+          const int mi = mb + r, ni = nb + c;
+          if (mi < M && ni < N) P[(size_t)ni * ld + off + mi] = -wt.acc[i][j][e];
+        }
   }
 };
+
+// Bottom block: P[j m + w + i] = -(L21 L11^{-1})(i, j), K restricted to
+// k >= j0 (L11^{-1} is lower triangular).
+__global__ void __launch_bounds__(kGemmThreads) k_form_p_bot(CholDev d, const uint32_t* lsup,
+                                                             int tiles_w) {
+  const uint32_t s = lsup[blockIdx.y];
+  const int w = (int)front_w(d, s), m = (int)front_m(d, s), u = m - w;
+  const int ti = blockIdx.x / tiles_w, tj = blockIdx.x % tiles_w;
+  if (ti * kBM >= u || tj * kBN >= w) return;
+  const double* A = d.F + d.front_off[s];
+  const double* V = d.Linv + d.inv_off[s];
+  gemm_tile(0, u, w, ti * kBM, tj * kBN, tj * kBN, w, 0, LoadColMajorT{A + w, m},
+            LoadColMajorT{V, w}, StoreNegCM{d.P + d.op_off[s], m, w});
+}
+
+// ---- solves -------------------------------------------------------------
+
+// r_s (own rows of front s) = b(perm) + the children's update rows pulled
+// into them (CholPlan::pull_*: children in a fixed order, deterministic),
+// written to rows first[s] .. of the permuted buffer r.
+__global__ void __launch_bounds__(256) k_gather_own(CholDev d, const uint32_t* lsup,
+                                                    const double* __restrict__ b,
+                                                    double* __restrict__ r) {
+  const uint32_t s = lsup[blockIdx.z];
+  const int W = (int)d.W;
+  const int c0 = blockIdx.y * 128;
+  const uint32_t w = front_w(d, s), f0 = d.first[s];
+  const uint32_t r0 = blockIdx.x * 8;
+  if (r0 >= w) return;
+  const uint32_t r1 = min(w, r0 + 8);
+  const unsigned long long g0 = d.rhs_off[s];
+  const double* __restrict__ R = d.R;
+  for (uint32_t rr = r0 + (threadIdx.x >> 5); rr < r1; rr += 8) {
+    const size_t g = g0 + rr;
+    const uint32_t e0 = d.pull_ptr[g], e1 = d.pull_ptr[g + 1];
+    const double* brow = b + (size_t)d.perm[f0 + rr] * W;
+    double* out = r + (size_t)(f0 + rr) * W;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + q * 32 + (threadIdx.x & 31);
+      if (c < W) {
+        double v = brow[c];
+        for (uint32_t e = e0; e < e1; ++e) v += R[(size_t)d.pull_src[e] * W + c];
+        out[c] = v;
+      }
+    }
+  }
+}
+
 struct LoadColMajor {  // X(k, i) = p[k * ld + i]   (i contiguous)
   static constexpr bool kKContig = false;
   const double* p;
@@ -445,107 +507,180 @@ struct LoadColMajor {  // X(k, i) = p[k * ld + i]   (i contiguous)
     return p + (size_t)k * ld + i;
   }
 };
-struct LoadGatherRows {  // X(k, c) = x[rows[k] * W + c]
-  static constexpr bool kKContig = false;
-  const double* x;
-  const uint32_t* rows;
-  int W;
-  __device__ __forceinline__ double operator()(int, int k, int c) const {
-    return x[(size_t)rows[k] * W + c];
+struct LoadRowMajor {  // X(k, i) = p[i * ld + k]   (k contiguous)
+  static constexpr bool kKContig = true;
+  const double* p;
+  int ld;
+  __device__ __forceinline__ double operator()(int, int k, int i) const {
+    return p[(size_t)i * ld + k];
   }
-  __device__ __forceinline__ const double* addr(int, int k, int c) const {
-    return x + (size_t)rows[k] * W + c;
+  __device__ __forceinline__ const double* addr(int, int k, int i) const {
+    return p + (size_t)i * ld + k;
   }
 };
-// out[(row0 + i) * W + c] (=, -=, or = base - v)
-template <int MODE>
-struct StoreRows {
+// [y_s; x_below](k, c): own rows from y, the rows below from x (str_idx lists
+// the own columns first, so rows[k] = first[s] + k for k < w)
+struct LoadYX {
+  static constexpr bool kKContig = false;
+  const double* y;
+  const double* x;
+  const uint32_t* rows;
+  int w, W;
+  __device__ __forceinline__ double operator()(int, int k, int c) const {
+    return (k < w ? y : x)[(size_t)rows[k] * W + c];
+  }
+  __device__ __forceinline__ const double* addr(int, int k, int c) const {
+    return (k < w ? y : x) + (size_t)rows[k] * W + c;
+  }
+};
+
+// Forward epilogue: rows < w -> y (own rows), rows >= w -> the update rows
+// U = pulled child updates + (-L21 L11^{-1} r) in d.R.  All loads of a
+// fragment are issued before its stores.
+struct StoreFwd {
+  double* y;        // y + first[s] * W
+  double* U;        // d.R + rhs_off[s] * W
+  const double* R;  // d.R (children's update rows)
+  const uint32_t* pull_ptr;  // + rhs_off[s]
+  const uint32_t* pull_src;
+  int w, W;
+  __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
+                                             const WarpTile& wt) const {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int mi = mb + i * 8 + (lane >> 2);
+      if (mi >= M) continue;
+      if (mi < w) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ni = nb + j * 8 + (lane & 3) * 2;
+          if (ni + 1 < N && !(W & 1)) {
+            *reinterpret_cast<double2*>(y + (size_t)mi * W + ni) =
+                make_double2(wt.acc[i][j][0], wt.acc[i][j][1]);
+          } else if (ni < N) {
+            y[(size_t)mi * W + ni] = wt.acc[i][j][0];
+            if (ni + 1 < N) y[(size_t)mi * W + ni + 1] = wt.acc[i][j][1];
+          }
+        }
+      } else {
+        const uint32_t e0 = pull_ptr[mi], e1 = pull_ptr[mi + 1];
+        double v[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j][0] = v[j][1] = 0.0;
+        // two pulled rows per iteration: all eight loads in flight together
+        uint32_t e = e0;
+        for (; e + 1 < e1; e += 2) {
+          const double* s0 = R + (size_t)pull_src[e] * W;
+          const double* s1 = R + (size_t)pull_src[e + 1] * W;
+          double2 t0[4], t1[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ni = nb + j * 8 + (lane & 3) * 2;
+            t0[j] = t1[j] = make_double2(0.0, 0.0);
+            if (ni + 1 < N && !(W & 1)) {
+              t0[j] = *reinterpret_cast<const double2*>(s0 + ni);
+              t1[j] = *reinterpret_cast<const double2*>(s1 + ni);
+            } else if (ni < N) {
+              t0[j].x = s0[ni];
+              t1[j].x = s1[ni];
+              if (ni + 1 < N) {
+                t0[j].y = s0[ni + 1];
+                t1[j].y = s1[ni + 1];
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {  // children in order: ((v + c_e) + c_{e+1})
+            v[j][0] = (v[j][0] + t0[j].x) + t1[j].x;
+            v[j][1] = (v[j][1] + t0[j].y) + t1[j].y;
+          }
+        }
+        if (e < e1) {
+          const double* src = R + (size_t)pull_src[e] * W;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ni = nb + j * 8 + (lane & 3) * 2;
+            if (ni + 1 < N && !(W & 1)) {
+              const double2 t = *reinterpret_cast<const double2*>(src + ni);
+              v[j][0] += t.x;
+              v[j][1] += t.y;
+            } else if (ni < N) {
+              v[j][0] += src[ni];
+              if (ni + 1 < N) v[j][1] += src[ni + 1];
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ni = nb + j * 8 + (lane & 3) * 2;
+          double* dst = U + (size_t)mi * W + ni;
+          if (ni + 1 < N && !(W & 1)) {
+            *reinterpret_cast<double2*>(dst) =
+                make_double2(v[j][0] + wt.acc[i][j][0], v[j][1] + wt.acc[i][j][1]);
+          } else if (ni < N) {
+            dst[0] = v[j][0] + wt.acc[i][j][0];
+            if (ni + 1 < N) dst[1] = v[j][1] + wt.acc[i][j][1];
+          }
+        }
+      }
+    }
+  }
+};
+
+struct StoreRowsW {  // out[mi * W + ni] = v
   double* out;
-  const double* base;
   int W;
   __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
                                              const WarpTile& wt) const {
-    double v[4][4][2];
-    if (MODE != 0) {  // all reads before the first store (see SubLower)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i) {
+      const int mi = mb + i * 8 + (lane >> 2);
+      if (mi >= M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            int r, c;
-            frag_rc(i, j, e, lane, &r, &c);
-            const int mi = mb + r, ni = nb + c;
-            const size_t o = (size_t)mi * W + ni;
-            v[i][j][e] = (mi < M && ni < N) ? (MODE == 1 ? out[o] : base[o]) : 0.0;
-          }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          int r, c;
-          frag_rc(i, j, e, lane, &r, &c);
-          const int mi = mb + r, ni = nb + c;
-          if (mi < M && ni < N) {
-            const size_t o = (size_t)mi * W + ni;
-            out[o] = MODE == 0 ? wt.acc[i][j][e] : v[i][j][e] - wt.acc[i][j][e];
-          }
+      for (int j = 0; j < 4; ++j) {
+        const int ni = nb + j * 8 + (lane & 3) * 2;
+        if (ni + 1 < N && !(W & 1))
+          *reinterpret_cast<double2*>(out + (size_t)mi * W + ni) =
+              make_double2(wt.acc[i][j][0], wt.acc[i][j][1]);
+        else if (ni < N) {
+          out[(size_t)mi * W + ni] = wt.acc[i][j][0];
+          if (ni + 1 < N) out[(size_t)mi * W + ni + 1] = wt.acc[i][j][1];
         }
+      }
+    }
   }
 };
 
-// Forward step 1: y_s = L11^{-1} R_s[0:w]
-__global__ void __launch_bounds__(kGemmThreads) k_fwd1(CholDev d, const uint32_t* lsup, double* y) {
-  const uint32_t s = lsup[blockIdx.z];
-  const int w = (int)front_w(d, s), W = (int)d.W;
-  if ((int)blockIdx.x * kBM >= w) return;
-  const double* V = d.Linv + d.inv_off[s];
-  const double* R = d.R + d.rhs_off[s] * W;
-  gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadRowMajor{V, w},
-            LoadColMajor{R, W}, StoreRows<0>{y + (size_t)d.first[s] * W, nullptr, W});
-}
-
-// Forward step 2: R_s[w:m] -= L21 y_s
-__global__ void __launch_bounds__(kGemmThreads) k_fwd2(CholDev d, const uint32_t* lsup,
-                                                       const double* y) {
+// Forward: [y_s; U_s] = P_s r_s (+ pulls), M = m, K = w.
+__global__ void __launch_bounds__(kGemmThreads, 4) k_fwd(CholDev d, const uint32_t* lsup,
+                                                      const double* r, double* y) {
   const uint32_t s = lsup[blockIdx.z];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
-  const int u = m - w;
-  if ((int)blockIdx.x * kBM >= u) return;
-  const double* A = d.F + d.front_off[s];
-  double* R = d.R + (d.rhs_off[s] + w) * W;
-  gemm_tile(0, u, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadColMajor{A + w, m},
-            LoadColMajor{y + (size_t)d.first[s] * W, W}, StoreRows<1>{R, nullptr, W});
+  if ((int)blockIdx.x * kBM >= m) return;
+  const size_t f0 = d.first[s];
+  const unsigned long long g0 = d.rhs_off[s];
+  // rows i < w of P are L11^{-1} (lower triangular): a tile inside the top
+  // block needs k <= i only
+  const int m0 = blockIdx.x * kBM;
+  const int kend = m0 + kBM <= w ? m0 + kBM : w;
+  gemm_tile(0, m, W, m0, blockIdx.y * kBN, 0, kend, 0,
+            LoadColMajor{d.P + d.op_off[s], m}, LoadColMajor{r + f0 * W, W},
+            StoreFwd{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W});
 }
 
-// Backward step 1: t_s = y_s - L21^T x[rows below]   (t_s stored in R_s[0:w])
-__global__ void __launch_bounds__(kGemmThreads) k_bwd1(CholDev d, const uint32_t* lsup,
-                                                       const double* y, const double* x) {
+// Backward: x_s = P_s^T [y_s; x_below], M = w, K = m.
+__global__ void __launch_bounds__(kGemmThreads, 4) k_bwd(CholDev d, const uint32_t* lsup,
+                                                      const double* y, double* x) {
   const uint32_t s = lsup[blockIdx.z];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
   if ((int)blockIdx.x * kBM >= w) return;
-  const double* A = d.F + d.front_off[s];
-  double* T = d.R + d.rhs_off[s] * W;
-  const uint32_t* rows = d.str_idx + d.str_ptr[s] + w;
-  gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, m - w, 0, LoadRowMajor{A + w, m},
-            LoadGatherRows{x, rows, W},
-            StoreRows<2>{T, y + (size_t)d.first[s] * W, W});
+  const uint32_t* rows = d.str_idx + d.str_ptr[s];
+  // P^T's top block is L11^{-T} (upper triangular): row i needs k >= i
+  const int m0 = blockIdx.x * kBM;
+  gemm_tile(0, w, W, m0, blockIdx.y * kBN, m0, m, 0,
+            LoadRowMajor{d.P + d.op_off[s], m}, LoadYX{y, x, rows, w, W},
+            StoreRowsW{x + (size_t)d.first[s] * W, W});
 }
-
-// Backward step 2: x_s = L11^{-T} t_s
-__global__ void __launch_bounds__(kGemmThreads) k_bwd2(CholDev d, const uint32_t* lsup, double* x) {
-  const uint32_t s = lsup[blockIdx.z];
-  const int w = (int)front_w(d, s), W = (int)d.W;
-  if ((int)blockIdx.x * kBM >= w) return;
-  const double* V = d.Linv + d.inv_off[s];
-  const double* T = d.R + d.rhs_off[s] * W;
-  gemm_tile(0, w, W, blockIdx.x * kBM, blockIdx.y * kBN, 0, w, 0, LoadColMajor{V, w},
-            LoadColMajor{T, W}, StoreRows<0>{x + (size_t)d.first[s] * W, nullptr, W});
-}
-
 
 // out[perm[j]] (+)= x[j]
 __global__ void k_unpermute(int n, int W, const uint32_t* perm, const double* __restrict__ xp,
@@ -689,6 +824,14 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
     const uint32_t nbk = (lv.maxw[l] + kIB - 1) / kIB;
     k_inv_diag<<<dim3(nbk, cnt), kIB, kInvDiagSmem, s>>>(d, ls);
     if (nbk > 1) k_inv_offdiag<<<dim3(nbk, cnt), kGemmThreads, 0, s>>>(d, ls, d.scratch);
+    {
+      const uint32_t tw = (lv.maxw[l] + 31) / 32;
+      k_form_p_top<<<dim3(std::min<uint32_t>(tw * tw, 64), cnt), 256, 0, s>>>(d, ls);
+      if (lv.maxu[l] > 0) {
+        const uint32_t tiles_w = (lv.maxw[l] + kBN - 1) / kBN, tiles_u = (lv.maxu[l] + kBM - 1) / kBM;
+        k_form_p_bot<<<dim3(tiles_u * tiles_w, cnt), kGemmThreads, 0, s>>>(d, ls, (int)tiles_w);
+      }
+    }
     lt.mark(l, 3);
   }
   lt.report(lv, "assemble", "panels", "inverse");
@@ -709,26 +852,26 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
   const int W = (int)d.W;
   const unsigned tn = (unsigned)((W + kBN - 1) / kBN);
   LevelTimer lt(s, "solve", lv.nlevels);
+  // forward, leaves first: r_s -> x rows (scratch until the backward pass
+  // overwrites them), [y_s; U_s] = P_s r_s
   for (uint32_t l = 0; l < lv.nlevels; ++l) {
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 0);
-    k_solve_gather<<<dim3((lv.maxm[l] + 31) / 32, (W + 63) / 64, cnt), 256, 0, s>>>(d, ls, b);
-    k_fwd1<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y);
+    k_gather_own<<<dim3((lv.maxw[l] + 7) / 8, (W + 127) / 128, cnt), 256, 0, s>>>(d, ls, b, x);
     lt.mark(l, 1);
-    if (lv.maxu[l] > 0)
-      k_fwd2<<<dim3((lv.maxu[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y);
+    k_fwd<<<dim3((lv.maxm[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x, y);
     lt.mark(l, 2);
   }
+  // backward, roots first: x_s = P_s^T [y_s; x_below]
   for (int l = (int)lv.nlevels - 1; l >= 0; --l) {
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 3);
-    k_bwd1<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x);
-    k_bwd2<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x);
+    k_bwd<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x);
     lt.mark(l, 4);
   }
-  lt.report(lv, "gather+fwd1", "fwd2", "bwd", true);
+  lt.report(lv, "gather", "fwd", "bwd", true);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ struct CholPlan {
   std::vector<uint64_t> front_off;        // nsup + 1, m_s^2 doubles each
   std::vector<uint64_t> inv_off;          // nsup + 1, w_s^2 doubles each
   std::vector<uint64_t> rhs_off;          // nsup + 1, m_s rows each (times W columns)
+  std::vector<uint64_t> op_off;           // nsup + 1, m_s x w_s doubles each (solve operator P_s)
   std::vector<uint64_t> rel_ptr;          // nsup + 1 (indexed by child)
   std::vector<uint32_t> rel_idx;          // child update row -> local row in the parent
   // "pull" form of the extend-add for the solves: front row g (global

@@ -22,6 +22,7 @@ struct CholDev {
   const unsigned long long* front_off = nullptr;
   const unsigned long long* inv_off = nullptr;
   const unsigned long long* rhs_off = nullptr;
+  const unsigned long long* op_off = nullptr;
   const uint32_t* perm = nullptr;
   const uint32_t* level_sup = nullptr;
   const uint32_t* level_ptr = nullptr;  // nlevels + 1 offsets into level_sup
@@ -30,7 +31,8 @@ struct CholDev {
   uint32_t nlevels = 0;
   double* F = nullptr;     // fronts (factor in place)
   double* Linv = nullptr;  // L11^{-1}, row-major per front
-  double* R = nullptr;     // per-front right-hand-side buffers (m_s x W)
+  double* P = nullptr;     // solve operators [L11^{-1}; -L21 L11^{-1}], m_s x w_s column-major
+  double* R = nullptr;     // per-front update rows (rows w_s .. m_s of an m_s x W panel)
   double* scratch = nullptr;  // blocked-inverse tiles (chol_scratch_doubles)
   unsigned long long linv_doubles = 0;
   int* flags = nullptr;    // [0] non-positive pivot

@@ -528,6 +528,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   p.front_off.assign(NS + 1, 0);
   p.inv_off.assign(NS + 1, 0);
   p.rhs_off.assign(NS + 1, 0);
+  p.op_off.assign(NS + 1, 0);
   p.nnz_l = 0;
   p.flops_factor = 0;
   p.flops_solve_per_rhs = 0;
@@ -536,13 +537,15 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     p.front_off[s + 1] = p.front_off[s] + m * m;
     p.inv_off[s + 1] = p.inv_off[s] + w * w;
     p.rhs_off[s + 1] = p.rhs_off[s] + m;
+    p.op_off[s + 1] = p.op_off[s] + m * w;
     p.nnz_l += w * m - w * (w - 1) / 2;
     p.max_front = std::max<uint32_t>(p.max_front, (uint32_t)m);
     p.max_width = std::max<uint32_t>(p.max_width, (uint32_t)w);
     // partial Cholesky: sum over pivots t of (m-t)^2 ; L11 inverse w^3/3
     for (uint64_t t = 0; t < w; ++t) p.flops_factor += (double)(m - t) * (m - t);
     p.flops_factor += (double)w * w * w / 3.0;
-    p.flops_solve_per_rhs += 2.0 * (2.0 * w * w + 2.0 * 2.0 * w * (m - w));
+    // one solve = forward [L11^{-1}; -L21 L11^{-1}] r (m x w) + backward (w x m)
+    p.flops_solve_per_rhs += 4.0 * (double)m * w;
   }
   lap("levels+stats");
   // (8) extend-add maps: child update rows -> parent local rows

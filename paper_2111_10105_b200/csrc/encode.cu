@@ -3,6 +3,8 @@
 // reference Release build has no FMA contraction (CMakeLists.txt:7-9).
 #include <cfloat>
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -56,6 +58,111 @@ __global__ void __launch_bounds__(kDeltaWarps * 32)
     for (int c = 0; c < kDeltaChunk; ++c) {
       const int f = f0 + c * 32 + lane;
       if (f < F) out[f] = acc[c];
+    }
+  }
+  if (bad) atomicOr(flags, 1 << a);
+}
+
+// K1, vectorised (the default when every row starts 16-byte aligned): one
+// warp per vertex row, each lane 16-byte loads of VEC consecutive frames,
+// CH chunks per pass (f32: 512 frames, f64: 256 frames per pass); the row's
+// neighbour indices are loaded once (lane t holds entry t) and broadcast by
+// shuffles, and neighbour p + 1's loads are issued before neighbour p's
+// adds, so two rows' worth of loads are in flight per warp.  The additions
+// run in the CSR order with _rn intrinsics, as k_delta (bit-identical).
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using V = float4;
+  static constexpr int N = 4;
+  __device__ static void get(const V& v, double* o) {
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+};
+template <>
+struct Vec16<double> {
+  using V = double2;
+  static constexpr int N = 2;
+  __device__ static void get(const V& v, double* o) {
+    o[0] = v.x; o[1] = v.y;
+  }
+};
+
+constexpr int kDeltaVecCh = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(kDeltaWarps * 32)
+    k_delta_vec(int n, int F, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
+                const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2,
+                double* __restrict__ delta, int* flags) {
+  using VT = Vec16<T>;
+  using V = typename VT::V;
+  constexpr int VEC = VT::N, CH = kDeltaVecCh, PASS = 32 * VEC * CH;
+  const int a = blockIdx.y;
+  const T* __restrict__ X = a == 0 ? x0 : (a == 1 ? x1 : x2);
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * kDeltaWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const uint32_t pb = rp[i], pe = rp[i + 1];
+  const int cnt = (int)(pe - pb);
+  const double deg = (double)(cnt - 1);
+  const uint32_t my_ci = lane < cnt ? ci[pb + lane] : 0u;
+  double* out = delta + ((size_t)a * n + i) * F;
+  bool bad = false;
+  const int nv = F / VEC;  // vectors per row
+  for (int f0 = 0; f0 < F; f0 += PASS) {
+    const int v0 = f0 / VEC;
+    double acc[CH * VEC];
+#pragma unroll
+    for (int c = 0; c < CH * VEC; ++c) acc[c] = 0.0;
+    auto col = [&](int p) -> uint32_t {
+      return p < 32 ? __shfl_sync(0xffffffffu, my_ci, p) : ci[pb + p];
+    };
+    V nxt[CH];
+    uint32_t jn = col(0);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int v = v0 + c * 32 + lane;
+      if (v < nv) nxt[c] = reinterpret_cast<const V*>(X + (size_t)jn * F)[v];
+    }
+    for (int p = 0; p < cnt; ++p) {
+      V cur[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
+      const uint32_t j = jn;
+      if (p + 1 < cnt) {
+        jn = col(p + 1);
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int v = v0 + c * 32 + lane;
+          if (v < nv) nxt[c] = reinterpret_cast<const V*>(X + (size_t)jn * F)[v];
+        }
+      }
+      const double w = (j == (uint32_t)i) ? deg : -1.0;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int v = v0 + c * 32 + lane;
+        if (v < nv) {
+          double xv[VEC];
+          VT::get(cur[c], xv);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            if (j == (uint32_t)i && !isfinite(xv[e])) bad = true;
+            acc[c * VEC + e] = __dadd_rn(acc[c * VEC + e], __dmul_rn(w, xv[e]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int v = v0 + c * 32 + lane;
+      if (v < nv) {
+        double* o = out + (size_t)v * VEC;
+#pragma unroll
+        for (int e = 0; e < VEC; e += 2)
+          *reinterpret_cast<double2*>(o + e) = make_double2(acc[c * VEC + e], acc[c * VEC + e + 1]);
+      }
     }
   }
   if (bad) atomicOr(flags, 1 << a);
@@ -263,6 +370,21 @@ cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
                          const uint32_t* lap_ci, const void* const x[3], bool f32, double* delta,
                          int* flags) {
   dim3 grid((n + kDeltaWarps - 1) / kDeltaWarps, 3);
+  const size_t esz = f32 ? 4 : 8;
+  bool vec = (F * esz) % 16 == 0;  // every row 16-byte aligned
+  for (int a = 0; a < 3; ++a) vec = vec && ((uintptr_t)x[a] % 16 == 0);
+  static const bool scalar = getenv("DMCG_DELTA_SCALAR") != nullptr;  // tests
+  if (vec && !scalar) {
+    if (f32)
+      k_delta_vec<float><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const float*)x[0],
+                                                           (const float*)x[1], (const float*)x[2],
+                                                           delta, flags);
+    else
+      k_delta_vec<double><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const double*)x[0],
+                                                            (const double*)x[1], (const double*)x[2],
+                                                            delta, flags);
+    return cudaGetLastError();
+  }
   if (f32)
     k_delta<float><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const float*)x[0],
                                                      (const float*)x[1], (const float*)x[2],

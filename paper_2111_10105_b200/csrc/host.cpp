@@ -647,9 +647,37 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->part_elems = splits * 3 * FF;
   p->d_part = (double*)get(p->part_elems * 8);
   if (p->oz_slices) {
-    const size_t fp = dmcg::oz_rows_pad((int)F), kp = dmcg::oz_k_pad((int)n);
-    p->d_oz_q = (int8_t*)get(3 * (size_t)p->oz_slices * fp * kp);
-    p->d_oz_max = (unsigned long long*)get(3 * fp * 8);
+    // one slice buffer for the three Ozaki contractions of the plan (they
+    // run one after another on the plan stream): the Gram (X^T X), the
+    // projection (U_k^T, delta rows) and the decode's reconstruction (c~
+    // rows, U~ rows); projection and reconstruction need K <= kOzKChunk
+    using dmcg::oz_slice_bytes;
+    using dmcg::oz_rows_pad;
+    auto env_s = [](const char* name, int dflt) {
+      const char* e = getenv(name);
+      return e ? std::max(3, std::min(7, atoi(e))) : dflt;
+    };
+    const bool kfit = k > 0 && dmcg::oz_k_pad((int)F) <= dmcg::kOzKChunk &&
+                      dmcg::oz_k_pad((int)k) <= dmcg::kOzKChunk;
+    p->oz_proj_slices = (kfit && variant_uses_delta(p->variant)) ? env_s("DMCG_OZ_PROJ_SLICES", 6) : 0;
+    p->oz_rec_slices = kfit ? env_s("DMCG_OZ_REC_SLICES", 5) : 0;
+    if (getenv("DMCG_NO_OZAKI_GEMMS")) p->oz_proj_slices = p->oz_rec_slices = 0;
+    size_t qb = oz_slice_bytes((int)F, (int)n, p->oz_slices, 3);
+    size_t mx = 3 * (size_t)oz_rows_pad((int)F);
+    if (p->oz_proj_slices) {
+      const int sp = p->oz_proj_slices;
+      qb = std::max(qb, oz_slice_bytes((int)k, (int)F, sp, 3) + oz_slice_bytes((int)n, (int)F, sp, 3));
+      mx = std::max(mx, 3 * (size_t)(oz_rows_pad((int)k) + oz_rows_pad((int)n)));
+    }
+    if (p->oz_rec_slices) {
+      const int sr = p->oz_rec_slices;
+      qb = std::max(qb, oz_slice_bytes((int)n, (int)k, sr, 3) + oz_slice_bytes((int)F, (int)k, sr, 3));
+      mx = std::max(mx, 3 * (size_t)(oz_rows_pad((int)n) + oz_rows_pad((int)F)));
+    }
+    p->oz_q_bytes = qb;
+    p->oz_max_elems = mx;
+    p->d_oz_q = (int8_t*)get(qb);
+    p->d_oz_max = (unsigned long long*)get(mx * 8);
   }
   p->d_U = (double*)get(3 * FF * 8);
   p->d_evals = (double*)get(3 * (size_t)F * 8);
@@ -661,6 +689,9 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     const size_t kf2 = p->kf + (p->kf & 1);
     jac = std::max(jac, 3 * (size_t)p->nb * 2 * kf2 * (kf2 + 1));
   }
+  // k_jacobi_blk keeps the eigenvectors of each (zero padded) 256 x 256
+  // problem in this scratch
+  jac = std::max(jac, 3 * (size_t)std::max<uint32_t>(p->nb, 1) * dmcg::kJacobiBlkWork);
   p->d_H = (double*)get(jac * 8);
   p->d_V = (double*)get(3 * FF * 8);
   p->d_qr_scr = (double*)get(3 * dmcg::qr_scratch_doubles((int)F, (int)kk) * 8);
@@ -828,6 +859,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   cd.front_off = (const unsigned long long*)get(cp.front_off.size() * 8);
   cd.inv_off = (const unsigned long long*)get(cp.inv_off.size() * 8);
   cd.rhs_off = (const unsigned long long*)get(cp.rhs_off.size() * 8);
+  cd.op_off = (const unsigned long long*)get(cp.op_off.size() * 8);
   cd.perm = (const uint32_t*)get(cp.perm.size() * 4);
   cd.level_sup = (const uint32_t*)get(cp.level_sup.size() * 4 + 4);
   cd.level_ptr = (const uint32_t*)get(cp.level_ptr.size() * 4 + 4);
@@ -836,6 +868,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   cd.nlevels = cp.nlevels;
   cd.F = (double*)get(cp.front_off[cp.nsup] * 8);
   cd.Linv = (double*)get(cp.inv_off[cp.nsup] * 8 + 8);
+  cd.P = (double*)get(cp.op_off[cp.nsup] * 8 + 8);
   cd.R = (double*)get(cp.rhs_off[cp.nsup] * p->W * 8);
   cd.flags = p->d_flags + 4;
   CholLevels& lv = p->levels;
@@ -881,6 +914,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   h2d((void*)cd.front_off, cp.front_off.data(), cp.front_off.size() * 8);
   h2d((void*)cd.inv_off, cp.inv_off.data(), cp.inv_off.size() * 8);
   h2d((void*)cd.rhs_off, cp.rhs_off.data(), cp.rhs_off.size() * 8);
+  h2d((void*)cd.op_off, cp.op_off.data(), cp.op_off.size() * 8);
   h2d((void*)cd.perm, cp.perm.data(), cp.perm.size() * 4);
   h2d((void*)cd.level_sup, cp.level_sup.data(), cp.level_sup.size() * 4);
   h2d((void*)cd.level_ptr, cp.level_ptr.data(), cp.level_ptr.size() * 4);
@@ -1244,6 +1278,16 @@ int dmcg_plan_upload(dmcg_plan* p, const dmcg_encoded* in) {
   return p->ctx->set_error(upload_impl(p, in));
 }
 
+int dmcg_plan_delta(dmcg_plan* p, int axis, double* delta_host) {
+  if (!p || !delta_host || axis < 0 || axis > 2 || p->nb > 1 || !p->d_delta) return DMCG_E_CONFIG;
+  cudaSetDevice(p->ctx->device);
+  const size_t nF = (size_t)p->n * p->F;
+  cudaStream_t s = p->ctx->stream;
+  cudaMemcpyAsync(delta_host, p->d_delta + axis * nF, nF * 8, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return DMCG_E_CUDA;
+  return DMCG_OK;
+}
+
 int dmcg_plan_basis(dmcg_plan* p, int axis, double* U_host, double* evals_host) {
   if (!p || axis < 0 || axis > 2) return DMCG_E_CONFIG;
   cudaSetDevice(p->ctx->device);
@@ -1534,6 +1578,14 @@ extern "C" int dmcg_debug_chol(uint32_t n, const uint32_t* faces, uint32_t n_fac
       x[0] = (double)p.front_off[p.nsup];
       x[1] = (double)p.inv_off[p.nsup];
       x[2] = (double)p.rhs_off[p.nsup];
+    }
+  }
+  if (const char* path = std::getenv("DMCG_DUMP_FRONTS")) {  // "level w m" per supernode
+    if (FILE* f = std::fopen(path, "w")) {
+      for (uint32_t l = 0; l + 1 < p.level_ptr.size(); ++l)
+        for (uint32_t q = p.level_ptr[l]; q < p.level_ptr[l + 1]; ++q)
+          std::fprintf(f, "%u %u %u\n", l, p.w(p.level_sup[q]), p.m(p.level_sup[q]));
+      std::fclose(f);
     }
   }
   if (W > 0) {

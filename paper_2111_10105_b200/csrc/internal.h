@@ -220,6 +220,10 @@ struct dmcg_plan {
   // Ozaki INT8 tensor-core Gram (ozaki.h; f32 storage, n_b = 1): the s
   // slices of X (rows = frames, K = vertex rows) and their row maxima
   int oz_slices = 0;               // 0: DMMA Gram
+  int oz_proj_slices = 0;          // Ozaki projection U_k^T delta^T (0: DMMA)
+  int oz_rec_slices = 0;           // Ozaki reconstruction U~ c~ (0: DMMA)
+  size_t oz_q_bytes = 0;           // d_oz_q capacity
+  size_t oz_max_elems = 0;         // d_oz_max capacity
   int8_t* d_oz_q = nullptr;        // 3 x s x F_pad x n_pad
   unsigned long long* d_oz_max = nullptr;  // 3 x F_pad
   double* d_U = nullptr;           // 3 x F x F (col-major)

@@ -54,8 +54,10 @@ cudaError_t launch_pack_rows(cudaStream_t s, const uint16_t* sym, long n, int ro
 
 // ---- basis.cu --------------------------------------------------------------
 // Round-robin Jacobi eigensolver of symmetric m x m A (col-major, per
-// batch).  work: nbatch * 2 * m2 * (m2 + 1) doubles (m2 = m + m%2).  Writes V
+// batch).  work: nbatch * max(2 * m2 * (m2 + 1), kJacobiBlkWork) doubles
+// (m2 = m + m%2; the block-Jacobi cluster kernel pads to 256).  Writes V
 // (m x m) and w (m).  flags[3] set on non-convergence.
+constexpr size_t kJacobiBlkWork = 256 * 256;
 cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, double* work,
                           double* V, double* w, int* flags);
 // Stable descending order of w: Vs[:, j] = V[:, idx[j]], ws[j] = w[idx[j]];

@@ -14,6 +14,8 @@
 //                  combine the diagonals in fp64.
 #include "ozaki.h"
 
+#include "common.cuh"
+
 #include <cudaTypedefs.h>
 
 #include <cmath>
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(192, 1)
     const int ea = oz_exp(__longlong_as_double(
         (long long)g.a_max[(long)b * g.a_rows_pad + min(mrow, g.a_rows_pad - 1)]));
     const uint32_t lane_addr = tbase + ((uint32_t)(quarter * 32) << 16);
+    double lo = INFINITY, hi = -INFINITY;
 #pragma unroll 1
     for (int c = 0; c < kOzBN / 16; ++c) {
       double v[16];
@@ -345,10 +348,18 @@ __global__ void __launch_bounds__(192, 1)
           if (ncol < g.N) {
             const int eb =
                 oz_exp(__longlong_as_double((long long)g.b_max[(long)b * g.b_rows_pad + ncol]));
-            dst[(long)ncol * g.out.sn] = ldexp(v[j], ea + eb);
+            const double r = ldexp(v[j], ea + eb);
+            dst[(long)ncol * g.out.sn] = r;
+            lo = fmin(lo, r);
+            hi = fmax(hi, r);
           }
         }
       }
+    }
+    if (g.out.keys && mrow < g.M && lo <= hi) {
+      unsigned long long* kp = g.out.keys + 2 * ((long)b * g.M + mrow);
+      atomicMin(kp, ordered_key(lo));
+      atomicMax(kp + 1, ordered_key(hi));
     }
     tc_fence_before();
   }
@@ -469,6 +480,32 @@ cudaError_t oz_gram(cudaStream_t st, const void* const x[3], bool f32, int n, in
   const long FF = (long)F * F;
   OzStore out{part, FF, 3 * FF, (long)F, 1L};
   return oz_gemm(st, sl, sl, out, gram_min_splits(F), splits);
+}
+
+cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, int s, int8_t* qa,
+                      unsigned long long* maxa, int8_t* qb, unsigned long long* maxb,
+                      const OzStore& out) {
+  if (A.K != B.K || A.batch != B.batch || oz_k_pad(A.K) > kOzKChunk) return cudaErrorInvalidValue;
+  OzSlices sa, sb;
+  sa.q = qa;
+  sa.maxbits = maxa;
+  sa.rows = A.rows;
+  sa.rows_pad = oz_rows_pad(A.rows);
+  sa.K = A.K;
+  sa.K_pad = oz_k_pad(A.K);
+  sa.s = s;
+  sa.batch = A.batch;
+  sb = sa;
+  sb.q = qb;
+  sb.maxbits = maxb;
+  sb.rows = B.rows;
+  sb.rows_pad = oz_rows_pad(B.rows);
+  cudaError_t e = oz_slice(st, A, sa);
+  if (e == cudaSuccess) e = oz_slice(st, B, sb);
+  if (e != cudaSuccess) return e;
+  int used = 0;
+  e = oz_gemm(st, sa, sb, out, 1, &used);
+  return (e == cudaSuccess && used != 1) ? cudaErrorInvalidValue : e;
 }
 
 cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const OzStore& out,

@@ -64,9 +64,12 @@ inline int oz_k_pad(int K) { return (K + kOzBK - 1) / kOzBK * kOzBK; }
 cudaError_t oz_slice(cudaStream_t st, const OzOperand& op, OzSlices& sl);
 
 // Epilogue: C(b, split, m, n) at C + b*sb + split*ssplit + m*sm + n*sn (fp64).
+// keys (optional, one split only): per-row running (min, max) as ordered
+// keys at keys[2 (b M + m)], [.. + 1] (the projection's row ranges).
 struct OzStore {
   double* C;
   long sb, ssplit, sm, sn;
+  unsigned long long* keys = nullptr;
 };
 
 // C[b](m, n) = sum_k A[b](m, k) B[b](n, k) over M = A.rows, N = B.rows,
@@ -75,6 +78,18 @@ struct OzStore {
 // *splits_out.  A and B may be the same OzSlices (the Gram).
 cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const OzStore& out,
                     int min_splits, int* splits_out);
+
+// C[b] = A[b] B[b]^T for two operand views (one K split: K_pad <= kOzKChunk),
+// slicing both into qa / qb (oz_slice_bytes each) and maxa / maxb
+// (batch x oz_rows_pad(rows) each): the projection U_k^T delta^T
+// (codec.cpp:420, with out.keys = the row ranges) and the reconstruction
+// U~ c~ (codec.cpp:531-532) of fp32-storage plans.
+inline size_t oz_slice_bytes(int rows, int K, int s, int batch) {
+  return (size_t)batch * s * oz_rows_pad(rows) * oz_k_pad(K);
+}
+cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, int s, int8_t* qa,
+                      unsigned long long* maxa, int8_t* qb, unsigned long long* maxb,
+                      const OzStore& out);
 
 // Splits oz_gemm will use for (A, B, min_splits).
 int oz_splits(const OzSlices& A, int min_splits);

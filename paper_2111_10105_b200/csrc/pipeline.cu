@@ -403,7 +403,21 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
     DMCG_TRY(launch_init_keys(s, 3L * k, p->d_keys));
     LoadDense<double, true> lU{p->d_U, FF, 1L, (long)F};
     StoreCoeffMinMax ep{p->d_C, p->d_keys};
-    if (variant_uses_delta(p->variant)) {
+    if (variant_uses_delta(p->variant) && p->oz_proj_slices) {
+      // INT8 tensor cores (Ozaki slices, ozaki.h): C[b](r, i) = sum_f U(f, r)
+      // delta(i, f), the row ranges folded into the epilogue
+      const int sp = p->oz_proj_slices;
+      const long nF = (long)n * F;
+      const double* d = p->d_delta;
+      OzOperand A{{p->d_U, p->d_U + FF, p->d_U + 2 * FF}, false, (long)F, 1L, k, F, 3};
+      OzOperand B{{d, d + nF, d + 2 * nF}, false, (long)F, 1L, n, F, 3};
+      int8_t* qa = p->d_oz_q;
+      int8_t* qb = qa + oz_slice_bytes(k, F, sp, 3);
+      unsigned long long* ma = p->d_oz_max;
+      unsigned long long* mb = ma + 3L * oz_rows_pad(k);
+      OzStore out{p->d_C, (long)k * n, 0L, (long)n, 1L, p->d_keys};
+      DMCG_TRY(oz_matmul(s, A, B, sp, qa, ma, qb, mb, out));
+    } else if (variant_uses_delta(p->variant)) {
       LoadDense<double, true> lD{p->d_delta, (long)n * F, 1L, (long)F};
       DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lD, ep));
     } else if (f32) {  // v2v: coeffs = U^T traj (codec.cpp:416-417)
@@ -716,11 +730,25 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void*
     DMCG_TRY(launch_dequant_rows(s, 3 * k, n, p->d_coeff_q, p->d_rowp, p->d_row_bits,
                                  p->d_flags + 1, Cd));
     DMCG_TRY(launch_dequant_dict(s, F_all, k, f0, F, p->d_dict_q, p->dict_bits, p->d_flags + 1, Ud));
-    LoadDense<double, false> la{Cd, (long)k * n, (long)n, 1L};   // A(r, i) = c~(r, i)
-    LoadDense<double, false> lb{Ud, (long)k * F, (long)F, 1L};   // B(r, f) = U~(f0 + f, r)
-    // delta~ (i, a*F + f): batch b = axis, rows = vertices, cols = frames
-    DMCG_TRY(launch_gemm(s, 3, n, F, k, 1, la, lb,
-                         StoreStrided{p->d_rm_delta, (long)F, (long)W, 1L}));
+    if (p->oz_rec_slices) {
+      // INT8 tensor cores (Ozaki slices): delta~(i, b F + f) = sum_r c~(b, r, i) U~(f, r)
+      const int sr = p->oz_rec_slices;
+      const long kn = (long)k * n, kF = (long)k * F;
+      OzOperand A{{Cd, Cd + kn, Cd + 2 * kn}, false, 1L, (long)n, n, k, 3};
+      OzOperand B{{Ud, Ud + kF, Ud + 2 * kF}, false, 1L, (long)F, F, k, 3};
+      int8_t* qa = p->d_oz_q;
+      int8_t* qb = qa + oz_slice_bytes(n, k, sr, 3);
+      unsigned long long* ma = p->d_oz_max;
+      unsigned long long* mb = ma + 3L * oz_rows_pad(n);
+      OzStore out{p->d_rm_delta, (long)F, 0L, (long)W, 1L};
+      DMCG_TRY(oz_matmul(s, A, B, sr, qa, ma, qb, mb, out));
+    } else {
+      LoadDense<double, false> la{Cd, (long)k * n, (long)n, 1L};   // A(r, i) = c~(r, i)
+      LoadDense<double, false> lb{Ud, (long)k * F, (long)F, 1L};   // B(r, f) = U~(f0 + f, r)
+      // delta~ (i, a*F + f): batch b = axis, rows = vertices, cols = frames
+      DMCG_TRY(launch_gemm(s, 3, n, F, k, 1, la, lb,
+                           StoreStrided{p->d_rm_delta, (long)F, (long)W, 1L}));
+    }
   } else {
     DMCG_TRY(cudaMemsetAsync(p->d_rm_delta, 0, nW * sizeof(double), s));
   }

@@ -184,10 +184,13 @@ def test_config2_parity_f32(codec):
     check_parity(codec, s, spec, f32_out=True)
 
 
-def test_cluster_jacobi_full_eigenbasis_parity():
-    """k_jacobi_cluster (the distributed Jacobi used when the matrix does not
-    fit one CTA) on the reference's full-eigenbasis path, forced at F = 64 and
-    checked with the full parity contract (subprocess: the switch is read once)."""
+@pytest.mark.parametrize("kernel", ["blk", "cols"])
+def test_cluster_jacobi_full_eigenbasis_parity(kernel):
+    """The distributed Jacobi used when the matrix does not fit one CTA —
+    k_jacobi_blk (block Jacobi over the cluster, the default) and
+    k_jacobi_cluster (one rotation step per cluster barrier, DMCG_JACOBI_COLS)
+    — on the reference's full-eigenbasis path, forced at F = 64 and checked
+    with the full parity contract (subprocess: the switch is read once)."""
     import os
     import subprocess
     import sys
@@ -198,7 +201,8 @@ def test_cluster_jacobi_full_eigenbasis_parity():
             "spec = synth.CONFIGS['c0']; cd = C.Codec(0);"
             "T.check_parity(cd, spec.make(), spec, rounds=0); print('ok')")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                       timeout=600, env=dict(os.environ, DMCG_JACOBI_CLUSTER="1"))
+                       timeout=600, env=dict(os.environ, DMCG_JACOBI_CLUSTER="1",
+                                             **({"DMCG_JACOBI_COLS": "1"} if kernel == "cols" else {})))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
 
