@@ -321,7 +321,14 @@ __global__ void k_sort_basis(int m, int ncols_store, const double* __restrict__ 
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     const double wi = sw[i];
     int rank = 0;
-    for (int j = 0; j < m; ++j) rank += (sw[j] > wi) || (sw[j] == wi && j < i);
+    // NaN (a non-finite input flagged by K1) ranks last, so idx stays a
+    // permutation and the gathers below stay in bounds
+    const bool ni = isnan(wi);
+    for (int j = 0; j < m; ++j) {
+      const double wj = sw[j];
+      const bool nj = isnan(wj);
+      rank += (wj > wi) || (ni && !nj) || ((wj == wi || (ni && nj)) && j < i);
+    }
     idx[rank] = i;
   }
   __syncthreads();
@@ -357,6 +364,7 @@ __global__ void k_canon_signs(int m, int c0, int ncols, double* Uall, long bs) {
       bi = oi;
     }
   }
+  if (bi >= m) bi = 0;  // an all-NaN column (non-finite input, flagged by K1)
   const bool flip = u[bi] < 0.0;
   if (flip)
     for (int i = lane; i < m; i += 32) u[i] = -u[i];

@@ -155,6 +155,7 @@ __device__ void canon_columns(int m, double* U) {
         bi = oi;
       }
     }
+    if (bi >= m) bi = 0;  // an all-NaN column (non-finite input, flagged by K1)
     const bool neg = u[bi] < 0.0;
     __syncwarp();
     if (neg)

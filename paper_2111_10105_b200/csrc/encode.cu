@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kDeltaWarps * 32)
 
 // K1, vectorised (the default when every row starts 16-byte aligned): one
 // warp per vertex row, each lane 16-byte loads of VEC consecutive frames,
-// CH chunks per pass (f32: 512 frames, f64: 256 frames per pass); the row's
+// CH chunks per pass (256 frames per pass); the row's
 // neighbour indices are loaded once (lane t holds entry t) and broadcast by
 // shuffles, and neighbour p + 1's loads are issued before neighbour p's
 // adds, so two rows' worth of loads are in flight per warp.  The additions
@@ -89,7 +89,10 @@ struct Vec16<double> {
   }
 };
 
-constexpr int kDeltaVecCh = 4;
+// chunks per pass: 8 accumulators per lane either way (f32: 256 frames,
+// f64: 256 frames per pass)
+template <typename T>
+constexpr int delta_vec_ch() { return sizeof(T) == 4 ? 2 : 4; }
 
 template <typename T>
 __global__ void __launch_bounds__(kDeltaWarps * 32)
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(kDeltaWarps * 32)
                 double* __restrict__ delta, int* flags) {
   using VT = Vec16<T>;
   using V = typename VT::V;
-  constexpr int VEC = VT::N, CH = kDeltaVecCh, PASS = 32 * VEC * CH;
+  constexpr int VEC = VT::N, CH = delta_vec_ch<T>(), PASS = 32 * VEC * CH;
   const int a = blockIdx.y;
   const T* __restrict__ X = a == 0 ? x0 : (a == 1 ? x1 : x2);
   const int lane = threadIdx.x & 31;

@@ -383,8 +383,11 @@ int dmcg_create(dmcg_ctx** out, int device) {
   if (cudaSetDevice(device) != cudaSuccess) return DMCG_E_CUDA;
   auto* c = new dmcg_ctx();
   c->device = device;
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->aux2, cudaStreamNonBlocking, prio_lo) != cudaSuccess) {
     delete c;
     return DMCG_E_CUDA;
   }
@@ -399,8 +402,10 @@ void dmcg_destroy(dmcg_ctx* c) {
   cudaStreamSynchronize(c->stream);
   c->pool.release_all();
   cudaStreamSynchronize(c->aux);
+  cudaStreamSynchronize(c->aux2);
   for (auto e : c->ev_timing) cudaEventDestroy(e);
   for (auto e : c->ev_plain) cudaEventDestroy(e);
+  cudaStreamDestroy(c->aux2);
   cudaStreamDestroy(c->aux);
   cudaStreamDestroy(c->stream);
   delete c;
@@ -526,7 +531,8 @@ void dmcg_plan_destroy(dmcg_plan* p) {
     if (g->exec) cudaGraphExecDestroy(g->exec);
   for (auto& kv : p->owned) p->ctx->pool.put(kv.first, kv.second);
   for (auto& e : p->ev) p->ctx->give_event(e, true);
-  for (auto e : {p->ev_fork, p->ev_join}) p->ctx->give_event(e, false);
+  for (auto e : {p->ev_fork, p->ev_join, p->ev_pf_fork, p->ev_pf_join}) p->ctx->give_event(e, false);
+  for (auto e : {p->ev_pf0, p->ev_pf1}) p->ctx->give_event(e, true);
   delete p;
 }
 
@@ -659,8 +665,11 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     };
     const bool kfit = k > 0 && dmcg::oz_k_pad((int)F) <= dmcg::kOzKChunk &&
                       dmcg::oz_k_pad((int)k) <= dmcg::kOzKChunk;
-    p->oz_proj_slices = (kfit && variant_uses_delta(p->variant)) ? env_s("DMCG_OZ_PROJ_SLICES", 6) : 0;
-    p->oz_rec_slices = kfit ? env_s("DMCG_OZ_REC_SLICES", 5) : 0;
+    // the projection stays on DMMA unless asked for: its K = F is short, so
+    // the slicing passes outweigh the tensor-core gain
+    p->oz_proj_slices = (kfit && variant_uses_delta(p->variant) && getenv("DMCG_OZ_PROJ"))
+                            ? env_s("DMCG_OZ_PROJ_SLICES", 6) : 0;
+    p->oz_rec_slices = kfit ? env_s("DMCG_OZ_REC_SLICES", 4) : 0;
     if (getenv("DMCG_NO_OZAKI_GEMMS")) p->oz_proj_slices = p->oz_rec_slices = 0;
     size_t qb = oz_slice_bytes((int)F, (int)n, p->oz_slices, 3);
     size_t mx = 3 * (size_t)oz_rows_pad((int)F);
@@ -700,6 +709,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_C = (double*)get(3 * kk * std::max<size_t>(n, kk) * 8);
   p->d_keys = (unsigned long long*)get(3 * kk * 2 * 8);
   p->d_flags = (int*)get(8 * sizeof(int));
+  p->d_pf_flag = (int*)get(sizeof(int));
   p->d_dict_q = (uint16_t*)get(3 * FF * 2);
   p->d_row_min = (float*)get(3 * kk * 4);
   p->d_row_max = (float*)get(3 * kk * 4);
@@ -728,6 +738,10 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   for (auto& e : p->ev) e = ctx->take_event(true);
   p->ev_fork = ctx->take_event(false);
   p->ev_join = ctx->take_event(false);
+  p->ev_pf_fork = ctx->take_event(false);
+  p->ev_pf_join = ctx->take_event(false);
+  p->ev_pf0 = ctx->take_event(true);
+  p->ev_pf1 = ctx->take_event(true);
   cudaStream_t s = ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;

@@ -116,6 +116,7 @@ struct dmcg_ctx {
   std::unique_ptr<dmcg::PendingAnalysis> pending;  // see PendingAnalysis
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // fork/join side stream (independent encode / decode phases)
+  cudaStream_t aux2 = nullptr; // low-priority stream: the decoder's factor during an encode
   std::string err;
   dmcg::DevicePool pool;
   dmcg_stats last_stats = {};  // stats of the last drop-in encode / decode
@@ -285,5 +286,14 @@ struct dmcg_plan {
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // ctx->stream <-> ctx->aux
   bool forked = false;
+  // Decoder factor overlapped with the encode (pipeline.cu prefactor_on):
+  // M = L^T L + S^T S depends only on the mesh and the plan's anchor set, so
+  // once the decode structures exist an encode factors M on ctx->aux2 while
+  // its own latency-bound basis phase leaves most SMs idle; the next decode
+  // takes that factor instead of refactoring.
+  cudaEvent_t ev_pf_fork = nullptr, ev_pf_join = nullptr, ev_pf0 = nullptr, ev_pf1 = nullptr;
+  int* d_pf_flag = nullptr;        // non-positive pivot of the overlapped factor
+  bool factor_pending = false;     // the last encode left a factor of M for the next decode
+  float ms_prefactor = 0.0f;
   dmcg_stats stats = {};
 };

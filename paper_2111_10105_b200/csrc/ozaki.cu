@@ -215,13 +215,16 @@ struct OzCfg {
   static constexpr int kA = kOzBM * kOzBK;                 // bytes of one A slice tile
   static constexpr int kB = kOzBN * kOzBK;                 // bytes of one B slice tile
   static constexpr int kStage = S * (kA + kB);
-  static constexpr int kStages = (196608 / kStage) < 8 ? (196608 / kStage) : 8;
-  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  // S <= 4: the accumulators fit 256 TMEM columns, so two CTAs share an SM
+  // (one's epilogue under the other's MMAs) with four stages each
+  static constexpr int kCtasPerSm = S <= 4 ? 2 : 1;
+  static constexpr int kStages = S <= 4 ? 4 : ((196608 / kStage) < 8 ? (196608 / kStage) : 8);
+  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/ + 4 * kOzBN;
   static constexpr int kCols = S * kOzBN <= 256 ? 256 : 512;  // TMEM allocation (power of 2)
 };
 
 template <int S>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, OzCfg<S>::kCtasPerSm)
     k_oz_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
               OzGemmArgs g) {
   using C = OzCfg<S>;
@@ -230,6 +233,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bars = (uint64_t*)(smem + C::kStages * C::kStage);
   // bars[0 .. kStages): full, [kStages .. 2 kStages): empty, [2 kStages]: tmem_full
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * C::kStages + 1);
+  int* col_exp = (int*)(tmem_slot + 4);  // kOzBN column exponents of this tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // work unit: batch, tile_m, tile_n, split
@@ -317,13 +321,21 @@ __global__ void __launch_bounds__(192, 1)
     // ===== epilogue: warps 2..5 own TMEM lanes 32 (warp % 4) .. +31 =====
     const int quarter = warp & 3;
     const int mrow = tm * kOzBM + quarter * 32 + lane;
+    const int ea = oz_exp(__longlong_as_double(
+        (long long)g.a_max[(long)b * g.a_rows_pad + min(mrow, g.a_rows_pad - 1)]));
+    {  // the tile's column exponents, once (epilogue warps 2..5 = threads 64..191)
+      const int t = threadIdx.x - 64;
+      if (t < kOzBN) {
+        const int ncol = min(tn * kOzBN + t, g.b_rows_pad - 1);
+        col_exp[t] = oz_exp(__longlong_as_double((long long)g.b_max[(long)b * g.b_rows_pad + ncol]));
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four epilogue warps only
+    }
+    const uint32_t lane_addr = tbase + ((uint32_t)(quarter * 32) << 16);
     if (nkb > 0) {
       mbar_wait(smem_u32(&bars[2 * C::kStages]), 0u);
       tc_fence_after();
     }
-    const int ea = oz_exp(__longlong_as_double(
-        (long long)g.a_max[(long)b * g.a_rows_pad + min(mrow, g.a_rows_pad - 1)]));
-    const uint32_t lane_addr = tbase + ((uint32_t)(quarter * 32) << 16);
     double lo = INFINITY, hi = -INFINITY;
 #pragma unroll 1
     for (int c = 0; c < kOzBN / 16; ++c) {
@@ -336,8 +348,9 @@ __global__ void __launch_bounds__(192, 1)
           int32_t raw[16];
           tmem_ld16(lane_addr + (uint32_t)((d - 2) * kOzBN + c * 16), raw);
           tmem_wait_ld();
+          const double wd = ldexp(1.0, -7 * d);  // exact: (double) raw * wd is exact
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += ldexp((double)raw[j], -7 * d);
+          for (int j = 0; j < 16; ++j) v[j] = fma((double)raw[j], wd, v[j]);
         }
       }
       if (mrow < g.M) {
@@ -346,9 +359,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < 16; ++j) {
           const int ncol = tn * kOzBN + c * 16 + j;
           if (ncol < g.N) {
-            const int eb =
-                oz_exp(__longlong_as_double((long long)g.b_max[(long)b * g.b_rows_pad + ncol]));
-            const double r = ldexp(v[j], ea + eb);
+            const double r = ldexp(v[j], ea + col_exp[c * 16 + j]);
             dst[(long)ncol * g.out.sn] = r;
             lo = fmin(lo, r);
             hi = fmax(hi, r);

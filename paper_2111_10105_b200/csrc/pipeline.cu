@@ -371,9 +371,34 @@ static Status enqueue_encode_blocks(dmcg_plan* p, const void* const x[3]) {
                               : enqueue_encode_blocks_t<double>(p, x);
 }
 
+// The decoder's numeric factor of M during the encode (see dmcg_plan::
+// factor_pending): only once the plan's decode structures exist (after its
+// first decode), for the direct solver of single-block, single-GPU plans.
+static bool prefactor_on(const dmcg_plan* p) {
+  static const bool off = getenv("DMCG_NO_PREFACTOR") != nullptr;
+  return !off && p->decode_ready && p->nb == 1 && !p->shard && p->variant != DMCG_V2V &&
+         p->cdev.P != nullptr;
+}
+
+// Fork: M's supernodal factor on the low-priority stream aux2 (it reads
+// only the plan's mesh structures; the encode never touches F / Linv / P).
+static Status fork_prefactor(dmcg_plan* p) {
+  cudaStream_t s = p->ctx->stream, sf = p->ctx->aux2;
+  DMCG_TRY(cudaEventRecord(p->ev_pf_fork, s));
+  DMCG_TRY(cudaStreamWaitEvent(sf, p->ev_pf_fork, 0));
+  DMCG_TRY(cudaMemsetAsync(p->d_pf_flag, 0, sizeof(int), sf));
+  DMCG_TRY(record_event(p->ev_pf0, sf));
+  CholDev cd = p->cdev;
+  cd.flags = p->d_pf_flag;
+  DMCG_TRY(chol_factor_device(sf, cd, p->levels));
+  DMCG_TRY(record_event(p->ev_pf1, sf));
+  DMCG_TRY(cudaEventRecord(p->ev_pf_join, sf));
+  return Status::ok();
+}
+
 // Every kernel of one encode on the plan stream (no host synchronisation:
 // capturable into a CUDA graph).
-static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
+static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefactor) {
   if (p->nb > 1) return enqueue_encode_blocks(p, x);
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
@@ -381,6 +406,10 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   const long FF = (long)F * F;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
   DMCG_TRY(record_event(p->ev[0], s));
+  if (prefactor) {
+    Status st = fork_prefactor(p);
+    if (!st.good()) return st;
+  }
   // K1 delta coordinates (codec.cpp:419); v2v codes the trajectories.
   if (variant_uses_delta(p->variant))
     DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
@@ -444,6 +473,7 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3]) {
   if (p->forked) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
   DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
   DMCG_TRY(record_event(p->ev[5], s));
+  if (prefactor) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_pf_join, 0));  // join (graph capture)
   return Status::ok();
 }
 
@@ -496,8 +526,9 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   cudaStream_t s = p->ctx->stream;
   const int k = (int)p->k, F = (int)p->F;
   const void* key[4] = {x[0], x[1], x[2], nullptr};
+  const bool pf = prefactor_on(p);
   {
-    Status st = run_graph(p, p->g_encode, key, 0, [&] { return enqueue_encode(p, x); });
+    Status st = run_graph(p, p->g_encode, key, pf ? 1 : 0, [&] { return enqueue_encode(p, x, pf); });
     if (!st.good()) return st;
   }
   p->oi_timed = p->nb == 1 && p->rounds > 0 && k < F && k > 0;
@@ -507,6 +538,8 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   float ms;
   cudaEventElapsedTime(&ms, p->ev[0], p->ev[5]);
   p->stats.ms_encode = ms;
+  p->factor_pending = pf;
+  if (pf) cudaEventElapsedTime(&p->ms_prefactor, p->ev_pf0, p->ev_pf1);
   cudaEventElapsedTime(&p->stats.ms_delta, p->ev[0], p->ev[1]);
   cudaEventElapsedTime(&p->stats.ms_gram, p->ev[1], p->ev[2]);
   cudaEventElapsedTime(&p->stats.ms_basis, p->ev[2], p->ev[3]);
@@ -689,14 +722,16 @@ Status shard_encode(dmcg_plan* p, const void* const x[3]) {
 // Frames [f0, f0 + Fw) only (the solve is column-separable: each frame
 // column's result does not depend on the others, so a window decodes to the
 // same bits as the full decode).
-static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, void* const out[3],
-                                    int f0, int Fw) {
+static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool pre,
+                                    void* const out[3], int f0, int Fw) {
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = Fw, F_all = (int)p->F, k = (int)p->k, W = 3 * Fw;
   CholDev cdev = p->cdev;
   cdev.W = (uint32_t)W;
   const bool f32 = p->dtype == DMCG_F32;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
+  if (pre && !factor)  // the overlapped factor's pivot flag
+    DMCG_TRY(cudaMemcpyAsync(p->d_flags + 4, p->d_pf_flag, sizeof(int), cudaMemcpyDeviceToDevice, s));
   DMCG_TRY(record_event(p->ev[0], s));
   const size_t nW = (size_t)n * W;
   // The right-hand sides (dequantise + reconstruct + L^T delta~ + S^T a) do
@@ -809,7 +844,10 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   cudaStream_t s = p->ctx->stream;
   const int k = (int)p->k;
   const int refine = opt ? opt->refine : 1;
-  const bool factor = !(opt && opt->reuse_factor && p->factor_valid);
+  // the factor of M left by the last encode (overlapped with it), else the
+  // caller's reuse_factor, else factor now
+  const bool pre = p->factor_pending;
+  const bool factor = !(pre || (opt && opt->reuse_factor && p->factor_valid));
   uint32_t f0 = opt ? opt->frame_begin : 0, Fw = opt ? opt->frame_count : 0;
   if (p->nb > 1) {  // blocks: one stacked solve over all padded frames
     if (f0 != 0 || (Fw != 0 && Fw != p->F_in))
@@ -825,10 +863,10 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   const int W = 3 * (int)Fw;
   const void* key[4] = {out[0], out[1], out[2], nullptr};
   {
-    const long long okey = ((long long)f0 << 40) | ((long long)Fw << 16) | (refine * 2) |
-                           (factor ? 1 : 0);
+    const long long okey = ((long long)f0 << 40) | ((long long)Fw << 16) | (refine * 4) |
+                           (pre ? 2 : 0) | (factor ? 1 : 0);
     Status st = run_graph(p, p->g_decode, key, okey, [&] {
-      return enqueue_decode_direct(p, refine, factor, out, (int)f0, (int)Fw);
+      return enqueue_decode_direct(p, refine, factor, pre, out, (int)f0, (int)Fw);
     });
     if (!st.good()) return st;
   }
@@ -857,8 +895,10 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
     return Status{DMCG_E_NUMERICAL,
                   "SingularSystem: anchored normal equations are not positive definite"};
   }
+  p->factor_pending = false;
   p->factor_valid = true;
-  if (!factor) p->stats.ms_factor = 0.0f;
+  // overlapped factor: its own time on aux2 during the encode
+  if (!factor) p->stats.ms_factor = pre ? p->ms_prefactor : 0.0f;
   return Status::ok();
 }
 

@@ -29,7 +29,10 @@ per = collections.defaultdict(dict)
 for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
-    per[(r[0], r[ki])][r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    try:
+        per[(r[0], r[ki])][r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    except ValueError:  # "n/a" (metric not collected for this launch)
+        continue
 agg = collections.defaultdict(lambda: collections.defaultdict(float))
 for (_, k), m in per.items():
     name = k.split("(")[0].replace("(anonymous namespace)::", "").replace("unnamed>::", "")[:58]
