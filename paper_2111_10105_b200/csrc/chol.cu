@@ -627,24 +627,54 @@ struct StoreFwd {
   }
 };
 
-struct StoreRowsW {  // out[mi * W + ni] = v
-  double* out;
-  int W;
+// Backward epilogue: x (permuted, read by the descendants' backward steps)
+// and the caller's output row perm[first + mi] in the original order
+// (= or += : the refinement accumulates its correction), replacing a
+// separate unpermute pass over n x W.
+struct StoreBwd {
+  double* x;            // x + first[s] * W
+  double* out;          // original-order output (n x W)
+  const uint32_t* perm;  // perm + first[s]
+  int W, accumulate;
   __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
                                              const WarpTile& wt) const {
+    const bool vec = !(W & 1);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int mi = mb + i * 8 + (lane >> 2);
       if (mi >= M) continue;
+      double* xr = x + (size_t)mi * W;
+      double* orow = out + (size_t)perm[mi] * W;
+      double prev[4][2];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int ni = nb + j * 8 + (lane & 3) * 2;
-        if (ni + 1 < N && !(W & 1))
-          *reinterpret_cast<double2*>(out + (size_t)mi * W + ni) =
-              make_double2(wt.acc[i][j][0], wt.acc[i][j][1]);
-        else if (ni < N) {
-          out[(size_t)mi * W + ni] = wt.acc[i][j][0];
-          if (ni + 1 < N) out[(size_t)mi * W + ni + 1] = wt.acc[i][j][1];
+        prev[j][0] = prev[j][1] = 0.0;
+        if (accumulate) {
+          if (ni + 1 < N && vec) {
+            const double2 t = *reinterpret_cast<const double2*>(orow + ni);
+            prev[j][0] = t.x;
+            prev[j][1] = t.y;
+          } else if (ni < N) {
+            prev[j][0] = orow[ni];
+            if (ni + 1 < N) prev[j][1] = orow[ni + 1];
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ni = nb + j * 8 + (lane & 3) * 2;
+        const double v0 = wt.acc[i][j][0], v1 = wt.acc[i][j][1];
+        if (ni + 1 < N && vec) {
+          *reinterpret_cast<double2*>(xr + ni) = make_double2(v0, v1);
+          *reinterpret_cast<double2*>(orow + ni) = make_double2(prev[j][0] + v0, prev[j][1] + v1);
+        } else if (ni < N) {
+          xr[ni] = v0;
+          orow[ni] = prev[j][0] + v0;
+          if (ni + 1 < N) {
+            xr[ni + 1] = v1;
+            orow[ni + 1] = prev[j][1] + v1;
+          }
         }
       }
     }
@@ -670,7 +700,8 @@ __global__ void __launch_bounds__(kGemmThreads, 4) k_fwd(CholDev d, const uint32
 
 // Backward: x_s = P_s^T [y_s; x_below], M = w, K = m.
 __global__ void __launch_bounds__(kGemmThreads, 4) k_bwd(CholDev d, const uint32_t* lsup,
-                                                      const double* y, double* x) {
+                                                      const double* y, double* x, double* out,
+                                                      int accumulate) {
   const uint32_t s = lsup[blockIdx.z];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
   if ((int)blockIdx.x * kBM >= w) return;
@@ -679,33 +710,72 @@ __global__ void __launch_bounds__(kGemmThreads, 4) k_bwd(CholDev d, const uint32
   const int m0 = blockIdx.x * kBM;
   gemm_tile(0, w, W, m0, blockIdx.y * kBN, m0, m, 0,
             LoadRowMajor{d.P + d.op_off[s], m}, LoadYX{y, x, rows, w, W},
-            StoreRowsW{x + (size_t)d.first[s] * W, W});
+            StoreBwd{x + (size_t)d.first[s] * W, out, d.perm + d.first[s], W, accumulate});
 }
 
-// out[perm[j]] (+)= x[j]
-__global__ void k_unpermute(int n, int W, const uint32_t* perm, const double* __restrict__ xp,
-                            double* __restrict__ out, int accumulate) {
-  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= (long)n * W) return;
-  const int j = (int)(t / W), c = (int)(t % W);
-  const size_t o = (size_t)perm[j] * W + c;
-  if (accumulate)
-    out[o] += xp[t];
-  else
-    out[o] = xp[t];
-}
-
-// r = b - M x   (M: CSR with float values, original order, n x W row-major)
-__global__ void k_residual(int n, int W, const uint32_t* __restrict__ rp,
-                           const uint32_t* __restrict__ ci, const float* __restrict__ val,
-                           const double* __restrict__ b, const double* __restrict__ x,
-                           double* __restrict__ r) {
-  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= (long)n * W) return;
-  const int i = (int)(t / W), c = (int)(t % W);
-  double acc = 0.0;
-  for (uint32_t e = rp[i]; e < rp[i + 1]; ++e) acc += (double)val[e] * x[(size_t)ci[e] * W + c];
-  r[t] = b[t] - acc;
+// r = b - M x   (M: CSR with float values, original order, n x W row-major).
+// One warp per (row, 256-column chunk): the row's CSR entries are read once
+// per warp (lane e holds entry e, broadcast by shuffles), every lane owns
+// four column pairs (double2, 512 contiguous bytes per warp access) and two
+// entries' loads are in flight per step.
+constexpr int kResCols = 256;
+__global__ void __launch_bounds__(256) k_residual(int n, int W, const uint32_t* __restrict__ rp,
+                                                  const uint32_t* __restrict__ ci,
+                                                  const float* __restrict__ val,
+                                                  const double* __restrict__ b,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ r) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int c0 = blockIdx.y * kResCols;
+  const uint32_t pb = rp[i], pe = rp[i + 1];
+  const int cnt = (int)(pe - pb);
+  const bool vec = !(W & 1);
+  double acc[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int e0 = 0; e0 < cnt; e0 += 32) {
+    const int me = e0 + lane;
+    const uint32_t my_c = me < cnt ? ci[pb + me] : 0u;
+    const double my_v = me < cnt ? (double)val[pb + me] : 0.0;
+    const int ne = min(32, cnt - e0);
+    for (int e = 0; e < ne; ++e) {
+      const uint32_t col = __shfl_sync(0xffffffffu, my_c, e);
+      const double v = __shfl_sync(0xffffffffu, my_v, e);
+      const double* xr = x + (size_t)col * W;
+      double2 t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + 64 * j + 2 * lane;
+        t[j] = make_double2(0.0, 0.0);
+        if (c + 1 < W && vec) {
+          t[j] = *reinterpret_cast<const double2*>(xr + c);
+        } else if (c < W) {
+          t[j].x = xr[c];
+          if (c + 1 < W) t[j].y = xr[c + 1];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[j][0] = fma(v, t[j].x, acc[j][0]);
+        acc[j][1] = fma(v, t[j].y, acc[j][1]);
+      }
+    }
+  }
+  const double* br = b + (size_t)i * W;
+  double* rr = r + (size_t)i * W;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + 64 * j + 2 * lane;
+    if (c + 1 < W && vec) {
+      const double2 bb = *reinterpret_cast<const double2*>(br + c);
+      *reinterpret_cast<double2*>(rr + c) = make_double2(bb.x - acc[j][0], bb.y - acc[j][1]);
+    } else if (c < W) {
+      rr[c] = br[c] - acc[j][0];
+      if (c + 1 < W) rr[c + 1] = br[c + 1] - acc[j][1];
+    }
+  }
 }
 
 }  // namespace
@@ -848,7 +918,7 @@ size_t chol_scratch_doubles(const CholLevels& lv) {
 }
 
 cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels& lv,
-                              const double* b, double* y, double* x) {
+                              const double* b, double* y, double* x, double* out, bool accumulate) {
   const int W = (int)d.W;
   const unsigned tn = (unsigned)((W + kBN - 1) / kBN);
   LevelTimer lt(s, "solve", lv.nlevels);
@@ -868,24 +938,19 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 3);
-    k_bwd<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x);
+    k_bwd<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x, out,
+                                                                               accumulate ? 1 : 0);
     lt.mark(l, 4);
   }
   lt.report(lv, "gather", "fwd", "bwd", true);
   return cudaGetLastError();
 }
 
-cudaError_t chol_unpermute(cudaStream_t s, int n, int W, const uint32_t* perm, const double* xp,
-                           double* out, bool accumulate) {
-  const long total = (long)n * W;
-  k_unpermute<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, W, perm, xp, out, accumulate);
-  return cudaGetLastError();
-}
-
 cudaError_t normal_residual(cudaStream_t s, int n, int W, const uint32_t* rp, const uint32_t* ci,
                             const float* val, const double* b, const double* x, double* r) {
-  const long total = (long)n * W;
-  k_residual<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, W, rp, ci, val, b, x, r);
+  if (n <= 0 || W <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((n + 7) / 8), (unsigned)((W + kResCols - 1) / kResCols));
+  k_residual<<<grid, 256, 0, s>>>(n, W, rp, ci, val, b, x, r);
   return cudaGetLastError();
 }
 

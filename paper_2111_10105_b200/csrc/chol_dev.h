@@ -48,10 +48,10 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
 // Doubles of scratch the blocked L11 inverse needs (CholDev::scratch).
 size_t chol_scratch_doubles(const CholLevels& lv);
 // b: n x W row-major in the original order; y, x: n x W in the permuted order.
+// out (original order, n x W) = x unpermuted (accumulate: out += x), written
+// by the backward pass itself.
 cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels& lv,
-                              const double* b, double* y, double* x);
-cudaError_t chol_unpermute(cudaStream_t s, int n, int W, const uint32_t* perm, const double* xp,
-                           double* out, bool accumulate);
+                              const double* b, double* y, double* x, double* out, bool accumulate);
 // r = b - M x for n x W row-major blocks (original order).
 cudaError_t normal_residual(cudaStream_t s, int n, int W, const uint32_t* rp, const uint32_t* ci,
                             const float* val, const double* b, const double* x, double* r);

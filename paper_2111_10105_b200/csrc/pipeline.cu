@@ -814,13 +814,13 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
   const bool mc = variant_uses_means(p->variant);
   const int nm = (int)cdev.n;
   const size_t o = mc ? (size_t)W : 0;
-  DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_b + o, p->d_rm_y, p->d_rm_xp));
-  DMCG_TRY(chol_unpermute(s, nm, W, cdev.perm, p->d_rm_xp, p->d_rm_x + o, false));
+  DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_b + o, p->d_rm_y, p->d_rm_xp,
+                             p->d_rm_x + o, false));
   for (int r = 0; r < refine; ++r) {
     DMCG_TRY(normal_residual(s, nm, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b + o,
                              p->d_rm_x + o, p->d_rm_r));
-    DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp));
-    DMCG_TRY(chol_unpermute(s, nm, W, cdev.perm, p->d_rm_xp, p->d_rm_x + o, true));
+    DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp,
+                               p->d_rm_x + o, true));
   }
   DMCG_TRY(record_event(p->ev[3], s));
   const double* shift = nullptr;
@@ -883,11 +883,11 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   p->stats.cg_iterations_max = 0;
   p->stats.cg_rel_residual_max = 0.0;
   const CholLevels& lv = p->levels;
-  int nl = 0;
-  for (uint32_t l = 0; l < lv.nlevels; ++l) nl += 2 + (int)((lv.maxw[l] + 31) / 32) * 2;
-  const int per_solve = (int)lv.nlevels * 5;
-  p->stats.kernel_launches_decode = (k > 0 ? 2 : 0) + 1 + nl + (1 + refine) * (per_solve + 1) +
-                                    refine + 1;
+  int nl = 0;  // factor: assemble, panels + trailing, inverse (2), P (2) per level
+  for (uint32_t l = 0; l < lv.nlevels; ++l) nl += 5 + (int)((lv.maxw[l] + 31) / 32) * 2;
+  const int per_solve = (int)lv.nlevels * 3;  // gather, forward, backward
+  p->stats.kernel_launches_decode = (k > 0 ? 2 : 0) + 1 + (factor ? nl : 0) +
+                                    (1 + refine) * per_solve + refine + 1;
   p->stats.flops_solve = (1 + refine) * p->chol.flops_solve_per_rhs * W;
   if (flags[1]) return Status{DMCG_E_CORRUPT, "CorruptPayload: packed value out of range"};
   if (flags[4]) {
