@@ -11,6 +11,8 @@
 // columns freeze, and each neighbour gather is exactly one 32 B sector.
 #include <cfloat>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -317,44 +319,111 @@ __global__ void __launch_bounds__(kCgThreads)
 
 // Row-major variants for the direct solver: vectors are n x W, row i =
 // [x frames | y frames | z frames] of vertex i.
-__global__ void k_rhs_rm(int n, int F, int W, int F_all, int f_off, const uint32_t* __restrict__ rp,
-                         const uint32_t* __restrict__ ci, const int32_t* __restrict__ apos, int n_c,
-                         const uint16_t* __restrict__ aq, const float* __restrict__ arng, int abits,
-                         const double* __restrict__ D, double* __restrict__ B, int* flags) {
-  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= (long)n * W) return;
-  const int i = (int)(t / W), c = (int)(t % W);
+// rhs = L^T delta~ + S^T a (row-major n x W, W = 3F): one warp per (row,
+// 256-column chunk), lane = four column pairs (double2), the row's CSR
+// entries broadcast by shuffles, each entry's loads issued before the
+// previous entry's adds; the additions run in CSR order with _rn
+// intrinsics (same arithmetic as the reference's sparse product order).
+constexpr int kRhsCols = 256;
+__global__ void __launch_bounds__(256)
+    k_rhs_rm(int n, int F, int W, int F_all, int f_off, const uint32_t* __restrict__ rp,
+             const uint32_t* __restrict__ ci, const int32_t* __restrict__ apos, int n_c,
+             const uint16_t* __restrict__ aq, const float* __restrict__ arng, int abits,
+             const double* __restrict__ D, double* __restrict__ B, int* flags) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const int c0 = blockIdx.y * kRhsCols;
   const uint32_t pb = rp[i], pe = rp[i + 1];
-  const double deg = (double)(pe - pb - 1);
-  double acc = 0.0;
-  for (uint32_t p = pb; p < pe; ++p) {
-    const uint32_t j = ci[p];
+  const int cnt = (int)(pe - pb);
+  const double deg = (double)(cnt - 1);
+  const bool vec = !(W & 1);
+  const uint32_t my_c = lane < cnt ? ci[pb + lane] : 0u;
+  auto col = [&](int e) -> uint32_t {
+    return e < 32 ? __shfl_sync(0xffffffffu, my_c, e) : ci[pb + e];
+  };
+  auto load = [&](uint32_t j, double2 (&t)[4]) {
+    const double* xr = D + (size_t)j * W;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + 64 * q + 2 * lane;
+      t[q] = make_double2(0.0, 0.0);
+      if (c + 1 < W && vec) {
+        t[q] = *reinterpret_cast<const double2*>(xr + c);
+      } else if (c < W) {
+        t[q].x = xr[c];
+        if (c + 1 < W) t[q].y = xr[c + 1];
+      }
+    }
+  };
+  double acc[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double2 nxt[4];
+  uint32_t jn = cnt > 0 ? col(0) : 0u;
+  if (cnt > 0) load(jn, nxt);
+  for (int e = 0; e < cnt; ++e) {
+    double2 cur[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+    const uint32_t j = jn;
+    if (e + 1 < cnt) {
+      jn = col(e + 1);
+      load(jn, nxt);
+    }
     const double v = (j == (uint32_t)i) ? deg : -1.0;
-    acc = __dadd_rn(acc, __dmul_rn(v, D[(size_t)j * W + c]));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(v, cur[q].x));
+      acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(v, cur[q].y));
+    }
   }
   const int slot = apos[i];
+  bool bad = false;
   if (slot >= 0) {
-    const int a = c / F, f = c % F;
-    const QParams q = make_qparams(arng[2 * a], arng[2 * a + 1], abits);
-    const uint32_t lv = aq[((size_t)a * n_c + slot) * F_all + f_off + f];
-    if (lv >= q.levels) atomicOr(flags, 1);
-    acc = __dadd_rn(acc, dequantize_level(q.min_, q.width, q.degenerate, lv));
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = c0 + 64 * q + 2 * lane + h;
+        if (c < W) {
+          const int a = c / F, f = c - a * F;
+          const QParams qp = make_qparams(arng[2 * a], arng[2 * a + 1], abits);
+          const uint32_t lv = aq[((size_t)a * n_c + slot) * F_all + f_off + f];
+          if (lv >= qp.levels) bad = true;
+          acc[q][h] = __dadd_rn(acc[q][h], dequantize_level(qp.min_, qp.width, qp.degenerate, lv));
+        }
+      }
   }
-  B[t] = acc;
+  if (bad) atomicOr(flags, 1);
+  double* br = B + (size_t)i * W;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + 64 * q + 2 * lane;
+    if (c + 1 < W && vec) {
+      *reinterpret_cast<double2*>(br + c) = make_double2(acc[q][0], acc[q][1]);
+    } else if (c < W) {
+      br[c] = acc[q][0];
+      if (c + 1 < W) br[c + 1] = acc[q][1];
+    }
+  }
 }
 
+// out_a(i, f_off + f) = X(i, a F + f) (+ shift): one CTA per vertex row (or
+// several rows per CTA), consecutive threads on consecutive frames, so both
+// the row-major read and the vertex-major writes are contiguous.
 template <typename T>
-__global__ void k_output_rm(int n, int F, int F_all, int f_off, const double* __restrict__ X, T* o0,
-                            T* o1, T* o2, const double* __restrict__ shift, int F_out) {
-  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  const long nF = (long)n * F_out;
-  if (t >= 3 * nF) return;
-  const int a = (int)(t / nF);
-  const long rem = t % nF;
-  const int i = (int)(rem / F_out), f = (int)(rem % F_out);
-  T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
-  const double v = X[(size_t)i * 3 * F + (size_t)a * F + f];
-  o[(size_t)i * F_all + f_off + f] = (T)(shift ? v + shift[a * F + f] : v);
+__global__ void __launch_bounds__(256)
+    k_output_rm(int n, int F, int F_all, int f_off, const double* __restrict__ X, T* o0, T* o1,
+                T* o2, const double* __restrict__ shift, int F_out) {
+  const int per = 3 * F_out;
+  for (int i = blockIdx.x; i < n; i += gridDim.x)
+    for (int r = threadIdx.x; r < per; r += blockDim.x) {
+      const int a = r / F_out, f = r - a * F_out;
+      T* o = a == 0 ? o0 : (a == 1 ? o1 : o2);
+      const double v = __ldcs(X + (size_t)i * 3 * F + (size_t)a * F + f);
+      o[(size_t)i * F_all + f_off + f] = (T)(shift ? v + shift[a * F + f] : v);
+    }
 }
 
 template <typename T>
@@ -449,19 +518,18 @@ cudaError_t launch_rhs_rm(cudaStream_t s, int n, int F, int F_all, int f_off,
                           const uint32_t* lap_rp, const uint32_t* lap_ci, const int32_t* anchor_pos,
                           int n_c, const uint16_t* anchor_q, const float* anchor_rng,
                           int anchor_bits, const double* D, double* B, int* flags) {
-  const long total = 3L * n * F;
-  k_rhs_rm<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(n, F, 3 * F, F_all, f_off, lap_rp,
-                                                           lap_ci, anchor_pos,
-                                                           n_c, anchor_q, anchor_rng, anchor_bits,
-                                                           D, B, flags);
+  if (n <= 0 || F <= 0) return cudaSuccess;
+  const int W = 3 * F;
+  const dim3 grid((unsigned)((n + 7) / 8), (unsigned)((W + kRhsCols - 1) / kRhsCols));
+  k_rhs_rm<<<grid, 256, 0, s>>>(n, F, W, F_all, f_off, lap_rp, lap_ci, anchor_pos, n_c, anchor_q,
+                                anchor_rng, anchor_bits, D, B, flags);
   return cudaGetLastError();
 }
 
 cudaError_t launch_output_rm(cudaStream_t s, int n, int F, int F_all, int f_off, const double* X,
                              void* const out[3], bool f32, const double* shift, int F_out) {
   if (F_out < 0) F_out = F;
-  const long total = 3L * n * F_out;
-  const unsigned grid = (unsigned)((total + 255) / 256);
+  const unsigned grid = (unsigned)std::min<long>(n, 148L * 32);
   if (f32)
     k_output_rm<float><<<grid, 256, 0, s>>>(n, F, F_all, f_off, X, (float*)out[0], (float*)out[1],
                                             (float*)out[2], shift, F_out);

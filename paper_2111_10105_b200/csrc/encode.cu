@@ -258,54 +258,6 @@ __global__ void k_quant_rows(int k, int n, const unsigned long long* __restrict_
 
 // Anchor payload (codec.cpp:444-471): global min/max over the anchor
 // trajectories of one axis, widened, then quantised anchor-major.
-template <typename T>
-__global__ void __launch_bounds__(1024)
-    k_anchors(int n_c, int F, const uint32_t* __restrict__ idx, const T* __restrict__ x0,
-              const T* __restrict__ x1, const T* __restrict__ x2, int bits, float* rng,
-              uint16_t* __restrict__ q) {
-  const int a = blockIdx.x;
-  const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
-  const long total = (long)n_c * F;
-  double lo = INFINITY, hi = -INFINITY;
-  for (long t = threadIdx.x; t < total; t += blockDim.x) {
-    const double v = (double)X[(size_t)idx[t / F] * F + t % F];
-    lo = fmin(lo, v);
-    hi = fmax(hi, v);
-  }
-  __shared__ double slo[32], shi[32];
-  __shared__ float sf[2];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    slo[w] = lo;
-    shi[w] = hi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
-      lo = fmin(lo, slo[i]);
-      hi = fmax(hi, shi[i]);
-    }
-    float flo, fhi;
-    widened_range(lo, hi, &flo, &fhi);
-    sf[0] = flo;
-    sf[1] = fhi;
-    rng[2 * a] = flo;
-    rng[2 * a + 1] = fhi;
-  }
-  __syncthreads();
-  const QParams qp = make_qparams(sf[0], sf[1], bits);
-  uint16_t* o = q + (size_t)a * total;
-  for (long t = threadIdx.x; t < total; t += blockDim.x) {
-    const double v = (double)X[(size_t)idx[t / F] * F + t % F];
-    o[t] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v);
-  }
-}
-
 // ---- vertex-row shards: the anchor payload split in two ------
 // The global anchor range is a min/max over every anchor trajectory, so a
 // shard first reduces its own anchors into ordered keys (combined across
@@ -313,15 +265,17 @@ __global__ void __launch_bounds__(1024)
 // its anchors with the global widened range.  min/max are exact, so the
 // levels equal the single-GPU k_anchors bits.
 template <typename T>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(256)
     k_anchor_keys(int na, int F, const uint32_t* __restrict__ rows, const T* __restrict__ x0,
                   const T* __restrict__ x1, const T* __restrict__ x2,
                   unsigned long long* keys) {
-  const int a = blockIdx.x;
+  // grid (chunks, 3): axis = blockIdx.y, element range split over blockIdx.x
+  const int a = blockIdx.y;
   const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
   const long total = (long)na * F;
   double lo = INFINITY, hi = -INFINITY;
-  for (long t = threadIdx.x; t < total; t += blockDim.x) {
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
     const double v = (double)X[(size_t)rows[t / F] * F + t % F];
     lo = fmin(lo, v);
     hi = fmax(hi, v);
@@ -337,24 +291,28 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// Anchor quantisation (codec.cpp:444-471) from the exact range keys: every
+// CTA derives the same widened float range (min / max are order-free, so the
+// levels are those of a single-pass reduction).
 template <typename T>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(256)
     k_anchor_quant(int na, int F, const uint32_t* __restrict__ rows, const T* __restrict__ x0,
                    const T* __restrict__ x1, const T* __restrict__ x2, int bits,
                    const unsigned long long* __restrict__ keys, float* rng,
                    uint16_t* __restrict__ q) {
-  const int a = blockIdx.x;
+  const int a = blockIdx.y;
   const T* X = a == 0 ? x0 : (a == 1 ? x1 : x2);
   float flo, fhi;
   widened_range(key_to_double(keys[2 * a]), key_to_double(keys[2 * a + 1]), &flo, &fhi);
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     rng[2 * a] = flo;
     rng[2 * a + 1] = fhi;
   }
   const QParams qp = make_qparams(flo, fhi, bits);
   const long total = (long)na * F;
   uint16_t* o = q + (size_t)a * total;
-  for (long t = threadIdx.x; t < total; t += blockDim.x) {
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total;
+       t += (long)gridDim.x * blockDim.x) {
     const double v = (double)X[(size_t)rows[t / F] * F + t % F];
     o[t] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v);
   }
@@ -447,40 +405,48 @@ cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long 
   return cudaGetLastError();
 }
 
-cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
-                           const void* const x[3], bool f32, int bits, float* rng, uint16_t* q) {
-  if (f32)
-    k_anchors<float><<<3, 1024, 0, s>>>(n_c, F, idx, (const float*)x[0], (const float*)x[1],
-                                        (const float*)x[2], bits, rng, q);
-  else
-    k_anchors<double><<<3, 1024, 0, s>>>(n_c, F, idx, (const double*)x[0], (const double*)x[1],
-                                         (const double*)x[2], bits, rng, q);
-  return cudaGetLastError();
+static unsigned anchor_chunks(long total) {
+  const long c = (total + 4 * 256 - 1) / (4 * 256);  // ~4 elements per thread
+  return (unsigned)(c < 1 ? 1 : (c > 296 ? 296 : c));
 }
 
 cudaError_t launch_anchor_keys(cudaStream_t s, int na, int F, const uint32_t* rows,
                                const void* const x[3], bool f32, unsigned long long* keys) {
   if (na <= 0) return cudaSuccess;
+  const dim3 grid(anchor_chunks((long)na * F), 3);
   if (f32)
-    k_anchor_keys<float><<<3, 1024, 0, s>>>(na, F, rows, (const float*)x[0], (const float*)x[1],
-                                            (const float*)x[2], keys);
+    k_anchor_keys<float><<<grid, 256, 0, s>>>(na, F, rows, (const float*)x[0], (const float*)x[1],
+                                              (const float*)x[2], keys);
   else
-    k_anchor_keys<double><<<3, 1024, 0, s>>>(na, F, rows, (const double*)x[0],
-                                             (const double*)x[1], (const double*)x[2], keys);
+    k_anchor_keys<double><<<grid, 256, 0, s>>>(na, F, rows, (const double*)x[0],
+                                               (const double*)x[1], (const double*)x[2], keys);
   return cudaGetLastError();
 }
 
 cudaError_t launch_anchor_quant(cudaStream_t s, int na, int F, const uint32_t* rows,
                                 const void* const x[3], bool f32, int bits,
                                 const unsigned long long* keys, float* rng, uint16_t* q) {
+  const dim3 grid(anchor_chunks((long)na * F), 3);
   if (f32)
-    k_anchor_quant<float><<<3, 1024, 0, s>>>(na, F, rows, (const float*)x[0], (const float*)x[1],
-                                             (const float*)x[2], bits, keys, rng, q);
+    k_anchor_quant<float><<<grid, 256, 0, s>>>(na, F, rows, (const float*)x[0], (const float*)x[1],
+                                               (const float*)x[2], bits, keys, rng, q);
   else
-    k_anchor_quant<double><<<3, 1024, 0, s>>>(na, F, rows, (const double*)x[0],
-                                              (const double*)x[1], (const double*)x[2], bits, keys,
-                                              rng, q);
+    k_anchor_quant<double><<<grid, 256, 0, s>>>(na, F, rows, (const double*)x[0],
+                                                (const double*)x[1], (const double*)x[2], bits, keys,
+                                                rng, q);
   return cudaGetLastError();
+}
+
+// Single-GPU anchors: range keys over many CTAs, then the quantisation
+// (the former one-CTA-per-axis kernel ran on 3 SMs).  keys: 3 pairs.
+cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
+                           const void* const x[3], bool f32, int bits, float* rng, uint16_t* q,
+                           unsigned long long* keys) {
+  if (n_c <= 0) return cudaSuccess;
+  cudaError_t e = launch_init_keys(s, 3, keys);
+  if (e == cudaSuccess) e = launch_anchor_keys(s, n_c, F, idx, x, f32, keys);
+  if (e == cudaSuccess) e = launch_anchor_quant(s, n_c, F, idx, x, f32, bits, keys, rng, q);
+  return e;
 }
 
 cudaError_t launch_flip_min_keys(cudaStream_t s, long rows, unsigned long long* keys) {

@@ -707,7 +707,8 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_w = (double*)get(3 * (size_t)F * 8);
   p->d_start = (double*)get(3 * (size_t)F * kk * 8);
   p->d_C = (double*)get(3 * kk * std::max<size_t>(n, kk) * 8);
-  p->d_keys = (unsigned long long*)get(3 * kk * 2 * 8);
+  // row (min, max) keys of the projection, then the 3 anchor-range pairs
+  p->d_keys = (unsigned long long*)get((3 * kk + 3) * 2 * 8);
   p->d_flags = (int*)get(8 * sizeof(int));
   p->d_pf_flag = (int*)get(sizeof(int));
   p->d_dict_q = (uint16_t*)get(3 * FF * 2);

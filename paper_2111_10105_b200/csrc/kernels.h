@@ -31,7 +31,8 @@ cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long 
                               uint8_t* rbits, uint16_t* q);
 // Anchor quantisation (codec.cpp:444-471), one CTA per axis.
 cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
-                           const void* const x[3], bool f32, int bits, float* rng, uint16_t* q);
+                           const void* const x[3], bool f32, int bits, float* rng, uint16_t* q,
+                           unsigned long long* keys);
 // Vertex-row shards: anchor min/max keys of the rows[na] local
 // anchor rows (keys: 3 x (min, max) ordered keys), then their levels with
 // the (allreduced) global widened range -> rng (3 x 2), q (3 x na x F).

@@ -358,7 +358,7 @@ static Status enqueue_encode_blocks_t(dmcg_plan* p, const void* const x[3]) {
   // anchors (codec.cpp:444-471): the padded frames repeat the last one, so
   // the range and the first F_in levels equal those of the unpadded input
   DMCG_TRY(launch_anchors(s, (int)p->n_c, Fp, p->d_anchor_idx, xs, f32, p->anchor_bits,
-                          p->d_anchor_rng, p->d_anchor_q));
+                          p->d_anchor_rng, p->d_anchor_q, p->d_keys + 6L * k));
   // encode_dictionaries (codec.cpp:290-328)
   DMCG_TRY(launch_dict_encode_blocks(s, nb, kf, p->dict_bits, p->diff_bits, p->d_U, p->d_bwork,
                                      p->d_dict_q, p->d_diff_rng));
@@ -465,7 +465,7 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefacto
   // K5b anchors (codec.cpp:444-471) or the per-frame means (codec.cpp:432-441).
   if (p->n_c)
     DMCG_TRY(launch_anchors(s, (int)p->n_c, F, p->d_anchor_idx, x, f32, p->anchor_bits,
-                            p->d_anchor_rng, p->d_anchor_q));
+                            p->d_anchor_rng, p->d_anchor_q, p->d_keys + 6L * k));
   if (variant_uses_means(p->variant))
     DMCG_TRY(launch_frame_means(s, n, F, x, f32, p->d_colsum, p->d_means));
   // K5a dictionary levels (encode_dictionaries first block), after the
