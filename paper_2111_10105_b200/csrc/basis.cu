@@ -7,6 +7,7 @@
 // reductions run in parallel order and use FMA, so results agree with the
 // oracle to rounding, not bit for bit (P3).
 #include <mutex>
+#include <string>
 #include <cfloat>
 #include <cstdio>
 #include <cstdlib>
@@ -445,8 +446,17 @@ __device__ void warp_gemm_tn(int M, int N, int K, PA A, int lda, PB B, int ldb, 
 // v = x / (x0 - beta)); the GPU multiplies by the reciprocal, a 1-ulp
 // difference inside the P3 tolerance.
 // ---------------------------------------------------------------------------
+__device__ long long g_pan_prof[8];
+__device__ long long g_pan_last;
 #ifndef PANEL_STAMP
-#define PANEL_STAMP(i)
+#define PANEL_STAMP(i)                                            \
+  do {                                                            \
+    if (lane == 0 && blockIdx.x == 32) {                          \
+      const long long _t = clock64();                             \
+      if ((i) > 0) g_pan_prof[(i)] += _t - g_pan_last;            \
+      g_pan_last = _t;                                            \
+    }                                                             \
+  } while (0)
 #endif
 #ifndef FACT_STAMP
 #define FACT_STAMP(i)
@@ -716,48 +726,73 @@ __device__ __forceinline__ double vfetch(const double* col, int g, int M, int di
 template <int PW, typename PZ, typename PY>
 __device__ void wy_vty(const PanelV<PZ>& V, int M, int pb, int nv, PY Y, int ldy, int nc,
                        double* W) {
+  // one 8-column tile of W per warp group, the M rows split over the warps
+  // left (ks groups), partial tiles summed in split order (deterministic)
+  __shared__ double vty_part[kOiThreads / 32][64];  // callers run kOiThreads threads
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int i = lane >> 2, q = lane & 3;
   const int ic = i < pb ? i : pb - 1;
   const double* acol = V.Z + (V.c0 + ic) * V.ld + V.c0;
   const bool avalid = i < pb;
-  for (int ct = warp; ct * 8 < nc; ct += nw) {
+  const int nct = (nc + 7) / 8;
+  const int ks = nct >= nw ? 1 : nw / nct;
+  const int nch = (M + 15) / 16;
+  for (int wt = warp; wt < nct * ks; wt += nw) {
+    const int ct = wt % nct, kc = wt / nct;
+    const int ch0 = (int)((long)nch * kc / ks), ch1 = (int)((long)nch * (kc + 1) / ks);
     const int c = ct * 8 + i;
     const bool bvalid = c < nc;
     const int cc = bvalid ? c : nc - 1;
     const double* bcol = cc < nv ? V.Z + (V.c0 + cc) * V.ld + V.c0 : Y + (cc - nv) * ldy;
     const int bdiag = cc < nv ? cc : -1;
     double acc[4][2] = {};
-    double av[4], bv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      av[u] = vfetch(acol, 4 * u + q, M, ic, avalid);
-      bv[u] = vfetch(bcol, 4 * u + q, M, bdiag, bvalid);
-    }
-    for (int k0 = 16; k0 < M + 16; k0 += 16) {
-      double an[4], bn[4];
+    if (ch0 < ch1) {
+      double av[4], bv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        an[u] = vfetch(acol, k0 + 4 * u + q, M, ic, avalid);
-        bn[u] = vfetch(bcol, k0 + 4 * u + q, M, bdiag, bvalid);
+        av[u] = vfetch(acol, 16 * ch0 + 4 * u + q, M, ic, avalid);
+        bv[u] = vfetch(bcol, 16 * ch0 + 4 * u + q, M, bdiag, bvalid);
       }
+      for (int ch = ch0 + 1; ch <= ch1; ++ch) {
+        const int k0 = 16 * ch;
+        double an[4], bn[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) dmma884(acc[u], av[u], bv[u]);
+        for (int u = 0; u < 4; ++u) {
+          an[u] = vfetch(acol, k0 + 4 * u + q, M, ic, avalid);
+          bn[u] = vfetch(bcol, k0 + 4 * u + q, M, bdiag, bvalid);
+        }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        av[u] = an[u];
-        bv[u] = bn[u];
+        for (int u = 0; u < 4; ++u) dmma884(acc[u], av[u], bv[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          av[u] = an[u];
+          bv[u] = bn[u];
+        }
       }
     }
+    if (ks == 1) {
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int co = ct * 8 + q * 2 + e;
-      if (i < PW && co < nc) W[i * nc + co] = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
+      for (int e = 0; e < 2; ++e) {
+        const int co = ct * 8 + q * 2 + e;
+        if (i < PW && co < nc) W[i * nc + co] = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        vty_part[wt][i * 8 + q * 2 + e] = (acc[0][e] + acc[1][e]) + (acc[2][e] + acc[3][e]);
+    }
+  }
+  if (ks > 1) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < PW * nc; t += blockDim.x) {
+      const int r = t / nc, co = t % nc, ct = co / 8;
+      double sum = 0.0;
+      for (int kc = 0; kc < ks; ++kc) sum += vty_part[ct + kc * nct][r * 8 + co % 8];
+      W[r * nc + co] = sum;
     }
   }
 }
 
-// W <- T^T W (trans) or T W, T upper triangular (PW x PW row-major).
 template <int PW>
 __device__ void wy_tw(const double* T, int pb, double* W, int ldw, int nc, bool trans) {
   for (int c = threadIdx.x; c < nc; c += blockDim.x) {
@@ -1160,6 +1195,125 @@ __global__ void k_fill_zero(double* p, long count) {
   if (t < count) p[t] = 0.0;
 }
 
+// Householder factor of a whole PW-column block by all kOiThreads threads
+// of the CTA (the rows split R per thread: g = tid + 256 t), with its dlarft
+// triangle T formed in the same reductions as warp_panel_qr_T: at column j
+// one block reduction sums the tail norm, x^T y_l for the later columns and
+// x^T v_l for the earlier reflectors (G(l, j) = v_l(j) + rinv x^T v_l).  Two
+// barriers per column instead of the blocked panel sequence (4-column
+// register panels + V^T Y + T + T W + update per panel).  Same reflector
+// formulas as warp_panel_qr_T / the oracle's householder_factor; the
+// reductions sum in a different order (rounding-level differences, P3).
+template <int R, int PW>
+__device__ void cta_panel_qr_T(double* Z, int m, int ld, int pb, double* tau, double* T) {
+  __shared__ double red[kOiThreads / 32][PW + 1];
+  __shared__ double tot[2 * PW + 1];  // [0, PW]: sums, [PW + 1, 2 PW]: row j of the block
+  const unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  double a[R][PW];
+#pragma unroll
+  for (int t = 0; t < R; ++t)
+#pragma unroll
+    for (int c = 0; c < PW; ++c) {
+      const int g = tid + kOiThreads * t;
+      a[t][c] = (c < pb && g < m) ? Z[c * ld + g] : 0.0;
+    }
+  double tv[PW], tr[PW];
+#pragma unroll
+  for (int i = 0; i < PW; ++i) tr[i] = tv[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < PW; ++j) {
+    double r[PW + 1];
+#pragma unroll
+    for (int l = 0; l <= PW; ++l) r[l] = 0.0;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int g = tid + kOiThreads * t;
+      const double x = g > j ? a[t][j] : 0.0;
+      r[PW] = fma(x, x, r[PW]);
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l != j) r[l] = fma(x, a[t][l], r[l]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r[PW] += __shfl_xor_sync(FULL, r[PW], o);
+#pragma unroll
+      for (int l = 0; l < PW; ++l)
+        if (l != j) r[l] += __shfl_xor_sync(FULL, r[l], o);
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int l = 0; l <= PW; ++l) red[warp][l] = r[l];
+    if (tid == j)  // row j (j < PW <= 256: thread j, t = 0)
+#pragma unroll
+      for (int l = 0; l < PW; ++l) tot[PW + 1 + l] = a[0][l];
+    __syncthreads();
+    if (tid <= PW) {
+      double sum = 0.0;
+      for (int w = 0; w < nw; ++w) sum += red[w][tid];
+      tot[tid] = sum;
+    }
+    __syncthreads();
+    const double tail = tot[PW];
+    const double x0 = tot[PW + 1 + j];
+    double rinv = 0.0, tj = 0.0, beta = x0;
+    if (tail > DBL_MIN) {
+      const double s2 = x0 * x0 + tail;
+      const double rs = rsqrt(s2);
+      const double nrm = s2 * rs;
+      beta = x0 >= 0.0 ? -nrm : nrm;
+      const double ibb = x0 >= 0.0 ? -rs : rs;
+      rinv = __drcp_rn(x0 - beta);
+      tj = (beta - x0) * ibb;
+    }
+    if (tid < PW) {  // thread l extends row l of T
+      double acc = 0.0;
+#pragma unroll
+      for (int mm = 0; mm < PW; ++mm)
+        if (mm < j && mm >= tid) acc = fma(tr[mm], fma(rinv, tot[mm], tot[PW + 1 + mm]), acc);
+      const double tl = tid < j ? -tj * acc : (tid == j ? tj : 0.0);
+      tr[j] = j < pb ? tl : 0.0;
+    }
+    double sl[PW];
+#pragma unroll
+    for (int l = 0; l < PW; ++l) sl[l] = l > j ? tj * fma(rinv, tot[l], tot[PW + 1 + l]) : 0.0;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int g = tid + kOiThreads * t;
+      if (g > j) a[t][j] *= rinv;
+    }
+    if (tid == j) a[0][j] = beta;
+    tv[j] = tj;
+#pragma unroll
+    for (int l = 0; l < PW; ++l) {
+      if (l <= j) continue;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int g = tid + kOiThreads * t;
+        if (g > j) a[t][l] = fma(-sl[l], a[t][j], a[t][l]);
+      }
+      if (tid == j) a[0][l] -= sl[l];
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < R; ++t)
+#pragma unroll
+    for (int c = 0; c < PW; ++c) {
+      const int g = tid + kOiThreads * t;
+      if (c < pb && g < m) Z[c * ld + g] = a[t][c];
+    }
+  if (tid == 0)
+#pragma unroll
+    for (int j = 0; j < PW; ++j)
+      if (j < pb) tau[j] = tv[j];
+  if (tid < PW)
+#pragma unroll
+    for (int i = 0; i < PW; ++i) T[tid * PW + i] = tid < pb ? tr[i] : 0.0;
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // Column-distributed orthogonal iterations (k_oi_cluster): the cluster's cs
 // CTAs of one axis each own a block of B columns of Z and Q (F x B in
@@ -1236,24 +1390,26 @@ __device__ void blk_vty(const double* Vb, int ldv, int nb, const double* Yb, int
     for (int e = 0; e < 2; ++e) part[warp * 64 + i * 8 + q * 2 + e] = acc[0][e] + acc[1][e];
   }
   __syncthreads();
-  if (T) {  // W = T^T (V^T Y) or T (V^T Y): one thread per column
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-      double w[B];
+  if (T) {  // W = T^T (V^T Y) or T (V^T Y): the partial sums, then one output per thread
+    double wsum = 0.0;
+    const int t = threadIdx.x;
+    const bool own = t < B * nc;
+    const int r = own ? t / nc : 0, c = own ? t % nc : 0;
+    if (own) {
+      const int tile = (r / 8) + TR * (c / 8);
+      for (int kc = 0; kc < nk; ++kc) wsum += part[(tile + kc * ntile) * 64 + (r % 8) * 8 + (c % 8)];
+      if (r >= nb) wsum = 0.0;
+    }
+    __syncthreads();
+    if (own) part[r * B + c] = wsum;  // w(l, c) at part[l B + c]
+    __syncthreads();
+    for (int u = threadIdx.x; u < nb * nc; u += blockDim.x) {
+      const int i = u / nc, cc = u % nc;
+      double acc = 0.0;
 #pragma unroll
-      for (int r = 0; r < B; ++r) {
-        const int tile = (r / 8) + TR * (c / 8);
-        double s = 0.0;
-        for (int kc = 0; kc < nk; ++kc) s += part[(tile + kc * ntile) * 64 + (r % 8) * 8 + (c % 8)];
-        w[r] = r < nb ? s : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < B; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < B; ++l)
-          if (trans ? (l <= i) : (l >= i)) acc = fma(trans ? T[l * B + i] : T[i * B + l], w[l], acc);
-        if (i < nb) W[i * B + c] = acc;
-      }
+      for (int l = 0; l < B; ++l)
+        if (trans ? (l <= i) : (l >= i)) acc = fma(trans ? T[l * B + i] : T[i * B + l], part[l * B + cc], acc);
+      W[i * B + cc] = acc;
     }
   } else {
     for (int t = threadIdx.x; t < nb * nc; t += blockDim.x) {
@@ -1313,14 +1469,16 @@ __device__ void blk_apply(const double* Vb, int ldv, int nb, const double* T, bo
                           double* Yb, int ldy, int nc, int M, double* W, double* part,
                           double* vstage, double* tstage, bool remote) {
   if (remote) {
-    constexpr int U = 8;
+    // Vb / T: the producer's mirror in global memory (L2; __ldcg: the lines
+    // change every round, L1 is not coherent), every thread's loads in flight
+    constexpr int U = 16;
     const int total = (nb - 1) * ldv + M;  // columns of M rows, ld ldv
     for (int t0 = threadIdx.x; t0 < total; t0 += U * blockDim.x) {
       double v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int t = t0 + u * blockDim.x;
-        v[u] = t < total ? Vb[t] : 0.0;
+        v[u] = t < total ? __ldcg(Vb + t) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1328,7 +1486,7 @@ __device__ void blk_apply(const double* Vb, int ldv, int nb, const double* T, bo
         if (t < total) vstage[t] = v[u];
       }
     }
-    for (int t = threadIdx.x; t < B * B; t += blockDim.x) tstage[t] = T[t];
+    for (int t = threadIdx.x; t < B * B; t += blockDim.x) tstage[t] = __ldcg(T + t);
     __syncthreads();
     Vb = vstage;
     T = tstage;
@@ -1983,10 +2141,21 @@ __global__ void __launch_bounds__(kJbThreads, 1)
 
 __device__ long long g_oic_prof[64 * 8];  // per-CTA cycle split of k_oi_cluster (DMCG_DEBUG)
 
+// Mirror of every CTA's published block reflector (V rows c0.. of its
+// block, T) in global memory, per axis and rank: the later CTAs copy it
+// from L2 instead of from the producer's shared memory (up to 15 CTAs read
+// each block; over DSMEM they all land on the producer's SM).
+__host__ __device__ constexpr size_t oi_mirror_stride(int ld, int B) { return (size_t)ld * B + (size_t)B * B; }
+
+// DMCG_OI_PANELS=blocked: the former 4-column register panels + blocked
+// update for B = 16 blocks (tests compare the two factorizations)
+__constant__ int c_oi_blocked = 0;
+__device__ __forceinline__ bool oi_blocked_panels() { return c_oi_blocked != 0; }
+
 template <int MAXR, int B>
 __global__ void __launch_bounds__(kOiThreads)
     k_oi_cluster(int F, int k, int rounds, const double* __restrict__ Rall,
-                 const double* __restrict__ start, double* Qall, double* Hall) {
+                 const double* __restrict__ start, double* Qall, double* Hall, double* mirror) {
   extern __shared__ double dyn[];
   __shared__ double s_tau[B];
   __shared__ double s_T[B * B];
@@ -2004,6 +2173,10 @@ __global__ void __launch_bounds__(kOiThreads)
   double* Ts = Vs + (size_t)ld * B;   // and its T
   double* scr = Ts + B * B;           // wqr_factor scratch (B > PW)
   const int c0 = rank * B, nb = min(B, k - c0);
+  const size_t mstride = oi_mirror_stride(ld, B);
+  double* mir_axis = mirror + (size_t)b * cs * mstride;
+  auto mir_v = [&](int q) { return mir_axis + (size_t)q * mstride; };
+  auto mir_t = [&](int q) { return mir_axis + (size_t)q * mstride + (size_t)ld * B; };
   // Rall == nullptr: QR only (Q of the start matrices, no R Q / H) — one
   // round of the implicit X (X^T Q) iteration, whose products run as GEMMs
   const double* R = Rall ? Rall + (size_t)b * F * F : nullptr;
@@ -2029,9 +2202,7 @@ __global__ void __launch_bounds__(kOiThreads)
       __syncthreads();
       long long t1 = clock64();
       t_wait += t1 - t0;
-      const double* Vp = cl.map_shared_rank(Zb, p);
-      const double* Tp = cl.map_shared_rank(s_T, p);
-      blk_apply<B>(Vp + p * B, ld, B, Tp, true, Zb + p * B, ld, nb, F - p * B, s_W, s_part,
+      blk_apply<B>(mir_v(p), ld, B, mir_t(p), true, Zb + p * B, ld, nb, F - p * B, s_W, s_part,
                    Vs + p * B, Ts, true);
       t0 = clock64();
       t_app += t0 - t1;
@@ -2041,11 +2212,14 @@ __global__ void __launch_bounds__(kOiThreads)
       if (B == PW) {
         if (warp == 0) warp_panel_qr_T<MAXR, PW>(Zb + c0, F - c0, ld, nb, s_tau, s_T, lane);
         __syncthreads();
+      } else if (!oi_blocked_panels()) {
+        cta_panel_qr_T<(32 * MAXR + kOiThreads - 1) / kOiThreads, B>(Zb + c0, F - c0, ld, nb, s_tau,
+                                                                     s_T);
       } else {
         wqr_factor<MAXR>(Zb + c0, F - c0, ld, nb, s_tau, scr, nb);
         blk_vty<B>(Zb + c0, ld, nb, Zb + c0, ld, nb, true, F - c0, s_W, s_part);
       }
-      if (B != PW && warp == 0) {
+      if (B != PW && oi_blocked_panels() && warp == 0) {
         // dlarft row j on lane j from G = s_W (row-major, ld B)
         if (lane < B) {
           const int j = lane;
@@ -2069,7 +2243,20 @@ __global__ void __launch_bounds__(kOiThreads)
       }
       __syncthreads();
     }
-    if (threadIdx.x == 0) st_release_cluster(&s_ready, epoch);
+    // publish: the block's reflectors (rows c0.. of the own columns) and T
+    // to the global mirror, then the release flag
+    if (nb > 0) {
+      const int total = (B - 1) * ld + (F - c0);
+      double* mv = mir_v(rank);
+      for (int t = threadIdx.x; t < total; t += blockDim.x) mv[t] = Zb[c0 + t];
+      double* mt = mir_t(rank);
+      for (int t = threadIdx.x; t < B * B; t += blockDim.x) mt[t] = s_T[t];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_cluster(&s_ready, epoch);
+    }
     long long t1 = clock64();
     t_fac += t1 - t0;
     // ---- thin Q block: Q_c = H_0 ... H_c E_c ------------------------------
@@ -2080,9 +2267,9 @@ __global__ void __launch_bounds__(kOiThreads)
     __syncthreads();
     for (int p = rank; p >= 0 && nb > 0; --p) {
       const bool own = p == rank;
-      const double* Vp = own ? Zb : cl.map_shared_rank(Zb, p);
-      const double* Tp = own ? s_T : cl.map_shared_rank(s_T, p);
-      blk_apply<B>(Vp + p * B, ld, own ? nb : B, Tp, false, Qb + p * B, ld, nb, F - p * B, s_W,
+      const double* Vp = own ? Zb + p * B : mir_v(p);
+      const double* Tp = own ? s_T : mir_t(p);
+      blk_apply<B>(Vp, ld, own ? nb : B, Tp, false, Qb + p * B, ld, nb, F - p * B, s_W,
                    s_part, Vs + p * B, Ts, !own);
     }
     t0 = clock64();
@@ -2373,7 +2560,7 @@ static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int r
 template <int MAXR, int B>
 static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                      const double* R, const double* start, double* Q, double* H,
-                                     bool* launched) {
+                                     double* mirror, bool* launched) {
   *launched = false;
   const int cs = (k + B - 1) / B;
   constexpr int PW = QrPanel<MAXR>::PW;
@@ -2408,19 +2595,39 @@ static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, i
     cudaGetLastError();
     return cudaSuccess;
   }
+  {
+    // DMCG_OI_PANELS=blocked (experiments, tests): stream-ordered, so it is
+    // also legal inside a graph capture of the plan stream
+    static const int blocked = [] {
+      const char* e = getenv("DMCG_OI_PANELS");
+      return (e && std::string(e) == "blocked") ? 1 : 0;
+    }();
+    if (blocked) {
+      cudaError_t e = cudaMemcpyToSymbolAsync(c_oi_blocked, &blocked, sizeof(blocked), 0,
+                                              cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
   static const bool dbg = getenv("DMCG_DEBUG") != nullptr;
   if (dbg)
     fprintf(stderr, "dmcg: k_oi_cluster F=%d k=%d B=%d cluster %d smem %zu (max active %d)\n", F,
             k, B, cs, smem, nclusters);
-  e = cudaLaunchKernelEx(&cfg, k_oi_cluster<MAXR, B>, F, k, rounds, R, start, Q, H);
+  e = cudaLaunchKernelEx(&cfg, k_oi_cluster<MAXR, B>, F, k, rounds, R, start, Q, H, mirror);
   *launched = e == cudaSuccess;
   if (dbg && e == cudaSuccess) {
     long long h[64 * 8];
     cudaStreamSynchronize(s);
     cudaMemcpyFromSymbol(h, g_oic_prof, sizeof(h));
-    for (int c = 0; c < cs && c < 64; ++c)
+    for (int c = 0; c < cs && c < 64; ++c) {
+      if (c == 0) {
+        long long pp[8];
+        cudaMemcpyFromSymbol(pp, g_pan_prof, sizeof(pp));
+        fprintf(stderr, "  warp_panel_qr (cta 32): load %lld columns %lld store %lld\n", pp[1], pp[2],
+                pp[4]);
+      }
       fprintf(stderr, "  cta %d: wait %lld apply %lld factor %lld form %lld sync %lld rq %lld\n", c,
               h[8 * c], h[8 * c + 1], h[8 * c + 2], h[8 * c + 3], h[8 * c + 4], h[8 * c + 5]);
+    }
   }
   return e;
 }
@@ -2428,43 +2635,48 @@ static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, i
 template <int MAXR>
 static cudaError_t oi_cluster_dispatch(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                        const double* R, const double* start, double* Q, double* H,
-                                       bool* launched) {
+                                       double* mirror, bool* launched) {
   *launched = false;
   if (k <= 0 || k >= F) return cudaSuccess;
   static const int bsel = getenv("DMCG_OI_B") ? atoi(getenv("DMCG_OI_B")) : 0;  // experiments
   if (bsel == 16 && (k + 15) / 16 <= 16)
-    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
+    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched);
   if ((k + 7) / 8 <= 16)
-    return oi_cluster_launch<MAXR, 8>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
+    return oi_cluster_launch<MAXR, 8>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched);
   if ((k + 15) / 16 <= 16)
-    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, launched);
+    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched);
   return cudaSuccess;
 }
 
+size_t oi_mirror_doubles(int F, int nbatch) {
+  return (size_t)nbatch * 16 * oi_mirror_stride(odd_ld(F), 16);
+}
+
 cudaError_t launch_qr_cluster(cudaStream_t s, int nbatch, int F, int k, const double* Z,
-                              double* Q) {
+                              double* Q, double* mirror) {
   if (F > 512 || k <= 0 || k >= F) return cudaErrorInvalidValue;
   bool done = false;
   cudaError_t e = cudaSuccess;
-  if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
-  else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
-  else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
-  else e = oi_cluster_dispatch<16>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, &done);
+  if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, mirror, &done);
+  else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, mirror, &done);
+  else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, mirror, &done);
+  else e = oi_cluster_dispatch<16>(s, nbatch, F, k, 0, nullptr, Z, Q, nullptr, mirror, &done);
   if (e == cudaSuccess && !done) e = cudaErrorNotSupported;  // no cluster of this size fits
   return e;
 }
 
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
-                            const double* start, double* Q, double* H, double* work, double* scr) {
+                            const double* start, double* Q, double* H, double* work, double* scr,
+                            double* mirror) {
   if (F > 512) return cudaErrorInvalidValue;
   static const bool legacy = getenv("DMCG_OI_LEGACY") != nullptr;
   if (!legacy) {
     bool done = false;
     cudaError_t e = cudaSuccess;
-    if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
-    else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
-    else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
-    else e = oi_cluster_dispatch<16>(s, nbatch, F, k, rounds, R, start, Q, H, &done);
+    if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, &done);
+    else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, &done);
+    else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, &done);
+    else e = oi_cluster_dispatch<16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, &done);
     if (e != cudaSuccess || done) return e;
   }
   if (F <= 64) return oi_fused_impl<2>(s, nbatch, F, k, rounds, R, start, Q, H, work, scr);

@@ -704,6 +704,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->d_H = (double*)get(jac * 8);
   p->d_V = (double*)get(3 * FF * 8);
   p->d_qr_scr = (double*)get(3 * dmcg::qr_scratch_doubles((int)F, (int)kk) * 8);
+  p->d_oi_mirror = (double*)get(dmcg::oi_mirror_doubles((int)F, 3) * 8);
   p->d_w = (double*)get(3 * (size_t)F * 8);
   p->d_start = (double*)get(3 * (size_t)F * kk * 8);
   p->d_C = (double*)get(3 * kk * std::max<size_t>(n, kk) * 8);

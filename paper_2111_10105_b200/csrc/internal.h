@@ -232,6 +232,7 @@ struct dmcg_plan {
   double *d_Q = nullptr, *d_Z = nullptr, *d_tau = nullptr;  // 3 x F x k, 3 x F
   double *d_H = nullptr, *d_V = nullptr, *d_w = nullptr;    // jacobi work (3 x m2 x m2)
   double* d_qr_scr = nullptr;      // 3 x qr_scratch_doubles(F, k) blocked-QR scratch
+  double* d_oi_mirror = nullptr;   // oi_mirror_doubles(F, 3): published OI block reflectors
   double* d_start = nullptr;       // 3 x F x k OI start matrices
   double* d_C = nullptr;           // 3 x k x n coefficients
   unsigned long long* d_keys = nullptr;  // 3 x k x 2 (min,max) ordered keys

@@ -74,12 +74,16 @@ cudaError_t launch_canon_signs(cudaStream_t s, int nbatch, int m, int c0, int nc
 // x {Z = R Q; Q = qr(Z)}, then H = Q^T R Q (symmetrised); R Q is spread over a
 // cluster of CTAs per axis (Q doubles as its L2 staging buffer).  work:
 // nbatch * 2 (F|1) k doubles (used when the pair does not fit in shared memory).
+// mirror: oi_mirror_doubles(F, nbatch) doubles (the published block
+// reflectors, read by the other CTAs of the cluster from L2).
 cudaError_t launch_oi_fused(cudaStream_t s, int nbatch, int F, int k, int rounds, const double* R,
-                            const double* start, double* Q, double* H, double* work, double* scr);
+                            const double* start, double* Q, double* H, double* work, double* scr,
+                            double* mirror);
+size_t oi_mirror_doubles(int F, int nbatch);
 // Q (F x k per batch) = thin Householder Q of Z (same kernel as the fused
 // OI, QR only): one round of the implicit X (X^T Q) iteration.
 cudaError_t launch_qr_cluster(cudaStream_t s, int nbatch, int F, int k, const double* Z,
-                              double* Q);
+                              double* Q, double* mirror);
 // U[:, k:F] = columns k..F-1 of the full Householder Q of U[:, :k].
 cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
                             double* scr);

@@ -205,7 +205,7 @@ Status implicit_oi(dmcg_plan* p, const void* const x[3], int nrows, dmcg_comm* c
     if (sp > cap) sp = cap;
     return gemm_splits(nrows, (int)(sp < 1 ? 1 : sp), nullptr);
   };
-  DMCG_TRY(launch_qr_cluster(s, 3, F, k, p->d_start, p->d_Q));
+  DMCG_TRY(launch_qr_cluster(s, 3, F, k, p->d_start, p->d_Q, p->d_oi_mirror));
   for (int r = 0; r <= p->rounds; ++r) {
     // P = X Q: M = rows, N = k, K = F
     DMCG_TRY(launch_gemm(s, 3, nrows, k, F, 1, lxk, lq, StoreStrided{P, nk, 1L, (long)nrows}));
@@ -218,7 +218,7 @@ Status implicit_oi(dmcg_plan* p, const void* const x[3], int nrows, dmcg_comm* c
       Status st = comm_allreduce_sum_f64(comm, p->d_Z, 3 * (size_t)Fk, s);
       if (!st.good()) return st;
     }
-    DMCG_TRY(launch_qr_cluster(s, 3, F, k, p->d_Z, p->d_Q));
+    DMCG_TRY(launch_qr_cluster(s, 3, F, k, p->d_Z, p->d_Q, p->d_oi_mirror));
   }
   // H = P^T P: M = N = k, K = rows (split-K), symmetrised
   const int sh = splits_for(k, k);
@@ -252,7 +252,7 @@ Status basis(dmcg_plan* p, const void* const x[3] = nullptr, int nrows = 0,
     if (!st.good()) return st;
   } else {
     DMCG_TRY(launch_oi_fused(s, 3, F, k, p->rounds, p->d_R, p->d_start, p->d_Q, H, p->d_H,
-                             p->d_qr_scr));
+                             p->d_qr_scr, p->d_oi_mirror));
   }
   DMCG_TRY(record_event(p->ev[7], s));
   DMCG_TRY(launch_jacobi(s, 3, k, H, p->d_H, p->d_V, p->d_w, p->d_flags + 3));
