@@ -115,22 +115,33 @@ class CompressedAnimation:
         return (self.F + self.pad) // self.n_b
 
     @classmethod
-    def allocate(cls, n, F, k_l, n_c, faces, n_b=1, **kw):
+    def allocate(cls, n, F, k_l, n_c, faces, n_b=1, pinned=False, **kw):
+        """Zeroed arrays for an encode of this shape; pinned=True places the
+        payload arrays in page-locked host memory (DMA-speed download/upload,
+        for callers that reuse the object across encodes)."""
         c = cls(n, F, k_l, n_c, np.ascontiguousarray(faces, dtype=np.uint32), **kw)
+        if pinned:
+            import torch
+
+            def zeros(shape, dt):
+                t = torch.zeros(shape, dtype=getattr(torch, np.dtype(dt).name), pin_memory=True)
+                return t.numpy()
+        else:
+            zeros = np.zeros
         c.n_b = max(int(n_b), 1)
         c.pad = (c.n_b - F % c.n_b) % c.n_b if c.n_b > 1 else 0
         kf = c.k_f
         rows = max(k_l, 1) * c.n_b
-        c.dict_q = [np.zeros((F, F) if c.n_b == 1 else (c.n_b, kf, kf), np.uint16)
+        c.dict_q = [zeros((F, F) if c.n_b == 1 else (c.n_b, kf, kf), np.uint16)
                     for _ in range(3)]
         c.diff_min = [np.zeros(max(c.n_b - 1, 1), np.float32) for _ in range(3)]
         c.diff_max = [np.zeros(max(c.n_b - 1, 1), np.float32) for _ in range(3)]
         c.row_min = [np.zeros(rows, np.float32) for _ in range(3)]
         c.row_max = [np.zeros(rows, np.float32) for _ in range(3)]
         c.row_bits = [np.zeros(rows, np.uint8) for _ in range(3)]
-        c.coeff_q = [np.zeros((rows, n), np.uint16) for _ in range(3)]
+        c.coeff_q = [zeros((rows, n), np.uint16) for _ in range(3)]
         c.anchor_idx = np.zeros(max(n_c, 1), np.uint32)
-        c.anchor_q = [np.zeros((max(n_c, 1), F), np.uint16) for _ in range(3)]
+        c.anchor_q = [zeros((max(n_c, 1), F), np.uint16) for _ in range(3)]
         c.means = [np.zeros(F, np.float32) for _ in range(3)]
         return c
 
@@ -207,8 +218,11 @@ class Codec:
     def handle(self):
         return self._ctx
 
-    def encode(self, seq, cfg: EncoderConfig) -> CompressedAnimation:
-        """dmc::encode (include/dmc/codec.hpp:90; src/codec.cpp:351-473)."""
+    def encode(self, seq, cfg: EncoderConfig, out: Optional[CompressedAnimation] = None
+               ) -> CompressedAnimation:
+        """dmc::encode (include/dmc/codec.hpp:90; src/codec.cpp:351-473).  `out`:
+        a CompressedAnimation of this shape to fill (e.g. allocate(..., pinned=True),
+        reused across calls); a new one is allocated otherwise."""
         axes = [np.ascontiguousarray(a) for a in seq.axes]
         dt = L.DMCG_F32 if axes[0].dtype == np.float32 else L.DMCG_F64
         axes = [a.astype(np.float32 if dt else np.float64, copy=False) for a in axes]
@@ -223,9 +237,16 @@ class Codec:
         cc = cfg.to_c()
         sizes = L.DmcgSizes()
         L.lib().dmcg_encoded_sizes(n, F, ctypes.byref(cc), ctypes.byref(sizes))
-        out = CompressedAnimation.allocate(n, F, cfg.k_l, sizes.anchor_idx, faces, n_b=cfg.n_b,
-                                           anchor_bits=cfg.anchor_bits, dict_bits=cfg.dict_bits,
-                                           diff_bits=cfg.diff_bits, variant=cfg.variant)
+        if out is None:
+            out = CompressedAnimation.allocate(n, F, cfg.k_l, sizes.anchor_idx, faces, n_b=cfg.n_b,
+                                               anchor_bits=cfg.anchor_bits, dict_bits=cfg.dict_bits,
+                                               diff_bits=cfg.diff_bits, variant=cfg.variant)
+        else:
+            assert (out.n, out.F, out.k_l, out.n_c, out.n_b) == (n, F, cfg.k_l, sizes.anchor_idx,
+                                                                 max(cfg.n_b, 1))
+            out.faces = faces
+            out.anchor_bits, out.dict_bits = cfg.anchor_bits, cfg.dict_bits
+            out.diff_bits, out.variant = cfg.diff_bits, cfg.variant
         e = out.to_c()
         _check(self._ctx, L.lib().dmcg_encode(self._ctx, ctypes.byref(s), ctypes.byref(cc),
                                               ctypes.byref(e)))

@@ -744,7 +744,10 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   p->ev_pf_join = ctx->take_event(false);
   p->ev_pf0 = ctx->take_event(true);
   p->ev_pf1 = ctx->take_event(true);
-  cudaStream_t s = ctx->stream;
+  // the plan's (pageable) uploads go on the side stream and are waited for
+  // here: a drop-in encode has already queued its input H2D on ctx->stream,
+  // which keeps running under the host-side plan work
+  cudaStream_t s = ctx->aux;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
   };

@@ -451,7 +451,9 @@ def test_oi_paths_agree(name):
     outs = []
     for tag, extra in (("dist", {}), ("rows8", {"DMCG_OI_LEGACY": "1"}),
                        ("one", {"DMCG_OI_LEGACY": "1", "DMCG_OI_CLUSTER": "1"}),
-                       ("jacc", {"DMCG_JACOBI_CLUSTER": "1"})):
+                       ("jacc", {"DMCG_JACOBI_CLUSTER": "1"}),
+                       ("b16", {"DMCG_OI_B": "16"}),
+                       ("b16blocked", {"DMCG_OI_B": "16", "DMCG_OI_PANELS": "blocked"})):
         path = f"/tmp/dmcg_oi_{name}_{tag}.npy"
         env = dict(os.environ, **extra)
         r = subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env,
@@ -462,6 +464,10 @@ def test_oi_paths_agree(name):
     assert np.abs(outs[0] - outs[1]).max() <= 1
     assert np.abs(outs[0] - outs[2]).max() <= 1
     assert np.abs(outs[0] - outs[3]).max() <= 1   # cluster Jacobi (Rayleigh-Ritz)
+    # 16-column blocks: the whole-CTA block factor (cta_panel_qr_T, the c3
+    # path) and the blocked 4-column register panels
+    assert np.abs(outs[0] - outs[4]).max() <= 1
+    assert np.abs(outs[0] - outs[5]).max() <= 1
 
 
 @pytest.mark.parametrize("name", ["c0", "c1"])
