@@ -1340,6 +1340,52 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   if (!ctx || !seq || !cfg || !out) return DMCG_E_CONFIG;
   cudaSetDevice(ctx->device);
   PhaseTimer tm("encode");
+  {
+    // The decoder's analysis of this mesh (normal matrix + symbolic
+    // Cholesky), started first on a host thread: it needs only the faces and
+    // the anchor set (dmcg_select_anchors is a function of n and the config),
+    // so it runs under the whole encode (input H2D, plan, kernels, download).
+    ctx->pending.reset();
+    static const bool off = std::getenv("DMCG_NO_OVERLAP") != nullptr;
+    if (!off && cfg->variant != DMCG_V2V && seq->faces && seq->n_faces && seq->n) {
+      auto pa = std::make_unique<PendingAnalysis>();
+      pa->n = seq->n;
+      pa->n_faces = seq->n_faces;
+      pa->faces_hash = hash_faces(seq->faces, seq->n_faces);
+      pa->reduced = variant_uses_means(cfg->variant);
+      if (!pa->reduced) {
+        const uint32_t n_c = dmcg_anchor_count(seq->n, cfg->anchor_fraction);
+        pa->anchors.resize(n_c);
+        if (n_c == 0 || dmcg_select_anchors(seq->n, n_c, cfg->anchor_strategy, cfg->seed,
+                                            pa->anchors.data()) != DMCG_OK)
+          pa.reset();
+      }
+      if (pa) {
+        std::vector<uint32_t> faces(seq->faces, seq->faces + 3 * (size_t)seq->n_faces);
+        PendingAnalysis* raw = pa.get();
+        pa->th = std::thread([raw, faces = std::move(faces)] {
+          const auto t0 = std::chrono::steady_clock::now();
+          MeshHost& m = raw->mesh;
+          if (!build_mesh(faces.data(), raw->n_faces, raw->n, &m).good()) {
+            raw->failed = true;
+            return;
+          }
+          m.anchor_pos.assign(raw->n, -1);
+          for (uint32_t t = 0; t < raw->anchors.size(); ++t)
+            m.anchor_pos[raw->anchors[t]] = (int32_t)t;
+          m.anchors = raw->anchors;
+          if (raw->reduced)
+            build_reduced_normal(&m);
+          else
+            build_normal_matrix(&m);
+          chol_analyze(raw->n - (raw->reduced ? 1 : 0), m.m_rp, m.m_ci, m.m_val, &raw->chol);
+          raw->seconds =
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        });
+        ctx->pending = std::move(pa);
+      }
+    }
+  }
   // The input upload goes first, into pool buffers: with pinned host memory
   // it runs on the copy engine while the host builds the mesh (CSR,
   // validation, anchors) for the plan below.
@@ -1371,35 +1417,10 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
                                nullptr, 0, &p);
   if (!st.good()) return ctx->set_error(st);
-  {  // the decoder's analysis of this mesh, overlapped with the GPU encode
+  // the early analysis keys on the plan's anchor set: drop it if they differ
+  if (ctx->pending && !std::equal(ctx->pending->anchors.begin(), ctx->pending->anchors.end(),
+                                  p->mesh.anchors.begin(), p->mesh.anchors.end()))
     ctx->pending.reset();
-    static const bool off = std::getenv("DMCG_NO_OVERLAP") != nullptr;
-    if (!off && cfg->variant != DMCG_V2V) {  // v2v decodes without a solve
-      auto pa = std::make_unique<PendingAnalysis>();
-      pa->n = seq->n;
-      pa->n_faces = seq->n_faces;
-      pa->faces_hash = hash_faces(seq->faces, seq->n_faces);
-      pa->anchors = p->mesh.anchors;
-      pa->mesh.n = p->mesh.n;
-      pa->mesh.lap_rp = p->mesh.lap_rp;
-      pa->mesh.lap_ci = p->mesh.lap_ci;
-      pa->mesh.anchor_pos = p->mesh.anchor_pos;
-      pa->reduced = variant_uses_means(cfg->variant);
-      PendingAnalysis* raw = pa.get();
-      pa->th = std::thread([raw] {
-        const auto t0 = std::chrono::steady_clock::now();
-        if (raw->reduced)
-          build_reduced_normal(&raw->mesh);
-        else
-          build_normal_matrix(&raw->mesh);
-        chol_analyze(raw->n - (raw->reduced ? 1 : 0), raw->mesh.m_rp, raw->mesh.m_ci,
-                     raw->mesh.m_val, &raw->chol);
-        raw->seconds =
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      });
-      ctx->pending = std::move(pa);
-    }
-  }
   tm.lap("plan");
   if (st.good()) st = plan_encode(p, d_in);
   tm.lap("h2d+kernels");
@@ -1479,6 +1500,7 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
               pa->faces_hash == hash_faces(in->faces, in->n_faces)))
     pa.reset();
   if (pa && pa->th.joinable()) pa->th.join();
+  if (pa && pa->failed) pa.reset();
   dmcg_plan* p = nullptr;
   Status st = plan_create_impl(ctx, in->n, in->F, out_dtype, in->faces, in->n_faces, &cfg,
                                in->anchor_idx, in->n_c, &p, pa ? &pa->mesh : nullptr, false);

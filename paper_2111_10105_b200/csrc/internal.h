@@ -96,6 +96,7 @@ struct PendingAnalysis {
   MeshHost mesh;    // lap_rp / lap_ci / anchor_pos in, m_rp / m_ci / m_val out
   CholPlan chol;
   double seconds = 0.0;
+  bool failed = false;  // the mesh did not validate (the encode reports it)
   std::thread th;
   ~PendingAnalysis() {
     if (th.joinable()) th.join();
