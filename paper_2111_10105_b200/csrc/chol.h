@@ -48,8 +48,12 @@ struct CholPlan {
 };
 
 // M given as a symmetric CSR (rows sorted, diagonal present).
+// g_rp / g_ci (optional): the 1-ring graph whose square is M's pattern (the
+// mesh Laplacian's structure), used for a cheaper nested-dissection ordering.
 void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector<uint32_t>& ci,
-                  const std::vector<float>& val, CholPlan* plan);
+                  const std::vector<float>& val, CholPlan* plan,
+                  const std::vector<uint32_t>* g_rp = nullptr,
+                  const std::vector<uint32_t>* g_ci = nullptr);
 
 // CPU reference numerics over the same structures (tests / debugging).
 // F: front_off[nsup] doubles, Linv: inv_off[nsup] doubles.  Returns false if

@@ -12,6 +12,8 @@
 #include <atomic>
 #include <functional>
 #include <thread>
+#include <mutex>
+#include <map>
 
 #include "chol.h"
 #include "par.h"
@@ -38,8 +40,12 @@ struct Graph {
 // id the other range never holds.
 class NestedDissection {
  public:
-  explicit NestedDissection(const Graph& g)
-      : g_(g), part_(g.n, 0), level_(g.n, -1), queue_(g.n), idx_(g.n), tmp_(g.n) {}
+  // wide: g is the 1-ring graph G of a matrix whose pattern is G^2 (M = L^T L
+  // + S^T S); two consecutive BFS levels of G separate G^2 (every 2-path
+  // between the levels before and after them passes through one of the two),
+  // at a third of the edge visits of BFS on G^2.
+  explicit NestedDissection(const Graph& g, bool wide = false)
+      : g_(g), wide_(wide), part_(g.n, 0), level_(g.n, -1), queue_(g.n), idx_(g.n), tmp_(g.n) {}
 
   std::vector<uint32_t> run() {
     for (uint32_t i = 0; i < g_.n; ++i) idx_[i] = i;
@@ -47,13 +53,22 @@ class NestedDissection {
     return std::move(idx_);
   }
 
+  // The splits of ranges of >= kSplitRecord vertices, (b << 32 | e) ->
+  // (end of A, end of B): in the final order, A | B | S of a range.  Rows of
+  // A reference only A (B, S come later or are not adjacent), so the
+  // elimination tree of A and of B can be built concurrently.
+  static constexpr uint32_t kSplitRecord = 8192;
+  std::map<uint64_t, std::pair<uint32_t, uint32_t>> splits;
+
  private:
-  static constexpr int kParDepth = 3;      // up to 2^3 concurrent ranges
+  static constexpr int kParDepth = 4;      // up to 2^4 concurrent ranges
   static constexpr uint32_t kParMin = 4096;  // smallest half worth a thread
   const Graph g_;
+  const bool wide_;
   std::vector<int32_t> part_, level_;
   std::vector<uint32_t> queue_, idx_, tmp_;
   std::atomic<int32_t> next_id_{1};
+  std::mutex split_mu_;
 
   int32_t part(uint32_t v) const { return __atomic_load_n(&part_[v], __ATOMIC_RELAXED); }
   void set_part(uint32_t v, int32_t id) { __atomic_store_n(&part_[v], id, __ATOMIC_RELAXED); }
@@ -74,6 +89,10 @@ class NestedDissection {
       if (split(t.b, t.e, t.id, &na, &ns) == 0) continue;  // no useful split
       const int32_t ia = next_id_.fetch_add(3), ib = ia + 1, is = ia + 2;
       const uint32_t e_a = t.b + na, e_b = t.e - ns;
+      if (t.e - t.b >= kSplitRecord) {
+        std::lock_guard<std::mutex> lk(split_mu_);
+        splits[((uint64_t)t.b << 32) | t.e] = {e_a, e_b};
+      }
       for (uint32_t q = t.b; q < e_a; ++q) set_part(idx_[q], ia);
       for (uint32_t q = e_a; q < e_b; ++q) set_part(idx_[q], ib);
       for (uint32_t q = e_b; q < t.e; ++q) set_part(idx_[q], is);
@@ -136,7 +155,8 @@ class NestedDissection {
     const uint32_t root = queue[cnt - 1];
     for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
     bfs(root, id, queue, &maxlev);
-    if (maxlev < 2) return 0;
+    const uint32_t wsep = wide_ ? 2u : 1u;  // separator levels
+    if (maxlev < 1 + wsep) return 0;
     // separator = the level where the running count first exceeds half
     std::vector<uint32_t> hist(maxlev + 2, 0);
     for (uint32_t q = b; q < e; ++q) hist[level_[idx_[q]]]++;
@@ -149,7 +169,8 @@ class NestedDissection {
       acc += hist[l];
     }
     if (sep == 0) sep = 1;
-    if (sep >= maxlev) sep = maxlev - 1;
+    if (sep + wsep > maxlev) sep = maxlev - wsep;
+    const uint32_t sep_hi = sep + wsep - 1;  // separator = levels [sep, sep_hi]
     uint32_t a = b, zb = 0, zs = 0;
     uint32_t* sbuf = queue;  // queue no longer needed
     for (uint32_t q = b; q < e; ++q) {
@@ -157,7 +178,7 @@ class NestedDissection {
       const uint32_t l = (uint32_t)level_[v];
       if (l < sep)
         idx_[a++] = v;
-      else if (l > sep)
+      else if (l > sep_hi)
         tmp[zb++] = v;
       else
         sbuf[zs++] = v;
@@ -173,7 +194,8 @@ class NestedDissection {
 }  // namespace
 
 void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector<uint32_t>& ci,
-                  const std::vector<float>& val, CholPlan* P) {
+                  const std::vector<float>& val, CholPlan* P, const std::vector<uint32_t>* g_rp,
+                  const std::vector<uint32_t>* g_ci) {
   CholPlan& p = *P;
   p = CholPlan();
   p.n = n;
@@ -188,8 +210,13 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     t_prev = t;
   };
   // (1) ordering
-  Graph g{n, rp.data(), ci.data()};
-  std::vector<uint32_t> perm0 = NestedDissection(g).run();
+  // the ordering runs on the 1-ring graph when the caller has it (M's pattern
+  // is its square), else on M's own graph
+  static const bool m_graph = std::getenv("DMCG_ND_MGRAPH") != nullptr;
+  const bool wide = g_rp && g_ci && g_rp->size() == (size_t)n + 1 && !m_graph;
+  Graph g = wide ? Graph{n, g_rp->data(), g_ci->data()} : Graph{n, rp.data(), ci.data()};
+  NestedDissection nd(g, wide);
+  std::vector<uint32_t> perm0 = nd.run();
   lap("ordering");
   std::vector<uint32_t> iperm0(n);
   for (uint32_t k = 0; k < n; ++k) iperm0[perm0[k]] = k;
@@ -218,22 +245,44 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       }
     });
   }
-  // (2) elimination tree (Liu, path compression) of P M P^T
+  // (2) elimination tree (Liu, path compression) of P M P^T; the two parts
+  // of every recorded dissection split are independent (rows of A touch only
+  // A), so their trees are built concurrently, the separator's rows after
   std::vector<int32_t> par(n, -1), anc(n, -1);
-  for (uint32_t k = 0; k < n; ++k) {
-    for (uint32_t q = lp[k]; q < lp[k + 1]; ++q) {
-      int32_t r = (int32_t)li[q];
-      while (anc[r] != -1 && anc[r] != (int32_t)k) {
-        const int32_t nx = anc[r];
-        anc[r] = (int32_t)k;
-        r = nx;
-      }
-      if (anc[r] == -1) {
-        anc[r] = (int32_t)k;
-        par[r] = (int32_t)k;
+  auto liu = [&](uint32_t k0, uint32_t k1) {
+    for (uint32_t k = k0; k < k1; ++k) {
+      for (uint32_t q = lp[k]; q < lp[k + 1]; ++q) {
+        int32_t r = (int32_t)li[q];
+        while (anc[r] != -1 && anc[r] != (int32_t)k) {
+          const int32_t nx = anc[r];
+          anc[r] = (int32_t)k;
+          r = nx;
+        }
+        if (anc[r] == -1) {
+          anc[r] = (int32_t)k;
+          par[r] = (int32_t)k;
+        }
       }
     }
-  }
+  };
+  std::function<void(uint32_t, uint32_t, int)> etree = [&](uint32_t b, uint32_t e, int depth) {
+    const auto it = nd.splits.find(((uint64_t)b << 32) | e);
+    if (it == nd.splits.end()) {
+      liu(b, e);
+      return;
+    }
+    const uint32_t ea = it->second.first, eb = it->second.second;
+    if (depth < 4) {
+      std::thread th([&, b, ea, depth] { etree(b, ea, depth + 1); });
+      etree(ea, eb, depth + 1);
+      th.join();
+    } else {
+      etree(b, ea, depth + 1);
+      etree(ea, eb, depth + 1);
+    }
+    liu(eb, e);
+  };
+  etree(0, n, 0);
   // (3) postorder (iterative DFS, children in increasing order)
   std::vector<int32_t> head(n, -1), nxt(n, -1);
   for (int32_t j = (int32_t)n - 1; j >= 0; --j)

@@ -395,10 +395,13 @@ int dmcg_create(dmcg_ctx** out, int device) {
   return DMCG_OK;
 }
 
+static void drop_pending_decode(dmcg_ctx* ctx);
+
 void dmcg_destroy(dmcg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   c->pending.reset();
+  drop_pending_decode(c);
   cudaStreamSynchronize(c->stream);
   c->pool.release_all();
   cudaStreamSynchronize(c->aux);
@@ -845,7 +848,9 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   // direct solver: symbolic analysis of M (host) + device structures
   {
     const auto t0 = std::chrono::steady_clock::now();
-    if (!p->chol_given) chol_analyze(nm, m.m_rp, m.m_ci, m.m_val, &p->chol);
+    if (!p->chol_given)
+      chol_analyze(nm, m.m_rp, m.m_ci, m.m_val, &p->chol, nm == n ? &m.lap_rp : nullptr,
+                   nm == n ? &m.lap_ci : nullptr);
     p->analyze_seconds = p->chol_given
                              ? p->analyze_seconds
                              : std::chrono::duration<double>(std::chrono::steady_clock::now() - t0)
@@ -1336,6 +1341,36 @@ int dmcg_ctx_stats(const dmcg_ctx* c, dmcg_stats* out) {
 void* dmcg_plan_stream(dmcg_plan* p) { return p ? (void*)p->ctx->stream : nullptr; }
 
 // ---- drop-in encode / decode -------------------------------------------------
+
+// A pending decode plan may still have its factor in flight on aux2.
+static void drop_pending_decode(dmcg_ctx* ctx) {
+  if (!ctx->pending_dec) return;
+  cudaStreamSynchronize(ctx->aux2);
+  if (ctx->pending_dec->plan) dmcg_plan_destroy(ctx->pending_dec->plan);
+  ctx->pending_dec.reset();
+}
+
+// The decode plan's config from a stream (dmcg_decode; the encode's
+// pending decode plan uses the same function on its own output).
+static Status decode_config(const dmcg_encoded* in, dmcg_config* cfg, std::vector<int>* rb) {
+  const uint32_t nb = in->n_b > 1 ? in->n_b : 1;
+  dmcg_config_default(cfg);
+  cfg->variant = in->variant;
+  cfg->k_l = in->k_l;
+  cfg->n_b = (uint16_t)nb;
+  rb->assign(in->k_l, 16);
+  for (uint32_t r = 0; r < in->k_l; ++r) (*rb)[r] = in->row_bits[0][r];
+  for (uint32_t r = 0; r < nb * in->k_l; ++r)
+    for (int a = 0; a < 3; ++a)
+      if (in->row_bits[a][r] < 1 || in->row_bits[a][r] > 16)
+        return {DMCG_E_CORRUPT, "CorruptStream: row bit depth outside 1..16"};
+  cfg->row_bits = rb->data();
+  cfg->n_row_bits = in->k_l;
+  cfg->anchor_bits = in->anchor_bits;
+  cfg->dict_bits = in->dict_bits;
+  cfg->diff_bits = in->diff_bits ? in->diff_bits : 8;
+  return Status::ok();
+}
 int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg_encoded* out) {
   if (!ctx || !seq || !cfg || !out) return DMCG_E_CONFIG;
   cudaSetDevice(ctx->device);
@@ -1378,7 +1413,8 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
             build_reduced_normal(&m);
           else
             build_normal_matrix(&m);
-          chol_analyze(raw->n - (raw->reduced ? 1 : 0), m.m_rp, m.m_ci, m.m_val, &raw->chol);
+          chol_analyze(raw->n - (raw->reduced ? 1 : 0), m.m_rp, m.m_ci, m.m_val, &raw->chol,
+                       raw->reduced ? nullptr : &m.lap_rp, raw->reduced ? nullptr : &m.lap_ci);
           raw->seconds =
               std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         });
@@ -1430,6 +1466,53 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
     out->faces = seq->faces;
   }
   tm.lap("download");
+  drop_pending_decode(ctx);
+  static const bool no_prep = std::getenv("DMCG_NO_OVERLAP") || std::getenv("DMCG_NO_PREFACTOR");
+  if (st.good() && !no_prep && ctx->pending && cfg->variant != DMCG_V2V && p->nb == 1) {
+    // the next dmcg_decode of this stream: its plan, decode structures and
+    // M's numeric factor (on aux2) prepared now, see PendingDecode
+    std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
+    if (pa->th.joinable()) pa->th.join();
+    dmcg_config dc;
+    std::vector<int> drb;
+    dmcg_plan* pdp = nullptr;
+    Status sp = pa->failed ? Status{DMCG_E_CONFIG, "analysis failed"} : decode_config(out, &dc, &drb);
+    if (sp.good())
+      sp = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, &dc,
+                            out->anchor_idx, p->n_c, &pdp, &pa->mesh, false);
+    if (sp.good()) {
+      pdp->mesh.m_rp = std::move(pa->mesh.m_rp);
+      pdp->mesh.m_ci = std::move(pa->mesh.m_ci);
+      pdp->mesh.m_val = std::move(pa->mesh.m_val);
+      pdp->chol = std::move(pa->chol);
+      pdp->analyze_seconds = pa->seconds;
+      pdp->chol_given = true;
+      sp = plan_prepare_decode(pdp);
+      if (sp.good()) sp = plan_prefactor_async(pdp);
+    }
+    if (sp.good()) {
+      auto pd = std::make_unique<PendingDecode>();
+      pd->plan = pdp;
+      pd->n = seq->n;
+      pd->F = seq->F;
+      pd->n_faces = seq->n_faces;
+      pd->faces_hash = pa->faces_hash;
+      pd->dtype = seq->dtype;
+      pd->variant = (int)out->variant;
+      pd->k_l = out->k_l;
+      pd->n_b = 1;
+      pd->anchor_bits = (int)out->anchor_bits;
+      pd->dict_bits = (int)out->dict_bits;
+      pd->diff_bits = dc.diff_bits;
+      pd->row_bits = drb;
+      pd->anchors.assign(out->anchor_idx, out->anchor_idx + p->n_c);
+      ctx->pending_dec = std::move(pd);
+    } else if (pdp) {
+      cudaStreamSynchronize(ctx->aux2);
+      dmcg_plan_destroy(pdp);
+    }
+    tm.lap("decode plan + factor");
+  }
   if (st.good()) {
     const dmcg_stats& e = p->stats;
     ctx->last_stats.ms_encode = e.ms_encode;
@@ -1474,25 +1557,50 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
     if (in->anchor_idx[t] >= in->n || (t && in->anchor_idx[t] <= in->anchor_idx[t - 1]))
       return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: anchor indices invalid"});
   dmcg_config cfg;
-  dmcg_config_default(&cfg);
-  cfg.variant = in->variant;
-  cfg.k_l = in->k_l;
-  cfg.n_b = (uint16_t)nb;
-  std::vector<int> rb(in->k_l, 16);
-  for (uint32_t r = 0; r < in->k_l; ++r) rb[r] = in->row_bits[0][r];
-  for (uint32_t r = 0; r < nb * in->k_l; ++r)
-    for (int a = 0; a < 3; ++a)
-      if (in->row_bits[a][r] < 1 || in->row_bits[a][r] > 16)
-        return ctx->set_error({DMCG_E_CORRUPT, "CorruptStream: row bit depth outside 1..16"});
-  cfg.row_bits = rb.data();
-  cfg.n_row_bits = in->k_l;
-  cfg.anchor_bits = in->anchor_bits;
-  cfg.dict_bits = in->dict_bits;
-  cfg.diff_bits = in->diff_bits ? in->diff_bits : 8;
+  std::vector<int> rb;
+  {
+    Status sc = decode_config(in, &cfg, &rb);
+    if (!sc.good()) return ctx->set_error(sc);
+  }
+  dmcg_decode_options o;
+  dmcg_decode_options_default(&o);
+  if (opt) o = *opt;
+  // The decode plan the last dmcg_encode prepared for its own stream (factor
+  // already running on aux2), taken on an exact match of what it depends on.
+  std::unique_ptr<PendingDecode> pd = std::move(ctx->pending_dec);
+  if (pd && !(o.solver == 0 && pd->n == in->n && pd->F == in->F && pd->dtype == out_dtype &&
+              pd->n_faces == in->n_faces && pd->variant == (int)in->variant &&
+              pd->k_l == in->k_l && pd->n_b == nb && pd->anchor_bits == (int)in->anchor_bits &&
+              pd->dict_bits == (int)in->dict_bits && pd->diff_bits == cfg.diff_bits &&
+              pd->row_bits == rb && pd->anchors.size() == in->n_c &&
+              std::equal(pd->anchors.begin(), pd->anchors.end(), in->anchor_idx) &&
+              pd->faces_hash == hash_faces(in->faces, in->n_faces))) {
+    // keep its host analysis (M, symbolic factor) when only the plan differs
+    // (e.g. another output dtype): it depends on mesh and anchors alone
+    if (pd->n == in->n && pd->n_faces == in->n_faces && pd->anchors.size() == in->n_c &&
+        std::equal(pd->anchors.begin(), pd->anchors.end(), in->anchor_idx) &&
+        variant_uses_means(pd->variant) == variant_uses_means(in->variant) &&
+        pd->faces_hash == hash_faces(in->faces, in->n_faces) && !ctx->pending) {
+      cudaStreamSynchronize(ctx->aux2);
+      auto pa2 = std::make_unique<PendingAnalysis>();
+      pa2->n = pd->n;
+      pa2->n_faces = pd->n_faces;
+      pa2->faces_hash = pd->faces_hash;
+      pa2->reduced = variant_uses_means(pd->variant);
+      pa2->anchors = pd->anchors;
+      pa2->mesh = std::move(pd->plan->mesh);
+      pa2->chol = std::move(pd->plan->chol);
+      pa2->seconds = pd->plan->analyze_seconds;
+      ctx->pending = std::move(pa2);
+    }
+    ctx->pending_dec = std::move(pd);
+    drop_pending_decode(ctx);
+  }
   // The analysis started by the last dmcg_encode (normal matrix, symbolic
   // Cholesky, and the Laplacian structure it was built from) is taken once,
   // and only when mesh and anchors match.
   std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
+  if (pd) pa.reset();  // the prepared plan already holds it
   if (pa && !(pa->n == in->n && pa->n_faces == in->n_faces &&
               pa->reduced == variant_uses_means(in->variant) &&
               pa->anchors.size() == in->n_c &&
@@ -1501,10 +1609,13 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
     pa.reset();
   if (pa && pa->th.joinable()) pa->th.join();
   if (pa && pa->failed) pa.reset();
-  dmcg_plan* p = nullptr;
-  Status st = plan_create_impl(ctx, in->n, in->F, out_dtype, in->faces, in->n_faces, &cfg,
-                               in->anchor_idx, in->n_c, &p, pa ? &pa->mesh : nullptr, false);
-  if (!st.good()) return ctx->set_error(st);
+  dmcg_plan* p = pd ? pd->plan : nullptr;
+  Status st = Status::ok();
+  if (!p) {
+    st = plan_create_impl(ctx, in->n, in->F, out_dtype, in->faces, in->n_faces, &cfg,
+                          in->anchor_idx, in->n_c, &p, pa ? &pa->mesh : nullptr, false);
+    if (!st.good()) return ctx->set_error(st);
+  }
   PhaseTimer tm("decode");
   if (pa) {
     p->mesh.m_rp = std::move(pa->mesh.m_rp);
@@ -1517,9 +1628,6 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   tm.lap("plan");
   st = upload_impl(p, in);
   tm.lap("upload");
-  dmcg_decode_options o;
-  dmcg_decode_options_default(&o);
-  if (opt) o = *opt;
   if (st.good() && o.solver == 0) st = plan_prepare_decode(p);
   tm.lap("prepare(analyze)");
   for (int a = 0; a < 3 && st.good(); ++a) {  // output staging (drop-in decode only)
@@ -1603,7 +1711,7 @@ extern "C" int dmcg_debug_chol(uint32_t n, const uint32_t* faces, uint32_t n_fac
   tm.lap("normal");
   CholPlan p;
   const auto t0 = std::chrono::steady_clock::now();
-  chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p);
+  chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p, &m.lap_rp, &m.lap_ci);
   const double secs =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (stats) {

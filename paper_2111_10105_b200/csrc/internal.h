@@ -79,6 +79,9 @@ struct PhaseTimer {
 void* plan_alloc(dmcg_plan* p, size_t bytes);
 // Builds the decode-side state on first use (host.cpp).
 Status plan_prepare_decode(dmcg_plan* p);
+// M's numeric factor on ctx->aux2 now (decode structures must exist); the
+// next decode of the plan takes it and waits for it before its solves.
+Status plan_prefactor_async(dmcg_plan* p);
 Status plan_prepare_normal(dmcg_plan* p);
 }  // namespace dmcg
 
@@ -112,9 +115,27 @@ size_t serialize_stream(const dmcg_encoded* e, uint8_t* out, size_t cap, dmcg_se
                         PayloadSpans* spans);
 }  // namespace dmcg
 
+namespace dmcg {
+// The decode plan a drop-in dmcg_encode prepares for the next dmcg_decode of
+// its own stream: created from the stream's config once the overlapped
+// analysis is done, decode structures uploaded, and M's numeric factor
+// launched on ctx->aux2 — so the factor runs while the encode returns and the
+// decode uploads the stream and reconstructs.  Taken once, only on an exact
+// match of everything the decode plan depends on; otherwise discarded.
+struct PendingDecode {
+  dmcg_plan* plan = nullptr;
+  uint32_t n = 0, F = 0, n_faces = 0, k_l = 0, n_b = 0;
+  int dtype = 0, variant = 0, anchor_bits = 0, dict_bits = 0, diff_bits = 0;
+  uint64_t faces_hash = 0;
+  std::vector<int> row_bits;
+  std::vector<uint32_t> anchors;
+};
+}  // namespace dmcg
+
 struct dmcg_ctx {
   int device = 0;
   std::unique_ptr<dmcg::PendingAnalysis> pending;  // see PendingAnalysis
+  std::unique_ptr<dmcg::PendingDecode> pending_dec;  // see PendingDecode
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // fork/join side stream (independent encode / decode phases)
   cudaStream_t aux2 = nullptr; // low-priority stream: the decoder's factor during an encode
@@ -296,6 +317,7 @@ struct dmcg_plan {
   cudaEvent_t ev_pf_fork = nullptr, ev_pf_join = nullptr, ev_pf0 = nullptr, ev_pf1 = nullptr;
   int* d_pf_flag = nullptr;        // non-positive pivot of the overlapped factor
   bool factor_pending = false;     // the last encode left a factor of M for the next decode
+  bool pf_unjoined = false;        // ... launched outside any graph: the decode waits ev_pf_join
   float ms_prefactor = 0.0f;
   dmcg_stats stats = {};
 };

@@ -396,6 +396,15 @@ static Status fork_prefactor(dmcg_plan* p) {
   return Status::ok();
 }
 
+Status plan_prefactor_async(dmcg_plan* p) {
+  if (!p->cdev.P || p->nb != 1 || p->shard) return Status{DMCG_E_UNSUPPORTED, "Unsupported: prefactor"};
+  Status st = fork_prefactor(p);
+  if (!st.good()) return st;
+  p->factor_pending = true;
+  p->pf_unjoined = true;
+  return Status::ok();
+}
+
 // Every kernel of one encode on the plan stream (no host synchronisation:
 // capturable into a CUDA graph).
 static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefactor) {
@@ -730,8 +739,6 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
   cdev.W = (uint32_t)W;
   const bool f32 = p->dtype == DMCG_F32;
   DMCG_TRY(cudaMemsetAsync(p->d_flags, 0, 8 * sizeof(int), s));
-  if (pre && !factor)  // the overlapped factor's pivot flag
-    DMCG_TRY(cudaMemcpyAsync(p->d_flags + 4, p->d_pf_flag, sizeof(int), cudaMemcpyDeviceToDevice, s));
   DMCG_TRY(record_event(p->ev[0], s));
   const size_t nW = (size_t)n * W;
   // The right-hand sides (dequantise + reconstruct + L^T delta~ + S^T a) do
@@ -811,6 +818,10 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
   DMCG_TRY(record_event(p->ev[5], s));
   // solve_anchored (solver.cpp:62-90) on all n rows, or solve_mean_constrained
   // (solver.cpp:105-133): vertex 0 pinned, unknowns = rows 1.. (offset W).
+  if (pre && !factor) {  // the overlapped factor: joined here if launched outside a graph
+    if (p->pf_unjoined) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_pf_join, 0));
+    DMCG_TRY(cudaMemcpyAsync(p->d_flags + 4, p->d_pf_flag, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  }
   const bool mc = variant_uses_means(p->variant);
   const int nm = (int)cdev.n;
   const size_t o = mc ? (size_t)W : 0;
@@ -895,7 +906,9 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
     return Status{DMCG_E_NUMERICAL,
                   "SingularSystem: anchored normal equations are not positive definite"};
   }
+  if (pre && p->pf_unjoined) cudaEventElapsedTime(&p->ms_prefactor, p->ev_pf0, p->ev_pf1);
   p->factor_pending = false;
+  p->pf_unjoined = false;
   p->factor_valid = true;
   // overlapped factor: its own time on aux2 during the encode
   if (!factor) p->stats.ms_factor = pre ? p->ms_prefactor : 0.0f;

@@ -16,7 +16,8 @@ cfg = codec.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=s
 npdt = np.float32 if spec.dtype == "f32" else np.float64
 pin = [torch.from_numpy(np.ascontiguousarray(x, dtype=npdt)).pin_memory().numpy() for x in s.axes]
 hs = synth.Sequence(s.faces, pin)
-out = [torch.empty(x.shape, dtype=torch.float64).pin_memory().numpy() for x in s.axes]
+out = [torch.empty(x.shape, dtype=torch.float32 if npdt == np.float32 else torch.float64)
+       .pin_memory().numpy() for x in s.axes]
 enc_buf = None  # the stream in page-locked arrays after the first (warm-up) call, as in bench.py
 for it in range(3):
     t0 = time.perf_counter()
@@ -25,6 +26,6 @@ for it in range(3):
         enc_buf = codec.CompressedAnimation.allocate(enc.n, enc.F, enc.k_l, enc.n_c, enc.faces,
                                                      n_b=enc.n_b, pinned=True, variant=enc.variant)
     t1 = time.perf_counter()
-    cd.decode(enc, out=out)
+    cd.decode(enc, out=out, dtype=npdt)
     t2 = time.perf_counter()
     print(f"e2e encode {1e3 * (t1 - t0):.2f} ms decode {1e3 * (t2 - t1):.2f} ms", flush=True)
