@@ -548,3 +548,23 @@ def test_gpu_distortion_metrics_match_reference_formulas(codec):
     assert np.allclose(rms, ref_rms, rtol=1e-12, atol=0)
     assert np.allclose(nm, ref_nm, rtol=1e-12, atol=0)
     assert np.allclose(vme, ref_vme, rtol=1e-12, atol=0)
+
+
+def test_dropin_pending_decode_plan(codec):
+    """dmcg_encode prepares the next dmcg_decode's plan and starts M's factor
+    (host.cpp PendingDecode): the decode that takes it returns the same bits
+    as a decode that builds its own plan, and a decode that cannot take it
+    (other output dtype) keeps its host analysis and decodes correctly."""
+    spec = synth.CONFIGS["c1"]
+    s = spec.make()
+    cfg = C.EncoderConfig(k_l=spec.k, row_bits=[spec.bits] * spec.k, oi_rounds=spec.rounds)
+    enc = codec.encode(s, cfg)
+    x_pending = codec.decode(enc)          # takes the prepared plan + factor
+    x_fresh = codec.decode(enc)            # nothing pending: own plan, own factor
+    for a in range(3):
+        assert np.array_equal(x_pending[a], x_fresh[a])
+    enc2 = codec.encode(s, cfg)
+    x32 = codec.decode(enc2, dtype=np.float32)  # dtype mismatch: analysis salvaged
+    bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
+    for a in range(3):
+        assert np.abs(x32[a].astype(np.float64) - x_fresh[a]).max() <= 1e-5 * bbox
