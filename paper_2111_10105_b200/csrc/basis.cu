@@ -1204,32 +1204,38 @@ __global__ void k_fill_zero(double* p, long count) {
 // register panels + V^T Y + T + T W + update per panel).  Same reflector
 // formulas as warp_panel_qr_T / the oracle's householder_factor; the
 // reductions sum in a different order (rounding-level differences, P3).
-template <int R, int PW>
+template <int R, int PW, int NT = kOiThreads>
 __device__ void cta_panel_qr_T(double* Z, int m, int ld, int pb, double* tau, double* T) {
   __shared__ double red[kOiThreads / 32][PW + 1];
   __shared__ double tot[2 * PW + 1];  // [0, PW]: sums, [PW + 1, 2 PW]: row j of the block
   const unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nw = blockDim.x >> 5;
+  const int nw = NT >> 5;
+  const bool act = tid < NT;  // threads >= NT only join the barriers
   double a[R][PW];
 #pragma unroll
   for (int t = 0; t < R; ++t)
 #pragma unroll
     for (int c = 0; c < PW; ++c) {
-      const int g = tid + kOiThreads * t;
-      a[t][c] = (c < pb && g < m) ? Z[c * ld + g] : 0.0;
+      const int g = tid + NT * t;
+      a[t][c] = (act && c < pb && g < m) ? Z[c * ld + g] : 0.0;
     }
   double tv[PW], tr[PW];
 #pragma unroll
   for (int i = 0; i < PW; ++i) tr[i] = tv[i] = 0.0;
 #pragma unroll
   for (int j = 0; j < PW; ++j) {
-    double r[PW + 1];
+    // 32 partial sums per thread (PW + 1 used), reduced over the warp by
+    // recursive halving: each round every lane sends the half it gives up
+    // and keeps the other, so lane L ends with the total of value L after
+    // 16 + 8 + 4 + 2 + 1 exchanges (not 5 (PW + 1): SHFL / DADD throughput)
+    static_assert(PW + 1 <= 32, "one value per lane");
+    double r[32];
 #pragma unroll
-    for (int l = 0; l <= PW; ++l) r[l] = 0.0;
+    for (int l = 0; l < 32; ++l) r[l] = 0.0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-      const int g = tid + kOiThreads * t;
+      const int g = tid + NT * t;
       const double x = g > j ? a[t][j] : 0.0;
       r[PW] = fma(x, x, r[PW]);
 #pragma unroll
@@ -1238,14 +1244,15 @@ __device__ void cta_panel_qr_T(double* Z, int m, int ld, int pb, double* tau, do
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      r[PW] += __shfl_xor_sync(FULL, r[PW], o);
+      const bool hi = (lane & o) != 0;
 #pragma unroll
-      for (int l = 0; l < PW; ++l)
-        if (l != j) r[l] += __shfl_xor_sync(FULL, r[l], o);
+      for (int i = 0; i < o; ++i) {
+        const double send = hi ? r[i] : r[i + o];
+        const double keep = hi ? r[i + o] : r[i];
+        r[i] = keep + __shfl_xor_sync(FULL, send, o);
+      }
     }
-    if (lane == 0)
-#pragma unroll
-      for (int l = 0; l <= PW; ++l) red[warp][l] = r[l];
+    if (act && lane <= PW) red[warp][lane] = r[0];
     if (tid == j)  // row j (j < PW <= 256: thread j, t = 0)
 #pragma unroll
       for (int l = 0; l < PW; ++l) tot[PW + 1 + l] = a[0][l];
@@ -1281,8 +1288,8 @@ __device__ void cta_panel_qr_T(double* Z, int m, int ld, int pb, double* tau, do
     for (int l = 0; l < PW; ++l) sl[l] = l > j ? tj * fma(rinv, tot[l], tot[PW + 1 + l]) : 0.0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-      const int g = tid + kOiThreads * t;
-      if (g > j) a[t][j] *= rinv;
+      const int g = tid + NT * t;
+      if (act && g > j) a[t][j] *= rinv;
     }
     if (tid == j) a[0][j] = beta;
     tv[j] = tj;
@@ -1291,8 +1298,8 @@ __device__ void cta_panel_qr_T(double* Z, int m, int ld, int pb, double* tau, do
       if (l <= j) continue;
 #pragma unroll
       for (int t = 0; t < R; ++t) {
-        const int g = tid + kOiThreads * t;
-        if (g > j) a[t][l] = fma(-sl[l], a[t][j], a[t][l]);
+        const int g = tid + NT * t;
+        if (act && g > j) a[t][l] = fma(-sl[l], a[t][j], a[t][l]);
       }
       if (tid == j) a[0][l] -= sl[l];
     }
@@ -1301,8 +1308,8 @@ __device__ void cta_panel_qr_T(double* Z, int m, int ld, int pb, double* tau, do
   for (int t = 0; t < R; ++t)
 #pragma unroll
     for (int c = 0; c < PW; ++c) {
-      const int g = tid + kOiThreads * t;
-      if (c < pb && g < m) Z[c * ld + g] = a[t][c];
+      const int g = tid + NT * t;
+      if (act && c < pb && g < m) Z[c * ld + g] = a[t][c];
     }
   if (tid == 0)
 #pragma unroll
