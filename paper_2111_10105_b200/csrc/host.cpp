@@ -1634,18 +1634,44 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
     p->d_x_out[a] = plan_alloc(p, (size_t)in->n * in->F * (out_dtype == DMCG_F32 ? 4 : 8));
     if (!p->d_x_out[a]) st = {DMCG_E_CUDA, "CudaError: device allocation failed"};
   }
-  if (st.good()) st = plan_decode(p, &o, p->d_x_out);
-  tm.lap("kernels");
   // D2H of the decoded frame window only (all frames by default): columns
   // outside the window of the caller's arrays are left untouched.
   const size_t es = out_dtype == DMCG_F32 ? 4 : 8;
-  const size_t f0 = o.frame_count ? o.frame_begin : 0;
-  const size_t fw = o.frame_count ? o.frame_count : in->F;
-  for (int a = 0; a < 3 && st.good(); ++a)
-    if (cudaMemcpy2DAsync((uint8_t*)out_axes[a] + f0 * es, in->F * es,
-                          (const uint8_t*)p->d_x_out[a] + f0 * es, in->F * es, fw * es, in->n,
-                          cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
-      st = {DMCG_E_CUDA, "CudaError: D2H copy failed"};
+  auto d2h = [&](size_t f0, size_t fw, cudaStream_t cs) {
+    for (int a = 0; a < 3 && st.good(); ++a)
+      if (cudaMemcpy2DAsync((uint8_t*)out_axes[a] + f0 * es, in->F * es,
+                            (const uint8_t*)p->d_x_out[a] + f0 * es, in->F * es, fw * es, in->n,
+                            cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+        st = {DMCG_E_CUDA, "CudaError: D2H copy failed"};
+  };
+  // The whole sequence in two frame windows (the solve is column-separable:
+  // each window decodes to the bits of the full decode, and the second reuses
+  // the factor), so the first window's D2H runs under the second's kernels.
+  static const bool no_split = std::getenv("DMCG_NO_DECODE_SPLIT") != nullptr;
+  const bool split = !no_split && st.good() && o.solver == 0 && !o.frame_count && p->nb == 1 &&
+                     in->F >= 64 && p->variant != DMCG_V2V;
+  if (split) {
+    const uint32_t Fh = in->F / 2;
+    dmcg_decode_options o1 = o, o2 = o;
+    o1.frame_begin = 0;
+    o1.frame_count = Fh;
+    o2.frame_begin = Fh;
+    o2.frame_count = in->F - Fh;
+    o2.reuse_factor = 1;
+    st = plan_decode(p, &o1, p->d_x_out);  // returns after its stream sync
+    if (st.good()) d2h(0, Fh, ctx->aux2);
+    if (st.good()) st = plan_decode(p, &o2, p->d_x_out);
+    tm.lap("kernels");
+    if (st.good()) d2h(Fh, in->F - Fh, ctx->stream);
+    if (cudaStreamSynchronize(ctx->aux2) != cudaSuccess && st.good())
+      st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
+  } else {
+    if (st.good()) st = plan_decode(p, &o, p->d_x_out);
+    tm.lap("kernels");
+    const size_t f0 = o.frame_count ? o.frame_begin : 0;
+    const size_t fw = o.frame_count ? o.frame_count : in->F;
+    d2h(f0, fw, ctx->stream);
+  }
   if (st.good() && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
     st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
   tm.lap("d2h");
