@@ -1837,10 +1837,13 @@ __global__ void __launch_bounds__(kJbThreads, 1)
   const int q = (int)cl.block_rank();
   const int b = blockIdx.x / kJbCs;
   constexpr int bw = kJbMaxBw, m2 = kJbNblk * bw, n2 = 2 * bw, h2 = bw;
-  const int tid = threadIdx.x, NT = blockDim.x;
-  // A column buffers: [phase][slot][bw][m2]; slot 0 = top block, 1 = bottom
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  // A column buffers: [phase][slot][bw][ldc]; slot 0 = top block, 1 =
+  // bottom; odd column stride ldc = m2 + 1, so the 8 columns of a DMMA
+  // fragment fall on different banks
+  constexpr int ldc = m2 + 1;
   auto Acol = [&](int ph, int j) {  // local column j < n2 of phase ph
-    return dyn + ((size_t)(ph * 2 + (j >= bw)) * bw + (j >= bw ? j - bw : j)) * m2;
+    return dyn + ((size_t)(ph * 2 + (j >= bw)) * bw + (j >= bw ? j - bw : j)) * ldc;
   };
   double* Vg = Vg_all + (size_t)b * m2 * m2;  // V(r, c) = Vg[c m2 + r]
   const double* Ain = Aall + (size_t)b * m * m;
@@ -1990,30 +1993,39 @@ __global__ void __launch_bounds__(kJbThreads, 1)
       cluster_sync_all();  // every J_p published
       long long tp2 = clock64();
       // ---- 2a. own columns: A[:, own] <- A[:, own] J_q ; V likewise ----
-      for (int r = tid; r < 2 * m2; r += NT) {
-        const bool isv = r >= m2;
-        const int rr2 = isv ? r - m2 : r;
-        double a[n2];
+      // FP64 tensor tiles (DMMA 8x8x4): every warp owns whole 8-row tiles
+      // (all 32 columns), so it reads a tile's rows completely before it
+      // overwrites them; J_q's fragments stay in registers for all tiles.
+      {
+        const int fr = lane >> 2, fk = lane & 3;
+        double bj[n2 / 4][n2 / 8];  // J(k = 4 ks + fk, n = 8 ct + fr)
 #pragma unroll
-        for (int j = 0; j < n2; ++j)
-          a[j] = isv ? Vg[(size_t)lcol(q, j) * m2 + rr2] : Acol(ph, j)[rr2];
+        for (int ks = 0; ks < n2 / 4; ++ks)
 #pragma unroll
-        for (int c0 = 0; c0 < n2; c0 += 8) {
-          double o[8];
+          for (int ct = 0; ct < n2 / 8; ++ct) bj[ks][ct] = sh.J[4 * ks + fk][8 * ct + fr];
+        for (int mt = warp; mt < 2 * m2 / 8; mt += NT / 32) {
+          const bool isv = mt * 8 >= m2;
+          const int r0 = isv ? mt * 8 - m2 : mt * 8;
+          double acc[n2 / 8][2];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            double acc = 0.0;
+          for (int ct = 0; ct < n2 / 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
 #pragma unroll
-            for (int j = 0; j < n2; ++j) acc = fma(a[j], sh.J[j][c0 + c], acc);
-            o[c] = acc;
+          for (int ks = 0; ks < n2 / 4; ++ks) {
+            const int k = 4 * ks + fk;
+            const double av = isv ? Vg[(size_t)lcol(q, k) * m2 + r0 + fr] : Acol(ph, k)[r0 + fr];
+#pragma unroll
+            for (int ct = 0; ct < n2 / 8; ++ct) dmma884(acc[ct], av, bj[ks][ct]);
           }
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            if (isv)
-              Vg[(size_t)lcol(q, c0 + c) * m2 + rr2] = o[c];
-            else
-              Acol(ph, c0 + c)[rr2] = o[c];
-          }
+          for (int ct = 0; ct < n2 / 8; ++ct)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = 8 * ct + 2 * fk + e;
+              if (isv)
+                Vg[(size_t)lcol(q, c) * m2 + r0 + fr] = acc[ct][e];
+              else
+                Acol(ph, c)[r0 + fr] = acc[ct][e];
+            }
         }
       }
       __syncthreads();
@@ -2022,39 +2034,60 @@ __global__ void __launch_bounds__(kJbThreads, 1)
       {
         // stage every other pair's J (DSMEM) at once: one barrier, not one per pair
         typedef double JT[kJbMaxS][kJbMaxS + 1];
-        JT* Js = reinterpret_cast<JT*>(dyn + (size_t)4 * bw * m2);
-        for (int t = tid; t < kJbCs * n2 * n2; t += NT) {
-          const int pp = t / (n2 * n2), e = t % (n2 * n2), i = e % n2, j = e / n2;
-          if (pp != q) Js[pp][i][j] = cl.map_shared_rank(&sh, pp)->J[i][j];
+        JT* Js = reinterpret_cast<JT*>(dyn + (size_t)4 * bw * ldc);
+        // eight remote loads in flight per thread (DSMEM latency, not bandwidth)
+        for (int t0 = tid; t0 < kJbCs * n2 * n2; t0 += 8 * NT) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int t = t0 + u * NT;
+            const int pp = t / (n2 * n2), e = t % (n2 * n2), i = e % n2, j = e / n2;
+            v[u] = (t < kJbCs * n2 * n2 && pp != q) ? cl.map_shared_rank(&sh, pp)->J[i][j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int t = t0 + u * NT;
+            const int pp = t / (n2 * n2), e = t % (n2 * n2), i = e % n2, j = e / n2;
+            if (t < kJbCs * n2 * n2 && pp != q) Js[pp][i][j] = v[u];
+          }
         }
         __syncthreads();
-        // thread: (pair, column j, rows i = i0 + 8 u): all reads of a
-        // column's pair rows precede its writes (the 8 threads of a
-        // (pair, column) are consecutive lanes; __syncwarp between)
-        for (int t = tid; t < kJbCs * n2 * 8; t += NT) {
-          const int pp = t / (n2 * 8), j = (t >> 3) % n2, i0 = t & 7;
-          double* col = Acol(ph, j);
-          if (pp == q) {  // own diagonal block: the inner result, exactly
+        // out(i, c) = sum_k J_p(k, i) A(R_p[k], c) as DMMA tiles: warp w owns
+        // tiles 2w, 2w + 1 (of 16 per pair) of every pair; all products into
+        // registers first, one barrier, then the stores (in place)
+        const int fr = lane >> 2, fk = lane & 3;
+        constexpr int kTiles = (n2 / 8) * (n2 / 8);
+        constexpr int kPerWarp = kTiles / (kJbThreads / 32);
+        double acc[kJbCs][kPerWarp][2];
 #pragma unroll
-            for (int u = 0; u < n2 / 8; ++u) col[lcol(q, i0 + 8 * u)] = sh.S[i0 + 8 * u][j];
-            continue;
+        for (int pp = 0; pp < kJbCs; ++pp) {
+#pragma unroll
+          for (int u = 0; u < kPerWarp; ++u) {
+            acc[pp][u][0] = acc[pp][u][1] = 0.0;
+            if (pp == q) continue;
+            const int tile = warp * kPerWarp + u, it = tile / (n2 / 8), ct = tile % (n2 / 8);
+#pragma unroll
+            for (int ks = 0; ks < n2 / 4; ++ks) {
+              const int k = 4 * ks + fk;
+              const double av = Js[pp][k][8 * it + fr];                 // A(m = i, k) = J_p(k, i)
+              const double bv = Acol(ph, 8 * ct + fr)[lcol(pp, k)];    // B(k, n = c)
+              dmma884(acc[pp][u], av, bv);
+            }
           }
-          double a[n2];
-#pragma unroll
-          for (int k = 0; k < n2; ++k) a[k] = col[lcol(pp, k)];
-          double o4[n2 / 8];
-#pragma unroll
-          for (int u = 0; u < n2 / 8; ++u) {
-            const int i = i0 + 8 * u;
-            double acc = 0.0;
-#pragma unroll
-            for (int k = 0; k < n2; ++k) acc = fma(Js[pp][k][i], a[k], acc);
-            o4[u] = acc;
-          }
-          __syncwarp();
-#pragma unroll
-          for (int u = 0; u < n2 / 8; ++u) col[lcol(pp, i0 + 8 * u)] = o4[u];
         }
+        __syncthreads();
+#pragma unroll
+        for (int pp = 0; pp < kJbCs; ++pp)
+#pragma unroll
+          for (int u = 0; u < kPerWarp; ++u) {
+            const int tile = warp * kPerWarp + u, it = tile / (n2 / 8), ct = tile % (n2 / 8);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * it + fr, c = 8 * ct + 2 * fk + e;
+              // own diagonal block: the inner result, exactly
+              Acol(ph, c)[lcol(pp, i)] = pp == q ? sh.S[i][c] : acc[pp][u][e];
+            }
+          }
         __syncthreads();
       }
       long long tp4 = clock64();
@@ -2069,12 +2102,12 @@ __global__ void __launch_bounds__(kJbThreads, 1)
         const int st_rank = q == 0 ? 0 : (q == 1 ? 0 : q - 1), st_slot = q == 1 ? 1 : 0;
         const int sb_rank = q < kJbCs - 1 ? q + 1 : q, sb_slot = q < kJbCs - 1 ? 1 : 0;
         const double* srct =
-            cl.map_shared_rank(dyn, st_rank) + ((size_t)(ph * 2 + st_slot) * bw) * m2;
+            cl.map_shared_rank(dyn, st_rank) + ((size_t)(ph * 2 + st_slot) * bw) * ldc;
         const double* srcb =
-            cl.map_shared_rank(dyn, sb_rank) + ((size_t)(ph * 2 + sb_slot) * bw) * m2;
-        double* dstt = dyn + ((size_t)(nph * 2 + 0) * bw) * m2;
-        double* dstb = dyn + ((size_t)(nph * 2 + 1) * bw) * m2;
-        const int tot = bw * m2;
+            cl.map_shared_rank(dyn, sb_rank) + ((size_t)(ph * 2 + sb_slot) * bw) * ldc;
+        double* dstt = dyn + ((size_t)(nph * 2 + 0) * bw) * ldc;
+        double* dstb = dyn + ((size_t)(nph * 2 + 1) * bw) * ldc;
+        const int tot = bw * ldc;
         for (int t0 = tid; t0 < tot; t0 += 8 * NT) {
           double vt[8], vb[8];
 #pragma unroll
@@ -2418,7 +2451,7 @@ cudaError_t launch_jacobi(cudaStream_t s, int nbatch, int m, const double* A, do
       const int bw = kJbMaxBw;  // zero padded to 256 (padding never rotates)
       const int mb2 = kJbNblk * bw;
       const size_t smem =
-          ((size_t)4 * bw * mb2 + (size_t)kJbCs * kJbMaxS * (kJbMaxS + 1)) * sizeof(double);
+          ((size_t)4 * bw * (mb2 + 1) + (size_t)kJbCs * kJbMaxS * (kJbMaxS + 1)) * sizeof(double);
       const void* fn = (const void*)k_jacobi_blk;
       if (smem <= smem_room(fn) && set_smem_attr(fn, smem) == cudaSuccess) {
         cudaLaunchConfig_t cfg = {};

@@ -245,6 +245,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       }
     });
   }
+  lap("lower pattern");
   // (2) elimination tree (Liu, path compression) of P M P^T; the two parts
   // of every recorded dissection split are independent (rows of A touch only
   // A), so their trees are built concurrently, the separator's rows after
@@ -283,6 +284,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     liu(eb, e);
   };
   etree(0, n, 0);
+  lap("etree");
   // (3) postorder (iterative DFS, children in increasing order)
   std::vector<int32_t> head(n, -1), nxt(n, -1);
   for (int32_t j = (int32_t)n - 1; j >= 0; --j)
@@ -319,6 +321,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     const int32_t q = par[post[j]];
     parent[j] = q == -1 ? -1 : (int32_t)ipost[q];
   }
+  lap("postorder");
   // upper pattern + values in the final numbering: column j holds the rows
   // i >= j (diagonal first is not required), used by the column counts,
   // the front structures and the scatter list
@@ -350,7 +353,7 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       }
     });
   }
-  lap("etree+post");
+  lap("upper pattern");
   // (4) column counts (Gilbert, Ng & Peyton 1994: row-subtree leaves and
   // least common ancestors, near O(nnz(M))).  The matrix is already in
   // postorder, so the postorder of the tree is the identity.
