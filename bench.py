@@ -333,6 +333,8 @@ def run_rows(args, rank, world, local, dist):
                        "rows_per_rank": info["n_own"], "halo_rows": info["n_halo"],
                        "frames_decoded_per_rank": f1 - f0,
                        "l2": "256 MiB flush between timed steps", "cg_rtol": args.rtol},
+            # `roofline` = the kernel with the largest share of the step (CUDA
+            # events); the others beside it
             "roofline": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
                          "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DMMA_TFLOPS,
@@ -580,6 +582,34 @@ def main():
     k7_flops = float(st["flops_factor"] + st["flops_solve"])
     k7_sec = float(np.median(fac_ms) + np.median(sol_ms)) / 1e3
     k7_achieved = k7_flops / k7_sec / 1e12 if k7_sec > 0 else 0.0
+    # the solve GEMMs (k_fwd / k_bwd, one launch per tree level and solve):
+    # one untimed pass with CUDA events around every launch (plan stream)
+    plan.set_kernel_timing(True)
+    plan.encode_device([t.data_ptr() for t in d_in])
+    plan.decode_device([t.data_ptr() for t in d_out], rtol=args.rtol)
+    torch.cuda.synchronize()
+    kst = plan.stats()
+    plan.set_kernel_timing(False)
+    solve_launches = int(st["levels"]) * 2  # per direction: levels x (solve + refinement)
+
+    def solve_roofline(name, ms, flops):
+        ach = flops / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": peak,
+                "peak_kind": "measured FP64 DMMA, whole GPU (profiles/r01_peaks.md)",
+                "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": traffic_of(args.config, name),
+                "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, mean per "
+                                  f"launch, {args.config} (profiles/roofline_traffic.json)",
+                "launches_per_step": solve_launches, "algorithmic_flops": flops / solve_launches,
+                "algorithmic_flops_per_step": flops, "ms": ms,
+                "share_of_step": ms / single_ms,
+                "share_basis": "summed launch times of one encode+decode timed alone (CUDA events "
+                               "around every launch on the plan stream)",
+                "model": "per solve 2 W sum_s m_s w_s (P_s r_s forward / P_s^T [y; x] backward), "
+                         "W = 3F; DESIGN.md §5"}
+    roof_fwd = solve_roofline("k_fwd", float(kst["ms_solve_fwd"]), float(kst["flops_solve_fwd"]))
+    roof_bwd = solve_roofline("k_bwd", float(kst["ms_solve_bwd"]), float(kst["flops_solve_bwd"]))
+    roof_main = roof_fwd if roof_fwd["ms"] >= roof_bwd["ms"] else roof_bwd
 
     # ---- e2e through the drop-in C ABI from pinned host memory -------------
     pinned = [torch.from_numpy(np.ascontiguousarray(x, dtype=npdt)).pin_memory() for x in s.axes]
@@ -674,7 +704,11 @@ def main():
                        "l2": "256 MiB flush between timed steps",
                        "plan": "mesh plan (CSR, anchors, normal matrix) built once outside value; "
                                "inside e2e", "cg_rtol": args.rtol},
-            "roofline": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
+            # `roofline` = the kernel with the largest share of the step (CUDA
+            # events); the others beside it
+            "roofline": roof_main,
+            "roofline_other_solve": roof_bwd if roof_main is roof_fwd else roof_fwd,
+            "roofline_oi": {"kernel": "k_oi_cluster", "bound": "tensor", "achieved": achieved,
                          "peak": peak, "peak_kind": "measured FP64 DMMA, whole GPU (profiles/r01_peaks.md)",
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": traffic_of(args.config, "k_oi_cluster"),

@@ -266,10 +266,18 @@ typedef struct {
   double analyze_seconds;     /* host symbolic analysis (plan creation) */
   float ms_oi;                /* fused orthogonal-iteration kernel (k_oi_fused), last encode */
   double flops_oi;            /* its algorithmic flops */
+  /* dmcg_plan_set_kernel_timing only (else 0): summed CUDA-event times of
+   * the solves' forward (k_fwd) and backward (k_bwd) GEMM launches of the
+   * last decode, and their algorithmic flops (2 W sum_s m_s w_s each, per solve) */
+  float ms_solve_fwd, ms_solve_bwd;
+  double flops_solve_fwd, flops_solve_bwd;
 } dmcg_stats;
 int dmcg_plan_stats(const dmcg_plan* plan, dmcg_stats* out);
 /* Stats of the last drop-in dmcg_encode / dmcg_decode on this context. */
 int dmcg_ctx_stats(const dmcg_ctx* ctx, dmcg_stats* out);
+/* Per-launch CUDA events around the solve GEMMs (stats ms_solve_fwd / _bwd)
+ * while on != 0; off by default (the events are extra graph nodes). */
+int dmcg_plan_set_kernel_timing(dmcg_plan* plan, int on);
 /* Stream the plan runs on (cudaStream_t), for event timing by callers. */
 void* dmcg_plan_stream(dmcg_plan* plan);
 /* serialize() of the plan's device-resident symbols: the

@@ -37,6 +37,7 @@ EXPORTS = [
     "dmcg_comm_destroy", "dmcg_shard_layout", "dmcg_plan_create_shard", "dmcg_shard_info_get",
     "dmcg_shard_encode_device", "dmcg_shard_encode_phase", "dmcg_shard_buffer",
     "dmcg_build_connectivity", "dmcg_host_error", "dmcg_ozaki_gemm", "dmcg_plan_delta",
+    "dmcg_plan_set_kernel_timing",
 ]
 
 
@@ -108,7 +109,9 @@ class DmcgStats(ctypes.Structure):
                 ("supernodes", ctypes.c_int), ("levels", ctypes.c_int),
                 ("nnz_factor", ctypes.c_longlong), ("flops_factor", ctypes.c_double),
                 ("flops_solve", ctypes.c_double), ("analyze_seconds", ctypes.c_double),
-                ("ms_oi", ctypes.c_float), ("flops_oi", ctypes.c_double)]
+                ("ms_oi", ctypes.c_float), ("flops_oi", ctypes.c_double),
+                ("ms_solve_fwd", ctypes.c_float), ("ms_solve_bwd", ctypes.c_float),
+                ("flops_solve_fwd", ctypes.c_double), ("flops_solve_bwd", ctypes.c_double)]
 
 
 _lib = None
@@ -170,6 +173,7 @@ def lib():
     L.dmcg_plan_upload.argtypes = [vp, ctypes.POINTER(DmcgEncoded)]
     L.dmcg_plan_basis.argtypes = [vp, ctypes.c_int, f64p, f64p]
     L.dmcg_plan_delta.argtypes = [vp, ctypes.c_int, f64p]
+    L.dmcg_plan_set_kernel_timing.argtypes = [vp, ctypes.c_int]
     L.dmcg_plan_stats.argtypes = [vp, ctypes.POINTER(DmcgStats)]
     L.dmcg_ctx_stats.argtypes = [vp, ctypes.POINTER(DmcgStats)]
     L.dmcg_plan_stream.argtypes = [vp]

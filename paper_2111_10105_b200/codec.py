@@ -336,6 +336,10 @@ class Plan:
         e = c.to_c()
         _check(self.codec.handle, L.lib().dmcg_plan_upload(self._p, ctypes.byref(e)))
 
+    def set_kernel_timing(self, on: bool):
+        """CUDA events around every solve GEMM launch (stats ms_solve_fwd / _bwd)."""
+        _check(self.codec.handle, L.lib().dmcg_plan_set_kernel_timing(self._p, 1 if on else 0))
+
     def delta(self, axis: int):
         """K1's delta coordinates (n x F, f64) of the last device encode."""
         d = np.zeros((self.n, self.F))

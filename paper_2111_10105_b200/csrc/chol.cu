@@ -918,7 +918,18 @@ size_t chol_scratch_doubles(const CholLevels& lv) {
 }
 
 cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels& lv,
-                              const double* b, double* y, double* x, double* out, bool accumulate) {
+                              const double* b, double* y, double* x, double* out, bool accumulate,
+                              const SolveEvents* tev) {
+  // timing points that stay event records inside a graph capture
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (tev && tev->ev) cudaStreamIsCapturing(s, &cap);
+  auto tmark = [&](uint32_t l, int k) {
+    if (!tev || !tev->ev) return;
+    if (cap == cudaStreamCaptureStatusActive)
+      cudaEventRecordWithFlags(tev->ev[4 * l + k], s, cudaEventRecordExternal);
+    else
+      cudaEventRecord(tev->ev[4 * l + k], s);
+  };
   const int W = (int)d.W;
   const unsigned tn = (unsigned)((W + kBN - 1) / kBN);
   LevelTimer lt(s, "solve", lv.nlevels);
@@ -930,7 +941,9 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     lt.mark(l, 0);
     k_gather_own<<<dim3((lv.maxw[l] + 7) / 8, (W + 127) / 128, cnt), 256, 0, s>>>(d, ls, b, x);
     lt.mark(l, 1);
+    tmark(l, 0);
     k_fwd<<<dim3((lv.maxm[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x, y);
+    tmark(l, 1);
     lt.mark(l, 2);
   }
   // backward, roots first: x_s = P_s^T [y_s; x_below]
@@ -938,8 +951,10 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 3);
+    tmark(l, 2);
     k_bwd<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x, out,
                                                                                accumulate ? 1 : 0);
+    tmark(l, 3);
     lt.mark(l, 4);
   }
   lt.report(lv, "gather", "fwd", "bwd", true);

@@ -48,10 +48,16 @@ cudaError_t chol_factor_device(cudaStream_t s, const CholDev& d, const CholLevel
 // Doubles of scratch the blocked L11 inverse needs (CholDev::scratch).
 size_t chol_scratch_doubles(const CholLevels& lv);
 // b: n x W row-major in the original order; y, x: n x W in the permuted order.
+// Optional per-launch timing: ev[4 l + 0 / 1] around level l's forward
+// GEMM, ev[4 l + 2 / 3] around its backward GEMM (4 nlevels events).
+struct SolveEvents {
+  cudaEvent_t* ev = nullptr;
+};
 // out (original order, n x W) = x unpermuted (accumulate: out += x), written
 // by the backward pass itself.
 cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels& lv,
-                              const double* b, double* y, double* x, double* out, bool accumulate);
+                              const double* b, double* y, double* x, double* out, bool accumulate,
+                              const SolveEvents* tev = nullptr);
 // r = b - M x for n x W row-major blocks (original order).
 cudaError_t normal_residual(cudaStream_t s, int n, int W, const uint32_t* rp, const uint32_t* ci,
                             const float* val, const double* b, const double* x, double* r);

@@ -536,6 +536,7 @@ void dmcg_plan_destroy(dmcg_plan* p) {
   for (auto& e : p->ev) p->ctx->give_event(e, true);
   for (auto e : {p->ev_fork, p->ev_join, p->ev_pf_fork, p->ev_pf_join}) p->ctx->give_event(e, false);
   for (auto e : {p->ev_pf0, p->ev_pf1}) p->ctx->give_event(e, true);
+  for (auto e : p->solve_ev) cudaEventDestroy(e);
   delete p;
 }
 
@@ -1339,6 +1340,12 @@ int dmcg_ctx_stats(const dmcg_ctx* c, dmcg_stats* out) {
 }
 
 void* dmcg_plan_stream(dmcg_plan* p) { return p ? (void*)p->ctx->stream : nullptr; }
+
+int dmcg_plan_set_kernel_timing(dmcg_plan* p, int on) {
+  if (!p) return DMCG_E_CONFIG;
+  p->kernel_timing = on != 0;
+  return DMCG_OK;
+}
 
 // ---- drop-in encode / decode -------------------------------------------------
 

@@ -318,6 +318,8 @@ struct dmcg_plan {
   int* d_pf_flag = nullptr;        // non-positive pivot of the overlapped factor
   bool factor_pending = false;     // the last encode left a factor of M for the next decode
   bool pf_unjoined = false;        // ... launched outside any graph: the decode waits ev_pf_join
+  bool kernel_timing = false;      // dmcg_plan_set_kernel_timing
+  std::vector<cudaEvent_t> solve_ev;  // (1 + refine) x 4 nlevels timing events
   float ms_prefactor = 0.0f;
   dmcg_stats stats = {};
 };

@@ -825,13 +825,26 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
   const bool mc = variant_uses_means(p->variant);
   const int nm = (int)cdev.n;
   const size_t o = mc ? (size_t)W : 0;
+  const size_t evl = 4 * (size_t)p->levels.nlevels;
+  if (p->kernel_timing && p->solve_ev.size() < (size_t)(1 + refine) * evl) {
+    const size_t have = p->solve_ev.size();
+    p->solve_ev.resize((size_t)(1 + refine) * evl);
+    for (size_t e = have; e < p->solve_ev.size(); ++e) cudaEventCreate(&p->solve_ev[e]);
+  }
+  auto tev = [&](int pass) {
+    SolveEvents t;
+    if (p->kernel_timing) t.ev = p->solve_ev.data() + (size_t)pass * evl;
+    return t;
+  };
+  const SolveEvents tev0 = tev(0);
   DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_b + o, p->d_rm_y, p->d_rm_xp,
-                             p->d_rm_x + o, false));
+                             p->d_rm_x + o, false, &tev0));
   for (int r = 0; r < refine; ++r) {
     DMCG_TRY(normal_residual(s, nm, W, p->d_m_rp, p->d_m_ci, p->d_m_val, p->d_rm_b + o,
                              p->d_rm_x + o, p->d_rm_r));
+    const SolveEvents tevr = tev(1 + r);
     DMCG_TRY(chol_solve_device(s, cdev, p->levels, p->d_rm_r, p->d_rm_y, p->d_rm_xp,
-                               p->d_rm_x + o, true));
+                               p->d_rm_x + o, true, &tevr));
   }
   DMCG_TRY(record_event(p->ev[3], s));
   const double* shift = nullptr;
@@ -874,8 +887,8 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   const int W = 3 * (int)Fw;
   const void* key[4] = {out[0], out[1], out[2], nullptr};
   {
-    const long long okey = ((long long)f0 << 40) | ((long long)Fw << 16) | (refine * 4) |
-                           (pre ? 2 : 0) | (factor ? 1 : 0);
+    const long long okey = ((long long)f0 << 40) | ((long long)Fw << 16) | (refine * 8) |
+                           (p->kernel_timing ? 4 : 0) | (pre ? 2 : 0) | (factor ? 1 : 0);
     Status st = run_graph(p, p->g_decode, key, okey, [&] {
       return enqueue_decode_direct(p, refine, factor, pre, out, (int)f0, (int)Fw);
     });
@@ -900,6 +913,21 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   p->stats.kernel_launches_decode = (k > 0 ? 2 : 0) + 1 + (factor ? nl : 0) +
                                     (1 + refine) * per_solve + refine + 1;
   p->stats.flops_solve = (1 + refine) * p->chol.flops_solve_per_rhs * W;
+  p->stats.ms_solve_fwd = p->stats.ms_solve_bwd = 0.0f;
+  p->stats.flops_solve_fwd = p->stats.flops_solve_bwd = 0.0;
+  if (p->kernel_timing) {  // the events completed with the stream sync above
+    const size_t evl = 4 * (size_t)lv.nlevels;
+    for (int pass = 0; pass <= refine; ++pass)
+      for (uint32_t l = 0; l < lv.nlevels; ++l) {
+        const cudaEvent_t* e = p->solve_ev.data() + pass * evl + 4 * l;
+        float a = 0.0f, b = 0.0f;
+        cudaEventElapsedTime(&a, e[0], e[1]);
+        cudaEventElapsedTime(&b, e[2], e[3]);
+        p->stats.ms_solve_fwd += a;
+        p->stats.ms_solve_bwd += b;
+      }
+    p->stats.flops_solve_fwd = p->stats.flops_solve_bwd = 0.5 * p->stats.flops_solve;
+  }
   if (flags[1]) return Status{DMCG_E_CORRUPT, "CorruptPayload: packed value out of range"};
   if (flags[4]) {
     p->factor_valid = false;
