@@ -10,6 +10,8 @@
 // multi-RHS solves are then pure batched GEMMs per level.
 #pragma once
 #include <cstdint>
+#include <map>
+#include <utility>
 #include <vector>
 
 namespace dmcg {
@@ -50,10 +52,19 @@ struct CholPlan {
 // M given as a symmetric CSR (rows sorted, diagonal present).
 // g_rp / g_ci (optional): the 1-ring graph whose square is M's pattern (the
 // mesh Laplacian's structure), used for a cheaper nested-dissection ordering.
+// pre (optional): the ordering of chol_order_graph on the same 1-ring graph,
+// computed ahead (it does not need M, so a caller can run it beside the
+// normal-matrix build).
+struct CholOrdering {
+  std::vector<uint32_t> perm0;  // elimination order before the postorder
+  std::map<uint64_t, std::pair<uint32_t, uint32_t>> splits;  // dissection ranges (see .cpp)
+};
+void chol_order_graph(uint32_t n, const std::vector<uint32_t>& g_rp,
+                      const std::vector<uint32_t>& g_ci, CholOrdering* out);
 void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector<uint32_t>& ci,
                   const std::vector<float>& val, CholPlan* plan,
                   const std::vector<uint32_t>* g_rp = nullptr,
-                  const std::vector<uint32_t>* g_ci = nullptr);
+                  const std::vector<uint32_t>* g_ci = nullptr, CholOrdering* pre = nullptr);
 
 // CPU reference numerics over the same structures (tests / debugging).
 // F: front_off[nsup] doubles, Linv: inv_off[nsup] doubles.  Returns false if

@@ -31,13 +31,18 @@ struct Graph {
 // Nested dissection on M's graph.  Each sub-problem is a contiguous range
 // of one index array, partitioned in place (parts A | B | separator S);
 // two BFS per split: from any vertex to the farthest one (pseudo-
-// peripheral), then the level structure from there.  Leaves of <= 48
-// vertices keep their order.  Because every range is partitioned in place
-// as A | B | S, the final index array IS the elimination order (old
-// indices; A's order, then B's, then S).  The two halves of the upper
-// dissection levels run on separate threads: they touch disjoint ranges,
-// and the only cross-range read (part_ of a neighbour) compares against an
-// id the other range never holds.
+// peripheral), then the level structure from there.  A BFS marks a vertex
+// visited by moving it to a fresh part id (one random read per edge, no
+// per-vertex level array) and its queue, which holds the vertices level by
+// level, is the new order of the range: A = the levels before the
+// separator, S = the separator levels, B = the levels after it are
+// contiguous pieces of the queue.  Leaves of <= 48 vertices keep their
+// order.  Because every range is partitioned in place as A | B | S, the
+// final index array IS the elimination order (old indices; A's order, then
+// B's, then S).  The two halves of the upper dissection levels run on
+// separate threads: they touch disjoint ranges, and the only cross-range
+// read (part_ of a neighbour) compares against an id the other range never
+// holds.
 class NestedDissection {
  public:
   // wide: g is the 1-ring graph G of a matrix whose pattern is G^2 (M = L^T L
@@ -45,7 +50,7 @@ class NestedDissection {
   // between the levels before and after them passes through one of the two),
   // at a third of the edge visits of BFS on G^2.
   explicit NestedDissection(const Graph& g, bool wide = false)
-      : g_(g), wide_(wide), part_(g.n, 0), level_(g.n, -1), queue_(g.n), idx_(g.n), tmp_(g.n) {}
+      : g_(g), wide_(wide), part_(g.n, 0), queue_(g.n), idx_(g.n), lstart_(2 * (size_t)g.n + 2) {}
 
   std::vector<uint32_t> run() {
     for (uint32_t i = 0; i < g_.n; ++i) idx_[i] = i;
@@ -65,8 +70,9 @@ class NestedDissection {
   static constexpr uint32_t kParMin = 4096;  // smallest half worth a thread
   const Graph g_;
   const bool wide_;
-  std::vector<int32_t> part_, level_;
-  std::vector<uint32_t> queue_, idx_, tmp_;
+  std::vector<int32_t> part_;
+  std::vector<uint32_t> queue_, idx_;
+  std::vector<uint32_t> lstart_;  // level starts of the last BFS of a range, at [2 b + level]
   std::atomic<int32_t> next_id_{1};
   std::mutex split_mu_;
 
@@ -86,16 +92,13 @@ class NestedDissection {
       st.pop_back();
       if (t.e - t.b <= 48) continue;
       uint32_t na, ns;
-      if (split(t.b, t.e, t.id, &na, &ns) == 0) continue;  // no useful split
-      const int32_t ia = next_id_.fetch_add(3), ib = ia + 1, is = ia + 2;
+      int32_t ia, ib;
+      if (split(t.b, t.e, t.id, &na, &ns, &ia, &ib) == 0) continue;  // no useful split
       const uint32_t e_a = t.b + na, e_b = t.e - ns;
       if (t.e - t.b >= kSplitRecord) {
         std::lock_guard<std::mutex> lk(split_mu_);
         splits[((uint64_t)t.b << 32) | t.e] = {e_a, e_b};
       }
-      for (uint32_t q = t.b; q < e_a; ++q) set_part(idx_[q], ia);
-      for (uint32_t q = e_a; q < e_b; ++q) set_part(idx_[q], ib);
-      for (uint32_t q = e_b; q < t.e; ++q) set_part(idx_[q], is);
       if (t.depth < kParDepth && na >= kParMin && e_b - e_a >= kParMin) {
         std::thread th([this, t, e_a, ia] { process(t.b, e_a, ia, t.depth + 1); });
         process(e_a, e_b, ib, t.depth + 1);
@@ -107,95 +110,104 @@ class NestedDissection {
     }
   }
 
-  // BFS over the vertices of part `id`; queue = range-local buffer.
-  uint32_t bfs(uint32_t root, int32_t id, uint32_t* queue, uint32_t* maxlev) {
-    uint32_t head = 0, tail = 0;
+  // BFS over the vertices of part `from`, moving every reached vertex to part
+  // `to`; queue = range-local buffer, lstart[l] = queue position where level l
+  // begins (lstart[levels] = reached).  Returns the number of levels.
+  uint32_t bfs(uint32_t root, int32_t from, int32_t to, uint32_t* queue, uint32_t* lstart,
+               uint32_t* reached) {
+    uint32_t head = 0, tail = 0, levels = 0;
     queue[tail++] = root;
-    level_[root] = 0;
-    uint32_t last = root;
+    set_part(root, to);
     while (head < tail) {
-      const uint32_t v = queue[head++];
-      last = v;
-      const int32_t lv = level_[v] + 1;
-      for (uint32_t p = g_.rp[v]; p < g_.rp[v + 1]; ++p) {
-        const uint32_t w = g_.ci[p];
-        if (part(w) == id && level_[w] < 0) {
-          level_[w] = lv;
-          queue[tail++] = w;
+      lstart[levels++] = head;
+      for (const uint32_t lend = tail; head < lend; ++head) {
+        const uint32_t v = queue[head];
+        for (uint32_t p = g_.rp[v]; p < g_.rp[v + 1]; ++p) {
+          const uint32_t w = g_.ci[p];
+          if (part(w) == from) {
+            set_part(w, to);
+            queue[tail++] = w;
+          }
         }
       }
     }
-    *maxlev = (uint32_t)level_[last];
-    return tail;
+    lstart[levels] = tail;
+    *reached = tail;
+    return levels;
   }
 
-  // Partitions idx_[b, e) into A | B | S.  Returns 0 if no split is made;
-  // a disconnected range becomes A = reached component, B = rest, S empty.
-  int split(uint32_t b, uint32_t e, int32_t id, uint32_t* na, uint32_t* ns) {
+  // Partitions idx_[b, e) (all of part `id`) into A | B | S; *ia / *ib = the
+  // part ids of A and B afterwards.  Returns 0 if no split is made (the range
+  // keeps one id, returned in *ia); a disconnected range becomes A = reached
+  // component, B = rest, S empty.
+  int split(uint32_t b, uint32_t e, int32_t id, uint32_t* na, uint32_t* ns, int32_t* ia,
+            int32_t* ib) {
     const uint32_t cnt = e - b;
     uint32_t* queue = queue_.data() + b;
-    uint32_t* tmp = tmp_.data() + b;
-    for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
-    uint32_t maxlev;
-    const uint32_t reached = bfs(idx_[b], id, queue, &maxlev);
+    uint32_t* lstart = lstart_.data() + 2 * (size_t)b;  // <= cnt + 1 entries of the range's 2 cnt
+    const int32_t t1 = next_id_.fetch_add(4), t2 = t1 + 1, t3 = t1 + 2, t4 = t1 + 3;
+    uint32_t reached;
+    uint32_t levels = bfs(idx_[b], id, t1, queue, lstart, &reached);
     if (reached < cnt) {
-      uint32_t a = b, z = 0;
+      // A = the reached component (now part t1) in BFS order, B = the rest (still `id`)
+      uint32_t z = reached;
       for (uint32_t q = b; q < e; ++q) {
         const uint32_t v = idx_[q];
-        if (level_[v] >= 0)
-          idx_[a++] = v;
-        else
-          tmp[z++] = v;
+        if (part(v) == id) queue[z++] = v;
       }
-      std::copy(tmp, tmp + z, idx_.begin() + a);
-      *na = a - b;
+      std::copy(queue, queue + cnt, idx_.begin() + b);
+      *na = reached;
       *ns = 0;
+      *ia = t1;
+      *ib = id;
       return 1;
     }
     const uint32_t root = queue[cnt - 1];
-    for (uint32_t q = b; q < e; ++q) level_[idx_[q]] = -1;
-    bfs(root, id, queue, &maxlev);
+    levels = bfs(root, t1, t2, queue, lstart, &reached);
+    const uint32_t maxlev = levels - 1;
     const uint32_t wsep = wide_ ? 2u : 1u;  // separator levels
-    if (maxlev < 1 + wsep) return 0;
+    *ia = t2;
+    if (maxlev < 1 + wsep) {
+      std::copy(queue, queue + cnt, idx_.begin() + b);
+      return 0;
+    }
     // separator = the level where the running count first exceeds half
-    std::vector<uint32_t> hist(maxlev + 2, 0);
-    for (uint32_t q = b; q < e; ++q) hist[level_[idx_[q]]]++;
-    uint32_t acc = 0, sep = 1;
-    for (uint32_t l = 0; l <= maxlev; ++l) {
-      if (acc + hist[l] > cnt / 2) {
+    uint32_t sep = 1;
+    for (uint32_t l = 0; l <= maxlev; ++l)
+      if (lstart[l + 1] > cnt / 2) {
         sep = l;
         break;
       }
-      acc += hist[l];
-    }
     if (sep == 0) sep = 1;
     if (sep + wsep > maxlev) sep = maxlev - wsep;
     const uint32_t sep_hi = sep + wsep - 1;  // separator = levels [sep, sep_hi]
-    uint32_t a = b, zb = 0, zs = 0;
-    uint32_t* sbuf = queue;  // queue no longer needed
-    for (uint32_t q = b; q < e; ++q) {
-      const uint32_t v = idx_[q];
-      const uint32_t l = (uint32_t)level_[v];
-      if (l < sep)
-        idx_[a++] = v;
-      else if (l > sep_hi)
-        tmp[zb++] = v;
-      else
-        sbuf[zs++] = v;
-    }
-    std::copy(tmp, tmp + zb, idx_.begin() + a);
-    std::copy(sbuf, sbuf + zs, idx_.begin() + a + zb);
-    *na = a - b;
-    *ns = zs;
+    const uint32_t a_end = lstart[sep], s_end = lstart[sep_hi + 1];
+    // new order: A = queue[0, a_end) | B = queue[s_end, cnt) | S = queue[a_end, s_end)
+    uint32_t* dst = idx_.data() + b;
+    std::copy(queue, queue + a_end, dst);
+    std::copy(queue + s_end, queue + cnt, dst + a_end);
+    std::copy(queue + a_end, queue + s_end, dst + a_end + (cnt - s_end));
+    for (uint32_t q = s_end; q < cnt; ++q) set_part(queue[q], t3);
+    for (uint32_t q = a_end; q < s_end; ++q) set_part(queue[q], t4);
+    *ib = t3;
+    *na = a_end;
+    *ns = s_end - a_end;
     return 2;
   }
 };
 
 }  // namespace
 
+void chol_order_graph(uint32_t n, const std::vector<uint32_t>& g_rp,
+                      const std::vector<uint32_t>& g_ci, CholOrdering* out) {
+  NestedDissection nd(Graph{n, g_rp.data(), g_ci.data()}, true);
+  out->perm0 = nd.run();
+  out->splits = std::move(nd.splits);
+}
+
 void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector<uint32_t>& ci,
                   const std::vector<float>& val, CholPlan* P, const std::vector<uint32_t>* g_rp,
-                  const std::vector<uint32_t>* g_ci) {
+                  const std::vector<uint32_t>* g_ci, CholOrdering* pre) {
   CholPlan& p = *P;
   p = CholPlan();
   p.n = n;
@@ -214,9 +226,16 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
   // is its square), else on M's own graph
   static const bool m_graph = std::getenv("DMCG_ND_MGRAPH") != nullptr;
   const bool wide = g_rp && g_ci && g_rp->size() == (size_t)n + 1 && !m_graph;
-  Graph g = wide ? Graph{n, g_rp->data(), g_ci->data()} : Graph{n, rp.data(), ci.data()};
-  NestedDissection nd(g, wide);
-  std::vector<uint32_t> perm0 = nd.run();
+  CholOrdering own;
+  if (!pre || pre->perm0.size() != n) {
+    Graph g = wide ? Graph{n, g_rp->data(), g_ci->data()} : Graph{n, rp.data(), ci.data()};
+    NestedDissection nd(g, wide);
+    own.perm0 = nd.run();
+    own.splits = std::move(nd.splits);
+    pre = &own;
+  }
+  std::vector<uint32_t>& perm0 = pre->perm0;
+  const auto& nd_splits = pre->splits;
   lap("ordering");
   std::vector<uint32_t> iperm0(n);
   for (uint32_t k = 0; k < n; ++k) iperm0[perm0[k]] = k;
@@ -267,8 +286,8 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
     }
   };
   std::function<void(uint32_t, uint32_t, int)> etree = [&](uint32_t b, uint32_t e, int depth) {
-    const auto it = nd.splits.find(((uint64_t)b << 32) | e);
-    if (it == nd.splits.end()) {
+    const auto it = nd_splits.find(((uint64_t)b << 32) | e);
+    if (it == nd_splits.end()) {
       liu(b, e);
       return;
     }
@@ -619,6 +638,27 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
       }
     }
   });
+  // (9) scatter list of M into the fronts (lower part, column-major local):
+  // on the pool from a helper thread, under the serial pull-list pass below
+  std::thread scatter_thread([&] {
+    p.a_ptr.assign(NS + 1, 0);
+    for (uint32_t s = 0; s < NS; ++s) p.a_ptr[s + 1] = up[p.first[s + 1]];
+    p.a_pos.resize(p.a_ptr[NS]);
+    p.a_val.resize(p.a_ptr[NS]);
+    parallel_for(NS, 64, [&](uint32_t s0, uint32_t s1, uint32_t) {
+      std::vector<int32_t> loc(n, -1);
+      for (uint32_t s = s0; s < s1; ++s) {
+        const uint32_t m = p.m(s), f0 = p.first[s], f1 = p.first[s + 1];
+        for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = (int32_t)t;
+        for (uint32_t j = f0; j < f1; ++j)
+          for (uint32_t q = up[j]; q < up[j + 1]; ++q) {
+            p.a_pos[q] = (j - f0) * m + (uint32_t)loc[ui[q]];
+            p.a_val[q] = uv[q];
+          }
+        for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = -1;
+      }
+    });
+  });
   // pull lists (see chol.h): count per parent row, then fill child by child
   {
     const uint64_t R = p.rhs_off[NS];
@@ -642,26 +682,8 @@ void chol_analyze(uint32_t n, const std::vector<uint32_t>& rp, const std::vector
         }
       }
   }
-  lap("rel maps");
-  // (9) scatter list of M into the fronts (lower part, column-major local)
-  p.a_ptr.assign(NS + 1, 0);
-  for (uint32_t s = 0; s < NS; ++s) p.a_ptr[s + 1] = up[p.first[s + 1]];
-  p.a_pos.resize(p.a_ptr[NS]);
-  p.a_val.resize(p.a_ptr[NS]);
-  parallel_for(NS, 64, [&](uint32_t s0, uint32_t s1, uint32_t) {
-    std::vector<int32_t> loc(n, -1);
-    for (uint32_t s = s0; s < s1; ++s) {
-      const uint32_t m = p.m(s), f0 = p.first[s], f1 = p.first[s + 1];
-      for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = (int32_t)t;
-      for (uint32_t j = f0; j < f1; ++j)
-        for (uint32_t q = up[j]; q < up[j + 1]; ++q) {
-          p.a_pos[q] = (j - f0) * m + (uint32_t)loc[ui[q]];
-          p.a_val[q] = uv[q];
-        }
-      for (uint32_t t = 0; t < m; ++t) loc[p.str_idx[p.str_ptr[s] + t]] = -1;
-    }
-  });
-  lap("scatter");
+  scatter_thread.join();
+  lap("rel maps+scatter");
 }
 
 // ---------------------------------------------------------------------------

@@ -8,7 +8,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <limits>
+#include <malloc.h>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <vector>
@@ -22,7 +25,8 @@ namespace dmcg {
 
 constexpr uint32_t kColBlock = 4;  // CG column-block width, = kCB in common.cuh
 
-Status plan_encode(dmcg_plan* p, const void* const x[3]);
+Status plan_encode(dmcg_plan* p, const void* const x[3],
+                   const std::function<void()>* between = nullptr);
 Status plan_decode(dmcg_plan* p, const dmcg_decode_options* opt, void* const out[3]);
 
 #define CUDA_OK(expr)                                                                      \
@@ -219,22 +223,28 @@ void build_normal_matrix(MeshHost* m) {
     cval[c] = std::move(va);
     crl[c] = std::move(rl);
   });
-  m->m_rp.assign((size_t)n + 1, 0);
-  size_t tot = 0;
-  for (uint32_t c = 0; c < nch; ++c) tot += cci[c].size();
-  m->m_ci.resize(tot);
-  m->m_val.resize(tot);
-  size_t o = 0;
-  uint32_t row = 0;
+  // concatenate: every chunk copies its rows to its offset (parallel)
+  std::vector<size_t> off(nch + 1, 0);
+  std::vector<uint32_t> row0(nch + 1, 0);
   for (uint32_t c = 0; c < nch; ++c) {
-    std::copy(cci[c].begin(), cci[c].end(), m->m_ci.begin() + o);
-    std::copy(cval[c].begin(), cval[c].end(), m->m_val.begin() + o);
-    o += cci[c].size();
-    for (uint32_t len : crl[c]) {
-      m->m_rp[row + 1] = m->m_rp[row] + len;
-      ++row;
-    }
+    off[c + 1] = off[c] + cci[c].size();
+    row0[c + 1] = row0[c] + (uint32_t)crl[c].size();
   }
+  m->m_rp.resize((size_t)n + 1);
+  m->m_ci.resize(off[nch]);
+  m->m_val.resize(off[nch]);
+  m->m_rp[0] = 0;
+  parallel_for(nch, 1, [&](uint32_t c0, uint32_t c1, uint32_t) {
+    for (uint32_t c = c0; c < c1; ++c) {
+      std::copy(cci[c].begin(), cci[c].end(), m->m_ci.begin() + off[c]);
+      std::copy(cval[c].begin(), cval[c].end(), m->m_val.begin() + off[c]);
+      uint32_t at = (uint32_t)off[c], row = row0[c];
+      for (uint32_t len : crl[c]) {
+        at += len;
+        m->m_rp[++row] = at;
+      }
+    }
+  });
 }
 
 void build_reduced_normal(MeshHost* m) {
@@ -371,7 +381,25 @@ extern "C" {
 
 int dmcg_abi_version(void) { return DMCG_ABI_VERSION; }
 
+// The decoder's host analysis (mesh CSR, normal matrix, symbolic Cholesky)
+// allocates and frees ~200 MB of index arrays per call.  With glibc's default
+// thresholds every such array is a fresh mmap whose first touch page-faults
+// (from 16 pool threads at once: they serialise on the mm lock); on the B200
+// host that is half of the analysis time (115 -> 65 ms for 262 144 vertices,
+// tools/analysis_bench.py).  Keep freed blocks on the heap instead: process-
+// wide, set once, DMCG_NO_MALLOPT=1 leaves the allocator alone.
+static void tune_host_allocator() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (std::getenv("DMCG_NO_MALLOPT")) return;
+    mallopt(M_MMAP_THRESHOLD, 32 << 20);  // glibc's upper limit
+    mallopt(M_TRIM_THRESHOLD, std::numeric_limits<int>::max());
+    mallopt(M_TOP_PAD, 256 << 20);
+  });
+}
+
 int dmcg_create(dmcg_ctx** out, int device) {
+  tune_host_allocator();
   if (!out) return DMCG_E_CONFIG;
   *out = nullptr;
   int count = 0;
@@ -547,7 +575,7 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
                                const uint32_t* faces, uint32_t n_faces, const dmcg_config* cfg,
                                const uint32_t* anchors_given, uint32_t n_c_given,
                                dmcg_plan** out, MeshHost* mesh_given = nullptr,
-                               bool encode_side = true) {
+                               bool encode_side = true, cudaStream_t up_stream = nullptr) {
   *out = nullptr;
   if (n == 0 || F == 0) return {DMCG_E_INDEX, "ValidationError: sequence is empty"};
   if (dtype != DMCG_F64 && dtype != DMCG_F32) return {DMCG_E_CONFIG, "ConfigError: bad dtype"};
@@ -564,6 +592,8 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     p->mesh.n = n;
     p->mesh.lap_rp = std::move(mesh_given->lap_rp);
     p->mesh.lap_ci = std::move(mesh_given->lap_ci);
+    p->mesh.adj_rp = std::move(mesh_given->adj_rp);  // present when the caller built the mesh
+    p->mesh.adj_ci = std::move(mesh_given->adj_ci);
   } else {
     st = build_mesh(faces, n_faces, n, &p->mesh);
   }
@@ -751,7 +781,8 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
   // the plan's (pageable) uploads go on the side stream and are waited for
   // here: a drop-in encode has already queued its input H2D on ctx->stream,
   // which keeps running under the host-side plan work
-  cudaStream_t s = ctx->aux;
+  cudaStream_t s = up_stream ? up_stream : ctx->aux;
+  p->up_stream = up_stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
   };
@@ -808,7 +839,7 @@ dmcg::Status dmcg::plan_prepare_normal(dmcg_plan* p) {
   p->d_m_val = (float*)plan_alloc(p, m.m_val.size() * 4);
   if (!p->d_m_rp || !p->d_m_ci || !p->d_m_val)
     return {DMCG_E_CUDA, "CudaError: device allocation failed"};
-  cudaStream_t s = p->ctx->stream;
+  cudaStream_t s = p->up_stream ? p->up_stream : p->ctx->stream;
   bool ok = cudaMemcpyAsync(p->d_m_rp, m.m_rp.data(), m.m_rp.size() * 4, cudaMemcpyHostToDevice,
                             s) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(p->d_m_ci, m.m_ci.data(), m.m_ci.size() * 4,
@@ -922,7 +953,7 @@ dmcg::Status dmcg::plan_prepare_decode(dmcg_plan* p) {
   p->stats.analyze_seconds = p->analyze_seconds;
   if (!ok) return {DMCG_E_CUDA, "CudaError: device allocation failed"};
   tm.lap("alloc");
-  cudaStream_t s = p->ctx->stream;
+  cudaStream_t s = p->up_stream ? p->up_stream : p->ctx->stream;
   auto h2d = [&](void* d, const void* h, size_t bytes) {
     if (bytes) ok = ok && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
   };
@@ -1063,7 +1094,11 @@ int dmcg_plan_decode_device(dmcg_plan* p, const dmcg_decode_options* opt, void* 
   return p->ctx->set_error(plan_decode(p, &o, d_out));
 }
 
-static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
+// download = issue (header fields + every D2H copy queued on the plan stream,
+// asynchronous for page-locked destinations) + a stream synchronise + finish
+// (host-side fix-ups).  dmcg_encode queues the copies behind its kernels and
+// prepares the next decode before waiting for them.
+static Status download_issue(dmcg_plan* p, dmcg_encoded* e) {
   cudaStream_t s = p->ctx->stream;
   // blocks: per axis nb k_f^2 dictionary levels and nb k_l rows; anchors
   // and frames unpadded (F_in) on the host
@@ -1082,7 +1117,7 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
   e->dict_bits = (uint8_t)p->dict_bits;
   e->diff_bits = (uint8_t)p->diff_bits;
   if (!e->faces) e->faces = p->faces.data();
-  float rng[6];
+  float* rng = p->h_anchor_rng;
   for (int a = 0; a < 3; ++a) {
     CUDA_OK(cudaMemcpyAsync(e->dict_q[a], p->d_dict_q + a * FF, FF * 2, cudaMemcpyDeviceToHost, s));
     if (k) {
@@ -1108,10 +1143,14 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
     if (variant_uses_means(p->variant) && e->means[a])
       CUDA_OK(cudaMemcpyAsync(e->means[a], p->d_means + a * F, F * 4, cudaMemcpyDeviceToHost, s));
   }
-  std::memset(rng, 0, sizeof(rng));
+  std::memset(rng, 0, 6 * sizeof(float));
   if (p->n_c)
-    CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
-  CUDA_OK(cudaStreamSynchronize(s));
+    CUDA_OK(cudaMemcpyAsync(rng, p->d_anchor_rng, 6 * sizeof(float), cudaMemcpyDeviceToHost, s));
+  return Status::ok();
+}
+static void download_finish(dmcg_plan* p, dmcg_encoded* e) {
+  const size_t n = p->n, k = p->k;
+  const float* rng = p->h_anchor_rng;
   if (p->n_c) std::memcpy(e->anchor_idx, p->mesh.anchors.data(), (size_t)p->n_c * 4);
   for (int a = 0; a < 3; ++a) {
     e->anchor_min[a] = rng[2 * a];
@@ -1123,6 +1162,12 @@ static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
     for (size_t r = 0; r < k; ++r)
       if (e->row_min[a][r] == e->row_max[a][r])
         std::memset(e->coeff_q[a] + r * n, 0, n * 2);
+}
+static Status download_impl(dmcg_plan* p, dmcg_encoded* e) {
+  Status st = download_issue(p, e);
+  if (!st.good()) return st;
+  CUDA_OK(cudaStreamSynchronize(p->ctx->stream));
+  download_finish(p, e);
   return Status::ok();
 }
 
@@ -1382,53 +1427,61 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   if (!ctx || !seq || !cfg || !out) return DMCG_E_CONFIG;
   cudaSetDevice(ctx->device);
   PhaseTimer tm("encode");
-  {
-    // The decoder's analysis of this mesh (normal matrix + symbolic
-    // Cholesky), started first on a host thread: it needs only the faces and
-    // the anchor set (dmcg_select_anchors is a function of n and the config),
-    // so it runs under the whole encode (input H2D, plan, kernels, download).
-    ctx->pending.reset();
+  // Started below, once the mesh CSR exists: the decoder's analysis of this
+  // mesh (normal matrix + symbolic Cholesky) on a host thread.  It needs only
+  // the Laplacian structure and the anchor set (dmcg_select_anchors is a
+  // function of n and the config), so it runs under the rest of the encode
+  // (input H2D, plan, kernels, download).
+  ctx->pending.reset();
+  auto start_analysis = [&](const MeshHost& built) {
     static const bool off = std::getenv("DMCG_NO_OVERLAP") != nullptr;
-    if (!off && cfg->variant != DMCG_V2V && seq->faces && seq->n_faces && seq->n) {
-      auto pa = std::make_unique<PendingAnalysis>();
-      pa->n = seq->n;
-      pa->n_faces = seq->n_faces;
-      pa->faces_hash = hash_faces(seq->faces, seq->n_faces);
-      pa->reduced = variant_uses_means(cfg->variant);
-      if (!pa->reduced) {
-        const uint32_t n_c = dmcg_anchor_count(seq->n, cfg->anchor_fraction);
-        pa->anchors.resize(n_c);
-        if (n_c == 0 || dmcg_select_anchors(seq->n, n_c, cfg->anchor_strategy, cfg->seed,
-                                            pa->anchors.data()) != DMCG_OK)
-          pa.reset();
-      }
-      if (pa) {
-        std::vector<uint32_t> faces(seq->faces, seq->faces + 3 * (size_t)seq->n_faces);
-        PendingAnalysis* raw = pa.get();
-        pa->th = std::thread([raw, faces = std::move(faces)] {
-          const auto t0 = std::chrono::steady_clock::now();
-          MeshHost& m = raw->mesh;
-          if (!build_mesh(faces.data(), raw->n_faces, raw->n, &m).good()) {
-            raw->failed = true;
-            return;
-          }
-          m.anchor_pos.assign(raw->n, -1);
-          for (uint32_t t = 0; t < raw->anchors.size(); ++t)
-            m.anchor_pos[raw->anchors[t]] = (int32_t)t;
-          m.anchors = raw->anchors;
-          if (raw->reduced)
-            build_reduced_normal(&m);
-          else
-            build_normal_matrix(&m);
-          chol_analyze(raw->n - (raw->reduced ? 1 : 0), m.m_rp, m.m_ci, m.m_val, &raw->chol,
-                       raw->reduced ? nullptr : &m.lap_rp, raw->reduced ? nullptr : &m.lap_ci);
-          raw->seconds =
-              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        });
-        ctx->pending = std::move(pa);
-      }
+    if (off || cfg->variant == DMCG_V2V || !seq->faces || !seq->n_faces || !seq->n) return;
+    auto pa = std::make_unique<PendingAnalysis>();
+    pa->n = seq->n;
+    pa->n_faces = seq->n_faces;
+    pa->faces_hash = hash_faces(seq->faces, seq->n_faces);
+    pa->reduced = variant_uses_means(cfg->variant);
+    if (!pa->reduced) {
+      const uint32_t n_c = dmcg_anchor_count(seq->n, cfg->anchor_fraction);
+      pa->anchors.resize(n_c);
+      if (n_c == 0 || dmcg_select_anchors(seq->n, n_c, cfg->anchor_strategy, cfg->seed,
+                                          pa->anchors.data()) != DMCG_OK)
+        return;
     }
-  }
+    // its own copy of the structure: the thread may outlive the encode plan
+    pa->mesh.n = built.n;
+    pa->mesh.lap_rp = built.lap_rp;
+    pa->mesh.lap_ci = built.lap_ci;
+    PendingAnalysis* raw = pa.get();
+    pa->th = std::thread([raw] {
+      const auto t0 = std::chrono::steady_clock::now();
+      PhaseTimer ta("analysis-thread");
+      MeshHost& m = raw->mesh;
+      m.anchor_pos.assign(raw->n, -1);
+      for (uint32_t t = 0; t < raw->anchors.size(); ++t)
+        m.anchor_pos[raw->anchors[t]] = (int32_t)t;
+      m.anchors = raw->anchors;
+      if (raw->reduced) {
+        build_reduced_normal(&m);
+        ta.lap("normal matrix");
+        chol_analyze(raw->n - 1, m.m_rp, m.m_ci, m.m_val, &raw->chol);
+      } else {
+        // the nested-dissection ordering needs only the 1-ring graph: it runs
+        // (on its own threads) beside the normal-matrix build (host pool)
+        CholOrdering ord;
+        std::thread order_thread([&] { chol_order_graph(raw->n, m.lap_rp, m.lap_ci, &ord); });
+        build_normal_matrix(&m);
+        ta.lap("normal matrix");
+        order_thread.join();
+        ta.lap("ordering (rest)");
+        chol_analyze(raw->n, m.m_rp, m.m_ci, m.m_val, &raw->chol, &m.lap_rp, &m.lap_ci, &ord);
+      }
+      ta.lap("chol_analyze");
+      raw->seconds =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+    ctx->pending = std::move(pa);
+  };
   // The input upload goes first, into pool buffers: with pinned host memory
   // it runs on the copy engine while the host builds the mesh (CSR,
   // validation, anchors) for the plan below.
@@ -1456,37 +1509,55 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
     if (!ok) return ctx->set_error({DMCG_E_CUDA, "CudaError: H2D copy failed"});
   }
   tm.lap("h2d issue");
+  // One mesh build (host pool) serves the plan and the analysis thread; the
+  // thread starts as soon as the CSR is there and then has the pool to itself
+  // (the rest of plan creation is serial host work and uploads).
+  // (Invalid input: plan_create_impl repeats the build and reports the error.)
+  MeshHost built;
+  const bool have_mesh = seq->faces && seq->n && seq->n_faces &&
+                         build_mesh(seq->faces, seq->n_faces, seq->n, &built).good();
+  tm.lap("mesh");
+  if (have_mesh) start_analysis(built);
   dmcg_plan* p = nullptr;
   Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
-                               nullptr, 0, &p);
+                               nullptr, 0, &p, have_mesh ? &built : nullptr);
   if (!st.good()) return ctx->set_error(st);
   // the early analysis keys on the plan's anchor set: drop it if they differ
   if (ctx->pending && !std::equal(ctx->pending->anchors.begin(), ctx->pending->anchors.end(),
                                   p->mesh.anchors.begin(), p->mesh.anchors.end()))
     ctx->pending.reset();
   tm.lap("plan");
-  if (st.good()) st = plan_encode(p, d_in);
-  tm.lap("h2d+kernels");
-  if (st.good()) {
-    if (!out->faces) out->faces = seq->faces;
-    st = download_impl(p, out);
-    out->faces = seq->faces;
-  }
-  tm.lap("download");
+  // The next dmcg_decode of this stream -- its plan, decode structures and M's
+  // numeric factor -- is prepared while the encode's kernels run: the host
+  // waits for the analysis thread, uploads on the low-priority stream aux2 and
+  // launches the factor there (it depends on mesh and anchors only, not on
+  // anything the encode computes).  See PendingDecode.
   drop_pending_decode(ctx);
   static const bool no_prep = std::getenv("DMCG_NO_OVERLAP") || std::getenv("DMCG_NO_PREFACTOR");
-  if (st.good() && !no_prep && ctx->pending && cfg->variant != DMCG_V2V && p->nb == 1) {
-    // the next dmcg_decode of this stream: its plan, decode structures and
-    // M's numeric factor (on aux2) prepared now, see PendingDecode
+  const std::function<void()> prepare_decode = [&] {
+    if (no_prep || !ctx->pending || cfg->variant == DMCG_V2V || p->nb != 1) return;
     std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
     if (pa->th.joinable()) pa->th.join();
+    PhaseTimer tp("prepare-decode");
+    // what decode_config() will read from the stream this encode writes
     dmcg_config dc;
-    std::vector<int> drb;
+    dmcg_config_default(&dc);
+    dc.variant = p->variant;
+    dc.k_l = p->k_l;
+    dc.n_b = 1;
+    std::vector<int> drb(p->row_bits.begin(), p->row_bits.begin() + p->k_l);
+    dc.row_bits = drb.data();
+    dc.n_row_bits = p->k_l;
+    dc.anchor_bits = p->anchor_bits;
+    dc.dict_bits = p->dict_bits;
+    dc.diff_bits = p->diff_bits ? p->diff_bits : 8;
     dmcg_plan* pdp = nullptr;
-    Status sp = pa->failed ? Status{DMCG_E_CONFIG, "analysis failed"} : decode_config(out, &dc, &drb);
+    const uint32_t no_anchor = 0;  // anchors "given" (empty) for the anchor-free variants
+    Status sp = pa->failed ? Status{DMCG_E_CONFIG, "analysis failed"} : Status::ok();
     if (sp.good())
       sp = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, &dc,
-                            out->anchor_idx, p->n_c, &pdp, &pa->mesh, false);
+                            p->n_c ? p->mesh.anchors.data() : &no_anchor, p->n_c, &pdp,
+                            &pa->mesh, false, ctx->aux2);
     if (sp.good()) {
       pdp->mesh.m_rp = std::move(pa->mesh.m_rp);
       pdp->mesh.m_ci = std::move(pa->mesh.m_ci);
@@ -1495,7 +1566,8 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
       pdp->analyze_seconds = pa->seconds;
       pdp->chol_given = true;
       sp = plan_prepare_decode(pdp);
-      if (sp.good()) sp = plan_prefactor_async(pdp);
+      pdp->up_stream = nullptr;  // the decode itself runs on the context stream
+      if (sp.good()) sp = plan_prefactor_async(pdp, false);
     }
     if (sp.good()) {
       auto pd = std::make_unique<PendingDecode>();
@@ -1505,21 +1577,46 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
       pd->n_faces = seq->n_faces;
       pd->faces_hash = pa->faces_hash;
       pd->dtype = seq->dtype;
-      pd->variant = (int)out->variant;
-      pd->k_l = out->k_l;
+      pd->variant = (int)p->variant;
+      pd->k_l = p->k_l;
       pd->n_b = 1;
-      pd->anchor_bits = (int)out->anchor_bits;
-      pd->dict_bits = (int)out->dict_bits;
+      pd->anchor_bits = (int)p->anchor_bits;
+      pd->dict_bits = (int)p->dict_bits;
       pd->diff_bits = dc.diff_bits;
       pd->row_bits = drb;
-      pd->anchors.assign(out->anchor_idx, out->anchor_idx + p->n_c);
+      pd->anchors = p->mesh.anchors;
       ctx->pending_dec = std::move(pd);
     } else if (pdp) {
       cudaStreamSynchronize(ctx->aux2);
       dmcg_plan_destroy(pdp);
     }
-    tm.lap("decode plan + factor");
+    tp.lap("plan + uploads + factor launch");
+  };
+  // between the launches and the wait: the stream's D2H copies queued behind
+  // the kernels (single-block streams; the blocks download reads pageable
+  // staging and stays after the wait), then the decode preparation
+  Status st_dl = Status::ok();
+  const bool early_dl = p->nb == 1;
+  const std::function<void()> between = [&] {
+    if (early_dl) {
+      if (!out->faces) out->faces = seq->faces;
+      st_dl = download_issue(p, out);
+      out->faces = seq->faces;
+    }
+    prepare_decode();
+  };
+  if (st.good()) st = plan_encode(p, d_in, &between);
+  tm.lap("h2d+kernels+download");
+  if (st.good() && early_dl) {
+    st = st_dl;
+    if (st.good()) download_finish(p, out);
+  } else if (st.good()) {
+    if (!out->faces) out->faces = seq->faces;
+    st = download_impl(p, out);
+    out->faces = seq->faces;
   }
+  tm.lap("download finish");
+  if (!st.good()) drop_pending_decode(ctx);
   if (st.good()) {
     const dmcg_stats& e = p->stats;
     ctx->last_stats.ms_encode = e.ms_encode;
@@ -1658,18 +1755,22 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
   const bool split = !no_split && st.good() && o.solver == 0 && !o.frame_count && p->nb == 1 &&
                      in->F >= 64 && p->variant != DMCG_V2V;
   if (split) {
-    const uint32_t Fh = in->F / 2;
-    dmcg_decode_options o1 = o, o2 = o;
-    o1.frame_begin = 0;
-    o1.frame_count = Fh;
-    o2.frame_begin = Fh;
-    o2.frame_count = in->F - Fh;
-    o2.reuse_factor = 1;
-    st = plan_decode(p, &o1, p->d_x_out);  // returns after its stream sync
-    if (st.good()) d2h(0, Fh, ctx->aux2);
-    if (st.good()) st = plan_decode(p, &o2, p->d_x_out);
-    tm.lap("kernels");
-    if (st.good()) d2h(Fh, in->F - Fh, ctx->stream);
+    static const int nwin_env = [] {
+      const char* e = std::getenv("DMCG_DECODE_WINDOWS");
+      return e ? std::max(2, std::min(8, std::atoi(e))) : 2;
+    }();
+    const uint32_t nwin = std::min<uint32_t>((uint32_t)nwin_env, in->F / 32);
+    for (uint32_t w = 0; w < nwin && st.good(); ++w) {
+      const uint32_t f0 = (uint32_t)((uint64_t)in->F * w / nwin);
+      const uint32_t f1 = (uint32_t)((uint64_t)in->F * (w + 1) / nwin);
+      dmcg_decode_options ow = o;
+      ow.frame_begin = f0;
+      ow.frame_count = f1 - f0;
+      if (w) ow.reuse_factor = 1;
+      st = plan_decode(p, &ow, p->d_x_out);  // returns after its stream sync
+      if (w + 1 == nwin) tm.lap("kernels");
+      if (st.good()) d2h(f0, f1 - f0, w + 1 == nwin ? ctx->stream : ctx->aux2);
+    }
     if (cudaStreamSynchronize(ctx->aux2) != cudaSuccess && st.good())
       st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
   } else {

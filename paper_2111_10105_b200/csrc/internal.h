@@ -81,7 +81,7 @@ void* plan_alloc(dmcg_plan* p, size_t bytes);
 Status plan_prepare_decode(dmcg_plan* p);
 // M's numeric factor on ctx->aux2 now (decode structures must exist); the
 // next decode of the plan takes it and waits for it before its solves.
-Status plan_prefactor_async(dmcg_plan* p);
+Status plan_prefactor_async(dmcg_plan* p, bool after_stream = true);
 Status plan_prepare_normal(dmcg_plan* p);
 }  // namespace dmcg
 
@@ -289,6 +289,8 @@ struct dmcg_plan {
   bool chol_given = false;
   bool factor_valid = false;        // cdev.F / Linv hold the numeric factor of M          // chol / mesh.m_* were filled by a PendingAnalysis
   bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
+  float h_anchor_rng[6] = {};        // download staging (anchor ranges)
+  cudaStream_t up_stream = nullptr;  // plan / decode-structure uploads (default: aux / ctx stream)
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
   dmcg::PlanGraph g_encode, g_decode;
 

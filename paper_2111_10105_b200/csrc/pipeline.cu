@@ -5,6 +5,7 @@
 #include <cstring>
 #include <string>
 
+#include <functional>
 #include "gemm.cuh"
 #include "internal.h"
 #include "ozaki.h"
@@ -382,10 +383,14 @@ static bool prefactor_on(const dmcg_plan* p) {
 
 // Fork: M's supernodal factor on the low-priority stream aux2 (it reads
 // only the plan's mesh structures; the encode never touches F / Linv / P).
-static Status fork_prefactor(dmcg_plan* p) {
+// after_stream = false: not ordered behind the plan stream (a fresh decode
+// plan whose uploads went through aux2 itself: dmcg_encode's preparation).
+static Status fork_prefactor(dmcg_plan* p, bool after_stream = true) {
   cudaStream_t s = p->ctx->stream, sf = p->ctx->aux2;
-  DMCG_TRY(cudaEventRecord(p->ev_pf_fork, s));
-  DMCG_TRY(cudaStreamWaitEvent(sf, p->ev_pf_fork, 0));
+  if (after_stream) {
+    DMCG_TRY(cudaEventRecord(p->ev_pf_fork, s));
+    DMCG_TRY(cudaStreamWaitEvent(sf, p->ev_pf_fork, 0));
+  }
   DMCG_TRY(cudaMemsetAsync(p->d_pf_flag, 0, sizeof(int), sf));
   DMCG_TRY(record_event(p->ev_pf0, sf));
   CholDev cd = p->cdev;
@@ -396,9 +401,9 @@ static Status fork_prefactor(dmcg_plan* p) {
   return Status::ok();
 }
 
-Status plan_prefactor_async(dmcg_plan* p) {
+Status plan_prefactor_async(dmcg_plan* p, bool after_stream) {
   if (!p->cdev.P || p->nb != 1 || p->shard) return Status{DMCG_E_UNSUPPORTED, "Unsupported: prefactor"};
-  Status st = fork_prefactor(p);
+  Status st = fork_prefactor(p, after_stream);
   if (!st.good()) return st;
   p->factor_pending = true;
   p->pf_unjoined = true;
@@ -531,7 +536,9 @@ static Status run_graph(dmcg_plan* p, PlanGraph& g, const void* const key[4], lo
 }
 
 // Host-side wrapper used by host.cpp.
-Status plan_encode(dmcg_plan* p, const void* const x[3]) {
+// between: host work to run after the launches are queued and before the
+// stream is waited for (dmcg_encode prepares the next decode there).
+Status plan_encode(dmcg_plan* p, const void* const x[3], const std::function<void()>* between) {
   cudaStream_t s = p->ctx->stream;
   const int k = (int)p->k, F = (int)p->F;
   const void* key[4] = {x[0], x[1], x[2], nullptr};
@@ -543,6 +550,7 @@ Status plan_encode(dmcg_plan* p, const void* const x[3]) {
   p->oi_timed = p->nb == 1 && p->rounds > 0 && k < F && k > 0;
   int flags[8];
   DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  if (between && *between) (*between)();
   DMCG_TRY(cudaStreamSynchronize(s));
   float ms;
   cudaEventElapsedTime(&ms, p->ev[0], p->ev[5]);
