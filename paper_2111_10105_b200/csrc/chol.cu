@@ -681,36 +681,43 @@ struct StoreBwd {
   }
 };
 
+// Tile shape of the solve GEMMs: 64 x 64 for the levels of wide fronts,
+// 32 x 128 (four warps side by side, 32-row granularity) for the levels of
+// narrow ones, where most M tiles of a 64-row grid would be half padding
+// (c3: 4106 leaf fronts of mean width 33).
 // Forward: [y_s; U_s] = P_s r_s (+ pulls), M = m, K = w.
+template <int BM, int BN>
 __global__ void __launch_bounds__(kGemmThreads, 4) k_fwd(CholDev d, const uint32_t* lsup,
                                                       const double* r, double* y) {
   const uint32_t s = lsup[blockIdx.z];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
-  if ((int)blockIdx.x * kBM >= m) return;
+  if ((int)blockIdx.x * BM >= m) return;
   const size_t f0 = d.first[s];
   const unsigned long long g0 = d.rhs_off[s];
   // rows i < w of P are L11^{-1} (lower triangular): a tile inside the top
   // block needs k <= i only
-  const int m0 = blockIdx.x * kBM;
-  const int kend = m0 + kBM <= w ? m0 + kBM : w;
-  gemm_tile(0, m, W, m0, blockIdx.y * kBN, 0, kend, 0,
-            LoadColMajor{d.P + d.op_off[s], m}, LoadColMajor{r + f0 * W, W},
-            StoreFwd{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W});
+  const int m0 = blockIdx.x * BM;
+  const int kend = m0 + BM <= w ? m0 + BM : w;
+  gemm_tile_async<BM, BN>(0, m, W, m0, blockIdx.y * BN, 0, kend, 0,
+                          LoadColMajor{d.P + d.op_off[s], m}, LoadColMajor{r + f0 * W, W},
+                          StoreFwd{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W});
 }
 
 // Backward: x_s = P_s^T [y_s; x_below], M = w, K = m.
+template <int BM, int BN>
 __global__ void __launch_bounds__(kGemmThreads, 4) k_bwd(CholDev d, const uint32_t* lsup,
                                                       const double* y, double* x, double* out,
                                                       int accumulate) {
   const uint32_t s = lsup[blockIdx.z];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
-  if ((int)blockIdx.x * kBM >= w) return;
+  if ((int)blockIdx.x * BM >= w) return;
   const uint32_t* rows = d.str_idx + d.str_ptr[s];
   // P^T's top block is L11^{-T} (upper triangular): row i needs k >= i
-  const int m0 = blockIdx.x * kBM;
-  gemm_tile(0, w, W, m0, blockIdx.y * kBN, m0, m, 0,
-            LoadRowMajor{d.P + d.op_off[s], m}, LoadYX{y, x, rows, w, W},
-            StoreBwd{x + (size_t)d.first[s] * W, out, d.perm + d.first[s], W, accumulate});
+  const int m0 = blockIdx.x * BM;
+  gemm_tile_async<BM, BN>(0, w, W, m0, blockIdx.y * BN, m0, m, 0,
+                          LoadRowMajor{d.P + d.op_off[s], m}, LoadYX{y, x, rows, w, W},
+                          StoreBwd{x + (size_t)d.first[s] * W, out, d.perm + d.first[s], W,
+                                   accumulate});
 }
 
 // r = b - M x   (M: CSR with float values, original order, n x W row-major).
@@ -932,6 +939,12 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
   };
   const int W = (int)d.W;
   const unsigned tn = (unsigned)((W + kBN - 1) / kBN);
+  // levels whose widest front has <= narrow_w own columns take the 32 x 128 tiles
+  static const uint32_t narrow_w = [] {
+    const char* e = std::getenv("DMCG_SOLVE_NARROW_W");
+    return e ? (uint32_t)std::atoi(e) : 200u;
+  }();
+  auto narrow = [&](uint32_t l) { return lv.maxw[l] <= narrow_w; };
   LevelTimer lt(s, "solve", lv.nlevels);
   // forward, leaves first: r_s -> x rows (scratch until the backward pass
   // overwrites them), [y_s; U_s] = P_s r_s
@@ -942,7 +955,12 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     k_gather_own<<<dim3((lv.maxw[l] + 7) / 8, (W + 127) / 128, cnt), 256, 0, s>>>(d, ls, b, x);
     lt.mark(l, 1);
     tmark(l, 0);
-    k_fwd<<<dim3((lv.maxm[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x, y);
+    if (narrow(l))
+      k_fwd<32, 128><<<dim3((lv.maxm[l] + 31) / 32, (W + 127) / 128, cnt), kGemmThreads, 0, s>>>(
+          d, ls, x, y);
+    else
+      k_fwd<kBM, kBN><<<dim3((lv.maxm[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x,
+                                                                                          y);
     tmark(l, 1);
     lt.mark(l, 2);
   }
@@ -952,8 +970,12 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 3);
     tmark(l, 2);
-    k_bwd<<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, y, x, out,
-                                                                               accumulate ? 1 : 0);
+    if (narrow(l))
+      k_bwd<32, 128><<<dim3((lv.maxw[l] + 31) / 32, (W + 127) / 128, cnt), kGemmThreads, 0, s>>>(
+          d, ls, y, x, out, accumulate ? 1 : 0);
+    else
+      k_bwd<kBM, kBN><<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(
+          d, ls, y, x, out, accumulate ? 1 : 0);
     tmark(l, 3);
     lt.mark(l, 4);
   }

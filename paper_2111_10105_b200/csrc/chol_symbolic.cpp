@@ -70,6 +70,11 @@ class NestedDissection {
   static constexpr uint32_t kParMin = 4096;  // smallest half worth a thread
   const Graph g_;
   const bool wide_;
+  // ranges of <= leaf_ vertices are not dissected further (one leaf front each)
+  const uint32_t leaf_ = [] {
+    const char* e = std::getenv("DMCG_ND_LEAF");
+    return e ? (uint32_t)std::max(49, std::atoi(e)) : 48u;
+  }();
   std::vector<int32_t> part_;
   std::vector<uint32_t> queue_, idx_;
   std::vector<uint32_t> lstart_;  // level starts of the last BFS of a range, at [2 b + level]
@@ -90,7 +95,7 @@ class NestedDissection {
     while (!st.empty()) {
       const Task t = st.back();
       st.pop_back();
-      if (t.e - t.b <= 48) continue;
+      if (t.e - t.b <= leaf_) continue;
       uint32_t na, ns;
       int32_t ia, ib;
       if (split(t.b, t.e, t.id, &na, &ns, &ia, &ib) == 0) continue;  // no useful split

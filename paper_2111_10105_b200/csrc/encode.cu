@@ -142,17 +142,32 @@ __global__ void __launch_bounds__(kDeltaWarps * 32)
           if (v < nv) nxt[c] = reinterpret_cast<const V*>(X + (size_t)jn * F)[v];
         }
       }
-      const double w = (j == (uint32_t)i) ? deg : -1.0;
+      // warp-uniform split: off the diagonal acc + (-1 * x) is acc - x (the
+      // product is exact), one DADD per element; the diagonal entry carries the
+      // degree product and validate_sequence's finiteness check
+      if (j != (uint32_t)i) {
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const int v = v0 + c * 32 + lane;
-        if (v < nv) {
-          double xv[VEC];
-          VT::get(cur[c], xv);
+        for (int c = 0; c < CH; ++c) {
+          const int v = v0 + c * 32 + lane;
+          if (v < nv) {
+            double xv[VEC];
+            VT::get(cur[c], xv);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            if (j == (uint32_t)i && !isfinite(xv[e])) bad = true;
-            acc[c * VEC + e] = __dadd_rn(acc[c * VEC + e], __dmul_rn(w, xv[e]));
+            for (int e = 0; e < VEC; ++e) acc[c * VEC + e] = __dsub_rn(acc[c * VEC + e], xv[e]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int v = v0 + c * 32 + lane;
+          if (v < nv) {
+            double xv[VEC];
+            VT::get(cur[c], xv);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              if (!isfinite(xv[e])) bad = true;
+              acc[c * VEC + e] = __dadd_rn(acc[c * VEC + e], __dmul_rn(deg, xv[e]));
+            }
           }
         }
       }

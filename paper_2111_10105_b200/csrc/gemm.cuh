@@ -56,10 +56,11 @@ struct RawLoader : std::false_type {};
 template <class T>
 struct RawLoader<T, std::void_t<decltype(&T::addr)>> : std::true_type {};
 
+// One raw ring, carved per tile shape: 64 x 64 (two warps by two) or 32 x 128
+// (four warps side by side: the solves' small fronts, chol.cu).
 constexpr int kAStages = 4, kABK = 8;
 struct GemmSmemAsync {
-  double As[kAStages][kABK][kBM + 4];
-  double Bs[kAStages][kABK][kBN + 4];
+  double raw[kAStages * kABK * ((32 + 4) + (128 + 4))];
 };
 __device__ __forceinline__ GemmSmemAsync& gemm_smem_async() {
   __shared__ GemmSmemAsync sm;
@@ -85,53 +86,95 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <class LA, class LB, class EP>
+// The DMMAs of one k-slice of KS rows for the first MI 8-row blocks of a
+// warp's 32x32 sub-tile (MI < 4 on ragged tiles: the padding's DMMAs are
+// skipped, which frees the tensor pipe for the other CTAs of the SM).
+template <int MI, int KS, typename TA, typename TB, int LDA, int LDB>
+__device__ __forceinline__ void warp_mma_slice(WarpTile& wt, const TA (*As)[LDA],
+                                               const TB (*Bs)[LDB], int wm, int wn, int lane) {
+#pragma unroll
+  for (int kk = 0; kk < KS / 4; ++kk) {
+    const int kr = kk * 4 + (lane & 3);
+    double a[MI > 0 ? MI : 1], bb[4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) a[i] = (double)As[kr][wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bb[j] = (double)Bs[kr][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(wt.acc[i][j], a[i], bb[j]);
+  }
+}
+template <int KS, typename TA, typename TB, int LDA, int LDB>
+__device__ __forceinline__ void warp_mma_slice_n(int mi_cnt, WarpTile& wt, const TA (*As)[LDA],
+                                                 const TB (*Bs)[LDB], int wm, int wn, int lane) {
+  switch (mi_cnt) {  // warp-uniform
+    case 4: warp_mma_slice<4, KS>(wt, As, Bs, wm, wn, lane); break;
+    case 3: warp_mma_slice<3, KS>(wt, As, Bs, wm, wn, lane); break;
+    case 2: warp_mma_slice<2, KS>(wt, As, Bs, wm, wn, lane); break;
+    case 1: warp_mma_slice<1, KS>(wt, As, Bs, wm, wn, lane); break;
+    default: break;
+  }
+}
+
+template <int BM = kBM, int BN = kBN, class LA, class LB, class EP>
 __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int n0, int kbeg,
                                                 int kend, int split, const LA& la, const LB& lb,
                                                 const EP& ep) {
+  static_assert(BM % 32 == 0 && BN % 32 == 0 && (BM / 32) * (BN / 32) == kGemmThreads / 32,
+                "one 32x32 sub-tile per warp");
+  static_assert(BM + BN <= 32 + 128, "ring size");
   // operand element types (double, or float upcast when fragments load):
   // the ring is declared for doubles and reinterpreted for narrower types
   using TA = std::remove_cv_t<std::remove_pointer_t<decltype(la.addr(0, 0, 0))>>;
   using TB = std::remove_cv_t<std::remove_pointer_t<decltype(lb.addr(0, 0, 0))>>;
   GemmSmemAsync& smd = gemm_smem_async();
   struct Ring {
-    TA (*As)[kABK][kBM + 4];
-    TB (*Bs)[kABK][kBN + 4];
-  } sm{reinterpret_cast<TA(*)[kABK][kBM + 4]>(smd.As),
-       reinterpret_cast<TB(*)[kABK][kBN + 4]>(smd.Bs)};
+    TA (*As)[kABK][BM + 4];
+    TB (*Bs)[kABK][BN + 4];
+  } sm{reinterpret_cast<TA(*)[kABK][BM + 4]>(smd.raw),
+       reinterpret_cast<TB(*)[kABK][BN + 4]>(smd.raw + kAStages * kABK * (BM + 4))};
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int wm = w >> 1, wn = w & 1;
+  constexpr int WN = BN / 32;
+  const int wm = w / WN, wn = w % WN;
   WarpTile wt;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) wt.acc[i][j][0] = wt.acc[i][j][1] = 0.0;
   const int nk = kend > kbeg ? (kend - kbeg + kABK - 1) / kABK : 0;
+  // 8-row blocks of this warp's 32x32 sub-tile that hold valid output
+  const int mi_cnt = min(4, max(0, (M - (m0 + wm * 32) + 7) >> 3));
   if (nk > 0) {
     const TA* adummy = la.addr(b, kbeg, m0);
     const TB* bdummy = lb.addr(b, kbeg, n0);
     auto issue = [&](int it) {
       const int buf = it % kAStages, kt = kbeg + it * kABK;
 #pragma unroll
-      for (int q = 0; q < (kABK * kBM) / kGemmThreads; ++q) {
+      for (int q = 0; q < (kABK * BM) / kGemmThreads; ++q) {
         const int e = t + q * kGemmThreads;
         int k, m;
         if (LA::kKContig) {
           k = e % kABK;
           m = e / kABK;
         } else {
-          m = e % kBM;
-          k = e / kBM;
+          m = e % BM;
+          k = e / BM;
         }
         const bool ok = kt + k < kend && m0 + m < M;
         cp_async_el(&sm.As[buf][k][m], ok ? la.addr(b, kt + k, m0 + m) : adummy, ok);
+      }
+#pragma unroll
+      for (int q = 0; q < (kABK * BN) / kGemmThreads; ++q) {
+        const int e = t + q * kGemmThreads;
         int kb, nb;
         if (LB::kKContig) {
           kb = e % kABK;
           nb = e / kABK;
         } else {
-          nb = e % kBN;
-          kb = e / kBN;
+          nb = e % BN;
+          kb = e / BN;
         }
         const bool okb = kt + kb < kend && n0 + nb < N;
         cp_async_el(&sm.Bs[buf][kb][nb], okb ? lb.addr(b, kt + kb, n0 + nb) : bdummy, okb);
@@ -148,19 +191,7 @@ __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int
       if (it + kAStages - 1 < nk) issue(it + kAStages - 1);
       cp_async_commit();
       const int buf = it % kAStages;
-#pragma unroll
-      for (int kk = 0; kk < kABK / 4; ++kk) {
-        const int kr = kk * 4 + (lane & 3);
-        double a[4], bb[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = (double)sm.As[buf][kr][wm * 32 + i * 8 + (lane >> 2)];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bb[j] = (double)sm.Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(wt.acc[i][j], a[i], bb[j]);
-      }
+      warp_mma_slice_n<kABK>(mi_cnt, wt, sm.As[buf], sm.Bs[buf], wm, wn, lane);
     }
     cp_async_wait<0>();
     __syncthreads();  // the ring may be refilled by a following tile
@@ -187,6 +218,7 @@ __device__ __forceinline__ void gemm_tile(int b, int M, int N, int m0, int n0, i
 #pragma unroll
     for (int j = 0; j < 4; ++j) wt.acc[i][j][0] = wt.acc[i][j][1] = 0.0;
 
+  const int mi_cnt = min(4, max(0, (M - (m0 + wm * 32) + 7) >> 3));  // see gemm_tile_async
   double ra[8], rb[8];
   auto load_tile = [&](int kt) {
 #pragma unroll
@@ -238,19 +270,7 @@ __device__ __forceinline__ void gemm_tile(int b, int M, int N, int m0, int n0, i
   for (int kt = kbeg; kt < kend; kt += kBK) {
     const bool more = kt + kBK < kend;
     if (more) load_tile(kt + kBK);
-#pragma unroll
-    for (int kk = 0; kk < kBK / 4; ++kk) {
-      const int kr = kk * 4 + (lane & 3);
-      double a[4], bb[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[buf][kr][wm * 32 + i * 8 + (lane >> 2)];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kr][wn * 32 + j * 8 + (lane >> 2)];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(wt.acc[i][j], a[i], bb[j]);
-    }
+    warp_mma_slice_n<kBK>(mi_cnt, wt, As[buf], Bs[buf], wm, wn, lane);
     if (more) store_tile(buf ^ 1);
     __syncthreads();
     buf ^= 1;
