@@ -518,6 +518,18 @@ struct LoadRowMajor {  // X(k, i) = p[i * ld + k]   (k contiguous)
     return p + (size_t)i * ld + k;
   }
 };
+// b(perm[k], c): the own rows of a leaf front straight from the caller's
+// right-hand side (leaves have no children to pull from, so r_s = b(own rows)
+// and the gather pass is skipped for them)
+struct LoadPermRows {
+  static constexpr bool kKContig = false;
+  const double* b;
+  const uint32_t* perm;  // perm + first[s]
+  int W;
+  __device__ __forceinline__ const double* addr(int, int k, int c) const {
+    return b + (size_t)perm[k] * W + c;
+  }
+};
 // [y_s; x_below](k, c): own rows from y, the rows below from x (str_idx lists
 // the own columns first, so rows[k] = first[s] + k for k < w)
 struct LoadYX {
@@ -632,7 +644,7 @@ struct StoreFwd {
 // (= or += : the refinement accumulates its correction), replacing a
 // separate unpermute pass over n x W.
 struct StoreBwd {
-  double* x;            // x + first[s] * W
+  double* x;            // x + first[s] * W; null: leaf fronts (no descendant reads them)
   double* out;          // original-order output (n x W)
   const uint32_t* perm;  // perm + first[s]
   int W, accumulate;
@@ -666,13 +678,13 @@ struct StoreBwd {
         const int ni = nb + j * 8 + (lane & 3) * 2;
         const double v0 = wt.acc[i][j][0], v1 = wt.acc[i][j][1];
         if (ni + 1 < N && vec) {
-          *reinterpret_cast<double2*>(xr + ni) = make_double2(v0, v1);
+          if (x) *reinterpret_cast<double2*>(xr + ni) = make_double2(v0, v1);
           *reinterpret_cast<double2*>(orow + ni) = make_double2(prev[j][0] + v0, prev[j][1] + v1);
         } else if (ni < N) {
-          xr[ni] = v0;
+          if (x) xr[ni] = v0;
           orow[ni] = prev[j][0] + v0;
           if (ni + 1 < N) {
-            xr[ni + 1] = v1;
+            if (x) xr[ni + 1] = v1;
             orow[ni + 1] = prev[j][1] + v1;
           }
         }
@@ -686,7 +698,7 @@ struct StoreBwd {
 // narrow ones, where most M tiles of a 64-row grid would be half padding
 // (c3: 4106 leaf fronts of mean width 33).
 // Forward: [y_s; U_s] = P_s r_s (+ pulls), M = m, K = w.
-template <int BM, int BN>
+template <int BM, int BN, bool LEAF>
 __global__ void __launch_bounds__(kGemmThreads, 4) k_fwd(CholDev d, const uint32_t* lsup,
                                                       const double* r, double* y) {
   const uint32_t s = lsup[blockIdx.z];
@@ -698,16 +710,21 @@ __global__ void __launch_bounds__(kGemmThreads, 4) k_fwd(CholDev d, const uint32
   // block needs k <= i only
   const int m0 = blockIdx.x * BM;
   const int kend = m0 + BM <= w ? m0 + BM : w;
-  gemm_tile_async<BM, BN>(0, m, W, m0, blockIdx.y * BN, 0, kend, 0,
-                          LoadColMajor{d.P + d.op_off[s], m}, LoadColMajor{r + f0 * W, W},
-                          StoreFwd{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W});
+  const StoreFwd ep{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W};
+  if constexpr (LEAF)  // r = the caller's b in the original order
+    gemm_tile_async<BM, BN>(0, m, W, m0, blockIdx.y * BN, 0, kend, 0,
+                            LoadColMajor{d.P + d.op_off[s], m}, LoadPermRows{r, d.perm + f0, W},
+                            ep);
+  else
+    gemm_tile_async<BM, BN>(0, m, W, m0, blockIdx.y * BN, 0, kend, 0,
+                            LoadColMajor{d.P + d.op_off[s], m}, LoadColMajor{r + f0 * W, W}, ep);
 }
 
 // Backward: x_s = P_s^T [y_s; x_below], M = w, K = m.
 template <int BM, int BN>
 __global__ void __launch_bounds__(kGemmThreads, 4) k_bwd(CholDev d, const uint32_t* lsup,
                                                       const double* y, double* x, double* out,
-                                                      int accumulate) {
+                                                      int accumulate, int leaf) {
   const uint32_t s = lsup[blockIdx.z];
   const int w = (int)front_w(d, s), m = (int)front_m(d, s), W = (int)d.W;
   if ((int)blockIdx.x * BM >= w) return;
@@ -716,8 +733,8 @@ __global__ void __launch_bounds__(kGemmThreads, 4) k_bwd(CholDev d, const uint32
   const int m0 = blockIdx.x * BM;
   gemm_tile_async<BM, BN>(0, w, W, m0, blockIdx.y * BN, m0, m, 0,
                           LoadRowMajor{d.P + d.op_off[s], m}, LoadYX{y, x, rows, w, W},
-                          StoreBwd{x + (size_t)d.first[s] * W, out, d.perm + d.first[s], W,
-                                   accumulate});
+                          StoreBwd{leaf ? nullptr : x + (size_t)d.first[s] * W, out, d.perm + d.first[s],
+                                   W, accumulate});
 }
 
 // r = b - M x   (M: CSR with float values, original order, n x W row-major).
@@ -952,15 +969,21 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     const uint32_t cnt = lv.count[l];
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 0);
-    k_gather_own<<<dim3((lv.maxw[l] + 7) / 8, (W + 127) / 128, cnt), 256, 0, s>>>(d, ls, b, x);
+    // level 0 = the leaves: no pulls, k_fwd reads b through perm itself
+    if (l > 0)
+      k_gather_own<<<dim3((lv.maxw[l] + 7) / 8, (W + 127) / 128, cnt), 256, 0, s>>>(d, ls, b, x);
     lt.mark(l, 1);
     tmark(l, 0);
-    if (narrow(l))
-      k_fwd<32, 128><<<dim3((lv.maxm[l] + 31) / 32, (W + 127) / 128, cnt), kGemmThreads, 0, s>>>(
-          d, ls, x, y);
+    const dim3 gn((lv.maxm[l] + 31) / 32, (W + 127) / 128, cnt);
+    const dim3 gw((lv.maxm[l] + kBM - 1) / kBM, tn, cnt);
+    if (l == 0 && narrow(l))
+      k_fwd<32, 128, true><<<gn, kGemmThreads, 0, s>>>(d, ls, b, y);
+    else if (l == 0)
+      k_fwd<kBM, kBN, true><<<gw, kGemmThreads, 0, s>>>(d, ls, b, y);
+    else if (narrow(l))
+      k_fwd<32, 128, false><<<gn, kGemmThreads, 0, s>>>(d, ls, x, y);
     else
-      k_fwd<kBM, kBN><<<dim3((lv.maxm[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(d, ls, x,
-                                                                                          y);
+      k_fwd<kBM, kBN, false><<<gw, kGemmThreads, 0, s>>>(d, ls, x, y);
     tmark(l, 1);
     lt.mark(l, 2);
   }
@@ -970,12 +993,13 @@ cudaError_t chol_solve_device(cudaStream_t s, const CholDev& d, const CholLevels
     const uint32_t* ls = d.level_sup + lv.offset[l];
     lt.mark(l, 3);
     tmark(l, 2);
+    // (the leaves' x rows are read by no descendant: not written, see k_bwd)
     if (narrow(l))
       k_bwd<32, 128><<<dim3((lv.maxw[l] + 31) / 32, (W + 127) / 128, cnt), kGemmThreads, 0, s>>>(
-          d, ls, y, x, out, accumulate ? 1 : 0);
+          d, ls, y, x, out, accumulate ? 1 : 0, l == 0 ? 1 : 0);
     else
       k_bwd<kBM, kBN><<<dim3((lv.maxw[l] + kBM - 1) / kBM, tn, cnt), kGemmThreads, 0, s>>>(
-          d, ls, y, x, out, accumulate ? 1 : 0);
+          d, ls, y, x, out, accumulate ? 1 : 0, l == 0 ? 1 : 0);
     tmark(l, 3);
     lt.mark(l, 4);
   }

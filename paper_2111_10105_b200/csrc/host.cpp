@@ -1760,9 +1760,25 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
       return e ? std::max(2, std::min(8, std::atoi(e))) : 2;
     }();
     const uint32_t nwin = std::min<uint32_t>((uint32_t)nwin_env, in->F / 32);
+    // two windows: the first one larger (in 64-frame steps), so that its D2H
+    // (which hides under the second window's kernels) carries more of the
+    // output and the exposed tail copy less
+    static const int first_pct = [] {
+      const char* e = std::getenv("DMCG_DECODE_FIRST_PCT");
+      return e ? std::max(10, std::min(90, std::atoi(e))) : 75;
+    }();
+    auto bound = [&](uint32_t w) -> uint32_t {
+      if (w == 0) return 0;
+      if (w >= nwin) return in->F;
+      if (nwin == 2 && in->F >= 256) {
+        const uint32_t b = (uint32_t)((uint64_t)in->F * first_pct / 100 + 32) / 64 * 64;
+        return std::max<uint32_t>(64, std::min<uint32_t>(b, in->F - 64));
+      }
+      return (uint32_t)((uint64_t)in->F * w / nwin);
+    };
     for (uint32_t w = 0; w < nwin && st.good(); ++w) {
-      const uint32_t f0 = (uint32_t)((uint64_t)in->F * w / nwin);
-      const uint32_t f1 = (uint32_t)((uint64_t)in->F * (w + 1) / nwin);
+      const uint32_t f0 = bound(w);
+      const uint32_t f1 = bound(w + 1);
       dmcg_decode_options ow = o;
       ow.frame_begin = f0;
       ow.frame_count = f1 - f0;
