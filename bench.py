@@ -69,6 +69,8 @@ def traffic_of(cfgname, kernel_prefix):
         data = json.load(open(TRAFFIC_PATH))[cfgname]
     except Exception:
         return None
+    if kernel_prefix in data:  # base name over all template instantiations
+        return int(data[kernel_prefix])
     for name, b in data.items():
         if name.replace("void ", "").startswith(kernel_prefix):
             return int(b)

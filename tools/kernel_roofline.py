@@ -59,4 +59,13 @@ if "--traffic-json" in sys.argv:
     path, cfg = sys.argv[i + 1], sys.argv[i + 2]
     data = json.load(open(path)) if os.path.exists(path) else {}
     data[cfg] = {name: a["bytes"] / a["n"] for name, a in agg.items()}
+    # template kernels: also one entry per base name over all instantiations
+    base = collections.defaultdict(lambda: [0.0, 0.0])
+    for name, a in agg.items():
+        b = name.replace("void ", "").split("<")[0]
+        base[b][0] += a["bytes"]
+        base[b][1] += a["n"]
+    for b, (by, cnt) in base.items():
+        if b and b not in data[cfg]:
+            data[cfg][b] = by / cnt
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
