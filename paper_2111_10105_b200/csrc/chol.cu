@@ -549,6 +549,7 @@ struct LoadYX {
 // Forward epilogue: rows < w -> y (own rows), rows >= w -> the update rows
 // U = pulled child updates + (-L21 L11^{-1} r) in d.R.  All loads of a
 // fragment are issued before its stores.
+template <bool ROWS>
 struct StoreFwd {
   double* y;        // y + first[s] * W
   double* U;        // d.R + rhs_off[s] * W
@@ -556,6 +557,93 @@ struct StoreFwd {
   const uint32_t* pull_ptr;  // + rhs_off[s]
   const uint32_t* pull_src;
   int w, W;
+  // Row-wise finish over the tile staged in shared memory (gemm.cuh
+  // RowEpilogue): warp q of 4 takes the rows q, q + 4, ...; its lanes own CPL
+  // consecutive columns each, so y / U rows are written and the children's
+  // update rows read in contiguous BN-double pieces.  The pull lists of all
+  // of a warp's rows are fetched up front by its lanes (lane l: the l-th row's
+  // range and first two sources), so the pull_ptr -> pull_src -> row chain is
+  // paid once per warp instead of once per thread and row block.
+  static constexpr bool kRowEpilogue = ROWS;  // leaves (no pulls) keep the fragment stores
+  template <int BM, int BN>
+  __device__ __forceinline__ void rows(int m0, int n0, int M, int N, const double* tile,
+                                       int ld) const {
+    constexpr int CPL = BN / 32;   // columns per lane (2 or 4)
+    constexpr int RPW = BM / 4;    // rows per warp (8 or 16)
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int c = lane * CPL, nc = n0 + c;
+    const bool vec = !(W & 1);  // rows 16-byte aligned (nc is even)
+    // lane l < RPW: the pull range of the warp's l-th row
+    uint32_t pe0 = 0, pe1 = 0, ps0 = 0, ps1 = 0;
+    {
+      const int mi = m0 + wp + 4 * lane;
+      if (lane < RPW && mi < M && mi >= w) {
+        pe0 = pull_ptr[mi];
+        pe1 = pull_ptr[mi + 1];
+        if (pe0 < pe1) ps0 = pull_src[pe0];
+        if (pe0 + 1 < pe1) ps1 = pull_src[pe0 + 1];
+      }
+    }
+    auto load_row = [&](const double* src, double (&v)[CPL]) {
+      if (vec && nc + CPL <= N) {
+#pragma unroll
+        for (int q = 0; q < CPL; q += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(src + nc + q);
+          v[q] = t2.x;
+          v[q + 1] = t2.y;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) v[q] = nc + q < N ? src[nc + q] : 0.0;
+      }
+    };
+    auto store_row = [&](double* dst, const double (&v)[CPL]) {
+      if (vec && nc + CPL <= N) {
+#pragma unroll
+        for (int q = 0; q < CPL; q += 2)
+          *reinterpret_cast<double2*>(dst + nc + q) = make_double2(v[q], v[q + 1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          if (nc + q < N) dst[nc + q] = v[q];
+      }
+    };
+#pragma unroll 2
+    for (int rq = 0; rq < RPW; ++rq) {
+      const int r = wp + 4 * rq, mi = m0 + r;
+      const uint32_t e0 = __shfl_sync(0xffffffffu, pe0, rq), e1 = __shfl_sync(0xffffffffu, pe1, rq);
+      const uint32_t s0 = __shfl_sync(0xffffffffu, ps0, rq), s1 = __shfl_sync(0xffffffffu, ps1, rq);
+      if (mi >= M) continue;  // warp-uniform
+      double acc[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) acc[q] = tile[r * ld + c + q];
+      if (mi < w) {
+        store_row(y + (size_t)mi * W, acc);
+        continue;
+      }
+      double v[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) v[q] = 0.0;
+      // children in order: ((v + c_e) + c_{e+1}) ..., two rows in flight
+      uint32_t e = e0;
+      for (; e + 1 < e1; e += 2) {
+        double t0[CPL], t1[CPL];
+        load_row(R + (size_t)(e == e0 ? s0 : pull_src[e]) * W, t0);
+        load_row(R + (size_t)(e == e0 ? s1 : pull_src[e + 1]) * W, t1);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) v[q] = (v[q] + t0[q]) + t1[q];
+      }
+      if (e < e1) {
+        double t0[CPL];
+        load_row(R + (size_t)(e == e0 ? s0 : pull_src[e]) * W, t0);
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) v[q] += t0[q];
+      }
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) v[q] += acc[q];
+      store_row(U + (size_t)mi * W, v);
+    }
+  }
   __device__ __forceinline__ void operator()(int, int, int mb, int nb, int lane, int M, int N,
                                              const WarpTile& wt) const {
 #pragma unroll
@@ -710,7 +798,7 @@ __global__ void __launch_bounds__(kGemmThreads, 4) k_fwd(CholDev d, const uint32
   // block needs k <= i only
   const int m0 = blockIdx.x * BM;
   const int kend = m0 + BM <= w ? m0 + BM : w;
-  const StoreFwd ep{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W};
+  const StoreFwd<!LEAF> ep{y + f0 * W, d.R + g0 * W, d.R, d.pull_ptr + g0, d.pull_src, w, W};
   if constexpr (LEAF)  // r = the caller's b in the original order
     gemm_tile_async<BM, BN>(0, m, W, m0, blockIdx.y * BN, 0, kend, 0,
                             LoadColMajor{d.P + d.op_off[s], m}, LoadPermRows{r, d.perm + f0, W},

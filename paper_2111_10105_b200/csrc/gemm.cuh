@@ -118,6 +118,18 @@ __device__ __forceinline__ void warp_mma_slice_n(int mi_cnt, WarpTile& wt, const
   }
 }
 
+// Epilogues with `static constexpr bool kRowEpilogue = true` get the CTA's
+// whole output tile staged in shared memory (the operand ring, free by then;
+// row stride BN + 8 doubles: the fragment stores of a quarter-warp hit 32
+// distinct banks) and finish it by rows:
+//   ep.template rows<BM, BN>(m0, n0, M, N, tile, BN + 8)
+// called by all 128 threads, so every output / gathered row is touched in
+// contiguous pieces of BN doubles and per-row index lookups are warp-wide.
+template <class EP, class = void>
+struct RowEpilogue : std::false_type {};
+template <class EP>
+struct RowEpilogue<EP, std::enable_if_t<EP::kRowEpilogue>> : std::true_type {};
+
 template <int BM = kBM, int BN = kBN, class LA, class LB, class EP>
 __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int n0, int kbeg,
                                                 int kend, int split, const LA& la, const LB& lb,
@@ -196,7 +208,22 @@ __device__ __forceinline__ void gemm_tile_async(int b, int M, int N, int m0, int
     cp_async_wait<0>();
     __syncthreads();  // the ring may be refilled by a following tile
   }
-  ep(b, split, m0 + wm * 32, n0 + wn * 32, lane, M, N, wt);
+  if constexpr (RowEpilogue<EP>::value) {
+    constexpr int LD = BN + 8;
+    static_assert(BM * LD <= (int)(sizeof(GemmSmemAsync) / sizeof(double)), "tile fits the ring");
+    double* tile = smd.raw;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<double2*>(tile + (wm * 32 + i * 8 + (lane >> 2)) * LD + wn * 32 + j * 8 +
+                                    (lane & 3) * 2) = make_double2(wt.acc[i][j][0], wt.acc[i][j][1]);
+    __syncthreads();
+    ep.template rows<BM, BN>(m0, n0, M, N, tile, LD);
+    __syncthreads();  // the ring may be refilled by a following tile
+  } else {
+    ep(b, split, m0 + wm * 32, n0 + wn * 32, lane, M, N, wt);
+  }
 }
 
 template <class LA, class LB, class EP>
