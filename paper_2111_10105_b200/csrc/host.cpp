@@ -1861,7 +1861,13 @@ extern "C" int dmcg_debug_chol(uint32_t n, const uint32_t* faces, uint32_t n_fac
   tm.lap("normal");
   CholPlan p;
   const auto t0 = std::chrono::steady_clock::now();
-  chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p, &m.lap_rp, &m.lap_ci);
+  if (std::getenv("DMCG_DEBUG_PREORDER")) {  // the drop-in's split: ordering ahead of M
+    CholOrdering ord;
+    chol_order_graph(n, m.lap_rp, m.lap_ci, &ord);
+    chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p, &m.lap_rp, &m.lap_ci, &ord);
+  } else {
+    chol_analyze(n, m.m_rp, m.m_ci, m.m_val, &p, &m.lap_rp, &m.lap_ci);
+  }
   const double secs =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (stats) {

@@ -80,3 +80,27 @@ def test_analysis_is_deterministic():
     x1, st1 = _debug_chol(s.faces, s.n, anchors, b)
     x2, st2 = _debug_chol(s.faces, s.n, anchors, b)
     assert np.array_equal(x1, x2) and np.array_equal(st1[:7], st2[:7])
+
+
+def test_preordered_analysis_matches(monkeypatch):
+    """The drop-in computes the nested-dissection ordering beside the normal-matrix
+    build (chol_order_graph, then chol_analyze with it): same plan, same solution bits
+    as the analysis that orders by itself."""
+    s = synth.grid(90, 80, 4)
+    anchors = O.select_anchors(s.n, O.anchor_count(s.n))
+    b = np.random.default_rng(3).standard_normal((s.n, 3))
+    x1, st1 = _debug_chol(s.faces, s.n, anchors, b)
+    monkeypatch.setenv("DMCG_DEBUG_PREORDER", "1")
+    x2, st2 = _debug_chol(s.faces, s.n, anchors, b)
+    assert np.array_equal(x1, x2) and np.array_equal(st1[:7], st2[:7])
+
+
+def test_ordering_fill_on_a_grid():
+    """Nested dissection by BFS level sets: on a k x k grid the factor of M = L^T L + S^T S
+    stays near the O(n log n) fill of a dissection ordering (a banded ordering of this
+    22 500-vertex grid would hold ~ 2 * 150 * n = 6.8 M entries)."""
+    s = synth.grid(150, 150, 2)
+    anchors = O.select_anchors(s.n, O.anchor_count(s.n))
+    _, st = _debug_chol(s.faces, s.n, anchors, np.ones((s.n, 1)))
+    nnz_l = st[2]
+    assert nnz_l < 3.5e6, nnz_l
