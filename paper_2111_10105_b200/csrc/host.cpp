@@ -1767,16 +1767,33 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
       const char* e = std::getenv("DMCG_DECODE_FIRST_PCT");
       return e ? std::max(10, std::min(90, std::atoi(e))) : 75;
     }();
+    // DMCG_DECODE_BOUNDS="f1,f2,...": explicit window boundaries (experiments)
+    static const std::vector<uint32_t> env_bounds = [] {
+      std::vector<uint32_t> v;
+      if (const char* e = std::getenv("DMCG_DECODE_BOUNDS"))
+        for (const char* q = e; *q;) {
+          char* end = nullptr;
+          const unsigned long x = std::strtoul(q, &end, 10);
+          if (end == q) break;
+          v.push_back((uint32_t)x);
+          q = *end ? end + 1 : end;
+        }
+      return v;
+    }();
+    bool use_env = !env_bounds.empty() && env_bounds.back() < in->F;
+    for (size_t i = 1; i < env_bounds.size(); ++i) use_env = use_env && env_bounds[i] > env_bounds[i - 1];
+    const uint32_t nwin_eff = use_env ? (uint32_t)env_bounds.size() + 1 : nwin;
     auto bound = [&](uint32_t w) -> uint32_t {
       if (w == 0) return 0;
-      if (w >= nwin) return in->F;
+      if (w >= nwin_eff) return in->F;
+      if (use_env) return env_bounds[w - 1];
       if (nwin == 2 && in->F >= 256) {
         const uint32_t b = (uint32_t)((uint64_t)in->F * first_pct / 100 + 32) / 64 * 64;
         return std::max<uint32_t>(64, std::min<uint32_t>(b, in->F - 64));
       }
       return (uint32_t)((uint64_t)in->F * w / nwin);
     };
-    for (uint32_t w = 0; w < nwin && st.good(); ++w) {
+    for (uint32_t w = 0; w < nwin_eff && st.good(); ++w) {
       const uint32_t f0 = bound(w);
       const uint32_t f1 = bound(w + 1);
       dmcg_decode_options ow = o;
@@ -1784,8 +1801,8 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
       ow.frame_count = f1 - f0;
       if (w) ow.reuse_factor = 1;
       st = plan_decode(p, &ow, p->d_x_out);  // returns after its stream sync
-      if (w + 1 == nwin) tm.lap("kernels");
-      if (st.good()) d2h(f0, f1 - f0, w + 1 == nwin ? ctx->stream : ctx->aux2);
+      if (w + 1 == nwin_eff) tm.lap("kernels");
+      if (st.good()) d2h(f0, f1 - f0, w + 1 == nwin_eff ? ctx->stream : ctx->aux2);
     }
     if (cudaStreamSynchronize(ctx->aux2) != cudaSuccess && st.good())
       st = {DMCG_E_CUDA, "CudaError: stream sync failed"};
