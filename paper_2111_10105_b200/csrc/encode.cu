@@ -201,18 +201,28 @@ __global__ void k_check_finite(long nF, const T* __restrict__ x0, const T* __res
 
 // Gram reduction: S = sum of split-K partials in split order, then
 // R = 0.5 * (S + S^T) exactly as spectral.cpp:38 symmetrises.
+// lower_only: the partials are bitwise symmetric and only their lower
+// triangle (f >= g) was computed (Ozaki Gram, ozaki.cu): both sums read it,
+// and 0.5 (s + s) == s exactly, the value the full product gives.
 __global__ void k_reduce_sym(int F, int splits, int nbatch, const double* __restrict__ part,
-                             double* __restrict__ R) {
+                             double* __restrict__ R, int lower_only) {
   const long FF = (long)F * F;
   const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (t >= FF) return;
   const int f = (int)(t / F), g = (int)(t % F);
   double s1 = 0.0, s2 = 0.0;
-  for (int sp = 0; sp < splits; ++sp) {
-    const double* P = part + ((long)sp * nbatch + b) * FF;
-    s1 = __dadd_rn(s1, P[(long)f * F + g]);
-    s2 = __dadd_rn(s2, P[(long)g * F + f]);
+  if (lower_only) {
+    const long lo = (long)max(f, g) * F + min(f, g);
+    for (int sp = 0; sp < splits; ++sp)
+      s1 = __dadd_rn(s1, part[((long)sp * nbatch + b) * FF + lo]);
+    s2 = s1;
+  } else {
+    for (int sp = 0; sp < splits; ++sp) {
+      const double* P = part + ((long)sp * nbatch + b) * FF;
+      s1 = __dadd_rn(s1, P[(long)f * F + g]);
+      s2 = __dadd_rn(s2, P[(long)g * F + f]);
+    }
   }
   R[b * FF + (long)g * F + f] = __dmul_rn(0.5, __dadd_rn(s1, s2));
 }
@@ -386,10 +396,10 @@ cudaError_t launch_check_finite(cudaStream_t s, int n, int F, const void* const 
 }
 
 cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, const double* part,
-                              double* R) {
+                              double* R, bool lower_only) {
   const long FF = (long)F * F;
   dim3 grid((unsigned)((FF + 255) / 256), nbatch);
-  k_reduce_sym<<<grid, 256, 0, s>>>(F, splits, nbatch, part, R);
+  k_reduce_sym<<<grid, 256, 0, s>>>(F, splits, nbatch, part, R, lower_only ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -18,7 +18,7 @@ cudaError_t launch_check_finite(cudaStream_t s, int n, int F, const void* const 
                                 int* flags);
 // Sum split-K Gram partials in split order and symmetrise (spectral.cpp:37-38).
 cudaError_t launch_reduce_sym(cudaStream_t s, int F, int splits, int nbatch, const double* part,
-                              double* R);
+                              double* R, bool lower_only = false);
 // Sum of split-K partials (row-major M x N) into column-major out (M x N).
 cudaError_t launch_reduce_sum(cudaStream_t s, int M, int N, int splits, int nbatch,
                               const double* part, double* out);

@@ -205,6 +205,7 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 struct OzGemmArgs {
   int M, N, tiles_m, tiles_n, splits, kb_total, kb_per_split;
   int a_rows_pad, b_rows_pad;
+  int syrk;  // A == B (Gram): only the tiles that reach the lower triangle are computed
   const unsigned long long* a_max;
   const unsigned long long* b_max;
   OzStore out;
@@ -247,6 +248,11 @@ __global__ void __launch_bounds__(192, OzCfg<S>::kCtasPerSm)
   const int kb0 = sp * g.kb_per_split;
   const int kb1 = min(g.kb_total, kb0 + g.kb_per_split);
   const int nkb = kb1 - kb0;
+  // Gram: the slice products are exact integers and the fp64 combination is
+  // the same expression for (f, g) and (g, f), so the partial is bitwise
+  // symmetric; a tile entirely above the diagonal is never read
+  // (k_reduce_sym, lower_only) and exits before any setup
+  if (g.syrk && tn * kOzBN > tm * kOzBM + (kOzBM - 1)) return;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < C::kStages; ++i) {
@@ -490,7 +496,7 @@ cudaError_t oz_gram(cudaStream_t st, const void* const x[3], bool f32, int n, in
   if (e != cudaSuccess) return e;
   const long FF = (long)F * F;
   OzStore out{part, FF, 3 * FF, (long)F, 1L};
-  return oz_gemm(st, sl, sl, out, gram_min_splits(F), splits);
+  return oz_gemm(st, sl, sl, out, gram_min_splits(F), splits, true);
 }
 
 cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, int s, int8_t* qa,
@@ -520,7 +526,7 @@ cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, i
 }
 
 cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const OzStore& out,
-                    int min_splits, int* splits_out) {
+                    int min_splits, int* splits_out, bool syrk) {
   if (A.s != B.s || A.K_pad != B.K_pad || A.batch != B.batch) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, kOzBM) || !make_map(&mb, B, kOzBN)) return cudaErrorInvalidValue;
@@ -532,6 +538,7 @@ cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const
   g.kb_total = A.K_pad / kOzBK;
   g.splits = oz_splits(A, min_splits);
   g.kb_per_split = (g.kb_total + g.splits - 1) / g.splits;
+  g.syrk = (syrk && A.q == B.q) ? 1 : 0;
   g.a_rows_pad = A.rows_pad;
   g.b_rows_pad = B.rows_pad;
   g.a_max = A.maxbits;

@@ -76,8 +76,10 @@ struct OzStore {
 // K = A.K (= B.K), split over ceil(K_pad / kOzKChunk) K ranges (or `splits`
 // if larger) written to separate partial slots.  Returns the split count via
 // *splits_out.  A and B may be the same OzSlices (the Gram).
+// syrk (A and B the same slices): tiles entirely above the diagonal are
+// skipped; the caller reads the lower triangle only.
 cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const OzStore& out,
-                    int min_splits, int* splits_out);
+                    int min_splits, int* splits_out, bool syrk = false);
 
 // C[b] = A[b] B[b]^T for two operand views (one K split: K_pad <= kOzKChunk),
 // slicing both into qa / qb (oz_slice_bytes each) and maxa / maxb

@@ -154,7 +154,8 @@ Status gram(dmcg_plan* p, const void* const x[3], int n) {
     int splits = 0;
     DMCG_TRY(oz_gram(s, x, std::is_same<T, float>::value, n, F, p->oz_slices, p->d_oz_q,
                      p->d_oz_max, p->d_part, &splits));
-    DMCG_TRY(launch_reduce_sym(s, F, splits, 3, p->d_part, p->d_R));
+    // oz_gram computes the tiles that reach the lower triangle only (SYRK)
+    DMCG_TRY(launch_reduce_sym(s, F, splits, 3, p->d_part, p->d_R, true));
     return Status::ok();
   }
   const int tiles = ((F + kBM - 1) / kBM) * ((F + kBN - 1) / kBN);
