@@ -343,6 +343,14 @@ __global__ void __launch_bounds__(192, OzCfg<S>::kCtasPerSm)
       tc_fence_after();
     }
     double lo = INFINITY, hi = -INFINITY;
+    // Unit-stride outputs go through shared memory (the operand stages are
+    // free once tmem_full has fired): a lane holds one ROW of the tile, so
+    // direct stores are 32 scattered 8-byte pieces per instruction; staged,
+    // the warp writes each row's 64 doubles as two contiguous 256-byte stores.
+    constexpr int kStgLd = kOzBN + 1;
+    static_assert(4 * 32 * kStgLd * 8 <= C::kStages * C::kStage, "staging fits the operand stages");
+    const bool staged = g.out.sn == 1;
+    double* stg = reinterpret_cast<double*>(smem) + quarter * (32 * kStgLd);
 #pragma unroll 1
     for (int c = 0; c < kOzBN / 16; ++c) {
       double v[16];
@@ -366,10 +374,28 @@ __global__ void __launch_bounds__(192, OzCfg<S>::kCtasPerSm)
           const int ncol = tn * kOzBN + c * 16 + j;
           if (ncol < g.N) {
             const double r = ldexp(v[j], ea + col_exp[c * 16 + j]);
-            dst[(long)ncol * g.out.sn] = r;
+            if (staged)
+              stg[lane * kStgLd + c * 16 + j] = r;
+            else
+              dst[(long)ncol * g.out.sn] = r;
             lo = fmin(lo, r);
             hi = fmax(hi, r);
           }
+        }
+      }
+    }
+    if (staged) {
+      __syncwarp();
+      const int m0 = tm * kOzBM + quarter * 32;
+#pragma unroll 4
+      for (int rr = 0; rr < 32; ++rr) {
+        if (m0 + rr >= g.M) break;
+        double* dst = g.out.C + b * g.out.sb + sp * g.out.ssplit + (long)(m0 + rr) * g.out.sm +
+                      tn * kOzBN;
+#pragma unroll
+        for (int h = 0; h < kOzBN / 32; ++h) {
+          const int col = lane + 32 * h;
+          if (tn * kOzBN + col < g.N) dst[col] = stg[rr * kStgLd + col];
         }
       }
     }
