@@ -91,10 +91,28 @@ __global__ void k_dequant_rows(int n, const uint16_t* __restrict__ q, const doub
   const uint16_t* qr = q + row * n;
   double* o = out + row * n;
   bool bad = false;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t lv = qr[i];
-    bad |= width != 0.0 && lv >= levels;
-    o[i] = width == 0.0 ? min_ : dequantize_level(min_, width, false, lv);
+  if ((n & 7) == 0 && (((uintptr_t)q | (uintptr_t)out) & 15) == 0) {
+    // eight symbols per thread: one 16-byte load, four 16-byte stores (the
+    // one-symbol loop keeps 2 bytes in flight per thread and ran at 0.75 TB/s)
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8; i < n;
+         i += gridDim.x * blockDim.x * 8) {
+      const uint4 pk = *reinterpret_cast<const uint4*>(qr + i);
+      const uint32_t w4[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint32_t l0 = w4[h] & 0xffffu, l1 = w4[h] >> 16;
+        bad |= width != 0.0 && (l0 >= levels || l1 >= levels);
+        const double v0 = width == 0.0 ? min_ : dequantize_level(min_, width, false, l0);
+        const double v1 = width == 0.0 ? min_ : dequantize_level(min_, width, false, l1);
+        *reinterpret_cast<double2*>(o + i + 2 * h) = make_double2(v0, v1);
+      }
+    }
+  } else {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const uint32_t lv = qr[i];
+      bad |= width != 0.0 && lv >= levels;
+      o[i] = width == 0.0 ? min_ : dequantize_level(min_, width, false, lv);
+    }
   }
   if (bad) atomicOr(flags, 1);
 }
@@ -481,7 +499,8 @@ cudaError_t launch_mean_shift(cudaStream_t s, int n, int Fw, int F_all, int f0, 
 cudaError_t launch_dequant_rows(cudaStream_t s, int rows, int n, const uint16_t* q,
                                 const double* rowp, const uint8_t* rbits, int* flags, double* out) {
   if (rows <= 0 || n <= 0) return cudaSuccess;
-  const int bx = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
+  const int per = (n & 7) == 0 ? 2048 : 256;  // symbols per CTA pass
+  const int bx = (n + per - 1) / per < 64 ? (n + per - 1) / per : 64;
   k_dequant_rows<<<dim3(bx, rows), 256, 0, s>>>(n, q, rowp, rbits, flags, out);
   return cudaGetLastError();
 }

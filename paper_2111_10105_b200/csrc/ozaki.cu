@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -99,16 +100,42 @@ __global__ void __launch_bounds__(256) k_oz_slice(OzOperand op, OzSlices sl) {
   uint32_t w[kOzMaxS][4];
 #pragma unroll
   for (int p = 0; p < kOzMaxS; ++p) w[p][0] = w[p][1] = w[p][2] = w[p][3] = 0u;
+  if constexpr (std::is_same<T, float>::value) {
+    // fp32 storage: the same digits in fp32 arithmetic.  x 2^-e, the products
+    // by 128 and the remainders are exact in fp32 (a 24-bit value loses 7 bits
+    // per digit), rint is the round-to-nearest-even of adding 1.5 * 2^23, and
+    // the digit's two's complement sits in the sum's low mantissa byte: no
+    // fp64 pipe and no XU conversions (which bound the fp64 loop below).
+    // Values that would be fp32 denormals after scaling are below every digit.
+    const float scale = (e > -127 && e < 127) ? __int_as_float((127 - e) << 23) : 0.0f;
+    constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    double y = ldexp(tile[r][kq + j], -e);  // |y| < 127.5 / 128, exact
+    for (int j = 0; j < 16; ++j) {
+      const float x = (float)tile[r][kq + j];
+      float y = scale != 0.0f ? __fmul_rn(x, scale) : ldexpf(x, -e);
 #pragma unroll
-    for (int p = 0; p < kOzMaxS; ++p) {
-      if (p < sl.s) {
-        y *= 128.0;
-        const double a = rint(y);  // balanced digits: |a_1| <= 127, |a_p| <= 64 (p > 1)
-        y -= a;                    // exact, |y| <= 1/2
-        w[p][j >> 2] |= (uint32_t)(uint8_t)(int8_t)(int)a << (8 * (j & 3));
+      for (int p = 0; p < kOzMaxS; ++p) {
+        if (p < sl.s) {
+          y = __fmul_rn(y, 128.0f);
+          const float m = __fadd_rn(y, kMagic);
+          const float a = __fsub_rn(m, kMagic);
+          y = __fsub_rn(y, a);
+          w[p][j >> 2] |= ((uint32_t)__float_as_int(m) & 0xffu) << (8 * (j & 3));
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      double y = ldexp(tile[r][kq + j], -e);  // |y| < 127.5 / 128, exact
+#pragma unroll
+      for (int p = 0; p < kOzMaxS; ++p) {
+        if (p < sl.s) {
+          y *= 128.0;
+          const double a = rint(y);  // balanced digits: |a_1| <= 127, |a_p| <= 64 (p > 1)
+          y -= a;                    // exact, |y| <= 1/2
+          w[p][j >> 2] |= (uint32_t)(uint8_t)(int8_t)(int)a << (8 * (j & 3));
+        }
       }
     }
   }
