@@ -26,8 +26,8 @@ template <typename T>
 __global__ void __launch_bounds__(kDeltaWarps * 32)
     k_delta(int n, int F, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
             const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2,
-            double* __restrict__ delta, int* flags) {
-  const int a = blockIdx.y;
+            double* __restrict__ delta, int* flags, int a0) {
+  const int a = blockIdx.y + a0;
   const T* __restrict__ X = a == 0 ? x0 : (a == 1 ? x1 : x2);
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * kDeltaWarps + (threadIdx.x >> 5);
@@ -98,11 +98,11 @@ template <typename T>
 __global__ void __launch_bounds__(kDeltaWarps * 32)
     k_delta_vec(int n, int F, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci,
                 const T* __restrict__ x0, const T* __restrict__ x1, const T* __restrict__ x2,
-                double* __restrict__ delta, int* flags) {
+                double* __restrict__ delta, int* flags, int a0) {
   using VT = Vec16<T>;
   using V = typename VT::V;
   constexpr int VEC = VT::N, CH = delta_vec_ch<T>(), PASS = 32 * VEC * CH;
-  const int a = blockIdx.y;
+  const int a = blockIdx.y + a0;  // a0: first axis of this launch
   const T* __restrict__ X = a == 0 ? x0 : (a == 1 ? x1 : x2);
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * kDeltaWarps + (threadIdx.x >> 5);
@@ -352,33 +352,37 @@ __global__ void k_flip_min_keys(long rows, unsigned long long* keys) {
 
 }  // namespace
 
+// axis < 0: all three axes in one launch; else that axis alone (the drop-in
+// encode runs an axis as soon as its input has arrived).
 cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
                          const uint32_t* lap_ci, const void* const x[3], bool f32, double* delta,
-                         int* flags) {
-  dim3 grid((n + kDeltaWarps - 1) / kDeltaWarps, 3);
+                         int* flags, int axis) {
+  const int a0 = axis < 0 ? 0 : axis;
+  dim3 grid((n + kDeltaWarps - 1) / kDeltaWarps, axis < 0 ? 3 : 1);
   const size_t esz = f32 ? 4 : 8;
   bool vec = (F * esz) % 16 == 0;  // every row 16-byte aligned
-  for (int a = 0; a < 3; ++a) vec = vec && ((uintptr_t)x[a] % 16 == 0);
+  for (int a = 0; a < 3; ++a)
+    if (axis < 0 || a == axis) vec = vec && ((uintptr_t)x[a] % 16 == 0);
   static const bool scalar = getenv("DMCG_DELTA_SCALAR") != nullptr;  // tests
   if (vec && !scalar) {
     if (f32)
       k_delta_vec<float><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const float*)x[0],
                                                            (const float*)x[1], (const float*)x[2],
-                                                           delta, flags);
+                                                           delta, flags, a0);
     else
       k_delta_vec<double><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const double*)x[0],
                                                             (const double*)x[1], (const double*)x[2],
-                                                            delta, flags);
+                                                            delta, flags, a0);
     return cudaGetLastError();
   }
   if (f32)
     k_delta<float><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const float*)x[0],
                                                      (const float*)x[1], (const float*)x[2],
-                                                     delta, flags);
+                                                     delta, flags, a0);
   else
     k_delta<double><<<grid, kDeltaWarps * 32, 0, s>>>(n, F, lap_rp, lap_ci, (const double*)x[0],
                                                       (const double*)x[1], (const double*)x[2],
-                                                      delta, flags);
+                                                      delta, flags, a0);
   return cudaGetLastError();
 }
 

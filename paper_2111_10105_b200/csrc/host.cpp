@@ -415,7 +415,11 @@ int dmcg_create(dmcg_ctx** out, int device) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->aux2, cudaStreamNonBlocking, prio_lo) != cudaSuccess) {
+      cudaStreamCreateWithPriority(&c->aux2, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_in[2], cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return DMCG_E_CUDA;
   }
@@ -434,6 +438,10 @@ void dmcg_destroy(dmcg_ctx* c) {
   c->pool.release_all();
   cudaStreamSynchronize(c->aux);
   cudaStreamSynchronize(c->aux2);
+  cudaStreamSynchronize(c->copy);
+  for (auto e : c->ev_in)
+    if (e) cudaEventDestroy(e);
+  cudaStreamDestroy(c->copy);
   for (auto e : c->ev_timing) cudaEventDestroy(e);
   for (auto e : c->ev_plain) cudaEventDestroy(e);
   cudaStreamDestroy(c->aux2);
@@ -804,6 +812,10 @@ static Status plan_create_impl(dmcg_ctx* ctx, uint32_t n, uint32_t F, int dtype,
     }
   tm.lap("events+start");
   if (encode_side) h2d(p->d_start, start.data(), start.size() * 8);
+  if (ctx->after_plan_uploads) {
+    ctx->after_plan_uploads();
+    ctx->after_plan_uploads = nullptr;
+  }
   if (ok) ok = cudaStreamSynchronize(s) == cudaSuccess;
   tm.lap("upload+sync");
   if (!ok) {
@@ -1493,20 +1505,42 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
     void** d;
     size_t bytes;
     ~InGuard() {
+      cudaStreamSynchronize(c->copy);
       cudaStreamSynchronize(c->stream);
       for (int a = 0; a < 3; ++a)
         if (d[a]) c->pool.put(d[a], bytes);
     }
   } in_guard{ctx, d_in, in_bytes};
+  // On its own stream, axis by axis in 32 MB pieces with an event after each
+  // axis: the plan's small (pageable) uploads slip between the pieces instead
+  // of queueing behind a whole axis on the copy engine, and the encode starts
+  // an axis' first kernels (K1, Gram) while the next axis is still in flight.
   if (in_bytes && seq->axes[0] && seq->axes[1] && seq->axes[2] &&
       (seq->dtype == DMCG_F64 || seq->dtype == DMCG_F32)) {
     bool ok = true;
     for (int a = 0; a < 3 && ok; ++a) {
       d_in[a] = ctx->pool.get(in_bytes);
-      ok = d_in[a] && cudaMemcpyAsync(d_in[a], seq->axes[a], in_bytes, cudaMemcpyHostToDevice,
-                                      ctx->stream) == cudaSuccess;
+      ok = d_in[a] != nullptr;
     }
-    if (!ok) return ctx->set_error({DMCG_E_CUDA, "CudaError: H2D copy failed"});
+    if (!ok) return ctx->set_error({DMCG_E_CUDA, "CudaError: device allocation failed"});
+    auto issue_axis = [ctx, seq, in_bytes](void* dst, int a) {
+      const size_t piece = (size_t)32 << 20;
+      bool good = true;
+      for (size_t off = 0; off < in_bytes && good; off += piece)
+        good = cudaMemcpyAsync((uint8_t*)dst + off, (const uint8_t*)seq->axes[a] + off,
+                               std::min(piece, in_bytes - off), cudaMemcpyHostToDevice,
+                               ctx->copy) == cudaSuccess;
+      return cudaEventRecord(ctx->ev_in[a], ctx->copy) == cudaSuccess && good;
+    };
+    // axis 0 now; axes 1 and 2 once the plan's uploads are queued (see
+    // dmcg_ctx::after_plan_uploads), or below if no plan gets that far
+    if (!issue_axis(d_in[0], 0)) return ctx->set_error({DMCG_E_CUDA, "CudaError: H2D copy failed"});
+    void* d1 = d_in[1];
+    void* d2 = d_in[2];
+    ctx->after_plan_uploads = [issue_axis, d1, d2] {
+      issue_axis(d1, 1);
+      issue_axis(d2, 2);
+    };
   }
   tm.lap("h2d issue");
   // One mesh build (host pool) serves the plan and the analysis thread; the
@@ -1521,6 +1555,10 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   dmcg_plan* p = nullptr;
   Status st = plan_create_impl(ctx, seq->n, seq->F, seq->dtype, seq->faces, seq->n_faces, cfg,
                                nullptr, 0, &p, have_mesh ? &built : nullptr);
+  if (ctx->after_plan_uploads) {  // plan creation failed before its uploads
+    ctx->after_plan_uploads();
+    ctx->after_plan_uploads = nullptr;
+  }
   if (!st.good()) return ctx->set_error(st);
   // the early analysis keys on the plan's anchor set: drop it if they differ
   if (ctx->pending && !std::equal(ctx->pending->anchors.begin(), ctx->pending->anchors.end(),
@@ -1537,8 +1575,9 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   const std::function<void()> prepare_decode = [&] {
     if (no_prep || !ctx->pending || cfg->variant == DMCG_V2V || p->nb != 1) return;
     std::unique_ptr<PendingAnalysis> pa = std::move(ctx->pending);
-    if (pa->th.joinable()) pa->th.join();
     PhaseTimer tp("prepare-decode");
+    if (pa->th.joinable()) pa->th.join();
+    tp.lap("wait for the analysis");
     // what decode_config() will read from the stream this encode writes
     dmcg_config dc;
     dmcg_config_default(&dc);
@@ -1598,13 +1637,17 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
   Status st_dl = Status::ok();
   const bool early_dl = p->nb == 1;
   const std::function<void()> between = [&] {
+    // the preparation first: a D2H copy into pageable memory (small header
+    // arrays of a caller that did not page-lock them) returns only once the
+    // kernels ahead of it have run
+    prepare_decode();
     if (early_dl) {
       if (!out->faces) out->faces = seq->faces;
       st_dl = download_issue(p, out);
       out->faces = seq->faces;
     }
-    prepare_decode();
   };
+  p->in_events = true;
   if (st.good()) st = plan_encode(p, d_in, &between);
   tm.lap("h2d+kernels+download");
   if (st.good() && early_dl) {

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <map>
+#include <functional>
 #include <memory>
 #include <string>
 #include <thread>
@@ -139,6 +140,12 @@ struct dmcg_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // fork/join side stream (independent encode / decode phases)
   cudaStream_t aux2 = nullptr; // low-priority stream: the decoder's factor during an encode
+  cudaStream_t copy = nullptr; // the drop-in encode's input H2D (chunked, one event per axis)
+  cudaEvent_t ev_in[3] = {nullptr, nullptr, nullptr};  // axis a of the input has arrived
+  // run once by the next plan creation right after it has issued its uploads
+  // (the drop-in encode queues input axes 1 and 2 there: queued earlier they
+  // would hold the copy engine's FIFO ahead of the plan's small uploads)
+  std::function<void()> after_plan_uploads;
   std::string err;
   dmcg::DevicePool pool;
   dmcg_stats last_stats = {};  // stats of the last drop-in encode / decode
@@ -290,6 +297,9 @@ struct dmcg_plan {
   bool factor_valid = false;        // cdev.F / Linv hold the numeric factor of M          // chol / mesh.m_* were filled by a PendingAnalysis
   bool oi_timed = false;            // ev[6..7] bracket k_oi_fused in the last encode
   float h_anchor_rng[6] = {};        // download staging (anchor ranges)
+  // drop-in encode: the input axes arrive on ctx->copy; the encode waits for
+  // ctx->ev_in[a] before the first kernel that reads axis a
+  bool in_events = false;
   cudaStream_t up_stream = nullptr;  // plan / decode-structure uploads (default: aux / ctx stream)
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
   dmcg::PlanGraph g_encode, g_decode;

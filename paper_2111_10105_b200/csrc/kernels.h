@@ -12,7 +12,7 @@ namespace dmcg {
 // f32 selects float input.  flags[0] |= 1<<axis on non-finite input.
 cudaError_t launch_delta(cudaStream_t s, int n, int F, const uint32_t* lap_rp,
                          const uint32_t* lap_ci, const void* const x[3], bool f32, double* delta,
-                         int* flags);
+                         int* flags, int axis = -1);
 // flags[0] |= 1 << axis on a non-finite coordinate (v2v: no K1 pass).
 cudaError_t launch_check_finite(cudaStream_t s, int n, int F, const void* const x[3], bool f32,
                                 int* flags);

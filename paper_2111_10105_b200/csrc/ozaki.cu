@@ -552,6 +552,28 @@ cudaError_t oz_gram(cudaStream_t st, const void* const x[3], bool f32, int n, in
   return oz_gemm(st, sl, sl, out, gram_min_splits(F), splits, true);
 }
 
+// One axis of oz_gram (the drop-in encode runs an axis as soon as its input has
+// arrived): same slices, same K splits and the same partial slots as the
+// batched call, so the reduced R is bit-identical.
+cudaError_t oz_gram_axis(cudaStream_t st, int a, const void* xa, bool f32, int n, int F, int s,
+                         int8_t* q, unsigned long long* maxbits, double* part, int* splits) {
+  OzOperand op{{xa, nullptr, nullptr}, f32, 1L, (long)F, F, n, 1};
+  OzSlices sl;
+  sl.rows = F;
+  sl.rows_pad = oz_rows_pad(F);
+  sl.K = n;
+  sl.K_pad = oz_k_pad(n);
+  sl.s = s;
+  sl.batch = 1;
+  sl.q = q + (size_t)a * s * sl.rows_pad * sl.K_pad;
+  sl.maxbits = maxbits + (size_t)a * sl.rows_pad;
+  cudaError_t e = oz_slice(st, op, sl);
+  if (e != cudaSuccess) return e;
+  const long FF = (long)F * F;
+  OzStore out{part + a * FF, FF, 3 * FF, (long)F, 1L};
+  return oz_gemm(st, sl, sl, out, oz_gram_splits(F, n, s), splits, true);
+}
+
 cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, int s, int8_t* qa,
                       unsigned long long* maxa, int8_t* qb, unsigned long long* maxb,
                       const OzStore& out) {

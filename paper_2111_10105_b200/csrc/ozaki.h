@@ -104,5 +104,8 @@ int oz_splits(const OzSlices& A, int min_splits);
 int oz_gram_splits(int F, int n, int s);
 cudaError_t oz_gram(cudaStream_t st, const void* const x[3], bool f32, int n, int F, int s,
                     int8_t* q, unsigned long long* maxbits, double* part, int* splits);
+// Axis a alone, into the same buffers and partial slots (bit-identical R).
+cudaError_t oz_gram_axis(cudaStream_t st, int a, const void* xa, bool f32, int n, int F, int s,
+                         int8_t* q, unsigned long long* maxbits, double* part, int* splits);
 
 }  // namespace dmcg

@@ -414,7 +414,12 @@ Status plan_prefactor_async(dmcg_plan* p, bool after_stream) {
 // Every kernel of one encode on the plan stream (no host synchronisation:
 // capturable into a CUDA graph).
 static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefactor) {
-  if (p->nb > 1) return enqueue_encode_blocks(p, x);
+  if (p->nb > 1) {
+    if (p->in_events)  // drop-in: the input axes arrive on the copy stream
+      for (int a = 0; a < 3; ++a)
+        DMCG_TRY(cudaStreamWaitEvent(p->ctx->stream, p->ctx->ev_in[a], 0));
+    return enqueue_encode_blocks(p, x);
+  }
   cudaStream_t s = p->ctx->stream;
   const int n = (int)p->n, F = (int)p->F, k = (int)p->k;
   const bool f32 = p->dtype == DMCG_F32;
@@ -425,17 +430,37 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefacto
     Status st = fork_prefactor(p);
     if (!st.good()) return st;
   }
-  // K1 delta coordinates (codec.cpp:419); v2v codes the trajectories.
-  if (variant_uses_delta(p->variant))
-    DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
-  else
-    DMCG_TRY(launch_check_finite(s, n, F, x, f32, p->d_flags));
-  DMCG_TRY(record_event(p->ev[1], s));
-  // K2 autocorrelation (spectral.cpp:35-39); the implicit OI never forms it.
   Status st = Status::ok();
-  if (!implicit_oi(p)) st = f32 ? gram<float>(p, x, n) : gram<double>(p, x, n);
-  if (!st.good()) return st;
-  DMCG_TRY(record_event(p->ev[2], s));
+  if (p->in_events && p->oz_slices && variant_uses_delta(p->variant) && !implicit_oi(p)) {
+    // drop-in encode, fp32 storage: K1 and the Gram slices / tiles of an axis
+    // as soon as that axis has arrived (ctx->ev_in), under the next axis' H2D;
+    // same kernels, K splits and partial slots as the batched calls below
+    // (bit-identical delta and R).  ms_delta then covers these interleaved
+    // launches and their waits, ms_gram the reduction.
+    int splits = 0;
+    for (int a = 0; a < 3; ++a) {
+      DMCG_TRY(cudaStreamWaitEvent(s, p->ctx->ev_in[a], 0));
+      DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags, a));
+      DMCG_TRY(oz_gram_axis(s, a, x[a], f32, n, F, p->oz_slices, p->d_oz_q, p->d_oz_max,
+                            p->d_part, &splits));
+    }
+    DMCG_TRY(record_event(p->ev[1], s));
+    DMCG_TRY(launch_reduce_sym(s, F, splits, 3, p->d_part, p->d_R, true));
+    DMCG_TRY(record_event(p->ev[2], s));
+  } else {
+    if (p->in_events)
+      for (int a = 0; a < 3; ++a) DMCG_TRY(cudaStreamWaitEvent(s, p->ctx->ev_in[a], 0));
+    // K1 delta coordinates (codec.cpp:419); v2v codes the trajectories.
+    if (variant_uses_delta(p->variant))
+      DMCG_TRY(launch_delta(s, n, F, p->d_lap_rp, p->d_lap_ci, x, f32, p->d_delta, p->d_flags));
+    else
+      DMCG_TRY(launch_check_finite(s, n, F, x, f32, p->d_flags));
+    DMCG_TRY(record_event(p->ev[1], s));
+    // K2 autocorrelation (spectral.cpp:35-39); the implicit OI never forms it.
+    if (!implicit_oi(p)) st = f32 ? gram<float>(p, x, n) : gram<double>(p, x, n);
+    if (!st.good()) return st;
+    DMCG_TRY(record_event(p->ev[2], s));
+  }
   // K3 basis.
   p->forked = false;
   st = basis(p, x, n);
@@ -544,14 +569,18 @@ Status plan_encode(dmcg_plan* p, const void* const x[3], const std::function<voi
   const int k = (int)p->k, F = (int)p->F;
   const void* key[4] = {x[0], x[1], x[2], nullptr};
   const bool pf = prefactor_on(p);
+  PhaseTimer tm("plan_encode");
   {
     Status st = run_graph(p, p->g_encode, key, pf ? 1 : 0, [&] { return enqueue_encode(p, x, pf); });
     if (!st.good()) return st;
   }
+  tm.lap("enqueue (host)");
   p->oi_timed = p->nb == 1 && p->rounds > 0 && k < F && k > 0;
   int flags[8];
-  DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
+  // (before the flags read-back: its pageable destination makes that copy wait
+  // for the kernels on the host)
   if (between && *between) (*between)();
+  DMCG_TRY(cudaMemcpyAsync(flags, p->d_flags, sizeof(flags), cudaMemcpyDeviceToHost, s));
   DMCG_TRY(cudaStreamSynchronize(s));
   float ms;
   cudaEventElapsedTime(&ms, p->ev[0], p->ev[5]);
