@@ -261,8 +261,9 @@ __global__ void k_init_keys(long rows, unsigned long long* keys) {
 // float range; one CTA per (row, axis).
 __global__ void k_quant_rows(int k, int n, const unsigned long long* __restrict__ keys,
                              const uint8_t* __restrict__ bits_in, const double* __restrict__ C,
-                             float* rmin, float* rmax, uint8_t* rbits, uint16_t* __restrict__ q) {
-  const int r = blockIdx.x, a = blockIdx.y;
+                             float* rmin, float* rmax, uint8_t* rbits, uint16_t* __restrict__ q,
+                             int a0) {
+  const int r = blockIdx.x, a = blockIdx.y + a0;
   const long row = (long)a * k + r;
   const double lo = key_to_double(keys[2 * row]);
   const double hi = key_to_double(keys[2 * row + 1]);
@@ -428,9 +429,10 @@ cudaError_t launch_init_keys(cudaStream_t s, long rows, unsigned long long* keys
 
 cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long long* keys,
                               const uint8_t* bits_in, const double* C, float* rmin, float* rmax,
-                              uint8_t* rbits, uint16_t* q) {
+                              uint8_t* rbits, uint16_t* q, int axis) {
   if (k <= 0) return cudaSuccess;
-  k_quant_rows<<<dim3(k, 3), 256, 0, s>>>(k, n, keys, bits_in, C, rmin, rmax, rbits, q);
+  k_quant_rows<<<dim3(k, axis < 0 ? 3 : 1), 256, 0, s>>>(k, n, keys, bits_in, C, rmin, rmax, rbits, q,
+                                                       axis < 0 ? 0 : axis);
   return cudaGetLastError();
 }
 

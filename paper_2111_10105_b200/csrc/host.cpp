@@ -419,7 +419,11 @@ int dmcg_create(dmcg_ctx** out, int device) {
       cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_in[0], cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_in[1], cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_in[2], cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_in[2], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_q[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_q[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_q[2], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_cp, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return DMCG_E_CUDA;
   }
@@ -441,6 +445,9 @@ void dmcg_destroy(dmcg_ctx* c) {
   cudaStreamSynchronize(c->copy);
   for (auto e : c->ev_in)
     if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_q)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_cp) cudaEventDestroy(c->ev_cp);
   cudaStreamDestroy(c->copy);
   for (auto e : c->ev_timing) cudaEventDestroy(e);
   for (auto e : c->ev_plain) cudaEventDestroy(e);
@@ -1136,8 +1143,9 @@ static Status download_issue(dmcg_plan* p, dmcg_encoded* e) {
       CUDA_OK(cudaMemcpyAsync(e->row_min[a], p->d_row_min + a * k, k * 4, cudaMemcpyDeviceToHost, s));
       CUDA_OK(cudaMemcpyAsync(e->row_max[a], p->d_row_max + a * k, k * 4, cudaMemcpyDeviceToHost, s));
       CUDA_OK(cudaMemcpyAsync(e->row_bits[a], p->d_row_bits + a * k, k, cudaMemcpyDeviceToHost, s));
-      CUDA_OK(cudaMemcpyAsync(e->coeff_q[a], p->d_coeff_q + a * k * n, k * n * 2,
-                              cudaMemcpyDeviceToHost, s));
+      if (!p->coeff_streamed)  // else already on its way (enqueue_encode, per axis)
+        CUDA_OK(cudaMemcpyAsync(e->coeff_q[a], p->d_coeff_q + a * k * n, k * n * 2,
+                                cudaMemcpyDeviceToHost, s));
     }
     if (p->n_c)
       CUDA_OK(cudaMemcpy2DAsync(e->anchor_q[a], Fo * 2, p->d_anchor_q + a * (size_t)p->n_c * F,
@@ -1648,6 +1656,17 @@ int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg
     }
   };
   p->in_events = true;
+  if (early_dl && p->k > 0) {  // page-locked coefficient arrays: stream them per axis
+    bool pinned = true;
+    for (int a = 0; a < 3 && pinned; ++a) {
+      cudaPointerAttributes at;
+      pinned = out->coeff_q[a] && cudaPointerGetAttributes(&at, out->coeff_q[a]) == cudaSuccess &&
+               at.type == cudaMemoryTypeHost;
+    }
+    cudaGetLastError();  // an unregistered pointer is not an error here
+    if (pinned)
+      for (int a = 0; a < 3; ++a) p->h_coeff_dst[a] = out->coeff_q[a];
+  }
   if (st.good()) st = plan_encode(p, d_in, &between);
   tm.lap("h2d+kernels+download");
   if (st.good() && early_dl) {

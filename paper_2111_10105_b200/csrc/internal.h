@@ -142,6 +142,8 @@ struct dmcg_ctx {
   cudaStream_t aux2 = nullptr; // low-priority stream: the decoder's factor during an encode
   cudaStream_t copy = nullptr; // the drop-in encode's input H2D (chunked, one event per axis)
   cudaEvent_t ev_in[3] = {nullptr, nullptr, nullptr};  // axis a of the input has arrived
+  cudaEvent_t ev_q[3] = {nullptr, nullptr, nullptr};   // axis a's coefficient symbols are quantised
+  cudaEvent_t ev_cp = nullptr;                         // the copy stream's D2H of them is done
   // run once by the next plan creation right after it has issued its uploads
   // (the drop-in encode queues input axes 1 and 2 there: queued earlier they
   // would hold the copy engine's FIFO ahead of the plan's small uploads)
@@ -300,6 +302,11 @@ struct dmcg_plan {
   // drop-in encode: the input axes arrive on ctx->copy; the encode waits for
   // ctx->ev_in[a] before the first kernel that reads axis a
   bool in_events = false;
+  // drop-in encode with page-locked output arrays: axis a's coefficient
+  // symbols go to h_coeff_dst[a] on ctx->copy as soon as they are quantised
+  // (per-axis projection + quantisation), under the next axes' kernels
+  void* h_coeff_dst[3] = {nullptr, nullptr, nullptr};
+  bool coeff_streamed = false;  // set by the encode when it did so (download skips them)
   cudaStream_t up_stream = nullptr;  // plan / decode-structure uploads (default: aux / ctx stream)
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)
   dmcg::PlanGraph g_encode, g_decode;

@@ -28,7 +28,7 @@ cudaError_t launch_init_keys(cudaStream_t s, long rows, unsigned long long* keys
 // quantize_rows (codec.cpp:244-265) from the row min/max keys.
 cudaError_t launch_quant_rows(cudaStream_t s, int k, int n, const unsigned long long* keys,
                               const uint8_t* bits_in, const double* C, float* rmin, float* rmax,
-                              uint8_t* rbits, uint16_t* q);
+                              uint8_t* rbits, uint16_t* q, int axis = -1);
 // Anchor quantisation (codec.cpp:444-471), one CTA per axis.
 cudaError_t launch_anchors(cudaStream_t s, int n_c, int F, const uint32_t* idx,
                            const void* const x[3], bool f32, int bits, float* rng, uint16_t* q,

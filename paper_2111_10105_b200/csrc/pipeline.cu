@@ -353,8 +353,9 @@ static Status enqueue_encode_blocks_t(dmcg_plan* p, const void* const x[3]) {
     const long nF = (long)n * Fp;
     LoadBlocks<double, true> lD{d, d + nF, d + 2 * nF, nb, (long)kf, 1L, (long)Fp};
     DMCG_TRY(launch_gemm(s, nbat, kl, n, kf, 1, lU, lD, StoreCoeffMinMax{p->d_C, p->d_keys}));
-    DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
-                               p->d_row_max, p->d_row_bits, p->d_coeff_q));
+    if (!p->coeff_streamed)
+      DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
+                                 p->d_row_max, p->d_row_bits, p->d_coeff_q));
   }
   DMCG_TRY(record_event(p->ev[4], s));
   // anchors (codec.cpp:444-471): the padded frames repeat the last one, so
@@ -486,6 +487,25 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefacto
       unsigned long long* mb = ma + 3L * oz_rows_pad(k);
       OzStore out{p->d_C, (long)k * n, 0L, (long)n, 1L, p->d_keys};
       DMCG_TRY(oz_matmul(s, A, B, sp, qa, ma, qb, mb, out));
+    } else if (variant_uses_delta(p->variant) && p->h_coeff_dst[0] && p->nb == 1) {
+      // drop-in encode into page-locked arrays: projection and quantisation
+      // axis by axis (same tiles and arithmetic as the batched launches), each
+      // axis' symbols leaving on the copy stream under the next axis' GEMM
+      const long kn = (long)k * n;
+      for (int a = 0; a < 3; ++a) {
+        LoadDense<double, true> lUa{p->d_U + a * FF, FF, 1L, (long)F};
+        LoadDense<double, true> lDa{p->d_delta + (long)a * n * F, (long)n * F, 1L, (long)F};
+        StoreCoeffMinMax epa{p->d_C + a * kn, p->d_keys + 2L * a * k};
+        DMCG_TRY(launch_gemm(s, 1, k, n, F, 1, lUa, lDa, epa));
+        DMCG_TRY(launch_quant_rows(s, k, n, p->d_keys, p->d_row_bits + 3 * k, p->d_C, p->d_row_min,
+                                   p->d_row_max, p->d_row_bits, p->d_coeff_q, a));
+        DMCG_TRY(cudaEventRecord(p->ctx->ev_q[a], s));
+        DMCG_TRY(cudaStreamWaitEvent(p->ctx->copy, p->ctx->ev_q[a], 0));
+        DMCG_TRY(cudaMemcpyAsync(p->h_coeff_dst[a], p->d_coeff_q + a * kn, kn * 2,
+                                 cudaMemcpyDeviceToHost, p->ctx->copy));
+      }
+      DMCG_TRY(cudaEventRecord(p->ctx->ev_cp, p->ctx->copy));
+      p->coeff_streamed = true;
     } else if (variant_uses_delta(p->variant)) {
       LoadDense<double, true> lD{p->d_delta, (long)n * F, 1L, (long)F};
       DMCG_TRY(launch_gemm(s, 3, k, n, F, 1, lU, lD, ep));
@@ -513,6 +533,8 @@ static Status enqueue_encode(dmcg_plan* p, const void* const x[3], bool prefacto
   if (p->forked) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_join, 0));
   DMCG_TRY(launch_quant_dict(s, 3 * FF, p->dict_bits, p->d_U, p->d_dict_q));
   DMCG_TRY(record_event(p->ev[5], s));
+  if (p->coeff_streamed)  // the plan stream's next wait covers the streamed symbols
+    DMCG_TRY(cudaStreamWaitEvent(s, p->ctx->ev_cp, 0));
   if (prefactor) DMCG_TRY(cudaStreamWaitEvent(s, p->ev_pf_join, 0));  // join (graph capture)
   return Status::ok();
 }

@@ -568,3 +568,35 @@ def test_dropin_pending_decode_plan(codec):
     bbox = float(np.linalg.norm([ax.max() - ax.min() for ax in s.axes]))
     for a in range(3):
         assert np.abs(x32[a].astype(np.float64) - x_fresh[a]).max() <= 1e-5 * bbox
+
+
+@pytest.mark.parametrize("f32", [True, False])
+def test_dropin_encode_pipelines_are_bit_identical(codec, f32):
+    """The drop-in encode pipelines its copies with its kernels -- K1 and the
+    (fp32-storage) Ozaki Gram of an axis under the next axis' H2D, and, into
+    page-locked output arrays, projection + quantisation axis by axis with each
+    axis' symbols leaving on the copy stream (pipeline.cu enqueue_encode) -- and a
+    reused plan on device-resident input runs the batched launches: every array
+    of the three encodes is identical."""
+    import torch
+    s = synth.grid(40, 36, 64, f32=f32, seed=9)
+    npdt = np.float32 if f32 else np.float64
+    cfg = C.EncoderConfig(k_l=16, row_bits=[12] * 16, oi_rounds=6)
+    g_page = codec.encode(s, cfg)                               # pageable outputs
+    buf = C.CompressedAnimation.allocate(g_page.n, g_page.F, g_page.k_l, g_page.n_c, s.faces,
+                                         pinned=True, variant=g_page.variant)
+    g_pin = codec.encode(s, cfg, out=buf)                        # streamed symbols
+    plan = C.Plan(codec, s.n, s.F, s.faces, cfg, dtype=npdt)     # batched launches
+    d_in = [torch.from_numpy(np.ascontiguousarray(x, dtype=npdt)).cuda() for x in s.axes]
+    plan.encode_device([t.data_ptr() for t in d_in])
+    g_plan = plan.download()
+    plan.close()
+    for g in (g_pin, g_plan):
+        assert np.array_equal(g.anchor_idx, g_page.anchor_idx)
+        for a in range(3):
+            assert np.array_equal(g.coeff_q[a], g_page.coeff_q[a])
+            assert np.array_equal(g.dict_q[a], g_page.dict_q[a])
+            assert np.array_equal(g.row_min[a], g_page.row_min[a])
+            assert np.array_equal(g.row_max[a], g_page.row_max[a])
+            assert np.array_equal(g.anchor_q[a], g_page.anchor_q[a])
+            assert g.anchor_min[a] == g_page.anchor_min[a] and g.anchor_max[a] == g_page.anchor_max[a]
