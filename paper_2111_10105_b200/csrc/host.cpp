@@ -1323,6 +1323,7 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
 
 static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
   cudaStream_t s = p->ctx->stream;
+  p->rec_a_valid = false;  // new coefficient symbols
   const size_t n = p->n, F = p->F, k = p->k, Fo = p->F_in;
   const size_t FF = p->nb > 1 ? (size_t)p->nb * p->kf * p->kf : F * F;
   float rng[6];
@@ -1844,11 +1845,17 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
     }();
     bool use_env = !env_bounds.empty() && env_bounds.back() < in->F;
     for (size_t i = 1; i < env_bounds.size(); ++i) use_env = use_env && env_bounds[i] > env_bounds[i - 1];
-    const uint32_t nwin_eff = use_env ? (uint32_t)env_bounds.size() + 1 : nwin;
+    // long sequences: three windows F/2 | F/2 - 64 | 64 frames (the copies of the
+    // first two hide under kernels, the exposed tail copy is 64 frames; the
+    // reconstruction's coefficient operand is sliced once, see rec_a_valid)
+    const bool three = !use_env && nwin == 2 && in->F >= 512 && in->F % 128 == 0 &&
+                       !std::getenv("DMCG_DECODE_FIRST_PCT") && !std::getenv("DMCG_DECODE_WINDOWS");
+    const uint32_t nwin_eff = use_env ? (uint32_t)env_bounds.size() + 1 : (three ? 3u : nwin);
     auto bound = [&](uint32_t w) -> uint32_t {
       if (w == 0) return 0;
       if (w >= nwin_eff) return in->F;
       if (use_env) return env_bounds[w - 1];
+      if (three) return w == 1 ? in->F / 2 : in->F - 64;
       if (nwin == 2 && in->F >= 256) {
         const uint32_t b = (uint32_t)((uint64_t)in->F * first_pct / 100 + 32) / 64 * 64;
         return std::max<uint32_t>(64, std::min<uint32_t>(b, in->F - 64));

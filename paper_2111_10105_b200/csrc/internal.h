@@ -306,6 +306,9 @@ struct dmcg_plan {
   // symbols go to h_coeff_dst[a] on ctx->copy as soon as they are quantised
   // (per-axis projection + quantisation), under the next axes' kernels
   void* h_coeff_dst[3] = {nullptr, nullptr, nullptr};
+  // the reconstruction's A operand (dequantised coefficients, their Ozaki
+  // slices) is still in place from an earlier frame window of the same stream
+  bool rec_a_valid = false;
   bool coeff_streamed = false;  // set by the encode when it did so (download skips them)
   cudaStream_t up_stream = nullptr;  // plan / decode-structure uploads (default: aux / ctx stream)
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)

@@ -576,7 +576,7 @@ cudaError_t oz_gram_axis(cudaStream_t st, int a, const void* xa, bool f32, int n
 
 cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, int s, int8_t* qa,
                       unsigned long long* maxa, int8_t* qb, unsigned long long* maxb,
-                      const OzStore& out) {
+                      const OzStore& out, bool a_sliced) {
   if (A.K != B.K || A.batch != B.batch || oz_k_pad(A.K) > kOzKChunk) return cudaErrorInvalidValue;
   OzSlices sa, sb;
   sa.q = qa;
@@ -592,7 +592,7 @@ cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, i
   sb.maxbits = maxb;
   sb.rows = B.rows;
   sb.rows_pad = oz_rows_pad(B.rows);
-  cudaError_t e = oz_slice(st, A, sa);
+  cudaError_t e = a_sliced ? cudaSuccess : oz_slice(st, A, sa);
   if (e == cudaSuccess) e = oz_slice(st, B, sb);
   if (e != cudaSuccess) return e;
   int used = 0;

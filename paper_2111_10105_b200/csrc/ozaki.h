@@ -89,9 +89,10 @@ cudaError_t oz_gemm(cudaStream_t st, const OzSlices& A, const OzSlices& B, const
 inline size_t oz_slice_bytes(int rows, int K, int s, int batch) {
   return (size_t)batch * s * oz_rows_pad(rows) * oz_k_pad(K);
 }
+// a_sliced: qa / maxa already hold A's slices (an earlier call on the same A).
 cudaError_t oz_matmul(cudaStream_t st, const OzOperand& A, const OzOperand& B, int s, int8_t* qa,
                       unsigned long long* maxa, int8_t* qb, unsigned long long* maxb,
-                      const OzStore& out);
+                      const OzStore& out, bool a_sliced = false);
 
 // Splits oz_gemm will use for (A, B, min_splits).
 int oz_splits(const OzSlices& A, int min_splits);

@@ -587,6 +587,7 @@ static Status run_graph(dmcg_plan* p, PlanGraph& g, const void* const key[4], lo
 // between: host work to run after the launches are queued and before the
 // stream is waited for (dmcg_encode prepares the next decode there).
 Status plan_encode(dmcg_plan* p, const void* const x[3], const std::function<void()>* between) {
+  p->rec_a_valid = false;  // the encode reuses the coefficient and slice buffers
   cudaStream_t s = p->ctx->stream;
   const int k = (int)p->k, F = (int)p->F;
   const void* key[4] = {x[0], x[1], x[2], nullptr};
@@ -829,8 +830,12 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
     // buffer) and U~[:, :k] over the window, then a plain f64 GEMM
     double* Cd = p->d_C;
     double* Ud = p->d_Ud;
-    DMCG_TRY(launch_dequant_rows(s, 3 * k, n, p->d_coeff_q, p->d_rowp, p->d_row_bits,
-                                 p->d_flags + 1, Cd));
+    // a later frame window of the same upload (the drop-in decode's second
+    // window): the dequantised coefficients and their slices are in place
+    const bool a_ready = p->rec_a_valid && p->oz_rec_slices && !p->use_graphs;
+    if (!a_ready)
+      DMCG_TRY(launch_dequant_rows(s, 3 * k, n, p->d_coeff_q, p->d_rowp, p->d_row_bits,
+                                   p->d_flags + 1, Cd));
     DMCG_TRY(launch_dequant_dict(s, F_all, k, f0, F, p->d_dict_q, p->dict_bits, p->d_flags + 1, Ud));
     if (p->oz_rec_slices) {
       // INT8 tensor cores (Ozaki slices): delta~(i, b F + f) = sum_r c~(b, r, i) U~(f, r)
@@ -843,7 +848,8 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
       unsigned long long* ma = p->d_oz_max;
       unsigned long long* mb = ma + 3L * oz_rows_pad(n);
       OzStore out{p->d_rm_delta, (long)F, 0L, (long)W, 1L};
-      DMCG_TRY(oz_matmul(s, A, B, sr, qa, ma, qb, mb, out));
+      DMCG_TRY(oz_matmul(s, A, B, sr, qa, ma, qb, mb, out, a_ready));
+      p->rec_a_valid = !p->use_graphs;
     } else {
       LoadDense<double, false> la{Cd, (long)k * n, (long)n, 1L};   // A(r, i) = c~(r, i)
       LoadDense<double, false> lb{Ud, (long)k * F, (long)F, 1L};   // B(r, f) = U~(f0 + f, r)
