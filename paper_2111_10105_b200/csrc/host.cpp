@@ -1321,9 +1321,25 @@ static Status plan_serialize_impl(dmcg_plan* p, uint8_t* out, size_t cap, dmcg_s
   return Status::ok();
 }
 
-static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
+// stream_coeffs (the drop-in decode of a single-block stream held in
+// page-locked arrays): the coefficient symbols, the bulk of the stream, go axis
+// by axis on the copy stream with an event each, and the reconstruction starts
+// on an axis while the next is in flight (pipeline.cu, coeff_events).
+static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e, bool stream_coeffs = false) {
   cudaStream_t s = p->ctx->stream;
   p->rec_a_valid = false;  // new coefficient symbols
+  if (stream_coeffs && p->k > 0 && p->nb == 1) {
+    for (int a = 0; a < 3 && stream_coeffs; ++a) {
+      cudaPointerAttributes at;
+      stream_coeffs = e->coeff_q[a] &&
+                      cudaPointerGetAttributes(&at, e->coeff_q[a]) == cudaSuccess &&
+                      at.type == cudaMemoryTypeHost;
+    }
+    cudaGetLastError();
+  } else {
+    stream_coeffs = false;
+  }
+  p->coeff_events = stream_coeffs;
   const size_t n = p->n, F = p->F, k = p->k, Fo = p->F_in;
   const size_t FF = p->nb > 1 ? (size_t)p->nb * p->kf * p->kf : F * F;
   float rng[6];
@@ -1344,7 +1360,8 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e) {
       CUDA_OK(cudaMemcpyAsync(p->d_row_max + a * k, e->row_max[a], k * 4, cudaMemcpyHostToDevice, s));
       CUDA_OK(cudaMemcpyAsync(p->d_row_bits + a * k, e->row_bits[a], k, cudaMemcpyHostToDevice, s));
       CUDA_OK(cudaMemcpyAsync(p->d_coeff_q + a * k * n, e->coeff_q[a], k * n * 2,
-                              cudaMemcpyHostToDevice, s));
+                              cudaMemcpyHostToDevice, stream_coeffs ? p->ctx->copy : s));
+      if (stream_coeffs) CUDA_OK(cudaEventRecord(p->ctx->ev_in[a], p->ctx->copy));
     }
     if (p->n_c)
       CUDA_OK(cudaMemcpy2DAsync(p->d_anchor_q + a * (size_t)p->n_c * F, F * 2, e->anchor_q[a],
@@ -1793,7 +1810,7 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
     p->chol_given = true;
   }
   tm.lap("plan");
-  st = upload_impl(p, in);
+  st = upload_impl(p, in, o.solver == 0 && !o.frame_count);
   tm.lap("upload");
   if (st.good() && o.solver == 0) st = plan_prepare_decode(p);
   tm.lap("prepare(analyze)");

@@ -309,6 +309,9 @@ struct dmcg_plan {
   // the reconstruction's A operand (dequantised coefficients, their Ozaki
   // slices) is still in place from an earlier frame window of the same stream
   bool rec_a_valid = false;
+  // drop-in decode from page-locked arrays: axis a's coefficient symbols arrive
+  // on ctx->copy (event ctx->ev_in[a]); the first reconstruction waits per axis
+  bool coeff_events = false;
   bool coeff_streamed = false;  // set by the encode when it did so (download skips them)
   cudaStream_t up_stream = nullptr;  // plan / decode-structure uploads (default: aux / ctx stream)
   bool use_graphs = false;          // reused plans replay CUDA graphs (dmcg_plan_create)

@@ -833,11 +833,54 @@ static Status enqueue_decode_direct(dmcg_plan* p, int refine, bool factor, bool 
     // a later frame window of the same upload (the drop-in decode's second
     // window): the dequantised coefficients and their slices are in place
     const bool a_ready = p->rec_a_valid && p->oz_rec_slices && !p->use_graphs;
-    if (!a_ready)
+    const bool per_axis = p->coeff_events && p->oz_rec_slices && !a_ready && !p->use_graphs;
+    if (p->coeff_events && !per_axis) {  // the symbols arrive on the copy stream
+      for (int a = 0; a < 3; ++a) DMCG_TRY(cudaStreamWaitEvent(s, p->ctx->ev_in[a], 0));
+      p->coeff_events = false;
+    }
+    if (!a_ready && !per_axis)
       DMCG_TRY(launch_dequant_rows(s, 3 * k, n, p->d_coeff_q, p->d_rowp, p->d_row_bits,
                                    p->d_flags + 1, Cd));
     DMCG_TRY(launch_dequant_dict(s, F_all, k, f0, F, p->d_dict_q, p->dict_bits, p->d_flags + 1, Ud));
-    if (p->oz_rec_slices) {
+    if (per_axis) {
+      // dequantise, slice and multiply axis a as soon as its symbols are in
+      // (same slices and tiles as the batched oz_matmul below: same bits)
+      const int sr = p->oz_rec_slices;
+      const long kn = (long)k * n, kF = (long)k * F;
+      OzSlices sa, sb;
+      sa.rows = n;
+      sa.rows_pad = oz_rows_pad(n);
+      sa.K = k;
+      sa.K_pad = oz_k_pad(k);
+      sa.s = sr;
+      sa.batch = 1;
+      sb = sa;
+      sb.rows = F;
+      sb.rows_pad = oz_rows_pad(F);
+      int8_t* qa = p->d_oz_q;
+      int8_t* qb = qa + oz_slice_bytes(n, k, sr, 3);
+      unsigned long long* ma = p->d_oz_max;
+      unsigned long long* mb = ma + 3L * oz_rows_pad(n);
+      for (int a = 0; a < 3; ++a) {
+        DMCG_TRY(cudaStreamWaitEvent(s, p->ctx->ev_in[a], 0));
+        DMCG_TRY(launch_dequant_rows(s, k, n, p->d_coeff_q + a * kn, p->d_rowp + 2L * a * k,
+                                     p->d_row_bits + a * k, p->d_flags + 1, Cd + a * kn));
+        OzOperand A{{Cd + a * kn, nullptr, nullptr}, false, 1L, (long)n, n, k, 1};
+        OzOperand B{{Ud + a * kF, nullptr, nullptr}, false, 1L, (long)F, F, k, 1};
+        sa.q = qa + (size_t)a * sr * sa.rows_pad * sa.K_pad;
+        sa.maxbits = ma + (size_t)a * sa.rows_pad;
+        sb.q = qb + (size_t)a * sr * sb.rows_pad * sb.K_pad;
+        sb.maxbits = mb + (size_t)a * sb.rows_pad;
+        DMCG_TRY(oz_slice(s, A, sa));
+        DMCG_TRY(oz_slice(s, B, sb));
+        OzStore outa{p->d_rm_delta + (long)a * F, 0L, 0L, (long)W, 1L};
+        int used = 0;
+        DMCG_TRY(oz_gemm(s, sa, sb, outa, 1, &used));
+        if (used != 1) return Status{DMCG_E_CUDA, "CudaError: reconstruction split"};
+      }
+      p->rec_a_valid = true;
+      p->coeff_events = false;
+    } else if (p->oz_rec_slices) {
       // INT8 tensor cores (Ozaki slices): delta~(i, b F + f) = sum_r c~(b, r, i) U~(f, r)
       const int sr = p->oz_rec_slices;
       const long kn = (long)k * n, kF = (long)k * F;
