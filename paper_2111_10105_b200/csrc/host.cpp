@@ -1340,6 +1340,8 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e, bool stream_coeff
     stream_coeffs = false;
   }
   p->coeff_events = stream_coeffs;
+  PhaseTimer tu("upload");
+  if (stream_coeffs) tu.lap("streamed symbols: yes");
   const size_t n = p->n, F = p->F, k = p->k, Fo = p->F_in;
   const size_t FF = p->nb > 1 ? (size_t)p->nb * p->kf * p->kf : F * F;
   float rng[6];
@@ -1359,9 +1361,9 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e, bool stream_coeff
       CUDA_OK(cudaMemcpyAsync(p->d_row_min + a * k, e->row_min[a], k * 4, cudaMemcpyHostToDevice, s));
       CUDA_OK(cudaMemcpyAsync(p->d_row_max + a * k, e->row_max[a], k * 4, cudaMemcpyHostToDevice, s));
       CUDA_OK(cudaMemcpyAsync(p->d_row_bits + a * k, e->row_bits[a], k, cudaMemcpyHostToDevice, s));
-      CUDA_OK(cudaMemcpyAsync(p->d_coeff_q + a * k * n, e->coeff_q[a], k * n * 2,
-                              cudaMemcpyHostToDevice, stream_coeffs ? p->ctx->copy : s));
-      if (stream_coeffs) CUDA_OK(cudaEventRecord(p->ctx->ev_in[a], p->ctx->copy));
+      if (!stream_coeffs)
+        CUDA_OK(cudaMemcpyAsync(p->d_coeff_q + a * k * n, e->coeff_q[a], k * n * 2,
+                                cudaMemcpyHostToDevice, s));
     }
     if (p->n_c)
       CUDA_OK(cudaMemcpy2DAsync(p->d_anchor_q + a * (size_t)p->n_c * F, F * 2, e->anchor_q[a],
@@ -1374,9 +1376,23 @@ static Status upload_impl(dmcg_plan* p, const dmcg_encoded* e, bool stream_coeff
     rng[2 * a + 1] = e->anchor_max[a];
   }
   CUDA_OK(cudaMemcpyAsync(p->d_anchor_rng, rng, sizeof(rng), cudaMemcpyHostToDevice, s));
+  // the streamed symbols last: the copy engine serves its queue in order, and
+  // the small arrays above must not wait behind 400 MB
+  if (stream_coeffs)
+    for (int a = 0; a < 3; ++a) {
+      CUDA_OK(cudaMemcpyAsync(p->d_coeff_q + a * k * n, e->coeff_q[a], k * n * 2,
+                              cudaMemcpyHostToDevice, p->ctx->copy));
+      CUDA_OK(cudaEventRecord(p->ctx->ev_in[a], p->ctx->copy));
+    }
   // the decoder's anchor padding (codec.cpp:483-495): frames F_in.. repeat the last
   if (p->n_c && F > Fo) CUDA_OK(launch_pad_anchor_levels(s, (int)p->n_c, (int)Fo, (int)F, p->d_anchor_q));
-  CUDA_OK(cudaStreamSynchronize(s));  // rng is a stack buffer
+  tu.lap("issue");
+  // dmcg_plan_upload returns with the copies done (the caller may reuse its
+  // arrays); the drop-in decode keeps the caller's arrays until it returns and
+  // lets its kernels follow the copies in stream order (the stack / vector
+  // sources above are pageable: staged before cudaMemcpyAsync returns)
+  if (!stream_coeffs) CUDA_OK(cudaStreamSynchronize(s));
+  tu.lap("sync");
   return Status::ok();
 }
 
