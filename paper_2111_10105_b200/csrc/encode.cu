@@ -278,6 +278,19 @@ __global__ void k_quant_rows(int k, int n, const unsigned long long* __restrict_
   }
   const double* c = C + row * n;
   uint16_t* o = q + row * n;
+  if ((n & 3) == 0 && (((uintptr_t)c | (uintptr_t)o) & 15) == 0) {
+    // four coefficients per thread: two 16-byte loads, one 8-byte store
+    for (int i = threadIdx.x * 4; i < n; i += blockDim.x * 4) {
+      const double2 v0 = *reinterpret_cast<const double2*>(c + i);
+      const double2 v1 = *reinterpret_cast<const double2*>(c + i + 2);
+      const uint32_t l0 = quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v0.x);
+      const uint32_t l1 = quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v0.y);
+      const uint32_t l2 = quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v1.x);
+      const uint32_t l3 = quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, v1.y);
+      *reinterpret_cast<uint2*>(o + i) = make_uint2(l0 | (l1 << 16), l2 | (l3 << 16));
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     o[i] = (uint16_t)quantize_level(qp.min_, qp.width, qp.levels, qp.degenerate, c[i]);
 }
