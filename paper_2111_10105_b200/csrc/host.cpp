@@ -1903,7 +1903,7 @@ int dmcg_decode(dmcg_ctx* ctx, const dmcg_encoded* in, const dmcg_decode_options
       ow.frame_count = f1 - f0;
       if (w) ow.reuse_factor = 1;
       st = plan_decode(p, &ow, p->d_x_out);  // returns after its stream sync
-      if (w + 1 == nwin_eff) tm.lap("kernels");
+      tm.lap(w + 1 == nwin_eff ? "kernels (last window)" : "kernels (window)");
       if (st.good()) d2h(f0, f1 - f0, w + 1 == nwin_eff ? ctx->stream : ctx->aux2);
     }
     if (cudaStreamSynchronize(ctx->aux2) != cudaSuccess && st.good())
