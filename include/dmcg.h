@@ -185,7 +185,12 @@ int dmcg_encoded_sizes(uint32_t n, uint32_t F, const dmcg_config* cfg, dmcg_size
 
 /* ---- drop-in entry points (host in, host out) --------------------------- */
 /* dmc::encode(const MeshSequence&, const EncoderConfig&)
- * (include/dmc/codec.hpp:90; src/codec.cpp:351-473). */
+ * (include/dmc/codec.hpp:90; src/codec.cpp:351-473).
+ * Host arrays may be pageable or page-locked; page-locked ones (seq->axes,
+ * out->coeff_q) let the copies run under the kernels axis by axis.  The call
+ * also prepares the decode of its own stream (plan, symbolic analysis, M's
+ * numeric factor) for the next dmcg_decode on this context; nothing is kept
+ * beyond that decode.  The same bits either way. */
 int dmcg_encode(dmcg_ctx* ctx, const dmcg_seq* seq, const dmcg_config* cfg, dmcg_encoded* out);
 /* dmc::decode(const CompressedAnimation&) (include/dmc/codec.hpp:91;
  * src/codec.cpp:475-552).  out_axes: 3 host arrays of n*F elements of
