@@ -1018,7 +1018,8 @@ static Status plan_decode_direct(dmcg_plan* p, const dmcg_decode_options* opt,
   const CholLevels& lv = p->levels;
   int nl = 0;  // factor: assemble, panels + trailing, inverse (2), P (2) per level
   for (uint32_t l = 0; l < lv.nlevels; ++l) nl += 5 + (int)((lv.maxw[l] + 31) / 32) * 2;
-  const int per_solve = (int)lv.nlevels * 3;  // gather, forward, backward
+  // gather, forward, backward per level (the leaf level has no gather pass)
+  const int per_solve = (int)lv.nlevels * 3 - (lv.nlevels ? 1 : 0);
   p->stats.kernel_launches_decode = (k > 0 ? 2 : 0) + 1 + (factor ? nl : 0) +
                                     (1 + refine) * per_solve + refine + 1;
   p->stats.flops_solve = (1 + refine) * p->chol.flops_solve_per_rhs * W;
