@@ -2195,7 +2195,8 @@ __device__ __forceinline__ bool oi_blocked_panels() { return c_oi_blocked != 0; 
 template <int MAXR, int B>
 __global__ void __launch_bounds__(kOiThreads)
     k_oi_cluster(int F, int k, int rounds, const double* __restrict__ Rall,
-                 const double* __restrict__ start, double* Qall, double* Hall, double* mirror) {
+                 const double* __restrict__ start, double* Qall, double* Hall, double* mirror,
+                 long start_bs, double* Call) {
   extern __shared__ double dyn[];
   __shared__ double s_tau[B];
   __shared__ double s_T[B * B];
@@ -2220,7 +2221,13 @@ __global__ void __launch_bounds__(kOiThreads)
   // Rall == nullptr: QR only (Q of the start matrices, no R Q / H) — one
   // round of the implicit X (X^T Q) iteration, whose products run as GEMMs
   const double* R = Rall ? Rall + (size_t)b * F * F : nullptr;
-  const double* S = start + (size_t)b * F * k;
+  // Call != nullptr (with Rall == nullptr, rounds == 0): completion mode.  The
+  // start matrix is U_k (axis stride start_bs); after the factor the cluster
+  // forms columns k..F-1 of the full Householder Q, H_0 ... H_{cs-1} e_j, from
+  // the mirrored block reflectors, B columns per CTA and pass, into
+  // Call + b start_bs + F k (k_complete does the same on ONE CTA per axis).
+  const bool complete = Call != nullptr;
+  const double* S = start + (size_t)b * (start_bs ? (size_t)start_bs : (size_t)F * k);
   for (int t = threadIdx.x; t < F * B; t += blockDim.x) {
     const int j = t / F, i = t % F;
     Zb[j * ld + i] = j < nb ? S[(size_t)(c0 + j) * F + i] : 0.0;
@@ -2305,7 +2312,7 @@ __global__ void __launch_bounds__(kOiThreads)
       Qb[j * ld + i] = (j < nb && i == c0 + j) ? 1.0 : 0.0;
     }
     __syncthreads();
-    for (int p = rank; p >= 0 && nb > 0; --p) {
+    for (int p = rank; p >= 0 && nb > 0 && !complete; --p) {
       const bool own = p == rank;
       const double* Vp = own ? Zb + p * B : mir_v(p);
       const double* Tp = own ? s_T : mir_t(p);
@@ -2317,6 +2324,30 @@ __global__ void __launch_bounds__(kOiThreads)
     cluster_sync_all();  // every remote read of this round's V is done
     t1 = clock64();
     t_sync += t1 - t0;
+    if (complete) {
+      // every block reflector of the factor is mirrored (the barrier above
+      // orders the other CTAs' mirror stores before these loads)
+      double* Co = Call + (size_t)b * (size_t)start_bs + (size_t)F * k;
+      const int ncomp = F - k;
+      for (int cb = rank; cb * B < ncomp; cb += cs) {
+        const int nbc = min(B, ncomp - cb * B), col0 = k + cb * B;
+        __syncthreads();
+        for (int t = threadIdx.x; t < F * B; t += blockDim.x) {
+          const int j = t / F, i = t % F;
+          Qb[j * ld + i] = (j < nbc && i == col0 + j) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        for (int p = cs - 1; p >= 0; --p)
+          blk_apply<B>(mir_v(p), ld, B, mir_t(p), false, Qb + p * B, ld, nbc, F - p * B, s_W,
+                       s_part, Vs + p * B, Ts, true);
+        __syncthreads();
+        for (int t = threadIdx.x; t < F * nbc; t += blockDim.x) {
+          const int j = t / F, i = t % F;
+          Co[(size_t)(cb * B + j) * F + i] = Qb[j * ld + i];
+        }
+      }
+      return;
+    }
     // ---- Z_c = R Q_c --------------------------------------------------------
     if (!R) break;
     if (nb > 0) rq_tasks(R, F, F, nb, Qb, ld, Zb, ld, 0, (F + 7) / 8);
@@ -2600,7 +2631,8 @@ static cudaError_t oi_fused_impl(cudaStream_t s, int nbatch, int F, int k, int r
 template <int MAXR, int B>
 static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                      const double* R, const double* start, double* Q, double* H,
-                                     double* mirror, bool* launched) {
+                                     double* mirror, bool* launched, long start_bs = 0,
+                                     double* complete_out = nullptr) {
   *launched = false;
   const int cs = (k + B - 1) / B;
   constexpr int PW = QrPanel<MAXR>::PW;
@@ -2652,7 +2684,8 @@ static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, i
   if (dbg)
     fprintf(stderr, "dmcg: k_oi_cluster F=%d k=%d B=%d cluster %d smem %zu (max active %d)\n", F,
             k, B, cs, smem, nclusters);
-  e = cudaLaunchKernelEx(&cfg, k_oi_cluster<MAXR, B>, F, k, rounds, R, start, Q, H, mirror);
+  e = cudaLaunchKernelEx(&cfg, k_oi_cluster<MAXR, B>, F, k, rounds, R, start, Q, H, mirror,
+                         start_bs, complete_out);
   *launched = e == cudaSuccess;
   if (dbg && e == cudaSuccess) {
     long long h[64 * 8];
@@ -2675,16 +2708,20 @@ static cudaError_t oi_cluster_launch(cudaStream_t s, int nbatch, int F, int k, i
 template <int MAXR>
 static cudaError_t oi_cluster_dispatch(cudaStream_t s, int nbatch, int F, int k, int rounds,
                                        const double* R, const double* start, double* Q, double* H,
-                                       double* mirror, bool* launched) {
+                                       double* mirror, bool* launched, long start_bs = 0,
+                                       double* complete_out = nullptr) {
   *launched = false;
   if (k <= 0 || k >= F) return cudaSuccess;
   static const int bsel = getenv("DMCG_OI_B") ? atoi(getenv("DMCG_OI_B")) : 0;  // experiments
   if (bsel == 16 && (k + 15) / 16 <= 16)
-    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched);
+    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched,
+                                       start_bs, complete_out);
   if ((k + 7) / 8 <= 16)
-    return oi_cluster_launch<MAXR, 8>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched);
+    return oi_cluster_launch<MAXR, 8>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched,
+                                      start_bs, complete_out);
   if ((k + 15) / 16 <= 16)
-    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched);
+    return oi_cluster_launch<MAXR, 16>(s, nbatch, F, k, rounds, R, start, Q, H, mirror, launched,
+                                       start_bs, complete_out);
   return cudaSuccess;
 }
 
@@ -2750,8 +2787,21 @@ static cudaError_t complete_impl(cudaStream_t s, int nbatch, int F, int k, doubl
 }
 
 cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
-                            double* scr) {
+                            double* scr, double* mirror) {
   if (F > 512) return cudaErrorInvalidValue;
+  // the OI's cluster (one per axis) factors U_k and forms the completion
+  // blocks on all its CTAs; k_complete (one CTA per axis) is the fallback
+  static const bool single = getenv("DMCG_COMPLETE_SINGLE") != nullptr;  // tests
+  if (mirror && !single && k > 0 && k < F) {
+    bool done = false;
+    const long FF = (long)F * F;
+    cudaError_t e = cudaSuccess;
+    if (F <= 64) e = oi_cluster_dispatch<2>(s, nbatch, F, k, 0, nullptr, U, nullptr, nullptr, mirror, &done, FF, U);
+    else if (F <= 128) e = oi_cluster_dispatch<4>(s, nbatch, F, k, 0, nullptr, U, nullptr, nullptr, mirror, &done, FF, U);
+    else if (F <= 256) e = oi_cluster_dispatch<8>(s, nbatch, F, k, 0, nullptr, U, nullptr, nullptr, mirror, &done, FF, U);
+    else e = oi_cluster_dispatch<16>(s, nbatch, F, k, 0, nullptr, U, nullptr, nullptr, mirror, &done, FF, U);
+    if (e != cudaSuccess || done) return e;
+  }
   if (F <= 64) return complete_impl<2>(s, nbatch, F, k, U, work, scr);
   if (F <= 128) return complete_impl<4>(s, nbatch, F, k, U, work, scr);
   if (F <= 256) return complete_impl<8>(s, nbatch, F, k, U, work, scr);

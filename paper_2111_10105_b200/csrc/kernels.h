@@ -86,7 +86,7 @@ cudaError_t launch_qr_cluster(cudaStream_t s, int nbatch, int F, int k, const do
                               double* Q, double* mirror);
 // U[:, k:F] = columns k..F-1 of the full Householder Q of U[:, :k].
 cudaError_t launch_complete(cudaStream_t s, int nbatch, int F, int k, double* U, double* work,
-                            double* scr);
+                            double* scr, double* mirror = nullptr);
 // Per-axis scratch (doubles) of the blocked QR used by the two kernels above.
 size_t qr_scratch_doubles(int F, int k);
 cudaError_t launch_fill_zero(cudaStream_t s, double* p, long count);

@@ -271,7 +271,7 @@ Status basis(dmcg_plan* p, const void* const x[3] = nullptr, int nrows = 0,
   cudaStream_t s2 = p->ctx->aux;
   DMCG_TRY(cudaEventRecord(p->ev_fork, s));
   DMCG_TRY(cudaStreamWaitEvent(s2, p->ev_fork, 0));
-  DMCG_TRY(launch_complete(s2, 3, F, k, p->d_U, p->d_H, p->d_qr_scr));
+  DMCG_TRY(launch_complete(s2, 3, F, k, p->d_U, p->d_H, p->d_qr_scr, p->d_oi_mirror));
   DMCG_TRY(launch_canon_signs(s2, 3, F, k, F - k, p->d_U, FF));
   for (int a = 0; a < 3; ++a)
     DMCG_TRY(launch_fill_zero(s2, p->d_evals + (long)a * F + k, F - k));
