@@ -71,8 +71,23 @@ __global__ void k_oz_rowmax_rows(OzOperand op, unsigned long long* maxbits, int 
   if (row >= op.rows) return;
   const long k0 = (long)blockIdx.y * kchunk;
   const long k1 = k0 + kchunk < op.K ? k0 + kchunk : op.K;
+  // eight independent loads in flight per thread (the dependent one-load loop
+  // ran at 29 % of HBM)
+  double m8[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) m8[u] = 0.0;
+  long k = k0;
+  for (; k + 8 <= k1; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = oz_ld<T>(op, b, row, k + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m8[u] = fmax(m8[u], fabs(v[u]));
+  }
+  for (; k < k1; ++k) m8[0] = fmax(m8[0], fabs(oz_ld<T>(op, b, row, k)));
   double m = 0.0;
-  for (long k = k0; k < k1; ++k) m = fmax(m, fabs(oz_ld<T>(op, b, row, k)));
+#pragma unroll
+  for (int u = 0; u < 8; ++u) m = fmax(m, m8[u]);
   atomicMax(maxbits + (long)b * rows_pad + row, (unsigned long long)__double_as_longlong(m));
 }
 
