@@ -100,12 +100,21 @@ __global__ void __launch_bounds__(256) k_oz_slice(OzOperand op, OzSlices sl) {
   const int b = blockIdx.z, r0 = blockIdx.y * 64;
   const long k0 = (long)blockIdx.x * 64;
   const int t = threadIdx.x;
-#pragma unroll 4
-  for (int j = 0; j < 16; ++j) {
-    const int i = t + 256 * j;
-    const int r = KCONTIG ? i / 64 : i % 64, k = KCONTIG ? i % 64 : i / 64;
-    const long gr = r0 + r, gk = k0 + k;
-    tile[r][k] = (gr < op.rows && gk < op.K) ? oz_ld<T>(op, b, gr, gk) : 0.0;
+  {  // all sixteen loads of the thread in flight, then the stores
+    double v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = t + 256 * j;
+      const int r = KCONTIG ? i / 64 : i % 64, k = KCONTIG ? i % 64 : i / 64;
+      const long gr = r0 + r, gk = k0 + k;
+      v[j] = (gr < op.rows && gk < op.K) ? oz_ld<T>(op, b, gr, gk) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int i = t + 256 * j;
+      const int r = KCONTIG ? i / 64 : i % 64, k = KCONTIG ? i % 64 : i / 64;
+      tile[r][k] = v[j];
+    }
   }
   __syncthreads();
   const int r = t >> 2, kq = (t & 3) * 16;
